@@ -1,0 +1,223 @@
+"""Hierarchical p-multigrid with additive Schwarz smoothing (oracle).
+TEST INFRASTRUCTURE ONLY.
+
+Level operators ("A_{l-1} = R_l A_l R_l^T", P:209-216 hierarchical
+matrices): A_q = A[I_q, I_q], I_q = DOFs of mode order <= q; R = [I 0] is index
+selection.  Levels: arithmetic p-sequence p, p-1, ..., 1.
+
+Additive Schwarz (Eq. AdditiveSchwarz):
+  M^{-1} = sum_i P_i (P_i^T A P_i)^{-1} P_i^T,
+blocks: elementwise = the free level DOFs supported on one cell;
+patchwise = the union over the 2^d cells around a grid vertex (every vertex,
+boundary ones included; empty blocks skipped).  Block inverses by dense LU
+(numpy.linalg.inv = LAPACK getrf/getri path, O8).  The sum is accumulated
+serially in block order (cell / vertex index, x fastest).
+
+V-cycle: Algorithm 1 with reading R1 (the residual is recomputed
+before every smoothing sweep, P:124-126 fixed-point smoothing), x~ = 0 on
+entry, n_s pre and post sweeps.
+Coarse level: 'direct' dense LU; 'as_pcg' CG with the
+undamped elementwise AS preconditioner at p = 1, x0 = 0, stop at
+||r|| < rtol ||r0|| (reading R4); 'jacobi_pcg' the same with diag(A0).
+Outer solver: flexible (Polak-Ribiere) PCG, x0 = 0, stop at the recursive
+||r_k||_2 / ||b||_2 < rtol (readings R5, R6).
+"""
+from __future__ import annotations
+
+import numpy as np
+import scipy.linalg as sla
+
+
+class Level:
+    def __init__(self, prob, q, block, A_full, omega):
+        dof = prob.dof
+        self.q = q
+        self.idx = dof.level_dofs(q)
+        self.n = len(self.idx)
+        self.A = A_full[self.idx][:, self.idx].tocsr()
+        self.omega = omega
+        pos = np.full(dof.ndof, -1, dtype=np.int64)
+        pos[self.idx] = np.arange(self.n)
+        mq = dof.level_m(q)
+        cd = dof.cell_dofs[:, :mq]
+        cfg = prob.cfg
+        blocks = []
+        if block == "element":
+            for c in range(cd.shape[0]):
+                g = cd[c][cd[c] >= 0]
+                if len(g):
+                    blocks.append(pos[g])
+        else:  # patch: 2^d cells around each grid vertex
+            n, d = cfg.n, cfg.dim
+            for v in range((n + 1) ** d):
+                vc = [(v // (n + 1) ** a) % (n + 1) for a in range(d)]
+                cells = []
+                for corner in range(1 << d):
+                    cc = [vc[a] - 1 + ((corner >> a) & 1) for a in range(d)]
+                    if all(0 <= x < n for x in cc):
+                        cells.append(sum(cc[a] * n ** a for a in range(d)))
+                g = np.unique(np.concatenate([cd[c][cd[c] >= 0] for c in sorted(cells)]))
+                if len(g):
+                    blocks.append(pos[g])
+        self.blocks = blocks
+        self.inv = [None] * len(blocks)
+        Ad = self.A
+        by_size = {}
+        for i, b in enumerate(blocks):
+            by_size.setdefault(len(b), []).append(i)
+        for size, ids in by_size.items():
+            stack = np.stack([Ad[blocks[i]][:, blocks[i]].toarray() for i in ids])
+            inv = np.linalg.inv(stack)
+            for k, i in enumerate(ids):
+                self.inv[i] = inv[k]
+
+    def schwarz(self, r):
+        """M^{-1} r = sum_i P_i A_i^{-1} P_i^T r, accumulated serially in block order."""
+        idx = np.concatenate(self.blocks)
+        vals = np.concatenate([self.inv[i] @ r[b] for i, b in enumerate(self.blocks)])
+        return np.bincount(idx, weights=vals, minlength=self.n)
+
+
+class Hierarchy:
+    def __init__(self, prob, block=None, omega=None, n_pre=None, n_post=None, coarse=None,
+                 coarse_rtol=None, coarse_maxit=None):
+        cfg = prob.cfg
+        self.prob = prob
+        self.block = block or cfg.block
+        if omega is None:
+            omega = cfg.omega if cfg.omega is not None else cfg.replace(block=self.block).omega_value
+        self.omega = omega
+        self.n_pre = cfg.n_pre if n_pre is None else n_pre
+        self.n_post = cfg.n_post if n_post is None else n_post
+        self.coarse = coarse or cfg.coarse
+        self.coarse_rtol = cfg.coarse_rtol if coarse_rtol is None else coarse_rtol
+        self.coarse_maxit = cfg.coarse_maxit if coarse_maxit is None else coarse_maxit
+        A = prob.A
+        self.levels = {}
+        for q in range(cfg.p, 0, -1):
+            blk = self.block if q > 1 else "element"   # coarse AS is elementwise (R11)
+            need_blocks = q > 1 or self.coarse == "as_pcg"
+            if need_blocks:
+                self.levels[q] = Level(prob, q, blk, A, self.omega if q > 1 else 1.0)
+            else:
+                lv = Level.__new__(Level)
+                lv.q = q
+                lv.idx = prob.dof.level_dofs(q)
+                lv.n = len(lv.idx)
+                lv.A = A[lv.idx][:, lv.idx].tocsr()
+                self.levels[q] = lv
+        # restriction selections: positions of I_{q-1} inside I_q
+        self.sel = {}
+        for q in range(cfg.p, 1, -1):
+            self.sel[q] = np.searchsorted(self.levels[q].idx, self.levels[q - 1].idx)
+        c = self.levels[1]
+        if self.coarse == "direct":
+            self.lu = sla.lu_factor(c.A.toarray())
+        elif self.coarse == "jacobi_pcg":
+            self.diag = c.A.diagonal()
+        self.coarse_iters = []
+
+    # -- coarse level --------------------------------------
+    def coarse_solve(self, b):
+        lv = self.levels[1]
+        if self.coarse == "direct":
+            return sla.lu_solve(self.lu, b)
+        prec = lv.schwarz if self.coarse == "as_pcg" else (lambda r: r / self.diag)
+        x, it = pcg(lambda v: lv.A @ v, b, prec, self.coarse_rtol, self.coarse_maxit,
+                    rel_to="r0")
+        self.coarse_iters.append(it)
+        return x
+
+    # -- Algorithm 1 -------------------------------------------------
+    def vcycle(self, b, q=None):
+        if q is None:
+            q = self.prob.cfg.p
+        if q == 1:
+            return self.coarse_solve(b)
+        lv = self.levels[q]
+        A = lv.A
+        w = self.omega
+        x = np.zeros(lv.n)
+        for _ in range(self.n_pre):            # pre-smoothing, residual per sweep (R1)
+            r = b - A @ x
+            x = x + w * lv.schwarz(r)
+        r = b - A @ x                           # update residual
+        e = self.vcycle(r[self.sel[q]], q - 1)  # r_{l-1} = R r_l
+        x[self.sel[q]] += e                     # x += R^T e
+        for _ in range(self.n_post):           # P:169 residual, then post-smoothing
+            r = b - A @ x
+            x = x + w * lv.schwarz(r)
+        return x
+
+    def fcg(self, b, rtol=None, maxit=None, force_iters=None):
+        cfg = self.prob.cfg
+        rtol = cfg.rtol if rtol is None else rtol
+        maxit = cfg.maxit if maxit is None else maxit
+        A = self.levels[cfg.p].A
+        return fcg(lambda v: A @ v, b, self.vcycle, rtol, maxit, force_iters=force_iters)
+
+
+def pcg(apply_A, b, prec, rtol, maxit, rel_to="b"):
+    """Standard preconditioned CG, x0 = 0 (coarse solver)."""
+    x = np.zeros_like(b)
+    r = b.copy()
+    nr0 = np.linalg.norm(r)
+    if nr0 == 0.0:
+        return x, 0
+    z = prec(r)
+    p = z.copy()
+    rz = r @ z
+    it = 0
+    while it < maxit:
+        q = apply_A(p)
+        pq = p @ q
+        if pq <= 0:
+            raise FloatingPointError("p^T A p <= 0 in coarse CG")
+        a = rz / pq
+        x += a * p
+        r -= a * q
+        it += 1
+        if np.linalg.norm(r) < rtol * nr0:
+            break
+        z = prec(r)
+        rz_new = r @ z
+        p = z + (rz_new / rz) * p
+        rz = rz_new
+    return x, it
+
+
+def fcg(apply_A, b, prec, rtol, maxit, force_iters=None):
+    """Flexible (Polak-Ribiere) PCG, x0 = 0 (R5/R6).
+    Returns (x, iterations, relative residual history [||r_k||/||b||])."""
+    x = np.zeros_like(b)
+    nb = np.linalg.norm(b)
+    if nb == 0.0:
+        return x, 0, [0.0]
+    r = b.copy()
+    z = prec(r)
+    p = z.copy()
+    rz = r @ z
+    hist = [1.0]
+    it = 0
+    while True:
+        q = apply_A(p)
+        pq = p @ q
+        if pq <= 0:
+            raise FloatingPointError("p^T A p <= 0 in FCG")
+        a = rz / pq
+        x = x + a * p
+        r_old = r
+        r = r - a * q
+        it += 1
+        hist.append(np.linalg.norm(r) / nb)
+        if force_iters is not None:
+            if it >= force_iters:
+                break
+        elif hist[-1] < rtol or it >= maxit:
+            break
+        z = prec(r)
+        rz_new = r @ z
+        beta = (rz_new - z @ r_old) / rz
+        p = z + beta * p
+        rz = rz_new
+    return x, it, hist

@@ -1,0 +1,103 @@
+"""The five BASELINE.json workloads (+ small parametric ones for tests).
+
+Readings of the paper applied here:
+  R2  V(5,5) sweeps ("five pre- and post-smoothing steps").
+  R3  omega = 1/3 (2D elementwise), 2/15 (3D elementwise), 1/6 (2D patch),
+      1/18 (3D patch).
+  R4  coarse p=1 solve: dense direct for config 1 ("direct solver,
+      if the system is small"), CG + undamped elementwise AS to 1e-12 otherwise
+      (PAPER.md:343).
+  R6  outer flexible CG to relative residual < 1e-10 (BASELINE.json configs).
+  R7  u = 0 strongly on Dirichlet box faces (bitmask bit 2*axis+side).
+  R10 tensor space for configs 1,2,3,5; trunk space for config 4.
+Only constants and recipes -- no method arithmetic.
+"""
+from __future__ import annotations
+
+import dataclasses
+from dataclasses import dataclass, field
+
+
+@dataclass(frozen=True)
+class Config:
+    name: str
+    dim: int
+    n: int                      # cells per axis
+    p: int                      # polynomial order
+    space: str = "tensor"       # "tensor" | "trunk"
+    physics: str = "poisson"    # "poisson" | "elasticity"
+    alpha: float = 1e-8         # fictitious stiffness factor
+    depth: int = 3              # space-tree integration depth
+    geometry: dict = field(default_factory=lambda: {"kind": "none"})
+    dirichlet: int = -1         # face bitmask; -1 = all faces
+    traction_face: int = -1     # face index (2*axis+side) with traction (1,0,0); -1 none
+    block: str = "element"      # "element" | "patch"
+    omega: float | None = None  # None -> paper's value for (dim, block)
+    n_pre: int = 5
+    n_post: int = 5
+    coarse: str = "as_pcg"      # "direct" | "as_pcg" | "jacobi_pcg"
+    coarse_rtol: float = 1e-12
+    coarse_maxit: int = 10000
+    rtol: float = 1e-10
+    maxit: int = 500
+    E: float = 1.0
+    nu: float = 0.3
+
+    @property
+    def n_f(self) -> int:
+        return self.dim if self.physics == "elasticity" else 1
+
+    @property
+    def dirichlet_mask(self) -> int:
+        return (1 << (2 * self.dim)) - 1 if self.dirichlet < 0 else self.dirichlet
+
+    @property
+    def omega_value(self) -> float:
+        if self.omega is not None:
+            return self.omega
+        # PAPER.md:300
+        table = {(2, "element"): 1.0 / 3.0, (3, "element"): 2.0 / 15.0,
+                 (2, "patch"): 1.0 / 6.0, (3, "patch"): 1.0 / 18.0}
+        return table[(self.dim, self.block)]
+
+    def replace(self, **kw) -> "Config":
+        return dataclasses.replace(self, **kw)
+
+
+CONFIGS = {
+    "cfg1": Config("cfg1", dim=2, n=16, p=3,
+                   geometry={"kind": "explicit", "centres": [[0.503, 0.497]], "radii": [0.23]},
+                   coarse="direct"),
+    "cfg2": Config("cfg2", dim=3, n=32, p=2,
+                   geometry={"kind": "seeded", "count": 8, "r_min": 0.05, "r_max": 0.12, "seed": 2}),
+    "cfg3": Config("cfg3", dim=3, n=64, p=4, block="patch",
+                   geometry={"kind": "seeded", "count": 64, "r_min": 0.03, "r_max": 0.08, "seed": 3}),
+    "cfg4": Config("cfg4", dim=3, n=64, p=3, space="trunk", physics="elasticity",
+                   geometry={"kind": "seeded", "count": 200, "r_min": 0.02, "r_max": 0.05, "seed": 4},
+                   dirichlet=0b000001, traction_face=1),
+    "cfg5": Config("cfg5", dim=3, n=256, p=3,
+                   geometry={"kind": "seeded", "count": 1000, "r_min": 0.01, "r_max": 0.03, "seed": 5}),
+}
+
+
+def get_config(name: str) -> Config:
+    return CONFIGS[name]
+
+
+def small_config(dim=3, n=4, p=2, space="tensor", physics="poisson", voids=None,
+                 seed=0, **kw) -> Config:
+    """A small parametric workload for tests.  voids: None (no voids), an int
+    (seeded count with radii in [0.08, 0.2]) or explicit (centres, radii)."""
+    if voids is None:
+        geom = {"kind": "none"}
+    elif isinstance(voids, int):
+        geom = {"kind": "seeded", "count": voids, "r_min": 0.08, "r_max": 0.2, "seed": seed}
+    else:
+        c, r = voids
+        geom = {"kind": "explicit", "centres": [list(map(float, x)) for x in c],
+                "radii": [float(x) for x in r]}
+    if physics == "elasticity":
+        kw.setdefault("dirichlet", 0b000001)
+        kw.setdefault("traction_face", 1)
+    return Config(f"small_d{dim}_n{n}_p{p}_{space}_{physics}", dim=dim, n=n, p=p, space=space,
+                  physics=physics, geometry=geom, **kw)
