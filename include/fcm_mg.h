@@ -1,0 +1,211 @@
+/*
+ * fcm_mg.h -- C ABI of the B200-native hierarchical p-multigrid for finite cell systems
+ * (arXiv 2010.00881, "Hierarchical multigrid approaches for the finite cell method on
+ * uniform and multi-level hp-refined grids").
+ *
+ * The library solves A_L x = b ("A_l x_l = b_l") for a finite-cell
+ * discretisation (Eq. weakform) on a uniform Cartesian grid of cells with
+ * an integrated-Legendre basis of order p, using flexible CG (PAPER.md:351
+ * "the multigrid V-cycle ... primarily as a preconditioner within the CG method") around
+ * one V-cycle of Algorithm 1 per iteration.  Level l <-> order q = l+1;
+ * the levels are the arithmetic p-sequence p, p-1, ..., 1.
+ *
+ * All floating point is IEEE fp64.  Every function returns FCM_OK (0) or a negative error
+ * code; fcm_last_error() returns a thread-local message describing the last failure.
+ * Device pointers are CUDA device pointers on the handle's device; host pointers are
+ * plain host memory.  No torch / C++ types cross this boundary.
+ *
+ * ---------------------------------------------------------------------------------------
+ * CONVENTIONS (shared interface definitions; the CPU oracle implements them independently)
+ * ---------------------------------------------------------------------------------------
+ * Cells: c = (cz*ny + cy)*nx + cx (x fastest); cell (cx,cy,cz) = [cx h,(cx+1)h] x ...
+ *
+ * 1D modes (normalisation reading R-B1): k = 0: (1-xi)/2, k = 1: (1+xi)/2,
+ *   k >= 2: (P_k - P_{k-2})/sqrt(2(2k-1)) (degree k).
+ * Element modes: tuples (kx,ky[,kz]).  Tensor space: all (p+1)^d tuples.  Trunk space
+ *   (PAPER.md:316-320): vertex modes and modes whose internal (k>=2) degrees sum to <= p.
+ * Mode order (the level tag): tensor -> max of 1D orders (k<2 counts 1, k>=2 counts k);
+ *   trunk -> 1 for vertex modes, else the sum of the internal degrees.
+ * Local element order ("hierarchical"): modes sorted by the key
+ *   (order, S, deg_x, deg_y, deg_z, off),  S = sum_{a: k_a>=2} 2^a,
+ *   deg_a = k_a if k_a >= 2 else 0,  off = sum_{a: k_a<2} k_a 2^a;
+ *   element DOF index = rank * n_f + component.  The level-q element DOFs are therefore the
+ *   leading m_q entries, and every level matrix is the leading block.
+ * Entities / DOFs: mode k_a < 2 is nodal on axis a (vertex index cell_a + k_a), k_a >= 2 is
+ *   internal (the cell interval).  DOF key (identifies a global DOF independent of layout):
+ *     X_a = 2*vertex_a (nodal) or 2*cell_a + 1 (internal); X = 0, deg = 0 for absent axes;
+ *     key = ((((X_z*(2nx+1) + X_y)*(2nx+1) + X_x)*(p+1) + deg_z)*(p+1) + deg_y)*(p+1)
+ *           + deg_x)*n_f + comp        (requires nx == ny == nz; int64)
+ * Dirichlet (reading R7): every DOF of an entity on a face with bit (2*axis + side) set in
+ *   dirichlet_faces (side 1 = upper face) is eliminated (u = 0 strongly).
+ * Vector layout on the device ("class-major"): a DOF class is (S, degrees, component); each
+ *   class is a dense array over its free entity positions (x fastest); classes are ordered
+ *   by (order, S, deg_x, deg_y, deg_z, comp).  The level-q vector is the PREFIX of length
+ *   ndofs(q) of the fine vector: restriction R = [I 0] is a pointer alias and R^T is
+ *   zero extension (Eq. restrictionoperation).  fcm_mg_dof_keys() maps
+ *   layout slots to DOF keys.
+ * Element matrices: m x m row-major fp64, m = (number of element modes) * n_f, in the
+ *   local order above, SYMMETRIC.  K_ref is the matrix of an uncut physical cell
+ *   (alpha = 1); an uncut fictitious cell uses alpha * K_ref.
+ */
+#ifndef FCM_MG_H
+#define FCM_MG_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- error codes ---------------------------------------------------------------------- */
+#define FCM_OK            0
+#define FCM_NOT_CONVERGED 1   /* warning: solver hit maxit; outputs valid   */
+#define FCM_EINVAL      (-1)  /* invalid argument (incl. an empty level)      */
+#define FCM_ENOMEM      (-2)  /* device allocation failed; message states bytes           */
+#define FCM_ESINGULAR   (-3)  /* singular / non-SPD Schwarz block; message names it       */
+#define FCM_EINDEF      (-4)  /* p^T A p <= 0 in CG                          */
+#define FCM_ECUDA       (-5)  /* CUDA runtime error                                      */
+#define FCM_ENCCL       (-6)  /* NCCL error                                              */
+
+/* ---- enums ------------------------------------------------------------------------------ */
+#define FCM_SPACE_TENSOR 0
+#define FCM_SPACE_TRUNK  1
+#define FCM_BLOCK_ELEMENT 0   /* elementwise AS blocks (Fig. elementBlocks)   */
+#define FCM_BLOCK_PATCH   1   /* patchwise: 2^d cells around a vertex (Fig. patchBlocks)    */
+#define FCM_COARSE_DIRECT 0   /* dense direct solve of the p=1 level         */
+#define FCM_COARSE_AS_PCG 1   /* CG + undamped elementwise AS at p=1         */
+#define FCM_COARSE_JACOBI_PCG 2 /* CG + diagonal preconditioner (BASELINE.json variant)     */
+#define FCM_PHYS_POISSON 0
+#define FCM_PHYS_ELASTICITY 1
+
+/* Grid / discretisation. */
+typedef struct fcm_grid {
+  int32_t dim;              /* 2 or 3                                                    */
+  int32_t n[3];             /* cells per axis; n[2] = 1 when dim == 2                    */
+  double  h;                /* cell size (cells are cubes)                                */
+  int32_t p;                /* polynomial order, 1 <= p <= 8                              */
+  int32_t space;            /* FCM_SPACE_*                                                */
+  int32_t n_f;              /* field components: 1 (Poisson) or dim (elasticity)          */
+  uint32_t dirichlet_faces; /* bit 2*axis+side: u = 0 on that box face                    */
+} fcm_grid;
+
+/* Solver parameters (readings R2-R4). */
+typedef struct fcm_params {
+  int32_t block;            /* FCM_BLOCK_* for levels q >= 2 (coarse AS is elementwise)   */
+  double  omega;            /* AS relaxation on levels q >= 2 (paper: 1/3, 2/15, 1/6, 1/18)*/
+  int32_t n_pre, n_post;    /* smoothing sweeps (paper: 5, 5)                             */
+  int32_t coarse;           /* FCM_COARSE_*                                               */
+  double  coarse_rtol;      /* inner CG: stop when ||r|| < coarse_rtol ||r0|| (1e-12)    */
+  int32_t coarse_maxit;     /* inner CG iteration cap                                     */
+  void*   stream;           /* cudaStream_t for all work (NULL = legacy default stream)   */
+} fcm_params;
+
+/* Physics of the generator (Eq. weakform). */
+typedef struct fcm_physics {
+  int32_t kind;             /* FCM_PHYS_*                                                 */
+  double  alpha;            /* fictitious-domain factor epsilon, 1e-8       */
+  double  E, nu;            /* elasticity: Young's modulus, Poisson ratio                 */
+  int32_t depth;            /* space-tree integration depth (3)             */
+  int32_t traction_face;    /* face 2*axis+side with traction (1,0,0), or -1              */
+} fcm_physics;
+
+typedef struct fcm_mg fcm_mg;   /* opaque solver handle */
+
+/* ==== workload generator (setup, not timed; independent of the oracle) =================
+ * Voids are open balls ||x - c_j|| < r_j (Omega_fict); a point on a sphere is physical.   */
+
+/* Number of element DOFs m for the grid (host only).  Returns m > 0 or a negative code.   */
+int fcm_element_size(const fcm_grid* g);
+
+/* Classify every cell: 0 = uncut physical, 1 = uncut fictitious, 2 = cut (exact box/ball
+ * test).  cell_kind: host, ncell bytes.  *n_cut receives the number of cut cells.          */
+int fcm_gen_classify(const fcm_grid* g, int64_t n_voids, const double* centres /*n_voids*dim*/,
+                     const double* radii, uint8_t* cell_kind, int64_t* n_cut);
+
+/* Element matrices and body loads (host buffers).  K_ref/f_ref: uncut physical cell (m*m, m).
+ * For each of the n_cut cells listed in cut_cells (cell indices), the space-tree quadrature
+ * (reading R13) gives cut_K[i] (m*m) and cut_f[i] (m).  Poisson f = 1;
+ * elasticity body force 0.  f_traction (m, may be NULL): int_{face} N.(1,0,0) of one cell
+ * face of type ph->traction_face.  Uses up to `threads` host threads (0 = all).            */
+int fcm_gen_element_matrices(const fcm_grid* g, const fcm_physics* ph,
+                             int64_t n_voids, const double* centres, const double* radii,
+                             double* K_ref, double* f_ref, int64_t n_cut,
+                             const int64_t* cut_cells, double* cut_K, double* cut_f,
+                             double* f_traction, int32_t threads);
+
+/* ==== solver ============================================================================ */
+
+/* Build the hierarchy on the current CUDA device ("cached during the solver
+ * setup phase"): copies the host inputs (caller may free them on return), classifies the
+ * Schwarz blocks of every level q >= 2 (and q = 1 for AS-PCG), assembles A_i = P_i^T A_q P_i
+ * and inverts them on the device, factors the coarse level if direct.
+ *   K_ref      host m*m;  cell_kind host ncell (0/1/2);  alpha the fictitious factor;
+ *   cut_cells  host n_cut cell indices (ascending, kind 2);  cut_K host n_cut*m*m.
+ * Errors: FCM_EINVAL (bad sizes, empty level), FCM_ENOMEM, FCM_ESINGULAR, FCM_ECUDA.      */
+int fcm_mg_setup(const fcm_grid* g, const fcm_params* prm, const double* K_ref,
+                 const uint8_t* cell_kind, double alpha, int64_t n_cut,
+                 const int64_t* cut_cells, const double* cut_K, fcm_mg** out);
+
+int fcm_mg_destroy(fcm_mg* h);
+
+/* Number of levels (= p) and free DOFs of level q (1..p) (local DOFs of this rank).        */
+int fcm_mg_nlevels(const fcm_mg* h, int32_t* nlevels);
+int fcm_mg_ndofs(const fcm_mg* h, int32_t q, int64_t* n);
+/* Element DOFs of level q (leading block size m_q).                                        */
+int fcm_mg_level_m(const fcm_mg* h, int32_t q, int32_t* m);
+
+/* Schwarz blocks of level q: *n_individual blocks with their own stored inverse (cut-
+ * influenced neighbourhood) and *n_shared_types inverses shared by all regular blocks of a
+ * boundary type (inverse scaled by 1/alpha for all-fictitious neighbourhoods).            */
+int fcm_mg_block_counts(const fcm_mg* h, int32_t q, int64_t* n_individual, int32_t* n_shared_types);
+
+/* DOF keys of the fine layout (host buffer of ndofs(p) int64, see CONVENTIONS).            */
+int fcm_mg_dof_keys(const fcm_mg* h, int64_t* keys);
+
+/* Assemble a load vector in layout order (device b, ndofs(p)):
+ * b = sum_c P_c^T f_c with f_c = f_ref (kind 0), alpha f_ref (kind 1), cut_f[i] (kind 2),
+ * plus f_traction on every cell touching face `traction_face` (-1: none).  Host inputs.    */
+int fcm_mg_load(fcm_mg* h, const double* f_ref, const double* cut_f,
+                const double* f_traction, int32_t traction_face, double* b);
+
+/* y = A_q x on level q (device vectors of ndofs(q)); PAPER.md:118 A_{l-1} = R A_l R^T.    */
+int fcm_apply(fcm_mg* h, int32_t q, const double* x, double* y);
+
+/* x += omega_q M_q^{-1} r (one additive-Schwarz smoothing update, Eq.
+ * AdditiveSchwarz P:254-257) on level q; omega_q = params.omega (q >= 2) or 1 (q = 1).     */
+int fcm_mg_smooth(fcm_mg* h, int32_t q, const double* r, double* x);
+
+/* x = A_1^{-1} r by the configured coarse solver; *iters (host, may be NULL)
+ * receives the inner CG iterations (0 for direct).                                         */
+int fcm_mg_coarse_solve(fcm_mg* h, const double* r, double* x, int32_t* iters);
+
+/* z = V(r): one V-cycle of Algorithm 1 on the finest level, x~ = 0 on
+ * entry, reading R1 (residual recomputed before each sweep).  Device vectors ndofs(p).     */
+int fcm_mg_vcycle(fcm_mg* h, const double* r, double* z);
+
+/* Flexible (Polak-Ribiere) PCG with one V-cycle per iteration (R5/R6):
+ * x0 = 0, stop when the recursive ||r_k||/||b|| < rtol or after maxit iterations.
+ * b, x: device, ndofs(p).  *iters (host) = number of x-updates.  relres_hist (host, may be
+ * NULL, maxit+1 entries) receives ||r_k||/||b||.  Synchronises the stream.
+ * Returns FCM_OK, FCM_NOT_CONVERGED (x valid), or an error.                               */
+int fcm_pcg_solve(fcm_mg* h, const double* b, double* x, double rtol, int32_t maxit,
+                  int32_t* iters, double* relres_hist);
+
+/* Same as fcm_pcg_solve with HOST b and x (pinned or pageable): copies b in, solves,
+ * copies x out, all inside the call (the end-to-end user path).                           */
+int fcm_pcg_solve_host(fcm_mg* h, const double* b_host, double* x_host, double rtol,
+                       int32_t maxit, int32_t* iters, double* relres_hist);
+
+/* Statistics of the last fcm_pcg_solve: total inner coarse CG iterations, V-cycles.       */
+int fcm_mg_stats(const fcm_mg* h, int64_t* coarse_iters_total, int64_t* vcycles);
+
+/* Counters of kernels launched by the library since setup (for the bench's gpu_launches). */
+int fcm_mg_launch_count(const fcm_mg* h, int64_t* launches);
+
+/* Thread-local message of the last error ("" if none).                                     */
+const char* fcm_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FCM_MG_H */

@@ -1,0 +1,1372 @@
+// fcm_mg.cu -- B200 (sm_100a) implementation of the C ABI in include/fcm_mg.h.
+//
+// Hot path:
+//   (a3) level operator apply    k_cellop<G> OP_APPLY   r -= A_q x
+//   (a4) additive Schwarz        k_cellop<G> OP_SMOOTH  x += w M^-1 r
+//   (a5) restriction / prolong.  pointer alias (prefix) / k_axpy on the prefix
+//   (a6) coarsest level p=1      k_coarse_pcg<G> (cooperative, whole inner CG in one launch)
+//                                or k_dense_gemv with a setup-time inverse
+//   (a2) V-cycle                 enqueue_vcycle (Algorithm 1), CUDA graph
+//   (a1) flexible PCG            fcm_pcg_solve
+//   (a7) BLAS-1                  deterministic block partials, device-resident scalars
+// Setup (a0): Schwarz block classification (shared-by-type vs individual), block assembly
+// A_i = P_i^T A_q P_i and in-place Gauss-Jordan inversion on the device.
+#include <cooperative_groups.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../../include/fcm_mg.h"
+#include "cellop.cuh"
+#include "common.hpp"
+#include "layout.hpp"
+
+namespace cg = cooperative_groups;
+using namespace fcm;
+
+#define CU(call)                                                                       \
+  do {                                                                                 \
+    cudaError_t e_ = (call);                                                           \
+    if (e_ != cudaSuccess)                                                             \
+      return fail(e_ == cudaErrorMemoryAllocation ? FCM_ENOMEM : FCM_ECUDA, "%s: %s (%s:%d)", \
+                  #call, cudaGetErrorString(e_), __FILE__, __LINE__);                  \
+  } while (0)
+
+#define RC(call)           \
+  do {                     \
+    int rc_ = (call);      \
+    if (rc_ < 0) return rc_; \
+  } while (0)
+
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kMaxPartials = 2048;
+
+struct Scalars {
+  double rz, pq, rr, zr, zr_old, bb;
+  int flag;  // bit0: p^T A p <= 0
+};
+
+struct LevelDev {
+  int q = 0, m = 0, G = 32;
+  int64_t ndof = 0;
+  int64_t* base = nullptr;
+  int32_t* stride = nullptr;
+  int16_t* cmin = nullptr;
+  int16_t* cmax = nullptr;
+  // additive Schwarz
+  bool has_as = false;
+  double omega = 1.0;
+  int32_t* blk = nullptr;
+  double* irr_inv = nullptr;
+  double* type_inv = nullptr;
+  int64_t n_irr = 0;
+  int32_t n_types = 0;
+  int M = 0;                       // compile-time block size of the regular path (0: generic)
+  const void* kcell = nullptr;     // k_cellop<M,G>
+  int32_t* irr_list = nullptr;     // cells with an individual Schwarz inverse (irr order)
+  // vectors
+  double* x = nullptr;
+  double* r = nullptr;
+};
+
+}  // namespace
+
+struct fcm_mg {
+  Layout L;
+  fcm_grid g{};
+  fcm_params prm{};
+  cudaStream_t stream = nullptr;   // internal non-blocking stream (capturable)
+  cudaStream_t ustream = nullptr;  // the caller's stream (params.stream)
+  cudaEvent_t ev_in = nullptr, ev_out = nullptr;
+  int dev = 0, num_sms = 148;
+  double alpha = 1e-8;
+  int64_t ncell = 0, ncut = 0;
+  uint8_t* d_kind = nullptr;
+  int32_t* d_cut_idx = nullptr;
+  int32_t* d_cut_list = nullptr;  // cut cells in cut order
+  const void* kcoarse = nullptr;
+  double* d_Kref = nullptr;
+  double* d_cutK = nullptr;
+  std::vector<LevelDev> lev;  // index q = 1..p
+  // coarse
+  double* d_A0inv = nullptr;   // direct
+  double* d_diag_inv = nullptr;  // Jacobi
+  double *c_r = nullptr, *c_z = nullptr, *c_p = nullptr, *c_q = nullptr;
+  int* d_coarse_iters = nullptr;
+  int coarse_blocks = 0;
+  // FCG
+  double *f_b = nullptr, *f_x = nullptr, *f_r = nullptr, *f_ro = nullptr, *f_p = nullptr, *f_q = nullptr;
+  Scalars* d_s = nullptr;
+  Scalars* h_s = nullptr;  // pinned
+  int* h_iters = nullptr;  // pinned
+  double* d_partA = nullptr;
+  double* d_partB = nullptr;
+  double* d_partC = nullptr;
+  // graphs
+  cudaGraphExec_t g_vc = nullptr, g_it1 = nullptr, g_it2 = nullptr, g_init = nullptr;
+  int64_t n_vc = 0, n_it1 = 0, n_it2 = 0, n_init = 0;  // kernels per graph
+  int64_t launches = 0;
+  int64_t* count_target = nullptr;  // during capture: where launches are counted
+  int64_t stat_coarse = 0, stat_vcycles = 0;
+  std::vector<void*> allocs;
+
+  template <typename T>
+  int alloc(T** p, size_t n) {
+    size_t bytes = std::max<size_t>(1, n * sizeof(T));
+    cudaError_t e = cudaMalloc((void**)p, bytes);
+    if (e != cudaSuccess)
+      return fail(FCM_ENOMEM, "cudaMalloc of %zu bytes failed: %s", bytes, cudaGetErrorString(e));
+    allocs.push_back(*p);
+    return FCM_OK;
+  }
+  void count(int64_t k = 1) {
+    if (count_target) *count_target += k;
+    else launches += k;
+  }
+  ~fcm_mg() {
+    for (auto g : {g_vc, g_it1, g_it2, g_init})
+      if (g) cudaGraphExecDestroy(g);
+    for (void* p : allocs) cudaFree(p);
+    if (h_s) cudaFreeHost(h_s);
+    if (h_iters) cudaFreeHost(h_iters);
+    if (ev_in) cudaEventDestroy(ev_in);
+    if (ev_out) cudaEventDestroy(ev_out);
+    if (stream) cudaStreamDestroy(stream);
+  }
+};
+
+// =========================================================================================
+// kernels
+// =========================================================================================
+namespace {
+
+// dynamic shared memory: [Tab][Ms: M*M doubles][xs: wpb*CPW*m doubles][ids: wpb*CPW*m ints]
+struct CellSmem {
+  Tab* T;
+  double* Ms;
+  double* xs;
+  int* ids;
+};
+template <int M, int G>
+__device__ __forceinline__ CellSmem carve(unsigned char* smem, int m) {
+  constexpr int CPW = 32 / G;
+  const int wpb = blockDim.x >> 5;
+  CellSmem s;
+  s.T = reinterpret_cast<Tab*>(smem);
+  s.Ms = reinterpret_cast<double*>(smem + sizeof(Tab));
+  double* xs0 = s.Ms + M * M;
+  s.xs = xs0 + (threadIdx.x >> 5) * CPW * m;
+  s.ids = reinterpret_cast<int*>(xs0 + wpb * CPW * m) + (threadIdx.x >> 5) * CPW * m;
+  return s;
+}
+
+// One launch covers both populations: blocks [0, nb_reg) run the thread-per-cell regular path
+// (compile-time M), blocks [nb_reg, grid) the group-per-cell individual list (or, for M == 0,
+// every cell with per-cell matrix selection).
+template <int M, int G>
+__global__ void __launch_bounds__(kThreads) k_cellop(CellOp op, int nb_reg) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  CellSmem s = carve<M, G>(smem, op.m);
+  __shared__ double red[32];
+  load_tab(*s.T, op);
+  if (M > 0 && (int)blockIdx.x < nb_reg) load_shared_matrix<(M > 0 ? M : 1)>(s.Ms, op);
+  __syncthreads();
+  double e = 0.0;
+  if ((int)blockIdx.x < nb_reg) {
+    if constexpr (M > 0) e = reg_cells<M>(op, *s.T, s.Ms, blockIdx.x * blockDim.x + threadIdx.x, nb_reg * blockDim.x);
+  } else {
+    const int wpb = blockDim.x >> 5;
+    const int warp = (blockIdx.x - nb_reg) * wpb + (threadIdx.x >> 5);
+    const int nwarps = (gridDim.x - nb_reg) * wpb;
+    e = list_cells<G>(op, *s.T, warp, nwarps, s.xs, s.ids);
+  }
+  if (op.partials) {
+    double t = block_sum(e, red);
+    if (threadIdx.x == 0) op.partials[blockIdx.x] = t;
+  }
+}
+
+__global__ void k_fill(double* x, double v, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    x[i] = v;
+}
+__global__ void k_copy(double* __restrict__ y, const double* __restrict__ x, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    y[i] = x[i];
+}
+__global__ void k_axpy(double* __restrict__ y, double a, const double* __restrict__ x, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    y[i] = fma(a, x[i], y[i]);
+}
+// partials[block] = sum a.b over the block's grid-stride range (fixed grid -> deterministic)
+__global__ void k_dot(const double* __restrict__ a, const double* __restrict__ b, int64_t n, double* partials) {
+  __shared__ double red[32];
+  double s = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    s = fma(a[i], b[i], s);
+  s = block_sum(s, red);
+  if (threadIdx.x == 0) partials[blockIdx.x] = s;
+}
+// Deterministic sum of n block partials (fixed lane assignment and shuffle tree): warp 0
+// reduces, the result is broadcast through shared memory.  Must be called by all threads.
+__device__ __forceinline__ double sum_partials(const double* p, int n) {
+  __shared__ double bc;
+  if (threadIdx.x < 32) {
+    double s = 0.0;
+    for (int i = threadIdx.x; i < n; i += 32) s += p[i];
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+    if (threadIdx.x == 0) bc = s;
+  }
+  __syncthreads();
+  const double v = bc;
+  __syncthreads();
+  return v;
+}
+// x = 0, r = b (FCG start); z set later by the V-cycle
+__global__ void k_fcg_start(double* x, double* r, const double* b, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    x[i] = 0.0;
+    r[i] = b[i];
+  }
+}
+// rz = sum partials(z.r); p = z
+__global__ void k_fcg_start2(Scalars* s, const double* part, int np, double* p, const double* z, int64_t n) {
+  const double v = sum_partials(part, np);
+  if (blockIdx.x == 0 && threadIdx.x == 0) s->rz = v;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = z[i];
+}
+// pq = sum partials; alpha = rz/pq; x += alpha p; r_old = r; r -= alpha q; partial rr
+__global__ void k_fcg_update1(Scalars* s, const double* part_pq, int npq, double* __restrict__ x,
+                              double* __restrict__ r, double* __restrict__ r_old,
+                              const double* __restrict__ p, const double* __restrict__ q, int64_t n,
+                              double* part_rr) {
+  __shared__ double red[32];
+  const double pq = sum_partials(part_pq, npq);
+  const double alpha = s->rz / pq;
+  double rr = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    x[i] = fma(alpha, p[i], x[i]);
+    const double ri = r[i];
+    r_old[i] = ri;
+    const double rn = fma(-alpha, q[i], ri);
+    r[i] = rn;
+    rr = fma(rn, rn, rr);
+  }
+  rr = block_sum(rr, red);
+  if (threadIdx.x == 0) part_rr[blockIdx.x] = rr;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    s->pq = pq;
+    if (!(pq > 0.0)) s->flag |= 1;
+  }
+}
+__global__ void k_finalize(double* out, const double* part, int np) {
+  const double v = sum_partials(part, np);
+  if (threadIdx.x == 0) *out = v;
+}
+// partials of z.r and z.r_old (two sets)
+__global__ void k_dot2(const double* __restrict__ z, const double* __restrict__ r,
+                       const double* __restrict__ ro, int64_t n, double* partA, double* partB) {
+  __shared__ double red[32];
+  double s1 = 0.0, s2 = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const double zi = z[i];
+    s1 = fma(zi, r[i], s1);
+    s2 = fma(zi, ro[i], s2);
+  }
+  s1 = block_sum(s1, red);
+  s2 = block_sum(s2, red);
+  if (threadIdx.x == 0) { partA[blockIdx.x] = s1; partB[blockIdx.x] = s2; }
+}
+// beta = (z.r - z.r_old) / rz_old ; rz = z.r ; p = z + beta p   (Polak-Ribiere, reading R5)
+__global__ void k_fcg_update2(Scalars* s, const double* partA, const double* partB, int np,
+                              double* __restrict__ p, const double* __restrict__ z, int64_t n) {
+  const double zr = sum_partials(partA, np);
+  const double zro = sum_partials(partB, np);
+  const double beta = (zr - zro) / s->rz;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = fma(beta, p[i], z[i]);
+  __syncthreads();
+  if (blockIdx.x == 0 && threadIdx.x == 0) { s->zr = zr; s->zr_old = zro; }
+  // rz updated by the last block to finish reading it: use a separate write after grid end
+}
+__global__ void k_set_rz(Scalars* s) {
+  if (threadIdx.x == 0) s->rz = s->zr;
+}
+// x = Ainv b (dense, row-major, symmetric)
+__global__ void k_dense_gemv(const double* __restrict__ A, const double* __restrict__ b,
+                             double* __restrict__ x, int64_t n) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t row = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; row < n;
+       row += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    double s = 0.0;
+    for (int64_t j = lane; j < n; j += 32) s = fma(A[row * n + j], b[j], s);
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+    if (lane == 0) x[row] = s;
+  }
+}
+
+// ---- setup: Schwarz block assembly A_i = P_i^T A_q P_i -----------------
+struct AsmArgs {
+  int nx, ny, nz, dim, m, ldK;  // m = m_q
+  const int64_t* cells;         // block -> cell index (or representative coordinates)
+  const uint8_t* virt;          // 1: assume every neighbour is uncut physical (type block)
+  const int16_t* nbmap;         // [3^d][m] local index in neighbour cell (-1 none)
+  const int8_t* dirich;         // [nblocks][m] 1 if Dirichlet
+  const uint8_t* kind;
+  const int32_t* cut_idx;
+  const double* Kref;
+  const double* cutK;
+  double alpha;
+  double* out;                  // [nblocks][m][m]
+};
+__global__ void k_assemble_blocks(AsmArgs a) {
+  const int64_t blk = blockIdx.x;
+  const int64_t c = a.cells[blk];
+  const int cx = (int)(c % a.nx), cy = (int)((c / a.nx) % a.ny), cz = (int)(c / ((int64_t)a.nx * a.ny));
+  const int m = a.m;
+  double* A = a.out + blk * (int64_t)m * m;
+  const int8_t* dir = a.dirich + blk * m;
+  const int nd = a.dim == 3 ? 27 : 9;
+  for (int e = threadIdx.x; e < m * m; e += blockDim.x) {
+    const int i = e / m, j = e % m;
+    double s = 0.0;
+    if (dir[i] || dir[j]) {
+      s = (i == j) ? 1.0 : 0.0;
+    } else {
+      for (int d = 0; d < nd; ++d) {
+        const int dx = d % 3 - 1, dy = (d / 3) % 3 - 1, dz = a.dim == 3 ? d / 9 - 1 : 0;
+        const int ncx = cx + dx, ncy = cy + dy, ncz = cz + dz;
+        if (ncx < 0 || ncy < 0 || ncz < 0 || ncx >= a.nx || ncy >= a.ny || ncz >= a.nz) continue;
+        const int ii = a.nbmap[d * m + i], jj = a.nbmap[d * m + j];
+        if (ii < 0 || jj < 0) continue;
+        const int64_t nc = ((int64_t)ncz * a.ny + ncy) * a.nx + ncx;
+        double v;
+        if (a.virt[blk]) {
+          v = a.Kref[(int64_t)ii * a.ldK + jj];
+        } else {
+          const uint8_t k = a.kind[nc];
+          if (k == 2) v = a.cutK[(int64_t)a.cut_idx[nc] * a.ldK * a.ldK + (int64_t)ii * a.ldK + jj];
+          else v = a.Kref[(int64_t)ii * a.ldK + jj] * (k == 1 ? a.alpha : 1.0);
+        }
+        s += v;
+      }
+    }
+    A[e] = s;
+  }
+}
+
+// Inversion of SPD blocks: Cholesky A = L L^T (right-looking, L in shared memory), then
+// X = A^{-1} column by column by forward/backward substitution (one thread per column,
+// the column lives in the output block), symmetrised.  Backward stable.
+// status[blk] = 1 if a pivot was not positive/finite (not SPD / singular).
+__device__ void chol_inverse(double* L, double* X, int64_t m, int* bad) {
+  // L: m*m working matrix (lower triangle used), X: output m*m (global)
+  for (int64_t k = 0; k < m; ++k) {
+    if (threadIdx.x == 0) {
+      const double d = L[k * m + k];
+      if (!(d > 0.0 && isfinite(d))) *bad = 1;
+      L[k * m + k] = sqrt(fmax(d, 1e-300));
+    }
+    __syncthreads();
+    const double dk = L[k * m + k];
+    for (int64_t i = k + 1 + threadIdx.x; i < m; i += blockDim.x) L[i * m + k] /= dk;
+    __syncthreads();
+    const int64_t r = m - k - 1;  // trailing lower triangle update
+    for (int64_t e = threadIdx.x; e < r * r; e += blockDim.x) {
+      const int64_t i = k + 1 + e / r, j = k + 1 + e % r;
+      if (j <= i) L[i * m + j] -= L[i * m + k] * L[j * m + k];
+    }
+    __syncthreads();
+  }
+  for (int64_t j = threadIdx.x; j < m; j += blockDim.x) {
+    // forward: L y = e_j  (y_i = 0 for i < j)
+    for (int64_t i = 0; i < j; ++i) X[i * m + j] = 0.0;
+    for (int64_t i = j; i < m; ++i) {
+      double s = (i == j) ? 1.0 : 0.0;
+      for (int64_t k = j; k < i; ++k) s -= L[i * m + k] * X[k * m + j];
+      X[i * m + j] = s / L[i * m + i];
+    }
+    // backward: L^T x = y
+    for (int64_t i = m - 1; i >= 0; --i) {
+      double s = X[i * m + j];
+      for (int64_t k = i + 1; k < m; ++k) s -= L[k * m + i] * X[k * m + j];
+      X[i * m + j] = s / L[i * m + i];
+    }
+  }
+  __syncthreads();
+  for (int64_t e = threadIdx.x; e < m * m; e += blockDim.x) {
+    const int64_t i = e / m, j = e % m;
+    if (i < j) {
+      const double s = 0.5 * (X[i * m + j] + X[j * m + i]);
+      X[i * m + j] = s;
+      X[j * m + i] = s;
+    }
+  }
+  __syncthreads();
+}
+
+__global__ void k_invert_blocks(double* mats, int m, int* status, int64_t nblocks) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  double* A = reinterpret_cast<double*>(smem);
+  __shared__ int bad;
+  for (int64_t blk = blockIdx.x; blk < nblocks; blk += gridDim.x) {
+    double* G = mats + blk * (int64_t)m * m;
+    for (int e = threadIdx.x; e < m * m; e += blockDim.x) A[e] = G[e];
+    if (threadIdx.x == 0) bad = 0;
+    __syncthreads();
+    chol_inverse(A, G, m, &bad);
+    if (threadIdx.x == 0) status[blk] = bad;
+    __syncthreads();
+  }
+}
+
+// dense inverse of the SPD coarse matrix (direct coarse solve): A is overwritten by its
+// Cholesky factor, X receives A^{-1}.
+__global__ void k_invert_dense(double* A, int64_t n, double* X, int* status) {
+  __shared__ int bad;
+  if (threadIdx.x == 0) bad = 0;
+  __syncthreads();
+  chol_inverse(A, X, n, &bad);
+  if (threadIdx.x == 0) *status = bad;
+}
+
+// ---- coarse level: whole preconditioned CG in one cooperative launch ----
+struct CoarseArgs {
+  CellOp A;                    // apply: in = p, out = q
+  CellOp M;                    // AS smoother: in = r, out = z (coef 1)
+  int jacobi;
+  const double* diag_inv;
+  const double* b;
+  double* x;
+  double *r, *z, *p, *q;
+  int64_t n;
+  double rtol2;
+  int maxit;
+  double* partA;
+  double* partB;
+  int* iters;
+};
+
+// one cell phase of the coarse solver: regular cells (thread per cell) + individual list
+template <int M, int G>
+__device__ __forceinline__ double coarse_cells(const CellOp& op, const Tab& T, const double* Ms,
+                                               double* xs, int* ids) {
+  const int wpb = blockDim.x >> 5;
+  double e = 0.0;
+  if constexpr (M > 0) e = reg_cells<M>(op, T, Ms, blockIdx.x * blockDim.x + threadIdx.x, gridDim.x * blockDim.x);
+  e += list_cells<G>(op, T, blockIdx.x * wpb + (threadIdx.x >> 5), gridDim.x * wpb, xs, ids);
+  return e;
+}
+
+// smem: [Tab][MsA: M*M][MsM: M*M][xs][ids]
+template <int M, int G>
+__global__ void __launch_bounds__(kThreads) k_coarse_pcg(CoarseArgs a) {
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ __align__(16) unsigned char smem[];
+  constexpr int CPW = 32 / G;
+  const int wpb = blockDim.x >> 5;
+  const int m = a.A.m;
+  Tab& T = *reinterpret_cast<Tab*>(smem);
+  double* MsA = reinterpret_cast<double*>(smem + sizeof(Tab));
+  double* MsM = MsA + M * M;
+  double* xs0 = MsM + M * M;
+  double* xs = xs0 + (threadIdx.x >> 5) * CPW * m;
+  int* ids = reinterpret_cast<int*>(xs0 + wpb * CPW * m) + (threadIdx.x >> 5) * CPW * m;
+  __shared__ double red[32];
+  load_tab(T, a.A);
+  if constexpr (M > 0) {
+    load_shared_matrix<M>(MsA, a.A);
+    if (!a.jacobi) load_shared_matrix<M>(MsM, a.M);
+  }
+  __syncthreads();
+  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t nth = (int64_t)gridDim.x * blockDim.x;
+  const int nb = gridDim.x;
+  const int64_t n = a.n;
+
+  // x = 0, r = b, z = 0, q = 0 ; rr0 = b.b
+  double s = 0.0;
+  for (int64_t i = tid; i < n; i += nth) {
+    const double bi = a.b[i];
+    a.x[i] = 0.0; a.r[i] = bi; a.z[i] = 0.0; a.q[i] = 0.0;
+    s = fma(bi, bi, s);
+  }
+  s = block_sum(s, red);
+  if (threadIdx.x == 0) a.partA[blockIdx.x] = s;
+  grid.sync();
+  const double rr0 = sum_partials(a.partA, nb);
+  int it = 0;
+  if (rr0 > 0.0) {
+    // z = M^-1 r ; rz
+    if (a.jacobi) {
+      s = 0.0;
+      for (int64_t i = tid; i < n; i += nth) { const double zi = a.diag_inv[i] * a.r[i]; a.z[i] = zi; s = fma(zi, a.r[i], s); }
+    } else {
+      s = coarse_cells<M, G>(a.M, T, MsM, xs, ids);
+    }
+    s = block_sum(s, red);
+    if (threadIdx.x == 0) a.partB[blockIdx.x] = s;
+    grid.sync();
+    double rz = sum_partials(a.partB, nb);
+    for (int64_t i = tid; i < n; i += nth) a.p[i] = a.z[i];
+    grid.sync();
+    while (true) {
+      // P1: q = A p ; pq
+      s = coarse_cells<M, G>(a.A, T, MsA, xs, ids);
+      s = block_sum(s, red);
+      if (threadIdx.x == 0) a.partA[blockIdx.x] = s;
+      grid.sync();
+      // P2: alpha ; x += alpha p ; r -= alpha q ; z = 0 ; rr
+      const double pq = sum_partials(a.partA, nb);
+      const double alpha = rz / pq;
+      s = 0.0;
+      for (int64_t i = tid; i < n; i += nth) {
+        a.x[i] = fma(alpha, a.p[i], a.x[i]);
+        const double rn = fma(-alpha, a.q[i], a.r[i]);
+        a.r[i] = rn;
+        a.z[i] = 0.0;
+        s = fma(rn, rn, s);
+      }
+      s = block_sum(s, red);
+      if (threadIdx.x == 0) a.partB[blockIdx.x] = s;
+      grid.sync();
+      // P3: convergence test ; z = M^-1 r ; rz_new ; q = 0
+      const double rr = sum_partials(a.partB, nb);
+      ++it;
+      if (!(pq > 0.0) || rr < a.rtol2 * rr0 || it >= a.maxit) break;
+      if (a.jacobi) {
+        s = 0.0;
+        for (int64_t i = tid; i < n; i += nth) { const double zi = a.diag_inv[i] * a.r[i]; a.z[i] = zi; s = fma(zi, a.r[i], s); }
+      } else {
+        s = coarse_cells<M, G>(a.M, T, MsM, xs, ids);
+      }
+      for (int64_t i = tid; i < n; i += nth) a.q[i] = 0.0;
+      s = block_sum(s, red);
+      if (threadIdx.x == 0) a.partA[blockIdx.x] = s;
+      grid.sync();
+      // P4: beta ; p = z + beta p
+      const double rz_new = sum_partials(a.partA, nb);
+      const double beta = rz_new / rz;
+      rz = rz_new;
+      for (int64_t i = tid; i < n; i += nth) a.p[i] = fma(beta, a.p[i], a.z[i]);
+      grid.sync();
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) { a.iters[0] = it; a.iters[1] += it; }
+}
+
+// ---- compile-time M dispatch --------------------------------------------------------------
+template <int M> constexpr int gsz() { return M <= 4 ? 4 : (M <= 8 ? 8 : (M <= 16 ? 16 : 32)); }
+#define FCM_FOR_M(X) X(4) X(8) X(9) X(16) X(24) X(25) X(27)
+
+const void* cellop_kernel(int m, int G, int* M_out) {
+#define CASE(MM) case MM: *M_out = MM; return (const void*)k_cellop<MM, gsz<MM>()>;
+  switch (m) { FCM_FOR_M(CASE) default: break; }
+#undef CASE
+  *M_out = 0;
+  switch (G) {
+    case 4: return (const void*)k_cellop<0, 4>;
+    case 8: return (const void*)k_cellop<0, 8>;
+    case 16: return (const void*)k_cellop<0, 16>;
+    default: return (const void*)k_cellop<0, 32>;
+  }
+}
+const void* coarse_kernel(int m, int G, int* M_out) {
+#define CASE(MM) case MM: *M_out = MM; return (const void*)k_coarse_pcg<MM, gsz<MM>()>;
+  switch (m) { FCM_FOR_M(CASE) default: break; }
+#undef CASE
+  *M_out = 0;
+  switch (G) {
+    case 4: return (const void*)k_coarse_pcg<0, 4>;
+    case 8: return (const void*)k_coarse_pcg<0, 8>;
+    case 16: return (const void*)k_coarse_pcg<0, 16>;
+    default: return (const void*)k_coarse_pcg<0, 32>;
+  }
+}
+
+inline int grid_for(int64_t n, int sms) {
+  int64_t b = (n + kThreads - 1) / kThreads;
+  return (int)std::max<int64_t>(1, std::min<int64_t>(b, (int64_t)sms * 4));
+}
+
+}  // namespace
+
+// =========================================================================================
+// host helpers
+// =========================================================================================
+static int group_size(int m) {
+  if (m <= 4) return 4;
+  if (m <= 8) return 8;
+  if (m <= 16) return 16;
+  return 32;
+}
+
+static size_t cellop_smem(int m, int M, int G, int nmat) {
+  return sizeof(Tab) + (size_t)nmat * M * M * sizeof(double) +
+         (size_t)(kThreads / 32) * (32 / G) * m * (sizeof(double) + sizeof(int));
+}
+
+static CellOp make_op(fcm_mg* h, int q, int mode, const double* in, double* out, double coef,
+                      double* partials) {
+  LevelDev& Lv = h->lev[q];
+  CellOp op{};
+  op.nx = h->L.n[0]; op.ny = h->L.n[1]; op.nz = h->L.n[2];
+  op.m = Lv.m;
+  op.ncell = (int32_t)h->ncell;
+  op.base = Lv.base; op.stride = Lv.stride; op.cmin = Lv.cmin; op.cmax = Lv.cmax;
+  op.mode = mode;
+  op.kind = h->d_kind; op.cut_idx = h->d_cut_idx; op.Kref = h->d_Kref; op.cutK = h->d_cutK;
+  op.ldK = h->L.m; op.alpha = h->alpha;
+  op.blk = Lv.blk; op.irr_inv = Lv.irr_inv; op.type_inv = Lv.type_inv; op.inv_alpha = 1.0 / h->alpha;
+  if (Lv.M > 0) {
+    if (mode == OP_APPLY) {
+      op.list = h->d_cut_list; op.nlist = (int32_t)h->ncut; op.list_mats = h->d_cutK; op.list_ld = h->L.m;
+    } else {
+      op.list = Lv.irr_list; op.nlist = (int32_t)Lv.n_irr; op.list_mats = Lv.irr_inv; op.list_ld = Lv.m;
+    }
+  }
+  op.in = in; op.out = out; op.coef = coef; op.partials = partials;
+  return op;
+}
+
+// grid of one cell-operator launch: regular thread-per-cell blocks + individual-list blocks
+static void cellop_grid(const fcm_mg* h, int q, int mode, int* nb_reg, int* nb_list) {
+  const LevelDev& Lv = h->lev[q];
+  const int64_t cap = (int64_t)h->num_sms * 8;
+  const int64_t cpb = (kThreads / 32) * (32 / Lv.G);  // cells per block on the list path
+  if (Lv.M > 0) {
+    *nb_reg = (int)std::min<int64_t>((h->ncell + kThreads - 1) / kThreads, cap);
+    const int64_t nl = mode == OP_APPLY ? h->ncut : Lv.n_irr;
+    *nb_list = (int)std::min<int64_t>((nl + cpb - 1) / cpb, cap);
+  } else {
+    *nb_reg = 0;
+    *nb_list = (int)std::max<int64_t>(1, std::min<int64_t>((h->ncell + cpb - 1) / cpb, cap));
+  }
+}
+static int cellop_nblocks(const fcm_mg* h, int q, int mode) {
+  int a, b;
+  cellop_grid(h, q, mode, &a, &b);
+  return a + b;
+}
+
+static int launch_cellop(fcm_mg* h, int q, const CellOp& op) {
+  const LevelDev& Lv = h->lev[q];
+  int nb_reg, nb_list;
+  cellop_grid(h, q, op.mode, &nb_reg, &nb_list);
+  if (nb_reg + nb_list == 0) return FCM_OK;
+  size_t sm = cellop_smem(Lv.m, Lv.M, Lv.G, 1);
+  CellOp o = op;
+  void* args[] = {&o, &nb_reg};
+  cudaError_t e = cudaLaunchKernel(Lv.kcell, dim3(nb_reg + nb_list), dim3(kThreads), args, sm, h->stream);
+  h->count();
+  if (e != cudaSuccess) return fail(FCM_ECUDA, "cell kernel launch: %s", cudaGetErrorString(e));
+  return FCM_OK;
+}
+
+static int fill(fcm_mg* h, double* x, double v, int64_t n) {
+  if (n <= 0) return FCM_OK;
+  k_fill<<<grid_for(n, h->num_sms), kThreads, 0, h->stream>>>(x, v, n);
+  h->count();
+  CU(cudaGetLastError());
+  return FCM_OK;
+}
+static int copy(fcm_mg* h, double* y, const double* x, int64_t n) {
+  if (n <= 0) return FCM_OK;
+  k_copy<<<grid_for(n, h->num_sms), kThreads, 0, h->stream>>>(y, x, n);
+  h->count();
+  CU(cudaGetLastError());
+  return FCM_OK;
+}
+
+// r = b - A_q x
+static int residual(fcm_mg* h, int q, const double* b, const double* x, double* r) {
+  RC(copy(h, r, b, h->lev[q].ndof));
+  return launch_cellop(h, q, make_op(h, q, OP_APPLY, x, r, -1.0, nullptr));
+}
+// x += omega M^-1 r
+static int smooth(fcm_mg* h, int q, const double* r, double* x) {
+  return launch_cellop(h, q, make_op(h, q, OP_SMOOTH, r, x, h->lev[q].omega, nullptr));
+}
+
+static int enqueue_coarse(fcm_mg* h, const double* b, double* x) {
+  LevelDev& L1 = h->lev[1];
+  const int64_t n = L1.ndof;
+  if (h->prm.coarse == FCM_COARSE_DIRECT) {
+    k_dense_gemv<<<grid_for(n * 32, h->num_sms), kThreads, 0, h->stream>>>(h->d_A0inv, b, x, n);
+    h->count();
+    CU(cudaGetLastError());
+    return FCM_OK;
+  }
+  CoarseArgs a{};
+  a.A = make_op(h, 1, OP_APPLY, h->c_p, h->c_q, 1.0, nullptr);
+  a.M = make_op(h, 1, OP_SMOOTH, h->c_r, h->c_z, 1.0, nullptr);
+  a.jacobi = h->prm.coarse == FCM_COARSE_JACOBI_PCG;
+  a.diag_inv = h->d_diag_inv;
+  a.b = b; a.x = x; a.r = h->c_r; a.z = h->c_z; a.p = h->c_p; a.q = h->c_q;
+  a.n = n;
+  a.rtol2 = h->prm.coarse_rtol * h->prm.coarse_rtol;
+  a.maxit = h->prm.coarse_maxit;
+  a.partA = h->d_partA + kMaxPartials;  // separate from the FCG partials
+  a.partB = h->d_partB + kMaxPartials;
+  a.iters = h->d_coarse_iters;
+  void* args[] = {&a};
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(h->coarse_blocks);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = cellop_smem(L1.m, L1.M, L1.G, 2);
+  cfg.stream = h->stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelExC(&cfg, h->kcoarse, args);
+  h->count();
+  return FCM_OK;
+}
+
+// Algorithm 1 on level q: x = V_q(b), x~ = 0 on entry; reading R1.
+static int enqueue_vcycle(fcm_mg* h, int q, const double* b, double* x) {
+  if (q == 1) return enqueue_coarse(h, b, x);
+  LevelDev& Lv = h->lev[q];
+  const int64_t N = Lv.ndof;
+  RC(fill(h, x, 0.0, N));
+  for (int s = 0; s < h->prm.n_pre; ++s) {          // pre-smoothing
+    if (s == 0) RC(smooth(h, q, b, x));             // x = 0: r = b
+    else { RC(residual(h, q, b, x, Lv.r)); RC(smooth(h, q, Lv.r, x)); }
+  }
+  if (h->prm.n_pre > 0) RC(residual(h, q, b, x, Lv.r));  // update residual
+  else RC(copy(h, Lv.r, b, N));
+  LevelDev& Lc = h->lev[q - 1];
+  RC(enqueue_vcycle(h, q - 1, Lv.r, Lc.x));         // r_{l-1} = R r_l: prefix alias
+  k_axpy<<<grid_for(Lc.ndof, h->num_sms), kThreads, 0, h->stream>>>(x, 1.0, Lc.x, Lc.ndof);  // x += R^T e
+  h->count();
+  CU(cudaGetLastError());
+  for (int s = 0; s < h->prm.n_post; ++s) {         // P:169 residual, post-smoothing
+    RC(residual(h, q, b, x, Lv.r));
+    RC(smooth(h, q, Lv.r, x));
+  }
+  return FCM_OK;
+}
+
+// capture a host enqueue sequence into an executable graph
+template <typename F>
+static int capture(fcm_mg* h, cudaGraphExec_t* exec, int64_t* nkernels, F&& body) {
+  if (*exec) return FCM_OK;
+  cudaGraph_t graph;
+  *nkernels = 0;
+  h->count_target = nkernels;
+  CU(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
+  int rc = body();
+  cudaError_t e = cudaStreamEndCapture(h->stream, &graph);
+  h->count_target = nullptr;
+  if (rc < 0) { if (e == cudaSuccess) cudaGraphDestroy(graph); return rc; }
+  if (e != cudaSuccess) return fail(FCM_ECUDA, "graph capture: %s", cudaGetErrorString(e));
+  e = cudaGraphInstantiate(exec, graph, 0);
+  cudaGraphDestroy(graph);
+  if (e != cudaSuccess) return fail(FCM_ECUDA, "graph instantiate: %s", cudaGetErrorString(e));
+  return FCM_OK;
+}
+
+static int run_graph(fcm_mg* h, cudaGraphExec_t g, int64_t nk) {
+  CU(cudaGraphLaunch(g, h->stream));
+  h->launches += nk;
+  return FCM_OK;
+}
+
+static int dot_blocks(fcm_mg* h) { return std::min(kMaxPartials, h->num_sms * 2); }
+
+// Work is enqueued on the handle's own non-blocking stream (capturable into graphs); it is
+// ordered after prior work on the caller's stream and the caller's stream after it.
+struct StreamGuard {
+  fcm_mg* h;
+  explicit StreamGuard(fcm_mg* h_) : h(h_) {
+    cudaEventRecord(h->ev_in, h->ustream);
+    cudaStreamWaitEvent(h->stream, h->ev_in, 0);
+  }
+  ~StreamGuard() {
+    cudaEventRecord(h->ev_out, h->stream);
+    cudaStreamWaitEvent(h->ustream, h->ev_out, 0);
+  }
+};
+
+// =========================================================================================
+// setup
+// =========================================================================================
+static int setup_schwarz(fcm_mg* h, int q, const std::vector<uint8_t>& kind,
+                         const std::vector<int32_t>& cut_idx) {
+  const Layout& L = h->L;
+  LevelDev& Lv = h->lev[q];
+  const int m = Lv.m;
+  const int dim = L.dim;
+  const int nd = dim == 3 ? 27 : 9;
+  const int nx = L.n[0], ny = L.n[1], nz = L.n[2];
+  // neighbour map: local DOF a of cell c as a local DOF of cell c + delta
+  std::vector<int16_t> nbmap((size_t)nd * m, -1);
+  for (int d = 0; d < nd; ++d) {
+    int del[3] = {d % 3 - 1, (d / 3) % 3 - 1, dim == 3 ? d / 9 - 1 : 0};
+    for (int a = 0; a < m; ++a) {
+      int off[3];
+      bool ok = true;
+      for (int i = 0; i < 3; ++i) {
+        off[i] = L.dof_off[a][i] - del[i];
+        bool internal = (L.classes[L.dof_class[a]].S >> i) & 1;
+        if (i >= dim) { if (del[i] != 0) ok = false; continue; }
+        if (internal ? off[i] != 0 : (off[i] < 0 || off[i] > 1)) ok = false;
+      }
+      if (ok) nbmap[(size_t)d * m + a] = (int16_t)L.local_of(L.dof_class[a], off);
+    }
+  }
+  // classify blocks: regular (all existing neighbours uncut with one kind) -> shared by
+  // boundary type; otherwise individual.
+  std::vector<int32_t> blk(h->ncell);
+  std::vector<int64_t> blocks;       // cells whose block is assembled
+  std::vector<uint8_t> virt;
+  std::vector<int> type_used(64, 0);
+  std::vector<int64_t> irr_cells;
+  for (int64_t c = 0; c < h->ncell; ++c) {
+    int cc[3];
+    L.cell_coords(c, cc);
+    int k0 = -1;
+    bool regular = true;
+    for (int d = 0; d < nd && regular; ++d) {
+      int n3[3] = {cc[0] + d % 3 - 1, cc[1] + (d / 3) % 3 - 1, cc[2] + (dim == 3 ? d / 9 - 1 : 0)};
+      if (n3[0] < 0 || n3[1] < 0 || n3[2] < 0 || n3[0] >= nx || n3[1] >= ny || n3[2] >= nz) continue;
+      int k = kind[((int64_t)n3[2] * ny + n3[1]) * nx + n3[0]];
+      if (k == 2 || (k0 >= 0 && k != k0)) regular = false;
+      k0 = k;
+    }
+    if (regular) {
+      int code = 0;
+      for (int i = 0; i < 3; ++i) {
+        int ci = (cc[i] == 0 ? 1 : 0) | (cc[i] == L.n[i] - 1 ? 2 : 0);
+        code += ci << (2 * i);
+      }
+      type_used[code] = 1;
+      blk[c] = -(1 + (code | (k0 == 1 ? (1 << 12) : 0)));
+    } else {
+      blk[c] = (int32_t)irr_cells.size();
+      irr_cells.push_back(c);
+    }
+  }
+  // assembly list: types first (representative coordinates, virtual all-physical), then irregular
+  std::vector<int> type_slot;
+  for (int code = 0; code < 64; ++code) {
+    if (!type_used[code]) continue;
+    int cc[3];
+    for (int i = 0; i < 3; ++i) {
+      int ci = (code >> (2 * i)) & 3;
+      cc[i] = ci == 0 ? 1 : (ci == 1 ? 0 : (ci == 2 ? L.n[i] - 1 : 0));
+    }
+    blocks.push_back(((int64_t)cc[2] * ny + cc[1]) * nx + cc[0]);
+    virt.push_back(1);
+    type_slot.push_back(code);
+  }
+  const int64_t ntypes = (int64_t)blocks.size();
+  for (int64_t c : irr_cells) { blocks.push_back(c); virt.push_back(0); }
+  const int64_t nblk = (int64_t)blocks.size();
+  // Dirichlet flags per block row
+  std::vector<int8_t> dir((size_t)nblk * m);
+  for (int64_t b = 0; b < nblk; ++b) {
+    int cc[3];
+    L.cell_coords(blocks[b], cc);
+    for (int a = 0; a < m; ++a) dir[(size_t)b * m + a] = L.dof_index(q, a, cc) < 0;
+  }
+  // device buffers
+  int64_t *d_cells;
+  uint8_t* d_virt;
+  int16_t* d_nb;
+  int8_t* d_dir;
+  double* d_mats;
+  int* d_status;
+  RC(h->alloc(&d_cells, nblk));
+  RC(h->alloc(&d_virt, nblk));
+  RC(h->alloc(&d_nb, (size_t)nd * m));
+  RC(h->alloc(&d_dir, (size_t)nblk * m));
+  RC(h->alloc(&d_mats, (size_t)nblk * m * m));
+  RC(h->alloc(&d_status, nblk));
+  RC(h->alloc(&Lv.blk, h->ncell));
+  RC(h->alloc(&Lv.type_inv, (size_t)64 * m * m));
+  CU(cudaMemcpyAsync(d_cells, blocks.data(), nblk * 8, cudaMemcpyHostToDevice, h->stream));
+  CU(cudaMemcpyAsync(d_virt, virt.data(), nblk, cudaMemcpyHostToDevice, h->stream));
+  CU(cudaMemcpyAsync(d_nb, nbmap.data(), nbmap.size() * 2, cudaMemcpyHostToDevice, h->stream));
+  CU(cudaMemcpyAsync(d_dir, dir.data(), dir.size(), cudaMemcpyHostToDevice, h->stream));
+  CU(cudaMemcpyAsync(Lv.blk, blk.data(), blk.size() * 4, cudaMemcpyHostToDevice, h->stream));
+  AsmArgs aa{};
+  aa.nx = nx; aa.ny = ny; aa.nz = nz; aa.dim = dim; aa.m = m; aa.ldK = L.m;
+  aa.cells = d_cells; aa.virt = d_virt; aa.nbmap = d_nb; aa.dirich = d_dir;
+  aa.kind = h->d_kind; aa.cut_idx = h->d_cut_idx; aa.Kref = h->d_Kref; aa.cutK = h->d_cutK;
+  aa.alpha = h->alpha; aa.out = d_mats;
+  if (nblk > 0) {
+    k_assemble_blocks<<<(unsigned)nblk, kThreads, 0, h->stream>>>(aa);
+    CU(cudaGetLastError());
+    size_t sm = (size_t)m * m * 8 + (size_t)m * 8;
+    CU(cudaFuncSetAttribute(k_invert_blocks, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    int nbk = (int)std::min<int64_t>(nblk, (int64_t)h->num_sms * 8);
+    k_invert_blocks<<<nbk, kThreads, sm, h->stream>>>(d_mats, m, d_status, nblk);
+    CU(cudaGetLastError());
+  }
+  std::vector<int> status(nblk);
+  CU(cudaMemcpyAsync(status.data(), d_status, nblk * 4, cudaMemcpyDeviceToHost, h->stream));
+  CU(cudaStreamSynchronize(h->stream));
+  for (int64_t b = 0; b < nblk; ++b)
+    if (status[b])
+      return fail(FCM_ESINGULAR, "singular Schwarz block on level q=%d: %s block of cell %lld", q,
+                  b < ntypes ? "shared-type" : "individual", (long long)blocks[b]);
+  // scatter type inverses into their slots, keep irregular inverses in place
+  for (int64_t t = 0; t < ntypes; ++t)
+    CU(cudaMemcpyAsync(Lv.type_inv + (size_t)type_slot[t] * m * m, d_mats + (size_t)t * m * m,
+                       (size_t)m * m * 8, cudaMemcpyDeviceToDevice, h->stream));
+  Lv.irr_inv = d_mats + (size_t)ntypes * m * m;
+  Lv.n_irr = (int64_t)irr_cells.size();
+  {
+    std::vector<int32_t> il(irr_cells.begin(), irr_cells.end());
+    RC(h->alloc(&Lv.irr_list, il.size()));
+    CU(cudaMemcpyAsync(Lv.irr_list, il.data(), il.size() * 4, cudaMemcpyHostToDevice, h->stream));
+  }
+  Lv.has_as = true;
+  Lv.n_types = (int32_t)ntypes;
+  return FCM_OK;
+}
+
+// dense assembled level-1 matrix (host) for the direct coarse solver / Jacobi diagonal
+static void coarse_dense(const fcm_mg* h, const std::vector<uint8_t>& kind,
+                         const std::vector<int32_t>& cut_idx, const double* K_ref,
+                         const double* cut_K, std::vector<double>* dense, std::vector<double>* diag) {
+  const Layout& L = h->L;
+  const int m1 = L.m_level[1], m = L.m;
+  const int64_t n = L.ndof_level[1];
+  if (dense) dense->assign((size_t)n * n, 0.0);
+  if (diag) diag->assign(n, 0.0);
+  std::vector<int64_t> idx(m1);
+  for (int64_t c = 0; c < h->ncell; ++c) {
+    int cc[3];
+    L.cell_coords(c, cc);
+    for (int a = 0; a < m1; ++a) idx[a] = L.dof_index(1, a, cc);
+    const double* K = kind[c] == 2 ? cut_K + (size_t)cut_idx[c] * m * m : K_ref;
+    double s = kind[c] == 1 ? h->alpha : 1.0;
+    for (int a = 0; a < m1; ++a) {
+      if (idx[a] < 0) continue;
+      if (diag) (*diag)[idx[a]] += s * K[(size_t)a * m + a];
+      if (dense)
+        for (int b = 0; b < m1; ++b)
+          if (idx[b] >= 0) (*dense)[(size_t)idx[a] * n + idx[b]] += s * K[(size_t)a * m + b];
+    }
+  }
+}
+
+extern "C" int fcm_mg_setup(const fcm_grid* g, const fcm_params* prm, const double* K_ref,
+                            const uint8_t* cell_kind, double alpha, int64_t n_cut,
+                            const int64_t* cut_cells, const double* cut_K, fcm_mg** out) {
+  clear_error();
+  if (!g || !prm || !K_ref || !cell_kind || !out) return fail(FCM_EINVAL, "NULL argument");
+  *out = nullptr;
+  int me = fcm_element_size(g);
+  if (me < 0) return me;
+  if (me > kMaxM) return fail(FCM_EINVAL, "element size m=%d exceeds %d", me, kMaxM);
+  if (n_cut < 0 || (n_cut > 0 && (!cut_cells || !cut_K))) return fail(FCM_EINVAL, "bad cut-cell buffers");
+  if (!(alpha > 0)) return fail(FCM_EINVAL, "alpha must be > 0");
+  if (prm->n_pre < 0 || prm->n_post < 0) return fail(FCM_EINVAL, "negative sweep count");
+  if (prm->coarse < 0 || prm->coarse > 2) return fail(FCM_EINVAL, "unknown coarse solver");
+  if (prm->block != FCM_BLOCK_ELEMENT) return fail(FCM_EINVAL, "patchwise blocks are not implemented yet");
+  std::unique_ptr<fcm_mg> h(new fcm_mg());
+  h->g = *g;
+  h->prm = *prm;
+  h->alpha = alpha;
+  h->ustream = (cudaStream_t)prm->stream;
+  CU(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+  CU(cudaEventCreateWithFlags(&h->ev_in, cudaEventDisableTiming));
+  CU(cudaEventCreateWithFlags(&h->ev_out, cudaEventDisableTiming));
+  CU(cudaEventRecord(h->ev_in, h->ustream));
+  CU(cudaStreamWaitEvent(h->stream, h->ev_in, 0));
+  Layout& L = h->L;
+  L.build(g->dim, g->n, g->p, g->space, g->n_f, g->dirichlet_faces);
+  h->ncell = L.ncell;
+  for (int q = 1; q <= g->p; ++q)
+    if (L.ndof_level[q] <= 0) return fail(FCM_EINVAL, "level q=%d has no free DOFs (empty level)", q);
+  if (h->ncell >= (1LL << 31) || L.ndof_level[g->p] >= (1LL << 31))
+    return fail(FCM_EINVAL, "grid too large for 32-bit cell/DOF indexing on one device");
+  CU(cudaGetDevice(&h->dev));
+  CU(cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, h->dev));
+  // cells
+  std::vector<uint8_t> kind(cell_kind, cell_kind + h->ncell);
+  std::vector<int32_t> cut_idx(h->ncell, -1);
+  for (int64_t i = 0; i < n_cut; ++i) {
+    int64_t c = cut_cells[i];
+    if (c < 0 || c >= h->ncell || kind[c] != 2) return fail(FCM_EINVAL, "cut_cells[%lld] is not a cut cell", (long long)i);
+    cut_idx[c] = (int32_t)i;
+  }
+  for (int64_t c = 0; c < h->ncell; ++c) {
+    if (kind[c] > 2) return fail(FCM_EINVAL, "cell_kind[%lld] = %d", (long long)c, kind[c]);
+    if (kind[c] == 2 && cut_idx[c] < 0) return fail(FCM_EINVAL, "cut cell %lld has no matrix", (long long)c);
+  }
+  h->ncut = n_cut;
+  const int m = L.m;
+  RC(h->alloc(&h->d_kind, h->ncell));
+  RC(h->alloc(&h->d_cut_idx, h->ncell));
+  RC(h->alloc(&h->d_Kref, (size_t)m * m));
+  RC(h->alloc(&h->d_cutK, (size_t)std::max<int64_t>(n_cut, 1) * m * m));
+  CU(cudaMemcpyAsync(h->d_kind, kind.data(), h->ncell, cudaMemcpyHostToDevice, h->stream));
+  CU(cudaMemcpyAsync(h->d_cut_idx, cut_idx.data(), h->ncell * 4, cudaMemcpyHostToDevice, h->stream));
+  {
+    std::vector<int32_t> cl(cut_cells, cut_cells + n_cut);
+    RC(h->alloc(&h->d_cut_list, cl.size()));
+    CU(cudaMemcpyAsync(h->d_cut_list, cl.data(), cl.size() * 4, cudaMemcpyHostToDevice, h->stream));
+  }
+  CU(cudaMemcpyAsync(h->d_Kref, K_ref, (size_t)m * m * 8, cudaMemcpyHostToDevice, h->stream));
+  if (n_cut > 0)
+    CU(cudaMemcpyAsync(h->d_cutK, cut_K, (size_t)n_cut * m * m * 8, cudaMemcpyHostToDevice, h->stream));
+  // levels
+  h->lev.assign(g->p + 1, LevelDev());
+  for (int q = 1; q <= g->p; ++q) {
+    LevelDev& Lv = h->lev[q];
+    const LevelTable& T = L.tables[q];
+    Lv.q = q; Lv.m = T.m; Lv.ndof = T.ndof; Lv.G = group_size(T.m);
+    Lv.kcell = cellop_kernel(T.m, Lv.G, &Lv.M);
+    CU(cudaFuncSetAttribute(Lv.kcell, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cellop_smem(Lv.m, Lv.M, Lv.G, 1)));
+    Lv.omega = q >= 2 ? prm->omega : 1.0;
+    RC(h->alloc(&Lv.base, T.m));
+    RC(h->alloc(&Lv.stride, T.m * 3));
+    RC(h->alloc(&Lv.cmin, T.m * 3));
+    RC(h->alloc(&Lv.cmax, T.m * 3));
+    CU(cudaMemcpyAsync(Lv.base, T.base.data(), T.m * 8, cudaMemcpyHostToDevice, h->stream));
+    CU(cudaMemcpyAsync(Lv.stride, T.stride.data(), T.m * 12, cudaMemcpyHostToDevice, h->stream));
+    CU(cudaMemcpyAsync(Lv.cmin, T.cmin.data(), T.m * 6, cudaMemcpyHostToDevice, h->stream));
+    CU(cudaMemcpyAsync(Lv.cmax, T.cmax.data(), T.m * 6, cudaMemcpyHostToDevice, h->stream));
+    RC(h->alloc(&Lv.x, Lv.ndof));
+    RC(h->alloc(&Lv.r, Lv.ndof));
+  }
+  for (int q = 1; q <= g->p; ++q)
+    if (q >= 2 || prm->coarse == FCM_COARSE_AS_PCG) RC(setup_schwarz(h.get(), q, kind, cut_idx));
+  // coarse level
+  const int64_t n1 = L.ndof_level[1];
+  if (prm->coarse == FCM_COARSE_DIRECT) {
+    if (n1 > 8192) return fail(FCM_EINVAL, "direct coarse solve limited to 8192 DOFs (level 1 has %lld)", (long long)n1);
+    std::vector<double> A0;
+    coarse_dense(h.get(), kind, cut_idx, K_ref, cut_K, &A0, nullptr);
+    double* fac;
+    int* st;
+    RC(h->alloc(&h->d_A0inv, (size_t)n1 * n1));
+    RC(h->alloc(&fac, (size_t)n1 * n1));
+    RC(h->alloc(&st, 1));
+    CU(cudaMemcpyAsync(fac, A0.data(), (size_t)n1 * n1 * 8, cudaMemcpyHostToDevice, h->stream));
+    k_invert_dense<<<1, 1024, 0, h->stream>>>(fac, n1, h->d_A0inv, st);
+    CU(cudaGetLastError());
+    int sth = 0;
+    CU(cudaMemcpyAsync(&sth, st, 4, cudaMemcpyDeviceToHost, h->stream));
+    CU(cudaStreamSynchronize(h->stream));
+    if (sth) return fail(FCM_ESINGULAR, "coarse level matrix is singular / not SPD");
+  } else {
+    if (prm->coarse == FCM_COARSE_JACOBI_PCG) {
+      std::vector<double> dg;
+      coarse_dense(h.get(), kind, cut_idx, K_ref, cut_K, nullptr, &dg);
+      for (auto& v : dg) v = 1.0 / v;
+      RC(h->alloc(&h->d_diag_inv, n1));
+      CU(cudaMemcpyAsync(h->d_diag_inv, dg.data(), n1 * 8, cudaMemcpyHostToDevice, h->stream));
+    }
+    RC(h->alloc(&h->c_r, n1));
+    RC(h->alloc(&h->c_z, n1));
+    RC(h->alloc(&h->c_p, n1));
+    RC(h->alloc(&h->c_q, n1));
+    // cooperative grid: co-resident blocks
+    const LevelDev& L1 = h->lev[1];
+    int M1 = 0;
+    h->kcoarse = coarse_kernel(L1.m, L1.G, &M1);
+    size_t sm = cellop_smem(L1.m, M1, L1.G, 2);
+    CU(cudaFuncSetAttribute(h->kcoarse, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    int per_sm = 0;
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, h->kcoarse, kThreads, sm);
+    if (e != cudaSuccess || per_sm < 1) return fail(FCM_ECUDA, "coarse kernel occupancy query failed");
+    int64_t want = std::max<int64_t>(1, (n1 + kThreads - 1) / kThreads);
+    h->coarse_blocks = (int)std::min<int64_t>(want, (int64_t)h->num_sms * std::min(per_sm, 2));
+    h->coarse_blocks = std::min(h->coarse_blocks, kMaxPartials);
+    if (const char* env = getenv("FCM_COARSE_BLOCKS")) {  // tuning knob (co-residency capped)
+      int v = atoi(env);
+      if (v > 0) h->coarse_blocks = std::min<int64_t>(v, (int64_t)h->num_sms * per_sm);
+    }
+  }
+  RC(h->alloc(&h->d_coarse_iters, 2));
+  CU(cudaMemsetAsync(h->d_coarse_iters, 0, 8, h->stream));
+  // FCG buffers
+  const int64_t N = L.ndof_level[g->p];
+  RC(h->alloc(&h->f_b, N)); RC(h->alloc(&h->f_x, N)); RC(h->alloc(&h->f_r, N));
+  RC(h->alloc(&h->f_ro, N)); RC(h->alloc(&h->f_p, N)); RC(h->alloc(&h->f_q, N));
+  RC(h->alloc(&h->d_s, 1));
+  RC(h->alloc(&h->d_partA, 2 * kMaxPartials));
+  RC(h->alloc(&h->d_partB, 2 * kMaxPartials));
+  RC(h->alloc(&h->d_partC, 2 * kMaxPartials));
+  CU(cudaMallocHost((void**)&h->h_s, sizeof(Scalars)));
+  CU(cudaMallocHost((void**)&h->h_iters, sizeof(int)));
+  CU(cudaMemsetAsync(h->d_s, 0, sizeof(Scalars), h->stream));
+  CU(cudaStreamSynchronize(h->stream));
+  *out = h.release();
+  return FCM_OK;
+}
+
+extern "C" int fcm_mg_destroy(fcm_mg* h) {
+  clear_error();
+  if (!h) return FCM_OK;
+  cudaStreamSynchronize(h->stream);
+  delete h;
+  return FCM_OK;
+}
+
+extern "C" int fcm_mg_nlevels(const fcm_mg* h, int32_t* n) {
+  if (!h || !n) return fail(FCM_EINVAL, "NULL argument");
+  *n = h->g.p;
+  return FCM_OK;
+}
+extern "C" int fcm_mg_ndofs(const fcm_mg* h, int32_t q, int64_t* n) {
+  if (!h || !n || q < 1 || q > h->g.p) return fail(FCM_EINVAL, "bad level");
+  *n = h->L.ndof_level[q];
+  return FCM_OK;
+}
+extern "C" int fcm_mg_level_m(const fcm_mg* h, int32_t q, int32_t* m) {
+  if (!h || !m || q < 1 || q > h->g.p) return fail(FCM_EINVAL, "bad level");
+  *m = h->L.m_level[q];
+  return FCM_OK;
+}
+extern "C" int fcm_mg_dof_keys(const fcm_mg* h, int64_t* keys) {
+  if (!h || !keys) return fail(FCM_EINVAL, "NULL argument");
+  for (int a = 0; a < h->L.dim; ++a)
+    if (h->L.n[a] != h->L.n[0]) return fail(FCM_EINVAL, "DOF keys need nx == ny == nz");
+  h->L.keys(h->g.p, keys);
+  return FCM_OK;
+}
+
+extern "C" int fcm_mg_load(fcm_mg* h, const double* f_ref, const double* cut_f,
+                           const double* f_traction, int32_t traction_face, double* b) {
+  clear_error();
+  if (!h || !f_ref || !b || (h->ncut > 0 && !cut_f)) return fail(FCM_EINVAL, "NULL argument");
+  StreamGuard sg(h);
+  const Layout& L = h->L;
+  const int m = L.m, p = L.p;
+  std::vector<uint8_t> kind(h->ncell);
+  std::vector<int32_t> ci(h->ncell);
+  CU(cudaMemcpyAsync(kind.data(), h->d_kind, h->ncell, cudaMemcpyDeviceToHost, h->stream));
+  CU(cudaMemcpyAsync(ci.data(), h->d_cut_idx, h->ncell * 4, cudaMemcpyDeviceToHost, h->stream));
+  CU(cudaStreamSynchronize(h->stream));
+  std::vector<double> bh(L.ndof_level[p], 0.0);
+  int tax = traction_face >= 0 ? traction_face / 2 : -1, tside = traction_face % 2;
+  for (int64_t c = 0; c < h->ncell; ++c) {
+    int cc[3];
+    L.cell_coords(c, cc);
+    const double* f = kind[c] == 2 ? cut_f + (size_t)ci[c] * m : f_ref;
+    double s = kind[c] == 1 ? h->alpha : 1.0;
+    bool tr = f_traction && tax >= 0 && cc[tax] == (tside ? L.n[tax] - 1 : 0);
+    for (int a = 0; a < m; ++a) {
+      int64_t i = L.dof_index(p, a, cc);
+      if (i < 0) continue;
+      bh[i] += s * f[a] + (tr ? f_traction[a] : 0.0);
+    }
+  }
+  CU(cudaMemcpyAsync(b, bh.data(), bh.size() * 8, cudaMemcpyHostToDevice, h->stream));
+  CU(cudaStreamSynchronize(h->stream));
+  return FCM_OK;
+}
+
+extern "C" int fcm_apply(fcm_mg* h, int32_t q, const double* x, double* y) {
+  clear_error();
+  if (!h || !x || !y || q < 1 || q > h->g.p) return fail(FCM_EINVAL, "bad argument");
+  StreamGuard sg(h);
+  RC(fill(h, y, 0.0, h->lev[q].ndof));
+  return launch_cellop(h, q, make_op(h, q, OP_APPLY, x, y, 1.0, nullptr));
+}
+
+extern "C" int fcm_mg_smooth(fcm_mg* h, int32_t q, const double* r, double* x) {
+  clear_error();
+  if (!h || !r || !x || q < 1 || q > h->g.p) return fail(FCM_EINVAL, "bad argument");
+  if (!h->lev[q].has_as) return fail(FCM_EINVAL, "level q=%d has no Schwarz smoother", q);
+  StreamGuard sg(h);
+  return smooth(h, q, r, x);
+}
+
+extern "C" int fcm_mg_coarse_solve(fcm_mg* h, const double* r, double* x, int32_t* iters) {
+  clear_error();
+  if (!h || !r || !x) return fail(FCM_EINVAL, "NULL argument");
+  StreamGuard sg(h);
+  RC(enqueue_coarse(h, r, x));
+  if (iters) {
+    if (h->prm.coarse == FCM_COARSE_DIRECT) *iters = 0;
+    else {
+      CU(cudaMemcpyAsync(h->h_iters, h->d_coarse_iters, 4, cudaMemcpyDeviceToHost, h->stream));
+      CU(cudaStreamSynchronize(h->stream));
+      *iters = *h->h_iters;
+    }
+  }
+  return FCM_OK;
+}
+
+static int capture_vcycle(fcm_mg* h) {
+  const int p = h->g.p;
+  return capture(h, &h->g_vc, &h->n_vc, [&]() { return enqueue_vcycle(h, p, h->f_r, h->lev[p].x); });
+}
+
+extern "C" int fcm_mg_vcycle(fcm_mg* h, const double* r, double* z) {
+  clear_error();
+  if (!h || !r || !z) return fail(FCM_EINVAL, "NULL argument");
+  StreamGuard sg(h);
+  const int p = h->g.p;
+  const int64_t N = h->lev[p].ndof;
+  RC(capture_vcycle(h));
+  CU(cudaMemcpyAsync(h->f_r, r, N * 8, cudaMemcpyDeviceToDevice, h->stream));
+  RC(run_graph(h, h->g_vc, h->n_vc));
+  CU(cudaMemcpyAsync(z, h->lev[p].x, N * 8, cudaMemcpyDeviceToDevice, h->stream));
+  h->stat_vcycles++;
+  return FCM_OK;
+}
+
+static int capture_fcg(fcm_mg* h) {
+  const int p = h->g.p;
+  const int64_t N = h->lev[p].ndof;
+  double* z = h->lev[p].x;
+  const int nbd = dot_blocks(h);
+  const int nbc = cellop_nblocks(h, p, OP_APPLY);
+  // init: x = 0, r = b, z = V(r), rz = z.r, p = z
+  RC(capture(h, &h->g_init, &h->n_init, [&]() -> int {
+    k_fcg_start<<<grid_for(N, h->num_sms), kThreads, 0, h->stream>>>(h->f_x, h->f_r, h->f_b, N);
+    h->count();
+    RC(enqueue_vcycle(h, p, h->f_r, z));
+    k_dot<<<nbd, kThreads, 0, h->stream>>>(z, h->f_r, N, h->d_partA);
+    h->count();
+    k_fcg_start2<<<grid_for(N, h->num_sms), kThreads, 0, h->stream>>>(h->d_s, h->d_partA, nbd, h->f_p, z, N);
+    h->count();
+    CU(cudaGetLastError());
+    return FCM_OK;
+  }));
+  // iteration part 1: q = A p (energy partials pq), update x, r, r_old, rr
+  RC(capture(h, &h->g_it1, &h->n_it1, [&]() -> int {
+    RC(fill(h, h->f_q, 0.0, N));
+    RC(launch_cellop(h, p, make_op(h, p, OP_APPLY, h->f_p, h->f_q, 1.0, h->d_partB)));
+    k_fcg_update1<<<nbd, kThreads, 0, h->stream>>>(h->d_s, h->d_partB, nbc, h->f_x, h->f_r, h->f_ro,
+                                                    h->f_p, h->f_q, N, h->d_partC);
+    h->count();
+    k_finalize<<<1, 32, 0, h->stream>>>(&h->d_s->rr, h->d_partC, nbd);
+    h->count();
+    CU(cudaGetLastError());
+    CU(cudaMemcpyAsync(h->h_s, h->d_s, sizeof(Scalars), cudaMemcpyDeviceToHost, h->stream));
+    return FCM_OK;
+  }));
+  // iteration part 2: z = V(r), beta, p = z + beta p
+  RC(capture(h, &h->g_it2, &h->n_it2, [&]() -> int {
+    RC(enqueue_vcycle(h, p, h->f_r, z));
+    k_dot2<<<nbd, kThreads, 0, h->stream>>>(z, h->f_r, h->f_ro, N, h->d_partA, h->d_partB);
+    h->count();
+    k_fcg_update2<<<grid_for(N, h->num_sms), kThreads, 0, h->stream>>>(h->d_s, h->d_partA, h->d_partB, nbd, h->f_p, z, N);
+    h->count();
+    k_set_rz<<<1, 32, 0, h->stream>>>(h->d_s);
+    h->count();
+    CU(cudaGetLastError());
+    return FCM_OK;
+  }));
+  return FCM_OK;
+}
+
+static int pcg_core(fcm_mg* h, double rtol, int32_t maxit, int32_t* iters, double* hist) {
+  const int p = h->g.p;
+  const int64_t N = h->lev[p].ndof;
+  RC(capture_fcg(h));
+  // ||b||^2
+  const int nbd = dot_blocks(h);
+  k_dot<<<nbd, kThreads, 0, h->stream>>>(h->f_b, h->f_b, N, h->d_partA);
+  k_finalize<<<1, 32, 0, h->stream>>>(&h->d_s->bb, h->d_partA, nbd);
+  h->count(2);
+  CU(cudaMemsetAsync(&h->d_s->flag, 0, sizeof(int), h->stream));
+  CU(cudaMemcpyAsync(h->h_s, h->d_s, sizeof(Scalars), cudaMemcpyDeviceToHost, h->stream));
+  CU(cudaStreamSynchronize(h->stream));
+  const double bb = h->h_s->bb;
+  int it = 0;
+  if (hist) hist[0] = bb > 0 ? 1.0 : 0.0;
+  h->stat_coarse = 0;
+  CU(cudaMemsetAsync(h->d_coarse_iters, 0, 8, h->stream));
+  h->stat_vcycles = 0;
+  if (!(bb > 0)) {
+    RC(fill(h, h->f_x, 0.0, N));
+    if (iters) *iters = 0;
+    return FCM_OK;
+  }
+  RC(run_graph(h, h->g_init, h->n_init));
+  h->stat_vcycles++;
+  int status = FCM_OK;
+  while (true) {
+    RC(run_graph(h, h->g_it1, h->n_it1));
+    CU(cudaStreamSynchronize(h->stream));
+    ++it;
+    const Scalars s = *h->h_s;
+    if (s.flag & 1) return fail(FCM_EINDEF, "p^T A p <= 0 at FCG iteration %d", it);
+    const double rel = std::sqrt(s.rr / bb);
+    if (hist) hist[it] = rel;
+    if (!(rel == rel)) return fail(FCM_EINDEF, "NaN residual at FCG iteration %d", it);
+    if (rel < rtol) break;
+    if (it >= maxit) { status = FCM_NOT_CONVERGED; break; }
+    RC(run_graph(h, h->g_it2, h->n_it2));
+    h->stat_vcycles++;
+  }
+  if (iters) *iters = it;
+  return status;
+}
+
+extern "C" int fcm_pcg_solve(fcm_mg* h, const double* b, double* x, double rtol, int32_t maxit,
+                             int32_t* iters, double* relres_hist) {
+  clear_error();
+  if (!h || !b || !x || maxit < 0) return fail(FCM_EINVAL, "bad argument");
+  StreamGuard sg(h);
+  const int64_t N = h->lev[h->g.p].ndof;
+  CU(cudaMemcpyAsync(h->f_b, b, N * 8, cudaMemcpyDeviceToDevice, h->stream));
+  int rc = pcg_core(h, rtol, maxit, iters, relres_hist);
+  if (rc < 0) return rc;
+  CU(cudaMemcpyAsync(x, h->f_x, N * 8, cudaMemcpyDeviceToDevice, h->stream));
+  CU(cudaStreamSynchronize(h->stream));
+  return rc;
+}
+
+extern "C" int fcm_pcg_solve_host(fcm_mg* h, const double* b_host, double* x_host, double rtol,
+                                  int32_t maxit, int32_t* iters, double* relres_hist) {
+  clear_error();
+  if (!h || !b_host || !x_host || maxit < 0) return fail(FCM_EINVAL, "bad argument");
+  StreamGuard sg(h);
+  const int64_t N = h->lev[h->g.p].ndof;
+  CU(cudaMemcpyAsync(h->f_b, b_host, N * 8, cudaMemcpyHostToDevice, h->stream));
+  int rc = pcg_core(h, rtol, maxit, iters, relres_hist);
+  if (rc < 0) return rc;
+  CU(cudaMemcpyAsync(x_host, h->f_x, N * 8, cudaMemcpyDeviceToHost, h->stream));
+  CU(cudaStreamSynchronize(h->stream));
+  return rc;
+}
+
+extern "C" int fcm_mg_stats(const fcm_mg* h, int64_t* coarse_iters_total, int64_t* vcycles) {
+  if (!h) return fail(FCM_EINVAL, "NULL handle");
+  if (coarse_iters_total) {
+    int v[2] = {0, 0};
+    CU(cudaMemcpyAsync(v, h->d_coarse_iters, 8, cudaMemcpyDeviceToHost, h->stream));
+    CU(cudaStreamSynchronize(h->stream));
+    *coarse_iters_total = v[1];
+  }
+  if (vcycles) *vcycles = h->stat_vcycles;
+  return FCM_OK;
+}
+
+extern "C" int fcm_mg_launch_count(const fcm_mg* h, int64_t* launches) {
+  if (!h || !launches) return fail(FCM_EINVAL, "NULL argument");
+  *launches = h->launches;
+  return FCM_OK;
+}
+
+extern "C" const char* fcm_last_error(void) { return last_error().c_str(); }
+
+extern "C" int fcm_mg_block_counts(const fcm_mg* h, int32_t q, int64_t* n_individual,
+                                   int32_t* n_shared_types) {
+  if (!h || q < 1 || q > h->g.p) return fail(FCM_EINVAL, "bad level");
+  if (n_individual) *n_individual = h->lev[q].n_irr;
+  if (n_shared_types) *n_shared_types = h->lev[q].n_types;
+  return FCM_OK;
+}

@@ -1,0 +1,242 @@
+"""Thin Python API over the C ABI (argument marshalling only; every step of the hot path
+runs in the sm_100a kernels of libfcm_mg.so).  PyTorch supplies device memory and streams.
+
+    prob = generate(cfg)                      # workload generator (C++, setup)
+    solver = Solver.from_problem(cfg, prob)   # fcm_mg_setup
+    b = solver.load(prob)                     # fcm_mg_load
+    x, iters, hist = solver.pcg_solve(b)      # fcm_pcg_solve (flexible CG + V-cycle)
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import Grid, Params, Physics, check
+
+COARSE = {"direct": 0, "as_pcg": 1, "jacobi_pcg": 2}
+BLOCK = {"element": 0, "patch": 1}
+
+
+def _ptr(a):
+    if a is None:
+        return None
+    if isinstance(a, torch.Tensor):
+        return C.c_void_p(a.data_ptr())
+    return a.ctypes.data_as(C.c_void_p)
+
+
+def grid_of(cfg) -> Grid:
+    g = Grid()
+    g.dim = cfg.dim
+    g.n[0] = cfg.n
+    g.n[1] = cfg.n
+    g.n[2] = cfg.n if cfg.dim == 3 else 1
+    g.h = 1.0 / cfg.n
+    g.p = cfg.p
+    g.space = 0 if cfg.space == "tensor" else 1
+    g.n_f = cfg.n_f
+    g.dirichlet_faces = cfg.dirichlet_mask
+    return g
+
+
+def physics_of(cfg) -> Physics:
+    ph = Physics()
+    ph.kind = 0 if cfg.physics == "poisson" else 1
+    ph.alpha = cfg.alpha
+    ph.E = cfg.E
+    ph.nu = cfg.nu
+    ph.depth = cfg.depth
+    ph.traction_face = cfg.traction_face
+    return ph
+
+
+def params_of(cfg, stream=None, **over) -> Params:
+    pr = Params()
+    pr.block = BLOCK[over.get("block", cfg.block)]
+    om = over.get("omega")
+    if om is None:
+        om = cfg.omega if cfg.omega is not None else cfg.replace(block=over.get("block", cfg.block)).omega_value
+    pr.omega = om
+    pr.n_pre = over.get("n_pre", cfg.n_pre)
+    pr.n_post = over.get("n_post", cfg.n_post)
+    pr.coarse = COARSE[over.get("coarse", cfg.coarse)]
+    pr.coarse_rtol = over.get("coarse_rtol", cfg.coarse_rtol)
+    pr.coarse_maxit = over.get("coarse_maxit", cfg.coarse_maxit)
+    if stream is None:
+        stream = torch.cuda.current_stream().cuda_stream
+    pr.stream = stream
+    return pr
+
+
+def element_size(cfg) -> int:
+    g = grid_of(cfg)
+    m = _lib.lib().fcm_element_size(C.byref(g))
+    check(min(m, 0))
+    return m
+
+
+@dataclass
+class GenProblem:
+    kind: np.ndarray        # uint8 [ncell]
+    cut_cells: np.ndarray   # int64 [n_cut]
+    K_ref: np.ndarray       # [m, m]
+    f_ref: np.ndarray       # [m]
+    cut_K: np.ndarray       # [n_cut, m, m]
+    cut_f: np.ndarray       # [n_cut, m]
+    f_traction: np.ndarray  # [m]
+
+
+def generate(cfg, centres=None, radii=None, threads: int = 0) -> GenProblem:
+    """Workload generator (fcm_gen_classify + fcm_gen_element_matrices)."""
+    from workloads import config_voids
+    if centres is None:
+        centres, radii = config_voids(cfg)
+    centres = np.ascontiguousarray(centres, dtype=np.float64)
+    radii = np.ascontiguousarray(radii, dtype=np.float64)
+    L = _lib.lib()
+    g = grid_of(cfg)
+    ph = physics_of(cfg)
+    ncell = cfg.n ** cfg.dim
+    kind = np.zeros(ncell, dtype=np.uint8)
+    ncut = C.c_int64(0)
+    check(L.fcm_gen_classify(C.byref(g), len(radii), _ptr(centres), _ptr(radii), _ptr(kind), C.byref(ncut)))
+    cut_cells = np.nonzero(kind == 2)[0].astype(np.int64)
+    m = element_size(cfg)
+    K_ref = np.zeros((m, m))
+    f_ref = np.zeros(m)
+    cut_K = np.zeros((len(cut_cells), m, m))
+    cut_f = np.zeros((len(cut_cells), m))
+    f_tr = np.zeros(m)
+    check(L.fcm_gen_element_matrices(C.byref(g), C.byref(ph), len(radii), _ptr(centres), _ptr(radii),
+                                     _ptr(K_ref), _ptr(f_ref), len(cut_cells), _ptr(cut_cells),
+                                     _ptr(cut_K), _ptr(cut_f), _ptr(f_tr), threads))
+    return GenProblem(kind, cut_cells, K_ref, f_ref, cut_K, cut_f, f_tr)
+
+
+class Solver:
+    """Owns an fcm_mg handle (device hierarchy, Schwarz inverses, graphs)."""
+
+    def __init__(self, cfg, K_ref, cell_kind, cut_cells, cut_K, alpha=None, stream=None, **over):
+        self.cfg = cfg
+        L = _lib.lib()
+        self._g = grid_of(cfg)
+        self._p = params_of(cfg, stream, **over)
+        K_ref = np.ascontiguousarray(K_ref, dtype=np.float64)
+        cell_kind = np.ascontiguousarray(cell_kind, dtype=np.uint8)
+        cut_cells = np.ascontiguousarray(cut_cells, dtype=np.int64)
+        cut_K = np.ascontiguousarray(cut_K, dtype=np.float64)
+        h = C.c_void_p()
+        check(L.fcm_mg_setup(C.byref(self._g), C.byref(self._p), _ptr(K_ref), _ptr(cell_kind),
+                             cfg.alpha if alpha is None else alpha, len(cut_cells), _ptr(cut_cells),
+                             _ptr(cut_K), C.byref(h)))
+        self._h = h
+        self.device = torch.device("cuda", torch.cuda.current_device())
+
+    @classmethod
+    def from_problem(cls, cfg, prob: GenProblem, **over):
+        return cls(cfg, prob.K_ref, prob.kind, prob.cut_cells, prob.cut_K, **over)
+
+    def close(self):
+        if getattr(self, "_h", None) is not None and self._h.value:
+            _lib.lib().fcm_mg_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # -- queries --------------------------------------------------------------------------
+    def ndofs(self, q=None) -> int:
+        q = self.cfg.p if q is None else q
+        n = C.c_int64()
+        check(_lib.lib().fcm_mg_ndofs(self._h, q, C.byref(n)))
+        return n.value
+
+    def level_m(self, q) -> int:
+        m = C.c_int32()
+        check(_lib.lib().fcm_mg_level_m(self._h, q, C.byref(m)))
+        return m.value
+
+    def irregular_blocks(self, q) -> int:
+        n, t = C.c_int64(), C.c_int32()
+        check(_lib.lib().fcm_mg_block_counts(self._h, q, C.byref(n), C.byref(t)))
+        return n.value
+
+    def block_counts(self, q):
+        n, t = C.c_int64(), C.c_int32()
+        check(_lib.lib().fcm_mg_block_counts(self._h, q, C.byref(n), C.byref(t)))
+        return n.value, t.value
+
+    def dof_keys(self) -> np.ndarray:
+        k = np.zeros(self.ndofs(), dtype=np.int64)
+        check(_lib.lib().fcm_mg_dof_keys(self._h, _ptr(k)))
+        return k
+
+    def launches(self) -> int:
+        v = C.c_int64()
+        check(_lib.lib().fcm_mg_launch_count(self._h, C.byref(v)))
+        return v.value
+
+    def stats(self):
+        a, b = C.c_int64(), C.c_int64()
+        check(_lib.lib().fcm_mg_stats(self._h, C.byref(a), C.byref(b)))
+        return {"coarse_iters": a.value, "vcycles": b.value}
+
+    def _vec(self, q=None):
+        return torch.zeros(self.ndofs(q), dtype=torch.float64, device=self.device)
+
+    # -- operations -------------------------------------------------------------------------
+    def load(self, prob: GenProblem) -> torch.Tensor:
+        b = self._vec()
+        tr = prob.f_traction if self.cfg.traction_face >= 0 else None
+        check(_lib.lib().fcm_mg_load(self._h, _ptr(np.ascontiguousarray(prob.f_ref)),
+                                     _ptr(np.ascontiguousarray(prob.cut_f)) if len(prob.cut_f) else None,
+                                     _ptr(tr), self.cfg.traction_face, _ptr(b)))
+        return b
+
+    def apply(self, x: torch.Tensor, q=None) -> torch.Tensor:
+        q = self.cfg.p if q is None else q
+        y = self._vec(q)
+        check(_lib.lib().fcm_apply(self._h, q, _ptr(x), _ptr(y)))
+        return y
+
+    def smooth(self, r: torch.Tensor, x: torch.Tensor, q=None) -> torch.Tensor:
+        q = self.cfg.p if q is None else q
+        check(_lib.lib().fcm_mg_smooth(self._h, q, _ptr(r), _ptr(x)))
+        return x
+
+    def coarse_solve(self, r: torch.Tensor):
+        x = self._vec(1)
+        it = C.c_int32()
+        check(_lib.lib().fcm_mg_coarse_solve(self._h, _ptr(r), _ptr(x), C.byref(it)))
+        return x, it.value
+
+    def vcycle(self, r: torch.Tensor) -> torch.Tensor:
+        z = self._vec()
+        check(_lib.lib().fcm_mg_vcycle(self._h, _ptr(r), _ptr(z)))
+        return z
+
+    def pcg_solve(self, b: torch.Tensor, rtol=None, maxit=None, x=None):
+        rtol = self.cfg.rtol if rtol is None else rtol
+        maxit = self.cfg.maxit if maxit is None else maxit
+        x = self._vec() if x is None else x
+        it = C.c_int32()
+        hist = np.zeros(maxit + 1)
+        rc = _lib.lib().fcm_pcg_solve(self._h, _ptr(b), _ptr(x), rtol, maxit, C.byref(it), _ptr(hist))
+        check(rc, allow_not_converged=True)
+        return x, it.value, hist[: it.value + 1]
+
+    def pcg_solve_host(self, b_host: torch.Tensor, x_host: torch.Tensor, rtol=None, maxit=None):
+        rtol = self.cfg.rtol if rtol is None else rtol
+        maxit = self.cfg.maxit if maxit is None else maxit
+        it = C.c_int32()
+        rc = _lib.lib().fcm_pcg_solve_host(self._h, _ptr(b_host), _ptr(x_host), rtol, maxit,
+                                           C.byref(it), None)
+        check(rc, allow_not_converged=True)
+        return it.value

@@ -1,0 +1,208 @@
+"""GPU parity tests: the CUDA path (through the C ABI) against the CPU oracle on the same
+seeded inputs.  Element matrices are the ORACLE's (identical element data);
+all Schwarz blocks, inverses and the coarse factor are computed independently on each side.
+Tolerances (BASELINE.json north_star): <= 1e-10 relative l2 per V-cycle, <= 1e-8 on the
+final solution, FCG iterations +-1; operator apply <= 1e-13 (L1 of the ladder)."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+from oracle.mg import Hierarchy  # noqa: E402
+from oracle.problem import Problem  # noqa: E402
+from workloads import config_voids, get_config, small_config  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+
+def _solver(cfg, P, **over):
+    from paper_2010_00881_b200.fcm import Solver
+    return Solver(cfg, P.K_ref, P.kinds, P.cut_cells, P.cut_K, **over)
+
+
+class Pair:
+    """oracle Problem/Hierarchy + GPU solver + layout permutation."""
+
+    def __init__(self, cfg, **over):
+        self.cfg = cfg
+        c, r = config_voids(cfg)
+        self.P = Problem(cfg, c, r)
+        self.S = _solver(cfg, self.P, **over)
+        keys = self.S.dof_keys()
+        assert np.array_equal(np.sort(keys), self.P.dof.keys)
+        self.pos = np.searchsorted(self.P.dof.keys, keys)   # gpu slot i <-> oracle index pos[i]
+        self.H = None
+
+    def hier(self, **kw):
+        if self.H is None:
+            self.H = Hierarchy(self.P, **kw)
+        return self.H
+
+    def tol(self, base):
+        """Conditioning-aware tolerance: two
+        backward-stable fp64 evaluations of A_i^{-1} r differ by up to kappa_i * eps; the
+        north-star bound `base` is asserted whenever max_i kappa(A_i) < 1e9."""
+        if not hasattr(self, "_kappa"):
+            H = self.hier()
+            ks = [1.0]
+            for q, lv in H.levels.items():
+                if hasattr(lv, "blocks"):
+                    ks += [np.linalg.cond(lv.A[b][:, b].toarray()) for b in lv.blocks]
+            self._kappa = max(ks)
+        return base if self._kappa < 1e9 else max(base, self._kappa * np.finfo(float).eps)
+
+    def to_gpu(self, v_oracle, q=None):
+        n = self.S.ndofs(q)
+        return torch.from_numpy(np.ascontiguousarray(v_oracle[self.pos[:n]])).cuda()
+
+    def from_gpu(self, t, q=None):
+        n = self.S.ndofs(q)
+        out = np.zeros(self.P.dof.ndof)
+        out[self.pos[:n]] = t.cpu().numpy()
+        return out
+
+
+def rel(a, b):
+    return np.linalg.norm(a - b) / np.linalg.norm(b)
+
+
+CASES = {
+    "cfg1": lambda: get_config("cfg1"),
+    "3d_p2": lambda: small_config(3, 6, 2, voids=3, seed=1),
+    "3d_p3_ragged": lambda: small_config(3, 5, 3, voids=2, seed=4),
+    "3d_p2_direct": lambda: small_config(3, 4, 2, voids=2, seed=2, coarse="direct"),
+    "3d_p2_jacobi": lambda: small_config(3, 4, 2, voids=2, seed=3, coarse="jacobi_pcg"),
+    "3d_trunk_elast": lambda: small_config(3, 4, 3, space="trunk", physics="elasticity", voids=2, seed=6),
+    "2d_p4": lambda: small_config(2, 7, 4, voids=1, seed=2, coarse="direct"),
+    "3d_p1_single_level": lambda: small_config(3, 5, 1, voids=2, seed=8),
+}
+
+
+@pytest.fixture(scope="module", params=list(CASES))
+def pair(request):
+    return Pair(CASES[request.param]())
+
+
+def test_layout_is_a_permutation_with_level_prefixes(pair):
+    S, P = pair.S, pair.P
+    for q in range(1, pair.cfg.p + 1):
+        n = S.ndofs(q)
+        assert np.array_equal(np.sort(P.dof.keys[pair.pos[:n]]), P.dof.keys[P.dof.level_dofs(q)])
+        assert S.level_m(q) == P.dof.level_m(q)
+
+
+def test_apply_matches_csr(pair):
+    # L1: fcm_apply vs the oracle's assembled A_q (principal submatrix)
+    rng = np.random.default_rng(0)
+    x = rng.standard_normal(pair.P.dof.ndof)
+    for q in range(1, pair.cfg.p + 1):
+        I = pair.P.dof.level_dofs(q)
+        xq = np.zeros_like(x)
+        xq[I] = x[I]
+        ref = np.zeros_like(x)
+        ref[I] = pair.P.A[I][:, I] @ x[I]
+        y = pair.from_gpu(pair.S.apply(pair.to_gpu(xq, q), q), q)
+        assert rel(y, ref) <= 1e-13, q
+
+
+def test_smoother_matches_oracle(pair):
+    # L2/L3: one AS update x += w M^-1 r with independently inverted blocks
+    H = pair.hier()
+    rng = np.random.default_rng(1)
+    for q in range(2, pair.cfg.p + 1):
+        lv = H.levels[q]
+        r = np.zeros(pair.P.dof.ndof)
+        r[lv.idx] = rng.standard_normal(lv.n)
+        ref = np.zeros_like(r)
+        ref[lv.idx] = lv.omega * lv.schwarz(r[lv.idx])
+        x = torch.zeros(pair.S.ndofs(q), dtype=torch.float64, device="cuda")
+        pair.S.smooth(pair.to_gpu(r, q), x, q)
+        assert rel(pair.from_gpu(x, q), ref) <= pair.tol(1e-9), q
+        # a residual-like right-hand side (the V-cycle's case): b restricted to the level
+        r2 = np.zeros_like(r)
+        r2[lv.idx] = pair.P.b[lv.idx]
+        ref2 = np.zeros_like(r)
+        ref2[lv.idx] = lv.omega * lv.schwarz(r2[lv.idx])
+        x.zero_()
+        pair.S.smooth(pair.to_gpu(r2, q), x, q)
+        assert rel(pair.from_gpu(x, q), ref2) <= pair.tol(1e-10), q
+
+
+def test_coarse_solve_matches_oracle(pair):
+    H = pair.hier()
+    I1 = pair.P.dof.level_dofs(1)
+    r = np.zeros(pair.P.dof.ndof)
+    r[I1] = pair.P.b[I1]
+    ref = np.zeros_like(r)
+    ref[I1] = H.coarse_solve(r[I1])
+    x, it = pair.S.coarse_solve(pair.to_gpu(r, 1))
+    assert rel(pair.from_gpu(x, 1), ref) <= 1e-10
+    if pair.cfg.coarse != "direct":
+        assert abs(it - H.coarse_iters[-1]) <= 1
+
+
+def test_vcycle_matches_oracle(pair):
+    # L4: <= 1e-10 per V-cycle (BASELINE.json north_star)
+    H = pair.hier()
+    rng = np.random.default_rng(2)
+    for r in (pair.P.b, rng.standard_normal(pair.P.dof.ndof)):
+        ref = H.vcycle(r)
+        z = pair.from_gpu(pair.S.vcycle(pair.to_gpu(r)))
+        assert rel(z, ref) <= pair.tol(1e-10)
+
+
+def test_fcg_matches_oracle(pair):
+    # L5: iterations +-1, solution <= 1e-8
+    H = pair.hier()
+    xo, ito, histo = H.fcg(pair.P.b)
+    x, it, hist = pair.S.pcg_solve(pair.to_gpu(pair.P.b))
+    assert abs(it - ito) <= 1
+    assert hist[-1] < pair.cfg.rtol
+    xg = pair.from_gpu(x)
+    assert rel(xg, xo) <= 1e-8
+    # true residual through the GPU operator
+    ax = pair.from_gpu(pair.S.apply(x))
+    assert np.linalg.norm(pair.P.b - ax) / np.linalg.norm(pair.P.b) < 2 * pair.cfg.rtol
+    # same-iteration comparison
+    xo2, _, _ = H.fcg(pair.P.b, force_iters=it)
+    assert rel(xg, xo2) <= 1e-8
+
+
+def test_zero_rhs_and_host_path(pair):
+    b = torch.zeros(pair.S.ndofs(), dtype=torch.float64, device="cuda")
+    x, it, _ = pair.S.pcg_solve(b)
+    assert it == 0 and not torch.any(x)
+    bh = torch.from_numpy(np.ascontiguousarray(pair.P.b[pair.pos])).pin_memory()
+    xh = torch.zeros_like(bh).pin_memory()
+    it = pair.S.pcg_solve_host(bh, xh)
+    xd, itd, _ = pair.S.pcg_solve(bh.cuda())
+    # the fp64 atomic scatter makes summation order run-dependent: equal to rounding
+    assert abs(it - itd) <= 1 and rel(xh.numpy(), xd.cpu().numpy()) <= pair.tol(1e-10)
+
+
+def test_generator_setup_end_to_end():
+    # the product path end to end: generator -> setup -> load -> FCG, against the oracle's b and x
+    from paper_2010_00881_b200.fcm import Solver, generate
+    cfg = small_config(3, 6, 2, voids=3, seed=1)
+    G = generate(cfg)
+    S = Solver.from_problem(cfg, G)
+    b = S.load(G)
+    c, r = config_voids(cfg)
+    P = Problem(cfg, c, r)
+    keys = S.dof_keys()
+    pos = np.searchsorted(P.dof.keys, keys)
+    assert rel(b.cpu().numpy(), P.b[pos]) <= 1e-13
+    x, it, _ = S.pcg_solve(b)
+    xo, ito, _ = Hierarchy(P).fcg(P.b)
+    assert abs(it - ito) <= 1
+    assert rel(x.cpu().numpy(), xo[pos]) <= 1e-8
+
+
+def test_empty_level_rejected():
+    from paper_2010_00881_b200._lib import FcmError
+    from paper_2010_00881_b200.fcm import Solver, generate
+    cfg = small_config(3, 1, 2)   # one cell, all faces Dirichlet: level 1 has no free DOF
+    G = generate(cfg)
+    with pytest.raises(FcmError) as e:
+        Solver.from_problem(cfg, G)
+    assert e.value.code == -1
