@@ -4,11 +4,13 @@
 // (Eq. AdditiveSchwarz: x += omega sum_i P_i A_i^{-1} P_i^T r).
 //
 // Two populations of cells, two mappings:
-//  * regular cells (uncut for the operator; shared-by-type blocks for the smoother) -- one
-//    THREAD per cell: the m gathered values live in registers (compile-time M, full unroll),
-//    the shared matrix (K_ref or the interior-type inverse) is broadcast from shared memory
-//    (every lane reads the same word), other boundary types read through L1.  32 lanes =
-//    32 consecutive cells along x, so every gather / scatter instruction is coalesced.
+//  * regular cells (uncut for the operator; shared-by-type blocks for the smoother) -- TS
+//    consecutive THREADS per cell (thread j owns a block of RB rows); the m gathered values
+//    live in registers (compile-time M, full unroll); the shared matrix (K_ref or the
+//    interior-type inverse) is read from shared memory as LDS.128 row pairs (all cells of a
+//    warp read the same words); other boundary types read through L1.  Consecutive lanes are
+//    consecutive cells along x, so every gather / scatter instruction is coalesced.  Cells away
+//    from Dirichlet faces take a gather path without bounds tests.
 //  * individual cells (cut cells / irregular blocks) -- one GROUP of G lanes per cell over a
 //    compact list; lane a owns rows a, a+G, ...; the individual matrix is streamed column-wise
 //    (Mat[b*ld + a], symmetric) so the G lanes read consecutive addresses.
@@ -22,12 +24,10 @@ constexpr int kMaxM = 128;  // largest element block handled by the cell kernels
 
 enum { OP_APPLY = 0, OP_SMOOTH = 1 };
 
-struct Tab {  // level table in shared memory; stride along x is 1 for every DOF class
-  int32_t base[kMaxM];
-  int32_t sy[kMaxM];
-  int32_t sz[kMaxM];
-  int16_t cmin[kMaxM][3];
-  int16_t cmax[kMaxM][3];
+struct Tab {      // level table in shared memory; stride along x is 1 for every DOF class
+  int4 g[kMaxM];  // {base, stride_y, stride_z, -}
+  int4 lo[kMaxM]; // free cell range of local DOF a: c_i in [lo_i, hi_i]
+  int4 hi[kMaxM];
 };
 
 struct CellOp {
@@ -38,6 +38,7 @@ struct CellOp {
   const int32_t* stride;
   const int16_t* cmin;
   const int16_t* cmax;
+  int ilo[3], ihi[3];         // cells whose every local DOF is free (no Dirichlet test needed)
   int mode;                   // OP_APPLY / OP_SMOOTH
   // APPLY (regular): K_ref (kind 0) or alpha K_ref (kind 1); kind 2 cells are in the list
   const uint8_t* kind;
@@ -60,94 +61,170 @@ struct CellOp {
   const double* irr_inv;
   // data: out[idx] += coef * scale * Mat * in_local
   const double* in;
+  // fused input (FUSE template): value = in + c1 * (in1 + c2 * in2)
+  const double* in1;
+  const double* in2;
+  double c1, c2;
   double* out;
   double coef;
-  double* partials;           // optional per-block sum of in_local^T (scale Mat in_local)
+  double* partials;           // per-block sum of in_local^T (scale Mat in_local), or nullptr
 };
 
 __device__ __forceinline__ void load_tab(Tab& T, const CellOp& op) {
   for (int a = threadIdx.x; a < op.m; a += blockDim.x) {
-    T.base[a] = (int32_t)op.base[a];
-    T.sy[a] = op.stride[a * 3 + 1];
-    T.sz[a] = op.stride[a * 3 + 2];
-    for (int i = 0; i < 3; ++i) {
-      T.cmin[a][i] = op.cmin[a * 3 + i];
-      T.cmax[a][i] = op.cmax[a * 3 + i];
-    }
+    T.g[a] = make_int4((int32_t)op.base[a], op.stride[a * 3 + 1], op.stride[a * 3 + 2], 0);
+    T.lo[a] = make_int4(op.cmin[a * 3 + 0], op.cmin[a * 3 + 1], op.cmin[a * 3 + 2], 0);
+    T.hi[a] = make_int4(op.cmax[a * 3 + 0], op.cmax[a * 3 + 1], op.cmax[a * 3 + 2], 0);
   }
 }
 
-// shared matrix of the regular path (row-major M x M): K_ref leading block or interior inverse
+template <bool FUSE>
+__device__ __forceinline__ double load_in(const CellOp& op, int i) {
+  double v = __ldg(op.in + i);
+  if constexpr (FUSE) v = fma(op.c1, fma(op.c2, __ldg(op.in2 + i), __ldg(op.in1 + i)), v);
+  return v;
+}
+
+__device__ __forceinline__ bool dof_free(const Tab& T, int a, int cx, int cy, int cz) {
+  const int4 lo = T.lo[a], hi = T.hi[a];
+  return (cx >= lo.x) & (cx <= hi.x) & (cy >= lo.y) & (cy <= hi.y) & (cz >= lo.z) & (cz <= hi.z);
+}
+__device__ __forceinline__ int dof_index(const Tab& T, int a, int cx, int cy, int cz) {
+  const int4 g = T.g[a];
+  return g.x + cx + cy * g.y + cz * g.z;
+}
+
+// shared matrix of the regular path, column-major with an even leading dimension MP so that
+// rows (a, a+1) of one column are one 16-byte LDS.128: Ms[b*MP + a] = Mat[a][b].
+template <int M> __host__ __device__ constexpr int padded() { return M + (M & 1); }
 template <int M>
 __device__ __forceinline__ void load_shared_matrix(double* Ms, const CellOp& op) {
-  if (op.mode == OP_APPLY) {
-    for (int e = threadIdx.x; e < M * M; e += blockDim.x) Ms[e] = op.Kref[(e / M) * op.ldK + e % M];
-  } else {
-    for (int e = threadIdx.x; e < M * M; e += blockDim.x) Ms[e] = op.type_inv[e];  // type code 0
+  constexpr int MP = padded<M>();
+  for (int e = threadIdx.x; e < M * MP; e += blockDim.x) {
+    const int b = e / MP, a = e % MP;
+    double v = 0.0;
+    if (a < M) v = (op.mode == OP_APPLY) ? op.Kref[a * op.ldK + b] : op.type_inv[a * M + b];  // type code 0
+    Ms[e] = v;
   }
 }
 
-template <int M>
+// rows of a cell are split over TS consecutive threads (blocked: thread j owns rows
+// [j*RB, j*RB+RB)), RB even so a thread's rows of one column are LDS.128 pairs.
+template <int M> __host__ __device__ constexpr int split_of() {
+  return M <= 4 ? 1 : (M <= 9 ? 2 : (M <= 16 ? 4 : 8));
+}
+template <int M, int TS> __host__ __device__ constexpr int rows_of() { return ((M + TS - 1) / TS + 1) / 2 * 2; }
+// per-warp shared scratch of the regular path (doubles): one padded x vector per cell slot
+template <int M, int TS> __host__ __device__ constexpr int reg_scratch() { return (32 / TS) * padded<M>(); }
+
+// A warp holds CPW = 32/TS cells; lane = slot*TS + j.  The TS lanes of a cell gather its M
+// values cooperatively (a = j, j+TS, ...) into shared memory, then every lane loads the whole
+// vector into registers and computes its RB rows.  Warp-synchronous (uniform trip count).
+template <int M, int TS, bool FUSE>
 __device__ __forceinline__ double reg_cells(const CellOp& op, const Tab& T, const double* __restrict__ Ms,
-                                            int t0, int nth) {
+                                            double* xs_warp, int warp, int nwarps) {
+  constexpr int RB = rows_of<M, TS>();
+  constexpr int MP = padded<M>();
+  constexpr int CPW = 32 / TS;
+  const int lane = threadIdx.x & 31;
+  const int slot = lane / TS;
+  const int j = lane % TS;
+  const int a_lo = j * RB;
+  double* xs = xs_warp + slot * MP;
+  const int nx = op.nx, ny = op.ny, ncell = op.ncell;
+  const int ilx = op.ilo[0], ihx = op.ihi[0], ily = op.ilo[1], ihy = op.ihi[1];
+  const int ilz = op.ilo[2], ihz = op.ihi[2];
+  const bool apply = op.mode == OP_APPLY;
+  const bool want_e = op.partials != nullptr;
+  double* __restrict__ out = op.out;
+  const double coef = op.coef;
   double energy = 0.0;
-  for (int c = t0; c < op.ncell; c += nth) {
+  const int per_round = nwarps * CPW;
+  const int rounds = (ncell + per_round - 1) / per_round;
+  for (int rnd = 0; rnd < rounds; ++rnd) {
+    const int c = (rnd * nwarps + warp) * CPW + slot;
+    bool act = c < ncell;
     double scale = 1.0;
     const double* Mg = nullptr;
-    if (op.mode == OP_APPLY) {
-      const int k = op.kind[c];
-      if (k == 2) continue;
-      scale = (k == 1) ? op.alpha : 1.0;
-    } else {
-      const int b = op.blk[c];
-      if (b >= 0) continue;
-      const int t = -b - 1;
-      scale = (t >> 12) ? op.inv_alpha : 1.0;
-      const int code = t & 0xff;
-      if (code != 0) Mg = op.type_inv + code * M * M;
+    if (act) {
+      if (apply) {
+        const int k = op.kind[c];
+        act = k != 2;
+        scale = (k == 1) ? op.alpha : 1.0;
+      } else {
+        const int b = op.blk[c];
+        act = b < 0;
+        const int t = -b - 1;
+        scale = (t >> 12) ? op.inv_alpha : 1.0;
+        const int code = t & 0xff;
+        if (code != 0) Mg = op.type_inv + code * M * M;
+      }
     }
-    const int cx = c % op.nx;
-    const int cyz = c / op.nx;
-    const int cy = cyz % op.ny;
-    const int cz = cyz / op.ny;
-    double x[M];
-    int idx[M];
+    int cx = 0, cy = 0, cz = 0;
+    bool inner = false;
+    if (act) {
+      cx = c % nx;
+      const int cyz = c / nx;
+      cy = cyz % ny;
+      cz = cyz / ny;
+      inner = (cx >= ilx) & (cx <= ihx) & (cy >= ily) & (cy <= ihy) & (cz >= ilz) & (cz <= ihz);
+      for (int a = j; a < M; a += TS)
+        xs[a] = (inner || dof_free(T, a, cx, cy, cz)) ? load_in<FUSE>(op, dof_index(T, a, cx, cy, cz)) : 0.0;
+    }
+    __syncwarp();
+    if (act) {
+    // the gathered vector stays in shared memory (xs[b] is one broadcast word per cell), which
+    // keeps the register footprint small enough for 4 resident blocks per SM
+    double acc[RB];
 #pragma unroll
-    for (int a = 0; a < M; ++a) {
-      const bool ok = (cx >= T.cmin[a][0]) & (cx <= T.cmax[a][0]) & (cy >= T.cmin[a][1]) &
-                      (cy <= T.cmax[a][1]) & (cz >= T.cmin[a][2]) & (cz <= T.cmax[a][2]);
-      const int i = T.base[a] + cx + cy * T.sy[a] + cz * T.sz[a];
-      idx[a] = ok ? i : -1;
-      x[a] = ok ? __ldg(op.in + i) : 0.0;
-    }
+    for (int i = 0; i < RB; ++i) acc[i] = 0.0;
     if (Mg == nullptr) {
+#pragma unroll 9
+      for (int b = 0; b < M; ++b) {
+        const double xb = xs[b];
 #pragma unroll
-      for (int a = 0; a < M; ++a) {
-        double acc = 0.0;
-#pragma unroll
-        for (int b = 0; b < M; ++b) acc = fma(Ms[a * M + b], x[b], acc);
-        const double y = scale * acc;
-        if (idx[a] >= 0) atomicAdd(op.out + idx[a], op.coef * y);
-        energy = fma(x[a], y, energy);
+        for (int i = 0; i < RB; i += 2) {
+          if (TS == 1 ? (i < M) : (a_lo + i < M)) {
+            const double2 v = *reinterpret_cast<const double2*>(Ms + b * MP + a_lo + i);
+            acc[i] = fma(v.x, xb, acc[i]);
+            acc[i + 1] = fma(v.y, xb, acc[i + 1]);   // pad row (a = M) reads 0
+          }
+        }
       }
     } else {
+#pragma unroll 9
+      for (int b = 0; b < M; ++b) {
+        const double xb = xs[b];
 #pragma unroll
-      for (int a = 0; a < M; ++a) {
-        double acc = 0.0;
-#pragma unroll
-        for (int b = 0; b < M; ++b) acc = fma(__ldg(Mg + a * M + b), x[b], acc);
-        const double y = scale * acc;
-        if (idx[a] >= 0) atomicAdd(op.out + idx[a], op.coef * y);
-        energy = fma(x[a], y, energy);
+        for (int i = 0; i < RB; ++i)
+          if (a_lo + i < M) acc[i] = fma(__ldg(Mg + (a_lo + i) * M + b), xb, acc[i]);
       }
     }
+#pragma unroll
+    for (int i = 0; i < RB; ++i) {
+      const int a = a_lo + i;
+      if (TS == 1 ? (i < M) : (a < M)) {
+        if (inner || dof_free(T, a, cx, cy, cz)) {
+          const int ia = dof_index(T, a, cx, cy, cz);
+          const double y = scale * acc[i];
+#ifdef FCM_DEBUG_NORED
+          out[ia] = coef * y;   // timing experiment only (wrong result)
+#else
+          atomicAdd(out + ia, coef * y);
+#endif
+          if (want_e) energy = fma(xs[a], y, energy);
+        }
+      }
+    }
+    }  // act
+    __syncwarp();
   }
   return energy;
 }
 
 // Individual cells (op.list != nullptr) or, without a compile-time M, all cells with per-cell
 // matrix selection.  Groups of G lanes per cell; xs/ids: per-warp shared scratch (CPW*m).
-template <int G>
+template <int G, bool FUSE>
 __device__ __forceinline__ double list_cells(const CellOp& op, const Tab& T, int warp, int nwarps,
                                              double* xs_warp, int* ids_warp) {
   constexpr int CPW = 32 / G;
@@ -159,6 +236,9 @@ __device__ __forceinline__ double list_cells(const CellOp& op, const Tab& T, int
   int* ids = ids_warp + grp * m;
   const bool generic = op.list == nullptr;
   const int count = generic ? op.ncell : op.nlist;
+  const int nx = op.nx, ny = op.ny;
+  double* __restrict__ out = op.out;
+  const double coef = op.coef;
   double energy = 0.0;
   const int per_round = nwarps * CPW;
   const int rounds = (count + per_round - 1) / per_round;
@@ -167,16 +247,15 @@ __device__ __forceinline__ double list_cells(const CellOp& op, const Tab& T, int
     const bool active = i < count;
     const int c = active ? (generic ? i : op.list[i]) : 0;
     if (active) {
-      const int cx = c % op.nx;
-      const int cyz = c / op.nx;
-      const int cy = cyz % op.ny;
-      const int cz = cyz / op.ny;
+      const int cx = c % nx;
+      const int cyz = c / nx;
+      const int cy = cyz % ny;
+      const int cz = cyz / ny;
       for (int a = gl; a < m; a += G) {
-        const bool ok = (cx >= T.cmin[a][0]) & (cx <= T.cmax[a][0]) & (cy >= T.cmin[a][1]) &
-                        (cy <= T.cmax[a][1]) & (cz >= T.cmin[a][2]) & (cz <= T.cmax[a][2]);
-        const int idx = T.base[a] + cx + cy * T.sy[a] + cz * T.sz[a];
+        const bool ok = dof_free(T, a, cx, cy, cz);
+        const int idx = dof_index(T, a, cx, cy, cz);
         ids[a] = ok ? idx : -1;
-        xs[a] = ok ? __ldg(op.in + idx) : 0.0;
+        xs[a] = ok ? load_in<FUSE>(op, idx) : 0.0;
       }
     }
     __syncwarp();
@@ -218,7 +297,7 @@ __device__ __forceinline__ double list_cells(const CellOp& op, const Tab& T, int
         if (b < m) acc0 = fma(__ldg(col + (size_t)b * ld), xs[b], acc0);
         const double y = scale * (acc0 + acc1);
         const int id = ids[a];
-        if (id >= 0) atomicAdd(op.out + id, op.coef * y);
+        if (id >= 0) atomicAdd(out + id, coef * y);
         energy = fma(xs[a], y, energy);
       }
     }

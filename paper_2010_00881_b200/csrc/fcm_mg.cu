@@ -24,6 +24,7 @@
 
 #include "../../include/fcm_mg.h"
 #include "cellop.cuh"
+#include "coarse.cuh"
 #include "common.hpp"
 #include "layout.hpp"
 
@@ -70,8 +71,11 @@ struct LevelDev {
   int64_t n_irr = 0;
   int32_t n_types = 0;
   int M = 0;                       // compile-time block size of the regular path (0: generic)
-  const void* kcell = nullptr;     // k_cellop<M,G>
+  const void* kreg = nullptr;      // k_cell_reg<M> (regular population)
+  const void* klist = nullptr;     // k_cell_list<G> (individual list / generic)
   int32_t* irr_list = nullptr;     // cells with an individual Schwarz inverse (irr order)
+  int ilo[3] = {0, 0, 0}, ihi[3] = {-1, -1, -1};  // cells with no Dirichlet DOF
+  int ts = 1;                      // threads per cell of the regular path
   // vectors
   double* x = nullptr;
   double* r = nullptr;
@@ -86,6 +90,8 @@ struct fcm_mg {
   cudaStream_t stream = nullptr;   // internal non-blocking stream (capturable)
   cudaStream_t ustream = nullptr;  // the caller's stream (params.stream)
   cudaEvent_t ev_in = nullptr, ev_out = nullptr;
+  cudaStream_t stream2 = nullptr;  // second branch: individual-cell kernels run concurrently
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   int dev = 0, num_sms = 148;
   double alpha = 1e-8;
   int64_t ncell = 0, ncut = 0;
@@ -99,7 +105,9 @@ struct fcm_mg {
   // coarse
   double* d_A0inv = nullptr;   // direct
   double* d_diag_inv = nullptr;  // Jacobi
-  double *c_r = nullptr, *c_z = nullptr, *c_p = nullptr, *c_q = nullptr;
+  double* c_vec[9] = {};  // r[2], z[2], w[2], q[2], p
+  double* c_part = nullptr;
+  GridCtl* c_ctl = nullptr;
   int* d_coarse_iters = nullptr;
   int coarse_blocks = 0;
   // FCG
@@ -140,6 +148,9 @@ struct fcm_mg {
     if (ev_in) cudaEventDestroy(ev_in);
     if (ev_out) cudaEventDestroy(ev_out);
     if (stream) cudaStreamDestroy(stream);
+    if (stream2) cudaStreamDestroy(stream2);
+    if (ev_fork) cudaEventDestroy(ev_fork);
+    if (ev_join) cudaEventDestroy(ev_join);
   }
 };
 
@@ -148,49 +159,43 @@ struct fcm_mg {
 // =========================================================================================
 namespace {
 
-// dynamic shared memory: [Tab][Ms: M*M doubles][xs: wpb*CPW*m doubles][ids: wpb*CPW*m ints]
-struct CellSmem {
-  Tab* T;
-  double* Ms;
-  double* xs;
-  int* ids;
-};
-template <int M, int G>
-__device__ __forceinline__ CellSmem carve(unsigned char* smem, int m) {
-  constexpr int CPW = 32 / G;
+// Regular population: one thread per cell (compile-time M); smem [Tab][Ms: M*MP doubles].
+template <int M, int TS>
+__global__ void __launch_bounds__(kThreads, 4) k_cell_reg(CellOp op) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  Tab& T = *reinterpret_cast<Tab*>(smem);
+  double* Ms = reinterpret_cast<double*>(smem + sizeof(Tab));
+  __shared__ double red[32];
+  load_tab(T, op);
+  load_shared_matrix<M>(Ms, op);
+  __syncthreads();
   const int wpb = blockDim.x >> 5;
-  CellSmem s;
-  s.T = reinterpret_cast<Tab*>(smem);
-  s.Ms = reinterpret_cast<double*>(smem + sizeof(Tab));
-  double* xs0 = s.Ms + M * M;
-  s.xs = xs0 + (threadIdx.x >> 5) * CPW * m;
-  s.ids = reinterpret_cast<int*>(xs0 + wpb * CPW * m) + (threadIdx.x >> 5) * CPW * m;
-  return s;
+  double* xs = Ms + M * padded<M>() + (threadIdx.x >> 5) * reg_scratch<M, TS>();
+  const double e = reg_cells<M, TS, false>(op, T, Ms, xs, blockIdx.x * wpb + (threadIdx.x >> 5), gridDim.x * wpb);
+  if (op.partials) {
+    const double t = block_sum(e, red);
+    if (threadIdx.x == 0) op.partials[blockIdx.x] = t;
+  }
 }
 
-// One launch covers both populations: blocks [0, nb_reg) run the thread-per-cell regular path
-// (compile-time M), blocks [nb_reg, grid) the group-per-cell individual list (or, for M == 0,
-// every cell with per-cell matrix selection).
-template <int M, int G>
-__global__ void __launch_bounds__(kThreads) k_cellop(CellOp op, int nb_reg) {
+// Individual population (or, without compile-time M, every cell): groups of G lanes per cell;
+// smem [Tab][xs: wpb*CPW*m doubles][ids: wpb*CPW*m ints].  Partials at part_off + block.
+template <int G>
+__global__ void __launch_bounds__(kThreads) k_cell_list(CellOp op, int part_off) {
   extern __shared__ __align__(16) unsigned char smem[];
-  CellSmem s = carve<M, G>(smem, op.m);
+  constexpr int CPW = 32 / G;
+  const int wpb = blockDim.x >> 5;
+  Tab& T = *reinterpret_cast<Tab*>(smem);
+  double* xs0 = reinterpret_cast<double*>(smem + sizeof(Tab));
+  double* xs = xs0 + (threadIdx.x >> 5) * CPW * op.m;
+  int* ids = reinterpret_cast<int*>(xs0 + wpb * CPW * op.m) + (threadIdx.x >> 5) * CPW * op.m;
   __shared__ double red[32];
-  load_tab(*s.T, op);
-  if (M > 0 && (int)blockIdx.x < nb_reg) load_shared_matrix<(M > 0 ? M : 1)>(s.Ms, op);
+  load_tab(T, op);
   __syncthreads();
-  double e = 0.0;
-  if ((int)blockIdx.x < nb_reg) {
-    if constexpr (M > 0) e = reg_cells<M>(op, *s.T, s.Ms, blockIdx.x * blockDim.x + threadIdx.x, nb_reg * blockDim.x);
-  } else {
-    const int wpb = blockDim.x >> 5;
-    const int warp = (blockIdx.x - nb_reg) * wpb + (threadIdx.x >> 5);
-    const int nwarps = (gridDim.x - nb_reg) * wpb;
-    e = list_cells<G>(op, *s.T, warp, nwarps, s.xs, s.ids);
-  }
+  const double e = list_cells<G, false>(op, T, blockIdx.x * wpb + (threadIdx.x >> 5), gridDim.x * wpb, xs, ids);
   if (op.partials) {
-    double t = block_sum(e, red);
-    if (threadIdx.x == 0) op.partials[blockIdx.x] = t;
+    const double t = block_sum(e, red);
+    if (threadIdx.x == 0) op.partials[part_off + blockIdx.x] = t;
   }
 }
 
@@ -439,145 +444,25 @@ __global__ void k_invert_dense(double* A, int64_t n, double* X, int* status) {
   if (threadIdx.x == 0) *status = bad;
 }
 
-// ---- coarse level: whole preconditioned CG in one cooperative launch ----
-struct CoarseArgs {
-  CellOp A;                    // apply: in = p, out = q
-  CellOp M;                    // AS smoother: in = r, out = z (coef 1)
-  int jacobi;
-  const double* diag_inv;
-  const double* b;
-  double* x;
-  double *r, *z, *p, *q;
-  int64_t n;
-  double rtol2;
-  int maxit;
-  double* partA;
-  double* partB;
-  int* iters;
-};
-
-// one cell phase of the coarse solver: regular cells (thread per cell) + individual list
-template <int M, int G>
-__device__ __forceinline__ double coarse_cells(const CellOp& op, const Tab& T, const double* Ms,
-                                               double* xs, int* ids) {
-  const int wpb = blockDim.x >> 5;
-  double e = 0.0;
-  if constexpr (M > 0) e = reg_cells<M>(op, T, Ms, blockIdx.x * blockDim.x + threadIdx.x, gridDim.x * blockDim.x);
-  e += list_cells<G>(op, T, blockIdx.x * wpb + (threadIdx.x >> 5), gridDim.x * wpb, xs, ids);
-  return e;
-}
-
-// smem: [Tab][MsA: M*M][MsM: M*M][xs][ids]
-template <int M, int G>
-__global__ void __launch_bounds__(kThreads) k_coarse_pcg(CoarseArgs a) {
-  cg::grid_group grid = cg::this_grid();
-  extern __shared__ __align__(16) unsigned char smem[];
-  constexpr int CPW = 32 / G;
-  const int wpb = blockDim.x >> 5;
-  const int m = a.A.m;
-  Tab& T = *reinterpret_cast<Tab*>(smem);
-  double* MsA = reinterpret_cast<double*>(smem + sizeof(Tab));
-  double* MsM = MsA + M * M;
-  double* xs0 = MsM + M * M;
-  double* xs = xs0 + (threadIdx.x >> 5) * CPW * m;
-  int* ids = reinterpret_cast<int*>(xs0 + wpb * CPW * m) + (threadIdx.x >> 5) * CPW * m;
-  __shared__ double red[32];
-  load_tab(T, a.A);
-  if constexpr (M > 0) {
-    load_shared_matrix<M>(MsA, a.A);
-    if (!a.jacobi) load_shared_matrix<M>(MsM, a.M);
-  }
-  __syncthreads();
-  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int64_t nth = (int64_t)gridDim.x * blockDim.x;
-  const int nb = gridDim.x;
-  const int64_t n = a.n;
-
-  // x = 0, r = b, z = 0, q = 0 ; rr0 = b.b
-  double s = 0.0;
-  for (int64_t i = tid; i < n; i += nth) {
-    const double bi = a.b[i];
-    a.x[i] = 0.0; a.r[i] = bi; a.z[i] = 0.0; a.q[i] = 0.0;
-    s = fma(bi, bi, s);
-  }
-  s = block_sum(s, red);
-  if (threadIdx.x == 0) a.partA[blockIdx.x] = s;
-  grid.sync();
-  const double rr0 = sum_partials(a.partA, nb);
-  int it = 0;
-  if (rr0 > 0.0) {
-    // z = M^-1 r ; rz
-    if (a.jacobi) {
-      s = 0.0;
-      for (int64_t i = tid; i < n; i += nth) { const double zi = a.diag_inv[i] * a.r[i]; a.z[i] = zi; s = fma(zi, a.r[i], s); }
-    } else {
-      s = coarse_cells<M, G>(a.M, T, MsM, xs, ids);
-    }
-    s = block_sum(s, red);
-    if (threadIdx.x == 0) a.partB[blockIdx.x] = s;
-    grid.sync();
-    double rz = sum_partials(a.partB, nb);
-    for (int64_t i = tid; i < n; i += nth) a.p[i] = a.z[i];
-    grid.sync();
-    while (true) {
-      // P1: q = A p ; pq
-      s = coarse_cells<M, G>(a.A, T, MsA, xs, ids);
-      s = block_sum(s, red);
-      if (threadIdx.x == 0) a.partA[blockIdx.x] = s;
-      grid.sync();
-      // P2: alpha ; x += alpha p ; r -= alpha q ; z = 0 ; rr
-      const double pq = sum_partials(a.partA, nb);
-      const double alpha = rz / pq;
-      s = 0.0;
-      for (int64_t i = tid; i < n; i += nth) {
-        a.x[i] = fma(alpha, a.p[i], a.x[i]);
-        const double rn = fma(-alpha, a.q[i], a.r[i]);
-        a.r[i] = rn;
-        a.z[i] = 0.0;
-        s = fma(rn, rn, s);
-      }
-      s = block_sum(s, red);
-      if (threadIdx.x == 0) a.partB[blockIdx.x] = s;
-      grid.sync();
-      // P3: convergence test ; z = M^-1 r ; rz_new ; q = 0
-      const double rr = sum_partials(a.partB, nb);
-      ++it;
-      if (!(pq > 0.0) || rr < a.rtol2 * rr0 || it >= a.maxit) break;
-      if (a.jacobi) {
-        s = 0.0;
-        for (int64_t i = tid; i < n; i += nth) { const double zi = a.diag_inv[i] * a.r[i]; a.z[i] = zi; s = fma(zi, a.r[i], s); }
-      } else {
-        s = coarse_cells<M, G>(a.M, T, MsM, xs, ids);
-      }
-      for (int64_t i = tid; i < n; i += nth) a.q[i] = 0.0;
-      s = block_sum(s, red);
-      if (threadIdx.x == 0) a.partA[blockIdx.x] = s;
-      grid.sync();
-      // P4: beta ; p = z + beta p
-      const double rz_new = sum_partials(a.partA, nb);
-      const double beta = rz_new / rz;
-      rz = rz_new;
-      for (int64_t i = tid; i < n; i += nth) a.p[i] = fma(beta, a.p[i], a.z[i]);
-      grid.sync();
-    }
-  }
-  if (blockIdx.x == 0 && threadIdx.x == 0) { a.iters[0] = it; a.iters[1] += it; }
-}
-
 // ---- compile-time M dispatch --------------------------------------------------------------
 template <int M> constexpr int gsz() { return M <= 4 ? 4 : (M <= 8 ? 8 : (M <= 16 ? 16 : 32)); }
 #define FCM_FOR_M(X) X(4) X(8) X(9) X(16) X(24) X(25) X(27)
 
-const void* cellop_kernel(int m, int G, int* M_out) {
-#define CASE(MM) case MM: *M_out = MM; return (const void*)k_cellop<MM, gsz<MM>()>;
+// ts1: force one thread per cell (tuning knob FCM_TS1)
+const void* reg_kernel(int m, int* M_out, bool ts1) {
+#define CASE(MM) case MM: *M_out = MM; \
+  return ts1 ? (const void*)k_cell_reg<MM, 1> : (const void*)k_cell_reg<MM, split_of<MM>()>;
   switch (m) { FCM_FOR_M(CASE) default: break; }
 #undef CASE
   *M_out = 0;
+  return nullptr;
+}
+const void* list_kernel(int G) {
   switch (G) {
-    case 4: return (const void*)k_cellop<0, 4>;
-    case 8: return (const void*)k_cellop<0, 8>;
-    case 16: return (const void*)k_cellop<0, 16>;
-    default: return (const void*)k_cellop<0, 32>;
+    case 4: return (const void*)k_cell_list<4>;
+    case 8: return (const void*)k_cell_list<8>;
+    case 16: return (const void*)k_cell_list<16>;
+    default: return (const void*)k_cell_list<32>;
   }
 }
 const void* coarse_kernel(int m, int G, int* M_out) {
@@ -610,9 +495,18 @@ static int group_size(int m) {
   return 32;
 }
 
-static size_t cellop_smem(int m, int M, int G, int nmat) {
-  return sizeof(Tab) + (size_t)nmat * M * M * sizeof(double) +
-         (size_t)(kThreads / 32) * (32 / G) * m * (sizeof(double) + sizeof(int));
+static int split_rt(int M) { return M <= 4 ? 1 : (M <= 9 ? 2 : (M <= 16 ? 4 : 8)); }  // = split_of<M>()
+static size_t reg_scratch_rt(int M, int TS) { return (size_t)(32 / TS) * (M + (M & 1)); }
+static size_t reg_smem(int M, int TS) {
+  return sizeof(Tab) + ((size_t)M * (M + (M & 1)) + (kThreads / 32) * reg_scratch_rt(M, TS)) * sizeof(double);
+}
+static size_t list_smem(int m, int G) {
+  return sizeof(Tab) + (size_t)(kThreads / 32) * (32 / G) * m * (sizeof(double) + sizeof(int));
+}
+// coarse: [Tab][MsA][MsM][reg scratch][list scratch]
+static size_t coarse_smem(int m, int M, int G) {
+  const int TS = M > 0 ? split_rt(M) : 1;
+  return reg_smem(M, TS) + (size_t)M * (M + (M & 1)) * 8 + list_smem(m, G) - sizeof(Tab);
 }
 
 static CellOp make_op(fcm_mg* h, int q, int mode, const double* in, double* out, double coef,
@@ -623,6 +517,7 @@ static CellOp make_op(fcm_mg* h, int q, int mode, const double* in, double* out,
   op.m = Lv.m;
   op.ncell = (int32_t)h->ncell;
   op.base = Lv.base; op.stride = Lv.stride; op.cmin = Lv.cmin; op.cmax = Lv.cmax;
+  for (int i = 0; i < 3; ++i) { op.ilo[i] = Lv.ilo[i]; op.ihi[i] = Lv.ihi[i]; }
   op.mode = mode;
   op.kind = h->d_kind; op.cut_idx = h->d_cut_idx; op.Kref = h->d_Kref; op.cutK = h->d_cutK;
   op.ldK = h->L.m; op.alpha = h->alpha;
@@ -644,7 +539,9 @@ static void cellop_grid(const fcm_mg* h, int q, int mode, int* nb_reg, int* nb_l
   const int64_t cap = (int64_t)h->num_sms * 8;
   const int64_t cpb = (kThreads / 32) * (32 / Lv.G);  // cells per block on the list path
   if (Lv.M > 0) {
-    *nb_reg = (int)std::min<int64_t>((h->ncell + kThreads - 1) / kThreads, cap);
+    const int64_t ts = Lv.ts;
+    const int64_t cells_per_blk = (kThreads / 32) * (32 / ts);
+    *nb_reg = (int)std::min<int64_t>((h->ncell + cells_per_blk - 1) / cells_per_blk, cap);
     const int64_t nl = mode == OP_APPLY ? h->ncut : Lv.n_irr;
     *nb_list = (int)std::min<int64_t>((nl + cpb - 1) / cpb, cap);
   } else {
@@ -658,17 +555,37 @@ static int cellop_nblocks(const fcm_mg* h, int q, int mode) {
   return a + b;
 }
 
+// One cell-operator application = regular kernel + individual-list kernel; the list kernel
+// runs on a forked branch (graph fork/join when captured) so both populations overlap.
 static int launch_cellop(fcm_mg* h, int q, const CellOp& op) {
   const LevelDev& Lv = h->lev[q];
   int nb_reg, nb_list;
   cellop_grid(h, q, op.mode, &nb_reg, &nb_list);
-  if (nb_reg + nb_list == 0) return FCM_OK;
-  size_t sm = cellop_smem(Lv.m, Lv.M, Lv.G, 1);
   CellOp o = op;
-  void* args[] = {&o, &nb_reg};
-  cudaError_t e = cudaLaunchKernel(Lv.kcell, dim3(nb_reg + nb_list), dim3(kThreads), args, sm, h->stream);
-  h->count();
-  if (e != cudaSuccess) return fail(FCM_ECUDA, "cell kernel launch: %s", cudaGetErrorString(e));
+  int off = nb_reg;
+  cudaError_t e = cudaSuccess;
+  const bool fork = nb_reg > 0 && nb_list > 0;
+  if (fork) {
+    CU(cudaEventRecord(h->ev_fork, h->stream));
+    CU(cudaStreamWaitEvent(h->stream2, h->ev_fork, 0));
+  }
+  if (nb_list > 0) {
+    void* args[] = {&o, &off};
+    e = cudaLaunchKernel(Lv.klist, dim3(nb_list), dim3(kThreads), args, list_smem(Lv.m, Lv.G),
+                         fork ? h->stream2 : h->stream);
+    h->count();
+    if (e != cudaSuccess) return fail(FCM_ECUDA, "list kernel launch: %s", cudaGetErrorString(e));
+  }
+  if (nb_reg > 0) {
+    void* args[] = {&o};
+    e = cudaLaunchKernel(Lv.kreg, dim3(nb_reg), dim3(kThreads), args, reg_smem(Lv.M, Lv.ts), h->stream);
+    h->count();
+    if (e != cudaSuccess) return fail(FCM_ECUDA, "regular kernel launch: %s", cudaGetErrorString(e));
+  }
+  if (fork) {
+    CU(cudaEventRecord(h->ev_join, h->stream2));
+    CU(cudaStreamWaitEvent(h->stream, h->ev_join, 0));
+  }
   return FCM_OK;
 }
 
@@ -707,22 +624,39 @@ static int enqueue_coarse(fcm_mg* h, const double* b, double* x) {
     return FCM_OK;
   }
   CoarseArgs a{};
-  a.A = make_op(h, 1, OP_APPLY, h->c_p, h->c_q, 1.0, nullptr);
-  a.M = make_op(h, 1, OP_SMOOTH, h->c_r, h->c_z, 1.0, nullptr);
+  a.A = make_op(h, 1, OP_APPLY, nullptr, nullptr, 1.0, nullptr);
+  a.M = make_op(h, 1, OP_SMOOTH, nullptr, nullptr, 1.0, nullptr);
   a.jacobi = h->prm.coarse == FCM_COARSE_JACOBI_PCG;
   a.diag_inv = h->d_diag_inv;
-  a.b = b; a.x = x; a.r = h->c_r; a.z = h->c_z; a.p = h->c_p; a.q = h->c_q;
+  a.b = b; a.x = x;
+  for (int i = 0; i < 2; ++i) {
+    a.r[i] = h->c_vec[i]; a.z[i] = h->c_vec[2 + i]; a.w[i] = h->c_vec[4 + i]; a.q[i] = h->c_vec[6 + i];
+  }
+  a.p = h->c_vec[8];
   a.n = n;
   a.rtol2 = h->prm.coarse_rtol * h->prm.coarse_rtol;
   a.maxit = h->prm.coarse_maxit;
-  a.partA = h->d_partA + kMaxPartials;  // separate from the FCG partials
-  a.partB = h->d_partB + kMaxPartials;
+  a.part = h->c_part;
+  a.part_stride = kMaxPartials;
+  a.ctl = h->c_ctl;
+  {  // split the grid between the individual lists and the regular population (coarse.cuh)
+    const int nb = h->coarse_blocks;
+    static const bool nosplit = getenv("FCM_COARSE_NOSPLIT") && atoi(getenv("FCM_COARSE_NOSPLIT")) > 0;
+    auto share = [&](int64_t nlist) {
+      if (L1.M == 0) return nb;
+      if (nlist <= 0 || nb < 2 || nosplit) return 0;
+      int64_t v = (2 * nb * nlist + h->ncell - 1) / h->ncell;
+      return (int)std::max<int64_t>(1, std::min<int64_t>(v, nb / 2));
+    };
+    a.nbl_A = share(h->ncut);
+    a.nbl_M = share(L1.n_irr);
+  }
   a.iters = h->d_coarse_iters;
   void* args[] = {&a};
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(h->coarse_blocks);
   cfg.blockDim = dim3(kThreads);
-  cfg.dynamicSmemBytes = cellop_smem(L1.m, L1.M, L1.G, 2);
+  cfg.dynamicSmemBytes = coarse_smem(L1.m, L1.M, L1.G);
   cfg.stream = h->stream;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeCooperative;
@@ -984,6 +918,9 @@ extern "C" int fcm_mg_setup(const fcm_grid* g, const fcm_params* prm, const doub
   h->alpha = alpha;
   h->ustream = (cudaStream_t)prm->stream;
   CU(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+  CU(cudaStreamCreateWithFlags(&h->stream2, cudaStreamNonBlocking));
+  CU(cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming));
+  CU(cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming));
   CU(cudaEventCreateWithFlags(&h->ev_in, cudaEventDisableTiming));
   CU(cudaEventCreateWithFlags(&h->ev_out, cudaEventDisableTiming));
   CU(cudaEventRecord(h->ev_in, h->ustream));
@@ -1031,8 +968,20 @@ extern "C" int fcm_mg_setup(const fcm_grid* g, const fcm_params* prm, const doub
     LevelDev& Lv = h->lev[q];
     const LevelTable& T = L.tables[q];
     Lv.q = q; Lv.m = T.m; Lv.ndof = T.ndof; Lv.G = group_size(T.m);
-    Lv.kcell = cellop_kernel(T.m, Lv.G, &Lv.M);
-    CU(cudaFuncSetAttribute(Lv.kcell, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cellop_smem(Lv.m, Lv.M, Lv.G, 1)));
+    const bool ts1 = getenv("FCM_TS1") && atoi(getenv("FCM_TS1")) > 0;
+    Lv.kreg = reg_kernel(T.m, &Lv.M, ts1);
+    Lv.ts = (ts1 || Lv.M == 0) ? 1 : split_rt(Lv.M);
+    for (int i = 0; i < 3; ++i) {
+      Lv.ilo[i] = 0;
+      Lv.ihi[i] = L.n[i] - 1;
+      for (int a = 0; a < T.m; ++a) {
+        Lv.ilo[i] = std::max<int>(Lv.ilo[i], T.cmin[a * 3 + i]);
+        Lv.ihi[i] = std::min<int>(Lv.ihi[i], T.cmax[a * 3 + i]);
+      }
+    }
+    Lv.klist = list_kernel(Lv.G);
+    if (Lv.kreg) CU(cudaFuncSetAttribute(Lv.kreg, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)reg_smem(Lv.M, Lv.ts)));
+    CU(cudaFuncSetAttribute(Lv.klist, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)list_smem(Lv.m, Lv.G)));
     Lv.omega = q >= 2 ? prm->omega : 1.0;
     RC(h->alloc(&Lv.base, T.m));
     RC(h->alloc(&Lv.stride, T.m * 3));
@@ -1073,15 +1022,15 @@ extern "C" int fcm_mg_setup(const fcm_grid* g, const fcm_params* prm, const doub
       RC(h->alloc(&h->d_diag_inv, n1));
       CU(cudaMemcpyAsync(h->d_diag_inv, dg.data(), n1 * 8, cudaMemcpyHostToDevice, h->stream));
     }
-    RC(h->alloc(&h->c_r, n1));
-    RC(h->alloc(&h->c_z, n1));
-    RC(h->alloc(&h->c_p, n1));
-    RC(h->alloc(&h->c_q, n1));
+    for (int i = 0; i < 9; ++i) RC(h->alloc(&h->c_vec[i], n1));
+    RC(h->alloc(&h->c_part, 4 * kMaxPartials));
+    RC(h->alloc(&h->c_ctl, 1));
+    CU(cudaMemsetAsync(h->c_ctl, 0, sizeof(GridCtl), h->stream));
     // cooperative grid: co-resident blocks
     const LevelDev& L1 = h->lev[1];
     int M1 = 0;
     h->kcoarse = coarse_kernel(L1.m, L1.G, &M1);
-    size_t sm = cellop_smem(L1.m, M1, L1.G, 2);
+    size_t sm = coarse_smem(L1.m, M1, L1.G);
     CU(cudaFuncSetAttribute(h->kcoarse, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     int per_sm = 0;
     cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, h->kcoarse, kThreads, sm);
