@@ -1035,7 +1035,8 @@ extern "C" int fcm_mg_setup(const fcm_grid* g, const fcm_params* prm, const doub
     int per_sm = 0;
     cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, h->kcoarse, kThreads, sm);
     if (e != cudaSuccess || per_sm < 1) return fail(FCM_ECUDA, "coarse kernel occupancy query failed");
-    int64_t want = std::max<int64_t>(1, (n1 + kThreads - 1) / kThreads);
+    // the cell phases run over ncell cells with up to 32 cells per warp: fill every SM
+    int64_t want = std::max<int64_t>(1, std::max<int64_t>((n1 + kThreads - 1) / kThreads, h->ncell / 64));
     h->coarse_blocks = (int)std::min<int64_t>(want, (int64_t)h->num_sms * std::min(per_sm, 2));
     h->coarse_blocks = std::min(h->coarse_blocks, kMaxPartials);
     if (const char* env = getenv("FCM_COARSE_BLOCKS")) {  // tuning knob (co-residency capped)
