@@ -193,8 +193,6 @@ __global__ void __launch_bounds__(256) k_coarse_pcg(CoarseArgs a) {
   const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t nth = (int64_t)gridDim.x * blockDim.x;
   const int64_t n = a.n;
-  double* PA = a.part;
-  double* PB = a.part + a.part_stride;
   // barrier generations continue from the previous launch's last release (no barrier of this
   // launch can complete before every block has read it)
   unsigned gen = ld_acquire_u32(&a.ctl->release);

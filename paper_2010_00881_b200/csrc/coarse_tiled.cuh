@@ -1,0 +1,505 @@
+// coarse_tiled.cuh -- the coarsest level (p = 1, PAPER.md:226-228 Remark) solved by CG with
+// the undamped elementwise additive-Schwarz preconditioner (reading R4), for
+// coarse levels small enough that every SM can hold its piece of the vertex grid, and every
+// matrix that piece touches, in shared memory (config 2: 35,937 vertices; the inner solve is
+// latency-bound there).
+//
+// Design (one cooperative launch for the whole inner solve, ONE grid barrier per iteration):
+//  * Each CTA owns a brick T of the vertex grid (the p = 1 DOFs are the vertex modes, n_f per
+//    vertex) and keeps r and s on T grown by two vertex rings (E2), u on T grown by one ring
+//    (E1), and p, x on T in shared memory for the whole solve.  Every matrix its cells use is
+//    staged in shared memory once per launch: the leading 2^d n_f block of K_ref, the shared
+//    Schwarz inverses (one per boundary type), and the individual cut-cell matrices / Schwarz
+//    inverses of the cells in its box (the host sizes the bricks so that they fit).
+//  * The operator and the smoother are applied VERTEX-CENTRIC (gather only, no atomics):
+//      (A v)_(v,i) = sum_{cells c ni v} s_c K_c[a_v(c)*nf+i, :] v_c
+//      (M r)_(v,i) = sum_{cells c ni v} s_c A_c^{-1}[a_v(c)*nf+i, :] r_c
+//    K_c = leading block of the cell matrix (K_ref scaled by 1 or alpha, or the cut cell's
+//    own), A_c^{-1} = the cell's Schwarz inverse (scaled by 1/alpha for all-fictitious type
+//    blocks).  Cells are visited in a fixed order, so every CTA that evaluates a vertex gets
+//    bit-identical values.
+//  * CG in the Chronopoulos-Gear form (same iterates as standard PCG in exact arithmetic):
+//      u = M r, w = A u, gamma = (r,u), delta = (w,u), rho = (r,r)   [one all-reduce]
+//      beta = gamma/gamma_old, alpha = gamma/(delta - beta*gamma/alpha_old)
+//      p = u + beta p, s = w + beta s, x += alpha p, r -= alpha s
+//    After the all-reduce every CTA reads the w its neighbours published (E2 halo) and updates
+//    s and r REDUNDANTLY on E2 with the same scalars; then u on E1 and w on T need no further
+//    exchange.  Hence one grid-wide synchronisation per iteration, which also carries the
+//    three dot products (deterministic: every CTA sums the block partials in block order).
+//  * Stop when rho < rtol^2 rho_0 (recursive residual), iterations = x updates (as the
+//    oracle's standard PCG, x0 = 0).
+#pragma once
+#include <climits>
+#include <cstdint>
+
+namespace fcm {
+
+struct TiledArgs {
+  int n[3];          // cells per axis (1 for absent axes)
+  int blo[3];        // tiled vertex box (union of the free ranges of all components)
+  int tile[3];       // brick size (vertices)
+  int ntile[3];      // bricks per axis
+  int e[3];          // E2 extents = tile + 4 (1 for absent axes)
+  int ec[3];         // cell box extents = tile + 3 (1 for absent axes)
+  int64_t voff[3];   // class-major offset of component j's vertex class
+  int vlo[3][3];     // free vertex range of component j
+  int vhi[3][3];
+  int max_indiv;     // individual-matrix slots per CTA (host: max over bricks)
+  int ntypes;        // shared Schwarz inverses staged (type codes in type_codes)
+  int type_codes[64];
+  // operator
+  const uint8_t* kind;
+  const int32_t* cut_idx;
+  const double* cutK;
+  int ldK;           // leading dimension of K_ref / cut matrices (fine element size)
+  const double* Kref;
+  double alpha;
+  // smoother
+  int jacobi;
+  const double* diag_inv;
+  const int32_t* blk;
+  const double* type_inv;   // [64][M1*M1]
+  const double* irr_inv;    // [n_irr][M1*M1]
+  double inv_alpha;
+  // vectors (class-major, level 1)
+  const double* b;
+  double* x;
+  double* wpub[2];          // published w (double-buffered by iteration parity)
+  double* part;             // [2][3][nblocks]
+  struct TiledCtl* ctl;     // barrier state (zero-initialised once per handle)
+  double rtol2;
+  int maxit;
+  int* iters;               // [0] = this solve, [1] += this solve
+  unsigned long long* prof; // optional per-block phase times (ns): [nblocks][4]
+  // n_f = 1: the two matrices most cells use, row-major 8x8 in the PARAMETER bank, so that a
+  // warp whose cells all use them takes its matrix operands straight from the constant cache
+  int fastK, fastT0;        // 1 if Kc / T0c are valid
+  double Kc[64];            // leading 8x8 block of K_ref
+  double T0c[64];           // interior-type Schwarz inverse (code 0, unscaled)
+};
+
+__device__ __forceinline__ unsigned long long t_now() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ unsigned t_ld_relaxed(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void t_st_release(unsigned* p, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// cell code: -1 = no cell (outside the grid); otherwise the matrix offset in the staged
+// matrix pool (doubles) | kScaleBit when the cell's scale is alpha (operator) or 1/alpha
+// (smoother)
+constexpr int kNoCell = -1;
+constexpr int kScaleBit = 1 << 30;
+
+// shared-memory layout (doubles first, then ints); see tiled_smem_bytes
+template <int DIM, int NF>
+struct TiledSmem {
+  double* r;    // [NF][E2]
+  double* s;    // [NF][E2]
+  double* u;    // [NF][E2] (valid on E1)
+  double* p;    // [NF][T]
+  double* x;    // [NF][T]
+  double* mat;  // pool: [K_ref block][types][individual]
+  int* gidx;    // [NF][E2] class-major index or -1
+  int* cop;     // [EC] operator code per cell
+  int* csm;     // [EC] smoother code per cell
+  int E2, EC, T;
+};
+
+// matrices are symmetric: stored packed lower-triangular, entry (a, b), b <= a, at a(a+1)/2 + b
+__host__ __device__ constexpr int packed_size(int m) { return m * (m + 1) / 2; }
+__host__ __device__ constexpr int packed_at(int a, int b) {
+  return a >= b ? a * (a + 1) / 2 + b : b * (b + 1) / 2 + a;
+}
+// matrix slot stride in the pool: odd number of doubles, so that 32 lanes reading the same
+// entry of 32 different slots hit distinct bank pairs (no conflicts beyond the 2 wavefronts)
+__host__ __device__ constexpr int slot_stride(int m) { return packed_size(m) | 1; }
+__host__ __device__ constexpr size_t tiled_smem_bytes(int dim, int nf, int E2, int EC, int T, int nmats) {
+  return (size_t)(3 * nf * E2 + 2 * nf * T) * 8 + (size_t)nmats * slot_stride((1 << dim) * nf) * 8 +
+         (size_t)nf * E2 * 4 + (size_t)EC * 8 + 16;
+}
+
+// one row of the vertex-centric gather: sum over the 2^d cells around E2 entry l (local
+// coordinates lx, ly, lz) of s_c Mat_c[a_v(c)*NF + i, :] . vec_c (all operands in smem)
+constexpr int kT0Slot = 1;   // pool slot of the first staged type (the host puts code 0 first)
+
+template <int DIM, int NF, bool SMOOTH>
+__device__ __forceinline__ double vertex_row(const TiledArgs& a, const TiledSmem<DIM, NF>& S,
+                                             const double* __restrict__ vec, int l, int lx, int ly,
+                                             int lz, int i) {
+  constexpr int NC = 1 << DIM;
+  constexpr int M1 = NC * NF;
+  const int e0 = a.e[0], e01 = a.e[0] * a.e[1];
+  const int ec0 = a.ec[0], ec01 = a.ec[0] * a.ec[1];
+  const double scale = SMOOTH ? a.inv_alpha : a.alpha;
+  double acc = 0.0;
+  if constexpr (NF == 1) {
+    constexpr int T0_OFF = kT0Slot * slot_stride(M1);
+    // the 3^d neighbourhood of the vertex, loaded once into registers
+    constexpr int N3 = DIM == 3 ? 27 : 9;
+    double nb[N3];
+#pragma unroll
+    for (int q = 0; q < N3; ++q) {
+      const int dx = q % 3 - 1, dy = (q / 3) % 3 - 1, dz = DIM == 3 ? q / 9 - 1 : 0;
+      nb[q] = vec[l + dx + dy * e0 + dz * e01];
+    }
+#pragma unroll
+    for (int kc = 0; kc < NC; ++kc) {
+      const int ox = kc & 1, oy = (kc >> 1) & 1, oz = (kc >> 2) & 1;
+      const int cl = (lz - oz) * ec01 + (ly - oy) * ec0 + (lx - ox);
+      const int code = SMOOTH ? S.csm[cl] : S.cop[cl];
+      double t = 0.0;
+      {
+        const double* mat = S.mat + (code == kNoCell ? 0 : (code & (kScaleBit - 1)));
+#pragma unroll
+        for (int k2 = 0; k2 < NC; ++k2) {
+          // corner k2 of the cell relative to the vertex (corner kc): offsets in {-1, 0, 1}
+          const int q = ((k2 & 1) - ox + 1) + 3 * (((k2 >> 1) & 1) - oy + 1) +
+                        (DIM == 3 ? 9 * (((k2 >> 2) & 1) - oz + 1) : 0);
+          t = fma(mat[packed_at(kc, k2)], nb[q], t);
+        }
+      }
+      if (code != kNoCell) acc = fma((code & kScaleBit) ? scale : 1.0, t, acc);
+    }
+  } else {
+#pragma unroll
+  for (int kc = 0; kc < NC; ++kc) {
+    const int ox = kc & 1, oy = (kc >> 1) & 1, oz = (kc >> 2) & 1;
+    // the cell box shares the E2 origin: cell local = vertex local - corner offset
+    const int cl = (lz - oz) * ec01 + (ly - oy) * ec0 + (lx - ox);
+    const int code = SMOOTH ? S.csm[cl] : S.cop[cl];
+    if (code == kNoCell) continue;
+    const double* mat = S.mat + (code & (kScaleBit - 1));
+    const int base = l - (ox + oy * e0 + oz * e01);
+    double t = 0.0;
+#pragma unroll
+    for (int k2 = 0; k2 < NC; ++k2) {
+      const int d = (k2 & 1) + ((k2 >> 1) & 1) * e0 + ((k2 >> 2) & 1) * e01;
+#pragma unroll
+      for (int j = 0; j < NF; ++j)
+        t = fma(mat[packed_at(kc * NF + i, k2 * NF + j)], vec[j * S.E2 + base + d], t);
+    }
+    acc = fma((code & kScaleBit) ? scale : 1.0, t, acc);
+  }
+  }
+  return acc;
+}
+
+// deterministic block reduction of three values; result valid in warp 0
+__device__ __forceinline__ void block_sum3(double& v0, double& v1, double& v2, double* red /*[3*32]*/) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    v0 += __shfl_xor_sync(0xffffffffu, v0, o);
+    v1 += __shfl_xor_sync(0xffffffffu, v1, o);
+    v2 += __shfl_xor_sync(0xffffffffu, v2, o);
+  }
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31, nw = blockDim.x >> 5;
+  if (l == 0) { red[w] = v0; red[32 + w] = v1; red[64 + w] = v2; }
+  __syncthreads();
+  if (w == 0) {
+    double a0 = l < nw ? red[l] : 0.0, a1 = l < nw ? red[32 + l] : 0.0, a2 = l < nw ? red[64 + l] : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      a0 += __shfl_xor_sync(0xffffffffu, a0, o);
+      a1 += __shfl_xor_sync(0xffffffffu, a1, o);
+      a2 += __shfl_xor_sync(0xffffffffu, a2, o);
+    }
+    v0 = a0; v1 = a1; v2 = a2;
+  }
+}
+
+// Grid barrier fused with a deterministic all-reduce of three doubles.  Each block posts its
+// partials in its own slot and adds 1 to one arrival counter (a single same-address RED per
+// block, release semantics); one thread per block polls the counter (acquire) until every
+// block of this generation has arrived (measured ~1.3 us on B200 for 128-148 blocks, vs ~4 us
+// when the last arrival reduces and re-releases).  Then warp 0 of every block sums all
+// partials in block order, so every block holds bit-identical totals.  Counter targets compare
+// modulo 2^32; partials are double-buffered by generation parity.
+struct TiledCtl {
+  unsigned count;          // arrivals (monotone)
+  unsigned pad0[31];
+  unsigned base;           // count at the end of the previous launch (written by block 0 last)
+  unsigned pad1[31];
+};
+
+__device__ __forceinline__ unsigned t_ld_acquire(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void t_red_release(unsigned* p, unsigned v) {
+  asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+__device__ __noinline__ void tiled_allreduce3(double v0, double v1, double v2, double* part,
+                                              TiledCtl* ctl, unsigned target, unsigned gen,
+                                              double* red, double* tot) {
+  block_sum3(v0, v1, v2, red);
+  const int nb = gridDim.x;
+  double* pp = part + (size_t)(gen & 1) * 3 * nb;
+  if (threadIdx.x < 32) {
+    const int l = threadIdx.x;
+    if (l == 0) {
+      __stcg(pp + blockIdx.x, v0);
+      __stcg(pp + nb + blockIdx.x, v1);
+      __stcg(pp + 2 * nb + blockIdx.x, v2);
+      t_red_release(&ctl->count, 1u);   // orders this block's earlier global writes (w, partials)
+      while ((int)(t_ld_acquire(&ctl->count) - target) < 0) {}
+    }
+    __syncwarp();
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+    for (int j = l; j < nb; j += 32) {
+      a0 += __ldcg(pp + j);
+      a1 += __ldcg(pp + nb + j);
+      a2 += __ldcg(pp + 2 * nb + j);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      a0 += __shfl_xor_sync(0xffffffffu, a0, o);
+      a1 += __shfl_xor_sync(0xffffffffu, a1, o);
+      a2 += __shfl_xor_sync(0xffffffffu, a2, o);
+    }
+    if (l == 0) { tot[0] = a0; tot[1] = a1; tot[2] = a2; }
+  }
+  __syncthreads();
+}
+
+template <int DIM, int NF>
+__global__ void __launch_bounds__(512, 1) k_coarse_tiled(TiledArgs a) {
+  constexpr int NC = 1 << DIM;
+  constexpr int M1 = NC * NF;
+  constexpr int MM = slot_stride(M1);
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ double red[96];
+  __shared__ double tot[3];
+  __shared__ int n_indiv;
+  __shared__ int type_slot[64];
+  TiledSmem<DIM, NF> S;
+  const int e0 = a.e[0], e1 = a.e[1], e2d = a.e[2];
+  const int t0 = a.tile[0], t1 = DIM > 1 ? a.tile[1] : 1, t2 = DIM > 2 ? a.tile[2] : 1;
+  S.E2 = e0 * e1 * e2d;
+  S.EC = a.ec[0] * a.ec[1] * a.ec[2];
+  S.T = t0 * t1 * t2;
+  const int nmat = 1 + a.ntypes + a.max_indiv;
+  {
+    double* d = reinterpret_cast<double*>(smem);
+    S.r = d; d += NF * S.E2;
+    S.s = d; d += NF * S.E2;
+    S.u = d; d += NF * S.E2;
+    S.p = d; d += NF * S.T;
+    S.x = d; d += NF * S.T;
+    S.mat = d; d += (size_t)nmat * MM;
+    S.gidx = reinterpret_cast<int*>(d);
+    S.cop = S.gidx + NF * S.E2;
+    S.csm = S.cop + S.EC;
+  }
+  // brick of this block
+  const int bt = blockIdx.x;
+  const int tix = bt % a.ntile[0], tiy = (bt / a.ntile[0]) % a.ntile[1], tiz = bt / (a.ntile[0] * a.ntile[1]);
+  const int o0 = a.blo[0] + tix * a.tile[0] - 2;
+  const int o1 = DIM > 1 ? a.blo[1] + tiy * a.tile[1] - 2 : 0;
+  const int o2 = DIM > 2 ? a.blo[2] + tiz * a.tile[2] - 2 : 0;
+  const int E2 = S.E2;
+  // ---- one-time staging: K_ref block, shared Schwarz inverses, cell codes ----------------
+  if (threadIdx.x == 0) n_indiv = 0;
+  for (int t = threadIdx.x; t < 64; t += blockDim.x) type_slot[t] = -1;
+  __syncthreads();
+  for (int t = threadIdx.x; t < a.ntypes; t += blockDim.x) type_slot[a.type_codes[t]] = t;
+  for (int t = threadIdx.x; t < M1 * M1; t += blockDim.x) {
+    const int r = t / M1, c = t % M1;
+    if (c <= r) S.mat[packed_at(r, c)] = a.Kref[r * a.ldK + c];
+  }
+  for (int t = threadIdx.x; t < a.ntypes * M1 * M1; t += blockDim.x) {
+    const int k = t / (M1 * M1), r = (t / M1) % M1, c = t % M1;
+    if (c <= r) S.mat[(1 + k) * MM + packed_at(r, c)] = a.type_inv[(size_t)a.type_codes[k] * M1 * M1 + r * M1 + c];
+  }
+  __syncthreads();
+  const int indiv0 = (1 + a.ntypes) * MM;   // first individual slot (doubles)
+  for (int t = threadIdx.x; t < S.EC; t += blockDim.x) {
+    const int lx = t % a.ec[0], ly = (t / a.ec[0]) % a.ec[1], lz = t / (a.ec[0] * a.ec[1]);
+    const int cx = o0 + lx, cy = o1 + ly, cz = o2 + lz;
+    int2 code = make_int2(kNoCell, kNoCell);
+    if (cx >= 0 && cy >= 0 && cz >= 0 && cx < a.n[0] && cy < a.n[1] && cz < a.n[2]) {
+      const int c = (cz * a.n[1] + cy) * a.n[0] + cx;
+      const int k = a.kind[c];
+      if (k == 2) {   // cut cell: its own (leading) matrix
+        const int slot = atomicAdd(&n_indiv, 1);
+        const double* src = a.cutK + (size_t)a.cut_idx[c] * a.ldK * a.ldK;
+        double* dst = S.mat + indiv0 + slot * MM;
+        for (int r = 0; r < M1; ++r)
+          for (int c2 = 0; c2 <= r; ++c2) dst[packed_at(r, c2)] = __ldg(src + r * a.ldK + c2);
+        code.x = indiv0 + slot * MM;
+      } else {
+        code.x = k == 1 ? kScaleBit : 0;
+      }
+      if (!a.jacobi) {
+        const int bq = a.blk[c];
+        if (bq >= 0) {   // irregular block: individual inverse
+          const int slot = atomicAdd(&n_indiv, 1);
+          const double* src = a.irr_inv + (size_t)bq * M1 * M1;
+          double* dst = S.mat + indiv0 + slot * MM;
+          for (int r = 0; r < M1; ++r)
+            for (int c2 = 0; c2 <= r; ++c2) dst[packed_at(r, c2)] = __ldg(src + r * M1 + c2);
+          code.y = indiv0 + slot * MM;
+        } else {
+          const int tt = -bq - 1;
+          code.y = (1 + type_slot[tt & 0xff]) * MM | ((tt >> 12) ? kScaleBit : 0);
+        }
+      }
+    }
+    S.cop[t] = code.x;
+    S.csm[t] = code.y;
+  }
+  for (int t = threadIdx.x; t < NF * E2; t += blockDim.x) {
+    const int j = t / E2, l = t % E2;
+    const int v0 = o0 + l % e0, v1 = o1 + (l / e0) % e1, v2 = o2 + l / (e0 * e1);
+    int g = -1;
+    if (v0 >= a.vlo[j][0] && v0 <= a.vhi[j][0] && v1 >= a.vlo[j][1] && v1 <= a.vhi[j][1] &&
+        v2 >= a.vlo[j][2] && v2 <= a.vhi[j][2]) {
+      const int s0 = a.vhi[j][0] - a.vlo[j][0] + 1, s1 = a.vhi[j][1] - a.vlo[j][1] + 1;
+      g = (int)a.voff[j] + (v0 - a.vlo[j][0]) + s0 * ((v1 - a.vlo[j][1]) + s1 * (v2 - a.vlo[j][2]));
+    }
+    S.gidx[t] = g;
+    S.r[t] = g >= 0 ? a.b[g] : 0.0;
+    S.s[t] = 0.0;
+    S.u[t] = 0.0;
+  }
+  for (int t = threadIdx.x; t < NF * S.T; t += blockDim.x) { S.p[t] = 0.0; S.x[t] = 0.0; }
+  __syncthreads();
+  // regions in local E2 coordinates: E1 = [1, tile+2], T = [2, tile+1] per present axis
+  const int g1x = t0 + 2, g1y = DIM > 1 ? t1 + 2 : 1, g1z = DIM > 2 ? t2 + 2 : 1;
+  const int nE1 = g1x * g1y * g1z;
+  const int nT = S.T;
+  const int shy1 = DIM > 1 ? 1 : 0, shz1 = DIM > 2 ? 1 : 0;
+  const int shy2 = DIM > 1 ? 2 : 0, shz2 = DIM > 2 ? 2 : 0;
+  auto t_local = [&](int q) {   // T entry q -> E2 linear index
+    const int lx = q % t0 + 2, ly = (q / t0) % t1 + shy2, lz = q / (t0 * t1) + shz2;
+    return (lz * e1 + ly) * e0 + lx;
+  };
+
+  auto smooth_E1 = [&]() {   // u = M r on E1
+    for (int t = threadIdx.x; t < NF * nE1; t += blockDim.x) {
+      const int i = t / nE1, q = t % nE1;
+      const int lx = q % g1x + 1, ly = (q / g1x) % g1y + shy1, lz = q / (g1x * g1y) + shz1;
+      const int l = (lz * e1 + ly) * e0 + lx;
+      const int gi = S.gidx[i * E2 + l];
+      double u = 0.0;
+      if (gi >= 0) {
+        if (a.jacobi) u = __ldg(a.diag_inv + gi) * S.r[i * E2 + l];
+        else u = vertex_row<DIM, NF, true>(a, S, S.r, l, lx, ly, lz, i);
+      }
+      S.u[i * E2 + l] = u;
+    }
+  };
+  // w = A u on T; publish w; partials (r,u), (w,u), (r,r)
+  auto apply_T = [&](double* wout, double& g, double& dl, double& rh) {
+    g = 0.0; dl = 0.0; rh = 0.0;
+    for (int t = threadIdx.x; t < NF * nT; t += blockDim.x) {
+      const int i = t / nT, q = t % nT;
+      const int lx = q % t0 + 2, ly = (q / t0) % t1 + shy2, lz = q / (t0 * t1) + shz2;
+      const int l = (lz * e1 + ly) * e0 + lx;
+      const int gi = S.gidx[i * E2 + l];
+      if (gi < 0) continue;
+      const double w = vertex_row<DIM, NF, false>(a, S, S.u, l, lx, ly, lz, i);
+      __stcg(wout + gi, w);
+      const double ri = S.r[i * E2 + l], ui = S.u[i * E2 + l];
+      g = fma(ri, ui, g);
+      dl = fma(w, ui, dl);
+      rh = fma(ri, ri, rh);
+    }
+  };
+
+  // the arrival counter continues from the previous launch (every block passed the same
+  // number of barriers, so it is a multiple of gridDim.x here)
+  const unsigned cnt0 = t_ld_relaxed(&a.ctl->base);
+  unsigned gen = 0;
+  double g_loc, d_loc, r_loc;
+  smooth_E1();
+  __syncthreads();
+  apply_T(a.wpub[0], g_loc, d_loc, r_loc);
+  tiled_allreduce3(g_loc, d_loc, r_loc, a.part, a.ctl, cnt0 + (gen + 1) * gridDim.x, gen + 1, red, tot); ++gen;
+  double gamma = tot[0], delta = tot[1];
+  const double rho0 = tot[2];
+  double rho = rho0;
+  double gamma_old = 1.0, alpha_old = 1.0;
+  int it = 0;
+  while (rho0 > 0.0 && !(rho < a.rtol2 * rho0) && it < a.maxit) {
+    double beta, alpha;
+    if (it == 0) {
+      beta = 0.0;
+      alpha = gamma / delta;
+    } else {
+      beta = gamma / gamma_old;
+      alpha = gamma / (delta - beta * gamma / alpha_old);
+    }
+    if (!(alpha > 0.0) || !(gamma > 0.0)) break;   // breakdown (not SPD): keep x_it
+    const unsigned long long tp0 = a.prof ? t_now() : 0ull;
+    // s = w + beta s, r -= alpha s on E2 (w of the neighbours published before the barrier)
+    const double* wv = a.wpub[it & 1];
+    for (int t0b = 0; t0b < NF * E2; t0b += 4 * blockDim.x) {   // 4 L2 loads in flight per thread
+      double wl[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int t = t0b + k * blockDim.x + threadIdx.x;
+        const int gi = t < NF * E2 ? S.gidx[t] : -1;
+        wl[k] = gi >= 0 ? __ldcg(wv + gi) : 0.0;
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int t = t0b + k * blockDim.x + threadIdx.x;
+        if (t < NF * E2 && S.gidx[t] >= 0) {
+          const double sv = fma(beta, S.s[t], wl[k]);
+          S.s[t] = sv;
+          S.r[t] = fma(-alpha, sv, S.r[t]);
+        }
+      }
+    }
+    // p = u + beta p, x += alpha p on T
+    for (int t = threadIdx.x; t < NF * nT; t += blockDim.x) {
+      const int i = t / nT, q = t % nT;
+      const double pv = fma(beta, S.p[t], S.u[i * E2 + t_local(q)]);
+      S.p[t] = pv;
+      S.x[t] = fma(alpha, pv, S.x[t]);
+    }
+    ++it;
+    gamma_old = gamma;
+    alpha_old = alpha;
+    __syncthreads();
+    const unsigned long long tp1 = a.prof ? t_now() : 0ull;
+    smooth_E1();
+    __syncthreads();
+    const unsigned long long tp2 = a.prof ? t_now() : 0ull;
+    apply_T(a.wpub[it & 1], g_loc, d_loc, r_loc);
+    __syncthreads();
+    const unsigned long long tp3 = a.prof ? t_now() : 0ull;
+    tiled_allreduce3(g_loc, d_loc, r_loc, a.part, a.ctl, cnt0 + (gen + 1) * gridDim.x, gen + 1, red, tot); ++gen;
+    if (a.prof && threadIdx.x == 0) {
+      const unsigned long long tp4 = t_now();
+      unsigned long long* pr = a.prof + 4 * blockIdx.x;
+      pr[0] += tp1 - tp0; pr[1] += tp2 - tp1; pr[2] += tp3 - tp2; pr[3] += tp4 - tp3;
+    }
+    gamma = tot[0];
+    delta = tot[1];
+    rho = tot[2];
+  }
+  // x on T -> global
+  for (int t = threadIdx.x; t < NF * nT; t += blockDim.x) {
+    const int i = t / nT, q = t % nT;
+    const int gi = S.gidx[i * E2 + t_local(q)];
+    if (gi >= 0) a.x[gi] = S.x[t];
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    a.iters[0] = it;
+    a.iters[1] += it;
+    a.ctl->base = cnt0 + gen * gridDim.x;   // every block has read base (all passed barrier 1)
+  }
+}
+
+}  // namespace fcm

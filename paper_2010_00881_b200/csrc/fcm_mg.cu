@@ -15,6 +15,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <climits>
 #include <cmath>
 #include <cstring>
 #include <map>
@@ -25,6 +26,7 @@
 #include "../../include/fcm_mg.h"
 #include "cellop.cuh"
 #include "coarse.cuh"
+#include "coarse_tiled.cuh"
 #include "common.hpp"
 #include "layout.hpp"
 
@@ -76,6 +78,8 @@ struct LevelDev {
   int32_t* irr_list = nullptr;     // cells with an individual Schwarz inverse (irr order)
   int ilo[3] = {0, 0, 0}, ihi[3] = {-1, -1, -1};  // cells with no Dirichlet DOF
   int ts = 1;                      // threads per cell of the regular path
+  std::vector<int32_t> blk_h;      // host copy of blk (tiled coarse setup)
+  std::vector<int> type_codes_h;   // boundary-type codes with a shared inverse
   // vectors
   double* x = nullptr;
   double* r = nullptr;
@@ -110,6 +114,11 @@ struct fcm_mg {
   GridCtl* c_ctl = nullptr;
   int* d_coarse_iters = nullptr;
   int coarse_blocks = 0;
+  // tiled coarse solver (coarse_tiled.cuh): used when every brick fits in shared memory
+  const void* ktiled = nullptr;
+  TiledArgs tiled{};
+  int t_blocks = 0;
+  size_t t_smem = 0;
   // FCG
   double *f_b = nullptr, *f_x = nullptr, *f_r = nullptr, *f_ro = nullptr, *f_p = nullptr, *f_q = nullptr;
   Scalars* d_s = nullptr;
@@ -477,6 +486,13 @@ const void* coarse_kernel(int m, int G, int* M_out) {
     default: return (const void*)k_coarse_pcg<0, 32>;
   }
 }
+const void* tiled_kernel(int dim, int nf) {
+  if (dim == 3 && nf == 1) return (const void*)k_coarse_tiled<3, 1>;
+  if (dim == 3 && nf == 3) return (const void*)k_coarse_tiled<3, 3>;
+  if (dim == 2 && nf == 1) return (const void*)k_coarse_tiled<2, 1>;
+  return nullptr;
+}
+constexpr int kTiledThreads = 512;
 
 inline int grid_for(int64_t n, int sms) {
   int64_t b = (n + kThreads - 1) / kThreads;
@@ -623,6 +639,25 @@ static int enqueue_coarse(fcm_mg* h, const double* b, double* x) {
     CU(cudaGetLastError());
     return FCM_OK;
   }
+  if (h->ktiled) {
+    TiledArgs a = h->tiled;
+    a.b = b;
+    a.x = x;
+    void* args[] = {&a};
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(h->t_blocks);
+    cfg.blockDim = dim3(kTiledThreads);
+    cfg.dynamicSmemBytes = h->t_smem;
+    cfg.stream = h->stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    CU(cudaLaunchKernelExC(&cfg, h->ktiled, args));
+    h->count();
+    return FCM_OK;
+  }
   CoarseArgs a{};
   a.A = make_op(h, 1, OP_APPLY, nullptr, nullptr, 1.0, nullptr);
   a.M = make_op(h, 1, OP_SMOOTH, nullptr, nullptr, 1.0, nullptr);
@@ -663,7 +698,7 @@ static int enqueue_coarse(fcm_mg* h, const double* b, double* x) {
   attr[0].val.cooperative = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  cudaError_t e = cudaLaunchKernelExC(&cfg, h->kcoarse, args);
+  CU(cudaLaunchKernelExC(&cfg, h->kcoarse, args));
   h->count();
   return FCM_OK;
 }
@@ -869,6 +904,8 @@ static int setup_schwarz(fcm_mg* h, int q, const std::vector<uint8_t>& kind,
   }
   Lv.has_as = true;
   Lv.n_types = (int32_t)ntypes;
+  Lv.blk_h = blk;
+  Lv.type_codes_h = type_slot;
   return FCM_OK;
 }
 
@@ -896,6 +933,165 @@ static void coarse_dense(const fcm_mg* h, const std::vector<uint8_t>& kind,
           if (idx[b] >= 0) (*dense)[(size_t)idx[a] * n + idx[b]] += s * K[(size_t)a * m + b];
     }
   }
+}
+
+// Tiled coarse solver (coarse_tiled.cuh): choose the vertex brick that minimises the
+// per-SM work (redundant halo evaluation included) such that one brick per SM fits in shared
+// memory; leaves h->ktiled null when the level is too large (the grid-wide kernel is used).
+static int setup_tiled(fcm_mg* h) {
+  const int env = getenv("FCM_COARSE_TILED") ? atoi(getenv("FCM_COARSE_TILED")) : 1;
+  if (!env) return FCM_OK;
+  const Layout& L = h->L;
+  const int dim = L.dim, nf = L.n_f;
+  const void* k = tiled_kernel(dim, nf);
+  if (!k) return FCM_OK;
+  const int NC = 1 << dim, M1 = NC * nf;
+  if (L.m_level[1] != M1) return FCM_OK;
+  // convention check: local DOF a < M1 is corner a / nf (bit i = offset along axis i), comp a % nf
+  TiledArgs t{};
+  for (int a = 0; a < M1; ++a) {
+    const DofClass& dc = L.classes[L.dof_class[a]];
+    if (dc.S != 0 || dc.order != 1 || dc.comp != a % nf) return FCM_OK;
+    for (int i = 0; i < dim; ++i)
+      if (L.dof_off[a][i] != ((a / nf) >> i & 1)) return FCM_OK;
+    const int j = a % nf;
+    t.voff[j] = dc.off;
+    for (int i = 0; i < 3; ++i) { t.vlo[j][i] = dc.lo[i]; t.vhi[j][i] = dc.hi[i]; }
+  }
+  if (L.ndof_level[1] >= (1LL << 31)) return FCM_OK;
+  int B[3];
+  for (int i = 0; i < 3; ++i) {
+    int lo = INT_MAX, hi = INT_MIN;
+    for (int j = 0; j < nf; ++j) { lo = std::min(lo, t.vlo[j][i]); hi = std::max(hi, t.vhi[j][i]); }
+    t.blo[i] = lo;
+    B[i] = hi - lo + 1;
+    t.n[i] = L.n[i];
+  }
+  const LevelDev& L1 = h->lev[1];
+  const bool jac = h->prm.coarse == FCM_COARSE_JACOBI_PCG;
+  if (!jac && (int)L1.type_codes_h.size() > 64) return FCM_OK;
+  // individual matrices per cell (cut-cell operator block + irregular Schwarz inverse), and
+  // their 3D prefix sums for box counts
+  const int nx = L.n[0], ny = L.n[1], nz = L.n[2];
+  std::vector<int> pre((size_t)(nx + 1) * (ny + 1) * (nz + 1), 0);
+  auto P = [&](int x, int y, int z) -> int& { return pre[((size_t)z * (ny + 1) + y) * (nx + 1) + x]; };
+  {
+    std::vector<uint8_t> kind(h->ncell);
+    CU(cudaMemcpy(kind.data(), h->d_kind, h->ncell, cudaMemcpyDeviceToHost));
+    for (int z = 0; z < nz; ++z)
+      for (int y = 0; y < ny; ++y)
+        for (int x = 0; x < nx; ++x) {
+          const int64_t c = ((int64_t)z * ny + y) * nx + x;
+          const int w = (kind[c] == 2) + ((!jac && L1.blk_h[c] >= 0) ? 1 : 0);
+          P(x + 1, y + 1, z + 1) = w + P(x, y + 1, z + 1) + P(x + 1, y, z + 1) + P(x + 1, y + 1, z) -
+                                   P(x, y, z + 1) - P(x, y + 1, z) - P(x + 1, y, z) + P(x, y, z);
+        }
+  }
+  auto box_count = [&](int x0, int x1, int y0, int y1, int z0, int z1) {  // inclusive cell box, clipped
+    x0 = std::max(x0, 0); y0 = std::max(y0, 0); z0 = std::max(z0, 0);
+    x1 = std::min(x1, nx - 1); y1 = std::min(y1, ny - 1); z1 = std::min(z1, nz - 1);
+    if (x0 > x1 || y0 > y1 || z0 > z1) return 0;
+    ++x1; ++y1; ++z1;
+    return P(x1, y1, z1) - P(x0, y1, z1) - P(x1, y0, z1) - P(x1, y1, z0) + P(x0, y0, z1) + P(x0, y1, z0) +
+           P(x1, y0, z0) - P(x0, y0, z0);
+  };
+  const int ntypes = jac ? 0 : (int)L1.type_codes_h.size();
+  int max_smem = 0;
+  CU(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, h->dev));
+  const size_t smem_cap = (size_t)max_smem - 2048;  // static shared memory of the kernel
+  double best = 1e300;
+  int bt[3] = {0, 0, 0}, best_indiv = 0;
+  const int R = kTiledThreads;
+  auto rounds = [&](int64_t w) { return (double)((w + R - 1) / R); };
+  const int tzmax = dim > 2 ? B[2] : 1, tymax = dim > 1 ? B[1] : 1;
+  for (int tz = 1; tz <= tzmax; ++tz)
+    for (int ty = 1; ty <= tymax; ++ty)
+      for (int tx = 1; tx <= B[0]; ++tx) {
+        const int ntl[3] = {(B[0] + tx - 1) / tx, (B[1] + ty - 1) / ty, (B[2] + tz - 1) / tz};
+        const int64_t nt = (int64_t)ntl[0] * ntl[1] * ntl[2];
+        if (nt > h->num_sms) continue;
+        const int e[3] = {tx + 4, dim > 1 ? ty + 4 : 1, dim > 2 ? tz + 4 : 1};
+        const int ec[3] = {tx + 3, dim > 1 ? ty + 3 : 1, dim > 2 ? tz + 3 : 1};
+        const int64_t E2 = (int64_t)e[0] * e[1] * e[2], EC = (int64_t)ec[0] * ec[1] * ec[2];
+        const int64_t T = (int64_t)tx * ty * tz;
+        if (tiled_smem_bytes(dim, nf, (int)E2, (int)EC, (int)T, 1 + ntypes) > smem_cap) continue;
+        const int64_t E1 = (int64_t)(tx + 2) * (dim > 1 ? ty + 2 : 1) * (dim > 2 ? tz + 2 : 1);
+        const double gather = NC * (M1 + 4.0);
+        const double cost = gather * R * (rounds(nf * E1) + rounds(nf * T)) + 6.0 * R * rounds(nf * E2);
+        if (cost >= best) continue;
+        int mx = 0;   // individual matrices of the worst brick's cell box
+        const int tt[3] = {tx, ty, tz};
+        for (int k = 0; k < ntl[2]; ++k)
+          for (int j = 0; j < ntl[1]; ++j)
+            for (int i = 0; i < ntl[0]; ++i) {
+              int lo[3], hi[3];
+              const int id[3] = {i, j, k};
+              for (int d = 0; d < 3; ++d) {
+                if (d < dim) { lo[d] = t.blo[d] + id[d] * tt[d] - 2; hi[d] = lo[d] + tt[d] + 2; }
+                else { lo[d] = 0; hi[d] = 0; }
+              }
+              mx = std::max(mx, box_count(lo[0], hi[0], lo[1], hi[1], lo[2], hi[2]));
+            }
+        if (tiled_smem_bytes(dim, nf, (int)E2, (int)EC, (int)T, 1 + ntypes + mx) > smem_cap) continue;
+        best = cost; bt[0] = tx; bt[1] = ty; bt[2] = tz; best_indiv = mx;
+      }
+  if (bt[0] == 0) return FCM_OK;
+  for (int i = 0; i < 3; ++i) {
+    t.tile[i] = bt[i];
+    t.ntile[i] = (B[i] + bt[i] - 1) / bt[i];
+    const bool present = i < dim;
+    t.e[i] = present ? bt[i] + 4 : 1;
+    t.ec[i] = present ? bt[i] + 3 : 1;
+  }
+  t.max_indiv = best_indiv;
+  t.ntypes = ntypes;
+  for (int i = 0; i < ntypes; ++i) t.type_codes[i] = L1.type_codes_h[i];
+  // parameter-bank copies of the leading K_ref block and the interior-type inverse (n_f = 1)
+  if (nf == 1 && M1 == 8) {
+    std::vector<double> kr((size_t)L.m * L.m);
+    CU(cudaMemcpy(kr.data(), h->d_Kref, kr.size() * 8, cudaMemcpyDeviceToHost));
+    for (int r = 0; r < 8; ++r)
+      for (int c = 0; c < 8; ++c) t.Kc[r * 8 + c] = kr[(size_t)r * L.m + c];
+    t.fastK = 1;
+    if (ntypes > 0 && L1.type_codes_h[0] == 0) {   // staged in pool slot 1 (kT0Slot)
+      CU(cudaMemcpy(t.T0c, L1.type_inv, 64 * 8, cudaMemcpyDeviceToHost));
+      t.fastT0 = 1;
+    }
+  }
+  const int E2 = t.e[0] * t.e[1] * t.e[2], EC = t.ec[0] * t.ec[1] * t.ec[2];
+  const size_t sm = tiled_smem_bytes(dim, nf, E2, EC, bt[0] * bt[1] * bt[2], 1 + ntypes + best_indiv);
+  CU(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+  int per_sm = 0;
+  CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kTiledThreads, sm));
+  const int nb = t.ntile[0] * t.ntile[1] * t.ntile[2];
+  if (per_sm < 1 || nb > per_sm * h->num_sms) return FCM_OK;
+  t.kind = h->d_kind; t.cut_idx = h->d_cut_idx; t.cutK = h->d_cutK; t.ldK = L.m; t.Kref = h->d_Kref;
+  t.alpha = h->alpha;
+  t.jacobi = h->prm.coarse == FCM_COARSE_JACOBI_PCG;
+  t.diag_inv = h->d_diag_inv;
+  t.blk = L1.blk; t.type_inv = L1.type_inv; t.irr_inv = L1.irr_inv; t.inv_alpha = 1.0 / h->alpha;
+  const int64_t n1 = L.ndof_level[1];
+  RC(h->alloc(&t.wpub[0], n1));
+  RC(h->alloc(&t.wpub[1], n1));
+  RC(h->alloc(&t.part, (size_t)6 * nb));
+  RC(h->alloc(&t.ctl, 1));
+  CU(cudaMemsetAsync(t.ctl, 0, sizeof(TiledCtl), h->stream));
+  t.rtol2 = h->prm.coarse_rtol * h->prm.coarse_rtol;
+  t.maxit = h->prm.coarse_maxit;
+  t.iters = h->d_coarse_iters;
+  if (getenv("FCM_TILED_PROF")) {
+    RC(h->alloc(&t.prof, (size_t)4 * nb));
+    CU(cudaMemsetAsync(t.prof, 0, (size_t)32 * nb, h->stream));
+  }
+  if (getenv("FCM_VERBOSE"))
+    fprintf(stderr, "[fcm] tiled coarse: box %d x %d x %d, tile %d x %d x %d, %d blocks, %d types, "
+            "<= %d individual matrices per brick, smem %zu B\n", B[0], B[1], B[2], bt[0], bt[1], bt[2], nb,
+            ntypes, best_indiv, sm);
+  h->tiled = t;
+  h->ktiled = k;
+  h->t_blocks = nb;
+  h->t_smem = sm;
+  return FCM_OK;
 }
 
 extern "C" int fcm_mg_setup(const fcm_grid* g, const fcm_params* prm, const double* K_ref,
@@ -996,6 +1192,8 @@ extern "C" int fcm_mg_setup(const fcm_grid* g, const fcm_params* prm, const doub
   }
   for (int q = 1; q <= g->p; ++q)
     if (q >= 2 || prm->coarse == FCM_COARSE_AS_PCG) RC(setup_schwarz(h.get(), q, kind, cut_idx));
+  RC(h->alloc(&h->d_coarse_iters, 2));
+  CU(cudaMemsetAsync(h->d_coarse_iters, 0, 8, h->stream));
   // coarse level
   const int64_t n1 = L.ndof_level[1];
   if (prm->coarse == FCM_COARSE_DIRECT) {
@@ -1043,9 +1241,8 @@ extern "C" int fcm_mg_setup(const fcm_grid* g, const fcm_params* prm, const doub
       int v = atoi(env);
       if (v > 0) h->coarse_blocks = std::min<int64_t>(v, (int64_t)h->num_sms * per_sm);
     }
+    RC(setup_tiled(h.get()));
   }
-  RC(h->alloc(&h->d_coarse_iters, 2));
-  CU(cudaMemsetAsync(h->d_coarse_iters, 0, 8, h->stream));
   // FCG buffers
   const int64_t N = L.ndof_level[g->p];
   RC(h->alloc(&h->f_b, N)); RC(h->alloc(&h->f_x, N)); RC(h->alloc(&h->f_r, N));
@@ -1151,6 +1348,20 @@ extern "C" int fcm_mg_coarse_solve(fcm_mg* h, const double* r, double* x, int32_
       CU(cudaMemcpyAsync(h->h_iters, h->d_coarse_iters, 4, cudaMemcpyDeviceToHost, h->stream));
       CU(cudaStreamSynchronize(h->stream));
       *iters = *h->h_iters;
+      if (h->ktiled && h->tiled.prof) {   // FCM_TILED_PROF: mean phase times per iteration
+        std::vector<unsigned long long> pr((size_t)4 * h->t_blocks);
+        CU(cudaMemcpy(pr.data(), h->tiled.prof, pr.size() * 8, cudaMemcpyDeviceToHost));
+        double mx[4] = {0, 0, 0, 0}, mean[4] = {0, 0, 0, 0};
+        for (int b = 0; b < h->t_blocks; ++b)
+          for (int k = 0; k < 4; ++k) {
+            mx[k] = std::max(mx[k], (double)pr[4 * b + k]);
+            mean[k] += (double)pr[4 * b + k] / h->t_blocks;
+          }
+        fprintf(stderr, "[fcm] tiled phases (ns, summed over solves; mean/max over blocks): update %.0f/%.0f "
+                "smooth %.0f/%.0f apply %.0f/%.0f allreduce %.0f/%.0f\n", mean[0], mx[0], mean[1], mx[1],
+                mean[2], mx[2], mean[3], mx[3]);
+        CU(cudaMemset(h->tiled.prof, 0, pr.size() * 8));
+      }
     }
   }
   return FCM_OK;

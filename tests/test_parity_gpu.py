@@ -206,3 +206,21 @@ def test_empty_level_rejected():
     with pytest.raises(FcmError) as e:
         Solver.from_problem(cfg, G)
     assert e.value.code == -1
+
+
+@pytest.mark.parametrize("tiled", ["1", "0"])
+@pytest.mark.parametrize("case", ["3d_p2", "3d_trunk_elast", "3d_p2_jacobi"])
+def test_coarse_kernels_both_paths(case, tiled, monkeypatch):
+    # the shared-memory tiled coarse PCG (small coarse levels) and the grid-wide kernel (large
+    # ones) against the oracle's coarse CG, on the same level; iterations +-1 (reading R16)
+    monkeypatch.setenv("FCM_COARSE_TILED", tiled)
+    pair = Pair(CASES[case]())
+    H = pair.hier()
+    I1 = pair.P.dof.level_dofs(1)
+    r = np.zeros(pair.P.dof.ndof)
+    r[I1] = pair.P.b[I1]
+    ref = np.zeros_like(r)
+    ref[I1] = H.coarse_solve(r[I1])
+    x, it = pair.S.coarse_solve(pair.to_gpu(r, 1))
+    assert rel(pair.from_gpu(x, 1), ref) <= 1e-10
+    assert abs(it - H.coarse_iters[-1]) <= 1
