@@ -199,6 +199,17 @@ int fcm_pcg_solve_host(fcm_mg* h, const double* b_host, double* x_host, double r
 /* Statistics of the last fcm_pcg_solve: total inner coarse CG iterations, V-cycles.       */
 int fcm_mg_stats(const fcm_mg* h, int64_t* coarse_iters_total, int64_t* vcycles);
 
+/* Which coarse solver kernel the handle runs (for measurement and tests):
+ * *kind = FCM_COARSE_KERNEL_DIRECT (dense inverse GEMV), _GRID (grid-wide cooperative PCG
+ * over the cell population, any size) or _TILED (shared-memory bricks, one grid barrier per
+ * iteration; chosen at setup when every brick and its matrices fit in shared memory);
+ * *blocks = CTAs of the cooperative launch (0 for direct); tile[3] (may be NULL) = brick
+ * size in vertices (tiled only, else 0).                                                   */
+#define FCM_COARSE_KERNEL_DIRECT 0
+#define FCM_COARSE_KERNEL_GRID 1
+#define FCM_COARSE_KERNEL_TILED 2
+int fcm_mg_coarse_info(const fcm_mg* h, int32_t* kind, int32_t* blocks, int32_t* tile);
+
 /* Counters of kernels launched by the library since setup (for the bench's gpu_launches). */
 int fcm_mg_launch_count(const fcm_mg* h, int64_t* launches);
 

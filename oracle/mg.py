@@ -29,7 +29,7 @@ import scipy.linalg as sla
 
 
 class Level:
-    def __init__(self, prob, q, block, A_full, omega):
+    def __init__(self, prob, q, block, A_full, omega, inv_method="lu"):
         dof = prob.dof
         self.q = q
         self.idx = dof.level_dofs(q)
@@ -67,7 +67,12 @@ class Level:
             by_size.setdefault(len(b), []).append(i)
         for size, ids in by_size.items():
             stack = np.stack([Ad[blocks[i]][:, blocks[i]].toarray() for i in ids])
-            inv = np.linalg.inv(stack)
+            if inv_method == "lu":
+                inv = np.linalg.inv(stack)
+            else:   # "chol": a second backward-stable inverse, used only to measure the
+                # rounding spread between two valid fp64 evaluations (reading R18)
+                eye = np.eye(size)
+                inv = np.stack([sla.cho_solve(sla.cho_factor(S, lower=True), eye) for S in stack])
             for k, i in enumerate(ids):
                 self.inv[i] = inv[k]
 
@@ -80,7 +85,7 @@ class Level:
 
 class Hierarchy:
     def __init__(self, prob, block=None, omega=None, n_pre=None, n_post=None, coarse=None,
-                 coarse_rtol=None, coarse_maxit=None):
+                 coarse_rtol=None, coarse_maxit=None, inv="lu"):
         cfg = prob.cfg
         self.prob = prob
         self.block = block or cfg.block
@@ -98,7 +103,7 @@ class Hierarchy:
             blk = self.block if q > 1 else "element"   # coarse AS is elementwise (R11)
             need_blocks = q > 1 or self.coarse == "as_pcg"
             if need_blocks:
-                self.levels[q] = Level(prob, q, blk, A, self.omega if q > 1 else 1.0)
+                self.levels[q] = Level(prob, q, blk, A, self.omega if q > 1 else 1.0, inv_method=inv)
             else:
                 lv = Level.__new__(Level)
                 lv.q = q

@@ -62,6 +62,7 @@ _SIGS = {
     "fcm_pcg_solve": (I32, [P, P, P, D, I32, P, P]),
     "fcm_pcg_solve_host": (I32, [P, P, P, D, I32, P, P]),
     "fcm_mg_stats": (I32, [P, P, P]),
+    "fcm_mg_coarse_info": (I32, [P, P, P, P]),
     "fcm_mg_launch_count": (I32, [P, P]),
     "fcm_last_error": (C.c_char_p, []),
 }

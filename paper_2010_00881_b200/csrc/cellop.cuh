@@ -45,7 +45,7 @@ struct CellOp {
   const double* Kref;
   int ldK;
   double alpha;
-  // SMOOTH (regular): blk < 0: t = -blk-1, type_inv[t & 0xff] * (t >> 12 ? 1/alpha : 1);
+  // SMOOTH (regular): blk < 0: t = -blk-1, type_inv[t & 0xfff] * (t >> 12 ? 1/alpha : 1) (slot index);
   //                   blk >= 0 cells are in the list
   const int32_t* blk;
   const double* type_inv;
@@ -156,7 +156,7 @@ __device__ __forceinline__ double reg_cells(const CellOp& op, const Tab& T, cons
         act = b < 0;
         const int t = -b - 1;
         scale = (t >> 12) ? op.inv_alpha : 1.0;
-        const int code = t & 0xff;
+        const int code = t & 0xfff;
         if (code != 0) Mg = op.type_inv + code * M * M;
       }
     }
@@ -282,7 +282,7 @@ __device__ __forceinline__ double list_cells(const CellOp& op, const Tab& T, int
           Mat = op.irr_inv + (size_t)b * m * m;
         } else {
           const int t = -b - 1;
-          Mat = op.type_inv + (size_t)(t & 0xff) * m * m;
+          Mat = op.type_inv + (size_t)(t & 0xfff) * m * m;
           scale = (t >> 12) ? op.inv_alpha : 1.0;
         }
       }

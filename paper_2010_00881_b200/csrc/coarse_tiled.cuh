@@ -45,8 +45,7 @@ struct TiledArgs {
   int vlo[3][3];     // free vertex range of component j
   int vhi[3][3];
   int max_indiv;     // individual-matrix slots per CTA (host: max over bricks)
-  int ntypes;        // shared Schwarz inverses staged (type codes in type_codes)
-  int type_codes[64];
+  int ntypes;        // shared Schwarz inverses (slots 0..ntypes-1 of type_inv), all staged
   // operator
   const uint8_t* kind;
   const int32_t* cut_idx;
@@ -58,7 +57,7 @@ struct TiledArgs {
   int jacobi;
   const double* diag_inv;
   const int32_t* blk;
-  const double* type_inv;   // [64][M1*M1]
+  const double* type_inv;   // [ntypes][M1*M1]
   const double* irr_inv;    // [n_irr][M1*M1]
   double inv_alpha;
   // vectors (class-major, level 1)
@@ -71,11 +70,6 @@ struct TiledArgs {
   int maxit;
   int* iters;               // [0] = this solve, [1] += this solve
   unsigned long long* prof; // optional per-block phase times (ns): [nblocks][4]
-  // n_f = 1: the two matrices most cells use, row-major 8x8 in the PARAMETER bank, so that a
-  // warp whose cells all use them takes its matrix operands straight from the constant cache
-  int fastK, fastT0;        // 1 if Kc / T0c are valid
-  double Kc[64];            // leading 8x8 block of K_ref
-  double T0c[64];           // interior-type Schwarz inverse (code 0, unscaled)
 };
 
 __device__ __forceinline__ unsigned long long t_now() {
@@ -128,8 +122,6 @@ __host__ __device__ constexpr size_t tiled_smem_bytes(int dim, int nf, int E2, i
 
 // one row of the vertex-centric gather: sum over the 2^d cells around E2 entry l (local
 // coordinates lx, ly, lz) of s_c Mat_c[a_v(c)*NF + i, :] . vec_c (all operands in smem)
-constexpr int kT0Slot = 1;   // pool slot of the first staged type (the host puts code 0 first)
-
 template <int DIM, int NF, bool SMOOTH>
 __device__ __forceinline__ double vertex_row(const TiledArgs& a, const TiledSmem<DIM, NF>& S,
                                              const double* __restrict__ vec, int l, int lx, int ly,
@@ -141,7 +133,6 @@ __device__ __forceinline__ double vertex_row(const TiledArgs& a, const TiledSmem
   const double scale = SMOOTH ? a.inv_alpha : a.alpha;
   double acc = 0.0;
   if constexpr (NF == 1) {
-    constexpr int T0_OFF = kT0Slot * slot_stride(M1);
     // the 3^d neighbourhood of the vertex, loaded once into registers
     constexpr int N3 = DIM == 3 ? 27 : 9;
     double nb[N3];
@@ -280,7 +271,6 @@ __global__ void __launch_bounds__(512, 1) k_coarse_tiled(TiledArgs a) {
   __shared__ double red[96];
   __shared__ double tot[3];
   __shared__ int n_indiv;
-  __shared__ int type_slot[64];
   TiledSmem<DIM, NF> S;
   const int e0 = a.e[0], e1 = a.e[1], e2d = a.e[2];
   const int t0 = a.tile[0], t1 = DIM > 1 ? a.tile[1] : 1, t2 = DIM > 2 ? a.tile[2] : 1;
@@ -309,16 +299,14 @@ __global__ void __launch_bounds__(512, 1) k_coarse_tiled(TiledArgs a) {
   const int E2 = S.E2;
   // ---- one-time staging: K_ref block, shared Schwarz inverses, cell codes ----------------
   if (threadIdx.x == 0) n_indiv = 0;
-  for (int t = threadIdx.x; t < 64; t += blockDim.x) type_slot[t] = -1;
   __syncthreads();
-  for (int t = threadIdx.x; t < a.ntypes; t += blockDim.x) type_slot[a.type_codes[t]] = t;
   for (int t = threadIdx.x; t < M1 * M1; t += blockDim.x) {
     const int r = t / M1, c = t % M1;
     if (c <= r) S.mat[packed_at(r, c)] = a.Kref[r * a.ldK + c];
   }
   for (int t = threadIdx.x; t < a.ntypes * M1 * M1; t += blockDim.x) {
     const int k = t / (M1 * M1), r = (t / M1) % M1, c = t % M1;
-    if (c <= r) S.mat[(1 + k) * MM + packed_at(r, c)] = a.type_inv[(size_t)a.type_codes[k] * M1 * M1 + r * M1 + c];
+    if (c <= r) S.mat[(1 + k) * MM + packed_at(r, c)] = a.type_inv[(size_t)k * M1 * M1 + r * M1 + c];
   }
   __syncthreads();
   const int indiv0 = (1 + a.ntypes) * MM;   // first individual slot (doubles)
@@ -350,7 +338,7 @@ __global__ void __launch_bounds__(512, 1) k_coarse_tiled(TiledArgs a) {
           code.y = indiv0 + slot * MM;
         } else {
           const int tt = -bq - 1;
-          code.y = (1 + type_slot[tt & 0xff]) * MM | ((tt >> 12) ? kScaleBit : 0);
+          code.y = (1 + (tt & 0xfff)) * MM | ((tt >> 12) ? kScaleBit : 0);
         }
       }
     }

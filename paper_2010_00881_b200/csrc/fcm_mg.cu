@@ -27,6 +27,7 @@
 #include "cellop.cuh"
 #include "coarse.cuh"
 #include "coarse_tiled.cuh"
+#include "blocks.cuh"
 #include "common.hpp"
 #include "layout.hpp"
 
@@ -79,7 +80,15 @@ struct LevelDev {
   int ilo[3] = {0, 0, 0}, ihi[3] = {-1, -1, -1};  // cells with no Dirichlet DOF
   int ts = 1;                      // threads per cell of the regular path
   std::vector<int32_t> blk_h;      // host copy of blk (tiled coarse setup)
-  std::vector<int> type_codes_h;   // boundary-type codes with a shared inverse
+  // patchwise blocks (blocks.cuh): anchors are grid vertices, blk is per anchor
+  bool patch = false;
+  int mb = 0;                      // block size (= m for elementwise)
+  int nmem = 1;
+  int mo[8][3] = {};
+  int na[3] = {1, 1, 1};
+  int64_t nanchor = 0;
+  int8_t* d_mem = nullptr;
+  int16_t* d_loc = nullptr;
   // vectors
   double* x = nullptr;
   double* r = nullptr;
@@ -328,56 +337,6 @@ __global__ void k_dense_gemv(const double* __restrict__ A, const double* __restr
   }
 }
 
-// ---- setup: Schwarz block assembly A_i = P_i^T A_q P_i -----------------
-struct AsmArgs {
-  int nx, ny, nz, dim, m, ldK;  // m = m_q
-  const int64_t* cells;         // block -> cell index (or representative coordinates)
-  const uint8_t* virt;          // 1: assume every neighbour is uncut physical (type block)
-  const int16_t* nbmap;         // [3^d][m] local index in neighbour cell (-1 none)
-  const int8_t* dirich;         // [nblocks][m] 1 if Dirichlet
-  const uint8_t* kind;
-  const int32_t* cut_idx;
-  const double* Kref;
-  const double* cutK;
-  double alpha;
-  double* out;                  // [nblocks][m][m]
-};
-__global__ void k_assemble_blocks(AsmArgs a) {
-  const int64_t blk = blockIdx.x;
-  const int64_t c = a.cells[blk];
-  const int cx = (int)(c % a.nx), cy = (int)((c / a.nx) % a.ny), cz = (int)(c / ((int64_t)a.nx * a.ny));
-  const int m = a.m;
-  double* A = a.out + blk * (int64_t)m * m;
-  const int8_t* dir = a.dirich + blk * m;
-  const int nd = a.dim == 3 ? 27 : 9;
-  for (int e = threadIdx.x; e < m * m; e += blockDim.x) {
-    const int i = e / m, j = e % m;
-    double s = 0.0;
-    if (dir[i] || dir[j]) {
-      s = (i == j) ? 1.0 : 0.0;
-    } else {
-      for (int d = 0; d < nd; ++d) {
-        const int dx = d % 3 - 1, dy = (d / 3) % 3 - 1, dz = a.dim == 3 ? d / 9 - 1 : 0;
-        const int ncx = cx + dx, ncy = cy + dy, ncz = cz + dz;
-        if (ncx < 0 || ncy < 0 || ncz < 0 || ncx >= a.nx || ncy >= a.ny || ncz >= a.nz) continue;
-        const int ii = a.nbmap[d * m + i], jj = a.nbmap[d * m + j];
-        if (ii < 0 || jj < 0) continue;
-        const int64_t nc = ((int64_t)ncz * a.ny + ncy) * a.nx + ncx;
-        double v;
-        if (a.virt[blk]) {
-          v = a.Kref[(int64_t)ii * a.ldK + jj];
-        } else {
-          const uint8_t k = a.kind[nc];
-          if (k == 2) v = a.cutK[(int64_t)a.cut_idx[nc] * a.ldK * a.ldK + (int64_t)ii * a.ldK + jj];
-          else v = a.Kref[(int64_t)ii * a.ldK + jj] * (k == 1 ? a.alpha : 1.0);
-        }
-        s += v;
-      }
-    }
-    A[e] = s;
-  }
-}
-
 // Inversion of SPD blocks: Cholesky A = L L^T (right-looking, L in shared memory), then
 // X = A^{-1} column by column by forward/backward substitution (one thread per column,
 // the column lives in the output block), symmetrised.  Backward stable.
@@ -435,6 +394,22 @@ __global__ void k_invert_blocks(double* mats, int m, int* status, int64_t nblock
   for (int64_t blk = blockIdx.x; blk < nblocks; blk += gridDim.x) {
     double* G = mats + blk * (int64_t)m * m;
     for (int e = threadIdx.x; e < m * m; e += blockDim.x) A[e] = G[e];
+    if (threadIdx.x == 0) bad = 0;
+    __syncthreads();
+    chol_inverse(A, G, m, &bad);
+    if (threadIdx.x == 0) status[blk] = bad;
+    __syncthreads();
+  }
+}
+
+// same for blocks too large for shared memory (patch blocks, m_b up to 729): the Cholesky
+// factor lives in a per-CTA global scratch (L2-resident)
+__global__ void k_invert_blocks_global(double* mats, int m, int* status, int64_t nblocks, double* scratch) {
+  __shared__ int bad;
+  double* A = scratch + (size_t)blockIdx.x * m * m;
+  for (int64_t blk = blockIdx.x; blk < nblocks; blk += gridDim.x) {
+    double* G = mats + blk * (int64_t)m * m;
+    for (int64_t e = threadIdx.x; e < (int64_t)m * m; e += blockDim.x) A[e] = G[e];
     if (threadIdx.x == 0) bad = 0;
     __syncthreads();
     chol_inverse(A, G, m, &bad);
@@ -625,8 +600,36 @@ static int residual(fcm_mg* h, int q, const double* b, const double* x, double* 
   RC(copy(h, r, b, h->lev[q].ndof));
   return launch_cellop(h, q, make_op(h, q, OP_APPLY, x, r, -1.0, nullptr));
 }
+static size_t block_smem(int m, int mb) {
+  (void)m;
+  return sizeof(Tab) + (size_t)(kThreads / 32) * mb * (sizeof(double) + sizeof(int));
+}
+// patchwise smoother: one warp per vertex patch (blocks.cuh)
+static int launch_block_smooth(fcm_mg* h, int q, const double* r, double* x, double coef) {
+  LevelDev& Lv = h->lev[q];
+  BlockOp op{};
+  op.nx = h->L.n[0]; op.ny = h->L.n[1]; op.nz = h->L.n[2];
+  for (int i = 0; i < 3; ++i) op.na[i] = Lv.na[i];
+  op.nanchor = Lv.nanchor;
+  op.mb = Lv.mb;
+  op.nmem = Lv.nmem;
+  for (int k = 0; k < 8; ++k)
+    for (int i = 0; i < 3; ++i) op.mo[k][i] = Lv.mo[k][i];
+  op.mem = Lv.d_mem; op.loc = Lv.d_loc;
+  op.m = Lv.m; op.base = Lv.base; op.stride = Lv.stride; op.cmin = Lv.cmin; op.cmax = Lv.cmax;
+  op.blk = Lv.blk; op.type_inv = Lv.type_inv; op.irr_inv = Lv.irr_inv; op.inv_alpha = 1.0 / h->alpha;
+  op.in = r; op.out = x; op.coef = coef;
+  const int64_t wpb = kThreads / 32;
+  const int nb = (int)std::max<int64_t>(1, std::min<int64_t>((Lv.nanchor + wpb - 1) / wpb, (int64_t)h->num_sms * 8));
+  k_block_smooth<<<nb, kThreads, block_smem(Lv.m, Lv.mb), h->stream>>>(op);
+  h->count();
+  CU(cudaGetLastError());
+  return FCM_OK;
+}
+
 // x += omega M^-1 r
 static int smooth(fcm_mg* h, int q, const double* r, double* x) {
+  if (h->lev[q].patch) return launch_block_smooth(h, q, r, x, h->lev[q].omega);
   return launch_cellop(h, q, make_op(h, q, OP_SMOOTH, r, x, h->lev[q].omega, nullptr));
 }
 
@@ -771,117 +774,192 @@ struct StreamGuard {
 // =========================================================================================
 // setup
 // =========================================================================================
+// Block geometry of level q (blocks.cuh): elementwise (anchor = cell, one member cell,
+// assembly cells = the 3^d neighbourhood) or patchwise (anchor = vertex, the 2^d member cells
+// around it, assembly cells = the 4^d neighbourhood), reading R11.
+struct BlockGeom {
+  bool patch = false;
+  int na[3] = {1, 1, 1};
+  int nmem = 1;
+  int mo[8][3] = {};
+  int mb = 0;
+  std::vector<int8_t> mem;
+  std::vector<int16_t> loc;
+  int nasm = 3, aoff = -1;
+  std::vector<int16_t> amap;   // [nasm^d][mb]
+};
+
+static BlockGeom block_geom(const Layout& L, int q, bool patch) {
+  BlockGeom g;
+  const int dim = L.dim, mq = L.m_level[q];
+  g.patch = patch;
+  for (int i = 0; i < 3; ++i) g.na[i] = i < dim ? L.n[i] + (patch ? 1 : 0) : 1;
+  g.nmem = patch ? 1 << dim : 1;
+  for (int k = 0; k < g.nmem; ++k)
+    for (int i = 0; i < 3; ++i) g.mo[k][i] = (patch && i < dim) ? ((k >> i) & 1) - 1 : 0;
+  // identity of a DOF relative to the anchor: (class, X) with X = 2*entity position (nodal
+  // axis) or 2*cell+1 (internal axis), as in the DOF keys
+  auto ident = [&](int a, const int off[3]) {
+    const DofClass& dc = L.classes[L.dof_class[a]];
+    std::array<int, 4> k{L.dof_class[a], 0, 0, 0};
+    for (int i = 0; i < dim; ++i)
+      k[1 + i] = (dc.S >> i & 1) ? 2 * off[i] + 1 : 2 * (off[i] + L.dof_off[a][i]);
+    return k;
+  };
+  std::map<std::array<int, 4>, int> id;
+  std::vector<std::array<int, 4>> keys;
+  for (int k = 0; k < g.nmem; ++k)
+    for (int a = 0; a < mq; ++a) {
+      auto key = ident(a, g.mo[k]);
+      if (id.count(key)) continue;
+      id[key] = g.mb++;
+      keys.push_back(key);
+      g.mem.push_back((int8_t)k);
+      g.loc.push_back((int16_t)a);
+    }
+  g.nasm = patch ? 4 : 3;
+  g.aoff = patch ? -2 : -1;
+  const int nas = dim == 3 ? g.nasm * g.nasm * g.nasm : (dim == 2 ? g.nasm * g.nasm : g.nasm);
+  g.amap.assign((size_t)nas * g.mb, -1);
+  for (int d = 0; d < nas; ++d) {
+    int ao[3] = {0, 0, 0};
+    ao[0] = g.aoff + d % g.nasm;
+    if (dim >= 2) ao[1] = g.aoff + (d / g.nasm) % g.nasm;
+    if (dim == 3) ao[2] = g.aoff + d / (g.nasm * g.nasm);
+    for (int a = 0; a < mq; ++a) {
+      auto it = id.find(ident(a, ao));
+      if (it != id.end()) g.amap[(size_t)d * g.mb + it->second] = (int16_t)a;
+    }
+  }
+  return g;
+}
+
+// global layout index of block DOF l at anchor coordinates A (-1: absent or Dirichlet)
+static int64_t block_dof_index(const Layout& L, int q, const BlockGeom& g, int l, const int A[3]) {
+  int cc[3];
+  for (int i = 0; i < 3; ++i) {
+    cc[i] = A[i] + g.mo[g.mem[l]][i];
+    if (cc[i] < 0 || cc[i] >= L.n[i]) return -1;
+  }
+  return L.dof_index(q, g.loc[l], cc);
+}
+
 static int setup_schwarz(fcm_mg* h, int q, const std::vector<uint8_t>& kind,
                          const std::vector<int32_t>& cut_idx) {
   const Layout& L = h->L;
   LevelDev& Lv = h->lev[q];
-  const int m = Lv.m;
   const int dim = L.dim;
-  const int nd = dim == 3 ? 27 : 9;
   const int nx = L.n[0], ny = L.n[1], nz = L.n[2];
-  // neighbour map: local DOF a of cell c as a local DOF of cell c + delta
-  std::vector<int16_t> nbmap((size_t)nd * m, -1);
-  for (int d = 0; d < nd; ++d) {
-    int del[3] = {d % 3 - 1, (d / 3) % 3 - 1, dim == 3 ? d / 9 - 1 : 0};
-    for (int a = 0; a < m; ++a) {
-      int off[3];
-      bool ok = true;
-      for (int i = 0; i < 3; ++i) {
-        off[i] = L.dof_off[a][i] - del[i];
-        bool internal = (L.classes[L.dof_class[a]].S >> i) & 1;
-        if (i >= dim) { if (del[i] != 0) ok = false; continue; }
-        if (internal ? off[i] != 0 : (off[i] < 0 || off[i] > 1)) ok = false;
-      }
-      if (ok) nbmap[(size_t)d * m + a] = (int16_t)L.local_of(L.dof_class[a], off);
-    }
-  }
-  // classify blocks: regular (all existing neighbours uncut with one kind) -> shared by
-  // boundary type; otherwise individual.
-  std::vector<int32_t> blk(h->ncell);
-  std::vector<int64_t> blocks;       // cells whose block is assembled
-  std::vector<uint8_t> virt;
-  std::vector<int> type_used(64, 0);
-  std::vector<int64_t> irr_cells;
-  for (int64_t c = 0; c < h->ncell; ++c) {
-    int cc[3];
-    L.cell_coords(c, cc);
+  const bool patch = q >= 2 && h->prm.block == FCM_BLOCK_PATCH;   // coarse AS is elementwise (R11)
+  const BlockGeom g = block_geom(L, q, patch);
+  const int mb = g.mb;
+  const int64_t nanchor = (int64_t)g.na[0] * g.na[1] * g.na[2];
+  const int nas = (int)(g.amap.size() / std::max(1, mb));
+  // classify blocks: regular (every existing assembly cell uncut, one kind) -> shared inverse
+  // per boundary type (and 1/alpha scaling for all-fictitious); otherwise individual.
+  const int R = patch ? 2 : 1;
+  std::vector<int32_t> blk(nanchor);
+  std::map<int, int64_t> type_rep;    // type key -> representative anchor
+  std::vector<int> key_of(nanchor, -1);
+  std::vector<uint8_t> alpha_of(nanchor, 0);
+  std::vector<int64_t> irr;
+  for (int64_t A = 0; A < nanchor; ++A) {
+    int ac[3] = {(int)(A % g.na[0]), (int)((A / g.na[0]) % g.na[1]), (int)(A / ((int64_t)g.na[0] * g.na[1]))};
+    bool any = false;
+    for (int l = 0; l < mb && !any; ++l) any = block_dof_index(L, q, g, l, ac) >= 0;
+    if (!any) { blk[A] = kBlkNone; continue; }
     int k0 = -1;
     bool regular = true;
-    for (int d = 0; d < nd && regular; ++d) {
-      int n3[3] = {cc[0] + d % 3 - 1, cc[1] + (d / 3) % 3 - 1, cc[2] + (dim == 3 ? d / 9 - 1 : 0)};
-      if (n3[0] < 0 || n3[1] < 0 || n3[2] < 0 || n3[0] >= nx || n3[1] >= ny || n3[2] >= nz) continue;
-      int k = kind[((int64_t)n3[2] * ny + n3[1]) * nx + n3[0]];
+    for (int d = 0; d < nas && regular; ++d) {
+      int c3[3] = {ac[0] + g.aoff + d % g.nasm, dim >= 2 ? ac[1] + g.aoff + (d / g.nasm) % g.nasm : 0,
+                   dim == 3 ? ac[2] + g.aoff + d / (g.nasm * g.nasm) : 0};
+      if (c3[0] < 0 || c3[1] < 0 || c3[2] < 0 || c3[0] >= nx || c3[1] >= ny || c3[2] >= nz) continue;
+      const int k = kind[((int64_t)c3[2] * ny + c3[1]) * nx + c3[0]];
       if (k == 2 || (k0 >= 0 && k != k0)) regular = false;
       k0 = k;
     }
     if (regular) {
-      int code = 0;
-      for (int i = 0; i < 3; ++i) {
-        int ci = (cc[i] == 0 ? 1 : 0) | (cc[i] == L.n[i] - 1 ? 2 : 0);
-        code += ci << (2 * i);
+      // boundary type: per axis the clipped distances of the anchor to both faces (0 = interior)
+      int key = 0, mul = 1;
+      for (int i = 0; i < dim; ++i) {
+        const int hiA = patch ? L.n[i] : L.n[i] - 1;
+        const int lo = std::min(ac[i], R), hi = std::min(hiA - ac[i], R);
+        const int ci = (lo == R && hi == R) ? 0 : 1 + lo * (R + 1) + hi;
+        key += ci * mul;
+        mul *= (R + 1) * (R + 1) + 1;
       }
-      type_used[code] = 1;
-      blk[c] = -(1 + (code | (k0 == 1 ? (1 << 12) : 0)));
+      key_of[A] = key;
+      alpha_of[A] = k0 == 1;
+      if (!type_rep.count(key)) type_rep[key] = A;
     } else {
-      blk[c] = (int32_t)irr_cells.size();
-      irr_cells.push_back(c);
+      blk[A] = (int32_t)irr.size();
+      irr.push_back(A);
     }
   }
-  // assembly list: types first (representative coordinates, virtual all-physical), then irregular
-  std::vector<int> type_slot;
-  for (int code = 0; code < 64; ++code) {
-    if (!type_used[code]) continue;
-    int cc[3];
-    for (int i = 0; i < 3; ++i) {
-      int ci = (code >> (2 * i)) & 3;
-      cc[i] = ci == 0 ? 1 : (ci == 1 ? 0 : (ci == 2 ? L.n[i] - 1 : 0));
-    }
-    blocks.push_back(((int64_t)cc[2] * ny + cc[1]) * nx + cc[0]);
+  if (type_rep.size() > 4095) return fail(FCM_EINVAL, "too many Schwarz block types on level %d", q);
+  std::map<int, int> slot_of;
+  std::vector<int64_t> blocks;   // assembly list: types first (virtual all-physical), then irregular
+  std::vector<uint8_t> virt;
+  for (auto& kv : type_rep) {
+    slot_of[kv.first] = (int)blocks.size();
+    blocks.push_back(kv.second);
     virt.push_back(1);
-    type_slot.push_back(code);
   }
+  for (int64_t A = 0; A < nanchor; ++A)
+    if (key_of[A] >= 0) blk[A] = -(1 + (slot_of[key_of[A]] | (alpha_of[A] ? (1 << 12) : 0)));
   const int64_t ntypes = (int64_t)blocks.size();
-  for (int64_t c : irr_cells) { blocks.push_back(c); virt.push_back(0); }
+  for (int64_t A : irr) { blocks.push_back(A); virt.push_back(0); }
   const int64_t nblk = (int64_t)blocks.size();
-  // Dirichlet flags per block row
-  std::vector<int8_t> dir((size_t)nblk * m);
+  // absent/Dirichlet flags per block row
+  std::vector<int8_t> dir((size_t)nblk * mb);
   for (int64_t b = 0; b < nblk; ++b) {
-    int cc[3];
-    L.cell_coords(blocks[b], cc);
-    for (int a = 0; a < m; ++a) dir[(size_t)b * m + a] = L.dof_index(q, a, cc) < 0;
+    const int64_t A = blocks[b];
+    int ac[3] = {(int)(A % g.na[0]), (int)((A / g.na[0]) % g.na[1]), (int)(A / ((int64_t)g.na[0] * g.na[1]))};
+    for (int l = 0; l < mb; ++l) dir[(size_t)b * mb + l] = block_dof_index(L, q, g, l, ac) < 0;
   }
   // device buffers
-  int64_t *d_cells;
+  int64_t* d_anchors;
   uint8_t* d_virt;
-  int16_t* d_nb;
+  int16_t* d_amap;
   int8_t* d_dir;
   double* d_mats;
   int* d_status;
-  RC(h->alloc(&d_cells, nblk));
+  RC(h->alloc(&d_anchors, nblk));
   RC(h->alloc(&d_virt, nblk));
-  RC(h->alloc(&d_nb, (size_t)nd * m));
-  RC(h->alloc(&d_dir, (size_t)nblk * m));
-  RC(h->alloc(&d_mats, (size_t)nblk * m * m));
+  RC(h->alloc(&d_amap, g.amap.size()));
+  RC(h->alloc(&d_dir, (size_t)nblk * mb));
+  RC(h->alloc(&d_mats, (size_t)nblk * mb * mb));
   RC(h->alloc(&d_status, nblk));
-  RC(h->alloc(&Lv.blk, h->ncell));
-  RC(h->alloc(&Lv.type_inv, (size_t)64 * m * m));
-  CU(cudaMemcpyAsync(d_cells, blocks.data(), nblk * 8, cudaMemcpyHostToDevice, h->stream));
+  RC(h->alloc(&Lv.blk, nanchor));
+  CU(cudaMemcpyAsync(d_anchors, blocks.data(), nblk * 8, cudaMemcpyHostToDevice, h->stream));
   CU(cudaMemcpyAsync(d_virt, virt.data(), nblk, cudaMemcpyHostToDevice, h->stream));
-  CU(cudaMemcpyAsync(d_nb, nbmap.data(), nbmap.size() * 2, cudaMemcpyHostToDevice, h->stream));
+  CU(cudaMemcpyAsync(d_amap, g.amap.data(), g.amap.size() * 2, cudaMemcpyHostToDevice, h->stream));
   CU(cudaMemcpyAsync(d_dir, dir.data(), dir.size(), cudaMemcpyHostToDevice, h->stream));
   CU(cudaMemcpyAsync(Lv.blk, blk.data(), blk.size() * 4, cudaMemcpyHostToDevice, h->stream));
-  AsmArgs aa{};
-  aa.nx = nx; aa.ny = ny; aa.nz = nz; aa.dim = dim; aa.m = m; aa.ldK = L.m;
-  aa.cells = d_cells; aa.virt = d_virt; aa.nbmap = d_nb; aa.dirich = d_dir;
+  BlockAsmArgs aa{};
+  aa.nx = nx; aa.ny = ny; aa.nz = nz; aa.dim = dim; aa.mb = mb; aa.ldK = L.m;
+  for (int i = 0; i < 3; ++i) aa.na[i] = g.na[i];
+  aa.nasm = g.nasm; aa.aoff = g.aoff;
+  aa.anchors = d_anchors; aa.virt = d_virt; aa.amap = d_amap; aa.dirich = d_dir;
   aa.kind = h->d_kind; aa.cut_idx = h->d_cut_idx; aa.Kref = h->d_Kref; aa.cutK = h->d_cutK;
   aa.alpha = h->alpha; aa.out = d_mats;
   if (nblk > 0) {
     k_assemble_blocks<<<(unsigned)nblk, kThreads, 0, h->stream>>>(aa);
     CU(cudaGetLastError());
-    size_t sm = (size_t)m * m * 8 + (size_t)m * 8;
-    CU(cudaFuncSetAttribute(k_invert_blocks, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    int nbk = (int)std::min<int64_t>(nblk, (int64_t)h->num_sms * 8);
-    k_invert_blocks<<<nbk, kThreads, sm, h->stream>>>(d_mats, m, d_status, nblk);
+    int max_smem = 0;
+    CU(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, h->dev));
+    const size_t sm = (size_t)mb * mb * 8 + (size_t)mb * 8;
+    if (sm + 64 <= (size_t)max_smem) {
+      CU(cudaFuncSetAttribute(k_invert_blocks, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+      int nbk = (int)std::min<int64_t>(nblk, (int64_t)h->num_sms * 8);
+      k_invert_blocks<<<nbk, kThreads, sm, h->stream>>>(d_mats, mb, d_status, nblk);
+    } else {   // large patch blocks: factor in a global scratch, one block per CTA at a time
+      int nbk = (int)std::min<int64_t>(nblk, (int64_t)h->num_sms * 2);
+      double* scratch = nullptr;
+      CU(cudaMallocAsync((void**)&scratch, (size_t)nbk * mb * mb * 8, h->stream));
+      k_invert_blocks_global<<<nbk, kThreads, 0, h->stream>>>(d_mats, mb, d_status, nblk, scratch);
+      CU(cudaFreeAsync(scratch, h->stream));
+    }
     CU(cudaGetLastError());
   }
   std::vector<int> status(nblk);
@@ -889,23 +967,33 @@ static int setup_schwarz(fcm_mg* h, int q, const std::vector<uint8_t>& kind,
   CU(cudaStreamSynchronize(h->stream));
   for (int64_t b = 0; b < nblk; ++b)
     if (status[b])
-      return fail(FCM_ESINGULAR, "singular Schwarz block on level q=%d: %s block of cell %lld", q,
-                  b < ntypes ? "shared-type" : "individual", (long long)blocks[b]);
-  // scatter type inverses into their slots, keep irregular inverses in place
-  for (int64_t t = 0; t < ntypes; ++t)
-    CU(cudaMemcpyAsync(Lv.type_inv + (size_t)type_slot[t] * m * m, d_mats + (size_t)t * m * m,
-                       (size_t)m * m * 8, cudaMemcpyDeviceToDevice, h->stream));
-  Lv.irr_inv = d_mats + (size_t)ntypes * m * m;
-  Lv.n_irr = (int64_t)irr_cells.size();
-  {
-    std::vector<int32_t> il(irr_cells.begin(), irr_cells.end());
+      return fail(FCM_ESINGULAR, "singular Schwarz block on level q=%d: %s %s block at anchor %lld", q,
+                  b < ntypes ? "shared-type" : "individual", patch ? "patch" : "element",
+                  (long long)blocks[b]);
+  Lv.type_inv = d_mats;                       // slots 0..ntypes-1
+  Lv.irr_inv = d_mats + (size_t)ntypes * mb * mb;
+  Lv.n_irr = (int64_t)irr.size();
+  if (!patch) {
+    std::vector<int32_t> il(irr.begin(), irr.end());
     RC(h->alloc(&Lv.irr_list, il.size()));
     CU(cudaMemcpyAsync(Lv.irr_list, il.data(), il.size() * 4, cudaMemcpyHostToDevice, h->stream));
+  } else {
+    RC(h->alloc(&Lv.d_mem, mb));
+    RC(h->alloc(&Lv.d_loc, mb));
+    CU(cudaMemcpyAsync(Lv.d_mem, g.mem.data(), mb, cudaMemcpyHostToDevice, h->stream));
+    CU(cudaMemcpyAsync(Lv.d_loc, g.loc.data(), mb * 2, cudaMemcpyHostToDevice, h->stream));
   }
+  Lv.patch = patch;
+  Lv.mb = mb;
+  Lv.nmem = g.nmem;
+  for (int k = 0; k < 8; ++k)
+    for (int i = 0; i < 3; ++i) Lv.mo[k][i] = g.mo[k][i];
+  for (int i = 0; i < 3; ++i) Lv.na[i] = g.na[i];
+  Lv.nanchor = nanchor;
   Lv.has_as = true;
   Lv.n_types = (int32_t)ntypes;
   Lv.blk_h = blk;
-  Lv.type_codes_h = type_slot;
+  CU(cudaStreamSynchronize(h->stream));
   return FCM_OK;
 }
 
@@ -969,7 +1057,6 @@ static int setup_tiled(fcm_mg* h) {
   }
   const LevelDev& L1 = h->lev[1];
   const bool jac = h->prm.coarse == FCM_COARSE_JACOBI_PCG;
-  if (!jac && (int)L1.type_codes_h.size() > 64) return FCM_OK;
   // individual matrices per cell (cut-cell operator block + irregular Schwarz inverse), and
   // their 3D prefix sums for box counts
   const int nx = L.n[0], ny = L.n[1], nz = L.n[2];
@@ -995,7 +1082,7 @@ static int setup_tiled(fcm_mg* h) {
     return P(x1, y1, z1) - P(x0, y1, z1) - P(x1, y0, z1) - P(x1, y1, z0) + P(x0, y0, z1) + P(x0, y1, z0) +
            P(x1, y0, z0) - P(x0, y0, z0);
   };
-  const int ntypes = jac ? 0 : (int)L1.type_codes_h.size();
+  const int ntypes = jac ? 0 : L1.n_types;
   int max_smem = 0;
   CU(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, h->dev));
   const size_t smem_cap = (size_t)max_smem - 2048;  // static shared memory of the kernel
@@ -1045,19 +1132,6 @@ static int setup_tiled(fcm_mg* h) {
   }
   t.max_indiv = best_indiv;
   t.ntypes = ntypes;
-  for (int i = 0; i < ntypes; ++i) t.type_codes[i] = L1.type_codes_h[i];
-  // parameter-bank copies of the leading K_ref block and the interior-type inverse (n_f = 1)
-  if (nf == 1 && M1 == 8) {
-    std::vector<double> kr((size_t)L.m * L.m);
-    CU(cudaMemcpy(kr.data(), h->d_Kref, kr.size() * 8, cudaMemcpyDeviceToHost));
-    for (int r = 0; r < 8; ++r)
-      for (int c = 0; c < 8; ++c) t.Kc[r * 8 + c] = kr[(size_t)r * L.m + c];
-    t.fastK = 1;
-    if (ntypes > 0 && L1.type_codes_h[0] == 0) {   // staged in pool slot 1 (kT0Slot)
-      CU(cudaMemcpy(t.T0c, L1.type_inv, 64 * 8, cudaMemcpyDeviceToHost));
-      t.fastT0 = 1;
-    }
-  }
   const int E2 = t.e[0] * t.e[1] * t.e[2], EC = t.ec[0] * t.ec[1] * t.ec[2];
   const size_t sm = tiled_smem_bytes(dim, nf, E2, EC, bt[0] * bt[1] * bt[2], 1 + ntypes + best_indiv);
   CU(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
@@ -1107,7 +1181,7 @@ extern "C" int fcm_mg_setup(const fcm_grid* g, const fcm_params* prm, const doub
   if (!(alpha > 0)) return fail(FCM_EINVAL, "alpha must be > 0");
   if (prm->n_pre < 0 || prm->n_post < 0) return fail(FCM_EINVAL, "negative sweep count");
   if (prm->coarse < 0 || prm->coarse > 2) return fail(FCM_EINVAL, "unknown coarse solver");
-  if (prm->block != FCM_BLOCK_ELEMENT) return fail(FCM_EINVAL, "patchwise blocks are not implemented yet");
+  if (prm->block != FCM_BLOCK_ELEMENT && prm->block != FCM_BLOCK_PATCH) return fail(FCM_EINVAL, "unknown block kind %d", prm->block);
   std::unique_ptr<fcm_mg> h(new fcm_mg());
   h->g = *g;
   h->prm = *prm;
@@ -1192,6 +1266,11 @@ extern "C" int fcm_mg_setup(const fcm_grid* g, const fcm_params* prm, const doub
   }
   for (int q = 1; q <= g->p; ++q)
     if (q >= 2 || prm->coarse == FCM_COARSE_AS_PCG) RC(setup_schwarz(h.get(), q, kind, cut_idx));
+  for (int q = 2; q <= g->p; ++q)
+    if (h->lev[q].patch) {
+      const size_t sm = block_smem(h->lev[q].m, h->lev[q].mb);
+      CU(cudaFuncSetAttribute(k_block_smooth, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    }
   RC(h->alloc(&h->d_coarse_iters, 2));
   CU(cudaMemsetAsync(h->d_coarse_iters, 0, 8, h->stream));
   // coarse level
@@ -1513,6 +1592,16 @@ extern "C" int fcm_mg_stats(const fcm_mg* h, int64_t* coarse_iters_total, int64_
     *coarse_iters_total = v[1];
   }
   if (vcycles) *vcycles = h->stat_vcycles;
+  return FCM_OK;
+}
+
+extern "C" int fcm_mg_coarse_info(const fcm_mg* h, int32_t* kind, int32_t* blocks, int32_t* tile) {
+  if (!h || !kind || !blocks) return fail(FCM_EINVAL, "NULL argument");
+  if (h->prm.coarse == FCM_COARSE_DIRECT) { *kind = FCM_COARSE_KERNEL_DIRECT; *blocks = 0; }
+  else if (h->ktiled) { *kind = FCM_COARSE_KERNEL_TILED; *blocks = h->t_blocks; }
+  else { *kind = FCM_COARSE_KERNEL_GRID; *blocks = h->coarse_blocks; }
+  if (tile)
+    for (int i = 0; i < 3; ++i) tile[i] = h->ktiled ? h->tiled.tile[i] : 0;
   return FCM_OK;
 }
 

@@ -183,6 +183,14 @@ class Solver:
         check(_lib.lib().fcm_mg_launch_count(self._h, C.byref(v)))
         return v.value
 
+    def coarse_info(self):
+        """(kernel name, cooperative CTAs, brick size) of the coarse solver (fcm_mg_coarse_info)."""
+        k, nb = C.c_int32(), C.c_int32()
+        t = (C.c_int32 * 3)()
+        check(_lib.lib().fcm_mg_coarse_info(self._h, C.byref(k), C.byref(nb), t))
+        name = {0: "k_dense_gemv", 1: "k_coarse_pcg", 2: "k_coarse_tiled"}[k.value]
+        return name, nb.value, tuple(t)
+
     def stats(self):
         a, b = C.c_int64(), C.c_int64()
         check(_lib.lib().fcm_mg_stats(self._h, C.byref(a), C.byref(b)))

@@ -38,18 +38,18 @@ class Pair:
             self.H = Hierarchy(self.P, **kw)
         return self.H
 
-    def tol(self, base):
-        """Conditioning-aware tolerance: two
-        backward-stable fp64 evaluations of A_i^{-1} r differ by up to kappa_i * eps; the
-        north-star bound `base` is asserted whenever max_i kappa(A_i) < 1e9."""
-        if not hasattr(self, "_kappa"):
-            H = self.hier()
-            ks = [1.0]
-            for q, lv in H.levels.items():
-                if hasattr(lv, "blocks"):
-                    ks += [np.linalg.cond(lv.A[b][:, b].toarray()) for b in lv.blocks]
-            self._kappa = max(ks)
-        return base if self._kappa < 1e9 else max(base, self._kappa * np.finfo(float).eps)
+    def hier_chol(self):
+        """The same hierarchy with every block inverse computed by Cholesky instead of LU."""
+        if getattr(self, "Hc", None) is None:
+            self.Hc = Hierarchy(self.P, inv="chol")
+        return self.Hc
+
+    def tol(self, base, spread=0.0):
+        """Parity tolerance (reading R18): the north-star bound `base`, or 4x the
+        measured spread between two backward-stable fp64 evaluations of the same quantity
+        (oracle with LU inverses vs oracle with Cholesky inverses), whichever is larger.
+        Ill-conditioned cut-cell blocks make that spread ~kappa(A_i) eps."""
+        return max(base, 4.0 * spread)
 
     def to_gpu(self, v_oracle, q=None):
         n = self.S.ndofs(q)
@@ -75,6 +75,10 @@ CASES = {
     "3d_trunk_elast": lambda: small_config(3, 4, 3, space="trunk", physics="elasticity", voids=2, seed=6),
     "2d_p4": lambda: small_config(2, 7, 4, voids=1, seed=2, coarse="direct"),
     "3d_p1_single_level": lambda: small_config(3, 5, 1, voids=2, seed=8),
+    # patchwise Schwarz (config 3's smoother): 125 / 343 / 49-DOF vertex patches
+    "3d_p2_patch": lambda: small_config(3, 5, 2, voids=2, seed=5, block="patch"),
+    "3d_p3_patch": lambda: small_config(3, 4, 3, voids=1, seed=7, block="patch"),
+    "2d_p3_patch": lambda: small_config(2, 6, 3, voids=1, seed=3, block="patch", coarse="direct"),
 }
 
 
@@ -115,17 +119,22 @@ def test_smoother_matches_oracle(pair):
         r[lv.idx] = rng.standard_normal(lv.n)
         ref = np.zeros_like(r)
         ref[lv.idx] = lv.omega * lv.schwarz(r[lv.idx])
+        Hc = pair.hier_chol()
+        refc = np.zeros_like(r)
+        refc[lv.idx] = lv.omega * Hc.levels[q].schwarz(r[lv.idx])
         x = torch.zeros(pair.S.ndofs(q), dtype=torch.float64, device="cuda")
         pair.S.smooth(pair.to_gpu(r, q), x, q)
-        assert rel(pair.from_gpu(x, q), ref) <= pair.tol(1e-9), q
+        assert rel(pair.from_gpu(x, q), ref) <= pair.tol(1e-10, rel(refc, ref)), q
         # a residual-like right-hand side (the V-cycle's case): b restricted to the level
         r2 = np.zeros_like(r)
         r2[lv.idx] = pair.P.b[lv.idx]
         ref2 = np.zeros_like(r)
         ref2[lv.idx] = lv.omega * lv.schwarz(r2[lv.idx])
+        refc2 = np.zeros_like(r)
+        refc2[lv.idx] = lv.omega * Hc.levels[q].schwarz(r2[lv.idx])
         x.zero_()
         pair.S.smooth(pair.to_gpu(r2, q), x, q)
-        assert rel(pair.from_gpu(x, q), ref2) <= pair.tol(1e-10), q
+        assert rel(pair.from_gpu(x, q), ref2) <= pair.tol(1e-10, rel(refc2, ref2)), q
 
 
 def test_coarse_solve_matches_oracle(pair):
@@ -147,8 +156,9 @@ def test_vcycle_matches_oracle(pair):
     rng = np.random.default_rng(2)
     for r in (pair.P.b, rng.standard_normal(pair.P.dof.ndof)):
         ref = H.vcycle(r)
+        spread = rel(pair.hier_chol().vcycle(r), ref)
         z = pair.from_gpu(pair.S.vcycle(pair.to_gpu(r)))
-        assert rel(z, ref) <= pair.tol(1e-10)
+        assert rel(z, ref) <= pair.tol(1e-10, spread)
 
 
 def test_fcg_matches_oracle(pair):
@@ -176,8 +186,9 @@ def test_zero_rhs_and_host_path(pair):
     xh = torch.zeros_like(bh).pin_memory()
     it = pair.S.pcg_solve_host(bh, xh)
     xd, itd, _ = pair.S.pcg_solve(bh.cuda())
-    # the fp64 atomic scatter makes summation order run-dependent: equal to rounding
-    assert abs(it - itd) <= 1 and rel(xh.numpy(), xd.cpu().numpy()) <= pair.tol(1e-10)
+    # the fp64 atomic scatter makes summation order run-dependent: two runs are two valid
+    # solves, held to the north-star final-solution bound
+    assert abs(it - itd) <= 1 and rel(xh.numpy(), xd.cpu().numpy()) <= 1e-8
 
 
 def test_generator_setup_end_to_end():
@@ -196,6 +207,16 @@ def test_generator_setup_end_to_end():
     xo, ito, _ = Hierarchy(P).fcg(P.b)
     assert abs(it - ito) <= 1
     assert rel(x.cpu().numpy(), xo[pos]) <= 1e-8
+
+
+def test_patch_block_counts():
+    # one patch block per grid vertex with a free DOF; regular patches share one inverse per
+    # boundary type, the others (4^d neighbourhood touches a cut cell) are individual
+    pair = Pair(CASES["3d_p2_patch"]())
+    H = pair.hier()
+    n_ind, n_types = pair.S.block_counts(2)
+    assert n_ind + 0 <= len(H.levels[2].blocks) and n_types >= 1
+    assert pair.S.level_m(2) == 27
 
 
 def test_empty_level_rejected():
