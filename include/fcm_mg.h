@@ -148,6 +148,56 @@ int fcm_mg_setup(const fcm_grid* g, const fcm_params* prm, const double* K_ref,
 
 int fcm_mg_destroy(fcm_mg* h);
 
+/* ==== multi-GPU: slab decomposition ================
+ * The cell grid is cut into contiguous layers along the LAST axis (z in 3D, y in 2D); rank r
+ * of N (one GPU each) owns cell layers [z_begin, z_end).  Its local vectors hold the DOFs of
+ * its own cells in the class-major layout of the slab (both interface vertex planes
+ * included, duplicated on the two neighbours); an interface DOF is owned by the LOWER rank
+ * for dot products.  Every operator / smoother scatter is followed by a sum-exchange of the
+ * interface planes over NCCL (grouped send/recv; a + b == b + a keeps both copies bit-
+ * identical); dots are reduced with ncclAllReduce.  Schwarz blocks of cells next to an
+ * interface are assembled with one ghost cell layer.  The coarse p = 1 problem is solved
+ * REPLICATED: the owned coarse residuals are all-gathered and every rank runs the coarse
+ * solver on the full p = 1 grid (no per-iteration communication in the inner CG).
+ * NCCL is loaded at run time (dlopen of libnccl.so.2, the one torch already loaded).      */
+
+/* Balanced partition of n cell layers over nranks (host only).                              */
+int fcm_slab_bounds(int32_t n, int32_t nranks, int32_t rank, int32_t* z_begin, int32_t* z_end);
+
+/* Host-only description of the local layout of slab [z_begin, z_end) of the GLOBAL grid g at
+ * level q: *ndofs local DOFs; keys (ndofs, may be NULL) their global DOF keys; owned (ndofs
+ * bytes, may be NULL) 1 where this rank owns the DOF; the interface plane slots at the bottom
+ * (*n_lo, lo_slots; empty when z_begin == 0) and top (*n_hi, hi_slots; empty when z_end == n)
+ * in exchange order (the neighbour's matching plane lists the same DOFs in the same order).
+ * Call with NULL arrays to get the sizes.                                                    */
+int fcm_slab_layout(const fcm_grid* g, int32_t z_begin, int32_t z_end, int32_t q, int64_t* ndofs,
+                    int64_t* keys, uint8_t* owned, int64_t* n_lo, int32_t* lo_slots,
+                    int64_t* n_hi, int32_t* hi_slots);
+
+/* Global level-1 slot of every local level-1 slot of the slab (host only).                  */
+int fcm_slab_coarse_map(const fcm_grid* g, int32_t z_begin, int32_t z_end, int64_t* n_local,
+                        int64_t* global_slots);
+
+/* 128-byte NCCL unique id (call on rank 0 and broadcast the bytes to the other ranks).      */
+int fcm_nccl_unique_id(void* id128);
+
+typedef struct fcm_slab {
+  int32_t rank, nranks;     /* this rank (uses the current CUDA device), number of ranks      */
+  int32_t z_begin, z_end;   /* owned cell layers (fcm_slab_bounds)                            */
+  const void* nccl_id;      /* 128 bytes from fcm_nccl_unique_id (ignored when nranks == 1)   */
+} fcm_slab;
+
+/* Slab version of fcm_mg_setup.  g is the GLOBAL grid; cell_kind the GLOBAL cell kinds;
+ * cut_cells / cut_K the cut cells (global indices, ascending) of the owned layers AND of the
+ * ghost layers z_begin-1 and z_end (when they exist); coarse_cut_cells / coarse_cut_K1 EVERY
+ * cut cell of the grid with the leading m_1 x m_1 block of its matrix (replicated coarse
+ * level).  Collective: every rank calls it with the same g, prm and nccl_id.               */
+int fcm_mg_setup_slab(const fcm_grid* g, const fcm_params* prm, const fcm_slab* slab,
+                      const double* K_ref, const uint8_t* cell_kind, double alpha,
+                      int64_t n_cut, const int64_t* cut_cells, const double* cut_K,
+                      int64_t n_coarse_cut, const int64_t* coarse_cut_cells,
+                      const double* coarse_cut_K1, fcm_mg** out);
+
 /* Number of levels (= p) and free DOFs of level q (1..p) (local DOFs of this rank).        */
 int fcm_mg_nlevels(const fcm_mg* h, int32_t* nlevels);
 int fcm_mg_ndofs(const fcm_mg* h, int32_t q, int64_t* n);

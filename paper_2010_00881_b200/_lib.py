@@ -32,6 +32,11 @@ class Params(C.Structure):
                 ("coarse_maxit", C.c_int32), ("stream", C.c_void_p)]
 
 
+class Slab(C.Structure):
+    _fields_ = [("rank", C.c_int32), ("nranks", C.c_int32), ("z_begin", C.c_int32), ("z_end", C.c_int32),
+                ("nccl_id", C.c_void_p)]
+
+
 class Physics(C.Structure):
     _fields_ = [("kind", C.c_int32), ("alpha", C.c_double), ("E", C.c_double), ("nu", C.c_double),
                 ("depth", C.c_int32), ("traction_face", C.c_int32)]
@@ -63,6 +68,11 @@ _SIGS = {
     "fcm_pcg_solve_host": (I32, [P, P, P, D, I32, P, P]),
     "fcm_mg_stats": (I32, [P, P, P]),
     "fcm_mg_coarse_info": (I32, [P, P, P, P]),
+    "fcm_slab_bounds": (I32, [I32, I32, I32, P, P]),
+    "fcm_slab_layout": (I32, [P, I32, I32, I32, P, P, P, P, P, P, P]),
+    "fcm_slab_coarse_map": (I32, [P, I32, I32, P, P]),
+    "fcm_nccl_unique_id": (I32, [P]),
+    "fcm_mg_setup_slab": (I32, [P, P, P, P, P, D, I64, P, P, I64, P, P, P]),
     "fcm_mg_launch_count": (I32, [P, P]),
     "fcm_last_error": (C.c_char_p, []),
 }

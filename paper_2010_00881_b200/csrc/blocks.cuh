@@ -16,7 +16,8 @@ namespace fcm {
 constexpr int kBlkNone = INT32_MIN;   // anchor whose block has no free DOF (skipped)
 
 struct BlockAsmArgs {
-  int nx, ny, nz, dim;
+  int nx, ny, nz, dim;          // owned cell grid (anchor coordinates are relative to it)
+  int lo[3], ne[3];             // cell arrays (kind, cut_idx) cover [lo, lo + ne) per axis
   int mb;                       // block size
   int ldK;                      // element matrix leading dimension (fine m)
   int na[3];                    // anchor grid extents
@@ -54,8 +55,10 @@ __global__ void k_assemble_blocks(BlockAsmArgs a) {
         const int cx = ax + a.aoff + d % a.nasm;
         const int cy = a.dim >= 2 ? ay + a.aoff + (d / a.nasm) % a.nasm : 0;
         const int cz = a.dim == 3 ? az + a.aoff + d / (a.nasm * a.nasm) : 0;
-        if (cx < 0 || cy < 0 || cz < 0 || cx >= a.nx || cy >= a.ny || cz >= a.nz) continue;
-        const int64_t c = ((int64_t)cz * a.ny + cy) * a.nx + cx;
+        if (cx < a.lo[0] || cy < a.lo[1] || cz < a.lo[2] || cx >= a.lo[0] + a.ne[0] ||
+            cy >= a.lo[1] + a.ne[1] || cz >= a.lo[2] + a.ne[2])
+          continue;
+        const int64_t c = ((int64_t)(cz - a.lo[2]) * a.ne[1] + (cy - a.lo[1])) * a.ne[0] + (cx - a.lo[0]);
         double v;
         if (a.virt[blk]) {
           v = a.Kref[(int64_t)ii * a.ldK + jj];

@@ -30,6 +30,8 @@
 #include "blocks.cuh"
 #include "common.hpp"
 #include "layout.hpp"
+#include "nccl_dl.hpp"
+#include "slab.hpp"
 
 namespace cg = cooperative_groups;
 using namespace fcm;
@@ -56,6 +58,8 @@ constexpr int kMaxPartials = 2048;
 struct Scalars {
   double rz, pq, rr, zr, zr_old, bb;
   int flag;  // bit0: p^T A p <= 0
+  int pad;
+  double red[4];  // slab mode: all-reduced partial sums (pq | zr, zr_old | rz)
 };
 
 struct LevelDev {
@@ -89,6 +93,11 @@ struct LevelDev {
   int64_t nanchor = 0;
   int8_t* d_mem = nullptr;
   int16_t* d_loc = nullptr;
+  // slab mode: interface planes (exchange order) and the smoother increment vector
+  int32_t* lo_idx = nullptr;
+  int32_t* hi_idx = nullptr;
+  int64_t n_lo = 0, n_hi = 0;
+  double* d = nullptr;
   // vectors
   double* x = nullptr;
   double* r = nullptr;
@@ -108,8 +117,10 @@ struct fcm_mg {
   int dev = 0, num_sms = 148;
   double alpha = 1e-8;
   int64_t ncell = 0, ncut = 0;
-  uint8_t* d_kind = nullptr;
+  uint8_t* d_kind = nullptr;        // owned cells (= d_kind_ext + owned offset)
   int32_t* d_cut_idx = nullptr;
+  uint8_t* d_kind_ext = nullptr;    // owned + ghost cell layers (Schwarz assembly)
+  int32_t* d_cut_idx_ext = nullptr;
   int32_t* d_cut_list = nullptr;  // cut cells in cut order
   const void* kcoarse = nullptr;
   double* d_Kref = nullptr;
@@ -143,6 +154,24 @@ struct fcm_mg {
   int64_t* count_target = nullptr;  // during capture: where launches are counted
   int64_t stat_coarse = 0, stat_vcycles = 0;
   std::vector<void*> allocs;
+  // slab decomposition (slab.hpp; nranks == 1: single GPU, no collective)
+  int rank = 0, nranks = 1, z0 = 0, z1 = 0;
+  int ext_lo = 0, ext_n = 0;        // ghost-extended cell layers along the slab axis (relative)
+  int64_t cut_first = 0;            // first owned cut cell in the cut-matrix array
+  ncclComm_t comm = nullptr;
+  double* x_send = nullptr;         // [2][max plane] bottom / top
+  double* x_recv = nullptr;
+  uint8_t* d_own = nullptr;         // owner mask of the fine level (dots)
+  fcm_mg* hg = nullptr;             // replicated global p = 1 problem (coarse solve)
+  bool borrowed_stream = false;
+  int32_t* c_pack = nullptr;        // owned local level-1 slots (allgather order)
+  int64_t c_count = 0, c_max = 0;
+  double* c_send = nullptr;
+  double* c_recv = nullptr;         // [nranks][c_max]
+  int64_t* c_unpack = nullptr;      // [nranks * c_max] global level-1 slot (-1 padding)
+  int64_t* c_extract = nullptr;     // [ndof_1 local] global level-1 slot
+  double* c_bg = nullptr;
+  double* c_xg = nullptr;
 
   template <typename T>
   int alloc(T** p, size_t n) {
@@ -157,7 +186,8 @@ struct fcm_mg {
     if (count_target) *count_target += k;
     else launches += k;
   }
-  ~fcm_mg() {
+  ~fcm_mg();
+  void release() {
     for (auto g : {g_vc, g_it1, g_it2, g_init})
       if (g) cudaGraphExecDestroy(g);
     for (void* p : allocs) cudaFree(p);
@@ -165,12 +195,17 @@ struct fcm_mg {
     if (h_iters) cudaFreeHost(h_iters);
     if (ev_in) cudaEventDestroy(ev_in);
     if (ev_out) cudaEventDestroy(ev_out);
-    if (stream) cudaStreamDestroy(stream);
+    if (stream && !borrowed_stream) cudaStreamDestroy(stream);
     if (stream2) cudaStreamDestroy(stream2);
     if (ev_fork) cudaEventDestroy(ev_fork);
     if (ev_join) cudaEventDestroy(ev_join);
   }
 };
+fcm_mg::~fcm_mg() {
+  if (hg) delete hg;
+  if (comm && nccl().ok) nccl().CommDestroy(comm);
+  release();
+}
 
 // =========================================================================================
 // kernels
@@ -217,6 +252,37 @@ __global__ void __launch_bounds__(kThreads) k_cell_list(CellOp op, int part_off)
   }
 }
 
+// slab mode: interface planes (index lists in exchange order)
+__global__ void k_zero_idx(double* __restrict__ v, const int32_t* __restrict__ idx, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    v[idx[i]] = 0.0;
+}
+__global__ void k_pack2(double* __restrict__ buf, const double* __restrict__ v, const int32_t* __restrict__ lo,
+                        int64_t nlo, const int32_t* __restrict__ hi, int64_t nhi, int64_t stride) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nlo + nhi; i += (int64_t)gridDim.x * blockDim.x)
+    buf[i < nlo ? i : stride + i - nlo] = v[i < nlo ? lo[i] : hi[i - nlo]];
+}
+// v[plane] = v[plane] + received neighbour partial (a + b == b + a on both ranks)
+__global__ void k_unpack_add2(double* __restrict__ v, const double* __restrict__ buf, const int32_t* __restrict__ lo,
+                              int64_t nlo, const int32_t* __restrict__ hi, int64_t nhi, int64_t stride) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nlo + nhi; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t j = i < nlo ? lo[i] : hi[i - nlo];
+    v[j] = v[j] + buf[i < nlo ? i : stride + i - nlo];
+  }
+}
+__global__ void k_gather32(double* __restrict__ out, const double* __restrict__ in, const int32_t* __restrict__ idx, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = in[idx[i]];
+}
+__global__ void k_gather64(double* __restrict__ out, const double* __restrict__ in, const int64_t* __restrict__ idx, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = in[idx[i]];
+}
+__global__ void k_scatter64(double* __restrict__ out, const double* __restrict__ in, const int64_t* __restrict__ idx, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    if (idx[i] >= 0) out[idx[i]] = in[i];
+}
+
 __global__ void k_fill(double* x, double v, int64_t n) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     x[i] = v;
@@ -230,11 +296,12 @@ __global__ void k_axpy(double* __restrict__ y, double a, const double* __restric
     y[i] = fma(a, x[i], y[i]);
 }
 // partials[block] = sum a.b over the block's grid-stride range (fixed grid -> deterministic)
-__global__ void k_dot(const double* __restrict__ a, const double* __restrict__ b, int64_t n, double* partials) {
+__global__ void k_dot(const double* __restrict__ a, const double* __restrict__ b, int64_t n, double* partials,
+                      const uint8_t* __restrict__ own = nullptr) {
   __shared__ double red[32];
   double s = 0.0;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-    s = fma(a[i], b[i], s);
+    if (!own || own[i]) s = fma(a[i], b[i], s);
   s = block_sum(s, red);
   if (threadIdx.x == 0) partials[blockIdx.x] = s;
 }
@@ -260,9 +327,10 @@ __global__ void k_fcg_start(double* x, double* r, const double* b, int64_t n) {
     r[i] = b[i];
   }
 }
-// rz = sum partials(z.r); p = z
-__global__ void k_fcg_start2(Scalars* s, const double* part, int np, double* p, const double* z, int64_t n) {
-  const double v = sum_partials(part, np);
+// rz = sum partials(z.r) (or the all-reduced value); p = z
+__global__ void k_fcg_start2(Scalars* s, const double* part, int np, double* p, const double* z, int64_t n,
+                             const double* pre = nullptr) {
+  const double v = pre ? *pre : sum_partials(part, np);
   if (blockIdx.x == 0 && threadIdx.x == 0) s->rz = v;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     p[i] = z[i];
@@ -271,9 +339,10 @@ __global__ void k_fcg_start2(Scalars* s, const double* part, int np, double* p, 
 __global__ void k_fcg_update1(Scalars* s, const double* part_pq, int npq, double* __restrict__ x,
                               double* __restrict__ r, double* __restrict__ r_old,
                               const double* __restrict__ p, const double* __restrict__ q, int64_t n,
-                              double* part_rr) {
+                              double* part_rr, const uint8_t* __restrict__ own = nullptr,
+                              const double* pre = nullptr) {
   __shared__ double red[32];
-  const double pq = sum_partials(part_pq, npq);
+  const double pq = pre ? *pre : sum_partials(part_pq, npq);
   const double alpha = s->rz / pq;
   double rr = 0.0;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
@@ -282,7 +351,7 @@ __global__ void k_fcg_update1(Scalars* s, const double* part_pq, int npq, double
     r_old[i] = ri;
     const double rn = fma(-alpha, q[i], ri);
     r[i] = rn;
-    rr = fma(rn, rn, rr);
+    if (!own || own[i]) rr = fma(rn, rn, rr);
   }
   rr = block_sum(rr, red);
   if (threadIdx.x == 0) part_rr[blockIdx.x] = rr;
@@ -295,12 +364,19 @@ __global__ void k_finalize(double* out, const double* part, int np) {
   const double v = sum_partials(part, np);
   if (threadIdx.x == 0) *out = v;
 }
+__global__ void k_finalize2(double* out, const double* partA, const double* partB, int np) {
+  const double a = sum_partials(partA, np);
+  const double b = sum_partials(partB, np);
+  if (threadIdx.x == 0) { out[0] = a; out[1] = b; }
+}
 // partials of z.r and z.r_old (two sets)
 __global__ void k_dot2(const double* __restrict__ z, const double* __restrict__ r,
-                       const double* __restrict__ ro, int64_t n, double* partA, double* partB) {
+                       const double* __restrict__ ro, int64_t n, double* partA, double* partB,
+                       const uint8_t* __restrict__ own = nullptr) {
   __shared__ double red[32];
   double s1 = 0.0, s2 = 0.0;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    if (own && !own[i]) continue;
     const double zi = z[i];
     s1 = fma(zi, r[i], s1);
     s2 = fma(zi, ro[i], s2);
@@ -311,9 +387,10 @@ __global__ void k_dot2(const double* __restrict__ z, const double* __restrict__ 
 }
 // beta = (z.r - z.r_old) / rz_old ; rz = z.r ; p = z + beta p   (Polak-Ribiere, reading R5)
 __global__ void k_fcg_update2(Scalars* s, const double* partA, const double* partB, int np,
-                              double* __restrict__ p, const double* __restrict__ z, int64_t n) {
-  const double zr = sum_partials(partA, np);
-  const double zro = sum_partials(partB, np);
+                              double* __restrict__ p, const double* __restrict__ z, int64_t n,
+                              const double* pre = nullptr) {
+  const double zr = pre ? pre[0] : sum_partials(partA, np);
+  const double zro = pre ? pre[1] : sum_partials(partB, np);
   const double beta = (zr - zro) / s->rz;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     p[i] = fma(beta, p[i], z[i]);
@@ -515,7 +592,8 @@ static CellOp make_op(fcm_mg* h, int q, int mode, const double* in, double* out,
   op.blk = Lv.blk; op.irr_inv = Lv.irr_inv; op.type_inv = Lv.type_inv; op.inv_alpha = 1.0 / h->alpha;
   if (Lv.M > 0) {
     if (mode == OP_APPLY) {
-      op.list = h->d_cut_list; op.nlist = (int32_t)h->ncut; op.list_mats = h->d_cutK; op.list_ld = h->L.m;
+      op.list = h->d_cut_list; op.nlist = (int32_t)h->ncut;
+      op.list_mats = h->d_cutK + (size_t)h->cut_first * h->L.m * h->L.m; op.list_ld = h->L.m;
     } else {
       op.list = Lv.irr_list; op.nlist = (int32_t)Lv.n_irr; op.list_mats = Lv.irr_inv; op.list_ld = Lv.m;
     }
@@ -595,10 +673,63 @@ static int copy(fcm_mg* h, double* y, const double* x, int64_t n) {
   return FCM_OK;
 }
 
-// r = b - A_q x
+#define NC(call)                                                                        \
+  do {                                                                                  \
+    ncclResult_t r_ = (call);                                                           \
+    if (r_ != ncclSuccess) return fail(FCM_ENCCL, "%s: %s", #call, nccl().GetErrorString(r_)); \
+  } while (0)
+
+// slab mode: sum the two copies of every interface plane of level q: pack the
+// bottom / top planes, grouped send/recv with the neighbours, add what came back.
+static int exchange(fcm_mg* h, int q, double* v) {
+  if (h->nranks <= 1) return FCM_OK;
+  LevelDev& Lv = h->lev[q];
+  const int64_t nlo = Lv.n_lo, nhi = Lv.n_hi, stride = h->lev[h->g.p].n_lo + h->lev[h->g.p].n_hi;
+  if (nlo + nhi == 0) return FCM_OK;
+  const int gb = grid_for(nlo + nhi, h->num_sms);
+  k_pack2<<<gb, kThreads, 0, h->stream>>>(h->x_send, v, Lv.lo_idx, nlo, Lv.hi_idx, nhi, stride);
+  h->count();
+  CU(cudaGetLastError());
+  NC(nccl().GroupStart());
+  if (nlo > 0) {   // bottom plane <-> rank - 1 (its top plane)
+    NC(nccl().Send(h->x_send, nlo, ncclFloat64, h->rank - 1, h->comm, h->stream));
+    NC(nccl().Recv(h->x_recv, nlo, ncclFloat64, h->rank - 1, h->comm, h->stream));
+  }
+  if (nhi > 0) {   // top plane <-> rank + 1 (its bottom plane)
+    NC(nccl().Send(h->x_send + stride, nhi, ncclFloat64, h->rank + 1, h->comm, h->stream));
+    NC(nccl().Recv(h->x_recv + stride, nhi, ncclFloat64, h->rank + 1, h->comm, h->stream));
+  }
+  NC(nccl().GroupEnd());
+  k_unpack_add2<<<gb, kThreads, 0, h->stream>>>(v, h->x_recv, Lv.lo_idx, nlo, Lv.hi_idx, nhi, stride);
+  h->count();
+  CU(cudaGetLastError());
+  return FCM_OK;
+}
+
+// all-reduce (sum) of n device doubles in place (slab mode)
+static int allreduce(fcm_mg* h, double* v, int n) {
+  if (h->nranks <= 1) return FCM_OK;
+  NC(nccl().AllReduce(v, v, n, ncclFloat64, ncclSum, h->comm, h->stream));
+  return FCM_OK;
+}
+
+// r = b - A_q x.  Slab mode: the lower rank owns an interface DOF, so only it starts from b
+// there; the exchange then adds the two partial sums of A x (same result on both ranks).
 static int residual(fcm_mg* h, int q, const double* b, const double* x, double* r) {
-  RC(copy(h, r, b, h->lev[q].ndof));
-  return launch_cellop(h, q, make_op(h, q, OP_APPLY, x, r, -1.0, nullptr));
+  LevelDev& Lv = h->lev[q];
+  RC(copy(h, r, b, Lv.ndof));
+  if (Lv.n_lo > 0) {
+    k_zero_idx<<<grid_for(Lv.n_lo, h->num_sms), kThreads, 0, h->stream>>>(r, Lv.lo_idx, Lv.n_lo);
+    h->count();
+  }
+  RC(launch_cellop(h, q, make_op(h, q, OP_APPLY, x, r, -1.0, nullptr)));
+  return exchange(h, q, r);
+}
+// y = A_q x (y overwritten)
+static int apply_op(fcm_mg* h, int q, const double* x, double* y, double* partials) {
+  RC(fill(h, y, 0.0, h->lev[q].ndof));
+  RC(launch_cellop(h, q, make_op(h, q, OP_APPLY, x, y, 1.0, partials)));
+  return exchange(h, q, y);
 }
 static size_t block_smem(int m, int mb) {
   (void)m;
@@ -627,13 +758,56 @@ static int launch_block_smooth(fcm_mg* h, int q, const double* r, double* x, dou
   return FCM_OK;
 }
 
-// x += omega M^-1 r
-static int smooth(fcm_mg* h, int q, const double* r, double* x) {
+static int smooth_into(fcm_mg* h, int q, const double* r, double* x) {
   if (h->lev[q].patch) return launch_block_smooth(h, q, r, x, h->lev[q].omega);
   return launch_cellop(h, q, make_op(h, q, OP_SMOOTH, r, x, h->lev[q].omega, nullptr));
 }
+// x += omega M^-1 r.  Slab mode: the increment is exchanged (x itself is consistent), so it
+// goes through d unless x is known to be zero.
+static int smooth(fcm_mg* h, int q, const double* r, double* x, bool x_is_zero = false) {
+  if (h->nranks <= 1) return smooth_into(h, q, r, x);
+  LevelDev& Lv = h->lev[q];
+  if (x_is_zero) {
+    RC(smooth_into(h, q, r, x));
+    return exchange(h, q, x);
+  }
+  RC(fill(h, Lv.d, 0.0, Lv.ndof));
+  RC(smooth_into(h, q, r, Lv.d));
+  RC(exchange(h, q, Lv.d));
+  k_axpy<<<grid_for(Lv.ndof, h->num_sms), kThreads, 0, h->stream>>>(x, 1.0, Lv.d, Lv.ndof);
+  h->count();
+  CU(cudaGetLastError());
+  return FCM_OK;
+}
+
+static int enqueue_coarse(fcm_mg* h, const double* b, double* x);
+// slab mode: replicated coarse solve -- all-gather the owned level-1 residual into the global
+// p = 1 vector, solve on every rank with the global handle, keep the local slots
+static int enqueue_coarse_slab(fcm_mg* h, const double* b, double* x) {
+  const int64_t n1 = h->lev[1].ndof;
+  k_gather32<<<grid_for(h->c_count, h->num_sms), kThreads, 0, h->stream>>>(h->c_send, b, h->c_pack, h->c_count);
+  h->count();
+  CU(cudaGetLastError());
+  NC(nccl().AllGather(h->c_send, h->c_recv, h->c_max, ncclFloat64, h->comm, h->stream));
+  const int64_t ntot = h->c_max * h->nranks;
+  k_scatter64<<<grid_for(ntot, h->num_sms), kThreads, 0, h->stream>>>(h->c_bg, h->c_recv, h->c_unpack, ntot);
+  h->count();
+  CU(cudaGetLastError());
+  fcm_mg* hg = h->hg;
+  hg->count_target = h->count_target;
+  const int rc = enqueue_coarse(hg, h->c_bg, h->c_xg);
+  h->launches += hg->launches;
+  hg->launches = 0;
+  hg->count_target = nullptr;
+  RC(rc);
+  k_gather64<<<grid_for(n1, h->num_sms), kThreads, 0, h->stream>>>(x, h->c_xg, h->c_extract, n1);
+  h->count();
+  CU(cudaGetLastError());
+  return FCM_OK;
+}
 
 static int enqueue_coarse(fcm_mg* h, const double* b, double* x) {
+  if (h->hg) return enqueue_coarse_slab(h, b, x);
   LevelDev& L1 = h->lev[1];
   const int64_t n = L1.ndof;
   if (h->prm.coarse == FCM_COARSE_DIRECT) {
@@ -713,7 +887,7 @@ static int enqueue_vcycle(fcm_mg* h, int q, const double* b, double* x) {
   const int64_t N = Lv.ndof;
   RC(fill(h, x, 0.0, N));
   for (int s = 0; s < h->prm.n_pre; ++s) {          // pre-smoothing
-    if (s == 0) RC(smooth(h, q, b, x));             // x = 0: r = b
+    if (s == 0) RC(smooth(h, q, b, x, true));       // x = 0: r = b
     else { RC(residual(h, q, b, x, Lv.r)); RC(smooth(h, q, Lv.r, x)); }
   }
   if (h->prm.n_pre > 0) RC(residual(h, q, b, x, Lv.r));  // update residual
@@ -852,6 +1026,11 @@ static int setup_schwarz(fcm_mg* h, int q, const std::vector<uint8_t>& kind,
   const int nx = L.n[0], ny = L.n[1], nz = L.n[2];
   const bool patch = q >= 2 && h->prm.block == FCM_BLOCK_PATCH;   // coarse AS is elementwise (R11)
   const BlockGeom g = block_geom(L, q, patch);
+  // cell arrays cover the owned cells plus the ghost layers of the slab (single GPU: the grid)
+  const int sax = dim - 1;
+  int elo[3] = {0, 0, 0}, ene[3] = {nx, ny, nz};
+  elo[sax] = h->ext_lo;
+  ene[sax] = h->ext_n;
   const int mb = g.mb;
   const int64_t nanchor = (int64_t)g.na[0] * g.na[1] * g.na[2];
   const int nas = (int)(g.amap.size() / std::max(1, mb));
@@ -873,8 +1052,10 @@ static int setup_schwarz(fcm_mg* h, int q, const std::vector<uint8_t>& kind,
     for (int d = 0; d < nas && regular; ++d) {
       int c3[3] = {ac[0] + g.aoff + d % g.nasm, dim >= 2 ? ac[1] + g.aoff + (d / g.nasm) % g.nasm : 0,
                    dim == 3 ? ac[2] + g.aoff + d / (g.nasm * g.nasm) : 0};
-      if (c3[0] < 0 || c3[1] < 0 || c3[2] < 0 || c3[0] >= nx || c3[1] >= ny || c3[2] >= nz) continue;
-      const int k = kind[((int64_t)c3[2] * ny + c3[1]) * nx + c3[0]];
+      bool inside = true;
+      for (int i = 0; i < 3; ++i) inside = inside && c3[i] >= elo[i] && c3[i] < elo[i] + ene[i];
+      if (!inside) continue;
+      const int k = kind[((int64_t)(c3[2] - elo[2]) * ene[1] + (c3[1] - elo[1])) * ene[0] + (c3[0] - elo[0])];
       if (k == 2 || (k0 >= 0 && k != k0)) regular = false;
       k0 = k;
     }
@@ -882,8 +1063,9 @@ static int setup_schwarz(fcm_mg* h, int q, const std::vector<uint8_t>& kind,
       // boundary type: per axis the clipped distances of the anchor to both faces (0 = interior)
       int key = 0, mul = 1;
       for (int i = 0; i < dim; ++i) {
-        const int hiA = patch ? L.n[i] : L.n[i] - 1;
-        const int lo = std::min(ac[i], R), hi = std::min(hiA - ac[i], R);
+        const int gi = ac[i] + (i == sax ? h->z0 : 0);   // global position along the axis
+        const int hiA = patch ? h->g.n[i] : h->g.n[i] - 1;
+        const int lo = std::min(gi, R), hi = std::min(hiA - gi, R);
         const int ci = (lo == R && hi == R) ? 0 : 1 + lo * (R + 1) + hi;
         key += ci * mul;
         mul *= (R + 1) * (R + 1) + 1;
@@ -938,10 +1120,11 @@ static int setup_schwarz(fcm_mg* h, int q, const std::vector<uint8_t>& kind,
   CU(cudaMemcpyAsync(Lv.blk, blk.data(), blk.size() * 4, cudaMemcpyHostToDevice, h->stream));
   BlockAsmArgs aa{};
   aa.nx = nx; aa.ny = ny; aa.nz = nz; aa.dim = dim; aa.mb = mb; aa.ldK = L.m;
+  for (int i = 0; i < 3; ++i) { aa.lo[i] = elo[i]; aa.ne[i] = ene[i]; }
   for (int i = 0; i < 3; ++i) aa.na[i] = g.na[i];
   aa.nasm = g.nasm; aa.aoff = g.aoff;
   aa.anchors = d_anchors; aa.virt = d_virt; aa.amap = d_amap; aa.dirich = d_dir;
-  aa.kind = h->d_kind; aa.cut_idx = h->d_cut_idx; aa.Kref = h->d_Kref; aa.cutK = h->d_cutK;
+  aa.kind = h->d_kind_ext; aa.cut_idx = h->d_cut_idx_ext; aa.Kref = h->d_Kref; aa.cutK = h->d_cutK;
   aa.alpha = h->alpha; aa.out = d_mats;
   if (nblk > 0) {
     k_assemble_blocks<<<(unsigned)nblk, kThreads, 0, h->stream>>>(aa);
@@ -1168,10 +1351,10 @@ static int setup_tiled(fcm_mg* h) {
   return FCM_OK;
 }
 
-extern "C" int fcm_mg_setup(const fcm_grid* g, const fcm_params* prm, const double* K_ref,
-                            const uint8_t* cell_kind, double alpha, int64_t n_cut,
-                            const int64_t* cut_cells, const double* cut_K, fcm_mg** out) {
-  clear_error();
+static int setup_impl(const fcm_grid* g, const fcm_params* prm, const fcm_slab* slab, const double* K_ref,
+                      const uint8_t* cell_kind, double alpha, int64_t n_cut, const int64_t* cut_cells,
+                      const double* cut_K, int64_t n_cc, const int64_t* cc_cells, const double* cc_K1,
+                      fcm_mg** out) {
   if (!g || !prm || !K_ref || !cell_kind || !out) return fail(FCM_EINVAL, "NULL argument");
   *out = nullptr;
   int me = fcm_element_size(g);
@@ -1182,10 +1365,25 @@ extern "C" int fcm_mg_setup(const fcm_grid* g, const fcm_params* prm, const doub
   if (prm->n_pre < 0 || prm->n_post < 0) return fail(FCM_EINVAL, "negative sweep count");
   if (prm->coarse < 0 || prm->coarse > 2) return fail(FCM_EINVAL, "unknown coarse solver");
   if (prm->block != FCM_BLOCK_ELEMENT && prm->block != FCM_BLOCK_PATCH) return fail(FCM_EINVAL, "unknown block kind %d", prm->block);
+  const int dim = g->dim, sax = dim - 1;
+  const int nsax = g->n[sax];
   std::unique_ptr<fcm_mg> h(new fcm_mg());
   h->g = *g;
   h->prm = *prm;
   h->alpha = alpha;
+  if (slab) {
+    if (slab->nranks < 1 || slab->rank < 0 || slab->rank >= slab->nranks || slab->z_begin < 0 ||
+        slab->z_end > nsax || slab->z_begin >= slab->z_end)
+      return fail(FCM_EINVAL, "bad slab (rank %d of %d, layers [%d, %d))", slab->rank, slab->nranks,
+                  slab->z_begin, slab->z_end);
+    h->rank = slab->rank; h->nranks = slab->nranks; h->z0 = slab->z_begin; h->z1 = slab->z_end;
+    if (h->nranks > 1 && prm->block == FCM_BLOCK_PATCH)
+      return fail(FCM_EINVAL, "patchwise blocks are single-GPU (config 3); use elementwise blocks with slabs");
+    if (h->nranks > 1 && (n_cc < 0 || (n_cc > 0 && (!cc_cells || !cc_K1))))
+      return fail(FCM_EINVAL, "slab setup needs every cut cell's leading p=1 block (replicated coarse level)");
+  } else {
+    h->z0 = 0; h->z1 = nsax;
+  }
   h->ustream = (cudaStream_t)prm->stream;
   CU(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
   CU(cudaStreamCreateWithFlags(&h->stream2, cudaStreamNonBlocking));
@@ -1195,8 +1393,14 @@ extern "C" int fcm_mg_setup(const fcm_grid* g, const fcm_params* prm, const doub
   CU(cudaEventCreateWithFlags(&h->ev_out, cudaEventDisableTiming));
   CU(cudaEventRecord(h->ev_in, h->ustream));
   CU(cudaStreamWaitEvent(h->stream, h->ev_in, 0));
+  if (h->nranks > 1) {
+    if (!nccl().ok) return fail(FCM_ENCCL, "libnccl.so.2 could not be loaded");
+    ncclUniqueId id;
+    std::memcpy(&id, slab->nccl_id, sizeof(id));
+    NC(nccl().CommInitRank(&h->comm, h->nranks, id, h->rank));
+  }
   Layout& L = h->L;
-  L.build(g->dim, g->n, g->p, g->space, g->n_f, g->dirichlet_faces);
+  slab_layout(L, dim, g->n, g->p, g->space, g->n_f, g->dirichlet_faces, h->z0, h->z1);
   h->ncell = L.ncell;
   for (int q = 1; q <= g->p; ++q)
     if (L.ndof_level[q] <= 0) return fail(FCM_EINVAL, "level q=%d has no free DOFs (empty level)", q);
@@ -1204,36 +1408,60 @@ extern "C" int fcm_mg_setup(const fcm_grid* g, const fcm_params* prm, const doub
     return fail(FCM_EINVAL, "grid too large for 32-bit cell/DOF indexing on one device");
   CU(cudaGetDevice(&h->dev));
   CU(cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, h->dev));
-  // cells
-  std::vector<uint8_t> kind(cell_kind, cell_kind + h->ncell);
-  std::vector<int32_t> cut_idx(h->ncell, -1);
+  // cells: owned layers [z0, z1) plus one ghost layer on each side that exists
+  int64_t plane = 1;
+  for (int i = 0; i < sax; ++i) plane *= g->n[i];
+  const int zg0 = std::max(h->z0 - 1, 0), zg1 = std::min(h->z1 + 1, nsax);
+  h->ext_lo = zg0 - h->z0;
+  h->ext_n = zg1 - zg0;
+  const int64_t ncell_ext = plane * (zg1 - zg0);
+  const int64_t own_off = plane * (h->z0 - zg0);
+  const int64_t c_ext0 = plane * zg0;   // global index of the first extended cell
+  std::vector<uint8_t> kind(cell_kind + c_ext0, cell_kind + c_ext0 + ncell_ext);
+  std::vector<int32_t> cut_idx(ncell_ext, -1);
+  h->cut_first = -1;
+  int64_t ncut_own = 0;
   for (int64_t i = 0; i < n_cut; ++i) {
-    int64_t c = cut_cells[i];
-    if (c < 0 || c >= h->ncell || kind[c] != 2) return fail(FCM_EINVAL, "cut_cells[%lld] is not a cut cell", (long long)i);
+    const int64_t c = cut_cells[i] - c_ext0;
+    if (c < 0 || c >= ncell_ext || kind[c] != 2)
+      return fail(FCM_EINVAL, "cut_cells[%lld] is not a cut cell of the (slab) grid", (long long)i);
+    if (i > 0 && cut_cells[i] <= cut_cells[i - 1]) return fail(FCM_EINVAL, "cut_cells must be ascending");
     cut_idx[c] = (int32_t)i;
+    if (c >= own_off && c < own_off + h->ncell) {
+      if (h->cut_first < 0) h->cut_first = i;
+      ++ncut_own;
+    }
   }
-  for (int64_t c = 0; c < h->ncell; ++c) {
-    if (kind[c] > 2) return fail(FCM_EINVAL, "cell_kind[%lld] = %d", (long long)c, kind[c]);
-    if (kind[c] == 2 && cut_idx[c] < 0) return fail(FCM_EINVAL, "cut cell %lld has no matrix", (long long)c);
+  if (h->cut_first < 0) h->cut_first = 0;
+  for (int64_t c = 0; c < ncell_ext; ++c) {
+    if (kind[c] > 2) return fail(FCM_EINVAL, "cell_kind[%lld] = %d", (long long)(c + c_ext0), kind[c]);
+    if (kind[c] == 2 && cut_idx[c] < 0) return fail(FCM_EINVAL, "cut cell %lld has no matrix", (long long)(c + c_ext0));
   }
-  h->ncut = n_cut;
+  h->ncut = ncut_own;
   const int m = L.m;
-  RC(h->alloc(&h->d_kind, h->ncell));
-  RC(h->alloc(&h->d_cut_idx, h->ncell));
+  RC(h->alloc(&h->d_kind_ext, ncell_ext));
+  RC(h->alloc(&h->d_cut_idx_ext, ncell_ext));
+  h->d_kind = h->d_kind_ext + own_off;
+  h->d_cut_idx = h->d_cut_idx_ext + own_off;
   RC(h->alloc(&h->d_Kref, (size_t)m * m));
   RC(h->alloc(&h->d_cutK, (size_t)std::max<int64_t>(n_cut, 1) * m * m));
-  CU(cudaMemcpyAsync(h->d_kind, kind.data(), h->ncell, cudaMemcpyHostToDevice, h->stream));
-  CU(cudaMemcpyAsync(h->d_cut_idx, cut_idx.data(), h->ncell * 4, cudaMemcpyHostToDevice, h->stream));
+  CU(cudaMemcpyAsync(h->d_kind_ext, kind.data(), ncell_ext, cudaMemcpyHostToDevice, h->stream));
+  CU(cudaMemcpyAsync(h->d_cut_idx_ext, cut_idx.data(), ncell_ext * 4, cudaMemcpyHostToDevice, h->stream));
   {
-    std::vector<int32_t> cl(cut_cells, cut_cells + n_cut);
+    std::vector<int32_t> cl;
+    for (int64_t i = h->cut_first; i < h->cut_first + ncut_own; ++i) cl.push_back((int32_t)(cut_cells[i] - c_ext0 - own_off));
     RC(h->alloc(&h->d_cut_list, cl.size()));
     CU(cudaMemcpyAsync(h->d_cut_list, cl.data(), cl.size() * 4, cudaMemcpyHostToDevice, h->stream));
   }
   CU(cudaMemcpyAsync(h->d_Kref, K_ref, (size_t)m * m * 8, cudaMemcpyHostToDevice, h->stream));
   if (n_cut > 0)
     CU(cudaMemcpyAsync(h->d_cutK, cut_K, (size_t)n_cut * m * m * 8, cudaMemcpyHostToDevice, h->stream));
+  // owned-cell views for the host-side helpers (coarse_dense)
+  std::vector<uint8_t> kind_own(kind.begin() + own_off, kind.begin() + own_off + h->ncell);
+  std::vector<int32_t> cut_idx_own(cut_idx.begin() + own_off, cut_idx.begin() + own_off + h->ncell);
   // levels
   h->lev.assign(g->p + 1, LevelDev());
+  int64_t max_plane = 0;
   for (int q = 1; q <= g->p; ++q) {
     LevelDev& Lv = h->lev[q];
     const LevelTable& T = L.tables[q];
@@ -1263,9 +1491,27 @@ extern "C" int fcm_mg_setup(const fcm_grid* g, const fcm_params* prm, const doub
     CU(cudaMemcpyAsync(Lv.cmax, T.cmax.data(), T.m * 6, cudaMemcpyHostToDevice, h->stream));
     RC(h->alloc(&Lv.x, Lv.ndof));
     RC(h->alloc(&Lv.r, Lv.ndof));
+    if (h->nranks > 1) {   // interface planes of this level (slab.hpp), exchange order
+      std::vector<int32_t> lo, hi;
+      if (h->z0 > 0) plane_slots(L, q, 0, lo);
+      if (h->z1 < nsax) plane_slots(L, q, h->z1 - h->z0, hi);
+      Lv.n_lo = (int64_t)lo.size();
+      Lv.n_hi = (int64_t)hi.size();
+      RC(h->alloc(&Lv.lo_idx, lo.size()));
+      RC(h->alloc(&Lv.hi_idx, hi.size()));
+      if (!lo.empty()) CU(cudaMemcpyAsync(Lv.lo_idx, lo.data(), lo.size() * 4, cudaMemcpyHostToDevice, h->stream));
+      if (!hi.empty()) CU(cudaMemcpyAsync(Lv.hi_idx, hi.data(), hi.size() * 4, cudaMemcpyHostToDevice, h->stream));
+      RC(h->alloc(&Lv.d, Lv.ndof));
+      max_plane = std::max<int64_t>(max_plane, Lv.n_lo + Lv.n_hi);
+    }
+  }
+  if (h->nranks > 1) {
+    RC(h->alloc(&h->x_send, 2 * std::max<int64_t>(max_plane, 1)));
+    RC(h->alloc(&h->x_recv, 2 * std::max<int64_t>(max_plane, 1)));
   }
   for (int q = 1; q <= g->p; ++q)
-    if (q >= 2 || prm->coarse == FCM_COARSE_AS_PCG) RC(setup_schwarz(h.get(), q, kind, cut_idx));
+    if (q >= 2 || (prm->coarse == FCM_COARSE_AS_PCG && h->nranks == 1))
+      RC(setup_schwarz(h.get(), q, kind, cut_idx));
   for (int q = 2; q <= g->p; ++q)
     if (h->lev[q].patch) {
       const size_t sm = block_smem(h->lev[q].m, h->lev[q].mb);
@@ -1275,10 +1521,70 @@ extern "C" int fcm_mg_setup(const fcm_grid* g, const fcm_params* prm, const doub
   CU(cudaMemsetAsync(h->d_coarse_iters, 0, 8, h->stream));
   // coarse level
   const int64_t n1 = L.ndof_level[1];
-  if (prm->coarse == FCM_COARSE_DIRECT) {
+  if (h->nranks > 1) {
+    // replicated global p = 1 problem: every rank solves it (fcm_slab; no inner-CG traffic)
+    fcm_grid g1 = *g;
+    g1.p = 1;
+    const int m1 = L.m_level[1];
+    std::vector<double> K1((size_t)m1 * m1);
+    for (int r = 0; r < m1; ++r)
+      for (int c = 0; c < m1; ++c) K1[(size_t)r * m1 + c] = K_ref[(size_t)r * m + c];
+    fcm_params p1 = *prm;
+    p1.stream = (void*)h->stream;
+    fcm_mg* hg = nullptr;
+    RC(setup_impl(&g1, &p1, nullptr, K1.data(), cell_kind, alpha, n_cc, cc_cells, cc_K1, 0, nullptr,
+                  nullptr, &hg));
+    h->hg = hg;
+    CU(cudaStreamSynchronize(hg->stream));
+    CU(cudaStreamDestroy(hg->stream));
+    hg->stream = h->stream;
+    hg->borrowed_stream = true;
+    // all-gather maps: rank j's owned level-1 slots -> global level-1 slots
+    Layout Lg;
+    Lg.build(dim, g->n, 1, g->space, g->n_f, g->dirichlet_faces);
+    std::vector<std::vector<int64_t>> own_glob(h->nranks);
+    std::vector<int32_t> pack;
+    std::vector<int64_t> extract;
+    for (int j = 0; j < h->nranks; ++j) {
+      int a0, a1;
+      slab_bounds(nsax, h->nranks, j, &a0, &a1);
+      Layout Lj;
+      slab_layout(Lj, dim, g->n, g->p, g->space, g->n_f, g->dirichlet_faces, a0, a1);
+      std::vector<int64_t> gs;
+      coarse_global_slots(Lj, Lg, gs);
+      std::vector<uint8_t> own;
+      owned_mask(Lj, 1, a0 > 0, own);
+      for (size_t i = 0; i < gs.size(); ++i)
+        if (own[i]) {
+          own_glob[j].push_back(gs[i]);
+          if (j == h->rank) pack.push_back((int32_t)i);
+        }
+      if (j == h->rank) {
+        if (a0 != h->z0 || a1 != h->z1) return fail(FCM_EINVAL, "slab [%d,%d) is not fcm_slab_bounds' partition", h->z0, h->z1);
+        extract = gs;
+      }
+    }
+    h->c_count = (int64_t)pack.size();
+    h->c_max = 0;
+    for (auto& v : own_glob) h->c_max = std::max<int64_t>(h->c_max, (int64_t)v.size());
+    std::vector<int64_t> unpack((size_t)h->nranks * h->c_max, -1);
+    for (int j = 0; j < h->nranks; ++j)
+      for (size_t i = 0; i < own_glob[j].size(); ++i) unpack[(size_t)j * h->c_max + i] = own_glob[j][i];
+    RC(h->alloc(&h->c_pack, pack.size()));
+    RC(h->alloc(&h->c_unpack, unpack.size()));
+    RC(h->alloc(&h->c_extract, extract.size()));
+    RC(h->alloc(&h->c_send, h->c_max));
+    RC(h->alloc(&h->c_recv, (size_t)h->nranks * h->c_max));
+    RC(h->alloc(&h->c_bg, Lg.ndof_level[1]));
+    RC(h->alloc(&h->c_xg, Lg.ndof_level[1]));
+    CU(cudaMemcpyAsync(h->c_pack, pack.data(), pack.size() * 4, cudaMemcpyHostToDevice, h->stream));
+    CU(cudaMemcpyAsync(h->c_unpack, unpack.data(), unpack.size() * 8, cudaMemcpyHostToDevice, h->stream));
+    CU(cudaMemcpyAsync(h->c_extract, extract.data(), extract.size() * 8, cudaMemcpyHostToDevice, h->stream));
+    CU(cudaMemsetAsync(h->c_send, 0, h->c_max * 8, h->stream));
+  } else if (prm->coarse == FCM_COARSE_DIRECT) {
     if (n1 > 8192) return fail(FCM_EINVAL, "direct coarse solve limited to 8192 DOFs (level 1 has %lld)", (long long)n1);
     std::vector<double> A0;
-    coarse_dense(h.get(), kind, cut_idx, K_ref, cut_K, &A0, nullptr);
+    coarse_dense(h.get(), kind_own, cut_idx_own, K_ref, cut_K, &A0, nullptr);
     double* fac;
     int* st;
     RC(h->alloc(&h->d_A0inv, (size_t)n1 * n1));
@@ -1294,7 +1600,7 @@ extern "C" int fcm_mg_setup(const fcm_grid* g, const fcm_params* prm, const doub
   } else {
     if (prm->coarse == FCM_COARSE_JACOBI_PCG) {
       std::vector<double> dg;
-      coarse_dense(h.get(), kind, cut_idx, K_ref, cut_K, nullptr, &dg);
+      coarse_dense(h.get(), kind_own, cut_idx_own, K_ref, cut_K, nullptr, &dg);
       for (auto& v : dg) v = 1.0 / v;
       RC(h->alloc(&h->d_diag_inv, n1));
       CU(cudaMemcpyAsync(h->d_diag_inv, dg.data(), n1 * 8, cudaMemcpyHostToDevice, h->stream));
@@ -1330,11 +1636,45 @@ extern "C" int fcm_mg_setup(const fcm_grid* g, const fcm_params* prm, const doub
   RC(h->alloc(&h->d_partA, 2 * kMaxPartials));
   RC(h->alloc(&h->d_partB, 2 * kMaxPartials));
   RC(h->alloc(&h->d_partC, 2 * kMaxPartials));
+  if (h->nranks > 1) {
+    std::vector<uint8_t> own;
+    owned_mask(L, g->p, h->z0 > 0, own);
+    RC(h->alloc(&h->d_own, own.size()));
+    CU(cudaMemcpyAsync(h->d_own, own.data(), own.size(), cudaMemcpyHostToDevice, h->stream));
+  }
   CU(cudaMallocHost((void**)&h->h_s, sizeof(Scalars)));
   CU(cudaMallocHost((void**)&h->h_iters, sizeof(int)));
   CU(cudaMemsetAsync(h->d_s, 0, sizeof(Scalars), h->stream));
   CU(cudaStreamSynchronize(h->stream));
   *out = h.release();
+  return FCM_OK;
+}
+
+extern "C" int fcm_mg_setup(const fcm_grid* g, const fcm_params* prm, const double* K_ref,
+                            const uint8_t* cell_kind, double alpha, int64_t n_cut,
+                            const int64_t* cut_cells, const double* cut_K, fcm_mg** out) {
+  clear_error();
+  return setup_impl(g, prm, nullptr, K_ref, cell_kind, alpha, n_cut, cut_cells, cut_K, 0, nullptr, nullptr, out);
+}
+
+extern "C" int fcm_mg_setup_slab(const fcm_grid* g, const fcm_params* prm, const fcm_slab* slab,
+                                 const double* K_ref, const uint8_t* cell_kind, double alpha,
+                                 int64_t n_cut, const int64_t* cut_cells, const double* cut_K,
+                                 int64_t n_coarse_cut, const int64_t* coarse_cut_cells,
+                                 const double* coarse_cut_K1, fcm_mg** out) {
+  clear_error();
+  if (!slab) return fail(FCM_EINVAL, "NULL slab");
+  return setup_impl(g, prm, slab, K_ref, cell_kind, alpha, n_cut, cut_cells, cut_K, n_coarse_cut,
+                    coarse_cut_cells, coarse_cut_K1, out);
+}
+
+extern "C" int fcm_nccl_unique_id(void* id128) {
+  clear_error();
+  if (!id128) return fail(FCM_EINVAL, "NULL argument");
+  if (!nccl().ok) return fail(FCM_ENCCL, "libnccl.so.2 could not be loaded");
+  ncclUniqueId id;
+  NC(nccl().GetUniqueId(&id));
+  std::memcpy(id128, &id, sizeof(id));
   return FCM_OK;
 }
 
@@ -1364,7 +1704,7 @@ extern "C" int fcm_mg_level_m(const fcm_mg* h, int32_t q, int32_t* m) {
 extern "C" int fcm_mg_dof_keys(const fcm_mg* h, int64_t* keys) {
   if (!h || !keys) return fail(FCM_EINVAL, "NULL argument");
   for (int a = 0; a < h->L.dim; ++a)
-    if (h->L.n[a] != h->L.n[0]) return fail(FCM_EINVAL, "DOF keys need nx == ny == nz");
+    if (h->g.n[a] != h->g.n[0]) return fail(FCM_EINVAL, "DOF keys need nx == ny == nz");
   h->L.keys(h->g.p, keys);
   return FCM_OK;
 }
@@ -1383,12 +1723,14 @@ extern "C" int fcm_mg_load(fcm_mg* h, const double* f_ref, const double* cut_f,
   CU(cudaStreamSynchronize(h->stream));
   std::vector<double> bh(L.ndof_level[p], 0.0);
   int tax = traction_face >= 0 ? traction_face / 2 : -1, tside = traction_face % 2;
+  const int sax = L.dim - 1;
   for (int64_t c = 0; c < h->ncell; ++c) {
     int cc[3];
     L.cell_coords(c, cc);
     const double* f = kind[c] == 2 ? cut_f + (size_t)ci[c] * m : f_ref;
     double s = kind[c] == 1 ? h->alpha : 1.0;
-    bool tr = f_traction && tax >= 0 && cc[tax] == (tside ? L.n[tax] - 1 : 0);
+    const int ct = tax >= 0 ? cc[tax] + (tax == sax ? h->z0 : 0) : 0;   // global coordinate
+    bool tr = f_traction && tax >= 0 && ct == (tside ? h->g.n[tax] - 1 : 0);
     for (int a = 0; a < m; ++a) {
       int64_t i = L.dof_index(p, a, cc);
       if (i < 0) continue;
@@ -1396,6 +1738,7 @@ extern "C" int fcm_mg_load(fcm_mg* h, const double* f_ref, const double* cut_f,
     }
   }
   CU(cudaMemcpyAsync(b, bh.data(), bh.size() * 8, cudaMemcpyHostToDevice, h->stream));
+  RC(exchange(h, p, b));   // slab mode: interface planes hold both ranks' contributions
   CU(cudaStreamSynchronize(h->stream));
   return FCM_OK;
 }
@@ -1404,8 +1747,7 @@ extern "C" int fcm_apply(fcm_mg* h, int32_t q, const double* x, double* y) {
   clear_error();
   if (!h || !x || !y || q < 1 || q > h->g.p) return fail(FCM_EINVAL, "bad argument");
   StreamGuard sg(h);
-  RC(fill(h, y, 0.0, h->lev[q].ndof));
-  return launch_cellop(h, q, make_op(h, q, OP_APPLY, x, y, 1.0, nullptr));
+  return apply_op(h, q, x, y, nullptr);
 }
 
 extern "C" int fcm_mg_smooth(fcm_mg* h, int32_t q, const double* r, double* x) {
@@ -1424,10 +1766,11 @@ extern "C" int fcm_mg_coarse_solve(fcm_mg* h, const double* r, double* x, int32_
   if (iters) {
     if (h->prm.coarse == FCM_COARSE_DIRECT) *iters = 0;
     else {
-      CU(cudaMemcpyAsync(h->h_iters, h->d_coarse_iters, 4, cudaMemcpyDeviceToHost, h->stream));
+      const fcm_mg* hc = h->hg ? h->hg : h;   // slab mode: the replicated coarse handle counts
+      CU(cudaMemcpyAsync(h->h_iters, hc->d_coarse_iters, 4, cudaMemcpyDeviceToHost, h->stream));
       CU(cudaStreamSynchronize(h->stream));
       *iters = *h->h_iters;
-      if (h->ktiled && h->tiled.prof) {   // FCM_TILED_PROF: mean phase times per iteration
+      if (hc->ktiled && hc->tiled.prof && !h->hg) {   // FCM_TILED_PROF: mean phase times per iteration
         std::vector<unsigned long long> pr((size_t)4 * h->t_blocks);
         CU(cudaMemcpy(pr.data(), h->tiled.prof, pr.size() * 8, cudaMemcpyDeviceToHost));
         double mx[4] = {0, 0, 0, 0}, mean[4] = {0, 0, 0, 0};
@@ -1471,14 +1814,25 @@ static int capture_fcg(fcm_mg* h) {
   double* z = h->lev[p].x;
   const int nbd = dot_blocks(h);
   const int nbc = cellop_nblocks(h, p, OP_APPLY);
+  // slab mode: partial sums are finalised on each rank, all-reduced, and the update kernels
+  // read the reduced scalars (red[]); dots skip the interface DOFs this rank does not own
+  const bool slab = h->nranks > 1;
+  const uint8_t* own = slab ? h->d_own : nullptr;
+  double* red = h->d_s->red;
   // init: x = 0, r = b, z = V(r), rz = z.r, p = z
   RC(capture(h, &h->g_init, &h->n_init, [&]() -> int {
     k_fcg_start<<<grid_for(N, h->num_sms), kThreads, 0, h->stream>>>(h->f_x, h->f_r, h->f_b, N);
     h->count();
     RC(enqueue_vcycle(h, p, h->f_r, z));
-    k_dot<<<nbd, kThreads, 0, h->stream>>>(z, h->f_r, N, h->d_partA);
+    k_dot<<<nbd, kThreads, 0, h->stream>>>(z, h->f_r, N, h->d_partA, own);
     h->count();
-    k_fcg_start2<<<grid_for(N, h->num_sms), kThreads, 0, h->stream>>>(h->d_s, h->d_partA, nbd, h->f_p, z, N);
+    if (slab) {
+      k_finalize<<<1, 32, 0, h->stream>>>(red + 3, h->d_partA, nbd);
+      h->count();
+      RC(allreduce(h, red + 3, 1));
+    }
+    k_fcg_start2<<<grid_for(N, h->num_sms), kThreads, 0, h->stream>>>(h->d_s, h->d_partA, nbd, h->f_p, z, N,
+                                                                      slab ? red + 3 : nullptr);
     h->count();
     CU(cudaGetLastError());
     return FCM_OK;
@@ -1487,21 +1841,34 @@ static int capture_fcg(fcm_mg* h) {
   RC(capture(h, &h->g_it1, &h->n_it1, [&]() -> int {
     RC(fill(h, h->f_q, 0.0, N));
     RC(launch_cellop(h, p, make_op(h, p, OP_APPLY, h->f_p, h->f_q, 1.0, h->d_partB)));
+    RC(exchange(h, p, h->f_q));
+    if (slab) {
+      k_finalize<<<1, 32, 0, h->stream>>>(red, h->d_partB, nbc);
+      h->count();
+      RC(allreduce(h, red, 1));
+    }
     k_fcg_update1<<<nbd, kThreads, 0, h->stream>>>(h->d_s, h->d_partB, nbc, h->f_x, h->f_r, h->f_ro,
-                                                    h->f_p, h->f_q, N, h->d_partC);
+                                                    h->f_p, h->f_q, N, h->d_partC, own, slab ? red : nullptr);
     h->count();
     k_finalize<<<1, 32, 0, h->stream>>>(&h->d_s->rr, h->d_partC, nbd);
     h->count();
     CU(cudaGetLastError());
+    if (slab) RC(allreduce(h, &h->d_s->rr, 1));
     CU(cudaMemcpyAsync(h->h_s, h->d_s, sizeof(Scalars), cudaMemcpyDeviceToHost, h->stream));
     return FCM_OK;
   }));
   // iteration part 2: z = V(r), beta, p = z + beta p
   RC(capture(h, &h->g_it2, &h->n_it2, [&]() -> int {
     RC(enqueue_vcycle(h, p, h->f_r, z));
-    k_dot2<<<nbd, kThreads, 0, h->stream>>>(z, h->f_r, h->f_ro, N, h->d_partA, h->d_partB);
+    k_dot2<<<nbd, kThreads, 0, h->stream>>>(z, h->f_r, h->f_ro, N, h->d_partA, h->d_partB, own);
     h->count();
-    k_fcg_update2<<<grid_for(N, h->num_sms), kThreads, 0, h->stream>>>(h->d_s, h->d_partA, h->d_partB, nbd, h->f_p, z, N);
+    if (slab) {
+      k_finalize2<<<1, 32, 0, h->stream>>>(red + 1, h->d_partA, h->d_partB, nbd);
+      h->count();
+      RC(allreduce(h, red + 1, 2));
+    }
+    k_fcg_update2<<<grid_for(N, h->num_sms), kThreads, 0, h->stream>>>(h->d_s, h->d_partA, h->d_partB, nbd, h->f_p, z, N,
+                                                                       slab ? red + 1 : nullptr);
     h->count();
     k_set_rz<<<1, 32, 0, h->stream>>>(h->d_s);
     h->count();
@@ -1517,9 +1884,10 @@ static int pcg_core(fcm_mg* h, double rtol, int32_t maxit, int32_t* iters, doubl
   RC(capture_fcg(h));
   // ||b||^2
   const int nbd = dot_blocks(h);
-  k_dot<<<nbd, kThreads, 0, h->stream>>>(h->f_b, h->f_b, N, h->d_partA);
+  k_dot<<<nbd, kThreads, 0, h->stream>>>(h->f_b, h->f_b, N, h->d_partA, h->nranks > 1 ? h->d_own : nullptr);
   k_finalize<<<1, 32, 0, h->stream>>>(&h->d_s->bb, h->d_partA, nbd);
   h->count(2);
+  RC(allreduce(h, &h->d_s->bb, 1));
   CU(cudaMemsetAsync(&h->d_s->flag, 0, sizeof(int), h->stream));
   CU(cudaMemcpyAsync(h->h_s, h->d_s, sizeof(Scalars), cudaMemcpyDeviceToHost, h->stream));
   CU(cudaStreamSynchronize(h->stream));
@@ -1527,7 +1895,7 @@ static int pcg_core(fcm_mg* h, double rtol, int32_t maxit, int32_t* iters, doubl
   int it = 0;
   if (hist) hist[0] = bb > 0 ? 1.0 : 0.0;
   h->stat_coarse = 0;
-  CU(cudaMemsetAsync(h->d_coarse_iters, 0, 8, h->stream));
+  CU(cudaMemsetAsync((h->hg ? h->hg : h)->d_coarse_iters, 0, 8, h->stream));
   h->stat_vcycles = 0;
   if (!(bb > 0)) {
     RC(fill(h, h->f_x, 0.0, N));
@@ -1587,7 +1955,7 @@ extern "C" int fcm_mg_stats(const fcm_mg* h, int64_t* coarse_iters_total, int64_
   if (!h) return fail(FCM_EINVAL, "NULL handle");
   if (coarse_iters_total) {
     int v[2] = {0, 0};
-    CU(cudaMemcpyAsync(v, h->d_coarse_iters, 8, cudaMemcpyDeviceToHost, h->stream));
+    CU(cudaMemcpyAsync(v, (h->hg ? h->hg : h)->d_coarse_iters, 8, cudaMemcpyDeviceToHost, h->stream));
     CU(cudaStreamSynchronize(h->stream));
     *coarse_iters_total = v[1];
   }
@@ -1597,6 +1965,7 @@ extern "C" int fcm_mg_stats(const fcm_mg* h, int64_t* coarse_iters_total, int64_
 
 extern "C" int fcm_mg_coarse_info(const fcm_mg* h, int32_t* kind, int32_t* blocks, int32_t* tile) {
   if (!h || !kind || !blocks) return fail(FCM_EINVAL, "NULL argument");
+  if (h->hg) return fcm_mg_coarse_info(h->hg, kind, blocks, tile);
   if (h->prm.coarse == FCM_COARSE_DIRECT) { *kind = FCM_COARSE_KERNEL_DIRECT; *blocks = 0; }
   else if (h->ktiled) { *kind = FCM_COARSE_KERNEL_TILED; *blocks = h->t_blocks; }
   else { *kind = FCM_COARSE_KERNEL_GRID; *blocks = h->coarse_blocks; }

@@ -54,6 +54,7 @@ struct Layout {
   std::vector<int64_t> ndof_level;   // index q
   std::vector<LevelTable> tables;    // index q
   int64_t ncell = 0;
+  int zoff = 0;                      // slab offset of the last axis (global DOF keys)
 
   static int mode_order(const int k[3], int dim, int space) {
     int mx = 1, sum = 0;
@@ -186,6 +187,7 @@ struct Layout {
           t /= std::max(1, dc.size[a]);
           if (a < dim) X[a] = (dc.S >> a & 1) ? 2 * pos + 1 : 2 * pos;
         }
+        X[dim - 1] += 2 * (int64_t)zoff;
         int64_t k = (X[2] * W + X[1]) * W + X[0];
         k = ((k * (p + 1) + dc.deg[2]) * (p + 1) + dc.deg[1]) * (p + 1) + dc.deg[0];
         out[dc.off + i] = k * n_f + dc.comp;

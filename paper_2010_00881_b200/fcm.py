@@ -15,7 +15,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from ._lib import Grid, Params, Physics, check
+from ._lib import Grid, Params, Physics, Slab, check
 
 COARSE = {"direct": 0, "as_pcg": 1, "jacobi_pcg": 2}
 BLOCK = {"element": 0, "patch": 1}
@@ -90,8 +90,20 @@ class GenProblem:
     f_traction: np.ndarray  # [m]
 
 
-def generate(cfg, centres=None, radii=None, threads: int = 0) -> GenProblem:
-    """Workload generator (fcm_gen_classify + fcm_gen_element_matrices)."""
+def classify(cfg, centres, radii):
+    centres = np.ascontiguousarray(centres, dtype=np.float64)
+    radii = np.ascontiguousarray(radii, dtype=np.float64)
+    g = grid_of(cfg)
+    kind = np.zeros(cfg.n ** cfg.dim, dtype=np.uint8)
+    ncut = C.c_int64(0)
+    check(_lib.lib().fcm_gen_classify(C.byref(g), len(radii), _ptr(centres), _ptr(radii), _ptr(kind),
+                                      C.byref(ncut)))
+    return kind, ncut.value
+
+
+def generate(cfg, centres=None, radii=None, threads: int = 0, cut_cells=None, kind=None) -> GenProblem:
+    """Workload generator (fcm_gen_classify + fcm_gen_element_matrices).  cut_cells: restrict
+    the cut-cell quadrature to these cells (slab + ghost layers in multi-GPU runs)."""
     from workloads import config_voids
     if centres is None:
         centres, radii = config_voids(cfg)
@@ -100,11 +112,11 @@ def generate(cfg, centres=None, radii=None, threads: int = 0) -> GenProblem:
     L = _lib.lib()
     g = grid_of(cfg)
     ph = physics_of(cfg)
-    ncell = cfg.n ** cfg.dim
-    kind = np.zeros(ncell, dtype=np.uint8)
-    ncut = C.c_int64(0)
-    check(L.fcm_gen_classify(C.byref(g), len(radii), _ptr(centres), _ptr(radii), _ptr(kind), C.byref(ncut)))
-    cut_cells = np.nonzero(kind == 2)[0].astype(np.int64)
+    if kind is None:
+        kind, _ = classify(cfg, centres, radii)
+    if cut_cells is None:
+        cut_cells = np.nonzero(kind == 2)[0].astype(np.int64)
+    cut_cells = np.ascontiguousarray(cut_cells, dtype=np.int64)
     m = element_size(cfg)
     K_ref = np.zeros((m, m))
     f_ref = np.zeros(m)
@@ -117,10 +129,50 @@ def generate(cfg, centres=None, radii=None, threads: int = 0) -> GenProblem:
     return GenProblem(kind, cut_cells, K_ref, f_ref, cut_K, cut_f, f_tr)
 
 
+# ---- slab decomposition (multi-GPU; include/fcm_mg.h "multi-GPU") -----------------------
+def slab_bounds(n: int, nranks: int, rank: int):
+    a, b = C.c_int32(), C.c_int32()
+    check(_lib.lib().fcm_slab_bounds(n, nranks, rank, C.byref(a), C.byref(b)))
+    return a.value, b.value
+
+
+def slab_layout(cfg, z_begin: int, z_end: int, q: int):
+    """Host-only local layout of a slab: (keys, owned mask, bottom plane slots, top plane slots)."""
+    L = _lib.lib()
+    g = grid_of(cfg)
+    n, nlo, nhi = C.c_int64(), C.c_int64(), C.c_int64()
+    check(L.fcm_slab_layout(C.byref(g), z_begin, z_end, q, C.byref(n), None, None, C.byref(nlo), None,
+                            C.byref(nhi), None))
+    keys = np.zeros(n.value, dtype=np.int64)
+    own = np.zeros(n.value, dtype=np.uint8)
+    lo = np.zeros(nlo.value, dtype=np.int32)
+    hi = np.zeros(nhi.value, dtype=np.int32)
+    check(L.fcm_slab_layout(C.byref(g), z_begin, z_end, q, C.byref(n), _ptr(keys), _ptr(own), C.byref(nlo),
+                            _ptr(lo) if len(lo) else None, C.byref(nhi), _ptr(hi) if len(hi) else None))
+    return keys, own.astype(bool), lo, hi
+
+
+def slab_coarse_map(cfg, z_begin: int, z_end: int) -> np.ndarray:
+    L = _lib.lib()
+    g = grid_of(cfg)
+    n = C.c_int64()
+    check(L.fcm_slab_coarse_map(C.byref(g), z_begin, z_end, C.byref(n), None))
+    out = np.zeros(n.value, dtype=np.int64)
+    check(L.fcm_slab_coarse_map(C.byref(g), z_begin, z_end, C.byref(n), _ptr(out)))
+    return out
+
+
+def nccl_unique_id() -> bytes:
+    buf = (C.c_char * 128)()
+    check(_lib.lib().fcm_nccl_unique_id(buf))
+    return bytes(buf)
+
+
 class Solver:
     """Owns an fcm_mg handle (device hierarchy, Schwarz inverses, graphs)."""
 
-    def __init__(self, cfg, K_ref, cell_kind, cut_cells, cut_K, alpha=None, stream=None, **over):
+    def __init__(self, cfg, K_ref, cell_kind, cut_cells, cut_K, alpha=None, stream=None, slab=None,
+                 coarse_cut=None, **over):
         self.cfg = cfg
         L = _lib.lib()
         self._g = grid_of(cfg)
@@ -130,11 +182,54 @@ class Solver:
         cut_cells = np.ascontiguousarray(cut_cells, dtype=np.int64)
         cut_K = np.ascontiguousarray(cut_K, dtype=np.float64)
         h = C.c_void_p()
-        check(L.fcm_mg_setup(C.byref(self._g), C.byref(self._p), _ptr(K_ref), _ptr(cell_kind),
-                             cfg.alpha if alpha is None else alpha, len(cut_cells), _ptr(cut_cells),
-                             _ptr(cut_K), C.byref(h)))
+        a = cfg.alpha if alpha is None else alpha
+        if slab is None:
+            check(L.fcm_mg_setup(C.byref(self._g), C.byref(self._p), _ptr(K_ref), _ptr(cell_kind), a,
+                                 len(cut_cells), _ptr(cut_cells), _ptr(cut_K), C.byref(h)))
+        else:
+            rank, nranks, z0, z1, nccl_id = slab
+            self._idbuf = C.create_string_buffer(bytes(nccl_id) if nccl_id else b"\0" * 128, 128)
+            sl = Slab(rank, nranks, z0, z1, C.cast(self._idbuf, C.c_void_p))
+            cc, cK1 = coarse_cut if coarse_cut is not None else (np.zeros(0, np.int64), np.zeros(0))
+            cc = np.ascontiguousarray(cc, dtype=np.int64)
+            cK1 = np.ascontiguousarray(cK1, dtype=np.float64)
+            check(L.fcm_mg_setup_slab(C.byref(self._g), C.byref(self._p), C.byref(sl), _ptr(K_ref),
+                                      _ptr(cell_kind), a, len(cut_cells), _ptr(cut_cells), _ptr(cut_K),
+                                      len(cc), _ptr(cc), _ptr(cK1), C.byref(h)))
+        self.slab = slab
         self._h = h
         self.device = torch.device("cuda", torch.cuda.current_device())
+
+    @classmethod
+    def distributed(cls, cfg, rank: int, nranks: int, threads: int = 0, **over):
+        """Slab-decomposed solver over torch.distributed ranks (one GPU each).  Each rank runs
+        the generator for its owned + ghost cell layers; the leading p = 1 blocks of every cut
+        cell (replicated coarse level) and the NCCL id are exchanged through torch.distributed
+        (plumbing).  Returns (solver, local GenProblem restricted to the slab)."""
+        import torch.distributed as dist
+        from workloads import config_voids
+        n = cfg.n
+        z0, z1 = slab_bounds(n, nranks, rank)
+        centres, radii = config_voids(cfg)
+        kind, _ = classify(cfg, centres, radii)
+        plane = n ** (cfg.dim - 1)
+        lo, hi = max(z0 - 1, 0) * plane, min(z1 + 1, n) * plane
+        cut_all = np.nonzero(kind == 2)[0].astype(np.int64)
+        cut_ext = cut_all[(cut_all >= lo) & (cut_all < hi)]
+        G = generate(cfg, centres, radii, threads=threads, cut_cells=cut_ext, kind=kind)
+        m1 = (2 ** cfg.dim) * cfg.n_f
+        own = (cut_ext >= z0 * plane) & (cut_ext < z1 * plane)
+        mine = (cut_ext[own], np.ascontiguousarray(G.cut_K[own][:, :m1, :m1]))
+        parts = [None] * nranks
+        dist.all_gather_object(parts, mine)
+        cc = np.concatenate([p_[0] for p_ in parts]) if parts else np.zeros(0, np.int64)
+        cK1 = np.concatenate([p_[1] for p_ in parts]) if parts else np.zeros((0, m1, m1))
+        order = np.argsort(cc)
+        ids = [nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(ids, src=0)
+        S = cls(cfg, G.K_ref, kind, cut_ext, G.cut_K, slab=(rank, nranks, z0, z1, ids[0]),
+                coarse_cut=(cc[order], cK1[order]), **over)
+        return S, G
 
     @classmethod
     def from_problem(cls, cfg, prob: GenProblem, **over):
