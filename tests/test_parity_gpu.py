@@ -245,3 +245,17 @@ def test_coarse_kernels_both_paths(case, tiled, monkeypatch):
     x, it = pair.S.coarse_solve(pair.to_gpu(r, 1))
     assert rel(pair.from_gpu(x, 1), ref) <= 1e-10
     assert abs(it - H.coarse_iters[-1]) <= 1
+
+
+def test_single_rank_slab_setup_matches_single_gpu():
+    # fcm_mg_setup_slab with one rank is the single-GPU path (no exchange, no replicated coarse)
+    from paper_2010_00881_b200.fcm import Solver, generate
+    cfg = small_config(3, 5, 2, voids=2, seed=5)
+    G = generate(cfg)
+    S1 = Solver.from_problem(cfg, G)
+    S2 = Solver(cfg, G.K_ref, G.kind, G.cut_cells, G.cut_K, slab=(0, 1, 0, cfg.n, None))
+    b1, b2 = S1.load(G), S2.load(G)
+    assert torch.equal(b1, b2)
+    x1, it1, _ = S1.pcg_solve(b1)
+    x2, it2, _ = S2.pcg_solve(b2)
+    assert it1 == it2 and rel(x2.cpu().numpy(), x1.cpu().numpy()) <= 1e-12
