@@ -83,6 +83,7 @@ struct LevelDev {
   int32_t* irr_list = nullptr;     // cells with an individual Schwarz inverse (irr order)
   int ilo[3] = {0, 0, 0}, ihi[3] = {-1, -1, -1};  // cells with no Dirichlet DOF
   int ts = 1;                      // threads per cell of the regular path
+  bool row = true;                 // regular path = k_cell_row (one thread per cell)
   std::vector<int32_t> blk_h;      // host copy of blk (tiled coarse setup)
   // patchwise blocks (blocks.cuh): anchors are grid vertices, blk is per anchor
   bool patch = false;
@@ -225,6 +226,26 @@ __global__ void __launch_bounds__(kThreads, 4) k_cell_reg(CellOp op) {
   const int wpb = blockDim.x >> 5;
   double* xs = Ms + M * padded<M>() + (threadIdx.x >> 5) * reg_scratch<M, TS>();
   const double e = reg_cells<M, TS, false>(op, T, Ms, xs, blockIdx.x * wpb + (threadIdx.x >> 5), gridDim.x * wpb);
+  if (op.partials) {
+    const double t = block_sum(e, red);
+    if (threadIdx.x == 0) op.partials[blockIdx.x] = t;
+  }
+}
+
+// Regular population, row-streaming form (row_cells): one thread per cell; smem [Tab][Ms: M*M]
+template <int M>
+__global__ void __launch_bounds__(kThreads) k_cell_row(CellOp op) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  Tab& T = *reinterpret_cast<Tab*>(smem);
+  double* Ms = reinterpret_cast<double*>(smem + sizeof(Tab));
+  __shared__ double red[32];
+  load_tab(T, op);
+  for (int e = threadIdx.x; e < M * M; e += blockDim.x) {
+    const int a = e / M, b = e % M;
+    Ms[e] = (op.mode == OP_APPLY) ? op.Kref[a * op.ldK + b] : op.type_inv[a * M + b];  // type slot 0
+  }
+  __syncthreads();
+  const double e = row_cells<M, row_split<M>()>(op, T, Ms);
   if (op.partials) {
     const double t = block_sum(e, red);
     if (threadIdx.x == 0) op.partials[blockIdx.x] = t;
@@ -510,9 +531,9 @@ template <int M> constexpr int gsz() { return M <= 4 ? 4 : (M <= 8 ? 8 : (M <= 1
 #define FCM_FOR_M(X) X(4) X(8) X(9) X(16) X(24) X(25) X(27)
 
 // ts1: force one thread per cell (tuning knob FCM_TS1)
-const void* reg_kernel(int m, int* M_out, bool ts1) {
+const void* reg_kernel(int m, int* M_out, bool ts1, bool row) {
 #define CASE(MM) case MM: *M_out = MM; \
-  return ts1 ? (const void*)k_cell_reg<MM, 1> : (const void*)k_cell_reg<MM, split_of<MM>()>;
+  return row ? (const void*)k_cell_row<MM> : ts1 ? (const void*)k_cell_reg<MM, 1> : (const void*)k_cell_reg<MM, split_of<MM>()>;
   switch (m) { FCM_FOR_M(CASE) default: break; }
 #undef CASE
   *M_out = 0;
@@ -567,6 +588,10 @@ static int split_rt(int M) { return M <= 4 ? 1 : (M <= 9 ? 2 : (M <= 16 ? 4 : 8)
 static size_t reg_scratch_rt(int M, int TS) { return (size_t)(32 / TS) * (M + (M & 1)); }
 static size_t reg_smem(int M, int TS) {
   return sizeof(Tab) + ((size_t)M * (M + (M & 1)) + (kThreads / 32) * reg_scratch_rt(M, TS)) * sizeof(double);
+}
+static size_t level_reg_smem(const LevelDev& Lv) {
+  if (Lv.row) return sizeof(Tab) + (size_t)Lv.M * Lv.M * sizeof(double);
+  return reg_smem(Lv.M, Lv.ts);
 }
 static size_t list_smem(int m, int G) {
   return sizeof(Tab) + (size_t)(kThreads / 32) * (32 / G) * m * (sizeof(double) + sizeof(int));
@@ -647,7 +672,7 @@ static int launch_cellop(fcm_mg* h, int q, const CellOp& op) {
   }
   if (nb_reg > 0) {
     void* args[] = {&o};
-    e = cudaLaunchKernel(Lv.kreg, dim3(nb_reg), dim3(kThreads), args, reg_smem(Lv.M, Lv.ts), h->stream);
+    e = cudaLaunchKernel(Lv.kreg, dim3(nb_reg), dim3(kThreads), args, level_reg_smem(Lv), h->stream);
     h->count();
     if (e != cudaSuccess) return fail(FCM_ECUDA, "regular kernel launch: %s", cudaGetErrorString(e));
   }
@@ -1467,8 +1492,9 @@ static int setup_impl(const fcm_grid* g, const fcm_params* prm, const fcm_slab* 
     const LevelTable& T = L.tables[q];
     Lv.q = q; Lv.m = T.m; Lv.ndof = T.ndof; Lv.G = group_size(T.m);
     const bool ts1 = getenv("FCM_TS1") && atoi(getenv("FCM_TS1")) > 0;
-    Lv.kreg = reg_kernel(T.m, &Lv.M, ts1);
-    Lv.ts = (ts1 || Lv.M == 0) ? 1 : split_rt(Lv.M);
+    Lv.row = !(getenv("FCM_CELL_ROW") && atoi(getenv("FCM_CELL_ROW")) == 0);
+    Lv.kreg = reg_kernel(T.m, &Lv.M, ts1, Lv.row);
+    Lv.ts = (ts1 || Lv.M == 0) ? 1 : (Lv.row ? (Lv.M <= 8 ? 1 : (Lv.M <= 16 ? 2 : 4)) : split_rt(Lv.M));
     for (int i = 0; i < 3; ++i) {
       Lv.ilo[i] = 0;
       Lv.ihi[i] = L.n[i] - 1;
@@ -1478,7 +1504,7 @@ static int setup_impl(const fcm_grid* g, const fcm_params* prm, const fcm_slab* 
       }
     }
     Lv.klist = list_kernel(Lv.G);
-    if (Lv.kreg) CU(cudaFuncSetAttribute(Lv.kreg, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)reg_smem(Lv.M, Lv.ts)));
+    if (Lv.kreg) CU(cudaFuncSetAttribute(Lv.kreg, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)level_reg_smem(Lv)));
     CU(cudaFuncSetAttribute(Lv.klist, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)list_smem(Lv.m, Lv.G)));
     Lv.omega = q >= 2 ? prm->omega : 1.0;
     RC(h->alloc(&Lv.base, T.m));
