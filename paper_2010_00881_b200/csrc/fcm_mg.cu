@@ -84,6 +84,9 @@ struct LevelDev {
   int ilo[3] = {0, 0, 0}, ihi[3] = {-1, -1, -1};  // cells with no Dirichlet DOF
   int ts = 1;                      // threads per cell of the regular path
   bool row = true;                 // regular path = k_cell_row (one thread per cell)
+  const void* kfused = nullptr;    // k_cellop<M, G>: both populations in one launch
+  const void* kparam = nullptr;    // k_cellop_p<M, G>: same, shared matrix in the parameter bank
+  std::vector<double> Kp, Tp;      // host copies of the shared matrices (row-major M x M)
   std::vector<int32_t> blk_h;      // host copy of blk (tiled coarse setup)
   // patchwise blocks (blocks.cuh): anchors are grid vertices, blk is per anchor
   bool patch = false;
@@ -245,7 +248,66 @@ __global__ void __launch_bounds__(kThreads) k_cell_row(CellOp op) {
     Ms[e] = (op.mode == OP_APPLY) ? op.Kref[a * op.ldK + b] : op.type_inv[a * M + b];  // type slot 0
   }
   __syncthreads();
-  const double e = row_cells<M, row_split<M>()>(op, T, Ms);
+  const double e = row_cells<M, row_split<M>()>(op, T, Ms, blockIdx.x, gridDim.x);
+  if (op.partials) {
+    const double t = block_sum(e, red);
+    if (threadIdx.x == 0) op.partials[blockIdx.x] = t;
+  }
+}
+
+// One launch for both populations: blocks [0, nb_reg) stream the regular cells (row_cells),
+// the others the individual list (list_cells); smem [Tab][max(Ms: M*M, list scratch)].
+template <int M, int G>
+__global__ void __launch_bounds__(kThreads) k_cellop(CellOp op, int nb_reg) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  Tab& T = *reinterpret_cast<Tab*>(smem);
+  double* Ms = reinterpret_cast<double*>(smem + sizeof(Tab));
+  __shared__ double red[32];
+  load_tab(T, op);
+  double e;
+  if ((int)blockIdx.x < nb_reg) {
+    for (int t = threadIdx.x; t < M * M; t += blockDim.x) {
+      const int a = t / M, b = t % M;
+      Ms[t] = (op.mode == OP_APPLY) ? op.Kref[a * op.ldK + b] : op.type_inv[a * M + b];  // type slot 0
+    }
+    __syncthreads();
+    e = row_cells<M, row_split<M>()>(op, T, Ms, blockIdx.x, nb_reg);
+  } else {
+    constexpr int CPW = 32 / G;
+    const int wpb = blockDim.x >> 5;
+    double* xs0 = Ms;
+    double* xs = xs0 + (threadIdx.x >> 5) * CPW * op.m;
+    int* ids = reinterpret_cast<int*>(xs0 + wpb * CPW * op.m) + (threadIdx.x >> 5) * CPW * op.m;
+    __syncthreads();
+    e = list_cells<G, false>(op, T, (blockIdx.x - nb_reg) * wpb + (threadIdx.x >> 5),
+                             (gridDim.x - nb_reg) * wpb, xs, ids);
+  }
+  if (op.partials) {
+    const double t = block_sum(e, red);
+    if (threadIdx.x == 0) op.partials[blockIdx.x] = t;
+  }
+}
+
+// Same with the shared matrix in the parameter bank (param_cells); smem [Tab][list scratch]
+template <int M, int G>
+__global__ void __launch_bounds__(kThreads) k_cellop_p(CellOp op, int nb_reg, MatParam<M> P) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  Tab& T = *reinterpret_cast<Tab*>(smem);
+  __shared__ double red[32];
+  load_tab(T, op);
+  __syncthreads();
+  double e;
+  if ((int)blockIdx.x < nb_reg) {
+    e = param_cells<M>(op, T, P, blockIdx.x, nb_reg);
+  } else {
+    constexpr int CPW = 32 / G;
+    const int wpb = blockDim.x >> 5;
+    double* xs0 = reinterpret_cast<double*>(smem + sizeof(Tab));
+    double* xs = xs0 + (threadIdx.x >> 5) * CPW * op.m;
+    int* ids = reinterpret_cast<int*>(xs0 + wpb * CPW * op.m) + (threadIdx.x >> 5) * CPW * op.m;
+    e = list_cells<G, false>(op, T, (blockIdx.x - nb_reg) * wpb + (threadIdx.x >> 5),
+                             (gridDim.x - nb_reg) * wpb, xs, ids);
+  }
   if (op.partials) {
     const double t = block_sum(e, red);
     if (threadIdx.x == 0) op.partials[blockIdx.x] = t;
@@ -539,6 +601,18 @@ const void* reg_kernel(int m, int* M_out, bool ts1, bool row) {
   *M_out = 0;
   return nullptr;
 }
+const void* param_kernel(int m) {
+#define CASE(MM) case MM: return (const void*)k_cellop_p<MM, gsz<MM>()>;
+  switch (m) { FCM_FOR_M(CASE) default: break; }
+#undef CASE
+  return nullptr;
+}
+const void* fused_kernel(int m) {
+#define CASE(MM) case MM: return (const void*)k_cellop<MM, gsz<MM>()>;
+  switch (m) { FCM_FOR_M(CASE) default: break; }
+#undef CASE
+  return nullptr;
+}
 const void* list_kernel(int G) {
   switch (G) {
     case 4: return (const void*)k_cell_list<4>;
@@ -577,6 +651,7 @@ inline int grid_for(int64_t n, int sms) {
 // =========================================================================================
 // host helpers
 // =========================================================================================
+static int gsz_rt(int M) { return M <= 4 ? 4 : (M <= 8 ? 8 : (M <= 16 ? 16 : 32)); }  // = gsz<M>()
 static int group_size(int m) {
   if (m <= 4) return 4;
   if (m <= 8) return 8;
@@ -633,7 +708,8 @@ static void cellop_grid(const fcm_mg* h, int q, int mode, int* nb_reg, int* nb_l
   const int64_t cap = (int64_t)h->num_sms * 8;
   const int64_t cpb = (kThreads / 32) * (32 / Lv.G);  // cells per block on the list path
   if (Lv.M > 0) {
-    const int64_t ts = Lv.ts;
+    const bool param = Lv.kparam && (mode == OP_APPLY ? !Lv.Kp.empty() : !Lv.Tp.empty());
+    const int64_t ts = param ? 1 : Lv.ts;
     const int64_t cells_per_blk = (kThreads / 32) * (32 / ts);
     *nb_reg = (int)std::min<int64_t>((h->ncell + cells_per_blk - 1) / cells_per_blk, cap);
     const int64_t nl = mode == OP_APPLY ? h->ncut : Lv.n_irr;
@@ -656,6 +732,27 @@ static int launch_cellop(fcm_mg* h, int q, const CellOp& op) {
   int nb_reg, nb_list;
   cellop_grid(h, q, op.mode, &nb_reg, &nb_list);
   CellOp o = op;
+  if (Lv.kparam && (op.mode == OP_APPLY ? !Lv.Kp.empty() : !Lv.Tp.empty())) {
+    const int nb_r = nb_reg;   // one thread per cell (cellop_grid)
+    alignas(16) unsigned char pbuf[8 * 40 * 40];
+    const std::vector<double>& src = op.mode == OP_APPLY ? Lv.Kp : Lv.Tp;
+    std::memcpy(pbuf, src.data(), src.size() * 8);
+    int nbr = nb_r;
+    void* args[] = {&o, &nbr, pbuf};
+    cudaError_t e = cudaLaunchKernel(Lv.kparam, dim3(nb_r + nb_list), dim3(kThreads), args,
+                                     list_smem(Lv.m, Lv.G), h->stream);
+    h->count();
+    if (e != cudaSuccess) return fail(FCM_ECUDA, "cell kernel launch: %s", cudaGetErrorString(e));
+    return FCM_OK;
+  }
+  if (Lv.kfused) {   // one launch, heterogeneous blocks
+    void* args[] = {&o, &nb_reg};
+    const size_t sm = std::max(level_reg_smem(Lv), list_smem(Lv.m, Lv.G));
+    cudaError_t e = cudaLaunchKernel(Lv.kfused, dim3(nb_reg + nb_list), dim3(kThreads), args, sm, h->stream);
+    h->count();
+    if (e != cudaSuccess) return fail(FCM_ECUDA, "cell kernel launch: %s", cudaGetErrorString(e));
+    return FCM_OK;
+  }
   int off = nb_reg;
   cudaError_t e = cudaSuccess;
   const bool fork = nb_reg > 0 && nb_list > 0;
@@ -1200,6 +1297,10 @@ static int setup_schwarz(fcm_mg* h, int q, const std::vector<uint8_t>& kind,
   Lv.nanchor = nanchor;
   Lv.has_as = true;
   Lv.n_types = (int32_t)ntypes;
+  if (Lv.kparam && !patch && ntypes > 0 && mb == Lv.M) {   // slot-0 inverse for the parameter bank
+    Lv.Tp.resize((size_t)mb * mb);
+    CU(cudaMemcpy(Lv.Tp.data(), Lv.type_inv, Lv.Tp.size() * 8, cudaMemcpyDeviceToHost));
+  }
   Lv.blk_h = blk;
   CU(cudaStreamSynchronize(h->stream));
   return FCM_OK;
@@ -1504,6 +1605,23 @@ static int setup_impl(const fcm_grid* g, const fcm_params* prm, const fcm_slab* 
       }
     }
     Lv.klist = list_kernel(Lv.G);
+    if (Lv.M > 0 && Lv.M <= 40 && gsz_rt(Lv.M) == Lv.G &&
+        !(getenv("FCM_CELL_PARAM") && atoi(getenv("FCM_CELL_PARAM")) == 0)) {
+      Lv.kparam = param_kernel(Lv.M);
+      if (Lv.kparam) {
+        CU(cudaFuncSetAttribute(Lv.kparam, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)list_smem(Lv.m, Lv.G)));
+        Lv.Kp.resize((size_t)Lv.M * Lv.M);
+        for (int a = 0; a < Lv.M; ++a)
+          for (int b = 0; b < Lv.M; ++b) Lv.Kp[(size_t)a * Lv.M + b] = K_ref[(size_t)a * m + b];
+      }
+    }
+    if (Lv.row && Lv.M > 0 && !(getenv("FCM_CELL_FUSED") && atoi(getenv("FCM_CELL_FUSED")) == 0)) {
+      Lv.kfused = fused_kernel(Lv.M);
+      if (Lv.kfused && gsz_rt(Lv.M) != Lv.G) Lv.kfused = nullptr;
+      if (Lv.kfused)
+        CU(cudaFuncSetAttribute(Lv.kfused, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)std::max(level_reg_smem(Lv), list_smem(Lv.m, Lv.G))));
+    }
     if (Lv.kreg) CU(cudaFuncSetAttribute(Lv.kreg, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)level_reg_smem(Lv)));
     CU(cudaFuncSetAttribute(Lv.klist, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)list_smem(Lv.m, Lv.G)));
     Lv.omega = q >= 2 ? prm->omega : 1.0;
