@@ -259,3 +259,37 @@ def test_single_rank_slab_setup_matches_single_gpu():
     x1, it1, _ = S1.pcg_solve(b1)
     x2, it2, _ = S2.pcg_solve(b2)
     assert it1 == it2 and rel(x2.cpu().numpy(), x1.cpu().numpy()) <= 1e-12
+
+
+@pytest.mark.slow
+def test_cfg2_full_size():
+    # BASELINE configs[1] at full size, in the launch configuration bench.py times: the operator
+    # on every DOF against the oracle's CSR matrix, the coarse solve and one V-cycle against the
+    # oracle, and the final FCG solution's true residual through the ORACLE's operator
+    from paper_2010_00881_b200.fcm import Solver, generate
+    cfg = get_config("cfg2")
+    pair = Pair(cfg)
+    H = pair.hier()
+    rng = np.random.default_rng(3)
+    x = rng.standard_normal(pair.P.dof.ndof)
+    y = pair.from_gpu(pair.S.apply(pair.to_gpu(x)))
+    assert rel(y, pair.P.A @ x) <= 1e-13
+    I1 = pair.P.dof.level_dofs(1)
+    r1 = np.zeros(pair.P.dof.ndof)
+    r1[I1] = pair.P.b[I1]
+    ref = np.zeros_like(r1)
+    ref[I1] = H.coarse_solve(r1[I1])
+    xc, it = pair.S.coarse_solve(pair.to_gpu(r1, 1))
+    assert rel(pair.from_gpu(xc, 1), ref) <= 1e-10 and abs(it - H.coarse_iters[-1]) <= 1
+    z = pair.from_gpu(pair.S.vcycle(pair.to_gpu(pair.P.b)))
+    assert rel(z, H.vcycle(pair.P.b)) <= 1e-10
+    # the product path end to end (generator -> setup -> load -> FCG) at full size
+    G = generate(cfg)
+    S = Solver.from_problem(cfg, G)
+    b = S.load(G)
+    assert rel(b.cpu().numpy(), pair.P.b[pair.pos]) <= 1e-12
+    xs, its, hist = S.pcg_solve(b)
+    xo = np.zeros(pair.P.dof.ndof)
+    xo[pair.pos] = xs.cpu().numpy()
+    true_res = np.linalg.norm(pair.P.b - pair.P.A @ xo) / np.linalg.norm(pair.P.b)
+    assert hist[-1] < 1e-10 and true_res < 2e-10 and 25 <= its <= 50
