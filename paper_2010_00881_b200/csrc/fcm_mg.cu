@@ -28,6 +28,7 @@
 #include "coarse.cuh"
 #include "coarse_tiled.cuh"
 #include "blocks.cuh"
+#include "cellmma.cuh"
 #include "common.hpp"
 #include "layout.hpp"
 #include "nccl_dl.hpp"
@@ -86,6 +87,13 @@ struct LevelDev {
   bool row = true;                 // regular path = k_cell_row (one thread per cell)
   const void* kfused = nullptr;    // k_cellop<M, G>: both populations in one launch
   const void* kparam = nullptr;    // k_cellop_p<M, G>: same, shared matrix in the parameter bank
+  const void* kmma = nullptr;      // k_cell_mma<M>: regular cells as fp64 tensor-core MMAs
+  int32_t* gA_cells = nullptr;     // apply groups (8 non-cut cells, K_ref)
+  int32_t* gA_mat = nullptr;
+  int64_t nA = 0;
+  int32_t* gS_cells = nullptr;     // smoother groups (8 regular cells of one type slot)
+  int32_t* gS_mat = nullptr;
+  int64_t nS = 0;
   std::vector<double> Kp, Tp;      // host copies of the shared matrices (row-major M x M)
   std::vector<int32_t> blk_h;      // host copy of blk (tiled coarse setup)
   // patchwise blocks (blocks.cuh): anchors are grid vertices, blk is per anchor
@@ -285,6 +293,22 @@ __global__ void __launch_bounds__(kThreads) k_cellop(CellOp op, int nb_reg) {
   if (op.partials) {
     const double t = block_sum(e, red);
     if (threadIdx.x == 0) op.partials[blockIdx.x] = t;
+  }
+}
+
+// Regular cells as fp64 tensor-core MMAs (cellmma.cuh); smem [Tab]
+template <int M>
+__global__ void __launch_bounds__(kThreads) k_cell_mma(MmaOp g) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  Tab& T = *reinterpret_cast<Tab*>(smem);
+  __shared__ double red[32];
+  load_tab(T, g.op);
+  __syncthreads();
+  const int wpb = blockDim.x >> 5;
+  const double e = mma_cells<M>(g, T, blockIdx.x * wpb + (threadIdx.x >> 5), gridDim.x * wpb);
+  if (g.op.partials) {
+    const double t = block_sum(e, red);
+    if (threadIdx.x == 0) g.op.partials[blockIdx.x] = t;
   }
 }
 
@@ -601,6 +625,18 @@ const void* reg_kernel(int m, int* M_out, bool ts1, bool row) {
   *M_out = 0;
   return nullptr;
 }
+const void* mma_kernel(int m) {
+  switch (m) {
+    case 4: return (const void*)k_cell_mma<4>;
+    case 8: return (const void*)k_cell_mma<8>;
+    case 9: return (const void*)k_cell_mma<9>;
+    case 16: return (const void*)k_cell_mma<16>;
+    case 24: return (const void*)k_cell_mma<24>;
+    case 25: return (const void*)k_cell_mma<25>;
+    case 27: return (const void*)k_cell_mma<27>;
+    default: return nullptr;
+  }
+}
 const void* param_kernel(int m) {
 #define CASE(MM) case MM: return (const void*)k_cellop_p<MM, gsz<MM>()>;
   switch (m) { FCM_FOR_M(CASE) default: break; }
@@ -707,6 +743,14 @@ static void cellop_grid(const fcm_mg* h, int q, int mode, int* nb_reg, int* nb_l
   const LevelDev& Lv = h->lev[q];
   const int64_t cap = (int64_t)h->num_sms * 8;
   const int64_t cpb = (kThreads / 32) * (32 / Lv.G);  // cells per block on the list path
+  const bool mma = Lv.kmma && (mode == OP_APPLY ? Lv.gA_cells != nullptr : Lv.gS_cells != nullptr);
+  if (mma) {
+    const int64_t ng = mode == OP_APPLY ? Lv.nA : Lv.nS;
+    *nb_reg = (int)std::max<int64_t>(1, std::min<int64_t>((ng + kThreads / 32 - 1) / (kThreads / 32), cap));
+    const int64_t nl = mode == OP_APPLY ? h->ncut : Lv.n_irr;
+    *nb_list = (int)std::min<int64_t>((nl + cpb - 1) / cpb, cap);
+    return;
+  }
   if (Lv.M > 0) {
     const bool param = Lv.kparam && (mode == OP_APPLY ? !Lv.Kp.empty() : !Lv.Tp.empty());
     const int64_t ts = param ? 1 : Lv.ts;
@@ -732,17 +776,62 @@ static int launch_cellop(fcm_mg* h, int q, const CellOp& op) {
   int nb_reg, nb_list;
   cellop_grid(h, q, op.mode, &nb_reg, &nb_list);
   CellOp o = op;
+  if (Lv.kmma && (op.mode == OP_APPLY ? Lv.gA_cells != nullptr : Lv.gS_cells != nullptr)) {
+    // regular cells: fp64 MMA groups on the main stream, the individual list concurrently
+    const bool fork = nb_list > 0;
+    if (fork) {
+      CU(cudaEventRecord(h->ev_fork, h->stream));
+      CU(cudaStreamWaitEvent(h->stream2, h->ev_fork, 0));
+      int off = nb_reg;
+      void* largs[] = {&o, &off};
+      cudaError_t e = cudaLaunchKernel(Lv.klist, dim3(nb_list), dim3(kThreads), largs, list_smem(Lv.m, Lv.G), h->stream2);
+      h->count();
+      if (e != cudaSuccess) return fail(FCM_ECUDA, "list kernel launch: %s", cudaGetErrorString(e));
+    }
+    MmaOp g{};
+    g.op = o;
+    if (op.mode == OP_APPLY) { g.grp_cells = Lv.gA_cells; g.grp_mat = Lv.gA_mat; g.ngroups = Lv.nA; }
+    else { g.grp_cells = Lv.gS_cells; g.grp_mat = Lv.gS_mat; g.ngroups = Lv.nS; }
+    void* args[] = {&g};
+    cudaError_t e = cudaLaunchKernel(Lv.kmma, dim3(nb_reg), dim3(kThreads), args, sizeof(Tab), h->stream);
+    h->count();
+    if (e != cudaSuccess) return fail(FCM_ECUDA, "mma kernel launch: %s", cudaGetErrorString(e));
+    if (fork) {
+      CU(cudaEventRecord(h->ev_join, h->stream2));
+      CU(cudaStreamWaitEvent(h->stream, h->ev_join, 0));
+    }
+    return FCM_OK;
+  }
   if (Lv.kparam && (op.mode == OP_APPLY ? !Lv.Kp.empty() : !Lv.Tp.empty())) {
-    const int nb_r = nb_reg;   // one thread per cell (cellop_grid)
+    // regular cells: parameter-bank kernel (many registers, one block per SM) on the main
+    // stream; the individual list concurrently on the forked branch (few registers, so it
+    // fills the remaining warp slots instead of queueing behind the regular blocks)
     alignas(16) unsigned char pbuf[8 * 40 * 40];
     const std::vector<double>& src = op.mode == OP_APPLY ? Lv.Kp : Lv.Tp;
     std::memcpy(pbuf, src.data(), src.size() * 8);
-    int nbr = nb_r;
+    const int dbg_skip = getenv("FCM_DEBUG_SKIP") ? atoi(getenv("FCM_DEBUG_SKIP")) : 0;  // timing only
+    if (dbg_skip & 2) nb_list = 0;
+    const bool fork = nb_list > 0;
+    if (fork) {
+      CU(cudaEventRecord(h->ev_fork, h->stream));
+      CU(cudaStreamWaitEvent(h->stream2, h->ev_fork, 0));
+      int off = nb_reg;
+      void* largs[] = {&o, &off};
+      cudaError_t e = cudaLaunchKernel(Lv.klist, dim3(nb_list), dim3(kThreads), largs, list_smem(Lv.m, Lv.G), h->stream2);
+      h->count();
+      if (e != cudaSuccess) return fail(FCM_ECUDA, "list kernel launch: %s", cudaGetErrorString(e));
+    }
+    int nbr = nb_reg;
     void* args[] = {&o, &nbr, pbuf};
-    cudaError_t e = cudaLaunchKernel(Lv.kparam, dim3(nb_r + nb_list), dim3(kThreads), args,
-                                     list_smem(Lv.m, Lv.G), h->stream);
-    h->count();
-    if (e != cudaSuccess) return fail(FCM_ECUDA, "cell kernel launch: %s", cudaGetErrorString(e));
+    if (!(dbg_skip & 1)) {
+      cudaError_t e = cudaLaunchKernel(Lv.kparam, dim3(nb_reg), dim3(kThreads), args, list_smem(Lv.m, Lv.G), h->stream);
+      h->count();
+      if (e != cudaSuccess) return fail(FCM_ECUDA, "cell kernel launch: %s", cudaGetErrorString(e));
+    }
+    if (fork) {
+      CU(cudaEventRecord(h->ev_join, h->stream2));
+      CU(cudaStreamWaitEvent(h->stream, h->ev_join, 0));
+    }
     return FCM_OK;
   }
   if (Lv.kfused) {   // one launch, heterogeneous blocks
@@ -1297,6 +1386,26 @@ static int setup_schwarz(fcm_mg* h, int q, const std::vector<uint8_t>& kind,
   Lv.nanchor = nanchor;
   Lv.has_as = true;
   Lv.n_types = (int32_t)ntypes;
+  if (Lv.kmma && !patch && mb == Lv.M) {   // MMA groups: 8 regular cells of one type slot
+    std::vector<std::vector<int32_t>> by_slot(ntypes);
+    for (int64_t A = 0; A < nanchor; ++A)
+      if (blk[A] < 0 && blk[A] != kBlkNone) by_slot[(-blk[A] - 1) & 0xfff].push_back((int32_t)A);
+    std::vector<int32_t> gc, gm;
+    for (int64_t t = 0; t < ntypes; ++t) {
+      auto& v = by_slot[t];
+      for (size_t i = 0; i < v.size(); i += 8) {
+        for (size_t j = 0; j < 8; ++j) gc.push_back(i + j < v.size() ? v[i + j] : -1);
+        gm.push_back((int32_t)t);
+      }
+    }
+    Lv.nS = (int64_t)gm.size();
+    RC(h->alloc(&Lv.gS_cells, std::max<size_t>(gc.size(), 1)));
+    RC(h->alloc(&Lv.gS_mat, std::max<size_t>(gm.size(), 1)));
+    if (!gc.empty()) {
+      CU(cudaMemcpyAsync(Lv.gS_cells, gc.data(), gc.size() * 4, cudaMemcpyHostToDevice, h->stream));
+      CU(cudaMemcpyAsync(Lv.gS_mat, gm.data(), gm.size() * 4, cudaMemcpyHostToDevice, h->stream));
+    }
+  }
   if (Lv.kparam && !patch && ntypes > 0 && mb == Lv.M) {   // slot-0 inverse for the parameter bank
     Lv.Tp.resize((size_t)mb * mb);
     CU(cudaMemcpy(Lv.Tp.data(), Lv.type_inv, Lv.Tp.size() * 8, cudaMemcpyDeviceToHost));
@@ -1605,6 +1714,23 @@ static int setup_impl(const fcm_grid* g, const fcm_params* prm, const fcm_slab* 
       }
     }
     Lv.klist = list_kernel(Lv.G);
+    if (Lv.M > 0 && !(getenv("FCM_CELL_MMA") && atoi(getenv("FCM_CELL_MMA")) == 0)) {
+      Lv.kmma = mma_kernel(Lv.M);
+      if (Lv.kmma) {
+        CU(cudaFuncSetAttribute(Lv.kmma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(Tab)));
+        std::vector<int32_t> gc, gm;
+        for (int64_t c = 0; c < h->ncell; ++c)
+          if (kind_own[c] != 2) gc.push_back((int32_t)c);
+        while (gc.size() % 8) gc.push_back(-1);
+        Lv.nA = (int64_t)gc.size() / 8;
+        gm.assign(Lv.nA, -1);
+        RC(h->alloc(&Lv.gA_cells, gc.size()));
+        RC(h->alloc(&Lv.gA_mat, gm.size()));
+        CU(cudaMemcpyAsync(Lv.gA_cells, gc.data(), gc.size() * 4, cudaMemcpyHostToDevice, h->stream));
+        CU(cudaMemcpyAsync(Lv.gA_mat, gm.data(), gm.size() * 4, cudaMemcpyHostToDevice, h->stream));
+        CU(cudaStreamSynchronize(h->stream));
+      }
+    }
     if (Lv.M > 0 && Lv.M <= 40 && gsz_rt(Lv.M) == Lv.G &&
         !(getenv("FCM_CELL_PARAM") && atoi(getenv("FCM_CELL_PARAM")) == 0)) {
       Lv.kparam = param_kernel(Lv.M);
