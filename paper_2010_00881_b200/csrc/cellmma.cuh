@@ -14,11 +14,20 @@
 
 namespace fcm {
 
+// group cell entry: cx | cy << 10 | cz << 20 | inner << 30 (inner: no Dirichlet DOF in the
+// cell, so no validity test), or -1 for padding; coordinates < 1024 per axis
+constexpr int kMmaInner = 1 << 30;
+
 struct MmaOp {
   CellOp op;                 // table / vectors / scales (op.mode selects kind vs blk scaling)
-  const int32_t* grp_cells;  // [ngroups][8] cell indices (-1 padding)
+  const int32_t* grp_cells;  // [ngroups][8] packed cell coordinates (see kMmaInner), -1 padding
   const int32_t* grp_mat;    // [ngroups] matrix slot: -1 = K_ref leading block, >= 0 type slot
   int64_t ngroups;
+  // fused copy cp_dst[0..cp_n) = cp_src (the next residual's "r = b"; cp_dst is not touched by
+  // the cell work of this launch), done by every block in a grid-stride loop
+  const double* cp_src;
+  double* cp_dst;
+  int64_t cp_n;
 };
 
 __device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, double b, double c0, double c1) {
@@ -28,65 +37,80 @@ __device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, dou
 }
 
 // cell scale: apply -> 1 or alpha (kind), smooth -> 1 or 1/alpha (type flag)
-__device__ __forceinline__ double cell_scale(const CellOp& op, int c) {
-  if (c < 0) return 0.0;
+__device__ __forceinline__ double cell_scale(const CellOp& op, int pc) {
+  if (pc < 0) return 0.0;
+  const int c = (pc & 1023) + op.nx * (((pc >> 10) & 1023) + op.ny * ((pc >> 20) & 1023));
   if (op.mode == OP_APPLY) return op.kind[c] == 1 ? op.alpha : 1.0;
   const int t = -op.blk[c] - 1;
   return (t >> 12) ? op.inv_alpha : 1.0;
 }
 
+// layout index of local DOF a of the packed cell pc, or -1 (padding / a >= M / Dirichlet)
 template <int M>
-__device__ __forceinline__ int mma_dof_index(const Tab& T, int a, int c, const CellOp& op) {
-  if (c < 0 || a >= M) return -1;
-  const int cx = c % op.nx, cyz = c / op.nx, cy = cyz % op.ny, cz = cyz / op.ny;
-  if (!dof_free(T, a, cx, cy, cz)) return -1;
+__device__ __forceinline__ int mma_dof_index(const Tab& T, int a, int pc) {
+  if (pc < 0 || a >= M) return -1;
+  const int cx = pc & 1023, cy = (pc >> 10) & 1023, cz = (pc >> 20) & 1023;
+  if (!(pc & kMmaInner) && !dof_free(T, a, cx, cy, cz)) return -1;
   return dof_index(T, a, cx, cy, cz);
 }
 
-// One warp per group of 8 cells (grid-stride over groups, groups sorted by matrix).
+// One warp per group of 8 cells (grid-stride over groups, groups sorted by matrix).  The
+// block's main matrix (K_ref's leading block for the apply, type slot 0 for the smoother) is
+// staged once per block in shared memory in FRAGMENT order (As[(rt*KT + kt)*32 + lane]), so
+// every MMA reads its A fragment with one conflict-free LDS.64 and the registers stay few
+// (4 blocks per SM); groups of other types read their fragments through L1.
 template <int M>
-__device__ __forceinline__ double mma_cells(const MmaOp& g, const Tab& T, int warp, int nwarps) {
+__device__ __forceinline__ void stage_fragments(double* As, const double* K, int ld) {
+  constexpr int MT = (M + 7) / 8, KT = (M + 3) / 4;
+  for (int t = threadIdx.x; t < MT * KT * 32; t += blockDim.x) {
+    const int lane = t & 31, f = t >> 5, rt = f / KT, kt = f % KT;
+    const int r = rt * 8 + (lane >> 2), k = kt * 4 + (lane & 3);
+    As[t] = (r < M && k < M) ? K[r * ld + k] : 0.0;
+  }
+}
+
+template <int M>
+__device__ __forceinline__ double mma_cells(const MmaOp& g, const Tab& T, const double* __restrict__ As,
+                                            int main_slot, int warp, int nwarps) {
   constexpr int MT = (M + 7) / 8;   // row tiles
   constexpr int KT = (M + 3) / 4;   // k tiles
   const CellOp& op = g.op;
   const int lane = threadIdx.x & 31;
   const int ar = lane >> 2, ac = lane & 3;
-  double A[MT][KT];
-  int cur = -2;   // matrix slot held in A
   double energy = 0.0;
   const bool want_e = op.partials != nullptr;
   for (int64_t gi = warp; gi < g.ngroups; gi += nwarps) {
     const int slot = __ldg(g.grp_mat + gi);   // warp-uniform
-    if (slot != cur) {
-      const double* K = slot < 0 ? op.Kref : op.type_inv + (size_t)slot * M * M;
-      const int ld = slot < 0 ? op.ldK : M;
-#pragma unroll
-      for (int rt = 0; rt < MT; ++rt)
-#pragma unroll
-        for (int kt = 0; kt < KT; ++kt) {
-          const int r = rt * 8 + ar, k = kt * 4 + ac;
-          A[rt][kt] = (r < M && k < M) ? __ldg(K + r * ld + k) : 0.0;
-        }
-      cur = slot;
-    }
     const int* cells = g.grp_cells + gi * 8;
     const int cg = __ldg(cells + ar);            // B column / gather cell of this lane
+    const int c0 = __ldg(cells + 2 * ac), c1 = __ldg(cells + 2 * ac + 1);   // output cells
     // gather: B[kt] = x[dof kt*4 + ac] of cell cg
     double B[KT];
 #pragma unroll
     for (int kt = 0; kt < KT; ++kt) {
-      const int idx = mma_dof_index<M>(T, kt * 4 + ac, cg, op);
+      const int idx = mma_dof_index<M>(T, kt * 4 + ac, cg);
       B[kt] = idx >= 0 ? __ldg(op.in + idx) : 0.0;
     }
-    const int c0 = __ldg(cells + 2 * ac), c1 = __ldg(cells + 2 * ac + 1);   // output cells
     const double s0 = op.coef * cell_scale(op, c0), s1 = op.coef * cell_scale(op, c1);
+    const bool main = slot == main_slot;
+    const double* K = slot < 0 ? op.Kref : op.type_inv + (size_t)slot * M * M;
+    const int ld = slot < 0 ? op.ldK : M;
 #pragma unroll
     for (int rt = 0; rt < MT; ++rt) {
       double d0 = 0.0, d1 = 0.0;
 #pragma unroll
-      for (int kt = 0; kt < KT; ++kt) dmma_8x8x4(d0, d1, A[rt][kt], B[kt], d0, d1);
+      for (int kt = 0; kt < KT; ++kt) {
+        double af;
+        if (main) {
+          af = As[(rt * KT + kt) * 32 + lane];
+        } else {
+          const int r = rt * 8 + ar, k = kt * 4 + ac;
+          af = (r < M && k < M) ? __ldg(K + r * ld + k) : 0.0;
+        }
+        dmma_8x8x4(d0, d1, af, B[kt], d0, d1);
+      }
       const int a = rt * 8 + ar;
-      const int i0 = mma_dof_index<M>(T, a, c0, op), i1 = mma_dof_index<M>(T, a, c1, op);
+      const int i0 = mma_dof_index<M>(T, a, c0), i1 = mma_dof_index<M>(T, a, c1);
       if (i0 >= 0) {
         atomicAdd(op.out + i0, s0 * d0);
         if (want_e) energy = fma(__ldg(op.in + i0), s0 / op.coef * d0, energy);

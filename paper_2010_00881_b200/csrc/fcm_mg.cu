@@ -110,6 +110,7 @@ struct LevelDev {
   int32_t* hi_idx = nullptr;
   int64_t n_lo = 0, n_hi = 0;
   double* d = nullptr;
+  double* r2 = nullptr;            // second residual buffer (fused-copy V-cycle)
   // vectors
   double* x = nullptr;
   double* r = nullptr;
@@ -297,15 +298,33 @@ __global__ void __launch_bounds__(kThreads) k_cellop(CellOp op, int nb_reg) {
 }
 
 // Regular cells as fp64 tensor-core MMAs (cellmma.cuh); smem [Tab]
-template <int M>
-__global__ void __launch_bounds__(kThreads) k_cell_mma(MmaOp g) {
+// One launch per cell operation: blocks [0, nb_mma) run the regular cells as fp64 MMAs
+// (cellmma.cuh), the others the individual list (list_cells); every block also does its share
+// of the fused copy.  smem [Tab][max(A fragments, list scratch)].
+template <int M, int G>
+__global__ void __launch_bounds__(kThreads, 4) k_cell_mma(MmaOp g, int nb_mma) {
   extern __shared__ __align__(16) unsigned char smem[];
   Tab& T = *reinterpret_cast<Tab*>(smem);
+  double* As = reinterpret_cast<double*>(smem + sizeof(Tab));
   __shared__ double red[32];
   load_tab(T, g.op);
+  const bool apply = g.op.mode == OP_APPLY;
+  const bool is_mma = (int)blockIdx.x < nb_mma;
+  if (is_mma) stage_fragments<M>(As, apply ? g.op.Kref : g.op.type_inv, apply ? g.op.ldK : M);
   __syncthreads();
   const int wpb = blockDim.x >> 5;
-  const double e = mma_cells<M>(g, T, blockIdx.x * wpb + (threadIdx.x >> 5), gridDim.x * wpb);
+  double e;
+  if (is_mma) {
+    e = mma_cells<M>(g, T, As, apply ? -1 : 0, blockIdx.x * wpb + (threadIdx.x >> 5), nb_mma * wpb);
+  } else {
+    constexpr int CPW = 32 / G;
+    double* xs = As + (threadIdx.x >> 5) * CPW * g.op.m;
+    int* ids = reinterpret_cast<int*>(As + wpb * CPW * g.op.m) + (threadIdx.x >> 5) * CPW * g.op.m;
+    e = list_cells<G, false>(g.op, T, (blockIdx.x - nb_mma) * wpb + (threadIdx.x >> 5),
+                             (gridDim.x - nb_mma) * wpb, xs, ids);
+  }
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < g.cp_n; i += (int64_t)gridDim.x * blockDim.x)
+    g.cp_dst[i] = g.cp_src[i];
   if (g.op.partials) {
     const double t = block_sum(e, red);
     if (threadIdx.x == 0) g.op.partials[blockIdx.x] = t;
@@ -397,6 +416,14 @@ __global__ void k_fill(double* x, double v, int64_t n) {
 __global__ void k_copy(double* __restrict__ y, const double* __restrict__ x, int64_t n) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     y[i] = x[i];
+}
+// y[0..n) += a x; dst[0..ncp) = src (fused copy of an unrelated buffer)
+__global__ void k_axpy_copy(double* __restrict__ y, double a, const double* __restrict__ x, int64_t n,
+                            double* __restrict__ dst, const double* __restrict__ src, int64_t ncp) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n || i < ncp; i += (int64_t)gridDim.x * blockDim.x) {
+    if (i < n) y[i] = fma(a, x[i], y[i]);
+    if (i < ncp) dst[i] = src[i];
+  }
 }
 __global__ void k_axpy(double* __restrict__ y, double a, const double* __restrict__ x, int64_t n) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
@@ -626,16 +653,10 @@ const void* reg_kernel(int m, int* M_out, bool ts1, bool row) {
   return nullptr;
 }
 const void* mma_kernel(int m) {
-  switch (m) {
-    case 4: return (const void*)k_cell_mma<4>;
-    case 8: return (const void*)k_cell_mma<8>;
-    case 9: return (const void*)k_cell_mma<9>;
-    case 16: return (const void*)k_cell_mma<16>;
-    case 24: return (const void*)k_cell_mma<24>;
-    case 25: return (const void*)k_cell_mma<25>;
-    case 27: return (const void*)k_cell_mma<27>;
-    default: return nullptr;
-  }
+#define CASE(MM) case MM: return (const void*)k_cell_mma<MM, gsz<MM>()>;
+  switch (m) { FCM_FOR_M(CASE) default: break; }
+#undef CASE
+  return nullptr;
 }
 const void* param_kernel(int m) {
 #define CASE(MM) case MM: return (const void*)k_cellop_p<MM, gsz<MM>()>;
@@ -700,6 +721,9 @@ static size_t reg_scratch_rt(int M, int TS) { return (size_t)(32 / TS) * (M + (M
 static size_t reg_smem(int M, int TS) {
   return sizeof(Tab) + ((size_t)M * (M + (M & 1)) + (kThreads / 32) * reg_scratch_rt(M, TS)) * sizeof(double);
 }
+static size_t mma_smem(int M) {
+  return sizeof(Tab) + (size_t)((M + 7) / 8) * ((M + 3) / 4) * 32 * sizeof(double);
+}
 static size_t level_reg_smem(const LevelDev& Lv) {
   if (Lv.row) return sizeof(Tab) + (size_t)Lv.M * Lv.M * sizeof(double);
   return reg_smem(Lv.M, Lv.ts);
@@ -745,8 +769,10 @@ static void cellop_grid(const fcm_mg* h, int q, int mode, int* nb_reg, int* nb_l
   const int64_t cpb = (kThreads / 32) * (32 / Lv.G);  // cells per block on the list path
   const bool mma = Lv.kmma && (mode == OP_APPLY ? Lv.gA_cells != nullptr : Lv.gS_cells != nullptr);
   if (mma) {
+    // one resident wave (4 blocks per SM); warps loop over the groups
     const int64_t ng = mode == OP_APPLY ? Lv.nA : Lv.nS;
-    *nb_reg = (int)std::max<int64_t>(1, std::min<int64_t>((ng + kThreads / 32 - 1) / (kThreads / 32), cap));
+    *nb_reg = (int)std::max<int64_t>(1, std::min<int64_t>((ng + kThreads / 32 - 1) / (kThreads / 32),
+                                                          (int64_t)h->num_sms * 4));
     const int64_t nl = mode == OP_APPLY ? h->ncut : Lv.n_irr;
     *nb_list = (int)std::min<int64_t>((nl + cpb - 1) / cpb, cap);
     return;
@@ -771,37 +797,29 @@ static int cellop_nblocks(const fcm_mg* h, int q, int mode) {
 
 // One cell-operator application = regular kernel + individual-list kernel; the list kernel
 // runs on a forked branch (graph fork/join when captured) so both populations overlap.
-static int launch_cellop(fcm_mg* h, int q, const CellOp& op) {
+static int copy(fcm_mg* h, double* y, const double* x, int64_t n);
+static int launch_cellop(fcm_mg* h, int q, const CellOp& op, double* cp_dst = nullptr,
+                         const double* cp_src = nullptr, int64_t cp_n = 0) {
   const LevelDev& Lv = h->lev[q];
   int nb_reg, nb_list;
   cellop_grid(h, q, op.mode, &nb_reg, &nb_list);
   CellOp o = op;
   if (Lv.kmma && (op.mode == OP_APPLY ? Lv.gA_cells != nullptr : Lv.gS_cells != nullptr)) {
-    // regular cells: fp64 MMA groups on the main stream, the individual list concurrently
-    const bool fork = nb_list > 0;
-    if (fork) {
-      CU(cudaEventRecord(h->ev_fork, h->stream));
-      CU(cudaStreamWaitEvent(h->stream2, h->ev_fork, 0));
-      int off = nb_reg;
-      void* largs[] = {&o, &off};
-      cudaError_t e = cudaLaunchKernel(Lv.klist, dim3(nb_list), dim3(kThreads), largs, list_smem(Lv.m, Lv.G), h->stream2);
-      h->count();
-      if (e != cudaSuccess) return fail(FCM_ECUDA, "list kernel launch: %s", cudaGetErrorString(e));
-    }
+    // one launch: regular cells as fp64 MMA groups, the individual list in the other blocks
     MmaOp g{};
     g.op = o;
     if (op.mode == OP_APPLY) { g.grp_cells = Lv.gA_cells; g.grp_mat = Lv.gA_mat; g.ngroups = Lv.nA; }
     else { g.grp_cells = Lv.gS_cells; g.grp_mat = Lv.gS_mat; g.ngroups = Lv.nS; }
-    void* args[] = {&g};
-    cudaError_t e = cudaLaunchKernel(Lv.kmma, dim3(nb_reg), dim3(kThreads), args, sizeof(Tab), h->stream);
+    g.cp_src = cp_src; g.cp_dst = cp_dst; g.cp_n = cp_dst ? cp_n : 0;
+    int nbm = nb_reg;
+    void* args[] = {&g, &nbm};
+    cudaError_t e = cudaLaunchKernel(Lv.kmma, dim3(nb_reg + nb_list), dim3(kThreads), args,
+                                     std::max(mma_smem(Lv.M), list_smem(Lv.m, Lv.G)), h->stream);
     h->count();
     if (e != cudaSuccess) return fail(FCM_ECUDA, "mma kernel launch: %s", cudaGetErrorString(e));
-    if (fork) {
-      CU(cudaEventRecord(h->ev_join, h->stream2));
-      CU(cudaStreamWaitEvent(h->stream, h->ev_join, 0));
-    }
     return FCM_OK;
   }
+  if (cp_dst) RC(copy(h, cp_dst, cp_src, cp_n));   // other paths: the copy as its own launch
   if (Lv.kparam && (op.mode == OP_APPLY ? !Lv.Kp.empty() : !Lv.Tp.empty())) {
     // regular cells: parameter-bank kernel (many registers, one block per SM) on the main
     // stream; the individual list concurrently on the forked branch (few registers, so it
@@ -926,9 +944,9 @@ static int allreduce(fcm_mg* h, double* v, int n) {
 
 // r = b - A_q x.  Slab mode: the lower rank owns an interface DOF, so only it starts from b
 // there; the exchange then adds the two partial sums of A x (same result on both ranks).
-static int residual(fcm_mg* h, int q, const double* b, const double* x, double* r) {
+static int residual(fcm_mg* h, int q, const double* b, const double* x, double* r, bool r_is_b = false) {
   LevelDev& Lv = h->lev[q];
-  RC(copy(h, r, b, Lv.ndof));
+  if (!r_is_b) RC(copy(h, r, b, Lv.ndof));
   if (Lv.n_lo > 0) {
     k_zero_idx<<<grid_for(Lv.n_lo, h->num_sms), kThreads, 0, h->stream>>>(r, Lv.lo_idx, Lv.n_lo);
     h->count();
@@ -969,14 +987,21 @@ static int launch_block_smooth(fcm_mg* h, int q, const double* r, double* x, dou
   return FCM_OK;
 }
 
-static int smooth_into(fcm_mg* h, int q, const double* r, double* x) {
-  if (h->lev[q].patch) return launch_block_smooth(h, q, r, x, h->lev[q].omega);
-  return launch_cellop(h, q, make_op(h, q, OP_SMOOTH, r, x, h->lev[q].omega, nullptr));
+static int smooth_into(fcm_mg* h, int q, const double* r, double* x, double* cp_dst = nullptr,
+                       const double* cp_src = nullptr) {
+  if (h->lev[q].patch) {
+    RC(launch_block_smooth(h, q, r, x, h->lev[q].omega));
+    if (cp_dst) RC(copy(h, cp_dst, cp_src, h->lev[q].ndof));
+    return FCM_OK;
+  }
+  return launch_cellop(h, q, make_op(h, q, OP_SMOOTH, r, x, h->lev[q].omega, nullptr), cp_dst, cp_src,
+                       h->lev[q].ndof);
 }
 // x += omega M^-1 r.  Slab mode: the increment is exchanged (x itself is consistent), so it
 // goes through d unless x is known to be zero.
-static int smooth(fcm_mg* h, int q, const double* r, double* x, bool x_is_zero = false) {
-  if (h->nranks <= 1) return smooth_into(h, q, r, x);
+static int smooth(fcm_mg* h, int q, const double* r, double* x, bool x_is_zero = false,
+                  double* cp_dst = nullptr, const double* cp_src = nullptr) {
+  if (h->nranks <= 1) return smooth_into(h, q, r, x, cp_dst, cp_src);
   LevelDev& Lv = h->lev[q];
   if (x_is_zero) {
     RC(smooth_into(h, q, r, x));
@@ -1096,21 +1121,36 @@ static int enqueue_vcycle(fcm_mg* h, int q, const double* b, double* x) {
   if (q == 1) return enqueue_coarse(h, b, x);
   LevelDev& Lv = h->lev[q];
   const int64_t N = Lv.ndof;
+  // single GPU, elementwise MMA path: the residual is double-buffered and each smoother launch
+  // also writes "r = b" into the buffer the next residual scatters into (no copy launches)
+  const bool fuse = Lv.kmma && h->nranks == 1 && !Lv.patch && Lv.r2;
+  double* rb[2] = {Lv.r, Lv.r2 ? Lv.r2 : Lv.r};
+  int cur = 0;
   RC(fill(h, x, 0.0, N));
   for (int s = 0; s < h->prm.n_pre; ++s) {          // pre-smoothing
-    if (s == 0) RC(smooth(h, q, b, x, true));       // x = 0: r = b
-    else { RC(residual(h, q, b, x, Lv.r)); RC(smooth(h, q, Lv.r, x)); }
+    if (s == 0) {
+      RC(smooth(h, q, b, x, true, fuse ? rb[cur] : nullptr, b));   // x = 0: r = b
+    } else {
+      RC(residual(h, q, b, x, rb[cur], fuse));
+      RC(smooth(h, q, rb[cur], x, false, fuse ? rb[cur ^ 1] : nullptr, b));
+      if (fuse) cur ^= 1;
+    }
   }
-  if (h->prm.n_pre > 0) RC(residual(h, q, b, x, Lv.r));  // update residual
-  else RC(copy(h, Lv.r, b, N));
+  if (h->prm.n_pre > 0) RC(residual(h, q, b, x, rb[cur], fuse));  // update residual
+  else RC(copy(h, rb[cur], b, N));
   LevelDev& Lc = h->lev[q - 1];
-  RC(enqueue_vcycle(h, q - 1, Lv.r, Lc.x));         // r_{l-1} = R r_l: prefix alias
-  k_axpy<<<grid_for(Lc.ndof, h->num_sms), kThreads, 0, h->stream>>>(x, 1.0, Lc.x, Lc.ndof);  // x += R^T e
+  RC(enqueue_vcycle(h, q - 1, rb[cur], Lc.x));      // r_{l-1} = R r_l: prefix alias
+  // x += R^T e (and, fused path, the next residual buffer = b)
+  k_axpy_copy<<<grid_for(N, h->num_sms), kThreads, 0, h->stream>>>(x, 1.0, Lc.x, Lc.ndof, fuse ? rb[cur ^ 1] : nullptr, b,
+                                                                    fuse ? N : 0);
   h->count();
   CU(cudaGetLastError());
+  if (fuse) cur ^= 1;
   for (int s = 0; s < h->prm.n_post; ++s) {         // P:169 residual, post-smoothing
-    RC(residual(h, q, b, x, Lv.r));
-    RC(smooth(h, q, Lv.r, x));
+    RC(residual(h, q, b, x, rb[cur], fuse));
+    const bool more = s + 1 < h->prm.n_post;
+    RC(smooth(h, q, rb[cur], x, false, fuse && more ? rb[cur ^ 1] : nullptr, b));
+    if (fuse) cur ^= 1;
   }
   return FCM_OK;
 }
@@ -1227,6 +1267,16 @@ static int64_t block_dof_index(const Layout& L, int q, const BlockGeom& g, int l
     if (cc[i] < 0 || cc[i] >= L.n[i]) return -1;
   }
   return L.dof_index(q, g.loc[l], cc);
+}
+
+// packed cell entry of an MMA group (cellmma.cuh): coordinates + "no Dirichlet DOF" flag
+static int32_t mma_pack(const fcm_mg* h, int q, int64_t c) {
+  int cc[3];
+  h->L.cell_coords(c, cc);
+  const LevelDev& Lv = h->lev[q];
+  bool inner = true;
+  for (int i = 0; i < 3; ++i) inner = inner && cc[i] >= Lv.ilo[i] && cc[i] <= Lv.ihi[i];
+  return cc[0] | (cc[1] << 10) | (cc[2] << 20) | (inner ? kMmaInner : 0);
 }
 
 static int setup_schwarz(fcm_mg* h, int q, const std::vector<uint8_t>& kind,
@@ -1394,7 +1444,7 @@ static int setup_schwarz(fcm_mg* h, int q, const std::vector<uint8_t>& kind,
     for (int64_t t = 0; t < ntypes; ++t) {
       auto& v = by_slot[t];
       for (size_t i = 0; i < v.size(); i += 8) {
-        for (size_t j = 0; j < 8; ++j) gc.push_back(i + j < v.size() ? v[i + j] : -1);
+        for (size_t j = 0; j < 8; ++j) gc.push_back(i + j < v.size() ? mma_pack(h, q, v[i + j]) : -1);
         gm.push_back((int32_t)t);
       }
     }
@@ -1715,12 +1765,15 @@ static int setup_impl(const fcm_grid* g, const fcm_params* prm, const fcm_slab* 
     }
     Lv.klist = list_kernel(Lv.G);
     if (Lv.M > 0 && !(getenv("FCM_CELL_MMA") && atoi(getenv("FCM_CELL_MMA")) == 0)) {
-      Lv.kmma = mma_kernel(Lv.M);
+      Lv.kmma = gsz_rt(Lv.M) == Lv.G ? mma_kernel(Lv.M) : nullptr;
+      for (int i = 0; i < 3; ++i)
+        if (L.n[i] > 1024) Lv.kmma = nullptr;   // packed coordinates
       if (Lv.kmma) {
-        CU(cudaFuncSetAttribute(Lv.kmma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(Tab)));
+        CU(cudaFuncSetAttribute(Lv.kmma, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)std::max(mma_smem(Lv.M), list_smem(Lv.m, Lv.G))));
         std::vector<int32_t> gc, gm;
         for (int64_t c = 0; c < h->ncell; ++c)
-          if (kind_own[c] != 2) gc.push_back((int32_t)c);
+          if (kind_own[c] != 2) gc.push_back(mma_pack(h.get(), q, c));
         while (gc.size() % 8) gc.push_back(-1);
         Lv.nA = (int64_t)gc.size() / 8;
         gm.assign(Lv.nA, -1);
@@ -1761,6 +1814,7 @@ static int setup_impl(const fcm_grid* g, const fcm_params* prm, const fcm_slab* 
     CU(cudaMemcpyAsync(Lv.cmax, T.cmax.data(), T.m * 6, cudaMemcpyHostToDevice, h->stream));
     RC(h->alloc(&Lv.x, Lv.ndof));
     RC(h->alloc(&Lv.r, Lv.ndof));
+    if (q >= 2) RC(h->alloc(&Lv.r2, Lv.ndof));
     if (h->nranks > 1) {   // interface planes of this level (slab.hpp), exchange order
       std::vector<int32_t> lo, hi;
       if (h->z0 > 0) plane_slots(L, q, 0, lo);
