@@ -69,19 +69,20 @@ __device__ __forceinline__ void stage_fragments(double* As, const double* K, int
   }
 }
 
-template <int M>
-__device__ __forceinline__ double mma_cells(const MmaOp& g, const Tab& T, const double* __restrict__ As,
+template <int M, bool FUSE = false>
+__device__ __forceinline__ double mma_cells(const CellOp& op, const int32_t* __restrict__ grp_cells,
+                                            const int32_t* __restrict__ grp_mat, int64_t ngroups,
+                                            const Tab& T, const double* __restrict__ As,
                                             int main_slot, int warp, int nwarps) {
   constexpr int MT = (M + 7) / 8;   // row tiles
   constexpr int KT = (M + 3) / 4;   // k tiles
-  const CellOp& op = g.op;
   const int lane = threadIdx.x & 31;
   const int ar = lane >> 2, ac = lane & 3;
   double energy = 0.0;
   const bool want_e = op.partials != nullptr;
-  for (int64_t gi = warp; gi < g.ngroups; gi += nwarps) {
-    const int slot = __ldg(g.grp_mat + gi);   // warp-uniform
-    const int* cells = g.grp_cells + gi * 8;
+  for (int64_t gi = warp; gi < ngroups; gi += nwarps) {
+    const int slot = __ldg(grp_mat + gi);   // warp-uniform
+    const int* cells = grp_cells + gi * 8;
     const int cg = __ldg(cells + ar);            // B column / gather cell of this lane
     const int c0 = __ldg(cells + 2 * ac), c1 = __ldg(cells + 2 * ac + 1);   // output cells
     // gather: B[kt] = x[dof kt*4 + ac] of cell cg
@@ -89,7 +90,7 @@ __device__ __forceinline__ double mma_cells(const MmaOp& g, const Tab& T, const 
 #pragma unroll
     for (int kt = 0; kt < KT; ++kt) {
       const int idx = mma_dof_index<M>(T, kt * 4 + ac, cg);
-      B[kt] = idx >= 0 ? __ldg(op.in + idx) : 0.0;
+      B[kt] = idx >= 0 ? load_in<FUSE>(op, idx) : 0.0;
     }
     const double s0 = op.coef * cell_scale(op, c0), s1 = op.coef * cell_scale(op, c1);
     const bool main = slot == main_slot;
@@ -113,11 +114,11 @@ __device__ __forceinline__ double mma_cells(const MmaOp& g, const Tab& T, const 
       const int i0 = mma_dof_index<M>(T, a, c0), i1 = mma_dof_index<M>(T, a, c1);
       if (i0 >= 0) {
         atomicAdd(op.out + i0, s0 * d0);
-        if (want_e) energy = fma(__ldg(op.in + i0), s0 / op.coef * d0, energy);
+        if (want_e) energy = fma(load_in<FUSE>(op, i0), s0 / op.coef * d0, energy);
       }
       if (i1 >= 0) {
         atomicAdd(op.out + i1, s1 * d1);
-        if (want_e) energy = fma(__ldg(op.in + i1), s1 / op.coef * d1, energy);
+        if (want_e) energy = fma(load_in<FUSE>(op, i1), s1 / op.coef * d1, energy);
       }
     }
   }

@@ -222,182 +222,6 @@ __device__ __forceinline__ double reg_cells(const CellOp& op, const Tab& T, cons
   return energy;
 }
 
-// Regular population, ROW-STREAMING form: TS threads per cell, thread j of a cell owns the
-// rows a = j, j+TS, ...; a warp holds 32/TS consecutive cells along x (lane = j*(32/TS) + cell),
-// so every gather / scatter instruction is coalesced.  Each thread gathers the M values of its
-// cell into registers (the TS copies hit L1); the shared matrix row a is read from shared
-// memory at one address per j (TS distinct addresses in distinct banks per instruction),
-// y_a = s Mat[a,:] x is formed and scattered immediately, so no accumulator array is kept.
-// Other boundary types (smoother) read their rows through L1.  Ms: row-major M x M.
-template <int M, int TS>
-__device__ __forceinline__ double row_cells(const CellOp& op, const Tab& T, const double* __restrict__ Ms,
-                                            int bid, int nblk) {
-  constexpr int CPW = 32 / TS;
-  const int nx = op.nx, ny = op.ny, ncell = op.ncell;
-  const int ilx = op.ilo[0], ihx = op.ihi[0], ily = op.ilo[1], ihy = op.ihi[1];
-  const int ilz = op.ilo[2], ihz = op.ihi[2];
-  const bool apply = op.mode == OP_APPLY;
-  const bool want_e = op.partials != nullptr;
-  double* __restrict__ out = op.out;
-  const double coef = op.coef;
-  const int lane = threadIdx.x & 31;
-  const int j = lane / CPW;
-  const int warp = (bid * blockDim.x + threadIdx.x) >> 5;
-  const int nwarp = (nblk * blockDim.x) >> 5;
-  double energy = 0.0;
-  for (int c0 = warp * CPW; c0 < ncell; c0 += nwarp * CPW) {
-    const int c = c0 + lane % CPW;
-    if (c >= ncell) continue;
-    bool act;
-    double scale = 1.0;
-    const double* Mg = Ms;
-    if (apply) {
-      const int k = op.kind[c];
-      act = k != 2;
-      scale = (k == 1) ? op.alpha : 1.0;
-    } else {
-      const int b = op.blk[c];
-      act = b < 0;
-      const int t = -b - 1;
-      scale = (t >> 12) ? op.inv_alpha : 1.0;
-      const int code = t & 0xfff;
-      if (code != 0) Mg = op.type_inv + code * M * M;
-    }
-    if (!act) continue;
-    const int cx = c % nx, cyz = c / nx, cy = cyz % ny, cz = cyz / ny;
-    const bool inner = (cx >= ilx) & (cx <= ihx) & (cy >= ily) & (cy <= ihy) & (cz >= ilz) & (cz <= ihz);
-    double x[M];
-#pragma unroll
-    for (int b = 0; b < M; ++b)
-      x[b] = (inner || dof_free(T, b, cx, cy, cz)) ? load_in<false>(op, dof_index(T, b, cx, cy, cz)) : 0.0;
-    const double cs = coef * scale;
-    const bool shared = Mg == Ms;   // (pointer compare only)
-#pragma unroll
-    for (int al = 0; al < (M + TS - 1) / TS; ++al) {
-      const int a = j + TS * al;
-      if (a < M) {
-        double acc0 = 0.0, acc1 = 0.0;
-        if (shared) {   // explicit shared-memory pointer: LDS (a select with Mg would be a generic LD)
-          const double* row = Ms + a * M;
-#pragma unroll
-          for (int b = 0; b + 1 < M; b += 2) {
-            acc0 = fma(row[b], x[b], acc0);
-            acc1 = fma(row[b + 1], x[b + 1], acc1);
-          }
-          if (M & 1) acc0 = fma(row[M - 1], x[M - 1], acc0);
-        } else {
-          const double* row = Mg + a * M;
-#pragma unroll
-          for (int b = 0; b + 1 < M; b += 2) {
-            acc0 = fma(__ldg(row + b), x[b], acc0);
-            acc1 = fma(__ldg(row + b + 1), x[b + 1], acc1);
-          }
-          if (M & 1) acc0 = fma(__ldg(row + M - 1), x[M - 1], acc0);
-        }
-        const double y = acc0 + acc1;
-        if (inner || dof_free(T, a, cx, cy, cz)) {
-          const int ia = dof_index(T, a, cx, cy, cz);
-          atomicAdd(out + ia, cs * y);
-          if (want_e) energy = fma(load_in<false>(op, ia), scale * y, energy);
-        }
-      }
-    }
-  }
-  return energy;
-}
-
-template <int M> __host__ __device__ constexpr int row_split() { return M <= 8 ? 1 : (M <= 16 ? 2 : 4); }
-
-// The shared matrix of the regular population passed BY VALUE as a kernel parameter (row-major
-// M x M, M <= 40 so that it fits the 32 KB parameter space): it lives in the constant bank, and
-// with one thread per cell every lane uses the same entry, so each DFMA takes its matrix
-// operand straight from the constant cache -- no shared-memory traffic for the matrix.
-template <int M>
-struct MatParam {
-  double v[M * M];
-};
-
-// Regular population, one thread per cell (consecutive lanes = consecutive cells along x,
-// coalesced gathers / scatters), x in registers, rows streamed from the parameter bank and
-// scattered immediately.  Cells away from Dirichlet faces take an index path without tests.
-// Other boundary types (smoother) read their rows through L1.
-template <int M>
-__device__ __forceinline__ double param_cells(const CellOp& op, const Tab& T, const MatParam<M>& P,
-                                              int bid, int nblk) {
-  const int nx = op.nx, ny = op.ny, ncell = op.ncell;
-  const int ilx = op.ilo[0], ihx = op.ihi[0], ily = op.ilo[1], ihy = op.ihi[1];
-  const int ilz = op.ilo[2], ihz = op.ihi[2];
-  const bool apply = op.mode == OP_APPLY;
-  const bool want_e = op.partials != nullptr;
-  double* __restrict__ out = op.out;
-  const double coef = op.coef;
-  double energy = 0.0;
-  for (int c = bid * blockDim.x + threadIdx.x; c < ncell; c += nblk * blockDim.x) {
-    bool act;
-    double scale = 1.0;
-    const double* Mg = nullptr;
-    if (apply) {
-      const int k = op.kind[c];
-      act = k != 2;
-      scale = (k == 1) ? op.alpha : 1.0;
-    } else {
-      const int b = op.blk[c];
-      act = b < 0;
-      const int t = -b - 1;
-      scale = (t >> 12) ? op.inv_alpha : 1.0;
-      const int code = t & 0xfff;
-      if (code != 0) Mg = op.type_inv + code * M * M;
-    }
-    if (!act) continue;
-    const int cx = c % nx, cyz = c / nx, cy = cyz % ny, cz = cyz / ny;
-    const bool inner = (cx >= ilx) & (cx <= ihx) & (cy >= ily) & (cy <= ihy) & (cz >= ilz) & (cz <= ihz);
-    double x[M];
-    int idx[M];
-#pragma unroll
-    for (int b = 0; b < M; ++b) {
-      const int4 g = T.g[b];
-      idx[b] = g.x + cx + cy * g.y + cz * g.z;
-      if (!inner && !dof_free(T, b, cx, cy, cz)) idx[b] = -1;
-      x[b] = idx[b] >= 0 ? __ldg(op.in + idx[b]) : 0.0;
-    }
-    const double cs = coef * scale;
-    if (Mg == nullptr) {
-#pragma unroll
-      for (int a = 0; a < M; ++a) {
-        double acc0 = 0.0, acc1 = 0.0;
-#pragma unroll
-        for (int b = 0; b + 1 < M; b += 2) {
-          acc0 = fma(P.v[a * M + b], x[b], acc0);
-          acc1 = fma(P.v[a * M + b + 1], x[b + 1], acc1);
-        }
-        if (M & 1) acc0 = fma(P.v[a * M + M - 1], x[M - 1], acc0);
-        const double y = acc0 + acc1;
-        if (idx[a] >= 0) {
-          atomicAdd(out + idx[a], cs * y);
-          if (want_e) energy = fma(x[a], scale * y, energy);
-        }
-      }
-    } else {
-#pragma unroll
-      for (int a = 0; a < M; ++a) {
-        double acc0 = 0.0, acc1 = 0.0;
-#pragma unroll
-        for (int b = 0; b + 1 < M; b += 2) {
-          acc0 = fma(__ldg(Mg + a * M + b), x[b], acc0);
-          acc1 = fma(__ldg(Mg + a * M + b + 1), x[b + 1], acc1);
-        }
-        if (M & 1) acc0 = fma(__ldg(Mg + a * M + M - 1), x[M - 1], acc0);
-        const double y = acc0 + acc1;
-        if (idx[a] >= 0) {
-          atomicAdd(out + idx[a], cs * y);
-          if (want_e) energy = fma(x[a], scale * y, energy);
-        }
-      }
-    }
-  }
-  return energy;
-}
-
 // Individual cells (op.list != nullptr) or, without a compile-time M, all cells with per-cell
 // matrix selection.  Groups of G lanes per cell; xs/ids: per-warp shared scratch (CPW*m).
 template <int G, bool FUSE>

@@ -23,6 +23,7 @@
 #pragma once
 #include <cooperative_groups.h>
 
+#include "cellmma.cuh"
 #include "cellop.cuh"
 
 namespace fcm {
@@ -56,6 +57,13 @@ struct CoarseArgs {
   GridCtl* ctl;
   int* iters;                  // [0] = this solve, [1] += this solve
   int nbl_A, nbl_M;            // blocks assigned to the individual lists of A / M
+  // regular cells as fp64 MMA groups (cellmma.cuh); null: thread-per-cell path (reg_cells)
+  const int32_t* gA_cells;
+  const int32_t* gA_mat;
+  int64_t nA;
+  const int32_t* gS_cells;
+  const int32_t* gS_mat;
+  int64_t nS;
 };
 
 __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
@@ -148,9 +156,19 @@ __device__ __noinline__ void barrier_reduce2(double va, double vb, double* pa, d
 // nbl == 0: every block does both populations.
 template <int M, int G, bool FUSE>
 __device__ __forceinline__ double coarse_cells(const CellOp& op, const Tab& T, const double* Ms,
-                                               double* xsr, double* xs, int* ids, int nbl) {
+                                               double* xsr, double* xs, int* ids, int nbl,
+                                               const int32_t* gcells = nullptr, const int32_t* gmat = nullptr,
+                                               int64_t ngroups = 0, const double* As = nullptr,
+                                               int main_slot = 0) {
   const int wpb = blockDim.x >> 5;
   const int wib = threadIdx.x >> 5;
+  if constexpr (M > 0 && M <= 32) {
+    if (gcells) {   // MMA groups and the individual list, both grid-strided over every warp
+      const int gw = blockIdx.x * wpb + wib, nw = gridDim.x * wpb;
+      const double e = mma_cells<M, FUSE>(op, gcells, gmat, ngroups, T, As, main_slot, gw, nw);
+      return e + list_cells<G, FUSE>(op, T, gw, nw, xs, ids);
+    }
+  }
   if (M > 0 && nbl == 0) {
     double e = 0.0;
     if constexpr (M > 0)
@@ -184,10 +202,18 @@ __global__ void __launch_bounds__(256) k_coarse_pcg(CoarseArgs a) {
   double* xs = xs0 + (threadIdx.x >> 5) * CPW * m;
   int* ids = reinterpret_cast<int*>(xs0 + wpb * CPW * m) + (threadIdx.x >> 5) * CPW * m;
   __shared__ double red[32];
+  constexpr int FR = (M > 0 && M <= 32) ? ((M + 7) / 8) * ((M + 3) / 4) * 32 : 0;   // fragment doubles
+  int* ids_end = reinterpret_cast<int*>(xs0 + wpb * CPW * m) + wpb * CPW * m;
+  double* AsA = reinterpret_cast<double*>(ids_end + ((wpb * CPW * m) & 1));   // 8-byte aligned
+  double* AsM = AsA + FR;
   load_tab(T, a.A);
   if constexpr (M > 0) {
     load_shared_matrix<M>(MsA, a.A);
     if (!a.jacobi) load_shared_matrix<M>(MsM, a.M);
+  }
+  if constexpr (M > 0 && M <= 32) {
+    if (a.gA_cells) stage_fragments<M>(AsA, a.A.Kref, a.A.ldK);
+    if (a.gS_cells && !a.jacobi) stage_fragments<M>(AsM, a.M.type_inv, M);
   }
   __syncthreads();
   const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -224,13 +250,13 @@ __global__ void __launch_bounds__(256) k_coarse_pcg(CoarseArgs a) {
       }
     } else {
       opM.in = a.r[0]; opM.in1 = nullptr; opM.out = a.z[0];
-      s2 = coarse_cells<M, G, false>(opM, T, MsM, xsr, xs, ids, a.nbl_M);
+      s2 = coarse_cells<M, G, false>(opM, T, MsM, xsr, xs, ids, a.nbl_M, a.gS_cells, a.gS_mat, a.nS, AsM, 0);
     }
     barrier_reduce2_cg(s2, 0.0, a.part, a.part_stride, ++gen, red, t1, t2);
     double rz = t1;
     // w0 = A z0 ; p = z0
     opA.in = a.z[0]; opA.in1 = nullptr; opA.out = a.w[0];
-    s1 = coarse_cells<M, G, false>(opA, T, MsA, xsr, xs, ids, a.nbl_A);
+    s1 = coarse_cells<M, G, false>(opA, T, MsA, xsr, xs, ids, a.nbl_A, a.gA_cells, a.gA_mat, a.nA, AsA, -1);
     for (int64_t i = tid; i < n; i += nth) a.p[i] = a.z[0][i];
     barrier_reduce2_cg(s1, 0.0, a.part, a.part_stride, ++gen, red, t1, t2);
     double pq = t1;
@@ -262,7 +288,7 @@ __global__ void __launch_bounds__(256) k_coarse_pcg(CoarseArgs a) {
       if (!a.jacobi) {
         opM.in = rC; opM.in1 = wC; opM.in2 = qO; opM.c1 = -alpha; opM.c2 = beta;
         opM.out = a.z[nx];
-        rz_loc = coarse_cells<M, G, true>(opM, T, MsM, xsr, xs, ids, a.nbl_M);
+        rz_loc = coarse_cells<M, G, true>(opM, T, MsM, xsr, xs, ids, a.nbl_M, a.gS_cells, a.gS_mat, a.nS, AsM, 0);
       }
       double rr, rz_new;
       barrier_reduce2_cg(rr_loc, rz_loc, a.part, a.part_stride, ++gen, red, rr, rz_new);
@@ -273,7 +299,7 @@ __global__ void __launch_bounds__(256) k_coarse_pcg(CoarseArgs a) {
       rz = rz_new;
       double* zN = a.z[nx];
       opA.in = zN; opA.in1 = nullptr; opA.out = a.w[nx];
-      const double zaz = coarse_cells<M, G, false>(opA, T, MsA, xsr, xs, ids, a.nbl_A);
+      const double zaz = coarse_cells<M, G, false>(opA, T, MsA, xsr, xs, ids, a.nbl_A, a.gA_cells, a.gA_mat, a.nA, AsA, -1);
       double zq = 0.0;
       for (int64_t i = tid; i < n; i += nth) {
         const double zi = zN[i];

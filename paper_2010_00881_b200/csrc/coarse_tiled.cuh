@@ -229,22 +229,29 @@ __device__ __forceinline__ void t_red_release(unsigned* p, unsigned v) {
   asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
-__device__ __noinline__ void tiled_allreduce3(double v0, double v1, double v2, double* part,
-                                              TiledCtl* ctl, unsigned target, unsigned gen,
-                                              double* red, double* tot) {
+// Arrival + wait: block partials posted, one RED per block, one polling thread; returns when
+// every block of this generation has arrived (all threads synchronised).
+__device__ __noinline__ void tiled_arrive_wait(double v0, double v1, double v2, double* part,
+                                               TiledCtl* ctl, unsigned target, unsigned gen,
+                                               double* red) {
   block_sum3(v0, v1, v2, red);
   const int nb = gridDim.x;
   double* pp = part + (size_t)(gen & 1) * 3 * nb;
+  if (threadIdx.x == 0) {
+    __stcg(pp + blockIdx.x, v0);
+    __stcg(pp + nb + blockIdx.x, v1);
+    __stcg(pp + 2 * nb + blockIdx.x, v2);
+    t_red_release(&ctl->count, 1u);   // orders this block's earlier global writes (w, partials)
+    while ((int)(t_ld_acquire(&ctl->count) - target) < 0) {}
+  }
+  __syncthreads();
+}
+// Totals of generation gen, summed in block order by warp 0 (bit-identical on every block);
+// call after tiled_arrive_wait; the caller synchronises before reading tot.
+__device__ __forceinline__ void tiled_totals(const double* part, unsigned gen, double* tot) {
   if (threadIdx.x < 32) {
-    const int l = threadIdx.x;
-    if (l == 0) {
-      __stcg(pp + blockIdx.x, v0);
-      __stcg(pp + nb + blockIdx.x, v1);
-      __stcg(pp + 2 * nb + blockIdx.x, v2);
-      t_red_release(&ctl->count, 1u);   // orders this block's earlier global writes (w, partials)
-      while ((int)(t_ld_acquire(&ctl->count) - target) < 0) {}
-    }
-    __syncwarp();
+    const int nb = gridDim.x, l = threadIdx.x;
+    const double* pp = part + (size_t)(gen & 1) * 3 * nb;
     double a0 = 0.0, a1 = 0.0, a2 = 0.0;
     for (int j = l; j < nb; j += 32) {
       a0 += __ldcg(pp + j);
@@ -259,11 +266,12 @@ __device__ __noinline__ void tiled_allreduce3(double v0, double v1, double v2, d
     }
     if (l == 0) { tot[0] = a0; tot[1] = a1; tot[2] = a2; }
   }
-  __syncthreads();
 }
 
+constexpr int kTiledThreads = 768;
+
 template <int DIM, int NF>
-__global__ void __launch_bounds__(512, 1) k_coarse_tiled(TiledArgs a) {
+__global__ void __launch_bounds__(kTiledThreads, 1) k_coarse_tiled(TiledArgs a) {
   constexpr int NC = 1 << DIM;
   constexpr int M1 = NC * NF;
   constexpr int MM = slot_stride(M1);
@@ -412,7 +420,22 @@ __global__ void __launch_bounds__(512, 1) k_coarse_tiled(TiledArgs a) {
   smooth_E1();
   __syncthreads();
   apply_T(a.wpub[0], g_loc, d_loc, r_loc);
-  tiled_allreduce3(g_loc, d_loc, r_loc, a.part, a.ctl, cnt0 + (gen + 1) * gridDim.x, gen + 1, red, tot); ++gen;
+  // w halo of the current generation, preloaded right after each barrier (overlaps the
+  // partial-sum reduction); the first 4*blockDim entries of E2 live in registers
+  double wl[4];
+  auto preload_w = [&](const double* wv) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int t = k * blockDim.x + threadIdx.x;
+      const int gi = t < NF * E2 ? S.gidx[t] : -1;
+      wl[k] = gi >= 0 ? __ldcg(wv + gi) : 0.0;
+    }
+  };
+  tiled_arrive_wait(g_loc, d_loc, r_loc, a.part, a.ctl, cnt0 + (gen + 1) * gridDim.x, gen + 1, red);
+  ++gen;
+  preload_w(a.wpub[0]);
+  tiled_totals(a.part, gen, tot);
+  __syncthreads();
   double gamma = tot[0], delta = tot[1];
   const double rho0 = tot[2];
   double rho = rho0;
@@ -431,23 +454,21 @@ __global__ void __launch_bounds__(512, 1) k_coarse_tiled(TiledArgs a) {
     const unsigned long long tp0 = a.prof ? t_now() : 0ull;
     // s = w + beta s, r -= alpha s on E2 (w of the neighbours published before the barrier)
     const double* wv = a.wpub[it & 1];
-    for (int t0b = 0; t0b < NF * E2; t0b += 4 * blockDim.x) {   // 4 L2 loads in flight per thread
-      double wl[4];
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const int t = t0b + k * blockDim.x + threadIdx.x;
-        const int gi = t < NF * E2 ? S.gidx[t] : -1;
-        wl[k] = gi >= 0 ? __ldcg(wv + gi) : 0.0;
+    for (int k = 0; k < 4; ++k) {   // preloaded part
+      const int t = k * blockDim.x + threadIdx.x;
+      if (t < NF * E2 && S.gidx[t] >= 0) {
+        const double sv = fma(beta, S.s[t], wl[k]);
+        S.s[t] = sv;
+        S.r[t] = fma(-alpha, sv, S.r[t]);
       }
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const int t = t0b + k * blockDim.x + threadIdx.x;
-        if (t < NF * E2 && S.gidx[t] >= 0) {
-          const double sv = fma(beta, S.s[t], wl[k]);
-          S.s[t] = sv;
-          S.r[t] = fma(-alpha, sv, S.r[t]);
-        }
-      }
+    }
+    for (int t = 4 * blockDim.x + threadIdx.x; t < NF * E2; t += blockDim.x) {   // rest (large bricks)
+      const int gi = S.gidx[t];
+      if (gi < 0) continue;
+      const double sv = fma(beta, S.s[t], __ldcg(wv + gi));
+      S.s[t] = sv;
+      S.r[t] = fma(-alpha, sv, S.r[t]);
     }
     // p = u + beta p, x += alpha p on T
     for (int t = threadIdx.x; t < NF * nT; t += blockDim.x) {
@@ -467,7 +488,11 @@ __global__ void __launch_bounds__(512, 1) k_coarse_tiled(TiledArgs a) {
     apply_T(a.wpub[it & 1], g_loc, d_loc, r_loc);
     __syncthreads();
     const unsigned long long tp3 = a.prof ? t_now() : 0ull;
-    tiled_allreduce3(g_loc, d_loc, r_loc, a.part, a.ctl, cnt0 + (gen + 1) * gridDim.x, gen + 1, red, tot); ++gen;
+    tiled_arrive_wait(g_loc, d_loc, r_loc, a.part, a.ctl, cnt0 + (gen + 1) * gridDim.x, gen + 1, red);
+    ++gen;
+    preload_w(a.wpub[it & 1]);
+    tiled_totals(a.part, gen, tot);
+    __syncthreads();
     if (a.prof && threadIdx.x == 0) {
       const unsigned long long tp4 = t_now();
       unsigned long long* pr = a.prof + 4 * blockIdx.x;

@@ -1,10 +1,13 @@
 // fcm_mg.cu -- B200 (sm_100a) implementation of the C ABI in include/fcm_mg.h.
 //
 // Hot path:
-//   (a3) level operator apply    k_cellop<G> OP_APPLY   r -= A_q x
-//   (a4) additive Schwarz        k_cellop<G> OP_SMOOTH  x += w M^-1 r
+//   (a3) level operator apply    k_cell_mma<M,G> OP_APPLY   r -= A_q x: regular
+//                                cells as fp64 MMA groups + individual cut cells (list) in one launch
+//   (a4) additive Schwarz        k_cell_mma<M,G> OP_SMOOTH  x += w M^-1 r;
+//                                k_block_smooth for patch blocks (blocks.cuh)
 //   (a5) restriction / prolong.  pointer alias (prefix) / k_axpy on the prefix
-//   (a6) coarsest level p=1      k_coarse_pcg<G> (cooperative, whole inner CG in one launch)
+//   (a6) coarsest level p=1      k_coarse_tiled (shared-memory bricks) or k_coarse_pcg (grid-wide),
+//                                cooperative, whole inner CG in one launch
 //                                or k_dense_gemv with a setup-time inverse
 //   (a2) V-cycle                 enqueue_vcycle (Algorithm 1), CUDA graph
 //   (a1) flexible PCG            fcm_pcg_solve
@@ -84,9 +87,6 @@ struct LevelDev {
   int32_t* irr_list = nullptr;     // cells with an individual Schwarz inverse (irr order)
   int ilo[3] = {0, 0, 0}, ihi[3] = {-1, -1, -1};  // cells with no Dirichlet DOF
   int ts = 1;                      // threads per cell of the regular path
-  bool row = true;                 // regular path = k_cell_row (one thread per cell)
-  const void* kfused = nullptr;    // k_cellop<M, G>: both populations in one launch
-  const void* kparam = nullptr;    // k_cellop_p<M, G>: same, shared matrix in the parameter bank
   const void* kmma = nullptr;      // k_cell_mma<M>: regular cells as fp64 tensor-core MMAs
   int32_t* gA_cells = nullptr;     // apply groups (8 non-cut cells, K_ref)
   int32_t* gA_mat = nullptr;
@@ -94,7 +94,6 @@ struct LevelDev {
   int32_t* gS_cells = nullptr;     // smoother groups (8 regular cells of one type slot)
   int32_t* gS_mat = nullptr;
   int64_t nS = 0;
-  std::vector<double> Kp, Tp;      // host copies of the shared matrices (row-major M x M)
   std::vector<int32_t> blk_h;      // host copy of blk (tiled coarse setup)
   // patchwise blocks (blocks.cuh): anchors are grid vertices, blk is per anchor
   bool patch = false;
@@ -244,60 +243,6 @@ __global__ void __launch_bounds__(kThreads, 4) k_cell_reg(CellOp op) {
   }
 }
 
-// Regular population, row-streaming form (row_cells): one thread per cell; smem [Tab][Ms: M*M]
-template <int M>
-__global__ void __launch_bounds__(kThreads) k_cell_row(CellOp op) {
-  extern __shared__ __align__(16) unsigned char smem[];
-  Tab& T = *reinterpret_cast<Tab*>(smem);
-  double* Ms = reinterpret_cast<double*>(smem + sizeof(Tab));
-  __shared__ double red[32];
-  load_tab(T, op);
-  for (int e = threadIdx.x; e < M * M; e += blockDim.x) {
-    const int a = e / M, b = e % M;
-    Ms[e] = (op.mode == OP_APPLY) ? op.Kref[a * op.ldK + b] : op.type_inv[a * M + b];  // type slot 0
-  }
-  __syncthreads();
-  const double e = row_cells<M, row_split<M>()>(op, T, Ms, blockIdx.x, gridDim.x);
-  if (op.partials) {
-    const double t = block_sum(e, red);
-    if (threadIdx.x == 0) op.partials[blockIdx.x] = t;
-  }
-}
-
-// One launch for both populations: blocks [0, nb_reg) stream the regular cells (row_cells),
-// the others the individual list (list_cells); smem [Tab][max(Ms: M*M, list scratch)].
-template <int M, int G>
-__global__ void __launch_bounds__(kThreads) k_cellop(CellOp op, int nb_reg) {
-  extern __shared__ __align__(16) unsigned char smem[];
-  Tab& T = *reinterpret_cast<Tab*>(smem);
-  double* Ms = reinterpret_cast<double*>(smem + sizeof(Tab));
-  __shared__ double red[32];
-  load_tab(T, op);
-  double e;
-  if ((int)blockIdx.x < nb_reg) {
-    for (int t = threadIdx.x; t < M * M; t += blockDim.x) {
-      const int a = t / M, b = t % M;
-      Ms[t] = (op.mode == OP_APPLY) ? op.Kref[a * op.ldK + b] : op.type_inv[a * M + b];  // type slot 0
-    }
-    __syncthreads();
-    e = row_cells<M, row_split<M>()>(op, T, Ms, blockIdx.x, nb_reg);
-  } else {
-    constexpr int CPW = 32 / G;
-    const int wpb = blockDim.x >> 5;
-    double* xs0 = Ms;
-    double* xs = xs0 + (threadIdx.x >> 5) * CPW * op.m;
-    int* ids = reinterpret_cast<int*>(xs0 + wpb * CPW * op.m) + (threadIdx.x >> 5) * CPW * op.m;
-    __syncthreads();
-    e = list_cells<G, false>(op, T, (blockIdx.x - nb_reg) * wpb + (threadIdx.x >> 5),
-                             (gridDim.x - nb_reg) * wpb, xs, ids);
-  }
-  if (op.partials) {
-    const double t = block_sum(e, red);
-    if (threadIdx.x == 0) op.partials[blockIdx.x] = t;
-  }
-}
-
-// Regular cells as fp64 tensor-core MMAs (cellmma.cuh); smem [Tab]
 // One launch per cell operation: blocks [0, nb_mma) run the regular cells as fp64 MMAs
 // (cellmma.cuh), the others the individual list (list_cells); every block also does its share
 // of the fused copy.  smem [Tab][max(A fragments, list scratch)].
@@ -315,7 +260,8 @@ __global__ void __launch_bounds__(kThreads, 4) k_cell_mma(MmaOp g, int nb_mma) {
   const int wpb = blockDim.x >> 5;
   double e;
   if (is_mma) {
-    e = mma_cells<M>(g, T, As, apply ? -1 : 0, blockIdx.x * wpb + (threadIdx.x >> 5), nb_mma * wpb);
+    e = mma_cells<M>(g.op, g.grp_cells, g.grp_mat, g.ngroups, T, As, apply ? -1 : 0,
+                     blockIdx.x * wpb + (threadIdx.x >> 5), nb_mma * wpb);
   } else {
     constexpr int CPW = 32 / G;
     double* xs = As + (threadIdx.x >> 5) * CPW * g.op.m;
@@ -328,32 +274,6 @@ __global__ void __launch_bounds__(kThreads, 4) k_cell_mma(MmaOp g, int nb_mma) {
   if (g.op.partials) {
     const double t = block_sum(e, red);
     if (threadIdx.x == 0) g.op.partials[blockIdx.x] = t;
-  }
-}
-
-// Same with the shared matrix in the parameter bank (param_cells); smem [Tab][list scratch]
-template <int M, int G>
-__global__ void __launch_bounds__(kThreads) k_cellop_p(CellOp op, int nb_reg, MatParam<M> P) {
-  extern __shared__ __align__(16) unsigned char smem[];
-  Tab& T = *reinterpret_cast<Tab*>(smem);
-  __shared__ double red[32];
-  load_tab(T, op);
-  __syncthreads();
-  double e;
-  if ((int)blockIdx.x < nb_reg) {
-    e = param_cells<M>(op, T, P, blockIdx.x, nb_reg);
-  } else {
-    constexpr int CPW = 32 / G;
-    const int wpb = blockDim.x >> 5;
-    double* xs0 = reinterpret_cast<double*>(smem + sizeof(Tab));
-    double* xs = xs0 + (threadIdx.x >> 5) * CPW * op.m;
-    int* ids = reinterpret_cast<int*>(xs0 + wpb * CPW * op.m) + (threadIdx.x >> 5) * CPW * op.m;
-    e = list_cells<G, false>(op, T, (blockIdx.x - nb_reg) * wpb + (threadIdx.x >> 5),
-                             (gridDim.x - nb_reg) * wpb, xs, ids);
-  }
-  if (op.partials) {
-    const double t = block_sum(e, red);
-    if (threadIdx.x == 0) op.partials[blockIdx.x] = t;
   }
 }
 
@@ -644,9 +564,9 @@ template <int M> constexpr int gsz() { return M <= 4 ? 4 : (M <= 8 ? 8 : (M <= 1
 #define FCM_FOR_M(X) X(4) X(8) X(9) X(16) X(24) X(25) X(27)
 
 // ts1: force one thread per cell (tuning knob FCM_TS1)
-const void* reg_kernel(int m, int* M_out, bool ts1, bool row) {
+const void* reg_kernel(int m, int* M_out, bool ts1) {
 #define CASE(MM) case MM: *M_out = MM; \
-  return row ? (const void*)k_cell_row<MM> : ts1 ? (const void*)k_cell_reg<MM, 1> : (const void*)k_cell_reg<MM, split_of<MM>()>;
+  return ts1 ? (const void*)k_cell_reg<MM, 1> : (const void*)k_cell_reg<MM, split_of<MM>()>;
   switch (m) { FCM_FOR_M(CASE) default: break; }
 #undef CASE
   *M_out = 0;
@@ -654,18 +574,6 @@ const void* reg_kernel(int m, int* M_out, bool ts1, bool row) {
 }
 const void* mma_kernel(int m) {
 #define CASE(MM) case MM: return (const void*)k_cell_mma<MM, gsz<MM>()>;
-  switch (m) { FCM_FOR_M(CASE) default: break; }
-#undef CASE
-  return nullptr;
-}
-const void* param_kernel(int m) {
-#define CASE(MM) case MM: return (const void*)k_cellop_p<MM, gsz<MM>()>;
-  switch (m) { FCM_FOR_M(CASE) default: break; }
-#undef CASE
-  return nullptr;
-}
-const void* fused_kernel(int m) {
-#define CASE(MM) case MM: return (const void*)k_cellop<MM, gsz<MM>()>;
   switch (m) { FCM_FOR_M(CASE) default: break; }
 #undef CASE
   return nullptr;
@@ -696,7 +604,6 @@ const void* tiled_kernel(int dim, int nf) {
   if (dim == 2 && nf == 1) return (const void*)k_coarse_tiled<2, 1>;
   return nullptr;
 }
-constexpr int kTiledThreads = 512;
 
 inline int grid_for(int64_t n, int sms) {
   int64_t b = (n + kThreads - 1) / kThreads;
@@ -724,17 +631,15 @@ static size_t reg_smem(int M, int TS) {
 static size_t mma_smem(int M) {
   return sizeof(Tab) + (size_t)((M + 7) / 8) * ((M + 3) / 4) * 32 * sizeof(double);
 }
-static size_t level_reg_smem(const LevelDev& Lv) {
-  if (Lv.row) return sizeof(Tab) + (size_t)Lv.M * Lv.M * sizeof(double);
-  return reg_smem(Lv.M, Lv.ts);
-}
+static size_t level_reg_smem(const LevelDev& Lv) { return reg_smem(Lv.M, Lv.ts); }
 static size_t list_smem(int m, int G) {
   return sizeof(Tab) + (size_t)(kThreads / 32) * (32 / G) * m * (sizeof(double) + sizeof(int));
 }
 // coarse: [Tab][MsA][MsM][reg scratch][list scratch]
 static size_t coarse_smem(int m, int M, int G) {
   const int TS = M > 0 ? split_rt(M) : 1;
-  return reg_smem(M, TS) + (size_t)M * (M + (M & 1)) * 8 + list_smem(m, G) - sizeof(Tab);
+  const size_t frag = (M > 0 && M <= 32) ? (size_t)2 * ((M + 7) / 8) * ((M + 3) / 4) * 32 * 8 + 8 : 0;
+  return reg_smem(M, TS) + (size_t)M * (M + (M & 1)) * 8 + list_smem(m, G) - sizeof(Tab) + frag;
 }
 
 static CellOp make_op(fcm_mg* h, int q, int mode, const double* in, double* out, double coef,
@@ -778,8 +683,7 @@ static void cellop_grid(const fcm_mg* h, int q, int mode, int* nb_reg, int* nb_l
     return;
   }
   if (Lv.M > 0) {
-    const bool param = Lv.kparam && (mode == OP_APPLY ? !Lv.Kp.empty() : !Lv.Tp.empty());
-    const int64_t ts = param ? 1 : Lv.ts;
+    const int64_t ts = Lv.ts;
     const int64_t cells_per_blk = (kThreads / 32) * (32 / ts);
     *nb_reg = (int)std::min<int64_t>((h->ncell + cells_per_blk - 1) / cells_per_blk, cap);
     const int64_t nl = mode == OP_APPLY ? h->ncut : Lv.n_irr;
@@ -820,46 +724,6 @@ static int launch_cellop(fcm_mg* h, int q, const CellOp& op, double* cp_dst = nu
     return FCM_OK;
   }
   if (cp_dst) RC(copy(h, cp_dst, cp_src, cp_n));   // other paths: the copy as its own launch
-  if (Lv.kparam && (op.mode == OP_APPLY ? !Lv.Kp.empty() : !Lv.Tp.empty())) {
-    // regular cells: parameter-bank kernel (many registers, one block per SM) on the main
-    // stream; the individual list concurrently on the forked branch (few registers, so it
-    // fills the remaining warp slots instead of queueing behind the regular blocks)
-    alignas(16) unsigned char pbuf[8 * 40 * 40];
-    const std::vector<double>& src = op.mode == OP_APPLY ? Lv.Kp : Lv.Tp;
-    std::memcpy(pbuf, src.data(), src.size() * 8);
-    const int dbg_skip = getenv("FCM_DEBUG_SKIP") ? atoi(getenv("FCM_DEBUG_SKIP")) : 0;  // timing only
-    if (dbg_skip & 2) nb_list = 0;
-    const bool fork = nb_list > 0;
-    if (fork) {
-      CU(cudaEventRecord(h->ev_fork, h->stream));
-      CU(cudaStreamWaitEvent(h->stream2, h->ev_fork, 0));
-      int off = nb_reg;
-      void* largs[] = {&o, &off};
-      cudaError_t e = cudaLaunchKernel(Lv.klist, dim3(nb_list), dim3(kThreads), largs, list_smem(Lv.m, Lv.G), h->stream2);
-      h->count();
-      if (e != cudaSuccess) return fail(FCM_ECUDA, "list kernel launch: %s", cudaGetErrorString(e));
-    }
-    int nbr = nb_reg;
-    void* args[] = {&o, &nbr, pbuf};
-    if (!(dbg_skip & 1)) {
-      cudaError_t e = cudaLaunchKernel(Lv.kparam, dim3(nb_reg), dim3(kThreads), args, list_smem(Lv.m, Lv.G), h->stream);
-      h->count();
-      if (e != cudaSuccess) return fail(FCM_ECUDA, "cell kernel launch: %s", cudaGetErrorString(e));
-    }
-    if (fork) {
-      CU(cudaEventRecord(h->ev_join, h->stream2));
-      CU(cudaStreamWaitEvent(h->stream, h->ev_join, 0));
-    }
-    return FCM_OK;
-  }
-  if (Lv.kfused) {   // one launch, heterogeneous blocks
-    void* args[] = {&o, &nb_reg};
-    const size_t sm = std::max(level_reg_smem(Lv), list_smem(Lv.m, Lv.G));
-    cudaError_t e = cudaLaunchKernel(Lv.kfused, dim3(nb_reg + nb_list), dim3(kThreads), args, sm, h->stream);
-    h->count();
-    if (e != cudaSuccess) return fail(FCM_ECUDA, "cell kernel launch: %s", cudaGetErrorString(e));
-    return FCM_OK;
-  }
   int off = nb_reg;
   cudaError_t e = cudaSuccess;
   const bool fork = nb_reg > 0 && nb_list > 0;
@@ -1100,6 +964,10 @@ static int enqueue_coarse(fcm_mg* h, const double* b, double* x) {
     a.nbl_M = share(L1.n_irr);
   }
   a.iters = h->d_coarse_iters;
+  if (L1.kmma) {   // regular cells as fp64 MMA groups (cellmma.cuh)
+    a.gA_cells = L1.gA_cells; a.gA_mat = L1.gA_mat; a.nA = L1.nA;
+    if (!a.jacobi) { a.gS_cells = L1.gS_cells; a.gS_mat = L1.gS_mat; a.nS = L1.nS; }
+  }
   void* args[] = {&a};
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(h->coarse_blocks);
@@ -1456,10 +1324,6 @@ static int setup_schwarz(fcm_mg* h, int q, const std::vector<uint8_t>& kind,
       CU(cudaMemcpyAsync(Lv.gS_mat, gm.data(), gm.size() * 4, cudaMemcpyHostToDevice, h->stream));
     }
   }
-  if (Lv.kparam && !patch && ntypes > 0 && mb == Lv.M) {   // slot-0 inverse for the parameter bank
-    Lv.Tp.resize((size_t)mb * mb);
-    CU(cudaMemcpy(Lv.Tp.data(), Lv.type_inv, Lv.Tp.size() * 8, cudaMemcpyDeviceToHost));
-  }
   Lv.blk_h = blk;
   CU(cudaStreamSynchronize(h->stream));
   return FCM_OK;
@@ -1752,9 +1616,8 @@ static int setup_impl(const fcm_grid* g, const fcm_params* prm, const fcm_slab* 
     const LevelTable& T = L.tables[q];
     Lv.q = q; Lv.m = T.m; Lv.ndof = T.ndof; Lv.G = group_size(T.m);
     const bool ts1 = getenv("FCM_TS1") && atoi(getenv("FCM_TS1")) > 0;
-    Lv.row = !(getenv("FCM_CELL_ROW") && atoi(getenv("FCM_CELL_ROW")) == 0);
-    Lv.kreg = reg_kernel(T.m, &Lv.M, ts1, Lv.row);
-    Lv.ts = (ts1 || Lv.M == 0) ? 1 : (Lv.row ? (Lv.M <= 8 ? 1 : (Lv.M <= 16 ? 2 : 4)) : split_rt(Lv.M));
+    Lv.kreg = reg_kernel(T.m, &Lv.M, ts1);
+    Lv.ts = (ts1 || Lv.M == 0) ? 1 : split_rt(Lv.M);
     for (int i = 0; i < 3; ++i) {
       Lv.ilo[i] = 0;
       Lv.ihi[i] = L.n[i] - 1;
@@ -1783,23 +1646,6 @@ static int setup_impl(const fcm_grid* g, const fcm_params* prm, const fcm_slab* 
         CU(cudaMemcpyAsync(Lv.gA_mat, gm.data(), gm.size() * 4, cudaMemcpyHostToDevice, h->stream));
         CU(cudaStreamSynchronize(h->stream));
       }
-    }
-    if (Lv.M > 0 && Lv.M <= 40 && gsz_rt(Lv.M) == Lv.G &&
-        !(getenv("FCM_CELL_PARAM") && atoi(getenv("FCM_CELL_PARAM")) == 0)) {
-      Lv.kparam = param_kernel(Lv.M);
-      if (Lv.kparam) {
-        CU(cudaFuncSetAttribute(Lv.kparam, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)list_smem(Lv.m, Lv.G)));
-        Lv.Kp.resize((size_t)Lv.M * Lv.M);
-        for (int a = 0; a < Lv.M; ++a)
-          for (int b = 0; b < Lv.M; ++b) Lv.Kp[(size_t)a * Lv.M + b] = K_ref[(size_t)a * m + b];
-      }
-    }
-    if (Lv.row && Lv.M > 0 && !(getenv("FCM_CELL_FUSED") && atoi(getenv("FCM_CELL_FUSED")) == 0)) {
-      Lv.kfused = fused_kernel(Lv.M);
-      if (Lv.kfused && gsz_rt(Lv.M) != Lv.G) Lv.kfused = nullptr;
-      if (Lv.kfused)
-        CU(cudaFuncSetAttribute(Lv.kfused, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)std::max(level_reg_smem(Lv), list_smem(Lv.m, Lv.G))));
     }
     if (Lv.kreg) CU(cudaFuncSetAttribute(Lv.kreg, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)level_reg_smem(Lv)));
     CU(cudaFuncSetAttribute(Lv.klist, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)list_smem(Lv.m, Lv.G)));
