@@ -268,7 +268,7 @@ __device__ __forceinline__ void tiled_totals(const double* part, unsigned gen, d
   }
 }
 
-constexpr int kTiledThreads = 768;
+constexpr int kTiledThreads = 512;
 
 template <int DIM, int NF>
 __global__ void __launch_bounds__(kTiledThreads, 1) k_coarse_tiled(TiledArgs a) {
