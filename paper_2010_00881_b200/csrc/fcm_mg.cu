@@ -586,8 +586,12 @@ const void* list_kernel(int G) {
     default: return (const void*)k_cell_list<32>;
   }
 }
+// coarse_group(): lanes per individual cell in the grid-wide coarse kernel.  Large coarse
+// levels (config 4: 75k individual 24x24 blocks per phase) are latency-bound on the list, so
+// m > 8 uses 8 lanes per cell (4 cells per warp in flight) instead of a whole warp.
+constexpr int coarse_group(int m) { return m <= 4 ? 4 : 8; }
 const void* coarse_kernel(int m, int G, int* M_out) {
-#define CASE(MM) case MM: *M_out = MM; return (const void*)k_coarse_pcg<MM, gsz<MM>()>;
+#define CASE(MM) case MM: *M_out = MM; return (const void*)k_coarse_pcg<MM, coarse_group(MM)>;
   switch (m) { FCM_FOR_M(CASE) default: break; }
 #undef CASE
   *M_out = 0;
@@ -972,7 +976,7 @@ static int enqueue_coarse(fcm_mg* h, const double* b, double* x) {
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(h->coarse_blocks);
   cfg.blockDim = dim3(kThreads);
-  cfg.dynamicSmemBytes = coarse_smem(L1.m, L1.M, L1.G);
+  cfg.dynamicSmemBytes = coarse_smem(L1.m, L1.M, L1.M > 0 ? coarse_group(L1.M) : L1.G);
   cfg.stream = h->stream;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeCooperative;
@@ -1783,7 +1787,7 @@ static int setup_impl(const fcm_grid* g, const fcm_params* prm, const fcm_slab* 
     const LevelDev& L1 = h->lev[1];
     int M1 = 0;
     h->kcoarse = coarse_kernel(L1.m, L1.G, &M1);
-    size_t sm = coarse_smem(L1.m, M1, L1.G);
+    size_t sm = coarse_smem(L1.m, M1, M1 > 0 ? coarse_group(M1) : L1.G);
     CU(cudaFuncSetAttribute(h->kcoarse, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     int per_sm = 0;
     cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, h->kcoarse, kThreads, sm);
