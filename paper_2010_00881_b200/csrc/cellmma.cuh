@@ -112,13 +112,26 @@ __device__ __forceinline__ double mma_cells(const CellOp& op, const int32_t* __r
       }
       const int a = rt * 8 + ar;
       const int i0 = mma_dof_index<M>(T, a, c0), i1 = mma_dof_index<M>(T, a, c1);
+      double x0 = 0.0, x1 = 0.0;
+      if (want_e) {   // x(a, n) lives in lane n*4 + a%4, fragment B[a/4], a/4 in {2rt, 2rt+1}
+        const int src0 = 2 * ac * 4 + (ar & 3), src1 = src0 + 4;
+        const double p00 = __shfl_sync(0xffffffffu, B[2 * rt], src0);
+        const double p10 = __shfl_sync(0xffffffffu, B[2 * rt], src1);
+        double p01 = 0.0, p11 = 0.0;
+        if (2 * rt + 1 < KT) {
+          p01 = __shfl_sync(0xffffffffu, B[2 * rt + 1], src0);
+          p11 = __shfl_sync(0xffffffffu, B[2 * rt + 1], src1);
+        }
+        x0 = (ar >> 2) ? p01 : p00;
+        x1 = (ar >> 2) ? p11 : p10;
+      }
       if (i0 >= 0) {
         atomicAdd(op.out + i0, s0 * d0);
-        if (want_e) energy = fma(load_in<FUSE>(op, i0), s0 / op.coef * d0, energy);
+        if (want_e) energy = fma(x0, s0 / op.coef * d0, energy);
       }
       if (i1 >= 0) {
         atomicAdd(op.out + i1, s1 * d1);
-        if (want_e) energy = fma(load_in<FUSE>(op, i1), s1 / op.coef * d1, energy);
+        if (want_e) energy = fma(x1, s1 / op.coef * d1, energy);
       }
     }
   }
