@@ -168,6 +168,7 @@ struct fcm_mg {
   std::vector<void*> allocs;
   // slab decomposition (slab.hpp; nranks == 1: single GPU, no collective)
   int rank = 0, nranks = 1, z0 = 0, z1 = 0;
+  bool multi = false;               // slab mode (nranks > 1, or FCM_FORCE_SLAB on one rank: tests)
   int ext_lo = 0, ext_n = 0;        // ghost-extended cell layers along the slab axis (relative)
   int64_t cut_first = 0;            // first owned cut cell in the cut-matrix array
   ncclComm_t comm = nullptr;
@@ -619,6 +620,20 @@ inline int grid_for(int64_t n, int sms) {
 // =========================================================================================
 // host helpers
 // =========================================================================================
+// Shared-memory opt-in of a kernel function: the attribute is per FUNCTION (shared by every
+// handle and level in the process), so it is raised to the device maximum once instead of to
+// the size one caller needs (a later, smaller setting would break an earlier handle).
+static int allow_smem(const void* func, size_t need) {
+  int dev = 0, mx = 0;
+  CU(cudaGetDevice(&dev));
+  CU(cudaDeviceGetAttribute(&mx, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+  cudaFuncAttributes fa;
+  CU(cudaFuncGetAttributes(&fa, func));
+  const int dyn_max = mx - (int)fa.sharedSizeBytes;   // static shared memory counts against the opt-in
+  if (need > (size_t)dyn_max) return fail(FCM_EINVAL, "kernel needs %zu B of dynamic shared memory (max %d)", need, dyn_max);
+  CU(cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn_max));
+  return FCM_OK;
+}
 static int gsz_rt(int M) { return M <= 4 ? 4 : (M <= 8 ? 8 : (M <= 16 ? 16 : 32)); }  // = gsz<M>()
 static int group_size(int m) {
   if (m <= 4) return 4;
@@ -779,7 +794,7 @@ static int copy(fcm_mg* h, double* y, const double* x, int64_t n) {
 // slab mode: sum the two copies of every interface plane of level q: pack the
 // bottom / top planes, grouped send/recv with the neighbours, add what came back.
 static int exchange(fcm_mg* h, int q, double* v) {
-  if (h->nranks <= 1) return FCM_OK;
+  if (!h->multi) return FCM_OK;
   LevelDev& Lv = h->lev[q];
   const int64_t nlo = Lv.n_lo, nhi = Lv.n_hi, stride = h->lev[h->g.p].n_lo + h->lev[h->g.p].n_hi;
   if (nlo + nhi == 0) return FCM_OK;
@@ -805,7 +820,7 @@ static int exchange(fcm_mg* h, int q, double* v) {
 
 // all-reduce (sum) of n device doubles in place (slab mode)
 static int allreduce(fcm_mg* h, double* v, int n) {
-  if (h->nranks <= 1) return FCM_OK;
+  if (!h->multi) return FCM_OK;
   NC(nccl().AllReduce(v, v, n, ncclFloat64, ncclSum, h->comm, h->stream));
   return FCM_OK;
 }
@@ -869,7 +884,7 @@ static int smooth_into(fcm_mg* h, int q, const double* r, double* x, double* cp_
 // goes through d unless x is known to be zero.
 static int smooth(fcm_mg* h, int q, const double* r, double* x, bool x_is_zero = false,
                   double* cp_dst = nullptr, const double* cp_src = nullptr) {
-  if (h->nranks <= 1) return smooth_into(h, q, r, x, cp_dst, cp_src);
+  if (!h->multi) return smooth_into(h, q, r, x, cp_dst, cp_src);
   LevelDev& Lv = h->lev[q];
   if (x_is_zero) {
     RC(smooth_into(h, q, r, x));
@@ -995,7 +1010,7 @@ static int enqueue_vcycle(fcm_mg* h, int q, const double* b, double* x) {
   const int64_t N = Lv.ndof;
   // single GPU, elementwise MMA path: the residual is double-buffered and each smoother launch
   // also writes "r = b" into the buffer the next residual scatters into (no copy launches)
-  const bool fuse = Lv.kmma && h->nranks == 1 && !Lv.patch && Lv.r2;
+  const bool fuse = Lv.kmma && !h->multi && !Lv.patch && Lv.r2;
   double* rb[2] = {Lv.r, Lv.r2 ? Lv.r2 : Lv.r};
   int cur = 0;
   RC(fill(h, x, 0.0, N));
@@ -1266,7 +1281,7 @@ static int setup_schwarz(fcm_mg* h, int q, const std::vector<uint8_t>& kind,
     CU(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, h->dev));
     const size_t sm = (size_t)mb * mb * 8 + (size_t)mb * 8;
     if (sm + 64 <= (size_t)max_smem) {
-      CU(cudaFuncSetAttribute(k_invert_blocks, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+      RC(allow_smem((const void*)k_invert_blocks, sm));
       int nbk = (int)std::min<int64_t>(nblk, (int64_t)h->num_sms * 8);
       k_invert_blocks<<<nbk, kThreads, sm, h->stream>>>(d_mats, mb, d_status, nblk);
     } else {   // large patch blocks: factor in a global scratch, one block per CTA at a time
@@ -1470,7 +1485,7 @@ static int setup_tiled(fcm_mg* h) {
   t.ntypes = ntypes;
   const int E2 = t.e[0] * t.e[1] * t.e[2], EC = t.ec[0] * t.ec[1] * t.ec[2];
   const size_t sm = tiled_smem_bytes(dim, nf, E2, EC, bt[0] * bt[1] * bt[2], 1 + ntypes + best_indiv);
-  CU(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+  RC(allow_smem(k, sm));
   int per_sm = 0;
   CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kTiledThreads, sm));
   const int nb = t.ntile[0] * t.ntile[1] * t.ntile[2];
@@ -1530,9 +1545,10 @@ static int setup_impl(const fcm_grid* g, const fcm_params* prm, const fcm_slab* 
       return fail(FCM_EINVAL, "bad slab (rank %d of %d, layers [%d, %d))", slab->rank, slab->nranks,
                   slab->z_begin, slab->z_end);
     h->rank = slab->rank; h->nranks = slab->nranks; h->z0 = slab->z_begin; h->z1 = slab->z_end;
+    h->multi = h->nranks > 1 || (getenv("FCM_FORCE_SLAB") && atoi(getenv("FCM_FORCE_SLAB")) > 0);
     if (h->nranks > 1 && prm->block == FCM_BLOCK_PATCH)
       return fail(FCM_EINVAL, "patchwise blocks are single-GPU (config 3); use elementwise blocks with slabs");
-    if (h->nranks > 1 && (n_cc < 0 || (n_cc > 0 && (!cc_cells || !cc_K1))))
+    if (h->multi && (n_cc < 0 || (n_cc > 0 && (!cc_cells || !cc_K1))))
       return fail(FCM_EINVAL, "slab setup needs every cut cell's leading p=1 block (replicated coarse level)");
   } else {
     h->z0 = 0; h->z1 = nsax;
@@ -1546,10 +1562,11 @@ static int setup_impl(const fcm_grid* g, const fcm_params* prm, const fcm_slab* 
   CU(cudaEventCreateWithFlags(&h->ev_out, cudaEventDisableTiming));
   CU(cudaEventRecord(h->ev_in, h->ustream));
   CU(cudaStreamWaitEvent(h->stream, h->ev_in, 0));
-  if (h->nranks > 1) {
+  if (h->multi) {
     if (!nccl().ok) return fail(FCM_ENCCL, "libnccl.so.2 could not be loaded");
     ncclUniqueId id;
-    std::memcpy(&id, slab->nccl_id, sizeof(id));
+    if (h->nranks == 1) NC(nccl().GetUniqueId(&id));   // forced slab mode on one rank
+    else std::memcpy(&id, slab->nccl_id, sizeof(id));
     NC(nccl().CommInitRank(&h->comm, h->nranks, id, h->rank));
   }
   Layout& L = h->L;
@@ -1636,8 +1653,7 @@ static int setup_impl(const fcm_grid* g, const fcm_params* prm, const fcm_slab* 
       for (int i = 0; i < 3; ++i)
         if (L.n[i] > 1024) Lv.kmma = nullptr;   // packed coordinates
       if (Lv.kmma) {
-        CU(cudaFuncSetAttribute(Lv.kmma, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)std::max(mma_smem(Lv.M), list_smem(Lv.m, Lv.G))));
+        RC(allow_smem(Lv.kmma, std::max(mma_smem(Lv.M), list_smem(Lv.m, Lv.G))));
         std::vector<int32_t> gc, gm;
         for (int64_t c = 0; c < h->ncell; ++c)
           if (kind_own[c] != 2) gc.push_back(mma_pack(h.get(), q, c));
@@ -1651,8 +1667,8 @@ static int setup_impl(const fcm_grid* g, const fcm_params* prm, const fcm_slab* 
         CU(cudaStreamSynchronize(h->stream));
       }
     }
-    if (Lv.kreg) CU(cudaFuncSetAttribute(Lv.kreg, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)level_reg_smem(Lv)));
-    CU(cudaFuncSetAttribute(Lv.klist, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)list_smem(Lv.m, Lv.G)));
+    if (Lv.kreg) RC(allow_smem(Lv.kreg, level_reg_smem(Lv)));
+    RC(allow_smem(Lv.klist, list_smem(Lv.m, Lv.G)));
     Lv.omega = q >= 2 ? prm->omega : 1.0;
     RC(h->alloc(&Lv.base, T.m));
     RC(h->alloc(&Lv.stride, T.m * 3));
@@ -1665,7 +1681,7 @@ static int setup_impl(const fcm_grid* g, const fcm_params* prm, const fcm_slab* 
     RC(h->alloc(&Lv.x, Lv.ndof));
     RC(h->alloc(&Lv.r, Lv.ndof));
     if (q >= 2) RC(h->alloc(&Lv.r2, Lv.ndof));
-    if (h->nranks > 1) {   // interface planes of this level (slab.hpp), exchange order
+    if (h->multi) {   // interface planes of this level (slab.hpp), exchange order
       std::vector<int32_t> lo, hi;
       if (h->z0 > 0) plane_slots(L, q, 0, lo);
       if (h->z1 < nsax) plane_slots(L, q, h->z1 - h->z0, hi);
@@ -1679,23 +1695,23 @@ static int setup_impl(const fcm_grid* g, const fcm_params* prm, const fcm_slab* 
       max_plane = std::max<int64_t>(max_plane, Lv.n_lo + Lv.n_hi);
     }
   }
-  if (h->nranks > 1) {
+  if (h->multi) {
     RC(h->alloc(&h->x_send, 2 * std::max<int64_t>(max_plane, 1)));
     RC(h->alloc(&h->x_recv, 2 * std::max<int64_t>(max_plane, 1)));
   }
   for (int q = 1; q <= g->p; ++q)
-    if (q >= 2 || (prm->coarse == FCM_COARSE_AS_PCG && h->nranks == 1))
+    if (q >= 2 || (prm->coarse == FCM_COARSE_AS_PCG && !h->multi))
       RC(setup_schwarz(h.get(), q, kind, cut_idx));
   for (int q = 2; q <= g->p; ++q)
     if (h->lev[q].patch) {
       const size_t sm = block_smem(h->lev[q].m, h->lev[q].mb);
-      CU(cudaFuncSetAttribute(k_block_smooth, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+      RC(allow_smem((const void*)k_block_smooth, sm));
     }
   RC(h->alloc(&h->d_coarse_iters, 2));
   CU(cudaMemsetAsync(h->d_coarse_iters, 0, 8, h->stream));
   // coarse level
   const int64_t n1 = L.ndof_level[1];
-  if (h->nranks > 1) {
+  if (h->multi) {
     // replicated global p = 1 problem: every rank solves it (fcm_slab; no inner-CG traffic)
     fcm_grid g1 = *g;
     g1.p = 1;
@@ -1788,7 +1804,7 @@ static int setup_impl(const fcm_grid* g, const fcm_params* prm, const fcm_slab* 
     int M1 = 0;
     h->kcoarse = coarse_kernel(L1.m, L1.G, &M1);
     size_t sm = coarse_smem(L1.m, M1, M1 > 0 ? coarse_group(M1) : L1.G);
-    CU(cudaFuncSetAttribute(h->kcoarse, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    RC(allow_smem(h->kcoarse, sm));
     int per_sm = 0;
     cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, h->kcoarse, kThreads, sm);
     if (e != cudaSuccess || per_sm < 1) return fail(FCM_ECUDA, "coarse kernel occupancy query failed");
@@ -1810,7 +1826,7 @@ static int setup_impl(const fcm_grid* g, const fcm_params* prm, const fcm_slab* 
   RC(h->alloc(&h->d_partA, 2 * kMaxPartials));
   RC(h->alloc(&h->d_partB, 2 * kMaxPartials));
   RC(h->alloc(&h->d_partC, 2 * kMaxPartials));
-  if (h->nranks > 1) {
+  if (h->multi) {
     std::vector<uint8_t> own;
     owned_mask(L, g->p, h->z0 > 0, own);
     RC(h->alloc(&h->d_own, own.size()));
@@ -1990,7 +2006,7 @@ static int capture_fcg(fcm_mg* h) {
   const int nbc = cellop_nblocks(h, p, OP_APPLY);
   // slab mode: partial sums are finalised on each rank, all-reduced, and the update kernels
   // read the reduced scalars (red[]); dots skip the interface DOFs this rank does not own
-  const bool slab = h->nranks > 1;
+  const bool slab = h->multi;
   const uint8_t* own = slab ? h->d_own : nullptr;
   double* red = h->d_s->red;
   // init: x = 0, r = b, z = V(r), rz = z.r, p = z
@@ -2058,7 +2074,7 @@ static int pcg_core(fcm_mg* h, double rtol, int32_t maxit, int32_t* iters, doubl
   RC(capture_fcg(h));
   // ||b||^2
   const int nbd = dot_blocks(h);
-  k_dot<<<nbd, kThreads, 0, h->stream>>>(h->f_b, h->f_b, N, h->d_partA, h->nranks > 1 ? h->d_own : nullptr);
+  k_dot<<<nbd, kThreads, 0, h->stream>>>(h->f_b, h->f_b, N, h->d_partA, h->multi ? h->d_own : nullptr);
   k_finalize<<<1, 32, 0, h->stream>>>(&h->d_s->bb, h->d_partA, nbd);
   h->count(2);
   RC(allreduce(h, &h->d_s->bb, 1));

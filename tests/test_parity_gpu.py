@@ -293,3 +293,28 @@ def test_cfg2_full_size():
     xo[pair.pos] = xs.cpu().numpy()
     true_res = np.linalg.norm(pair.P.b - pair.P.A @ xo) / np.linalg.norm(pair.P.b)
     assert hist[-1] < 1e-10 and true_res < 2e-10 and 25 <= its <= 50
+
+
+@pytest.mark.parametrize("case", ["3d_p2", "3d_trunk_elast"])
+def test_forced_slab_mode_single_rank(case, monkeypatch):
+    # the slab machinery on one rank (FCM_FORCE_SLAB): NCCL communicator of size 1, all-reduced
+    # dots with the owner mask, smoother increments through d, and the REPLICATED coarse level
+    # (all-gather of the coarse residual + the global p = 1 handle on the same stream) -- the
+    # device side of the multi-GPU path minus the plane exchange, against the single-GPU path
+    from paper_2010_00881_b200.fcm import Solver, generate
+    cfg = CASES[case]()
+    G = generate(cfg)
+    m1 = (2 ** cfg.dim) * cfg.n_f
+    S1 = Solver.from_problem(cfg, G)
+    monkeypatch.setenv("FCM_FORCE_SLAB", "1")
+    S2 = Solver(cfg, G.K_ref, G.kind, G.cut_cells, G.cut_K, slab=(0, 1, 0, cfg.n, None),
+                coarse_cut=(G.cut_cells, np.ascontiguousarray(G.cut_K[:, :m1, :m1])))
+    b1, b2 = S1.load(G), S2.load(G)
+    assert torch.equal(b1, b2)
+    assert rel(S2.vcycle(b2).cpu().numpy(), S1.vcycle(b1).cpu().numpy()) <= 1e-10
+    xc1, it1 = S1.coarse_solve(b1[: S1.ndofs(1)].clone())
+    xc2, it2 = S2.coarse_solve(b2[: S2.ndofs(1)].clone())
+    assert abs(it1 - it2) <= 1 and rel(xc2.cpu().numpy(), xc1.cpu().numpy()) <= 1e-10
+    x1, i1, _ = S1.pcg_solve(b1)
+    x2, i2, _ = S2.pcg_solve(b2)
+    assert abs(i1 - i2) <= 1 and rel(x2.cpu().numpy(), x1.cpu().numpy()) <= 1e-8
