@@ -70,16 +70,6 @@ struct TiledArgs {
   int maxit;
   int* iters;               // [0] = this solve, [1] += this solve
   unsigned long long* prof; // optional per-block phase times (ns): [nblocks][4]
-  // k_coarse_mma (coarse_mma.cuh): per-brick lists of the individual cells with their packed
-  // matrices in 32-cell SoA chunks (host-built; brick b owns list positions [off[b], off[b+1]),
-  // off[b] a multiple of 32), read through L1 instead of being staged in shared memory
-  const int32_t* ism_off;   // smoother: irregular blocks of the brick's cell box
-  const int32_t* ism_cell;  // cell-box index (-1 padding)
-  const double* ism_mat;
-  const int32_t* iop_off;   // operator: cut cells touching the brick
-  const int32_t* iop_cell;
-  const double* iop_mat;
-  int max_groups;           // shared-memory capacity of each regular-group list
 };
 
 __device__ __forceinline__ unsigned long long t_now() {

@@ -30,7 +30,6 @@
 #include "cellop.cuh"
 #include "coarse.cuh"
 #include "coarse_tiled.cuh"
-#include "coarse_mma.cuh"
 #include "blocks.cuh"
 #include "cellmma.cuh"
 #include "common.hpp"
@@ -1409,140 +1408,6 @@ static int setup_tiled(fcm_mg* h) {
   }
   const LevelDev& L1 = h->lev[1];
   const bool jac = h->prm.coarse == FCM_COARSE_JACOBI_PCG;
-  // ---- k_coarse_mma (coarse_mma.cuh): 3D scalar AS levels; individual matrices from L1/L2 ----
-  const int v2env = getenv("FCM_COARSE_MMA") ? atoi(getenv("FCM_COARSE_MMA")) : 1;
-  if (v2env && dim == 3 && nf == 1 && !jac && L1.n_types <= 64) {
-    int max_smem = 0;
-    CU(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, h->dev));
-    cudaFuncAttributes fa;
-    CU(cudaFuncGetAttributes(&fa, (const void*)k_coarse_mma));
-    const size_t cap = (size_t)max_smem - fa.sharedSizeBytes;
-    double best = 1e300;
-    int bt[3] = {0, 0, 0};
-    for (int tz = 1; tz <= B[2]; ++tz)
-      for (int ty = 1; ty <= B[1]; ++ty)
-        for (int tx = 1; tx <= B[0]; ++tx) {
-          const int64_t nt = (int64_t)((B[0] + tx - 1) / tx) * ((B[1] + ty - 1) / ty) * ((B[2] + tz - 1) / tz);
-          if (nt > h->num_sms) continue;
-          const int64_t E2 = (int64_t)(tx + 4) * (ty + 4) * (tz + 4), EC = (int64_t)(tx + 3) * (ty + 3) * (tz + 3);
-          const int64_t T = (int64_t)tx * ty * tz, E1 = (int64_t)(tx + 2) * (ty + 2) * (tz + 2);
-          if (EC >= 8192 || mma_tiled_smem_bytes((int)E2, (int)EC, (int)T, L1.n_types, (int)EC) > cap) continue;
-          const double cost = 2.0 * EC + E1 + T + 0.5 * E2;   // cell products, vertex sums, updates
-          if (cost < best) { best = cost; bt[0] = tx; bt[1] = ty; bt[2] = tz; }
-        }
-    if (bt[0] > 0) {
-      for (int i = 0; i < 3; ++i) {
-        t.tile[i] = bt[i];
-        t.ntile[i] = (B[i] + bt[i] - 1) / bt[i];
-        t.e[i] = bt[i] + 4;
-        t.ec[i] = bt[i] + 3;
-      }
-      const int nb = t.ntile[0] * t.ntile[1] * t.ntile[2];
-      const int E2 = t.e[0] * t.e[1] * t.e[2], EC = t.ec[0] * t.ec[1] * t.ec[2], T = bt[0] * bt[1] * bt[2];
-      // per-brick individual lists, padded to 32, matrices packed in 32-cell SoA chunks
-      const int m = L.m;
-      const int nx = L.n[0], ny = L.n[1], nz = L.n[2];
-      std::vector<uint8_t> kind(h->ncell);
-      std::vector<int32_t> cidx(h->ncell);
-      CU(cudaMemcpy(kind.data(), h->d_kind, h->ncell, cudaMemcpyDeviceToHost));
-      CU(cudaMemcpy(cidx.data(), h->d_cut_idx, h->ncell * 4, cudaMemcpyDeviceToHost));
-      std::vector<double> irr((size_t)L1.n_irr * 64), cutK;
-      if (L1.n_irr) CU(cudaMemcpy(irr.data(), L1.irr_inv, irr.size() * 8, cudaMemcpyDeviceToHost));
-      int64_t ncut_all = 0;
-      for (int64_t c = 0; c < h->ncell; ++c) ncut_all = std::max<int64_t>(ncut_all, cidx[c] + 1);
-      cutK.resize((size_t)ncut_all * m * m);
-      if (ncut_all) CU(cudaMemcpy(cutK.data(), h->d_cutK, cutK.size() * 8, cudaMemcpyDeviceToHost));
-      std::vector<int32_t> sm_off(nb + 1, 0), op_off(nb + 1, 0), sm_cell, op_cell;
-      std::vector<const double*> sm_src, op_src;
-      std::vector<int> sm_ld, op_ld;
-      for (int b = 0; b < nb; ++b) {
-        const int ti[3] = {b % t.ntile[0], (b / t.ntile[0]) % t.ntile[1], b / (t.ntile[0] * t.ntile[1])};
-        int o[3];
-        for (int i = 0; i < 3; ++i) o[i] = t.blo[i] + ti[i] * bt[i] - 2;
-        for (int lz = 0; lz < t.ec[2]; ++lz)
-          for (int ly = 0; ly < t.ec[1]; ++ly)
-            for (int lx = 0; lx < t.ec[0]; ++lx) {
-              const int cx = o[0] + lx, cy = o[1] + ly, cz = o[2] + lz;
-              if (cx < 0 || cy < 0 || cz < 0 || cx >= nx || cy >= ny || cz >= nz) continue;
-              const int64_t c = ((int64_t)cz * ny + cy) * nx + cx;
-              const int lc = (lz * t.ec[1] + ly) * t.ec[0] + lx;
-              if (L1.blk_h[c] >= 0) {
-                sm_cell.push_back(lc);
-                sm_src.push_back(irr.data() + (size_t)L1.blk_h[c] * 64);
-                sm_ld.push_back(8);
-              }
-              const bool tbox = lx >= 1 && lx <= bt[0] + 1 && ly >= 1 && ly <= bt[1] + 1 && lz >= 1 && lz <= bt[2] + 1;
-              if (kind[c] == 2 && tbox) {
-                op_cell.push_back(lc);
-                op_src.push_back(cutK.data() + (size_t)cidx[c] * m * m);
-                op_ld.push_back(m);
-              }
-            }
-        while (sm_cell.size() % 32) { sm_cell.push_back(-1); sm_src.push_back(nullptr); sm_ld.push_back(0); }
-        while (op_cell.size() % 32) { op_cell.push_back(-1); op_src.push_back(nullptr); op_ld.push_back(0); }
-        sm_off[b + 1] = (int32_t)sm_cell.size();
-        op_off[b + 1] = (int32_t)op_cell.size();
-      }
-      auto soa = [&](const std::vector<const double*>& src, const std::vector<int>& ld) {
-        std::vector<double> out(src.size() * 36, 0.0);
-        for (size_t i = 0; i < src.size(); ++i) {
-          if (!src[i]) continue;
-          for (int ra = 0; ra < 8; ++ra)
-            for (int cb = 0; cb <= ra; ++cb)
-              out[((i / 32) * 36 + ra * (ra + 1) / 2 + cb) * 32 + (i % 32)] = src[i][ra * ld[i] + cb];
-        }
-        return out;
-      };
-      std::vector<double> sm_mat = soa(sm_src, sm_ld), op_mat = soa(op_src, op_ld);
-      int32_t *d_smo, *d_smc, *d_opo, *d_opc;
-      double *d_smm, *d_opm;
-      RC(h->alloc(&d_smo, sm_off.size())); RC(h->alloc(&d_opo, op_off.size()));
-      RC(h->alloc(&d_smc, std::max<size_t>(1, sm_cell.size()))); RC(h->alloc(&d_opc, std::max<size_t>(1, op_cell.size())));
-      RC(h->alloc(&d_smm, std::max<size_t>(1, sm_mat.size()))); RC(h->alloc(&d_opm, std::max<size_t>(1, op_mat.size())));
-      CU(cudaMemcpy(d_smo, sm_off.data(), sm_off.size() * 4, cudaMemcpyHostToDevice));
-      CU(cudaMemcpy(d_opo, op_off.data(), op_off.size() * 4, cudaMemcpyHostToDevice));
-      if (!sm_cell.empty()) CU(cudaMemcpy(d_smc, sm_cell.data(), sm_cell.size() * 4, cudaMemcpyHostToDevice));
-      if (!op_cell.empty()) CU(cudaMemcpy(d_opc, op_cell.data(), op_cell.size() * 4, cudaMemcpyHostToDevice));
-      if (!sm_mat.empty()) CU(cudaMemcpy(d_smm, sm_mat.data(), sm_mat.size() * 8, cudaMemcpyHostToDevice));
-      if (!op_mat.empty()) CU(cudaMemcpy(d_opm, op_mat.data(), op_mat.size() * 8, cudaMemcpyHostToDevice));
-      t.ism_off = d_smo; t.ism_cell = d_smc; t.ism_mat = d_smm;
-      t.iop_off = d_opo; t.iop_cell = d_opc; t.iop_mat = d_opm;
-      t.max_groups = EC;
-      t.ntypes = L1.n_types;
-      t.kind = h->d_kind; t.cut_idx = h->d_cut_idx; t.cutK = h->d_cutK; t.ldK = L.m; t.Kref = h->d_Kref;
-      t.alpha = h->alpha; t.jacobi = 0;
-      t.blk = L1.blk; t.type_inv = L1.type_inv; t.irr_inv = L1.irr_inv; t.inv_alpha = 1.0 / h->alpha;
-      const size_t sm = mma_tiled_smem_bytes(E2, EC, T, L1.n_types, EC);
-      const void* kk = (const void*)k_coarse_mma;
-      RC(allow_smem(kk, sm));
-      int per_sm = 0;
-      CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kk, kTiledThreads, sm));
-      if (per_sm >= 1 && nb <= per_sm * h->num_sms) {
-        const int64_t n1 = L.ndof_level[1];
-        RC(h->alloc(&t.wpub[0], n1));
-        RC(h->alloc(&t.wpub[1], n1));
-        RC(h->alloc(&t.part, (size_t)6 * nb));
-        RC(h->alloc(&t.ctl, 1));
-        CU(cudaMemsetAsync(t.ctl, 0, sizeof(TiledCtl), h->stream));
-        t.rtol2 = h->prm.coarse_rtol * h->prm.coarse_rtol;
-        t.maxit = h->prm.coarse_maxit;
-        t.iters = h->d_coarse_iters;
-        if (getenv("FCM_TILED_PROF")) {
-          RC(h->alloc(&t.prof, (size_t)4 * nb));
-          CU(cudaMemsetAsync(t.prof, 0, (size_t)32 * nb, h->stream));
-        }
-        if (getenv("FCM_VERBOSE"))
-          fprintf(stderr, "[fcm] mma tiled coarse: box %d x %d x %d, tile %d x %d x %d, %d blocks, %d types, "
-                  "individual %zu (smoother) %zu (operator) list entries, smem %zu B\n", B[0], B[1], B[2], bt[0],
-                  bt[1], bt[2], nb, L1.n_types, sm_cell.size(), op_cell.size(), sm);
-        h->tiled = t;
-        h->ktiled = kk;
-        h->t_blocks = nb;
-        h->t_smem = sm;
-        return FCM_OK;
-      }
-    }
-  }
   // individual matrices per cell (cut-cell operator block + irregular Schwarz inverse), and
   // their 3D prefix sums for box counts
   const int nx = L.n[0], ny = L.n[1], nz = L.n[2];
