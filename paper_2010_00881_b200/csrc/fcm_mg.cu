@@ -169,6 +169,7 @@ struct fcm_mg {
   // slab decomposition (slab.hpp; nranks == 1: single GPU, no collective)
   int rank = 0, nranks = 1, z0 = 0, z1 = 0;
   bool multi = false;               // slab mode (nranks > 1, or FCM_FORCE_SLAB on one rank: tests)
+  int mma_bps = 4, list_bps = 8;    // blocks per SM of the MMA / list parts of k_cell_mma
   int ext_lo = 0, ext_n = 0;        // ghost-extended cell layers along the slab axis (relative)
   int64_t cut_first = 0;            // first owned cut cell in the cut-matrix array
   ncclComm_t comm = nullptr;
@@ -693,12 +694,13 @@ static void cellop_grid(const fcm_mg* h, int q, int mode, int* nb_reg, int* nb_l
   const int64_t cpb = (kThreads / 32) * (32 / Lv.G);  // cells per block on the list path
   const bool mma = Lv.kmma && (mode == OP_APPLY ? Lv.gA_cells != nullptr : Lv.gS_cells != nullptr);
   if (mma) {
-    // one resident wave (4 blocks per SM); warps loop over the groups
+    // MMA blocks: h->mma_bps per SM (staging of the A fragments amortised over the groups a
+    // warp loops over); list blocks: up to list_bps per SM
     const int64_t ng = mode == OP_APPLY ? Lv.nA : Lv.nS;
     *nb_reg = (int)std::max<int64_t>(1, std::min<int64_t>((ng + kThreads / 32 - 1) / (kThreads / 32),
-                                                          (int64_t)h->num_sms * 4));
+                                                          (int64_t)h->num_sms * h->mma_bps));
     const int64_t nl = mode == OP_APPLY ? h->ncut : Lv.n_irr;
-    *nb_list = (int)std::min<int64_t>((nl + cpb - 1) / cpb, cap);
+    *nb_list = (int)std::min<int64_t>((nl + cpb - 1) / cpb, (int64_t)h->num_sms * h->list_bps);
     return;
   }
   if (Lv.M > 0) {
@@ -1539,6 +1541,8 @@ static int setup_impl(const fcm_grid* g, const fcm_params* prm, const fcm_slab* 
   h->g = *g;
   h->prm = *prm;
   h->alpha = alpha;
+  if (const char* e = getenv("FCM_MMA_BPS")) h->mma_bps = std::max(1, atoi(e));
+  if (const char* e = getenv("FCM_LIST_BPS")) h->list_bps = std::max(1, atoi(e));
   if (slab) {
     if (slab->nranks < 1 || slab->rank < 0 || slab->rank >= slab->nranks || slab->z_begin < 0 ||
         slab->z_end > nsax || slab->z_begin >= slab->z_end)
