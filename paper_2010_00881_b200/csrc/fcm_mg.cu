@@ -249,7 +249,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_cell_reg(CellOp op) {
 // (cellmma.cuh), the others the individual list (list_cells); every block also does its share
 // of the fused copy.  smem [Tab][max(A fragments, list scratch)].
 template <int M, int G>
-__global__ void __launch_bounds__(kThreads, 4) k_cell_mma(MmaOp g, int nb_mma) {
+__global__ void __launch_bounds__(kThreads, M > 32 ? 2 : 4) k_cell_mma(MmaOp g, int nb_mma) {
   extern __shared__ __align__(16) unsigned char smem[];
   Tab& T = *reinterpret_cast<Tab*>(smem);
   double* As = reinterpret_cast<double*>(smem + sizeof(Tab));
@@ -576,7 +576,7 @@ const void* reg_kernel(int m, int* M_out, bool ts1) {
 }
 const void* mma_kernel(int m) {
 #define CASE(MM) case MM: return (const void*)k_cell_mma<MM, gsz<MM>()>;
-  switch (m) { FCM_FOR_M(CASE) default: break; }
+  switch (m) { FCM_FOR_M(CASE) CASE(64) default: break; }   // 64: tensor p = 3 (config 5)
 #undef CASE
   return nullptr;
 }
@@ -675,7 +675,8 @@ static CellOp make_op(fcm_mg* h, int q, int mode, const double* in, double* out,
   op.kind = h->d_kind; op.cut_idx = h->d_cut_idx; op.Kref = h->d_Kref; op.cutK = h->d_cutK;
   op.ldK = h->L.m; op.alpha = h->alpha;
   op.blk = Lv.blk; op.irr_inv = Lv.irr_inv; op.type_inv = Lv.type_inv; op.inv_alpha = 1.0 / h->alpha;
-  if (Lv.M > 0) {
+  const bool mma = Lv.kmma && (mode == OP_APPLY ? Lv.gA_cells != nullptr : Lv.gS_cells != nullptr);
+  if (Lv.M > 0 || mma) {   // the regular population has its own kernel: list = individual cells
     if (mode == OP_APPLY) {
       op.list = h->d_cut_list; op.nlist = (int32_t)h->ncut;
       op.list_mats = h->d_cutK + (size_t)h->cut_first * h->L.m * h->L.m; op.list_ld = h->L.m;
@@ -739,7 +740,7 @@ static int launch_cellop(fcm_mg* h, int q, const CellOp& op, double* cp_dst = nu
     int nbm = nb_reg;
     void* args[] = {&g, &nbm};
     cudaError_t e = cudaLaunchKernel(Lv.kmma, dim3(nb_reg + nb_list), dim3(kThreads), args,
-                                     std::max(mma_smem(Lv.M), list_smem(Lv.m, Lv.G)), h->stream);
+                                     std::max(mma_smem(Lv.m), list_smem(Lv.m, Lv.G)), h->stream);
     h->count();
     if (e != cudaSuccess) return fail(FCM_ECUDA, "mma kernel launch: %s", cudaGetErrorString(e));
     return FCM_OK;
@@ -1325,7 +1326,7 @@ static int setup_schwarz(fcm_mg* h, int q, const std::vector<uint8_t>& kind,
   Lv.nanchor = nanchor;
   Lv.has_as = true;
   Lv.n_types = (int32_t)ntypes;
-  if (Lv.kmma && !patch && mb == Lv.M) {   // MMA groups: 8 regular cells of one type slot
+  if (Lv.kmma && !patch && mb == Lv.m) {   // MMA groups: 8 regular cells of one type slot
     std::vector<std::vector<int32_t>> by_slot(ntypes);
     for (int64_t A = 0; A < nanchor; ++A)
       if (blk[A] < 0 && blk[A] != kBlkNone) by_slot[(-blk[A] - 1) & 0xfff].push_back((int32_t)A);
@@ -1652,12 +1653,12 @@ static int setup_impl(const fcm_grid* g, const fcm_params* prm, const fcm_slab* 
       }
     }
     Lv.klist = list_kernel(Lv.G);
-    if (Lv.M > 0 && !(getenv("FCM_CELL_MMA") && atoi(getenv("FCM_CELL_MMA")) == 0)) {
-      Lv.kmma = gsz_rt(Lv.M) == Lv.G ? mma_kernel(Lv.M) : nullptr;
+    if (!(getenv("FCM_CELL_MMA") && atoi(getenv("FCM_CELL_MMA")) == 0)) {
+      Lv.kmma = gsz_rt(Lv.m) == Lv.G ? mma_kernel(Lv.m) : nullptr;
       for (int i = 0; i < 3; ++i)
         if (L.n[i] > 1024) Lv.kmma = nullptr;   // packed coordinates
       if (Lv.kmma) {
-        RC(allow_smem(Lv.kmma, std::max(mma_smem(Lv.M), list_smem(Lv.m, Lv.G))));
+        RC(allow_smem(Lv.kmma, std::max(mma_smem(Lv.m), list_smem(Lv.m, Lv.G))));
         std::vector<int32_t> gc, gm;
         for (int64_t c = 0; c < h->ncell; ++c)
           if (kind_own[c] != 2) gc.push_back(mma_pack(h.get(), q, c));
