@@ -64,6 +64,9 @@ struct Scalars {
   int flag;  // bit0: p^T A p <= 0
   int pad;
   double red[4];  // slab mode: all-reduced partial sums (pq | zr, zr_old | rz)
+  // device-side FCG loop (k_fcg_check): iteration count, stop test, history
+  int it, maxit;
+  double rtol2;
 };
 
 struct LevelDev {
@@ -161,6 +164,10 @@ struct fcm_mg {
   double* d_partC = nullptr;
   // graphs
   cudaGraphExec_t g_vc = nullptr, g_it1 = nullptr, g_it2 = nullptr, g_init = nullptr;
+  cudaGraphExec_t g_solve = nullptr;   // whole FCG: init, it1, check, WHILE { it2, it1, check }
+  int64_t n_loop = 0, n_head = 0;      // kernels per loop trip / in the head
+  double* d_hist = nullptr;
+  int hist_cap = 0;
   int64_t n_vc = 0, n_it1 = 0, n_it2 = 0, n_init = 0;  // kernels per graph
   int64_t launches = 0;
   int64_t* count_target = nullptr;  // during capture: where launches are counted
@@ -202,7 +209,7 @@ struct fcm_mg {
   }
   ~fcm_mg();
   void release() {
-    for (auto g : {g_vc, g_it1, g_it2, g_init})
+    for (auto g : {g_vc, g_it1, g_it2, g_init, g_solve})
       if (g) cudaGraphExecDestroy(g);
     for (void* p : allocs) cudaFree(p);
     if (h_s) cudaFreeHost(h_s);
@@ -453,6 +460,17 @@ __global__ void k_fcg_update2(Scalars* s, const double* partA, const double* par
   __syncthreads();
   if (blockIdx.x == 0 && threadIdx.x == 0) { s->zr = zr; s->zr_old = zro; }
   // rz updated by the last block to finish reading it: use a separate write after grid end
+}
+// device-side FCG loop: after each x-update, count the iteration, record ||r||/||b||, and keep
+// the WHILE node running unless converged (strict <, reading R6), maxit reached, p^T A p <= 0
+// or NaN (the host reports the reason after the single synchronisation)
+__global__ void k_fcg_check(Scalars* s, cudaGraphConditionalHandle cond, double* hist) {
+  if (threadIdx.x != 0) return;
+  const int it = ++s->it;
+  const double rel2 = s->rr / s->bb;
+  if (hist && it <= s->maxit + 1) hist[it] = sqrt(rel2);
+  const bool stop = (s->flag & 1) || !(rel2 == rel2) || rel2 < s->rtol2 || it >= s->maxit;
+  cudaGraphSetConditional(cond, stop ? 0u : 1u);
 }
 __global__ void k_set_rz(Scalars* s) {
   if (threadIdx.x == 0) s->rz = s->zr;
@@ -2015,7 +2033,7 @@ static int capture_fcg(fcm_mg* h) {
   const uint8_t* own = slab ? h->d_own : nullptr;
   double* red = h->d_s->red;
   // init: x = 0, r = b, z = V(r), rz = z.r, p = z
-  RC(capture(h, &h->g_init, &h->n_init, [&]() -> int {
+  auto init_body = [&]() -> int {
     k_fcg_start<<<grid_for(N, h->num_sms), kThreads, 0, h->stream>>>(h->f_x, h->f_r, h->f_b, N);
     h->count();
     RC(enqueue_vcycle(h, p, h->f_r, z));
@@ -2031,9 +2049,9 @@ static int capture_fcg(fcm_mg* h) {
     h->count();
     CU(cudaGetLastError());
     return FCM_OK;
-  }));
+  };
   // iteration part 1: q = A p (energy partials pq), update x, r, r_old, rr
-  RC(capture(h, &h->g_it1, &h->n_it1, [&]() -> int {
+  auto it1_body = [&](bool d2h) -> int {
     RC(fill(h, h->f_q, 0.0, N));
     RC(launch_cellop(h, p, make_op(h, p, OP_APPLY, h->f_p, h->f_q, 1.0, h->d_partB)));
     RC(exchange(h, p, h->f_q));
@@ -2049,11 +2067,11 @@ static int capture_fcg(fcm_mg* h) {
     h->count();
     CU(cudaGetLastError());
     if (slab) RC(allreduce(h, &h->d_s->rr, 1));
-    CU(cudaMemcpyAsync(h->h_s, h->d_s, sizeof(Scalars), cudaMemcpyDeviceToHost, h->stream));
+    if (d2h) CU(cudaMemcpyAsync(h->h_s, h->d_s, sizeof(Scalars), cudaMemcpyDeviceToHost, h->stream));
     return FCM_OK;
-  }));
+  };
   // iteration part 2: z = V(r), beta, p = z + beta p
-  RC(capture(h, &h->g_it2, &h->n_it2, [&]() -> int {
+  auto it2_body = [&]() -> int {
     RC(enqueue_vcycle(h, p, h->f_r, z));
     k_dot2<<<nbd, kThreads, 0, h->stream>>>(z, h->f_r, h->f_ro, N, h->d_partA, h->d_partB, own);
     h->count();
@@ -2069,13 +2087,77 @@ static int capture_fcg(fcm_mg* h) {
     h->count();
     CU(cudaGetLastError());
     return FCM_OK;
-  }));
+  };
+  RC(capture(h, &h->g_init, &h->n_init, init_body));
+  RC(capture(h, &h->g_it1, &h->n_it1, [&]() { return it1_body(true); }));
+  RC(capture(h, &h->g_it2, &h->n_it2, it2_body));
+  // the whole solve as ONE graph with a device-side WHILE loop (conditional node): no host
+  // round trip per iteration (FCM_HOST_LOOP=1 keeps the per-iteration host loop)
+  // (slab mode keeps the host loop: NCCL work is not placed inside conditional bodies)
+  if (!h->g_solve && !h->multi && !(getenv("FCM_HOST_LOOP") && atoi(getenv("FCM_HOST_LOOP")) > 0)) {
+    cudaGraph_t G, body;
+    CU(cudaGraphCreate(&G, 0));
+    cudaGraphConditionalHandle cond;
+    CU(cudaGraphConditionalHandleCreate(&cond, G, 1, cudaGraphCondAssignDefault));
+    int64_t nk = 0;
+    h->count_target = &nk;
+    CU(cudaStreamBeginCaptureToGraph(h->stream, G, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+    int rc = init_body();
+    if (rc >= 0) rc = it1_body(false);
+    if (rc >= 0) {
+      k_fcg_check<<<1, 32, 0, h->stream>>>(h->d_s, cond, h->d_hist);
+      h->count();
+    }
+    cudaGraphNode_t wnode = nullptr;
+    if (rc >= 0) {
+      cudaStreamCaptureStatus st;
+      cudaGraph_t cg_;
+      const cudaGraphNode_t* deps = nullptr;
+      size_t ndeps = 0;
+      cudaError_t e = cudaStreamGetCaptureInfo_v3(h->stream, &st, nullptr, &cg_, &deps, nullptr, &ndeps);
+      cudaGraphNodeParams cp{};
+      cp.type = cudaGraphNodeTypeConditional;
+      cp.conditional.handle = cond;
+      cp.conditional.type = cudaGraphCondTypeWhile;
+      cp.conditional.size = 1;
+      if (e == cudaSuccess) e = cudaGraphAddNode(&wnode, G, deps, ndeps, &cp);
+      if (e == cudaSuccess) e = cudaStreamUpdateCaptureDependencies(h->stream, &wnode, 1, cudaStreamSetCaptureDependencies);
+      if (e != cudaSuccess) rc = fail(FCM_ECUDA, "conditional node: %s", cudaGetErrorString(e));
+      body = cp.conditional.phGraph_out[0];
+    }
+    cudaGraph_t Gout;
+    cudaError_t e = cudaStreamEndCapture(h->stream, &Gout);
+    h->n_head = nk;
+    if (rc >= 0 && e == cudaSuccess) {
+      nk = 0;
+      CU(cudaStreamBeginCaptureToGraph(h->stream, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+      rc = it2_body();
+      if (rc >= 0) rc = it1_body(false);
+      if (rc >= 0) {
+        k_fcg_check<<<1, 32, 0, h->stream>>>(h->d_s, cond, h->d_hist);
+        h->count();
+      }
+      cudaGraph_t bout;
+      e = cudaStreamEndCapture(h->stream, &bout);
+      h->n_loop = nk;
+    }
+    h->count_target = nullptr;
+    if (rc >= 0 && e == cudaSuccess) e = cudaGraphInstantiate(&h->g_solve, G, 0);
+    cudaGraphDestroy(G);
+    if (rc < 0) return rc;
+    if (e != cudaSuccess) return fail(FCM_ECUDA, "device-loop graph: %s", cudaGetErrorString(e));
+  }
   return FCM_OK;
 }
 
 static int pcg_core(fcm_mg* h, double rtol, int32_t maxit, int32_t* iters, double* hist) {
   const int p = h->g.p;
   const int64_t N = h->lev[p].ndof;
+  if (maxit + 2 > h->hist_cap) {   // device history buffer (baked into the device-loop graph)
+    if (h->g_solve) { cudaGraphExecDestroy(h->g_solve); h->g_solve = nullptr; }
+    h->hist_cap = std::max(maxit + 2, 512);
+    RC(h->alloc(&h->d_hist, h->hist_cap));
+  }
   RC(capture_fcg(h));
   // ||b||^2
   const int nbd = dot_blocks(h);
@@ -2096,6 +2178,29 @@ static int pcg_core(fcm_mg* h, double rtol, int32_t maxit, int32_t* iters, doubl
     RC(fill(h, h->f_x, 0.0, N));
     if (iters) *iters = 0;
     return FCM_OK;
+  }
+  if (h->g_solve) {   // one graph launch, one synchronisation
+    h->h_s->it = 0;
+    h->h_s->maxit = maxit;
+    h->h_s->rtol2 = rtol * rtol;
+    CU(cudaMemcpyAsync(&h->d_s->it, &h->h_s->it, sizeof(int) * 2 + sizeof(double), cudaMemcpyHostToDevice, h->stream));
+    CU(cudaGraphLaunch(h->g_solve, h->stream));
+    CU(cudaMemcpyAsync(h->h_s, h->d_s, sizeof(Scalars), cudaMemcpyDeviceToHost, h->stream));
+    CU(cudaStreamSynchronize(h->stream));
+    const Scalars s = *h->h_s;
+    it = s.it;
+    h->launches += h->n_head + (int64_t)(it - 1) * h->n_loop;
+    h->stat_vcycles = it;
+    if (hist && it > 0) {
+      std::vector<double> hh(it + 1);
+      CU(cudaMemcpy(hh.data(), h->d_hist, (it + 1) * sizeof(double), cudaMemcpyDeviceToHost));
+      for (int i = 1; i <= it; ++i) hist[i] = hh[i];
+    }
+    if (iters) *iters = it;
+    if (s.flag & 1) return fail(FCM_EINDEF, "p^T A p <= 0 at FCG iteration %d", it);
+    const double rel = std::sqrt(s.rr / bb);
+    if (!(rel == rel)) return fail(FCM_EINDEF, "NaN residual at FCG iteration %d", it);
+    return rel < rtol ? FCM_OK : FCM_NOT_CONVERGED;
   }
   RC(run_graph(h, h->g_init, h->n_init));
   h->stat_vcycles++;
