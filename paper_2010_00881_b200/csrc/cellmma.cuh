@@ -14,9 +14,12 @@
 
 namespace fcm {
 
-// group cell entry: cx | cy << 10 | cz << 20 | inner << 30 (inner: no Dirichlet DOF in the
-// cell, so no validity test), or -1 for padding; coordinates < 1024 per axis
+// group cell entry: cx | cy << 10 | cz << 20 | inner << 30 | scaled << 31 (inner: no
+// Dirichlet DOF in the cell, so no validity test; scaled: the cell's scale is alpha (operator,
+// fictitious cell) or 1/alpha (smoother, all-fictitious type) -- carried in the entry so no
+// per-cell table lookup sits on the latency path), or -1 for padding; coordinates < 1023
 constexpr int kMmaInner = 1 << 30;
+constexpr unsigned kMmaScaled = 1u << 31;
 
 struct MmaOp {
   CellOp op;                 // table / vectors / scales (op.mode selects kind vs blk scaling)
@@ -38,17 +41,15 @@ __device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, dou
 
 // cell scale: apply -> 1 or alpha (kind), smooth -> 1 or 1/alpha (type flag)
 __device__ __forceinline__ double cell_scale(const CellOp& op, int pc) {
-  if (pc < 0) return 0.0;
-  const int c = (pc & 1023) + op.nx * (((pc >> 10) & 1023) + op.ny * ((pc >> 20) & 1023));
-  if (op.mode == OP_APPLY) return op.kind[c] == 1 ? op.alpha : 1.0;
-  const int t = -op.blk[c] - 1;
-  return (t >> 12) ? op.inv_alpha : 1.0;
+  if (pc == -1) return 0.0;
+  if (!((unsigned)pc & kMmaScaled)) return 1.0;
+  return op.mode == OP_APPLY ? op.alpha : op.inv_alpha;
 }
 
 // layout index of local DOF a of the packed cell pc, or -1 (padding / a >= M / Dirichlet)
 template <int M>
 __device__ __forceinline__ int mma_dof_index(const Tab& T, int a, int pc) {
-  if (pc < 0 || a >= M) return -1;
+  if (pc == -1 || a >= M) return -1;
   const int cx = pc & 1023, cy = (pc >> 10) & 1023, cz = (pc >> 20) & 1023;
   if (!(pc & kMmaInner) && !dof_free(T, a, cx, cy, cz)) return -1;
   return dof_index(T, a, cx, cy, cz);

@@ -1178,13 +1178,14 @@ static int64_t block_dof_index(const Layout& L, int q, const BlockGeom& g, int l
 }
 
 // packed cell entry of an MMA group (cellmma.cuh): coordinates + "no Dirichlet DOF" flag
-static int32_t mma_pack(const fcm_mg* h, int q, int64_t c) {
+static int32_t mma_pack(const fcm_mg* h, int q, int64_t c, bool scaled) {
   int cc[3];
   h->L.cell_coords(c, cc);
   const LevelDev& Lv = h->lev[q];
   bool inner = true;
   for (int i = 0; i < 3; ++i) inner = inner && cc[i] >= Lv.ilo[i] && cc[i] <= Lv.ihi[i];
-  return cc[0] | (cc[1] << 10) | (cc[2] << 20) | (inner ? kMmaInner : 0);
+  return (int32_t)((unsigned)(cc[0] | (cc[1] << 10) | (cc[2] << 20) | (inner ? kMmaInner : 0)) |
+                   (scaled ? kMmaScaled : 0u));
 }
 
 static int setup_schwarz(fcm_mg* h, int q, const std::vector<uint8_t>& kind,
@@ -1352,7 +1353,7 @@ static int setup_schwarz(fcm_mg* h, int q, const std::vector<uint8_t>& kind,
     for (int64_t t = 0; t < ntypes; ++t) {
       auto& v = by_slot[t];
       for (size_t i = 0; i < v.size(); i += 8) {
-        for (size_t j = 0; j < 8; ++j) gc.push_back(i + j < v.size() ? mma_pack(h, q, v[i + j]) : -1);
+        for (size_t j = 0; j < 8; ++j) gc.push_back(i + j < v.size() ? mma_pack(h, q, v[i + j], ((-blk[v[i + j]] - 1) >> 12) & 1) : -1);
         gm.push_back((int32_t)t);
       }
     }
@@ -1674,12 +1675,12 @@ static int setup_impl(const fcm_grid* g, const fcm_params* prm, const fcm_slab* 
     if (!(getenv("FCM_CELL_MMA") && atoi(getenv("FCM_CELL_MMA")) == 0)) {
       Lv.kmma = gsz_rt(Lv.m) == Lv.G ? mma_kernel(Lv.m) : nullptr;
       for (int i = 0; i < 3; ++i)
-        if (L.n[i] > 1024) Lv.kmma = nullptr;   // packed coordinates
+        if (L.n[i] >= 1023) Lv.kmma = nullptr;   // packed coordinates (padding = all ones)
       if (Lv.kmma) {
         RC(allow_smem(Lv.kmma, std::max(mma_smem(Lv.m), list_smem(Lv.m, Lv.G))));
         std::vector<int32_t> gc, gm;
         for (int64_t c = 0; c < h->ncell; ++c)
-          if (kind_own[c] != 2) gc.push_back(mma_pack(h.get(), q, c));
+          if (kind_own[c] != 2) gc.push_back(mma_pack(h.get(), q, c, kind_own[c] == 1));
         while (gc.size() % 8) gc.push_back(-1);
         Lv.nA = (int64_t)gc.size() / 8;
         gm.assign(Lv.nA, -1);
