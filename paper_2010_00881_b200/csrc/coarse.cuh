@@ -187,7 +187,7 @@ __device__ __forceinline__ double coarse_cells(const CellOp& op, const Tab& T, c
 
 // smem: [Tab][MsA: M*MP][MsM: M*MP][reg scratch][list xs][list ids]
 template <int M, int G>
-__global__ void __launch_bounds__(256) k_coarse_pcg(CoarseArgs a) {
+__global__ void __launch_bounds__(256, (M > 0 && M <= 8) ? 4 : ((M > 0 && M <= 32) ? 3 : 2)) k_coarse_pcg(CoarseArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   constexpr int CPW = 32 / G;
   constexpr int MP = M > 0 ? padded<M>() : 0;

@@ -1834,7 +1834,7 @@ static int setup_impl(const fcm_grid* g, const fcm_params* prm, const fcm_slab* 
     if (e != cudaSuccess || per_sm < 1) return fail(FCM_ECUDA, "coarse kernel occupancy query failed");
     // the cell phases run over ncell cells with up to 32 cells per warp: fill every SM
     int64_t want = std::max<int64_t>(1, std::max<int64_t>((n1 + kThreads - 1) / kThreads, h->ncell / 64));
-    h->coarse_blocks = (int)std::min<int64_t>(want, (int64_t)h->num_sms * std::min(per_sm, 2));
+    h->coarse_blocks = (int)std::min<int64_t>(want, (int64_t)h->num_sms * std::min(per_sm, 4));
     h->coarse_blocks = std::min(h->coarse_blocks, kMaxPartials);
     if (const char* env = getenv("FCM_COARSE_BLOCKS")) {  // tuning knob (co-residency capped)
       int v = atoi(env);
