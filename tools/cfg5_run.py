@@ -24,6 +24,7 @@ def log(*a):
 
 
 log("setup done", out)
+log("irregular", out["irregular_blocks"])
 
 
 def ev_time(fn, reps):
