@@ -207,11 +207,7 @@ __device__ __forceinline__ double reg_cells(const CellOp& op, const Tab& T, cons
         if (inner || dof_free(T, a, cx, cy, cz)) {
           const int ia = dof_index(T, a, cx, cy, cz);
           const double y = scale * acc[i];
-#ifdef FCM_DEBUG_NORED
-          out[ia] = coef * y;   // timing experiment only (wrong result)
-#else
           atomicAdd(out + ia, coef * y);
-#endif
           if (want_e) energy = fma(xs[a], y, energy);
         }
       }

@@ -110,47 +110,6 @@ __device__ __noinline__ void barrier_reduce2_cg(double va, double vb, double* pa
   __syncthreads();
 }
 
-__device__ __noinline__ void barrier_reduce2(double va, double vb, double* pa, double* pb, GridCtl* ctl,
-                                             unsigned gen, double* red, double& ta, double& tb) {
-  __shared__ double s_tot[2];
-  va = block_sum(va, red);
-  vb = block_sum(vb, red);
-  if (threadIdx.x == 0) {
-    pa[blockIdx.x] = va;
-    pb[blockIdx.x] = vb;
-    __threadfence();                                      // release this block's writes
-    st_release_u32(&ctl->flags[blockIdx.x], gen);
-  }
-  if (blockIdx.x == 0) {
-    for (int i = threadIdx.x; i < (int)gridDim.x; i += blockDim.x)
-      while (ld_acquire_u32(&ctl->flags[i]) != gen) {}
-    __syncthreads();
-    double sa = 0.0, sb = 0.0;
-    for (int i = threadIdx.x; i < (int)gridDim.x; i += blockDim.x) {
-      sa += __ldcg(pa + i);
-      sb += __ldcg(pb + i);
-    }
-    sa = block_sum(sa, red);
-    sb = block_sum(sb, red);
-    if (threadIdx.x == 0) {
-      ctl->tot[0] = sa;
-      ctl->tot[1] = sb;
-      __threadfence();
-      st_release_u32(&ctl->release, gen);
-      s_tot[0] = sa;
-      s_tot[1] = sb;
-    }
-  } else if (threadIdx.x == 0) {
-    while (ld_acquire_u32(&ctl->release) != gen) {}
-    s_tot[0] = __ldcg(&ctl->tot[0]);
-    s_tot[1] = __ldcg(&ctl->tot[1]);
-  }
-  __syncthreads();
-  ta = s_tot[0];
-  tb = s_tot[1];
-  __syncthreads();
-}
-
 // One cell phase: blocks [0, nbl) stream the individual list (group per cell), the other blocks
 // run the regular population (thread(s) per cell) concurrently.  M == 0: all blocks generic;
 // nbl == 0: every block does both populations.

@@ -583,10 +583,8 @@ __global__ void k_invert_dense(double* A, int64_t n, double* X, int* status) {
 template <int M> constexpr int gsz() { return M <= 4 ? 4 : (M <= 8 ? 8 : (M <= 16 ? 16 : 32)); }
 #define FCM_FOR_M(X) X(4) X(8) X(9) X(16) X(24) X(25) X(27)
 
-// ts1: force one thread per cell (tuning knob FCM_TS1)
-const void* reg_kernel(int m, int* M_out, bool ts1) {
-#define CASE(MM) case MM: *M_out = MM; \
-  return ts1 ? (const void*)k_cell_reg<MM, 1> : (const void*)k_cell_reg<MM, split_of<MM>()>;
+const void* reg_kernel(int m, int* M_out) {
+#define CASE(MM) case MM: *M_out = MM; return (const void*)k_cell_reg<MM, split_of<MM>()>;
   switch (m) { FCM_FOR_M(CASE) default: break; }
 #undef CASE
   *M_out = 0;
@@ -993,10 +991,9 @@ static int enqueue_coarse(fcm_mg* h, const double* b, double* x) {
   a.ctl = h->c_ctl;
   {  // split the grid between the individual lists and the regular population (coarse.cuh)
     const int nb = h->coarse_blocks;
-    static const bool nosplit = getenv("FCM_COARSE_NOSPLIT") && atoi(getenv("FCM_COARSE_NOSPLIT")) > 0;
     auto share = [&](int64_t nlist) {
       if (L1.M == 0) return nb;
-      if (nlist <= 0 || nb < 2 || nosplit) return 0;
+      if (nlist <= 0 || nb < 2) return 0;
       int64_t v = (2 * nb * nlist + h->ncell - 1) / h->ncell;
       return (int)std::max<int64_t>(1, std::min<int64_t>(v, nb / 2));
     };
@@ -1660,9 +1657,8 @@ static int setup_impl(const fcm_grid* g, const fcm_params* prm, const fcm_slab* 
     LevelDev& Lv = h->lev[q];
     const LevelTable& T = L.tables[q];
     Lv.q = q; Lv.m = T.m; Lv.ndof = T.ndof; Lv.G = group_size(T.m);
-    const bool ts1 = getenv("FCM_TS1") && atoi(getenv("FCM_TS1")) > 0;
-    Lv.kreg = reg_kernel(T.m, &Lv.M, ts1);
-    Lv.ts = (ts1 || Lv.M == 0) ? 1 : split_rt(Lv.M);
+    Lv.kreg = reg_kernel(T.m, &Lv.M);
+    Lv.ts = Lv.M == 0 ? 1 : split_rt(Lv.M);
     for (int i = 0; i < 3; ++i) {
       Lv.ilo[i] = 0;
       Lv.ihi[i] = L.n[i] - 1;
