@@ -81,11 +81,23 @@ __device__ __forceinline__ double mma_cells(const CellOp& op, const int32_t* __r
   const int ar = lane >> 2, ac = lane & 3;
   double energy = 0.0;
   const bool want_e = op.partials != nullptr;
+  // the next group's descriptor is loaded one trip ahead (software pipelining: its latency
+  // overlaps this group's gathers and MMAs)
+  int n_slot = 0, n_cg = -1, n_c0 = -1, n_c1 = -1;
+  if (warp < ngroups) {
+    const int* cells = grp_cells + (int64_t)warp * 8;
+    n_slot = __ldg(grp_mat + warp);
+    n_cg = __ldg(cells + ar); n_c0 = __ldg(cells + 2 * ac); n_c1 = __ldg(cells + 2 * ac + 1);
+  }
   for (int64_t gi = warp; gi < ngroups; gi += nwarps) {
-    const int slot = __ldg(grp_mat + gi);   // warp-uniform
-    const int* cells = grp_cells + gi * 8;
-    const int cg = __ldg(cells + ar);            // B column / gather cell of this lane
-    const int c0 = __ldg(cells + 2 * ac), c1 = __ldg(cells + 2 * ac + 1);   // output cells
+    const int slot = n_slot;   // warp-uniform
+    const int cg = n_cg;       // B column / gather cell of this lane
+    const int c0 = n_c0, c1 = n_c1;   // output cells
+    if (gi + nwarps < ngroups) {
+      const int* cells = grp_cells + (gi + nwarps) * 8;
+      n_slot = __ldg(grp_mat + gi + nwarps);
+      n_cg = __ldg(cells + ar); n_c0 = __ldg(cells + 2 * ac); n_c1 = __ldg(cells + 2 * ac + 1);
+    }
     // gather: B[kt] = x[dof kt*4 + ac] of cell cg
     double B[KT];
 #pragma unroll

@@ -64,6 +64,9 @@ struct CoarseArgs {
   const int32_t* gS_cells;
   const int32_t* gS_mat;
   int64_t nS;
+  // large levels: r_{k+1} is written by the vector loop and the smoother reads it after one
+  // more grid barrier (one gather instead of the three of the fused form)
+  int split_s;
 };
 
 __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
@@ -245,9 +248,16 @@ __global__ void __launch_bounds__(256, (M > 0 && M <= 8) ? 4 : ((M > 0 && M <= 3
         }
       }
       if (!a.jacobi) {
-        opM.in = rC; opM.in1 = wC; opM.in2 = qO; opM.c1 = -alpha; opM.c2 = beta;
-        opM.out = a.z[nx];
-        rz_loc = coarse_cells<M, G, true>(opM, T, MsM, xsr, xs, ids, a.nbl_M, a.gS_cells, a.gS_mat, a.nS, AsM, 0);
+        if (a.split_s) {   // r_{k+1} complete in memory first
+          cooperative_groups::this_grid().sync();
+          opM.in = rN; opM.in1 = nullptr;
+          opM.out = a.z[nx];
+          rz_loc = coarse_cells<M, G, false>(opM, T, MsM, xsr, xs, ids, a.nbl_M, a.gS_cells, a.gS_mat, a.nS, AsM, 0);
+        } else {
+          opM.in = rC; opM.in1 = wC; opM.in2 = qO; opM.c1 = -alpha; opM.c2 = beta;
+          opM.out = a.z[nx];
+          rz_loc = coarse_cells<M, G, true>(opM, T, MsM, xsr, xs, ids, a.nbl_M, a.gS_cells, a.gS_mat, a.nS, AsM, 0);
+        }
       }
       double rr, rz_new;
       barrier_reduce2_cg(rr_loc, rz_loc, a.part, a.part_stride, ++gen, red, rr, rz_new);

@@ -1001,6 +1001,10 @@ static int enqueue_coarse(fcm_mg* h, const double* b, double* x) {
     a.nbl_M = share(L1.n_irr);
   }
   a.iters = h->d_coarse_iters;
+  {   // fused r update in the smoother gather for L2-resident levels, split above ~2M DOFs
+    const char* e = getenv("FCM_COARSE_SPLIT");
+    a.split_s = e ? atoi(e) > 0 : (n >= (int64_t)2000000);
+  }
   if (L1.kmma) {   // regular cells as fp64 MMA groups (cellmma.cuh)
     a.gA_cells = L1.gA_cells; a.gA_mat = L1.gA_mat; a.nA = L1.nA;
     if (!a.jacobi) { a.gS_cells = L1.gS_cells; a.gS_mat = L1.gS_mat; a.nS = L1.nS; }
