@@ -154,6 +154,31 @@ class Hierarchy:
             x = x + w * lv.schwarz(r)
         return x
 
+    def mg_solve(self, b, rtol=None, maxit=None):
+        """Multigrid as a stand-alone solver: x_0 = 0,
+        x_i = x_{i-1} + V(b - A x_{i-1}); stop when ||b - A x_i|| / ||b|| < rtol (strict) or
+        after maxit V-cycles.  Returns x, i, [||r_0||/||b||, ..., ||r_i||/||b||]; the contraction
+        numbers rho_i (Eq. contraction) are hist[1:] / hist[:-1]."""
+        cfg = self.prob.cfg
+        rtol = cfg.rtol if rtol is None else rtol
+        maxit = cfg.maxit if maxit is None else maxit
+        A = self.levels[cfg.p].A
+        nb = np.linalg.norm(b)
+        x = np.zeros_like(b)
+        if nb == 0:
+            return x, 0, [0.0]
+        r = b.copy()
+        hist = [1.0]
+        it = 0
+        while it < maxit:
+            x = x + self.vcycle(r)
+            r = b - A @ x
+            it += 1
+            hist.append(np.linalg.norm(r) / nb)
+            if hist[-1] < rtol:
+                break
+        return x, it, hist
+
     def fcg(self, b, rtol=None, maxit=None, force_iters=None):
         cfg = self.prob.cfg
         rtol = cfg.rtol if rtol is None else rtol

@@ -153,7 +153,8 @@ def test_vcycle_special_cases(small3d):
 
 def test_standalone_mg_contracts(cfg1):
     # multigrid as a solver x += V(b - A x); every contraction number rho_i < 1
-    # (a sign error in the coarse correction or a wrong omega makes it diverge)
+    # (a sign error in the coarse correction or a wrong omega makes it diverge).  The loop is
+    # retyped here and must agree with Hierarchy.mg_solve step by step.
     H = Hierarchy(cfg1)
     A, b = cfg1.A, cfg1.b
     x = np.zeros_like(b)
@@ -163,6 +164,21 @@ def test_standalone_mg_contracts(cfg1):
         res.append(np.linalg.norm(b - A @ x))
     rho = np.array(res[1:]) / np.array(res[:-1])
     assert rho.max() < 0.9
+    xm, it, hist = H.mg_solve(b, rtol=0.0, maxit=12)
+    assert it == 12 and np.allclose(np.array(hist), np.array(res) / res[0], rtol=1e-9)
+    assert np.linalg.norm(xm - x) <= 1e-12 * np.linalg.norm(x)
+
+
+def test_standalone_mg_single_level_is_exact():
+    # one level with a direct coarse solve: V = A^{-1}, so the stand-alone solver
+    # reaches the solution in one cycle (closed form: rho_1 = 0 up to rounding)
+    from workloads import small_config
+    P = Problem(small_config(3, 4, 1, voids=1, seed=3, coarse="direct"))
+    H = Hierarchy(P)
+    x, it, hist = H.mg_solve(P.b, rtol=1e-12, maxit=5)
+    assert it == 1 and hist[1] < 1e-12
+    xd = np.linalg.solve(P.A.toarray(), P.b)
+    assert np.linalg.norm(x - xd) <= 1e-11 * np.linalg.norm(xd)
 
 
 def test_coarse_cg_matches_direct(small3d):
