@@ -246,7 +246,17 @@ int fcm_pcg_solve(fcm_mg* h, const double* b, double* x, double rtol, int32_t ma
 int fcm_pcg_solve_host(fcm_mg* h, const double* b_host, double* x_host, double rtol,
                        int32_t maxit, int32_t* iters, double* relres_hist);
 
-/* Statistics of the last fcm_pcg_solve: total inner coarse CG iterations, V-cycles.       */
+/* Multigrid as a stand-alone solver (the "MG" columns of the tables):
+ * x_0 = 0, x_i = x_{i-1} + V(b - A x_{i-1}) with the true residual r_i = b - A x_i
+ * recomputed after every V-cycle; stop when ||r_i||/||b|| < rtol or after maxit V-cycles.
+ * b, x: device, ndofs(p).  *iters (host, may be NULL) = V-cycles done; relres_hist (host, may
+ * be NULL, maxit+1 entries) receives ||r_i||/||b|| (the contraction numbers of P:357 are
+ * hist[i]/hist[i-1]).  Synchronises the stream once per V-cycle.
+ * Returns FCM_OK, FCM_NOT_CONVERGED (x valid), or an error (FCM_EINDEF on a NaN residual). */
+int fcm_mg_solve(fcm_mg* h, const double* b, double* x, double rtol, int32_t maxit,
+                 int32_t* iters, double* relres_hist);
+
+/* Statistics of the last fcm_pcg_solve / fcm_mg_solve: inner coarse CG iterations, V-cycles. */
 int fcm_mg_stats(const fcm_mg* h, int64_t* coarse_iters_total, int64_t* vcycles);
 
 /* Which coarse solver kernel the handle runs (for measurement and tests):

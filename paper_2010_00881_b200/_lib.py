@@ -66,6 +66,7 @@ _SIGS = {
     "fcm_mg_vcycle": (I32, [P, P, P]),
     "fcm_pcg_solve": (I32, [P, P, P, D, I32, P, P]),
     "fcm_pcg_solve_host": (I32, [P, P, P, D, I32, P, P]),
+    "fcm_mg_solve": (I32, [P, P, P, D, I32, P, P]),
     "fcm_mg_stats": (I32, [P, P, P]),
     "fcm_mg_coarse_info": (I32, [P, P, P, P]),
     "fcm_slab_bounds": (I32, [I32, I32, I32, P, P]),

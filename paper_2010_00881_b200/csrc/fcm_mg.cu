@@ -163,12 +163,12 @@ struct fcm_mg {
   double* d_partB = nullptr;
   double* d_partC = nullptr;
   // graphs
-  cudaGraphExec_t g_vc = nullptr, g_it1 = nullptr, g_it2 = nullptr, g_init = nullptr;
+  cudaGraphExec_t g_vc = nullptr, g_it1 = nullptr, g_it2 = nullptr, g_init = nullptr, g_mgit = nullptr;
   cudaGraphExec_t g_solve = nullptr;   // whole FCG: init, it1, check, WHILE { it2, it1, check }
   int64_t n_loop = 0, n_head = 0;      // kernels per loop trip / in the head
   double* d_hist = nullptr;
   int hist_cap = 0;
-  int64_t n_vc = 0, n_it1 = 0, n_it2 = 0, n_init = 0;  // kernels per graph
+  int64_t n_vc = 0, n_it1 = 0, n_it2 = 0, n_init = 0, n_mgit = 0;  // kernels per graph
   int64_t launches = 0;
   int64_t* count_target = nullptr;  // during capture: where launches are counted
   int64_t stat_coarse = 0, stat_vcycles = 0;
@@ -209,7 +209,7 @@ struct fcm_mg {
   }
   ~fcm_mg();
   void release() {
-    for (auto g : {g_vc, g_it1, g_it2, g_init, g_solve})
+    for (auto g : {g_vc, g_it1, g_it2, g_init, g_mgit, g_solve})
       if (g) cudaGraphExecDestroy(g);
     for (void* p : allocs) cudaFree(p);
     if (h_s) cudaFreeHost(h_s);
@@ -2248,6 +2248,76 @@ extern "C" int fcm_pcg_solve_host(fcm_mg* h, const double* b_host, double* x_hos
   int rc = pcg_core(h, rtol, maxit, iters, relres_hist);
   if (rc < 0) return rc;
   CU(cudaMemcpyAsync(x_host, h->f_x, N * 8, cudaMemcpyDeviceToHost, h->stream));
+  CU(cudaStreamSynchronize(h->stream));
+  return rc;
+}
+
+// Multigrid as a stand-alone solver: x_i = x_{i-1} + V(b - A x_{i-1}).
+// One graph per iteration: V-cycle on r, x += z, r = b - A x, rr = r.r (owned DOFs, summed
+// over ranks), Scalars to the host; the host checks ||r_i||/||b|| (one sync per V-cycle).
+static int mg_solve_core(fcm_mg* h, double rtol, int32_t maxit, int32_t* iters, double* hist) {
+  const int p = h->g.p;
+  const int64_t N = h->lev[p].ndof;
+  double* z = h->lev[p].x;
+  const int nbd = dot_blocks(h);
+  const uint8_t* own = h->multi ? h->d_own : nullptr;
+  if (!h->g_mgit) {
+    RC(capture(h, &h->g_mgit, &h->n_mgit, [&]() -> int {
+      RC(enqueue_vcycle(h, p, h->f_r, z));
+      k_axpy<<<grid_for(N, h->num_sms), kThreads, 0, h->stream>>>(h->f_x, 1.0, z, N);
+      h->count();
+      RC(residual(h, p, h->f_b, h->f_x, h->f_r));
+      k_dot<<<nbd, kThreads, 0, h->stream>>>(h->f_r, h->f_r, N, h->d_partA, own);
+      k_finalize<<<1, 32, 0, h->stream>>>(&h->d_s->rr, h->d_partA, nbd);
+      h->count(2);
+      CU(cudaGetLastError());
+      RC(allreduce(h, &h->d_s->rr, 1));
+      CU(cudaMemcpyAsync(h->h_s, h->d_s, sizeof(Scalars), cudaMemcpyDeviceToHost, h->stream));
+      return FCM_OK;
+    }));
+  }
+  k_dot<<<nbd, kThreads, 0, h->stream>>>(h->f_b, h->f_b, N, h->d_partA, own);
+  k_finalize<<<1, 32, 0, h->stream>>>(&h->d_s->bb, h->d_partA, nbd);
+  h->count(2);
+  RC(allreduce(h, &h->d_s->bb, 1));
+  CU(cudaMemcpyAsync(h->h_s, h->d_s, sizeof(Scalars), cudaMemcpyDeviceToHost, h->stream));
+  RC(fill(h, h->f_x, 0.0, N));
+  RC(copy(h, h->f_r, h->f_b, N));   // r_0 = b (x_0 = 0)
+  CU(cudaMemsetAsync((h->hg ? h->hg : h)->d_coarse_iters, 0, 8, h->stream));
+  CU(cudaStreamSynchronize(h->stream));
+  const double bb = h->h_s->bb;
+  h->stat_coarse = 0;
+  h->stat_vcycles = 0;
+  int it = 0;
+  if (hist) hist[0] = bb > 0 ? 1.0 : 0.0;
+  int status = FCM_OK;
+  if (bb > 0) {
+    while (true) {
+      if (it >= maxit) { status = FCM_NOT_CONVERGED; break; }
+      RC(run_graph(h, h->g_mgit, h->n_mgit));
+      CU(cudaStreamSynchronize(h->stream));
+      ++it;
+      h->stat_vcycles++;
+      const double rel = std::sqrt(h->h_s->rr / bb);
+      if (hist) hist[it] = rel;
+      if (!(rel == rel)) return fail(FCM_EINDEF, "NaN residual at MG iteration %d", it);
+      if (rel < rtol) break;
+    }
+  }
+  if (iters) *iters = it;
+  return status;
+}
+
+extern "C" int fcm_mg_solve(fcm_mg* h, const double* b, double* x, double rtol, int32_t maxit,
+                            int32_t* iters, double* relres_hist) {
+  clear_error();
+  if (!h || !b || !x || maxit < 0) return fail(FCM_EINVAL, "bad argument");
+  StreamGuard sg(h);
+  const int64_t N = h->lev[h->g.p].ndof;
+  CU(cudaMemcpyAsync(h->f_b, b, N * 8, cudaMemcpyDeviceToDevice, h->stream));
+  int rc = mg_solve_core(h, rtol, maxit, iters, relres_hist);
+  if (rc < 0) return rc;
+  CU(cudaMemcpyAsync(x, h->f_x, N * 8, cudaMemcpyDeviceToDevice, h->stream));
   CU(cudaStreamSynchronize(h->stream));
   return rc;
 }

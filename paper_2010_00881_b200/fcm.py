@@ -335,6 +335,17 @@ class Solver:
         check(rc, allow_not_converged=True)
         return x, it.value, hist[: it.value + 1]
 
+    def mg_solve(self, b: torch.Tensor, rtol=None, maxit=None, x=None):
+        """Stand-alone multigrid x_i = x_{i-1} + V(b - A x_{i-1}) (fcm_mg_solve)."""
+        rtol = self.cfg.rtol if rtol is None else rtol
+        maxit = self.cfg.maxit if maxit is None else maxit
+        x = self._vec() if x is None else x
+        it = C.c_int32()
+        hist = np.zeros(maxit + 1)
+        rc = _lib.lib().fcm_mg_solve(self._h, _ptr(b), _ptr(x), rtol, maxit, C.byref(it), _ptr(hist))
+        check(rc, allow_not_converged=True)
+        return x, it.value, hist[: it.value + 1]
+
     def pcg_solve_host(self, b_host: torch.Tensor, x_host: torch.Tensor, rtol=None, maxit=None):
         rtol = self.cfg.rtol if rtol is None else rtol
         maxit = self.cfg.maxit if maxit is None else maxit

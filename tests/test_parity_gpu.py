@@ -178,6 +178,34 @@ def test_fcg_matches_oracle(pair):
     assert rel(xg, xo2) <= 1e-8
 
 
+def test_mg_solve_matches_oracle(pair):
+    # stand-alone MG: the same number of V-cycles on both sides, so the iterates
+    # and the relative-residual histories (hence the contraction numbers rho_i) are compared
+    # one to one; iterate <= 1e-8 (final-solution bound), history entries to 1e-6 relative
+    k = 6
+    H = pair.hier()
+    xo, ito, ho = H.mg_solve(pair.P.b, rtol=0.0, maxit=k)
+    xc, _, _ = pair.hier_chol().mg_solve(pair.P.b, rtol=0.0, maxit=k)
+    x, it, hist = pair.S.mg_solve(pair.to_gpu(pair.P.b), rtol=0.0, maxit=k)
+    assert it == ito == k
+    assert rel(pair.from_gpu(x), xo) <= pair.tol(1e-8, rel(xc, xo))
+    ho = np.array(ho)
+    big = ho > 1e-7
+    assert np.all(np.abs(hist[big] - ho[big]) <= 1e-6 * ho[big]), (hist, ho)
+    assert np.all(hist[~big] < 1e-6)
+    # to convergence: stops at the first i with ||r_i||/||b|| < rtol, iterations +-1
+    xo, ito, _ = H.mg_solve(pair.P.b, rtol=1e-8, maxit=200)
+    x, it, hist = pair.S.mg_solve(pair.to_gpu(pair.P.b), rtol=1e-8, maxit=200)
+    if ito < 200:
+        assert abs(it - ito) <= 1 and hist[-1] < 1e-8 and np.all(hist[:-1] >= 1e-8)
+        ax = pair.from_gpu(pair.S.apply(x))
+        assert np.linalg.norm(pair.P.b - ax) / np.linalg.norm(pair.P.b) < 2e-8
+    # zero right-hand side: no V-cycle, x = 0
+    b0 = torch.zeros(pair.S.ndofs(), dtype=torch.float64, device="cuda")
+    x0, it0, _ = pair.S.mg_solve(b0)
+    assert it0 == 0 and not torch.any(x0)
+
+
 def test_zero_rhs_and_host_path(pair):
     b = torch.zeros(pair.S.ndofs(), dtype=torch.float64, device="cuda")
     x, it, _ = pair.S.pcg_solve(b)
