@@ -70,6 +70,13 @@ struct TiledArgs {
   int maxit;
   int* iters;               // [0] = this solve, [1] += this solve
   unsigned long long* prof; // optional per-block phase times (ns): [nblocks][4]
+  // constant-coefficient fast path (NF == 1): a vertex whose 2^d cells all use the K_ref block
+  // (operator) or the type-0 Schwarz inverse (smoother) with one scale applies the 3^d-point
+  // stencil sum_{kc,k2: o(k2)-o(kc)=d} Mat[kc][k2] instead of the per-cell gather (coefficients
+  // read from the parameter bank, no shared-memory matrix traffic)
+  int fast;
+  double st_op[27];
+  double st_sm[27];
 };
 
 __device__ __forceinline__ unsigned long long t_now() {
@@ -91,6 +98,8 @@ __device__ __forceinline__ void t_st_release(unsigned* p, unsigned v) {
 // (smoother)
 constexpr int kNoCell = -1;
 constexpr int kScaleBit = 1 << 30;
+// per-vertex flags: operator / smoother stencil applies, and its scale (alpha resp. 1/alpha)
+constexpr int kVfOp = 1, kVfOpScaled = 2, kVfSm = 4, kVfSmScaled = 8;
 
 // shared-memory layout (doubles first, then ints); see tiled_smem_bytes
 template <int DIM, int NF>
@@ -104,6 +113,10 @@ struct TiledSmem {
   int* gidx;    // [NF][E2] class-major index or -1
   int* cop;     // [EC] operator code per cell
   int* csm;     // [EC] smoother code per cell
+  unsigned char* vf;   // [E2] fast-path flags (kVf*)
+  int* lsm;     // NF == 1: smoother rows (E1 vertices with a free DOF), stencil rows first;
+  int* lop;     //          operator rows (T), stencil rows first; entry = l | cell base << 16
+  int nsm, nop;
   int E2, EC, T;
 };
 
@@ -115,19 +128,18 @@ __host__ __device__ constexpr int packed_at(int a, int b) {
 // matrix slot stride in the pool: odd number of doubles, so that 32 lanes reading the same
 // entry of 32 different slots hit distinct bank pairs (no conflicts beyond the 2 wavefronts)
 __host__ __device__ constexpr int slot_stride(int m) { return packed_size(m) | 1; }
-__host__ __device__ constexpr size_t tiled_smem_bytes(int dim, int nf, int E2, int EC, int T, int nmats) {
+__host__ __device__ constexpr size_t tiled_smem_bytes(int dim, int nf, int E2, int E1, int EC, int T, int nmats) {
   return (size_t)(3 * nf * E2 + 2 * nf * T) * 8 + (size_t)nmats * slot_stride((1 << dim) * nf) * 8 +
-         (size_t)nf * E2 * 4 + (size_t)EC * 8 + 16;
+         (size_t)nf * E2 * 4 + (size_t)EC * 8 + (size_t)((E2 + 15) & ~15) +
+         (nf == 1 ? (size_t)(E1 + T) * 4 : 0) + 16;
 }
 
 // one row of the vertex-centric gather: sum over the 2^d cells around E2 entry l (local
 // coordinates lx, ly, lz) of s_c Mat_c[a_v(c)*NF + i, :] . vec_c (all operands in smem)
 template <int DIM, int NF, bool SMOOTH>
 __device__ __forceinline__ double vertex_row(const TiledArgs& a, const TiledSmem<DIM, NF>& S,
-                                             const double* __restrict__ vec, int l, int lx, int ly,
-                                             int lz, int i) {
+                                             const double* __restrict__ vec, int l, int cb, int i) {
   constexpr int NC = 1 << DIM;
-  constexpr int M1 = NC * NF;
   const int e0 = a.e[0], e01 = a.e[0] * a.e[1];
   const int ec0 = a.ec[0], ec01 = a.ec[0] * a.ec[1];
   const double scale = SMOOTH ? a.inv_alpha : a.alpha;
@@ -141,11 +153,17 @@ __device__ __forceinline__ double vertex_row(const TiledArgs& a, const TiledSmem
       const int dx = q % 3 - 1, dy = (q / 3) % 3 - 1, dz = DIM == 3 ? q / 9 - 1 : 0;
       nb[q] = vec[l + dx + dy * e0 + dz * e01];
     }
+    const int f = S.vf[l];
+    if (f & (SMOOTH ? kVfSm : kVfOp)) {
+      const double* st = SMOOTH ? a.st_sm : a.st_op;
+#pragma unroll
+      for (int q = 0; q < N3; ++q) acc = fma(st[q], nb[q], acc);
+      return (f & (SMOOTH ? kVfSmScaled : kVfOpScaled)) ? scale * acc : acc;
+    }
 #pragma unroll
     for (int kc = 0; kc < NC; ++kc) {
       const int ox = kc & 1, oy = (kc >> 1) & 1, oz = (kc >> 2) & 1;
-      const int cl = (lz - oz) * ec01 + (ly - oy) * ec0 + (lx - ox);
-      const int code = SMOOTH ? S.csm[cl] : S.cop[cl];
+      const int code = SMOOTH ? S.csm[cb - (oz * ec01 + oy * ec0 + ox)] : S.cop[cb - (oz * ec01 + oy * ec0 + ox)];
       double t = 0.0;
       {
         const double* mat = S.mat + (code == kNoCell ? 0 : (code & (kScaleBit - 1)));
@@ -164,8 +182,7 @@ __device__ __forceinline__ double vertex_row(const TiledArgs& a, const TiledSmem
   for (int kc = 0; kc < NC; ++kc) {
     const int ox = kc & 1, oy = (kc >> 1) & 1, oz = (kc >> 2) & 1;
     // the cell box shares the E2 origin: cell local = vertex local - corner offset
-    const int cl = (lz - oz) * ec01 + (ly - oy) * ec0 + (lx - ox);
-    const int code = SMOOTH ? S.csm[cl] : S.cop[cl];
+    const int code = SMOOTH ? S.csm[cb - (oz * ec01 + oy * ec0 + ox)] : S.cop[cb - (oz * ec01 + oy * ec0 + ox)];
     if (code == kNoCell) continue;
     const double* mat = S.mat + (code & (kScaleBit - 1));
     const int base = l - (ox + oy * e0 + oz * e01);
@@ -297,6 +314,10 @@ __global__ void __launch_bounds__(kTiledThreads, 1) k_coarse_tiled(TiledArgs a) 
     S.gidx = reinterpret_cast<int*>(d);
     S.cop = S.gidx + NF * S.E2;
     S.csm = S.cop + S.EC;
+    S.vf = reinterpret_cast<unsigned char*>(S.csm + S.EC);
+    S.lsm = reinterpret_cast<int*>(S.vf + ((S.E2 + 15) & ~15));
+    const int ne1 = (a.tile[0] + 2) * (DIM > 1 ? a.tile[1] + 2 : 1) * (DIM > 2 ? a.tile[2] + 2 : 1);
+    S.lop = S.lsm + ne1;
   }
   // brick of this block
   const int bt = blockIdx.x;
@@ -369,6 +390,79 @@ __global__ void __launch_bounds__(kTiledThreads, 1) k_coarse_tiled(TiledArgs a) 
   }
   for (int t = threadIdx.x; t < NF * S.T; t += blockDim.x) { S.p[t] = 0.0; S.x[t] = 0.0; }
   __syncthreads();
+  // fast-path flags of the E1 vertices (every block derives them from the same cell data, so
+  // a vertex evaluated by several blocks still gets bit-identical values)
+  for (int t = threadIdx.x; t < E2; t += blockDim.x) {
+    const int lx = t % e0, ly = (t / e0) % e1, lz = t / (e0 * e1);
+    int f = 0;
+    const bool in1 = lx >= 1 && lx <= e0 - 2 && (DIM < 2 || (ly >= 1 && ly <= e1 - 2)) &&
+                     (DIM < 3 || (lz >= 1 && lz <= e2d - 2));
+    if (NF == 1 && a.fast && in1) {
+      const int ec0 = a.ec[0], ec01 = a.ec[0] * a.ec[1];
+      const int c0 = S.cop[lz * ec01 + ly * ec0 + lx], s0 = S.csm[lz * ec01 + ly * ec0 + lx];
+      bool op = c0 != kNoCell && (c0 & ~kScaleBit) == 0, sm = !a.jacobi && s0 != kNoCell && (s0 & ~kScaleBit) == MM;
+      for (int kc = 1; kc < NC; ++kc) {
+        const int cl = (lz - ((kc >> 2) & 1)) * ec01 + (ly - ((kc >> 1) & 1)) * ec0 + (lx - (kc & 1));
+        op = op && S.cop[cl] == c0;
+        sm = sm && S.csm[cl] == s0;
+      }
+      if (op) f |= kVfOp | ((c0 & kScaleBit) ? kVfOpScaled : 0);
+      if (sm) f |= kVfSm | ((s0 & kScaleBit) ? kVfSmScaled : 0);
+    }
+    S.vf[t] = (unsigned char)f;
+  }
+  // NF == 1: row lists, stencil rows first, so that warps do not diverge between the two
+  // paths (the order inside a list does not change any value: rows are independent)
+  __shared__ int lcnt[4];
+  if constexpr (NF == 1) {
+    if (threadIdx.x < 4) lcnt[threadIdx.x] = 0;
+    __syncthreads();
+    const int gx = a.tile[0] + 2, gy = DIM > 1 ? a.tile[1] + 2 : 1, gz = DIM > 2 ? a.tile[2] + 2 : 1;
+    const int ne1 = gx * gy * gz;
+    const int lane = threadIdx.x & 31;
+    for (int pass = 0; pass < 2; ++pass) {
+      for (int t0 = 0; t0 < ne1; t0 += blockDim.x) {   // E1 entries, T entries flagged
+        const int q = t0 + threadIdx.x;
+        int l = 0, cb = 0;
+        bool valid = false, inT = false;
+        if (q < ne1) {
+          const int lx = q % gx + 1, ly = DIM > 1 ? (q / gx) % gy + 1 : 0, lz = DIM > 2 ? q / (gx * gy) + 1 : 0;
+          l = (lz * e1 + ly) * e0 + lx;
+          cb = (lz * a.ec[1] + ly) * a.ec[0] + lx;
+          valid = S.gidx[l] >= 0;
+          inT = lx >= 2 && lx <= e0 - 3 && (DIM < 2 || (ly >= 2 && ly <= e1 - 3)) && (DIM < 3 || (lz >= 2 && lz <= e2d - 3));
+        }
+        const int f = valid ? S.vf[l] : 0;
+        const unsigned lt = (1u << lane) - 1u;
+        // smoother list (counter 0 = fast, 1 = general), operator list (2, 3)
+#pragma unroll
+        for (int w = 0; w < 2; ++w) {
+          const bool in = valid && (w == 0 || inT);
+          const bool fast = in && (f & (w == 0 ? kVfSm : kVfOp));
+          const unsigned bf = __ballot_sync(0xffffffffu, fast), bg = __ballot_sync(0xffffffffu, in && !fast);
+          if (pass == 0) {
+            if (lane == 0) { atomicAdd(&lcnt[2 * w], __popc(bf)); atomicAdd(&lcnt[2 * w + 1], __popc(bg)); }
+          } else {
+            int bfo = 0, bgo = 0;
+            if (lane == 0) { bfo = atomicAdd(&lcnt[2 * w], __popc(bf)); bgo = atomicAdd(&lcnt[2 * w + 1], __popc(bg)); }
+            bfo = __shfl_sync(0xffffffffu, bfo, 0);
+            bgo = __shfl_sync(0xffffffffu, bgo, 0);
+            int* lst = w == 0 ? S.lsm : S.lop;
+            if (fast) lst[bfo + __popc(bf & lt)] = l | (cb << 16);
+            else if (in) lst[bgo + __popc(bg & lt)] = l | (cb << 16);
+          }
+        }
+      }
+      __syncthreads();
+      if (pass == 0) {
+        S.nsm = lcnt[0] + lcnt[1];
+        S.nop = lcnt[2] + lcnt[3];
+        __syncthreads();
+        if (threadIdx.x == 0) { lcnt[1] = lcnt[0]; lcnt[0] = 0; lcnt[3] = lcnt[2]; lcnt[2] = 0; }
+        __syncthreads();
+      }
+    }
+  }
   // regions in local E2 coordinates: E1 = [1, tile+2], T = [2, tile+1] per present axis
   const int g1x = t0 + 2, g1y = DIM > 1 ? t1 + 2 : 1, g1z = DIM > 2 ? t2 + 2 : 1;
   const int nE1 = g1x * g1y * g1z;
@@ -381,6 +475,13 @@ __global__ void __launch_bounds__(kTiledThreads, 1) k_coarse_tiled(TiledArgs a) 
   };
 
   auto smooth_E1 = [&]() {   // u = M r on E1
+    if constexpr (NF == 1) {
+      for (int k = threadIdx.x; k < S.nsm; k += blockDim.x) {
+        const int e = S.lsm[k], l = e & 0xffff;
+        S.u[l] = a.jacobi ? __ldg(a.diag_inv + S.gidx[l]) * S.r[l]
+                          : vertex_row<DIM, NF, true>(a, S, S.r, l, e >> 16, 0);
+      }
+    } else {
     for (int t = threadIdx.x; t < NF * nE1; t += blockDim.x) {
       const int i = t / nE1, q = t % nE1;
       const int lx = q % g1x + 1, ly = (q / g1x) % g1y + shy1, lz = q / (g1x * g1y) + shz1;
@@ -389,26 +490,39 @@ __global__ void __launch_bounds__(kTiledThreads, 1) k_coarse_tiled(TiledArgs a) 
       double u = 0.0;
       if (gi >= 0) {
         if (a.jacobi) u = __ldg(a.diag_inv + gi) * S.r[i * E2 + l];
-        else u = vertex_row<DIM, NF, true>(a, S, S.r, l, lx, ly, lz, i);
+        else u = vertex_row<DIM, NF, true>(a, S, S.r, l, (lz * a.ec[1] + ly) * a.ec[0] + lx, i);
       }
       S.u[i * E2 + l] = u;
+    }
     }
   };
   // w = A u on T; publish w; partials (r,u), (w,u), (r,r)
   auto apply_T = [&](double* wout, double& g, double& dl, double& rh) {
     g = 0.0; dl = 0.0; rh = 0.0;
+    if constexpr (NF == 1) {
+      for (int k = threadIdx.x; k < S.nop; k += blockDim.x) {
+        const int e = S.lop[k], l = e & 0xffff;
+        const double w = vertex_row<DIM, NF, false>(a, S, S.u, l, e >> 16, 0);
+        __stcg(wout + S.gidx[l], w);
+        const double ri = S.r[l], ui = S.u[l];
+        g = fma(ri, ui, g);
+        dl = fma(w, ui, dl);
+        rh = fma(ri, ri, rh);
+      }
+    } else {
     for (int t = threadIdx.x; t < NF * nT; t += blockDim.x) {
       const int i = t / nT, q = t % nT;
       const int lx = q % t0 + 2, ly = (q / t0) % t1 + shy2, lz = q / (t0 * t1) + shz2;
       const int l = (lz * e1 + ly) * e0 + lx;
       const int gi = S.gidx[i * E2 + l];
       if (gi < 0) continue;
-      const double w = vertex_row<DIM, NF, false>(a, S, S.u, l, lx, ly, lz, i);
+      const double w = vertex_row<DIM, NF, false>(a, S, S.u, l, (lz * a.ec[1] + ly) * a.ec[0] + lx, i);
       __stcg(wout + gi, w);
       const double ri = S.r[i * E2 + l], ui = S.u[i * E2 + l];
       g = fma(ri, ui, g);
       dl = fma(w, ui, dl);
       rh = fma(ri, ri, rh);
+    }
     }
   };
 

@@ -1468,6 +1468,11 @@ static int setup_tiled(fcm_mg* h) {
   for (int tz = 1; tz <= tzmax; ++tz)
     for (int ty = 1; ty <= tymax; ++ty)
       for (int tx = 1; tx <= B[0]; ++tx) {
+        if (const char* ft = getenv("FCM_TILE")) {   // measurement override "x,y,z"
+          int fx = 0, fy = 1, fz = 1;
+          sscanf(ft, "%d,%d,%d", &fx, &fy, &fz);
+          if (tx != fx || ty != fy || tz != fz) continue;
+        }
         const int ntl[3] = {(B[0] + tx - 1) / tx, (B[1] + ty - 1) / ty, (B[2] + tz - 1) / tz};
         const int64_t nt = (int64_t)ntl[0] * ntl[1] * ntl[2];
         if (nt > h->num_sms) continue;
@@ -1475,8 +1480,9 @@ static int setup_tiled(fcm_mg* h) {
         const int ec[3] = {tx + 3, dim > 1 ? ty + 3 : 1, dim > 2 ? tz + 3 : 1};
         const int64_t E2 = (int64_t)e[0] * e[1] * e[2], EC = (int64_t)ec[0] * ec[1] * ec[2];
         const int64_t T = (int64_t)tx * ty * tz;
-        if (tiled_smem_bytes(dim, nf, (int)E2, (int)EC, (int)T, 1 + ntypes) > smem_cap) continue;
         const int64_t E1 = (int64_t)(tx + 2) * (dim > 1 ? ty + 2 : 1) * (dim > 2 ? tz + 2 : 1);
+        if (E2 >= 65536 || EC >= 32768) continue;   // row-list entries pack (l, cell base) in 16 bits each
+        if (tiled_smem_bytes(dim, nf, (int)E2, (int)E1, (int)EC, (int)T, 1 + ntypes) > smem_cap) continue;
         const double gather = NC * (M1 + 4.0);
         const double cost = gather * R * (rounds(nf * E1) + rounds(nf * T)) + 6.0 * R * rounds(nf * E2);
         if (cost >= best) continue;
@@ -1493,7 +1499,7 @@ static int setup_tiled(fcm_mg* h) {
               }
               mx = std::max(mx, box_count(lo[0], hi[0], lo[1], hi[1], lo[2], hi[2]));
             }
-        if (tiled_smem_bytes(dim, nf, (int)E2, (int)EC, (int)T, 1 + ntypes + mx) > smem_cap) continue;
+        if (tiled_smem_bytes(dim, nf, (int)E2, (int)E1, (int)EC, (int)T, 1 + ntypes + mx) > smem_cap) continue;
         best = cost; bt[0] = tx; bt[1] = ty; bt[2] = tz; best_indiv = mx;
       }
   if (bt[0] == 0) return FCM_OK;
@@ -1507,7 +1513,8 @@ static int setup_tiled(fcm_mg* h) {
   t.max_indiv = best_indiv;
   t.ntypes = ntypes;
   const int E2 = t.e[0] * t.e[1] * t.e[2], EC = t.ec[0] * t.ec[1] * t.ec[2];
-  const size_t sm = tiled_smem_bytes(dim, nf, E2, EC, bt[0] * bt[1] * bt[2], 1 + ntypes + best_indiv);
+  const int E1 = (bt[0] + 2) * (dim > 1 ? bt[1] + 2 : 1) * (dim > 2 ? bt[2] + 2 : 1);
+  const size_t sm = tiled_smem_bytes(dim, nf, E2, E1, EC, bt[0] * bt[1] * bt[2], 1 + ntypes + best_indiv);
   RC(allow_smem(k, sm));
   int per_sm = 0;
   CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kTiledThreads, sm));
@@ -1518,6 +1525,26 @@ static int setup_tiled(fcm_mg* h) {
   t.jacobi = h->prm.coarse == FCM_COARSE_JACOBI_PCG;
   t.diag_inv = h->d_diag_inv;
   t.blk = L1.blk; t.type_inv = L1.type_inv; t.irr_inv = L1.irr_inv; t.inv_alpha = 1.0 / h->alpha;
+  // constant-coefficient stencils of the fast path (scalar problems): offsets o(k) = corner
+  // bits of local vertex mode k, coefficient of the neighbour at o(k2) - o(kc) (FCM_TILED_FAST=0
+  // disables)
+  t.fast = 0;
+  if (nf == 1 && !(getenv("FCM_TILED_FAST") && atoi(getenv("FCM_TILED_FAST")) == 0)) {
+    std::vector<double> K((size_t)L.m * L.m), Mi((size_t)M1 * M1, 0.0);
+    CU(cudaStreamSynchronize(h->stream));   // the inverses were computed on the handle's stream
+    CU(cudaMemcpy(K.data(), h->d_Kref, K.size() * 8, cudaMemcpyDeviceToHost));
+    const bool sm = !t.jacobi && ntypes > 0;
+    if (sm) CU(cudaMemcpy(Mi.data(), L1.type_inv, Mi.size() * 8, cudaMemcpyDeviceToHost));
+    for (int q = 0; q < 27; ++q) { t.st_op[q] = 0.0; t.st_sm[q] = 0.0; }
+    for (int kc = 0; kc < M1; ++kc)
+      for (int k2 = 0; k2 < M1; ++k2) {
+        int q = 0, mul = 1;
+        for (int d = 0; d < dim; ++d, mul *= 3) q += (((k2 >> d) & 1) - ((kc >> d) & 1) + 1) * mul;
+        t.st_op[q] += K[(size_t)kc * L.m + k2];
+        if (sm) t.st_sm[q] += Mi[(size_t)kc * M1 + k2];
+      }
+    t.fast = 1;
+  }
   const int64_t n1 = L.ndof_level[1];
   RC(h->alloc(&t.wpub[0], n1));
   RC(h->alloc(&t.wpub[1], n1));
@@ -1996,6 +2023,13 @@ extern "C" int fcm_mg_coarse_solve(fcm_mg* h, const double* r, double* x, int32_
         fprintf(stderr, "[fcm] tiled phases (ns, summed over solves; mean/max over blocks): update %.0f/%.0f "
                 "smooth %.0f/%.0f apply %.0f/%.0f allreduce %.0f/%.0f\n", mean[0], mx[0], mean[1], mx[1],
                 mean[2], mx[2], mean[3], mx[3]);
+        std::vector<std::pair<double, int>> w(h->t_blocks);
+        for (int b = 0; b < h->t_blocks; ++b) w[b] = {(double)(pr[4 * b + 1] + pr[4 * b + 2]), b};
+        std::sort(w.begin(), w.end());
+        fprintf(stderr, "[fcm] smooth+apply per block: min %.0f median %.0f; top:", w[0].first, w[w.size() / 2].first);
+        for (int k = 0; k < 8 && k < (int)w.size(); ++k)
+          fprintf(stderr, " %d:%.0f", w[w.size() - 1 - k].second, w[w.size() - 1 - k].first);
+        fprintf(stderr, "\n");
         CU(cudaMemset(h->tiled.prof, 0, pr.size() * 8));
       }
     }
