@@ -36,11 +36,12 @@ namespace fcm {
 
 struct TiledArgs {
   int n[3];          // cells per axis (1 for absent axes)
-  int blo[3];        // tiled vertex box (union of the free ranges of all components)
-  int tile[3];       // brick size (vertices)
-  int ntile[3];      // bricks per axis
-  int e[3];          // E2 extents = tile + 4 (1 for absent axes)
-  int ec[3];         // cell box extents = tile + 3 (1 for absent axes)
+  // bricks: [nblocks][6] = vertex origin (3), extents (3) of each CTA's brick T; they partition
+  // the vertex box (the union of the free ranges of all components).  Per brick, E2 extents
+  // are tile + 4 and the cell box tile + 3 (1 for absent axes).
+  const int* brick;
+  int tile[3];       // largest brick extents (reporting only)
+  int blo[3];        // vertex box origin (host bookkeeping)
   int64_t voff[3];   // class-major offset of component j's vertex class
   int vlo[3][3];     // free vertex range of component j
   int vhi[3][3];
@@ -118,6 +119,7 @@ struct TiledSmem {
   int* lop;     //          operator rows (T), stencil rows first; entry = l | cell base << 16
   int nsm, nop;
   int E2, EC, T;
+  int e0, e01, ec0, ec01;   // strides of E2 and of the cell box
 };
 
 // matrices are symmetric: stored packed lower-triangular, entry (a, b), b <= a, at a(a+1)/2 + b
@@ -140,8 +142,8 @@ template <int DIM, int NF, bool SMOOTH>
 __device__ __forceinline__ double vertex_row(const TiledArgs& a, const TiledSmem<DIM, NF>& S,
                                              const double* __restrict__ vec, int l, int cb, int i) {
   constexpr int NC = 1 << DIM;
-  const int e0 = a.e[0], e01 = a.e[0] * a.e[1];
-  const int ec0 = a.ec[0], ec01 = a.ec[0] * a.ec[1];
+  const int e0 = S.e0, e01 = S.e01;
+  const int ec0 = S.ec0, ec01 = S.ec01;
   const double scale = SMOOTH ? a.inv_alpha : a.alpha;
   double acc = 0.0;
   if constexpr (NF == 1) {
@@ -297,11 +299,19 @@ __global__ void __launch_bounds__(kTiledThreads, 1) k_coarse_tiled(TiledArgs a) 
   __shared__ double tot[3];
   __shared__ int n_indiv;
   TiledSmem<DIM, NF> S;
-  const int e0 = a.e[0], e1 = a.e[1], e2d = a.e[2];
-  const int t0 = a.tile[0], t1 = DIM > 1 ? a.tile[1] : 1, t2 = DIM > 2 ? a.tile[2] : 1;
+  // brick of this block
+  const int* br = a.brick + 6 * blockIdx.x;
+  const int t0 = br[3], t1 = DIM > 1 ? br[4] : 1, t2 = DIM > 2 ? br[5] : 1;
+  const int e0 = t0 + 4, e1 = DIM > 1 ? t1 + 4 : 1, e2d = DIM > 2 ? t2 + 4 : 1;
+  const int ec0 = t0 + 3, ec1 = DIM > 1 ? t1 + 3 : 1, ec2 = DIM > 2 ? t2 + 3 : 1;
+  const int ec01 = ec0 * ec1;
   S.E2 = e0 * e1 * e2d;
-  S.EC = a.ec[0] * a.ec[1] * a.ec[2];
+  S.EC = ec0 * ec1 * ec2;
   S.T = t0 * t1 * t2;
+  S.e0 = e0; S.e01 = e0 * e1; S.ec0 = ec0; S.ec01 = ec01;
+  const int o0 = br[0] - 2;
+  const int o1 = DIM > 1 ? br[1] - 2 : 0;
+  const int o2 = DIM > 2 ? br[2] - 2 : 0;
   const int nmat = 1 + a.ntypes + a.max_indiv;
   {
     double* d = reinterpret_cast<double*>(smem);
@@ -316,15 +326,9 @@ __global__ void __launch_bounds__(kTiledThreads, 1) k_coarse_tiled(TiledArgs a) 
     S.csm = S.cop + S.EC;
     S.vf = reinterpret_cast<unsigned char*>(S.csm + S.EC);
     S.lsm = reinterpret_cast<int*>(S.vf + ((S.E2 + 15) & ~15));
-    const int ne1 = (a.tile[0] + 2) * (DIM > 1 ? a.tile[1] + 2 : 1) * (DIM > 2 ? a.tile[2] + 2 : 1);
+    const int ne1 = (t0 + 2) * (DIM > 1 ? t1 + 2 : 1) * (DIM > 2 ? t2 + 2 : 1);
     S.lop = S.lsm + ne1;
   }
-  // brick of this block
-  const int bt = blockIdx.x;
-  const int tix = bt % a.ntile[0], tiy = (bt / a.ntile[0]) % a.ntile[1], tiz = bt / (a.ntile[0] * a.ntile[1]);
-  const int o0 = a.blo[0] + tix * a.tile[0] - 2;
-  const int o1 = DIM > 1 ? a.blo[1] + tiy * a.tile[1] - 2 : 0;
-  const int o2 = DIM > 2 ? a.blo[2] + tiz * a.tile[2] - 2 : 0;
   const int E2 = S.E2;
   // ---- one-time staging: K_ref block, shared Schwarz inverses, cell codes ----------------
   if (threadIdx.x == 0) n_indiv = 0;
@@ -340,7 +344,7 @@ __global__ void __launch_bounds__(kTiledThreads, 1) k_coarse_tiled(TiledArgs a) 
   __syncthreads();
   const int indiv0 = (1 + a.ntypes) * MM;   // first individual slot (doubles)
   for (int t = threadIdx.x; t < S.EC; t += blockDim.x) {
-    const int lx = t % a.ec[0], ly = (t / a.ec[0]) % a.ec[1], lz = t / (a.ec[0] * a.ec[1]);
+    const int lx = t % ec0, ly = (t / ec0) % ec1, lz = t / ec01;
     const int cx = o0 + lx, cy = o1 + ly, cz = o2 + lz;
     int2 code = make_int2(kNoCell, kNoCell);
     if (cx >= 0 && cy >= 0 && cz >= 0 && cx < a.n[0] && cy < a.n[1] && cz < a.n[2]) {
@@ -398,7 +402,6 @@ __global__ void __launch_bounds__(kTiledThreads, 1) k_coarse_tiled(TiledArgs a) 
     const bool in1 = lx >= 1 && lx <= e0 - 2 && (DIM < 2 || (ly >= 1 && ly <= e1 - 2)) &&
                      (DIM < 3 || (lz >= 1 && lz <= e2d - 2));
     if (NF == 1 && a.fast && in1) {
-      const int ec0 = a.ec[0], ec01 = a.ec[0] * a.ec[1];
       const int c0 = S.cop[lz * ec01 + ly * ec0 + lx], s0 = S.csm[lz * ec01 + ly * ec0 + lx];
       bool op = c0 != kNoCell && (c0 & ~kScaleBit) == 0, sm = !a.jacobi && s0 != kNoCell && (s0 & ~kScaleBit) == MM;
       for (int kc = 1; kc < NC; ++kc) {
@@ -417,7 +420,7 @@ __global__ void __launch_bounds__(kTiledThreads, 1) k_coarse_tiled(TiledArgs a) 
   if constexpr (NF == 1) {
     if (threadIdx.x < 4) lcnt[threadIdx.x] = 0;
     __syncthreads();
-    const int gx = a.tile[0] + 2, gy = DIM > 1 ? a.tile[1] + 2 : 1, gz = DIM > 2 ? a.tile[2] + 2 : 1;
+    const int gx = t0 + 2, gy = DIM > 1 ? t1 + 2 : 1, gz = DIM > 2 ? t2 + 2 : 1;
     const int ne1 = gx * gy * gz;
     const int lane = threadIdx.x & 31;
     for (int pass = 0; pass < 2; ++pass) {
@@ -428,7 +431,7 @@ __global__ void __launch_bounds__(kTiledThreads, 1) k_coarse_tiled(TiledArgs a) 
         if (q < ne1) {
           const int lx = q % gx + 1, ly = DIM > 1 ? (q / gx) % gy + 1 : 0, lz = DIM > 2 ? q / (gx * gy) + 1 : 0;
           l = (lz * e1 + ly) * e0 + lx;
-          cb = (lz * a.ec[1] + ly) * a.ec[0] + lx;
+          cb = (lz * ec1 + ly) * ec0 + lx;
           valid = S.gidx[l] >= 0;
           inT = lx >= 2 && lx <= e0 - 3 && (DIM < 2 || (ly >= 2 && ly <= e1 - 3)) && (DIM < 3 || (lz >= 2 && lz <= e2d - 3));
         }
@@ -490,7 +493,7 @@ __global__ void __launch_bounds__(kTiledThreads, 1) k_coarse_tiled(TiledArgs a) 
       double u = 0.0;
       if (gi >= 0) {
         if (a.jacobi) u = __ldg(a.diag_inv + gi) * S.r[i * E2 + l];
-        else u = vertex_row<DIM, NF, true>(a, S, S.r, l, (lz * a.ec[1] + ly) * a.ec[0] + lx, i);
+        else u = vertex_row<DIM, NF, true>(a, S, S.r, l, (lz * ec1 + ly) * ec0 + lx, i);
       }
       S.u[i * E2 + l] = u;
     }
@@ -516,7 +519,7 @@ __global__ void __launch_bounds__(kTiledThreads, 1) k_coarse_tiled(TiledArgs a) 
       const int l = (lz * e1 + ly) * e0 + lx;
       const int gi = S.gidx[i * E2 + l];
       if (gi < 0) continue;
-      const double w = vertex_row<DIM, NF, false>(a, S, S.u, l, (lz * a.ec[1] + ly) * a.ec[0] + lx, i);
+      const double w = vertex_row<DIM, NF, false>(a, S, S.u, l, (lz * ec1 + ly) * ec0 + lx, i);
       __stcg(wout + gi, w);
       const double ri = S.r[i * E2 + l], ui = S.u[i * E2 + l];
       g = fma(ri, ui, g);

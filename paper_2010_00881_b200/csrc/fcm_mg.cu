@@ -21,6 +21,7 @@
 #include <climits>
 #include <cmath>
 #include <cstring>
+#include <functional>
 #include <map>
 #include <memory>
 #include <string>
@@ -1460,65 +1461,194 @@ static int setup_tiled(fcm_mg* h) {
   int max_smem = 0;
   CU(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, h->dev));
   const size_t smem_cap = (size_t)max_smem - 2048;  // static shared memory of the kernel
+  // Per-brick cost model (ns per iteration, measured on B200 with FCM_TILED_PROF): a
+  // smoother or operator row costs c_fast on the stencil path, c_gen on the per-cell gather
+  // path; the E2 update c_upd per entry.  The iteration time is the slowest brick's, so a
+  // partition is scored by its maximum brick cost.
+  const double c_fast = 1.2, c_gen = 4.2, c_upd = 0.45;
+  std::vector<uint8_t> kind_h(h->ncell);
+  CU(cudaMemcpy(kind_h.data(), h->d_kind, h->ncell, cudaMemcpyDeviceToHost));
+  const int B0 = B[0], B1 = B[1], B2 = B[2];
+  std::vector<double> PS((size_t)(B0 + 1) * (B1 + 1) * (B2 + 1), 0.0), PO(PS.size(), 0.0);
+  auto PI = [&](int x, int y, int z) { return ((size_t)z * (B1 + 1) + y) * (B0 + 1) + x; };
+  for (int z = 0; z < B2; ++z)
+    for (int y = 0; y < B1; ++y)
+      for (int x = 0; x < B0; ++x) {
+        const int gv[3] = {t.blo[0] + x, t.blo[1] + y, t.blo[2] + z};
+        bool sm = nf == 1 && !jac && ntypes > 0, op = nf == 1;
+        int s0 = 0, k0 = -1;
+        for (int kc = 0; kc < NC; ++kc) {
+          int c3[3] = {0, 0, 0};
+          bool ex = true;
+          for (int d = 0; d < dim; ++d) {
+            c3[d] = gv[d] - ((kc >> d) & 1);
+            ex = ex && c3[d] >= 0 && c3[d] < L.n[d];
+          }
+          if (!ex) { sm = op = false; break; }
+          const int64_t c = ((int64_t)c3[2] * ny + c3[1]) * nx + c3[0];
+          const int bq = sm ? L1.blk_h[c] : 0, kd = kind_h[c];   // (no Schwarz blocks with Jacobi)
+          if (bq >= 0 || bq == kBlkNone || ((-bq - 1) & 0xfff) != 0 || (kc > 0 && bq != s0)) sm = false;
+          if (kd == 2 || (kc > 0 && kd != k0)) op = false;
+          s0 = bq; k0 = kd;
+        }
+        const double wsm = nf * (sm ? c_fast : c_gen), wop = nf * (op ? c_fast : c_gen);
+        PS[PI(x + 1, y + 1, z + 1)] = wsm + PS[PI(x, y + 1, z + 1)] + PS[PI(x + 1, y, z + 1)] + PS[PI(x + 1, y + 1, z)] -
+                                      PS[PI(x, y, z + 1)] - PS[PI(x, y + 1, z)] - PS[PI(x + 1, y, z)] + PS[PI(x, y, z)];
+        PO[PI(x + 1, y + 1, z + 1)] = wop + PO[PI(x, y + 1, z + 1)] + PO[PI(x + 1, y, z + 1)] + PO[PI(x + 1, y + 1, z)] -
+                                      PO[PI(x, y, z + 1)] - PO[PI(x, y + 1, z)] - PO[PI(x + 1, y, z)] + PO[PI(x, y, z)];
+      }
+  // sum of per-vertex weights over an inclusive local vertex box, clipped to the vertex box
+  auto vsum = [&](const std::vector<double>& Pw, const int lo[3], const int hi[3]) {
+    int a[3], b[3];
+    for (int d = 0; d < 3; ++d) {
+      a[d] = std::max(lo[d], 0);
+      b[d] = std::min(hi[d], B[d] - 1) + 1;
+      if (a[d] >= b[d]) return 0.0;
+    }
+    return Pw[PI(b[0], b[1], b[2])] - Pw[PI(a[0], b[1], b[2])] - Pw[PI(b[0], a[1], b[2])] - Pw[PI(b[0], b[1], a[2])] +
+           Pw[PI(a[0], a[1], b[2])] + Pw[PI(a[0], b[1], a[2])] + Pw[PI(b[0], a[1], a[2])] - Pw[PI(a[0], a[1], a[2])];
+  };
+  struct Brick { int lo[3], hi[3]; };   // local vertex coordinates, inclusive
+  auto brick_cost = [&](const Brick& b) {
+    int l1[3], h1[3];
+    int64_t e2 = 1;
+    for (int d = 0; d < 3; ++d) {
+      const bool pr = d < dim;
+      l1[d] = b.lo[d] - (pr ? 1 : 0); h1[d] = b.hi[d] + (pr ? 1 : 0);
+      e2 *= pr ? b.hi[d] - b.lo[d] + 5 : 1;
+    }
+    return vsum(PS, l1, h1) + vsum(PO, b.lo, b.hi) + c_upd * nf * e2;
+  };
+  // shared-memory need of a brick (individual matrices of its cell box counted exactly)
+  auto brick_smem = [&](const Brick& b, int* indiv) -> size_t {
+    int lo[3], hi[3], ext[3];
+    for (int d = 0; d < 3; ++d) {
+      if (d < dim) { lo[d] = t.blo[d] + b.lo[d] - 2; hi[d] = t.blo[d] + b.hi[d] + 1; }
+      else { lo[d] = 0; hi[d] = 0; }
+      ext[d] = d < dim ? b.hi[d] - b.lo[d] + 1 : 1;
+    }
+    *indiv = box_count(lo[0], hi[0], lo[1], hi[1], lo[2], hi[2]);
+    const int E2 = (ext[0] + 4) * (dim > 1 ? ext[1] + 4 : 1) * (dim > 2 ? ext[2] + 4 : 1);
+    const int EC = (ext[0] + 3) * (dim > 1 ? ext[1] + 3 : 1) * (dim > 2 ? ext[2] + 3 : 1);
+    const int E1 = (ext[0] + 2) * (dim > 1 ? ext[1] + 2 : 1) * (dim > 2 ? ext[2] + 2 : 1);
+    if (E2 >= 65536 || EC >= 32768) return SIZE_MAX;   // row-list entries pack (l, cell base) in 16 bits
+    return tiled_smem_bytes(dim, nf, E2, E1, EC, ext[0] * ext[1] * ext[2], 1 + ntypes);
+  };
+  // a partition is feasible when, with the largest individual-matrix count of any brick, every
+  // brick fits; returns the dynamic shared memory (0 = infeasible)
+  auto part_smem = [&](const std::vector<Brick>& bs, int* max_indiv) -> size_t {
+    size_t base = 0;
+    int mi = 0;
+    for (const Brick& b : bs) {
+      int ind = 0;
+      const size_t sm = brick_smem(b, &ind);
+      if (sm == SIZE_MAX) return 0;
+      base = std::max(base, sm);
+      mi = std::max(mi, ind);
+    }
+    const size_t tot = base + (size_t)mi * slot_stride(M1) * 8;
+    *max_indiv = mi;
+    return tot <= smem_cap ? tot : 0;
+  };
+  auto part_cost = [&](const std::vector<Brick>& bs) {
+    double c = 0.0;
+    for (const Brick& b : bs) c = std::max(c, brick_cost(b));
+    return c;
+  };
+  std::vector<Brick> best_bs;
   double best = 1e300;
-  int bt[3] = {0, 0, 0}, best_indiv = 0;
-  const int R = kTiledThreads;
-  auto rounds = [&](int64_t w) { return (double)((w + R - 1) / R); };
+  size_t best_sm = 0;
+  int best_indiv = 0;
+  auto consider = [&](std::vector<Brick>&& bs) {
+    if (bs.empty() || (int)bs.size() > h->num_sms) return;
+    const double c = part_cost(bs);
+    if (c >= best) return;
+    int mi = 0;
+    const size_t sm = part_smem(bs, &mi);
+    if (!sm) return;
+    best = c; best_sm = sm; best_indiv = mi; best_bs = std::move(bs);
+  };
+  const char* ft = getenv("FCM_TILE");   // measurement override: "x,y,z" (uniform) or "bisect"
+  const bool only_uniform = ft && strcmp(ft, "bisect") != 0, only_bisect = ft && !only_uniform;
+  // (a) uniform bricks
   const int tzmax = dim > 2 ? B[2] : 1, tymax = dim > 1 ? B[1] : 1;
-  for (int tz = 1; tz <= tzmax; ++tz)
+  for (int tz = 1; tz <= tzmax && !only_bisect; ++tz)
     for (int ty = 1; ty <= tymax; ++ty)
       for (int tx = 1; tx <= B[0]; ++tx) {
-        if (const char* ft = getenv("FCM_TILE")) {   // measurement override "x,y,z"
+        if (only_uniform) {
           int fx = 0, fy = 1, fz = 1;
           sscanf(ft, "%d,%d,%d", &fx, &fy, &fz);
           if (tx != fx || ty != fy || tz != fz) continue;
         }
-        const int ntl[3] = {(B[0] + tx - 1) / tx, (B[1] + ty - 1) / ty, (B[2] + tz - 1) / tz};
-        const int64_t nt = (int64_t)ntl[0] * ntl[1] * ntl[2];
-        if (nt > h->num_sms) continue;
-        const int e[3] = {tx + 4, dim > 1 ? ty + 4 : 1, dim > 2 ? tz + 4 : 1};
-        const int ec[3] = {tx + 3, dim > 1 ? ty + 3 : 1, dim > 2 ? tz + 3 : 1};
-        const int64_t E2 = (int64_t)e[0] * e[1] * e[2], EC = (int64_t)ec[0] * ec[1] * ec[2];
-        const int64_t T = (int64_t)tx * ty * tz;
-        const int64_t E1 = (int64_t)(tx + 2) * (dim > 1 ? ty + 2 : 1) * (dim > 2 ? tz + 2 : 1);
-        if (E2 >= 65536 || EC >= 32768) continue;   // row-list entries pack (l, cell base) in 16 bits each
-        if (tiled_smem_bytes(dim, nf, (int)E2, (int)E1, (int)EC, (int)T, 1 + ntypes) > smem_cap) continue;
-        const double gather = NC * (M1 + 4.0);
-        const double cost = gather * R * (rounds(nf * E1) + rounds(nf * T)) + 6.0 * R * rounds(nf * E2);
-        if (cost >= best) continue;
-        int mx = 0;   // individual matrices of the worst brick's cell box
         const int tt[3] = {tx, ty, tz};
-        for (int k = 0; k < ntl[2]; ++k)
-          for (int j = 0; j < ntl[1]; ++j)
-            for (int i = 0; i < ntl[0]; ++i) {
-              int lo[3], hi[3];
-              const int id[3] = {i, j, k};
-              for (int d = 0; d < 3; ++d) {
-                if (d < dim) { lo[d] = t.blo[d] + id[d] * tt[d] - 2; hi[d] = lo[d] + tt[d] + 2; }
-                else { lo[d] = 0; hi[d] = 0; }
-              }
-              mx = std::max(mx, box_count(lo[0], hi[0], lo[1], hi[1], lo[2], hi[2]));
+        const int ntl[3] = {(B[0] + tx - 1) / tx, (B[1] + ty - 1) / ty, (B[2] + tz - 1) / tz};
+        if ((int64_t)ntl[0] * ntl[1] * ntl[2] > h->num_sms) continue;
+        std::vector<Brick> bs;
+        for (int kz = 0; kz < ntl[2]; ++kz)
+          for (int ky = 0; ky < ntl[1]; ++ky)
+            for (int kx = 0; kx < ntl[0]; ++kx) {
+              Brick b;
+              const int id[3] = {kx, ky, kz};
+              for (int d = 0; d < 3; ++d) { b.lo[d] = id[d] * tt[d]; b.hi[d] = std::min(b.lo[d] + tt[d], B[d]) - 1; }
+              bs.push_back(b);
             }
-        if (tiled_smem_bytes(dim, nf, (int)E2, (int)E1, (int)EC, (int)T, 1 + ntypes + mx) > smem_cap) continue;
-        best = cost; bt[0] = tx; bt[1] = ty; bt[2] = tz; best_indiv = mx;
+        consider(std::move(bs));
       }
-  if (bt[0] == 0) return FCM_OK;
-  for (int i = 0; i < 3; ++i) {
-    t.tile[i] = bt[i];
-    t.ntile[i] = (B[i] + bt[i] - 1) / bt[i];
-    const bool present = i < dim;
-    t.e[i] = present ? bt[i] + 4 : 1;
-    t.ec[i] = present ? bt[i] + 3 : 1;
+  // (b) recursive bisection balancing the modelled cost (bricks of unequal size where cut
+  //     cells make rows expensive); leaf counts up to one brick per SM
+  std::function<void(const Brick&, int, std::vector<Brick>&)> bisect = [&](const Brick& b, int nl, std::vector<Brick>& out) {
+    if (nl == 1) { out.push_back(b); return; }
+    const int na = nl / 2, nb2 = nl - na;
+    int ext[3], emax = 0;
+    for (int d = 0; d < dim; ++d) { ext[d] = b.hi[d] - b.lo[d] + 1; emax = std::max(emax, ext[d]); }
+    double bs = 1e300;
+    Brick ba{}, bb{};
+    for (int d = 0; d < dim; ++d) {
+      if (ext[d] < 2 || 2 * ext[d] < emax) continue;   // split along the longer axes only
+      for (int p = b.lo[d] + 1; p <= b.hi[d]; ++p) {
+        Brick l = b, r = b;
+        l.hi[d] = p - 1; r.lo[d] = p;
+        int64_t vl = 1, vr = 1;
+        for (int q = 0; q < dim; ++q) { vl *= l.hi[q] - l.lo[q] + 1; vr *= r.hi[q] - r.lo[q] + 1; }
+        if (vl < na || vr < nb2) continue;
+        const double sc = std::max(brick_cost(l) / na, brick_cost(r) / nb2);
+        if (sc < bs) { bs = sc; ba = l; bb = r; }
+      }
+    }
+    if (bs == 1e300) { out.clear(); return; }
+    bisect(ba, na, out);
+    if (out.empty()) return;
+    bisect(bb, nb2, out);
+  };
+  if (!only_uniform) {
+    Brick all{};
+    for (int d = 0; d < 3; ++d) { all.lo[d] = 0; all.hi[d] = B[d] - 1; }
+    for (int nl = h->num_sms; nl >= std::max(1, h->num_sms / 2); nl -= 4) {
+      std::vector<Brick> bs;
+      bisect(all, nl, bs);
+      consider(std::move(bs));
+    }
   }
+  if (best_bs.empty()) return FCM_OK;
+  const int nb = (int)best_bs.size();
+  std::vector<int> bh((size_t)6 * nb);
+  for (int i = 0; i < 3; ++i) t.tile[i] = 0;
+  for (int b = 0; b < nb; ++b)
+    for (int d = 0; d < 3; ++d) {
+      bh[6 * b + d] = t.blo[d] + best_bs[b].lo[d];
+      bh[6 * b + 3 + d] = best_bs[b].hi[d] - best_bs[b].lo[d] + 1;
+      t.tile[d] = std::max(t.tile[d], bh[6 * b + 3 + d]);
+    }
+  int* d_brick = nullptr;
+  RC(h->alloc(&d_brick, bh.size()));
+  CU(cudaMemcpy(d_brick, bh.data(), bh.size() * sizeof(int), cudaMemcpyHostToDevice));
+  t.brick = d_brick;
   t.max_indiv = best_indiv;
   t.ntypes = ntypes;
-  const int E2 = t.e[0] * t.e[1] * t.e[2], EC = t.ec[0] * t.ec[1] * t.ec[2];
-  const int E1 = (bt[0] + 2) * (dim > 1 ? bt[1] + 2 : 1) * (dim > 2 ? bt[2] + 2 : 1);
-  const size_t sm = tiled_smem_bytes(dim, nf, E2, E1, EC, bt[0] * bt[1] * bt[2], 1 + ntypes + best_indiv);
+  const size_t sm = best_sm;
   RC(allow_smem(k, sm));
   int per_sm = 0;
   CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kTiledThreads, sm));
-  const int nb = t.ntile[0] * t.ntile[1] * t.ntile[2];
   if (per_sm < 1 || nb > per_sm * h->num_sms) return FCM_OK;
   t.kind = h->d_kind; t.cut_idx = h->d_cut_idx; t.cutK = h->d_cutK; t.ldK = L.m; t.Kref = h->d_Kref;
   t.alpha = h->alpha;
@@ -1559,9 +1689,9 @@ static int setup_tiled(fcm_mg* h) {
     CU(cudaMemsetAsync(t.prof, 0, (size_t)32 * nb, h->stream));
   }
   if (getenv("FCM_VERBOSE"))
-    fprintf(stderr, "[fcm] tiled coarse: box %d x %d x %d, tile %d x %d x %d, %d blocks, %d types, "
-            "<= %d individual matrices per brick, smem %zu B\n", B[0], B[1], B[2], bt[0], bt[1], bt[2], nb,
-            ntypes, best_indiv, sm);
+    fprintf(stderr, "[fcm] tiled coarse: box %d x %d x %d, %d bricks (largest %d x %d x %d), modelled max "
+            "brick cost %.0f ns/iteration, %d types, <= %d individual matrices per brick, smem %zu B\n",
+            B[0], B[1], B[2], nb, t.tile[0], t.tile[1], t.tile[2], best, ntypes, best_indiv, sm);
   h->tiled = t;
   h->ktiled = k;
   h->t_blocks = nb;
