@@ -155,6 +155,7 @@ struct fcm_mg {
   TiledArgs tiled{};
   int t_blocks = 0;
   size_t t_smem = 0;
+  std::vector<double> t_feat;   // FCM_TILED_PROF: per-brick model features (calibration)
   // FCG
   double *f_b = nullptr, *f_x = nullptr, *f_r = nullptr, *f_ro = nullptr, *f_p = nullptr, *f_q = nullptr;
   Scalars* d_s = nullptr;
@@ -1461,11 +1462,12 @@ static int setup_tiled(fcm_mg* h) {
   int max_smem = 0;
   CU(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, h->dev));
   const size_t smem_cap = (size_t)max_smem - 2048;  // static shared memory of the kernel
-  // Per-brick cost model (ns per iteration, measured on B200 with FCM_TILED_PROF): a
-  // smoother or operator row costs c_fast on the stencil path, c_gen on the per-cell gather
-  // path; the E2 update c_upd per entry.  The iteration time is the slowest brick's, so a
-  // partition is scored by its maximum brick cost.
-  const double c_fast = 1.2, c_gen = 4.2, c_upd = 0.45;
+  // Per-brick cost model (ns per iteration; least-squares fit of the per-brick phase times
+  // measured on B200 with FCM_TILED_PROF/FCM_TILED_DUMP over 268 bricks of two partitions of
+  // config 2, 5 % rms): smoother rows c_fs (stencil) / c_gs (gather), operator rows c_fo /
+  // c_go, c_ind per individual matrix staged, c_upd per E2 entry.  The iteration time is the
+  // slowest brick's, so a partition is scored by its maximum brick cost.
+  const double c_fs = 1.95, c_gs = 3.2, c_fo = 3.17, c_go = 4.31, c_ind = 2.0, c_upd = 0.17;
   std::vector<uint8_t> kind_h(h->ncell);
   CU(cudaMemcpy(kind_h.data(), h->d_kind, h->ncell, cudaMemcpyDeviceToHost));
   const int B0 = B[0], B1 = B[1], B2 = B[2];
@@ -1491,7 +1493,7 @@ static int setup_tiled(fcm_mg* h) {
           if (kd == 2 || (kc > 0 && kd != k0)) op = false;
           s0 = bq; k0 = kd;
         }
-        const double wsm = nf * (sm ? c_fast : c_gen), wop = nf * (op ? c_fast : c_gen);
+        const double wsm = nf * (sm ? c_fs : c_gs), wop = nf * (op ? c_fo : c_go);
         PS[PI(x + 1, y + 1, z + 1)] = wsm + PS[PI(x, y + 1, z + 1)] + PS[PI(x + 1, y, z + 1)] + PS[PI(x + 1, y + 1, z)] -
                                       PS[PI(x, y, z + 1)] - PS[PI(x, y + 1, z)] - PS[PI(x + 1, y, z)] + PS[PI(x, y, z)];
         PO[PI(x + 1, y + 1, z + 1)] = wop + PO[PI(x, y + 1, z + 1)] + PO[PI(x + 1, y, z + 1)] + PO[PI(x + 1, y + 1, z)] -
@@ -1517,7 +1519,13 @@ static int setup_tiled(fcm_mg* h) {
       l1[d] = b.lo[d] - (pr ? 1 : 0); h1[d] = b.hi[d] + (pr ? 1 : 0);
       e2 *= pr ? b.hi[d] - b.lo[d] + 5 : 1;
     }
-    return vsum(PS, l1, h1) + vsum(PO, b.lo, b.hi) + c_upd * nf * e2;
+    int cl[3], ch[3];   // cell box of the brick
+    for (int d = 0; d < 3; ++d) {
+      cl[d] = d < dim ? t.blo[d] + b.lo[d] - 2 : 0;
+      ch[d] = d < dim ? t.blo[d] + b.hi[d] + 1 : 0;
+    }
+    return vsum(PS, l1, h1) + vsum(PO, b.lo, b.hi) + c_upd * nf * e2 +
+           c_ind * box_count(cl[0], ch[0], cl[1], ch[1], cl[2], ch[2]);
   };
   // shared-memory need of a brick (individual matrices of its cell box counted exactly)
   auto brick_smem = [&](const Brick& b, int* indiv) -> size_t {
@@ -1630,6 +1638,30 @@ static int setup_tiled(fcm_mg* h) {
     }
   }
   if (best_bs.empty()) return FCM_OK;
+  if (getenv("FCM_TILED_PROF")) {   // features: fast/gather smoother rows, fast/gather operator rows, E2, indiv
+    // (per-row unit weights: rerun the prefix sums with c_fast = 1, c_gen = 0 and vice versa)
+    h->t_feat.clear();
+    for (const Brick& b : best_bs) {
+      int l1[3], h1[3];
+      int64_t e2 = 1;
+      for (int d = 0; d < 3; ++d) {
+        const bool pr = d < dim;
+        l1[d] = b.lo[d] - (pr ? 1 : 0); h1[d] = b.hi[d] + (pr ? 1 : 0);
+        e2 *= pr ? b.hi[d] - b.lo[d] + 5 : 1;
+      }
+      const double ssum = vsum(PS, l1, h1), osum = vsum(PO, b.lo, b.hi);
+      int64_t n1 = 1, nt = 1;
+      for (int d = 0; d < 3; ++d) {
+        n1 *= std::min(h1[d], B[d] - 1) - std::max(l1[d], 0) + 1;
+        nt *= b.hi[d] - b.lo[d] + 1;
+      }
+      // rows: fast*c_fast + gen*c_gen = sum, fast + gen = n -> solve for the counts
+      const double sg = (ssum - c_fs * n1 * nf) / (c_gs - c_fs), og = (osum - c_fo * nt * nf) / (c_go - c_fo);
+      int ind = 0;
+      brick_smem(b, &ind);
+      for (double v : {n1 * nf - sg, sg, nt * nf - og, og, (double)e2, (double)ind}) h->t_feat.push_back(v);
+    }
+  }
   const int nb = (int)best_bs.size();
   std::vector<int> bh((size_t)6 * nb);
   for (int i = 0; i < 3; ++i) t.tile[i] = 0;
@@ -2160,6 +2192,11 @@ extern "C" int fcm_mg_coarse_solve(fcm_mg* h, const double* r, double* x, int32_
         for (int k = 0; k < 8 && k < (int)w.size(); ++k)
           fprintf(stderr, " %d:%.0f", w[w.size() - 1 - k].second, w[w.size() - 1 - k].first);
         fprintf(stderr, "\n");
+        if (getenv("FCM_TILED_DUMP"))
+          for (int b = 0; b < h->t_blocks && (size_t)(6 * b + 5) < h->t_feat.size(); ++b)
+            fprintf(stderr, "[fcm] brick %d feat %.0f %.0f %.0f %.0f %.0f %.0f time %llu %llu %llu %llu\n", b,
+                    h->t_feat[6 * b], h->t_feat[6 * b + 1], h->t_feat[6 * b + 2], h->t_feat[6 * b + 3],
+                    h->t_feat[6 * b + 4], h->t_feat[6 * b + 5], pr[4 * b], pr[4 * b + 1], pr[4 * b + 2], pr[4 * b + 3]);
         CU(cudaMemset(h->tiled.prof, 0, pr.size() * 8));
       }
     }
