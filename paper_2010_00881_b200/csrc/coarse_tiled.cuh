@@ -25,7 +25,9 @@
 //    After the all-reduce every CTA reads the w its neighbours published (E2 halo) and updates
 //    s and r REDUNDANTLY on E2 with the same scalars; then u on E1 and w on T need no further
 //    exchange.  Hence one grid-wide synchronisation per iteration, which also carries the
-//    three dot products (deterministic: every CTA sums the block partials in block order).
+//    three dot products: accumulated with fp64 atomics (every CTA reads the same totals; the
+//    summation order varies run to run), or, with FCM_TILED_ATOMIC=0, summed by every CTA in
+//    block order (bit-reproducible).
 //  * Stop when rho < rtol^2 rho_0 (recursive residual), iterations = x updates (as the
 //    oracle's standard PCG, x0 = 0).
 #pragma once
@@ -66,6 +68,7 @@ struct TiledArgs {
   double* x;
   double* wpub[2];          // published w (double-buffered by iteration parity)
   double* part;             // [2][3][nblocks]
+  double* acc;              // [3][4] fp64-atomic dot accumulators, or null (see tiled_arrive_wait)
   struct TiledCtl* ctl;     // barrier state (zero-initialised once per handle)
   double rtol2;
   int maxit;
@@ -250,16 +253,29 @@ __device__ __forceinline__ void t_red_release(unsigned* p, unsigned v) {
 
 // Arrival + wait: block partials posted, one RED per block, one polling thread; returns when
 // every block of this generation has arrived (all threads synchronised).
+// atomic_dots: the block sums are added with fp64 atomics into acc[G % 3][3] (G = global
+// generation) instead of being posted per block; readers then load 3 doubles instead of
+// 3 x gridDim partials (no same-line read storm on L2), at the price of a run-dependent
+// summation order (every block still reads the same totals).  acc[(G+2) % 3] is zeroed by
+// block 0 after barrier G: its last readers (generation G-1) have passed barrier G, and its
+// next writers (generation G+2) start after barrier G+1, which block 0 reaches after the zeroing.
 __device__ __noinline__ void tiled_arrive_wait(double v0, double v1, double v2, double* part,
                                                TiledCtl* ctl, unsigned target, unsigned gen,
-                                               double* red) {
+                                               double* red, double* acc, unsigned G) {
   block_sum3(v0, v1, v2, red);
   const int nb = gridDim.x;
   double* pp = part + (size_t)(gen & 1) * 3 * nb;
   if (threadIdx.x == 0) {
-    __stcg(pp + blockIdx.x, v0);
-    __stcg(pp + nb + blockIdx.x, v1);
-    __stcg(pp + 2 * nb + blockIdx.x, v2);
+    if (acc) {
+      double* ac = acc + 4 * (G % 3);
+      atomicAdd(ac, v0);
+      atomicAdd(ac + 1, v1);
+      atomicAdd(ac + 2, v2);
+    } else {
+      __stcg(pp + blockIdx.x, v0);
+      __stcg(pp + nb + blockIdx.x, v1);
+      __stcg(pp + 2 * nb + blockIdx.x, v2);
+    }
     t_red_release(&ctl->count, 1u);   // orders this block's earlier global writes (w, partials)
     while ((int)(t_ld_acquire(&ctl->count) - target) < 0) {}
   }
@@ -267,7 +283,13 @@ __device__ __noinline__ void tiled_arrive_wait(double v0, double v1, double v2, 
 }
 // Totals of generation gen, summed in block order by warp 0 (bit-identical on every block);
 // call after tiled_arrive_wait; the caller synchronises before reading tot.
-__device__ __forceinline__ void tiled_totals(const double* part, unsigned gen, double* tot) {
+__device__ __forceinline__ void tiled_totals(const double* part, unsigned gen, double* tot, double* acc,
+                                             unsigned G) {
+  if (acc) {
+    if (threadIdx.x < 3) tot[threadIdx.x] = __ldcg(acc + 4 * (G % 3) + threadIdx.x);
+    if (blockIdx.x == 0 && threadIdx.x >= 32 && threadIdx.x < 35) acc[4 * ((G + 2) % 3) + threadIdx.x - 32] = 0.0;
+    return;
+  }
   if (threadIdx.x < 32) {
     const int nb = gridDim.x, l = threadIdx.x;
     const double* pp = part + (size_t)(gen & 1) * 3 * nb;
@@ -548,10 +570,11 @@ __global__ void __launch_bounds__(kTiledThreads, 1) k_coarse_tiled(TiledArgs a) 
       wl[k] = gi >= 0 ? __ldcg(wv + gi) : 0.0;
     }
   };
-  tiled_arrive_wait(g_loc, d_loc, r_loc, a.part, a.ctl, cnt0 + (gen + 1) * gridDim.x, gen + 1, red);
+  const unsigned G0 = cnt0 / gridDim.x;   // global generation before this launch
+  tiled_arrive_wait(g_loc, d_loc, r_loc, a.part, a.ctl, cnt0 + (gen + 1) * gridDim.x, gen + 1, red, a.acc, G0 + gen + 1);
   ++gen;
   preload_w(a.wpub[0]);
-  tiled_totals(a.part, gen, tot);
+  tiled_totals(a.part, gen, tot, a.acc, G0 + gen);
   __syncthreads();
   double gamma = tot[0], delta = tot[1];
   const double rho0 = tot[2];
@@ -605,10 +628,10 @@ __global__ void __launch_bounds__(kTiledThreads, 1) k_coarse_tiled(TiledArgs a) 
     apply_T(a.wpub[it & 1], g_loc, d_loc, r_loc);
     __syncthreads();
     const unsigned long long tp3 = a.prof ? t_now() : 0ull;
-    tiled_arrive_wait(g_loc, d_loc, r_loc, a.part, a.ctl, cnt0 + (gen + 1) * gridDim.x, gen + 1, red);
+    tiled_arrive_wait(g_loc, d_loc, r_loc, a.part, a.ctl, cnt0 + (gen + 1) * gridDim.x, gen + 1, red, a.acc, G0 + gen + 1);
     ++gen;
     preload_w(a.wpub[it & 1]);
-    tiled_totals(a.part, gen, tot);
+    tiled_totals(a.part, gen, tot, a.acc, G0 + gen);
     __syncthreads();
     if (a.prof && threadIdx.x == 0) {
       const unsigned long long tp4 = t_now();

@@ -1711,6 +1711,13 @@ static int setup_tiled(fcm_mg* h) {
   RC(h->alloc(&t.wpub[0], n1));
   RC(h->alloc(&t.wpub[1], n1));
   RC(h->alloc(&t.part, (size_t)6 * nb));
+  t.acc = nullptr;
+  // fp64-atomic dot accumulators (default; FCM_TILED_ATOMIC=0 = block-order partial sums,
+  // bit-reproducible run to run, ~0.7 us slower per inner iteration at cfg2)
+  if (!(getenv("FCM_TILED_ATOMIC") && atoi(getenv("FCM_TILED_ATOMIC")) == 0)) {
+    RC(h->alloc(&t.acc, 12));
+    CU(cudaMemsetAsync(t.acc, 0, 12 * 8, h->stream));
+  }
   RC(h->alloc(&t.ctl, 1));
   CU(cudaMemsetAsync(t.ctl, 0, sizeof(TiledCtl), h->stream));
   t.rtol2 = h->prm.coarse_rtol * h->prm.coarse_rtol;
