@@ -179,6 +179,7 @@ struct fcm_mg {
   int rank = 0, nranks = 1, z0 = 0, z1 = 0;
   bool multi = false;               // slab mode (nranks > 1, or FCM_FORCE_SLAB on one rank: tests)
   int mma_bps = 4, list_bps = 8;    // blocks per SM of the MMA / list parts of k_cell_mma
+  int pdl = 1;                      // programmatic dependent launch of k_cell_mma (FCM_PDL)
   int ext_lo = 0, ext_n = 0;        // ghost-extended cell layers along the slab axis (relative)
   int64_t cut_first = 0;            // first owned cut cell in the cut-matrix array
   ncclComm_t comm = nullptr;
@@ -266,8 +267,14 @@ __global__ void __launch_bounds__(kThreads, M > 32 ? 2 : 4) k_cell_mma(MmaOp g, 
   load_tab(T, g.op);
   const bool apply = g.op.mode == OP_APPLY;
   const bool is_mma = (int)blockIdx.x < nb_mma;
+  // programmatic dependent launch: let the next launch's blocks be scheduled as soon as every
+  // block of this one is running; the prologue above and the staging below touch only static
+  // data (tables, K_ref, Schwarz inverses), so they overlap the previous launch's tail, and
+  // griddepcontrol.wait (a no-op without the launch attribute) orders the vector accesses
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   if (is_mma) stage_fragments<M>(As, apply ? g.op.Kref : g.op.type_inv, apply ? g.op.ldK : M);
   __syncthreads();
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   const int wpb = blockDim.x >> 5;
   double e;
   if (is_mma) {
@@ -757,8 +764,17 @@ static int launch_cellop(fcm_mg* h, int q, const CellOp& op, double* cp_dst = nu
     g.cp_src = cp_src; g.cp_dst = cp_dst; g.cp_n = cp_dst ? cp_n : 0;
     int nbm = nb_reg;
     void* args[] = {&g, &nbm};
-    cudaError_t e = cudaLaunchKernel(Lv.kmma, dim3(nb_reg + nb_list), dim3(kThreads), args,
-                                     std::max(mma_smem(Lv.m), list_smem(Lv.m, Lv.G)), h->stream);
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(nb_reg + nb_list);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = std::max(mma_smem(Lv.m), list_smem(Lv.m, Lv.G));
+    cfg.stream = h->stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = h->pdl ? 1 : 0;
+    cudaError_t e = cudaLaunchKernelExC(&cfg, Lv.kmma, args);
     h->count();
     if (e != cudaSuccess) return fail(FCM_ECUDA, "mma kernel launch: %s", cudaGetErrorString(e));
     return FCM_OK;
@@ -1760,6 +1776,7 @@ static int setup_impl(const fcm_grid* g, const fcm_params* prm, const fcm_slab* 
   h->alpha = alpha;
   if (const char* e = getenv("FCM_MMA_BPS")) h->mma_bps = std::max(1, atoi(e));
   if (const char* e = getenv("FCM_LIST_BPS")) h->list_bps = std::max(1, atoi(e));
+  if (const char* e = getenv("FCM_PDL")) h->pdl = atoi(e) > 0;
   if (slab) {
     if (slab->nranks < 1 || slab->rank < 0 || slab->rank >= slab->nranks || slab->z_begin < 0 ||
         slab->z_end > nsax || slab->z_begin >= slab->z_end)
