@@ -220,7 +220,9 @@ __device__ __forceinline__ double reg_cells(const CellOp& op, const Tab& T, cons
 
 // Individual cells (op.list != nullptr) or, without a compile-time M, all cells with per-cell
 // matrix selection.  Groups of G lanes per cell; xs/ids: per-warp shared scratch (CPW*m).
-template <int G, bool FUSE>
+// MC: compile-time m (0 = runtime): the row loop is fully unrolled, so all m matrix loads of
+// a row are in flight at once (one L2/HBM latency per cell instead of one per load pair)
+template <int G, bool FUSE, int MC = 0>
 __device__ __forceinline__ double list_cells(const CellOp& op, const Tab& T, int warp, int nwarps,
                                              double* xs_warp, int* ids_warp) {
   constexpr int CPW = 32 / G;
@@ -285,12 +287,28 @@ __device__ __forceinline__ double list_cells(const CellOp& op, const Tab& T, int
       for (int a = gl; a < m; a += G) {
         double acc0 = 0.0, acc1 = 0.0;
         const double* col = Mat + a;
-        int b = 0;
-        for (; b + 2 <= m; b += 2) {
-          acc0 = fma(__ldg(col + (size_t)b * ld), xs[b], acc0);
-          acc1 = fma(__ldg(col + (size_t)(b + 1) * ld), xs[b + 1], acc1);
+        if constexpr (MC > 0) {
+          double mv[MC];
+#pragma unroll
+          for (int b = 0; b < MC; ++b) mv[b] = __ldg(col + (size_t)b * ld);
+          double acc2 = 0.0, acc3 = 0.0;
+#pragma unroll
+          for (int b = 0; b < MC; b += 4) {
+            acc0 = fma(mv[b], xs[b], acc0);
+            if (b + 1 < MC) acc1 = fma(mv[b + 1], xs[b + 1], acc1);
+            if (b + 2 < MC) acc2 = fma(mv[b + 2], xs[b + 2], acc2);
+            if (b + 3 < MC) acc3 = fma(mv[b + 3], xs[b + 3], acc3);
+          }
+          acc0 += acc2;
+          acc1 += acc3;
+        } else {
+          int b = 0;
+          for (; b + 2 <= m; b += 2) {
+            acc0 = fma(__ldg(col + (size_t)b * ld), xs[b], acc0);
+            acc1 = fma(__ldg(col + (size_t)(b + 1) * ld), xs[b + 1], acc1);
+          }
+          if (b < m) acc0 = fma(__ldg(col + (size_t)b * ld), xs[b], acc0);
         }
-        if (b < m) acc0 = fma(__ldg(col + (size_t)b * ld), xs[b], acc0);
         const double y = scale * (acc0 + acc1);
         const int id = ids[a];
         if (id >= 0) atomicAdd(out + id, coef * y);

@@ -128,18 +128,18 @@ __device__ __forceinline__ double coarse_cells(const CellOp& op, const Tab& T, c
     if (gcells) {   // MMA groups and the individual list, both grid-strided over every warp
       const int gw = blockIdx.x * wpb + wib, nw = gridDim.x * wpb;
       const double e = mma_cells<M, FUSE>(op, gcells, gmat, ngroups, T, As, main_slot, gw, nw);
-      return e + list_cells<G, FUSE>(op, T, gw, nw, xs, ids);
+      return e + list_cells<G, FUSE, (M > 0 && M <= 32 ? M : 0)>(op, T, gw, nw, xs, ids);
     }
   }
   if (M > 0 && nbl == 0) {
     double e = 0.0;
     if constexpr (M > 0)
       e = reg_cells<M, split_of<M>(), FUSE>(op, T, Ms, xsr, blockIdx.x * wpb + wib, gridDim.x * wpb);
-    return e + list_cells<G, FUSE>(op, T, blockIdx.x * wpb + wib, gridDim.x * wpb, xs, ids);
+    return e + list_cells<G, FUSE, (M > 0 && M <= 32 ? M : 0)>(op, T, blockIdx.x * wpb + wib, gridDim.x * wpb, xs, ids);
   }
   if (M == 0 || (int)blockIdx.x < nbl) {
     const int nb = M == 0 ? gridDim.x : nbl;
-    return list_cells<G, FUSE>(op, T, blockIdx.x * wpb + wib, nb * wpb, xs, ids);
+    return list_cells<G, FUSE, (M > 0 && M <= 32 ? M : 0)>(op, T, blockIdx.x * wpb + wib, nb * wpb, xs, ids);
   }
   if constexpr (M > 0)
     return reg_cells<M, split_of<M>(), FUSE>(op, T, Ms, xsr, (blockIdx.x - nbl) * wpb + wib,

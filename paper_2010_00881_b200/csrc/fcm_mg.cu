@@ -284,8 +284,8 @@ __global__ void __launch_bounds__(kThreads, M > 32 ? 2 : 4) k_cell_mma(MmaOp g, 
     constexpr int CPW = 32 / G;
     double* xs = As + (threadIdx.x >> 5) * CPW * g.op.m;
     int* ids = reinterpret_cast<int*>(As + wpb * CPW * g.op.m) + (threadIdx.x >> 5) * CPW * g.op.m;
-    e = list_cells<G, false>(g.op, T, (blockIdx.x - nb_mma) * wpb + (threadIdx.x >> 5),
-                             (gridDim.x - nb_mma) * wpb, xs, ids);
+    e = list_cells<G, false, (M <= 32 ? M : 0)>(g.op, T, (blockIdx.x - nb_mma) * wpb + (threadIdx.x >> 5),
+                                               (gridDim.x - nb_mma) * wpb, xs, ids);
   }
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < g.cp_n; i += (int64_t)gridDim.x * blockDim.x)
     g.cp_dst[i] = g.cp_src[i];
