@@ -257,13 +257,22 @@ def test_empty_level_rejected():
     assert e.value.code == -1
 
 
+COARSE_CASES = dict(CASES)
+# 2D coarse CG+AS (k_coarse_tiled<2,1>) and a 3D level of 11^3 vertices with voids (many bricks
+# of unequal size from the cost-balanced bisection, stencil and gather rows mixed)
+COARSE_CASES["2d_p3_aspcg"] = lambda: small_config(2, 9, 3, voids=1, seed=2)
+COARSE_CASES["3d_n12_p2"] = lambda: small_config(3, 12, 2, voids=3, seed=11)
+
+
 @pytest.mark.parametrize("tiled", ["1", "0"])
-@pytest.mark.parametrize("case", ["3d_p2", "3d_trunk_elast", "3d_p2_jacobi"])
+@pytest.mark.parametrize("case", ["3d_p2", "3d_trunk_elast", "3d_p2_jacobi", "2d_p3_aspcg", "3d_n12_p2"])
 def test_coarse_kernels_both_paths(case, tiled, monkeypatch):
     # the shared-memory tiled coarse PCG (small coarse levels) and the grid-wide kernel (large
     # ones) against the oracle's coarse CG, on the same level; iterations +-1 (reading R16)
     monkeypatch.setenv("FCM_COARSE_TILED", tiled)
-    pair = Pair(CASES[case]())
+    pair = Pair(COARSE_CASES[case]())
+    name, _, _ = pair.S.coarse_info()
+    assert (name == "k_coarse_tiled") == (tiled == "1")   # levels this small always fit the tiled kernel
     H = pair.hier()
     I1 = pair.P.dof.level_dofs(1)
     r = np.zeros(pair.P.dof.ndof)
