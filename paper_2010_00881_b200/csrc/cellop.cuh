@@ -303,6 +303,16 @@ __device__ __forceinline__ double list_cells(const CellOp& op, const Tab& T, int
           acc1 += acc3;
         } else {
           int b = 0;
+          for (; b + 16 <= m; b += 16) {   // 16 column loads in flight per trip
+            double mv[16];
+#pragma unroll
+            for (int j = 0; j < 16; ++j) mv[j] = __ldg(col + (size_t)(b + j) * ld);
+#pragma unroll
+            for (int j = 0; j < 16; j += 2) {
+              acc0 = fma(mv[j], xs[b + j], acc0);
+              acc1 = fma(mv[j + 1], xs[b + j + 1], acc1);
+            }
+          }
           for (; b + 2 <= m; b += 2) {
             acc0 = fma(__ldg(col + (size_t)b * ld), xs[b], acc0);
             acc1 = fma(__ldg(col + (size_t)(b + 1) * ld), xs[b + 1], acc1);
