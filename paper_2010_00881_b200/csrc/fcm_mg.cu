@@ -347,7 +347,17 @@ __global__ void k_scatter64(double* __restrict__ out, const double* __restrict__
     if (idx[i] >= 0) out[idx[i]] = in[i];
 }
 
+// Programmatic dependent launch (launches through pdl_launch): wait until the preceding
+// kernel has completed and its writes are visible, then let the next launch be scheduled.
+// A no-op for ordinary launches.
+#define FCM_PDL_ENTRY()                                      \
+  do {                                                       \
+    asm volatile("griddepcontrol.wait;" ::: "memory");       \
+    asm volatile("griddepcontrol.launch_dependents;" :::);   \
+  } while (0)
+
 __global__ void k_fill(double* x, double v, int64_t n) {
+  FCM_PDL_ENTRY();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     x[i] = v;
 }
@@ -358,6 +368,7 @@ __global__ void k_copy(double* __restrict__ y, const double* __restrict__ x, int
 // y[0..n) += a x; dst[0..ncp) = src (fused copy of an unrelated buffer)
 __global__ void k_axpy_copy(double* __restrict__ y, double a, const double* __restrict__ x, int64_t n,
                             double* __restrict__ dst, const double* __restrict__ src, int64_t ncp) {
+  FCM_PDL_ENTRY();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n || i < ncp; i += (int64_t)gridDim.x * blockDim.x) {
     if (i < n) y[i] = fma(a, x[i], y[i]);
     if (i < ncp) dst[i] = src[i];
@@ -370,6 +381,7 @@ __global__ void k_axpy(double* __restrict__ y, double a, const double* __restric
 // partials[block] = sum a.b over the block's grid-stride range (fixed grid -> deterministic)
 __global__ void k_dot(const double* __restrict__ a, const double* __restrict__ b, int64_t n, double* partials,
                       const uint8_t* __restrict__ own = nullptr) {
+  FCM_PDL_ENTRY();
   __shared__ double red[32];
   double s = 0.0;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
@@ -413,6 +425,7 @@ __global__ void k_fcg_update1(Scalars* s, const double* part_pq, int npq, double
                               const double* __restrict__ p, const double* __restrict__ q, int64_t n,
                               double* part_rr, const uint8_t* __restrict__ own = nullptr,
                               const double* pre = nullptr) {
+  FCM_PDL_ENTRY();
   __shared__ double red[32];
   const double pq = pre ? *pre : sum_partials(part_pq, npq);
   const double alpha = s->rz / pq;
@@ -433,10 +446,12 @@ __global__ void k_fcg_update1(Scalars* s, const double* part_pq, int npq, double
   }
 }
 __global__ void k_finalize(double* out, const double* part, int np) {
+  FCM_PDL_ENTRY();
   const double v = sum_partials(part, np);
   if (threadIdx.x == 0) *out = v;
 }
 __global__ void k_finalize2(double* out, const double* partA, const double* partB, int np) {
+  FCM_PDL_ENTRY();
   const double a = sum_partials(partA, np);
   const double b = sum_partials(partB, np);
   if (threadIdx.x == 0) { out[0] = a; out[1] = b; }
@@ -445,6 +460,7 @@ __global__ void k_finalize2(double* out, const double* partA, const double* part
 __global__ void k_dot2(const double* __restrict__ z, const double* __restrict__ r,
                        const double* __restrict__ ro, int64_t n, double* partA, double* partB,
                        const uint8_t* __restrict__ own = nullptr) {
+  FCM_PDL_ENTRY();
   __shared__ double red[32];
   double s1 = 0.0, s2 = 0.0;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
@@ -461,6 +477,7 @@ __global__ void k_dot2(const double* __restrict__ z, const double* __restrict__ 
 __global__ void k_fcg_update2(Scalars* s, const double* partA, const double* partB, int np,
                               double* __restrict__ p, const double* __restrict__ z, int64_t n,
                               const double* pre = nullptr) {
+  FCM_PDL_ENTRY();
   const double zr = pre ? pre[0] : sum_partials(partA, np);
   const double zro = pre ? pre[1] : sum_partials(partB, np);
   const double beta = (zr - zro) / s->rz;
@@ -482,6 +499,7 @@ __global__ void k_fcg_check(Scalars* s, cudaGraphConditionalHandle cond, double*
   cudaGraphSetConditional(cond, stop ? 0u : 1u);
 }
 __global__ void k_set_rz(Scalars* s) {
+  FCM_PDL_ENTRY();
   if (threadIdx.x == 0) s->rz = s->zr;
 }
 // x = Ainv b (dense, row-major, symmetric)
@@ -807,9 +825,25 @@ static int launch_cellop(fcm_mg* h, int q, const CellOp& op, double* cp_dst = nu
   return FCM_OK;
 }
 
+// launch with the programmatic-stream-serialization attribute (kernels that begin with
+// FCM_PDL_ENTRY), so a launch's scheduling overlaps the tail of the previous one
+template <typename... KArgs, typename... Args>
+static cudaError_t pdl_launch(fcm_mg* h, void (*k)(KArgs...), dim3 grid, dim3 block, Args... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = h->stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = h->pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(args)...);
+}
 static int fill(fcm_mg* h, double* x, double v, int64_t n) {
   if (n <= 0) return FCM_OK;
-  k_fill<<<grid_for(n, h->num_sms), kThreads, 0, h->stream>>>(x, v, n);
+  CU(pdl_launch(h, k_fill, dim3(grid_for(n, h->num_sms)), dim3(kThreads), x, v, n));
   h->count();
   CU(cudaGetLastError());
   return FCM_OK;
@@ -1068,8 +1102,8 @@ static int enqueue_vcycle(fcm_mg* h, int q, const double* b, double* x) {
   LevelDev& Lc = h->lev[q - 1];
   RC(enqueue_vcycle(h, q - 1, rb[cur], Lc.x));      // r_{l-1} = R r_l: prefix alias
   // x += R^T e (and, fused path, the next residual buffer = b)
-  k_axpy_copy<<<grid_for(N, h->num_sms), kThreads, 0, h->stream>>>(x, 1.0, Lc.x, Lc.ndof, fuse ? rb[cur ^ 1] : nullptr, b,
-                                                                    fuse ? N : 0);
+  CU(pdl_launch(h, k_axpy_copy, dim3(grid_for(N, h->num_sms)), dim3(kThreads), x, 1.0, Lc.x, Lc.ndof, fuse ? rb[cur ^ 1] : nullptr, b,
+                                                                    fuse ? N : 0));
   h->count();
   CU(cudaGetLastError());
   if (fuse) cur ^= 1;
@@ -2263,10 +2297,10 @@ static int capture_fcg(fcm_mg* h) {
     k_fcg_start<<<grid_for(N, h->num_sms), kThreads, 0, h->stream>>>(h->f_x, h->f_r, h->f_b, N);
     h->count();
     RC(enqueue_vcycle(h, p, h->f_r, z));
-    k_dot<<<nbd, kThreads, 0, h->stream>>>(z, h->f_r, N, h->d_partA, own);
+    CU(pdl_launch(h, k_dot, dim3(nbd), dim3(kThreads), z, h->f_r, N, h->d_partA, own));
     h->count();
     if (slab) {
-      k_finalize<<<1, 32, 0, h->stream>>>(red + 3, h->d_partA, nbd);
+      CU(pdl_launch(h, k_finalize, dim3(1), dim3(32), red + 3, h->d_partA, nbd));
       h->count();
       RC(allreduce(h, red + 3, 1));
     }
@@ -2282,14 +2316,14 @@ static int capture_fcg(fcm_mg* h) {
     RC(launch_cellop(h, p, make_op(h, p, OP_APPLY, h->f_p, h->f_q, 1.0, h->d_partB)));
     RC(exchange(h, p, h->f_q));
     if (slab) {
-      k_finalize<<<1, 32, 0, h->stream>>>(red, h->d_partB, nbc);
+      CU(pdl_launch(h, k_finalize, dim3(1), dim3(32), red, h->d_partB, nbc));
       h->count();
       RC(allreduce(h, red, 1));
     }
-    k_fcg_update1<<<nbd, kThreads, 0, h->stream>>>(h->d_s, h->d_partB, nbc, h->f_x, h->f_r, h->f_ro,
-                                                    h->f_p, h->f_q, N, h->d_partC, own, slab ? red : nullptr);
+    CU(pdl_launch(h, k_fcg_update1, dim3(nbd), dim3(kThreads), h->d_s, h->d_partB, nbc, h->f_x, h->f_r, h->f_ro,
+                                                    h->f_p, h->f_q, N, h->d_partC, own, slab ? red : nullptr));
     h->count();
-    k_finalize<<<1, 32, 0, h->stream>>>(&h->d_s->rr, h->d_partC, nbd);
+    CU(pdl_launch(h, k_finalize, dim3(1), dim3(32), &h->d_s->rr, h->d_partC, nbd));
     h->count();
     CU(cudaGetLastError());
     if (slab) RC(allreduce(h, &h->d_s->rr, 1));
@@ -2299,17 +2333,17 @@ static int capture_fcg(fcm_mg* h) {
   // iteration part 2: z = V(r), beta, p = z + beta p
   auto it2_body = [&]() -> int {
     RC(enqueue_vcycle(h, p, h->f_r, z));
-    k_dot2<<<nbd, kThreads, 0, h->stream>>>(z, h->f_r, h->f_ro, N, h->d_partA, h->d_partB, own);
+    CU(pdl_launch(h, k_dot2, dim3(nbd), dim3(kThreads), z, h->f_r, h->f_ro, N, h->d_partA, h->d_partB, own));
     h->count();
     if (slab) {
-      k_finalize2<<<1, 32, 0, h->stream>>>(red + 1, h->d_partA, h->d_partB, nbd);
+      CU(pdl_launch(h, k_finalize2, dim3(1), dim3(32), red + 1, h->d_partA, h->d_partB, nbd));
       h->count();
       RC(allreduce(h, red + 1, 2));
     }
-    k_fcg_update2<<<grid_for(N, h->num_sms), kThreads, 0, h->stream>>>(h->d_s, h->d_partA, h->d_partB, nbd, h->f_p, z, N,
-                                                                       slab ? red + 1 : nullptr);
+    CU(pdl_launch(h, k_fcg_update2, dim3(grid_for(N, h->num_sms)), dim3(kThreads), h->d_s, h->d_partA, h->d_partB, nbd, h->f_p, z, N,
+                                                                       slab ? red + 1 : nullptr));
     h->count();
-    k_set_rz<<<1, 32, 0, h->stream>>>(h->d_s);
+    CU(pdl_launch(h, k_set_rz, dim3(1), dim3(32), h->d_s));
     h->count();
     CU(cudaGetLastError());
     return FCM_OK;
@@ -2387,8 +2421,8 @@ static int pcg_core(fcm_mg* h, double rtol, int32_t maxit, int32_t* iters, doubl
   RC(capture_fcg(h));
   // ||b||^2
   const int nbd = dot_blocks(h);
-  k_dot<<<nbd, kThreads, 0, h->stream>>>(h->f_b, h->f_b, N, h->d_partA, h->multi ? h->d_own : nullptr);
-  k_finalize<<<1, 32, 0, h->stream>>>(&h->d_s->bb, h->d_partA, nbd);
+  CU(pdl_launch(h, k_dot, dim3(nbd), dim3(kThreads), h->f_b, h->f_b, N, h->d_partA, h->multi ? h->d_own : nullptr));
+  CU(pdl_launch(h, k_finalize, dim3(1), dim3(32), &h->d_s->bb, h->d_partA, nbd));
   h->count(2);
   RC(allreduce(h, &h->d_s->bb, 1));
   CU(cudaMemsetAsync(&h->d_s->flag, 0, sizeof(int), h->stream));
@@ -2492,8 +2526,8 @@ static int mg_solve_core(fcm_mg* h, double rtol, int32_t maxit, int32_t* iters, 
       k_axpy<<<grid_for(N, h->num_sms), kThreads, 0, h->stream>>>(h->f_x, 1.0, z, N);
       h->count();
       RC(residual(h, p, h->f_b, h->f_x, h->f_r));
-      k_dot<<<nbd, kThreads, 0, h->stream>>>(h->f_r, h->f_r, N, h->d_partA, own);
-      k_finalize<<<1, 32, 0, h->stream>>>(&h->d_s->rr, h->d_partA, nbd);
+      CU(pdl_launch(h, k_dot, dim3(nbd), dim3(kThreads), h->f_r, h->f_r, N, h->d_partA, own));
+      CU(pdl_launch(h, k_finalize, dim3(1), dim3(32), &h->d_s->rr, h->d_partA, nbd));
       h->count(2);
       CU(cudaGetLastError());
       RC(allreduce(h, &h->d_s->rr, 1));
@@ -2501,8 +2535,8 @@ static int mg_solve_core(fcm_mg* h, double rtol, int32_t maxit, int32_t* iters, 
       return FCM_OK;
     }));
   }
-  k_dot<<<nbd, kThreads, 0, h->stream>>>(h->f_b, h->f_b, N, h->d_partA, own);
-  k_finalize<<<1, 32, 0, h->stream>>>(&h->d_s->bb, h->d_partA, nbd);
+  CU(pdl_launch(h, k_dot, dim3(nbd), dim3(kThreads), h->f_b, h->f_b, N, h->d_partA, own));
+  CU(pdl_launch(h, k_finalize, dim3(1), dim3(32), &h->d_s->bb, h->d_partA, nbd));
   h->count(2);
   RC(allreduce(h, &h->d_s->bb, 1));
   CU(cudaMemcpyAsync(h->h_s, h->d_s, sizeof(Scalars), cudaMemcpyDeviceToHost, h->stream));
