@@ -93,9 +93,6 @@ __device__ __forceinline__ unsigned t_ld_relaxed(const unsigned* p) {
   asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
-__device__ __forceinline__ void t_st_release(unsigned* p, unsigned v) {
-  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
 
 // cell code: -1 = no cell (outside the grid); otherwise the matrix offset in the staged
 // matrix pool (doubles) | kScaleBit when the cell's scale is alpha (operator) or 1/alpha
