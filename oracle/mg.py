@@ -9,7 +9,10 @@ Additive Schwarz (Eq. AdditiveSchwarz):
   M^{-1} = sum_i P_i (P_i^T A P_i)^{-1} P_i^T,
 blocks (P:259): elementwise = the free level DOFs supported on one cell;
 patchwise = the union over the 2^d cells around a grid vertex (every vertex,
-boundary ones included; empty blocks skipped).  Block inverses by dense LU
+boundary ones included; empty blocks skipped) -- patch_rule "closure", the DOFs
+whose support intersects the patch, size (2p+1)^d as Table 1 (P:316-320) prints;
+patch_rule "interior" (reading R19, a variant kept only for the paper's
+iteration-count pin) keeps the DOFs whose whole support lies inside the patch.  Block inverses by dense LU
 (numpy.linalg.inv = LAPACK getrf/getri path, O8).  The sum is accumulated
 serially in block order (cell / vertex index, x fastest).
 
@@ -29,7 +32,7 @@ import scipy.linalg as sla
 
 
 class Level:
-    def __init__(self, prob, q, block, A_full, omega, inv_method="lu"):
+    def __init__(self, prob, q, block, A_full, omega, inv_method="lu", patch_rule="closure"):
         dof = prob.dof
         self.q = q
         self.idx = dof.level_dofs(q)
@@ -49,6 +52,10 @@ class Level:
                     blocks.append(pos[g])
         else:  # patch: 2^d cells around each grid vertex
             n, d = cfg.n, cfg.dim
+            if patch_rule == "interior":
+                # number of cells in the support of each DOF (reading R19 variant)
+                ok = cd >= 0
+                nsup = np.bincount(cd[ok], minlength=dof.ndof)
             for v in range((n + 1) ** d):
                 vc = [(v // (n + 1) ** a) % (n + 1) for a in range(d)]
                 cells = []
@@ -56,7 +63,14 @@ class Level:
                     cc = [vc[a] - 1 + ((corner >> a) & 1) for a in range(d)]
                     if all(0 <= x < n for x in cc):
                         cells.append(sum(cc[a] * n ** a for a in range(d)))
-                g = np.unique(np.concatenate([cd[c][cd[c] >= 0] for c in sorted(cells)]))
+                allg = np.concatenate([cd[c][cd[c] >= 0] for c in sorted(cells)])
+                if patch_rule == "closure":
+                    # every DOF whose support intersects the patch (Table 1: (2p+1)^d)
+                    g = np.unique(allg)
+                else:
+                    # "interior": only DOFs whose whole support lies inside the patch
+                    g, cnt = np.unique(allg, return_counts=True)
+                    g = g[cnt == nsup[g]]
                 if len(g):
                     blocks.append(pos[g])
         self.blocks = blocks
@@ -85,7 +99,7 @@ class Level:
 
 class Hierarchy:
     def __init__(self, prob, block=None, omega=None, n_pre=None, n_post=None, coarse=None,
-                 coarse_rtol=None, coarse_maxit=None, inv="lu"):
+                 coarse_rtol=None, coarse_maxit=None, inv="lu", patch_rule="closure"):
         cfg = prob.cfg
         self.prob = prob
         self.block = block or cfg.block
@@ -103,7 +117,8 @@ class Hierarchy:
             blk = self.block if q > 1 else "element"   # coarse AS is elementwise (R11)
             need_blocks = q > 1 or self.coarse == "as_pcg"
             if need_blocks:
-                self.levels[q] = Level(prob, q, blk, A, self.omega if q > 1 else 1.0, inv_method=inv)
+                self.levels[q] = Level(prob, q, blk, A, self.omega if q > 1 else 1.0, inv_method=inv,
+                                       patch_rule=patch_rule)
             else:
                 lv = Level.__new__(Level)
                 lv.q = q

@@ -237,6 +237,10 @@ struct TiledCtl {
   unsigned pad0[31];
   unsigned base;           // count at the end of the previous launch (written by block 0 last)
   unsigned pad1[31];
+  // global barrier generation at the end of the previous launch (written by block 0 last);
+  // 64-bit and explicit, so the accumulator rotation (G % 3) never depends on the wrapping
+  // 32-bit arrival counter (2^32 is not a multiple of the grid size)
+  unsigned long long gbase;
 };
 
 __device__ __forceinline__ unsigned t_ld_acquire(const unsigned* p) {
@@ -258,7 +262,7 @@ __device__ __forceinline__ void t_red_release(unsigned* p, unsigned v) {
 // next writers (generation G+2) start after barrier G+1, which block 0 reaches after the zeroing.
 __device__ __noinline__ void tiled_arrive_wait(double v0, double v1, double v2, double* part,
                                                TiledCtl* ctl, unsigned target, unsigned gen,
-                                               double* red, double* acc, unsigned G) {
+                                               double* red, double* acc, unsigned long long G) {
   block_sum3(v0, v1, v2, red);
   const int nb = gridDim.x;
   double* pp = part + (size_t)(gen & 1) * 3 * nb;
@@ -281,7 +285,7 @@ __device__ __noinline__ void tiled_arrive_wait(double v0, double v1, double v2, 
 // Totals of generation gen, summed in block order by warp 0 (bit-identical on every block);
 // call after tiled_arrive_wait; the caller synchronises before reading tot.
 __device__ __forceinline__ void tiled_totals(const double* part, unsigned gen, double* tot, double* acc,
-                                             unsigned G) {
+                                             unsigned long long G) {
   if (acc) {
     if (threadIdx.x < 3) tot[threadIdx.x] = __ldcg(acc + 4 * (G % 3) + threadIdx.x);
     if (blockIdx.x == 0 && threadIdx.x >= 32 && threadIdx.x < 35) acc[4 * ((G + 2) % 3) + threadIdx.x - 32] = 0.0;
@@ -567,7 +571,7 @@ __global__ void __launch_bounds__(kTiledThreads, 1) k_coarse_tiled(TiledArgs a) 
       wl[k] = gi >= 0 ? __ldcg(wv + gi) : 0.0;
     }
   };
-  const unsigned G0 = cnt0 / gridDim.x;   // global generation before this launch
+  const unsigned long long G0 = *(volatile const unsigned long long*)&a.ctl->gbase;   // generation before this launch
   tiled_arrive_wait(g_loc, d_loc, r_loc, a.part, a.ctl, cnt0 + (gen + 1) * gridDim.x, gen + 1, red, a.acc, G0 + gen + 1);
   ++gen;
   preload_w(a.wpub[0]);
@@ -649,6 +653,7 @@ __global__ void __launch_bounds__(kTiledThreads, 1) k_coarse_tiled(TiledArgs a) 
     a.iters[0] = it;
     a.iters[1] += it;
     a.ctl->base = cnt0 + gen * gridDim.x;   // every block has read base (all passed barrier 1)
+    a.ctl->gbase = G0 + gen;
   }
 }
 

@@ -1808,8 +1808,11 @@ static int setup_impl(const fcm_grid* g, const fcm_params* prm, const fcm_slab* 
   h->g = *g;
   h->prm = *prm;
   h->alpha = alpha;
-  if (const char* e = getenv("FCM_MMA_BPS")) h->mma_bps = std::max(1, atoi(e));
-  if (const char* e = getenv("FCM_LIST_BPS")) h->list_bps = std::max(1, atoi(e));
+  // blocks per SM of the two k_cell_mma populations; clamped so that one launch never has more
+  // blocks than the 2 * kMaxPartials energy partials d_partA/B/C hold (sum_partials reads them all)
+  const int bps_cap = std::max(1, (2 * kMaxPartials) / (2 * std::max(1, h->num_sms)));
+  if (const char* e = getenv("FCM_MMA_BPS")) h->mma_bps = std::min(bps_cap, std::max(1, atoi(e)));
+  if (const char* e = getenv("FCM_LIST_BPS")) h->list_bps = std::min(bps_cap, std::max(1, atoi(e)));
   if (const char* e = getenv("FCM_PDL")) h->pdl = atoi(e) > 0;
   if (slab) {
     if (slab->nranks < 1 || slab->rank < 0 || slab->rank >= slab->nranks || slab->z_begin < 0 ||
@@ -2434,10 +2437,10 @@ static int pcg_core(fcm_mg* h, double rtol, int32_t maxit, int32_t* iters, doubl
   h->stat_coarse = 0;
   CU(cudaMemsetAsync((h->hg ? h->hg : h)->d_coarse_iters, 0, 8, h->stream));
   h->stat_vcycles = 0;
-  if (!(bb > 0)) {
+  if (!(bb > 0) || maxit == 0) {   // b = 0: x = 0 (R6); maxit = 0: no x-update, x = x0 = 0
     RC(fill(h, h->f_x, 0.0, N));
     if (iters) *iters = 0;
-    return FCM_OK;
+    return bb > 0 ? FCM_NOT_CONVERGED : FCM_OK;
   }
   if (h->g_solve) {   // one graph launch, one synchronisation
     h->h_s->it = 0;

@@ -29,6 +29,26 @@ def _ptr(a):
     return a.ctypes.data_as(C.c_void_p)
 
 
+def _vecptr(t, n, device=None, name="vector"):
+    """Pointer of a caller-supplied vector after checking what the C ABI assumes (fp64,
+    contiguous, exactly n entries, on the handle's device -- or on the host when device is
+    None); a mismatch raises ValueError instead of reading or writing out of bounds."""
+    if not isinstance(t, torch.Tensor):
+        raise ValueError(f"{name}: expected a torch.Tensor, got {type(t).__name__}")
+    if t.dtype != torch.float64:
+        raise ValueError(f"{name}: dtype {t.dtype}, expected torch.float64")
+    if not t.is_contiguous():
+        raise ValueError(f"{name}: not contiguous")
+    if t.numel() != n:
+        raise ValueError(f"{name}: {t.numel()} entries, expected {n}")
+    if device is None:
+        if t.is_cuda:
+            raise ValueError(f"{name}: expected a host tensor")
+    elif t.device != device:
+        raise ValueError(f"{name}: on {t.device}, expected {device}")
+    return C.c_void_p(t.data_ptr())
+
+
 def grid_of(cfg) -> Grid:
     g = Grid()
     g.dim = cfg.dim
@@ -291,6 +311,9 @@ class Solver:
         check(_lib.lib().fcm_mg_stats(self._h, C.byref(a), C.byref(b)))
         return {"coarse_iters": a.value, "vcycles": b.value}
 
+    def _dv(self, t, q, name):
+        return _vecptr(t, self.ndofs(q), self.device, name)
+
     def _vec(self, q=None):
         return torch.zeros(self.ndofs(q), dtype=torch.float64, device=self.device)
 
@@ -306,23 +329,23 @@ class Solver:
     def apply(self, x: torch.Tensor, q=None) -> torch.Tensor:
         q = self.cfg.p if q is None else q
         y = self._vec(q)
-        check(_lib.lib().fcm_apply(self._h, q, _ptr(x), _ptr(y)))
+        check(_lib.lib().fcm_apply(self._h, q, self._dv(x, q, "x"), _ptr(y)))
         return y
 
     def smooth(self, r: torch.Tensor, x: torch.Tensor, q=None) -> torch.Tensor:
         q = self.cfg.p if q is None else q
-        check(_lib.lib().fcm_mg_smooth(self._h, q, _ptr(r), _ptr(x)))
+        check(_lib.lib().fcm_mg_smooth(self._h, q, self._dv(r, q, "r"), self._dv(x, q, "x")))
         return x
 
     def coarse_solve(self, r: torch.Tensor):
         x = self._vec(1)
         it = C.c_int32()
-        check(_lib.lib().fcm_mg_coarse_solve(self._h, _ptr(r), _ptr(x), C.byref(it)))
+        check(_lib.lib().fcm_mg_coarse_solve(self._h, self._dv(r, 1, "r"), _ptr(x), C.byref(it)))
         return x, it.value
 
     def vcycle(self, r: torch.Tensor) -> torch.Tensor:
         z = self._vec()
-        check(_lib.lib().fcm_mg_vcycle(self._h, _ptr(r), _ptr(z)))
+        check(_lib.lib().fcm_mg_vcycle(self._h, self._dv(r, None, "r"), _ptr(z)))
         return z
 
     def pcg_solve(self, b: torch.Tensor, rtol=None, maxit=None, x=None):
@@ -331,7 +354,8 @@ class Solver:
         x = self._vec() if x is None else x
         it = C.c_int32()
         hist = np.zeros(maxit + 1)
-        rc = _lib.lib().fcm_pcg_solve(self._h, _ptr(b), _ptr(x), rtol, maxit, C.byref(it), _ptr(hist))
+        rc = _lib.lib().fcm_pcg_solve(self._h, self._dv(b, None, "b"), self._dv(x, None, "x"), rtol, maxit,
+                                      C.byref(it), _ptr(hist))
         check(rc, allow_not_converged=True)
         return x, it.value, hist[: it.value + 1]
 
@@ -342,7 +366,8 @@ class Solver:
         x = self._vec() if x is None else x
         it = C.c_int32()
         hist = np.zeros(maxit + 1)
-        rc = _lib.lib().fcm_mg_solve(self._h, _ptr(b), _ptr(x), rtol, maxit, C.byref(it), _ptr(hist))
+        rc = _lib.lib().fcm_mg_solve(self._h, self._dv(b, None, "b"), self._dv(x, None, "x"), rtol, maxit,
+                                     C.byref(it), _ptr(hist))
         check(rc, allow_not_converged=True)
         return x, it.value, hist[: it.value + 1]
 
@@ -350,7 +375,9 @@ class Solver:
         rtol = self.cfg.rtol if rtol is None else rtol
         maxit = self.cfg.maxit if maxit is None else maxit
         it = C.c_int32()
-        rc = _lib.lib().fcm_pcg_solve_host(self._h, _ptr(b_host), _ptr(x_host), rtol, maxit,
+        n = self.ndofs()
+        rc = _lib.lib().fcm_pcg_solve_host(self._h, _vecptr(b_host, n, None, "b_host"),
+                                           _vecptr(x_host, n, None, "x_host"), rtol, maxit,
                                            C.byref(it), None)
         check(rc, allow_not_converged=True)
         return it.value

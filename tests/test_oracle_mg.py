@@ -258,3 +258,116 @@ def test_paper_iteration_counts_2d_elementwise(n):
         assert H.omega == GOLD["omega"]["2d_element"]
         _, it, _ = H.fcg(P.b, rtol=1e-9)
         assert abs(it - tab[str(p)][col]) <= 2, (p, it)
+
+
+# ---- the paper's own test problem (Sec. 4.1, psi = 0): penalty BC + manufactured source ----
+def _square(n, p, block="element", **kw):
+    from oracle.paper_square import SquareProblem
+    return SquareProblem(n, p, block, **kw)
+
+
+def test_square_problem_harness():
+    # the harness itself, pinned without the multigrid: with a stiff penalty
+    # the discrete solution converges spectrally to the manufactured u_bar at the vertices
+    # (a wrong source sign, kappa or penalty term would leave an O(1) error); with the paper's
+    # beta = 1e4 the boundary penalty error ~ kappa |du/dn| / beta ~ 1e-5 dominates.
+    errs = []
+    for p in (2, 3, 5):
+        P = _square(8, p, beta=1e8)
+        x = spla.spsolve(P.A.tocsc(), P.b)
+        errs.append(P.nodal_error(x))
+    assert errs[0] < 5e-6 and errs[1] < errs[0] / 5 and errs[2] < 5e-9, errs
+    P = _square(8, 3)
+    x = spla.spsolve(P.A.tocsc(), P.b)
+    assert 1e-6 < P.nodal_error(x) < 3e-5
+    # SPD with the penalty
+    assert abs(P.A - P.A.T).max() < 1e-12 * abs(P.A).max()
+
+
+@pytest.mark.parametrize("n", [8, 16])
+def test_paper_square_elementwise_cg_counts_exact(n):
+    # P11: CG + p-MG (V(5,5), elementwise AS, omega = 1/3), psi = 0, tol 1e-9: the oracle on
+    # the paper's own problem reproduces every printed count exactly.
+    tab = GOLD["cg_mg_psi0_elementwise"]
+    col = {8: 0, 16: 1}[n]
+    got = []
+    for p in (2, 3, 4, 5):
+        H = Hierarchy(_square(n, p))
+        assert H.omega == GOLD["omega"]["2d_element"]
+        _, it, _ = H.fcg(H.prob.b, rtol=GOLD["square_problem"]["tol"])
+        got.append(it)
+    assert got == [tab[str(p)][col] for p in (2, 3, 4, 5)], got
+
+
+def test_paper_square_elementwise_mg_solver_counts():
+    # multigrid as a stand-alone solver, h = 1/8: printed 12/10/17/14
+    tab = GOLD["mg_solver_psi0_elementwise"]
+    for p in (2, 3, 4, 5):
+        H = Hierarchy(_square(8, p))
+        _, it, hist = H.mg_solve(H.prob.b, rtol=1e-9, maxit=100)
+        assert abs(it - tab[str(p)][0]) <= 1, (p, it)
+        rho = np.array(hist[1:]) / np.array(hist[:-1])
+        assert rho.max() < 0.5
+
+
+def test_paper_square_patchwise_counts():
+    # Reading R19.  Table 1 fixes the patch block as every DOF whose
+    # support intersects the 2^d cells around a vertex, m = (2p+1)^d ("closure").  With those
+    # blocks the oracle needs 3 CG iterations where the paper prints 5-6: a
+    # superset of the blocks the printed counts imply.  The same patch machinery with the
+    # "interior" membership predicate (support inside the patch, m = (2p-1)^d) reproduces the
+    # printed CG counts to +-1 -- pinning the vertex enumeration, boundary clipping and
+    # assembled sub-blocks -- and the closure blocks can only be stronger (never more iterations).
+    tab = GOLD["cg_mg_psi0_patchwise"]
+    for p in (2, 3, 4, 5):
+        P = _square(8, p, "patch")
+        Hi = Hierarchy(P, patch_rule="interior")
+        assert Hi.omega == GOLD["omega"]["2d_patch"]
+        _, it_i, _ = Hi.fcg(P.b, rtol=1e-9)
+        assert abs(it_i - tab[str(p)][0]) <= 1, (p, it_i)
+        Hc = Hierarchy(P)
+        _, it_c, _ = Hc.fcg(P.b, rtol=1e-9)
+        assert it_c <= it_i <= tab[str(p)][0] + 1
+        sizes_c = {len(b) for b in Hc.levels[p].blocks}
+        sizes_i = {len(b) for b in Hi.levels[p].blocks}
+        assert max(sizes_c) == (2 * p + 1) ** 2 and (2 * p - 1) ** 2 in sizes_i
+        for bi, bc in zip(Hi.levels[p].blocks, Hc.levels[p].blocks):   # same vertex order
+            assert set(bi) <= set(bc)
+
+
+def _patch_by_keys(dof, v, q, n, d):
+    """Independent enumeration of a closure patch block from the DOF keys alone: the free
+    level-q DOFs whose entity (key coordinates X = 2*vertex or 2*cell+1 per axis) lies in the
+    closed box of the 2^d cells around vertex v (clipped to the grid)."""
+    p = dof.cfg.p
+    per = (p + 1) ** 3 * dof.cfg.n_f
+    ent = dof.keys // per
+    X = [ent % (2 * n + 1), (ent // (2 * n + 1)) % (2 * n + 1), ent // (2 * n + 1) ** 2]
+    vc = [(v // (n + 1) ** a) % (n + 1) for a in range(d)]
+    ok = dof.dof_order <= q
+    for a in range(d):
+        lo, hi = max(vc[a] - 1, 0), min(vc[a] + 1, n)
+        ok &= (X[a] >= 2 * lo) & (X[a] <= 2 * hi)
+    return np.nonzero(ok)[0]
+
+
+@pytest.mark.parametrize("dim,n,p", [(2, 4, 3), (3, 3, 2), (3, 3, 4)])
+def test_patch_membership_matches_key_enumeration(dim, n, p):
+    # every vertex (interior, face, edge, corner; strong Dirichlet on all faces) on every
+    # level: the oracle's patch block == the key-box enumeration; interior vertices have
+    # Table 1's (2q+1)^d free DOFs when no Dirichlet entity is inside the box
+    P = Problem(small_config(dim, n, p, coarse="direct", block="patch"))
+    H = Hierarchy(P)
+    for q in range(2, p + 1):
+        lv = H.levels[q]
+        blocks = {tuple(sorted(lv.idx[b])) for b in lv.blocks}
+        ref = set()
+        for v in range((n + 1) ** dim):
+            g = _patch_by_keys(P.dof, v, q, n, dim)
+            if len(g):
+                ref.add(tuple(sorted(g)))
+            vc = [(v // (n + 1) ** a) % (n + 1) for a in range(dim)]
+            if all(2 <= c <= n - 2 for c in vc):
+                assert len(g) == (2 * q + 1) ** dim
+        assert blocks == ref, q
+        assert max(len(b) for b in lv.blocks) <= (2 * q + 1) ** dim
