@@ -256,6 +256,23 @@ int fcm_pcg_solve_host(fcm_mg* h, const double* b_host, double* x_host, double r
 int fcm_mg_solve(fcm_mg* h, const double* b, double* x, double rtol, int32_t maxit,
                  int32_t* iters, double* relres_hist);
 
+/* Parity protocol (ladder L2/L4): export the additive-Schwarz block inverses
+ * A_i^{-1} = (P_i^T A_q P_i)^{-1} (Eq. AdditiveSchwarz) exactly as level q's
+ * smoother applies them, so that a reference implementation can run the same smoother and
+ * V-cycle on identical setup data.  Two-call protocol: with all buffers NULL, *n_blocks and
+ * *block_size receive the number of blocks with at least one free DOF and m_b (elementwise: the
+ * level element size; patchwise: the (2q+1)^d-slot patch).  Otherwise (host buffers):
+ *   anchors   [n_blocks]            anchor of block i (cell index, or vertex index x fastest over
+ *                                   (n+1)^d for patches), ascending -- may be NULL;
+ *   dof_index [n_blocks * m_b]      layout index (0 <= . < ndofs(q)) of block row l, -1 where the
+ *                                   slot holds no free DOF (absent or Dirichlet: identity row);
+ *   inv       [n_blocks * m_b^2]    the inverse, row-major, in the block's slot order; shared-type
+ *                                   blocks are expanded (and scaled by 1/alpha for all-fictitious
+ *                                   neighbourhoods), individual blocks unpacked.
+ * Errors: FCM_EINVAL (bad handle/level, level without a smoother), FCM_ECUDA.                */
+int fcm_mg_export_block_inverses(const fcm_mg* h, int32_t q, int64_t* n_blocks, int32_t* block_size,
+                                 int64_t* anchors, int32_t* dof_index, double* inv);
+
 /* Statistics of the last fcm_pcg_solve / fcm_mg_solve: inner coarse CG iterations, V-cycles. */
 int fcm_mg_stats(const fcm_mg* h, int64_t* coarse_iters_total, int64_t* vcycles);
 

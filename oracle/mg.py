@@ -90,6 +90,13 @@ class Level:
             for k, i in enumerate(ids):
                 self.inv[i] = inv[k]
 
+    def set_blocks(self, blocks, inverses):
+        """Replace this level's blocks and inverses by externally supplied ones (the identical-
+        setup parity protocol: the GPU exports its inverses, the oracle's
+        smoother then runs on the same setup data).  blocks: level-local index arrays."""
+        self.blocks = [np.asarray(b, dtype=np.int64) for b in blocks]
+        self.inv = [np.asarray(a, dtype=np.float64) for a in inverses]
+
     def schwarz(self, r):
         """M^{-1} r = sum_i P_i A_i^{-1} P_i^T r, accumulated serially in block order."""
         idx = np.concatenate(self.blocks)
@@ -194,12 +201,13 @@ class Hierarchy:
                 break
         return x, it, hist
 
-    def fcg(self, b, rtol=None, maxit=None, force_iters=None):
+    def fcg(self, b, rtol=None, maxit=None, force_iters=None, callback=None):
         cfg = self.prob.cfg
         rtol = cfg.rtol if rtol is None else rtol
         maxit = cfg.maxit if maxit is None else maxit
         A = self.levels[cfg.p].A
-        return fcg(lambda v: A @ v, b, self.vcycle, rtol, maxit, force_iters=force_iters)
+        return fcg(lambda v: A @ v, b, self.vcycle, rtol, maxit, force_iters=force_iters,
+                   callback=callback)
 
 
 def pcg(apply_A, b, prec, rtol, maxit, rel_to="b"):
@@ -231,9 +239,10 @@ def pcg(apply_A, b, prec, rtol, maxit, rel_to="b"):
     return x, it
 
 
-def fcg(apply_A, b, prec, rtol, maxit, force_iters=None):
+def fcg(apply_A, b, prec, rtol, maxit, force_iters=None, callback=None):
     """Flexible (Polak-Ribiere) PCG, x0 = 0 (P:351-354, R5/R6).
-    Returns (x, iterations, relative residual history [||r_k||/||b||])."""
+    Returns (x, iterations, relative residual history [||r_k||/||b||]).
+    callback(k, x_k), if given, sees every iterate (test bookkeeping only)."""
     x = np.zeros_like(b)
     nb = np.linalg.norm(b)
     if nb == 0.0:
@@ -255,6 +264,8 @@ def fcg(apply_A, b, prec, rtol, maxit, force_iters=None):
         r = r - a * q
         it += 1
         hist.append(np.linalg.norm(r) / nb)
+        if callback is not None:
+            callback(it, x)
         if force_iters is not None:
             if it >= force_iters:
                 break

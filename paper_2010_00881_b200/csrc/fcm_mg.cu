@@ -2622,3 +2622,45 @@ extern "C" int fcm_mg_block_counts(const fcm_mg* h, int32_t q, int64_t* n_indivi
   if (n_shared_types) *n_shared_types = h->lev[q].n_types;
   return FCM_OK;
 }
+
+// Parity protocol: the block inverses exactly as the smoother applies them.
+extern "C" int fcm_mg_export_block_inverses(const fcm_mg* h, int32_t q, int64_t* n_blocks, int32_t* block_size,
+                                            int64_t* anchors, int32_t* dof_index, double* inv) {
+  clear_error();
+  if (!h || q < 1 || q > h->g.p) return fail(FCM_EINVAL, "bad handle or level");
+  const LevelDev& Lv = h->lev[q];
+  if (!Lv.has_as) return fail(FCM_EINVAL, "level %d has no additive-Schwarz smoother", q);
+  if (!n_blocks || !block_size) return fail(FCM_EINVAL, "NULL count arguments");
+  const BlockGeom g = block_geom(h->L, q, Lv.patch);
+  const int mb = g.mb;
+  std::vector<int64_t> list;
+  for (int64_t A = 0; A < (int64_t)Lv.blk_h.size(); ++A)
+    if (Lv.blk_h[A] != kBlkNone) list.push_back(A);
+  *n_blocks = (int64_t)list.size();
+  *block_size = mb;
+  if (!anchors && !dof_index && !inv) return FCM_OK;
+  const size_t mm = (size_t)mb * mb;
+  std::vector<double> tmp(mm);
+  for (size_t i = 0; i < list.size(); ++i) {
+    const int64_t A = list[i];
+    if (anchors) anchors[i] = A;
+    int ac[3] = {(int)(A % g.na[0]), (int)((A / g.na[0]) % g.na[1]), (int)(A / ((int64_t)g.na[0] * g.na[1]))};
+    if (dof_index)
+      for (int l = 0; l < mb; ++l) dof_index[i * mb + l] = (int32_t)block_dof_index(h->L, q, g, l, ac);
+    if (inv) {
+      const int32_t bq = Lv.blk_h[A];
+      const double* src;
+      double scale = 1.0;
+      if (bq >= 0) {
+        src = Lv.irr_inv + (size_t)bq * mm;
+      } else {
+        const int t = -bq - 1;
+        src = Lv.type_inv + (size_t)(t & 0xfff) * mm;
+        if (t >> 12) scale = 1.0 / h->alpha;
+      }
+      CU(cudaMemcpy(tmp.data(), src, mm * sizeof(double), cudaMemcpyDeviceToHost));
+      for (size_t e = 0; e < mm; ++e) inv[i * mm + e] = tmp[e] * scale;
+    }
+  }
+  return FCM_OK;
+}

@@ -288,6 +288,20 @@ class Solver:
         check(_lib.lib().fcm_mg_block_counts(self._h, q, C.byref(n), C.byref(t)))
         return n.value, t.value
 
+    def export_block_inverses(self, q):
+        """(anchors [n], dof_index [n, m_b] (-1: no free DOF), inverses [n, m_b, m_b]) of level
+        q's Schwarz blocks exactly as the smoother applies them (fcm_mg_export_block_inverses,
+        the parity protocol of SURVEY §8(c))."""
+        L = _lib.lib()
+        n, mb = C.c_int64(), C.c_int32()
+        check(L.fcm_mg_export_block_inverses(self._h, q, C.byref(n), C.byref(mb), None, None, None))
+        anchors = np.zeros(n.value, dtype=np.int64)
+        idx = np.zeros((n.value, mb.value), dtype=np.int32)
+        inv = np.zeros((n.value, mb.value, mb.value))
+        check(L.fcm_mg_export_block_inverses(self._h, q, C.byref(n), C.byref(mb), _ptr(anchors),
+                                             _ptr(idx), _ptr(inv)))
+        return anchors, idx, inv
+
     def dof_keys(self) -> np.ndarray:
         k = np.zeros(self.ndofs(), dtype=np.int64)
         check(_lib.lib().fcm_mg_dof_keys(self._h, _ptr(k)))
