@@ -133,6 +133,16 @@ int fcm_gen_element_matrices(const fcm_grid* g, const fcm_physics* ph,
                              const int64_t* cut_cells, double* cut_K, double* cut_f,
                              double* f_traction, int32_t threads);
 
+/* The cut-cell part of fcm_gen_element_matrices on the CURRENT CUDA DEVICE:
+ * the same space-tree quadrature (reading R13) with one CTA per cut cell, box
+ * classification bit-identical to the host generator, uncut leaves in Kronecker form, depth-
+ * limit cut leaves with alpha per Gauss point.  Host in/out buffers as in
+ * fcm_gen_element_matrices (cut_K n_cut*m*m, cut_f n_cut*m, cut_f may be NULL).
+ * Poisson only, depth <= 4, m <= 128: otherwise FCM_EINVAL (use the host generator).       */
+int fcm_gen_cut_matrices_device(const fcm_grid* g, const fcm_physics* ph, int64_t n_voids,
+                                const double* centres, const double* radii, int64_t n_cut,
+                                const int64_t* cut_cells, double* cut_K, double* cut_f);
+
 /* ==== solver ============================================================================ */
 
 /* Build the hierarchy on the current CUDA device ("cached during the solver

@@ -9,7 +9,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "libfcm_mg.so")
-SOURCES = [os.path.join(HERE, "csrc", f) for f in ("fcm_mg.cu", "gen.cpp", "slab.cpp")]
+SOURCES = [os.path.join(HERE, "csrc", f) for f in ("fcm_mg.cu", "quad.cu", "gen.cpp", "slab.cpp")]
 HEADERS = sorted(os.path.join(HERE, "csrc", f) for f in os.listdir(os.path.join(HERE, "csrc"))
                  if f.endswith((".cuh", ".hpp", ".h"))) + [os.path.join(ROOT, "include", "fcm_mg.h")]
 

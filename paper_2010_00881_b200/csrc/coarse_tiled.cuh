@@ -440,6 +440,7 @@ __global__ void __launch_bounds__(kTiledThreads, 1) k_coarse_tiled(TiledArgs a) 
   // NF == 1: row lists, stencil rows first, so that warps do not diverge between the two
   // paths (the order inside a list does not change any value: rows are independent)
   __shared__ int lcnt[4];
+  __shared__ int wcnt[32][4];
   if constexpr (NF == 1) {
     if (threadIdx.x < 4) lcnt[threadIdx.x] = 0;
     __syncthreads();
@@ -460,24 +461,35 @@ __global__ void __launch_bounds__(kTiledThreads, 1) k_coarse_tiled(TiledArgs a) 
         }
         const int f = valid ? S.vf[l] : 0;
         const unsigned lt = (1u << lane) - 1u;
-        // smoother list (counter 0 = fast, 1 = general), operator list (2, 3)
+        // smoother list (counter 0 = fast, 1 = general), operator list (2, 3).  Slots are
+        // assigned in (chunk, warp, lane) order -- a deterministic row order, so each thread's
+        // dot-product partials (and the block sums) are summed in the same order every launch
+        const int wid = threadIdx.x >> 5;
+        unsigned bfw[2], bgw[2];
+        bool inw[2], fastw[2];
 #pragma unroll
         for (int w = 0; w < 2; ++w) {
-          const bool in = valid && (w == 0 || inT);
-          const bool fast = in && (f & (w == 0 ? kVfSm : kVfOp));
-          const unsigned bf = __ballot_sync(0xffffffffu, fast), bg = __ballot_sync(0xffffffffu, in && !fast);
-          if (pass == 0) {
-            if (lane == 0) { atomicAdd(&lcnt[2 * w], __popc(bf)); atomicAdd(&lcnt[2 * w + 1], __popc(bg)); }
-          } else {
-            int bfo = 0, bgo = 0;
-            if (lane == 0) { bfo = atomicAdd(&lcnt[2 * w], __popc(bf)); bgo = atomicAdd(&lcnt[2 * w + 1], __popc(bg)); }
-            bfo = __shfl_sync(0xffffffffu, bfo, 0);
-            bgo = __shfl_sync(0xffffffffu, bgo, 0);
+          inw[w] = valid && (w == 0 || inT);
+          fastw[w] = inw[w] && (f & (w == 0 ? kVfSm : kVfOp));
+          bfw[w] = __ballot_sync(0xffffffffu, fastw[w]);
+          bgw[w] = __ballot_sync(0xffffffffu, inw[w] && !fastw[w]);
+          if (lane == 0) { wcnt[wid][2 * w] = __popc(bfw[w]); wcnt[wid][2 * w + 1] = __popc(bgw[w]); }
+        }
+        __syncthreads();
+        if (pass == 1) {
+#pragma unroll
+          for (int w = 0; w < 2; ++w) {
+            int bfo = lcnt[2 * w], bgo = lcnt[2 * w + 1];
+            for (int v = 0; v < wid; ++v) { bfo += wcnt[v][2 * w]; bgo += wcnt[v][2 * w + 1]; }
             int* lst = w == 0 ? S.lsm : S.lop;
-            if (fast) lst[bfo + __popc(bf & lt)] = l | (cb << 16);
-            else if (in) lst[bgo + __popc(bg & lt)] = l | (cb << 16);
+            if (fastw[w]) lst[bfo + __popc(bfw[w] & lt)] = l | (cb << 16);
+            else if (inw[w]) lst[bgo + __popc(bgw[w] & lt)] = l | (cb << 16);
           }
         }
+        __syncthreads();
+        if (threadIdx.x < 4)
+          for (int v = 0; v < (int)(blockDim.x >> 5); ++v) lcnt[threadIdx.x] += wcnt[v][threadIdx.x];
+        __syncthreads();
       }
       __syncthreads();
       if (pass == 0) {

@@ -121,9 +121,19 @@ def classify(cfg, centres, radii):
     return kind, ncut.value
 
 
-def generate(cfg, centres=None, radii=None, threads: int = 0, cut_cells=None, kind=None) -> GenProblem:
+def device_quadrature_ok(cfg) -> bool:
+    """fcm_gen_cut_matrices_device handles this workload (Poisson, depth <= 4, m <= 128) and a
+    CUDA device is present."""
+    return (cfg.physics == "poisson" and cfg.depth <= 4 and (cfg.p + 1) ** cfg.dim <= 128
+            and torch.cuda.is_available())
+
+
+def generate(cfg, centres=None, radii=None, threads: int = 0, cut_cells=None, kind=None,
+             device=None) -> GenProblem:
     """Workload generator (fcm_gen_classify + fcm_gen_element_matrices).  cut_cells: restrict
-    the cut-cell quadrature to these cells (slab + ghost layers in multi-GPU runs)."""
+    the cut-cell quadrature to these cells (slab + ghost layers in multi-GPU runs).
+    device: cut-cell quadrature on the GPU (fcm_gen_cut_matrices_device); None = whenever
+    device_quadrature_ok(cfg)."""
     from workloads import config_voids
     if centres is None:
         centres, radii = config_voids(cfg)
@@ -143,9 +153,19 @@ def generate(cfg, centres=None, radii=None, threads: int = 0, cut_cells=None, ki
     cut_K = np.zeros((len(cut_cells), m, m))
     cut_f = np.zeros((len(cut_cells), m))
     f_tr = np.zeros(m)
-    check(L.fcm_gen_element_matrices(C.byref(g), C.byref(ph), len(radii), _ptr(centres), _ptr(radii),
-                                     _ptr(K_ref), _ptr(f_ref), len(cut_cells), _ptr(cut_cells),
-                                     _ptr(cut_K), _ptr(cut_f), _ptr(f_tr), threads))
+    if device is None:
+        device = device_quadrature_ok(cfg)
+    if device:
+        # K_ref, f_ref, f_traction on the host (one cell), the cut cells on the device
+        check(L.fcm_gen_element_matrices(C.byref(g), C.byref(ph), len(radii), _ptr(centres), _ptr(radii),
+                                         _ptr(K_ref), _ptr(f_ref), 0, None, None, None, _ptr(f_tr), threads))
+        torch.cuda.init()
+        check(L.fcm_gen_cut_matrices_device(C.byref(g), C.byref(ph), len(radii), _ptr(centres), _ptr(radii),
+                                            len(cut_cells), _ptr(cut_cells), _ptr(cut_K), _ptr(cut_f)))
+    else:
+        check(L.fcm_gen_element_matrices(C.byref(g), C.byref(ph), len(radii), _ptr(centres), _ptr(radii),
+                                         _ptr(K_ref), _ptr(f_ref), len(cut_cells), _ptr(cut_cells),
+                                         _ptr(cut_K), _ptr(cut_f), _ptr(f_tr), threads))
     return GenProblem(kind, cut_cells, K_ref, f_ref, cut_K, cut_f, f_tr)
 
 
