@@ -115,7 +115,7 @@ __global__ void __launch_bounds__(256) k_block_smooth(BlockOp op) {
   __syncthreads();
   for (int64_t A = (int64_t)blockIdx.x * wpb + w; A < op.nanchor; A += (int64_t)gridDim.x * wpb) {
     const int32_t bq = op.blk[A];
-    if (bq == kBlkNone) continue;   // warp-uniform
+    if (bq == kBlkNone || bq >= 0) continue;   // warp-uniform; individual blocks: k_patch_irr
     const int ax = (int)(A % op.na[0]), ay = (int)((A / op.na[0]) % op.na[1]);
     const int az = (int)(A / ((int64_t)op.na[0] * op.na[1]));
     for (int l = lane; l < mb; l += 32) {

@@ -32,6 +32,7 @@
 #include "coarse.cuh"
 #include "coarse_tiled.cuh"
 #include "blocks.cuh"
+#include "patch.cuh"
 #include "cellmma.cuh"
 #include "common.hpp"
 #include "layout.hpp"
@@ -54,6 +55,10 @@ using namespace fcm;
     int rc_ = (call);      \
     if (rc_ < 0) return rc_; \
   } while (0)
+
+namespace fcm {
+void ref1d_matrices(int p, double* M, double* K);   // gen.cpp
+}
 
 namespace {
 
@@ -108,6 +113,19 @@ struct LevelDev {
   int64_t nanchor = 0;
   int8_t* d_mem = nullptr;
   int16_t* d_loc = nullptr;
+  // patch levels at scale (patch.cuh): tile-packed individual inverses, regular-anchor list,
+  // fast-diagonalisation tables
+  int nt = 0;                      // 32x32 tiles per dimension of a packed inverse
+  int64_t pstride = 0;             // doubles per packed inverse
+  int64_t* irr_anchor = nullptr;   // [n_irr] anchor of individual block i
+  int32_t* reg_list = nullptr;     // regular anchors (fast diagonalisation / k_block_smooth)
+  int64_t n_reg = 0;
+  bool fd = false;
+  double* fd_tabs = nullptr;       // [3][ncls][S*S + S]
+  int* fd_cls = nullptr;           // [na0 + na1 + na2] axis class of each anchor coordinate
+  int fd_ncls = 0;
+  int16_t* fd_midx = nullptr;      // [(q+1)^3] local DOF of element mode (kx,ky,kz)
+  double fd_s = 1.0;
   // slab mode: interface planes (exchange order) and the smoother increment vector
   int32_t* lo_idx = nullptr;
   int32_t* hi_idx = nullptr;
@@ -918,26 +936,69 @@ static size_t block_smem(int m, int mb) {
   (void)m;
   return sizeof(Tab) + (size_t)(kThreads / 32) * mb * (sizeof(double) + sizeof(int));
 }
-// patchwise smoother: one warp per vertex patch (blocks.cuh)
+// patchwise smoother (patch.cuh): the individual (irregular) patches stream their tile-packed
+// inverses (k_patch_irr, forked onto the second stream) while the regular patches run by fast
+// diagonalisation (k_patch_fd) or, off the tensor-Poisson case, the dense shared-type kernel
+static size_t fd_smem(const fcm_mg* h, int q);
+static size_t irr_smem(int nt);
 static int launch_block_smooth(fcm_mg* h, int q, const double* r, double* x, double coef) {
   LevelDev& Lv = h->lev[q];
-  BlockOp op{};
-  op.nx = h->L.n[0]; op.ny = h->L.n[1]; op.nz = h->L.n[2];
-  for (int i = 0; i < 3; ++i) op.na[i] = Lv.na[i];
-  op.nanchor = Lv.nanchor;
-  op.mb = Lv.mb;
-  op.nmem = Lv.nmem;
-  for (int k = 0; k < 8; ++k)
-    for (int i = 0; i < 3; ++i) op.mo[k][i] = Lv.mo[k][i];
-  op.mem = Lv.d_mem; op.loc = Lv.d_loc;
-  op.m = Lv.m; op.base = Lv.base; op.stride = Lv.stride; op.cmin = Lv.cmin; op.cmax = Lv.cmax;
-  op.blk = Lv.blk; op.type_inv = Lv.type_inv; op.irr_inv = Lv.irr_inv; op.inv_alpha = 1.0 / h->alpha;
-  op.in = r; op.out = x; op.coef = coef;
-  const int64_t wpb = kThreads / 32;
-  const int nb = (int)std::max<int64_t>(1, std::min<int64_t>((Lv.nanchor + wpb - 1) / wpb, (int64_t)h->num_sms * 8));
-  k_block_smooth<<<nb, kThreads, block_smem(Lv.m, Lv.mb), h->stream>>>(op);
-  h->count();
-  CU(cudaGetLastError());
+  const bool fork = Lv.n_irr > 0 && Lv.n_reg > 0;
+  if (fork) {
+    CU(cudaEventRecord(h->ev_fork, h->stream));
+    CU(cudaStreamWaitEvent(h->stream2, h->ev_fork, 0));
+  }
+  if (Lv.n_irr > 0) {
+    PatchIrrOp op{};
+    op.nx = h->L.n[0]; op.ny = h->L.n[1]; op.nz = h->L.n[2];
+    for (int i = 0; i < 3; ++i) op.na[i] = Lv.na[i];
+    op.mb = Lv.mb; op.nt = Lv.nt; op.stride = Lv.pstride; op.n_irr = Lv.n_irr;
+    op.anchors = Lv.irr_anchor; op.mem = Lv.d_mem; op.loc = Lv.d_loc;
+    for (int k = 0; k < 8; ++k)
+      for (int i = 0; i < 3; ++i) op.mo[k][i] = Lv.mo[k][i];
+    op.base = Lv.base; op.stride3 = Lv.stride; op.cmin = Lv.cmin; op.cmax = Lv.cmax; op.m = Lv.m;
+    op.inv = Lv.irr_inv; op.in = r; op.out = x; op.coef = coef;
+    const int nb = (int)std::min<int64_t>(Lv.n_irr, h->num_sms);
+    k_patch_irr<<<nb, kIrrWarps * 32, irr_smem(Lv.nt), fork ? h->stream2 : h->stream>>>(op);
+    h->count();
+    CU(cudaGetLastError());
+  }
+  if (Lv.n_reg > 0) {
+    if (Lv.fd) {
+      PatchFdOp op{};
+      op.nx = h->L.n[0]; op.ny = h->L.n[1]; op.nz = h->L.n[2]; op.dim = h->L.dim;
+      for (int i = 0; i < 3; ++i) op.na[i] = Lv.na[i];
+      op.q = q; op.S = 2 * q + 1; op.nreg = Lv.n_reg; op.anchors = Lv.reg_list; op.blk = Lv.blk;
+      op.cls = Lv.fd_cls; op.tabs = Lv.fd_tabs; op.ncls = Lv.fd_ncls; op.s_fac = Lv.fd_s;
+      op.inv_alpha = 1.0 / h->alpha; op.modeidx = Lv.fd_midx;
+      op.base = Lv.base; op.stride3 = Lv.stride; op.cmin = Lv.cmin; op.cmax = Lv.cmax; op.m = Lv.m;
+      op.in = r; op.out = x; op.coef = coef;
+      const int nb = (int)std::max<int64_t>(1, std::min<int64_t>((Lv.n_reg + kFdWarps - 1) / kFdWarps, (int64_t)h->num_sms * 2));
+      k_patch_fd<<<nb, kFdWarps * 32, fd_smem(h, q), h->stream>>>(op);
+    } else {
+      BlockOp op{};
+      op.nx = h->L.n[0]; op.ny = h->L.n[1]; op.nz = h->L.n[2];
+      for (int i = 0; i < 3; ++i) op.na[i] = Lv.na[i];
+      op.nanchor = Lv.nanchor;
+      op.mb = Lv.mb;
+      op.nmem = Lv.nmem;
+      for (int k = 0; k < 8; ++k)
+        for (int i = 0; i < 3; ++i) op.mo[k][i] = Lv.mo[k][i];
+      op.mem = Lv.d_mem; op.loc = Lv.d_loc;
+      op.m = Lv.m; op.base = Lv.base; op.stride = Lv.stride; op.cmin = Lv.cmin; op.cmax = Lv.cmax;
+      op.blk = Lv.blk; op.type_inv = Lv.type_inv; op.irr_inv = nullptr; op.inv_alpha = 1.0 / h->alpha;
+      op.in = r; op.out = x; op.coef = coef;
+      const int64_t wpb = kThreads / 32;
+      const int nb = (int)std::max<int64_t>(1, std::min<int64_t>((Lv.nanchor + wpb - 1) / wpb, (int64_t)h->num_sms * 8));
+      k_block_smooth<<<nb, kThreads, block_smem(Lv.m, Lv.mb), h->stream>>>(op);
+    }
+    h->count();
+    CU(cudaGetLastError());
+  }
+  if (fork) {
+    CU(cudaEventRecord(h->ev_join, h->stream2));
+    CU(cudaStreamWaitEvent(h->stream, h->ev_join, 0));
+  }
   return FCM_OK;
 }
 
@@ -1241,6 +1302,326 @@ static int32_t mma_pack(const fcm_mg* h, int q, int64_t c, bool scaled) {
                    (scaled ? kMmaScaled : 0u));
 }
 
+
+// ---- patch levels at scale (patch.cuh) -----------------------------------------------------
+// Generalised symmetric eigenproblem K S = M S Lambda, S^T M S = I, for n <= 9 (host, fp64):
+// M = L L^T, C = L^-1 K L^-T, cyclic Jacobi C = Q Lambda Q^T, S = L^-T Q.
+static bool gen_eig(int n, const std::vector<double>& K, const std::vector<double>& M, std::vector<double>& S,
+                    std::vector<double>& lam) {
+  std::vector<double> Lc(n * n, 0.0), C(n * n), Q(n * n, 0.0), T(n * n);
+  for (int j = 0; j < n; ++j) {
+    double d = M[j * n + j];
+    for (int k = 0; k < j; ++k) d -= Lc[j * n + k] * Lc[j * n + k];
+    if (!(d > 0)) return false;
+    Lc[j * n + j] = std::sqrt(d);
+    for (int i = j + 1; i < n; ++i) {
+      double v = M[i * n + j];
+      for (int k = 0; k < j; ++k) v -= Lc[i * n + k] * Lc[j * n + k];
+      Lc[i * n + j] = v / Lc[j * n + j];
+    }
+  }
+  // T = L^-1 K (forward substitution per column), C = T L^-T (= L^-1 T^T)^T
+  for (int c = 0; c < n; ++c)
+    for (int i = 0; i < n; ++i) {
+      double v = K[i * n + c];
+      for (int k = 0; k < i; ++k) v -= Lc[i * n + k] * T[k * n + c];
+      T[i * n + c] = v / Lc[i * n + i];
+    }
+  for (int r = 0; r < n; ++r)   // C[r][:] = L^-1 (T[r][:])^T
+    for (int i = 0; i < n; ++i) {
+      double v = T[r * n + i];
+      for (int k = 0; k < i; ++k) v -= Lc[i * n + k] * C[r * n + k];
+      C[r * n + i] = v / Lc[i * n + i];
+    }
+  for (int i = 0; i < n; ++i) {
+    for (int j = 0; j < i; ++j) C[i * n + j] = C[j * n + i] = 0.5 * (C[i * n + j] + C[j * n + i]);
+    Q[i * n + i] = 1.0;
+  }
+  for (int sweep = 0; sweep < 100; ++sweep) {
+    double off = 0.0, tot = 0.0;
+    for (int i = 0; i < n; ++i)
+      for (int j = 0; j < n; ++j) (i == j ? tot : off) += C[i * n + j] * C[i * n + j];
+    if (off <= 1e-30 * (tot + off)) break;
+    for (int p = 0; p < n; ++p)
+      for (int r = p + 1; r < n; ++r) {
+        const double apr = C[p * n + r];
+        if (apr == 0.0) continue;
+        const double th = (C[r * n + r] - C[p * n + p]) / (2.0 * apr);
+        const double t = (th >= 0 ? 1.0 : -1.0) / (std::fabs(th) + std::sqrt(th * th + 1.0));
+        const double c = 1.0 / std::sqrt(t * t + 1.0), sn = t * c;
+        for (int k = 0; k < n; ++k) {   // columns p, r
+          const double ckp = C[k * n + p], ckr = C[k * n + r];
+          C[k * n + p] = c * ckp - sn * ckr;
+          C[k * n + r] = sn * ckp + c * ckr;
+        }
+        for (int k = 0; k < n; ++k) {   // rows p, r
+          const double cpk = C[p * n + k], crk = C[r * n + k];
+          C[p * n + k] = c * cpk - sn * crk;
+          C[r * n + k] = sn * cpk + c * crk;
+        }
+        for (int k = 0; k < n; ++k) {
+          const double qkp = Q[k * n + p], qkr = Q[k * n + r];
+          Q[k * n + p] = c * qkp - sn * qkr;
+          Q[k * n + r] = sn * qkp + c * qkr;
+        }
+      }
+  }
+  lam.assign(n, 0.0);
+  for (int i = 0; i < n; ++i) lam[i] = C[i * n + i];
+  S.assign(n * n, 0.0);   // S = L^-T Q: back substitution per column
+  for (int c = 0; c < n; ++c)
+    for (int i = n - 1; i >= 0; --i) {
+      double v = Q[i * n + c];
+      for (int k = i + 1; k < n; ++k) v -= Lc[k * n + i] * S[k * n + c];
+      S[i * n + c] = v / Lc[i * n + i];
+    }
+  return true;
+}
+
+// Fast-diagonalisation tables of a tensor Poisson patch level (patch.cuh k_patch_fd): valid
+// when K_ref is the Kronecker form s (K (x) M (x) M + ...) of the 1D reference matrices
+// (checked to 1e-12); per axis and per axis class (clipped distances of the vertex to the two
+// faces, R = 2 as in the type key) the assembled 1D matrices over the present patch slots.
+static int setup_patch_fd(fcm_mg* h, int q, const double* K_ref_host) {
+  const Layout& L = h->L;
+  LevelDev& Lv = h->lev[q];
+  if (h->g.space != 0 || h->g.n_f != 1 || h->multi || q > 4) return FCM_OK;
+  const int dim = L.dim, p = L.p, P1 = p + 1, S = 2 * q + 1;
+  std::vector<double> M1(P1 * P1), K1(P1 * P1);
+  ref1d_matrices(p, M1.data(), K1.data());
+  const double sfac = std::pow(0.5 * h->g.h, dim - 2);
+  // check K_ref against the Kronecker form
+  double mx = 0.0, err = 0.0;
+  const int m = L.m;
+  for (int I = 0; I < m; ++I)
+    for (int J = 0; J < m; ++J) {
+      double sum = 0.0;
+      for (int gd = 0; gd < dim; ++gd) {
+        double t = 1.0;
+        for (int a = 0; a < dim; ++a)
+          t *= (a == gd ? K1 : M1)[L.modes[I].k[a] * P1 + L.modes[J].k[a]];
+        sum += t;
+      }
+      const double kr = K_ref_host[(size_t)I * m + J];
+      mx = std::max(mx, std::fabs(kr));
+      err = std::max(err, std::fabs(kr - sfac * sum));
+    }
+  if (!(err <= 1e-12 * mx)) return FCM_OK;   // not Kronecker: dense k_block_smooth path
+  const int R = 2, ncls = (R + 1) * (R + 1) + 1;
+  const int tsz = S * S + S;
+  std::vector<double> tabs((size_t)3 * ncls * tsz, 0.0);
+  std::vector<int> cls;
+  std::vector<int16_t> midx((q + 1) * (q + 1) * (q + 1), -1);
+  for (int a = 0; a < L.m_level[q]; ++a) {
+    const int* k = L.modes[a].k;
+    midx[(k[2] * (q + 1) + k[1]) * (q + 1) + k[0]] = (int16_t)a;
+  }
+  for (int ax = 0; ax < 3; ++ax) {
+    const int n = L.n[ax];
+    const int na = ax < dim ? n + 1 : 1;
+    std::vector<char> done(ncls, 0);
+    for (int v = 0; v < na; ++v) {
+      if (ax >= dim) { cls.push_back(0); continue; }
+      const int lo = std::min(v, R), hi = std::min(n - v, R);
+      const int ci = (lo == R && hi == R) ? 0 : 1 + lo * (R + 1) + hi;
+      cls.push_back(ci);
+      if (done[ci]) continue;
+      done[ci] = 1;
+      // slots present, assembled 1D matrices over the slots
+      const bool dlo = (L.dmask >> (2 * ax)) & 1, dhi = (L.dmask >> (2 * ax + 1)) & 1;
+      auto vslot_ok = [&](int P) { return P >= 0 && P <= n && !(P == 0 && dlo) && !(P == n && dhi); };
+      std::vector<char> pres(S, 0);
+      pres[0] = vslot_ok(v - 1);
+      pres[q] = vslot_ok(v);
+      pres[2 * q] = vslot_ok(v + 1);
+      for (int s2 = 1; s2 < q; ++s2) pres[s2] = (v - 1 >= 0 && v - 1 < n);
+      for (int s2 = q + 1; s2 < 2 * q; ++s2) pres[s2] = (v < n);
+      auto slot_of = [&](int c, int k) -> int {   // cell c, 1D mode k -> patch slot or -1
+        if (k >= 2) {
+          if (k > q) return -1;
+          if (c == v - 1) return k - 1;
+          if (c == v) return q + k - 1;
+          return -1;
+        }
+        const int P = c + k;
+        if (P == v - 1) return 0;
+        if (P == v) return q;
+        if (P == v + 1) return 2 * q;
+        return -1;
+      };
+      std::vector<double> Ka(S * S, 0.0), Ma(S * S, 0.0);
+      for (int c = v - 2; c <= v + 1; ++c) {
+        if (c < 0 || c >= n) continue;
+        for (int i = 0; i <= q; ++i)
+          for (int j = 0; j <= q; ++j) {
+            const int si = slot_of(c, i), sj = slot_of(c, j);
+            if (si < 0 || sj < 0 || !pres[si] || !pres[sj]) continue;
+            Ka[si * S + sj] += K1[i * P1 + j];
+            Ma[si * S + sj] += M1[i * P1 + j];
+          }
+      }
+      std::vector<int> ps;
+      for (int s2 = 0; s2 < S; ++s2) if (pres[s2]) ps.push_back(s2);
+      const int nq = (int)ps.size();
+      std::vector<double> Kc(nq * nq), Mc(nq * nq), Sv, lam;
+      for (int i = 0; i < nq; ++i)
+        for (int j = 0; j < nq; ++j) { Kc[i * nq + j] = Ka[ps[i] * S + ps[j]]; Mc[i * nq + j] = Ma[ps[i] * S + ps[j]]; }
+      if (!gen_eig(nq, Kc, Mc, Sv, lam)) return FCM_OK;
+      double* t = tabs.data() + ((size_t)ax * ncls + ci) * tsz;
+      for (int i = 0; i < nq; ++i)
+        for (int j = 0; j < nq; ++j) t[ps[i] * S + j] = Sv[i * nq + j];
+      for (int j = 0; j < S; ++j) t[S * S + j] = j < nq ? lam[j] : 1.0;
+    }
+  }
+  RC(h->alloc(&Lv.fd_tabs, tabs.size()));
+  RC(h->alloc(&Lv.fd_cls, cls.size()));
+  RC(h->alloc(&Lv.fd_midx, midx.size()));
+  CU(cudaMemcpyAsync(Lv.fd_tabs, tabs.data(), tabs.size() * 8, cudaMemcpyHostToDevice, h->stream));
+  CU(cudaMemcpyAsync(Lv.fd_cls, cls.data(), cls.size() * 4, cudaMemcpyHostToDevice, h->stream));
+  CU(cudaMemcpyAsync(Lv.fd_midx, midx.data(), midx.size() * 2, cudaMemcpyHostToDevice, h->stream));
+  CU(cudaStreamSynchronize(h->stream));
+  Lv.fd_ncls = ncls;
+  Lv.fd_s = sfac;
+  Lv.fd = !(getenv("FCM_PATCH_FD") && atoi(getenv("FCM_PATCH_FD")) == 0);
+  return FCM_OK;
+}
+
+static size_t fd_smem(const fcm_mg* h, int q) {
+  const int S = 2 * q + 1, S3 = h->L.dim == 3 ? S * S * S : S * S, nmi = (q + 1) * (q + 1) * (q + 1);
+  return sizeof(Tab) + (size_t)3 * h->lev[q].fd_ncls * (S * S + S) * 8 + ((nmi * 2 + 15) / 16) * 16 +
+         (size_t)kFdWarps * (2 * S3 + (S3 + 1) / 2) * 8;
+}
+static size_t irr_smem(int nt) {
+  const size_t MPd = 32 * (size_t)nt;
+  return (MPd * 20 + 127) / 128 * 128 + (size_t)kIrrWarps * kIrrStages * 1024 * 8 +
+         (size_t)kIrrWarps * kIrrStages * 8 + sizeof(Tab);
+}
+
+// Assemble and invert the patch blocks of level q: shared types (full storage, type_inv) and
+// individual blocks (tile-packed, irr_inv), through a chunked workspace: k_patch_asm (cell
+// loop) -> batched blocked Gauss-Jordan -> copy (types) / k_pack_tiles (individual).
+static int setup_patch_blocks(fcm_mg* h, int q, const BlockGeom& g, const std::vector<int32_t>& blk,
+                              const std::vector<int64_t>& blocks, int64_t ntypes, const std::vector<int8_t>& dir) {
+  const Layout& L = h->L;
+  LevelDev& Lv = h->lev[q];
+  if (h->multi) return fail(FCM_EINVAL, "patchwise blocks are single-GPU (level %d)", q);
+  const int dim = L.dim, mb = g.mb, mq = L.m_level[q];
+  const int nt = (mb + 31) / 32, MP = 32 * nt;
+  const int64_t nblk = (int64_t)blocks.size(), n_irr = nblk - ntypes;
+  const int nas = (int)(g.amap.size() / mb);
+  std::vector<int16_t> alist((size_t)nas * mq, -1);
+  for (int d = 0; d < nas; ++d)
+    for (int l = 0; l < mb; ++l) {
+      const int a = g.amap[(size_t)d * mb + l];
+      if (a >= 0) alist[(size_t)d * mq + a] = (int16_t)l;
+    }
+  Lv.nt = nt;
+  Lv.pstride = tile_pack_size(nt);
+  RC(h->alloc(&Lv.type_inv, std::max<int64_t>(ntypes, 1) * mb * mb));
+  RC(h->alloc(&Lv.irr_inv, std::max<int64_t>(n_irr, 1) * Lv.pstride));
+  RC(h->alloc(&Lv.blk, blk.size()));
+  RC(h->alloc(&Lv.irr_anchor, std::max<int64_t>(n_irr, 1)));
+  CU(cudaMemcpyAsync(Lv.blk, blk.data(), blk.size() * 4, cudaMemcpyHostToDevice, h->stream));
+  if (n_irr > 0)
+    CU(cudaMemcpyAsync(Lv.irr_anchor, blocks.data() + ntypes, n_irr * 8, cudaMemcpyHostToDevice, h->stream));
+  // workspace chunk: up to 4 GiB and a quarter of the free memory
+  size_t fr = 0, tot = 0;
+  CU(cudaMemGetInfo(&fr, &tot));
+  const size_t per = (size_t)MP * MP * 8 + (size_t)mb + 16;
+  int64_t chunk = (int64_t)std::max<size_t>(1, std::min<size_t>((size_t)4 << 30, fr / 4) / per);
+  chunk = std::min<int64_t>(chunk, std::max<int64_t>(nblk, 1));
+  double* W = nullptr;
+  int64_t* d_anc = nullptr;
+  int8_t* d_dir = nullptr;
+  int16_t* d_alist = nullptr;
+  int* d_status = nullptr;
+  CU(cudaMallocAsync((void**)&W, (size_t)chunk * MP * MP * 8, h->stream));
+  CU(cudaMallocAsync((void**)&d_anc, (size_t)chunk * 8, h->stream));
+  CU(cudaMallocAsync((void**)&d_dir, (size_t)chunk * mb, h->stream));
+  CU(cudaMallocAsync((void**)&d_alist, alist.size() * 2, h->stream));
+  CU(cudaMallocAsync((void**)&d_status, (size_t)chunk * 4, h->stream));
+  CU(cudaMemcpyAsync(d_alist, alist.data(), alist.size() * 2, cudaMemcpyHostToDevice, h->stream));
+  std::vector<int> status(chunk);
+  int rc = FCM_OK;
+  for (int64_t c0 = 0; c0 < nblk && rc == FCM_OK; ) {
+    // types and individual blocks are never mixed in one chunk (different assembly)
+    const bool types = c0 < ntypes;
+    const int64_t nc = std::min<int64_t>(chunk, (types ? ntypes : nblk) - c0);
+    CU(cudaMemcpyAsync(d_anc, blocks.data() + c0, nc * 8, cudaMemcpyHostToDevice, h->stream));
+    CU(cudaMemcpyAsync(d_dir, dir.data() + (size_t)c0 * mb, (size_t)nc * mb, cudaMemcpyHostToDevice, h->stream));
+    CU(cudaMemsetAsync(W, 0, (size_t)nc * MP * MP * 8, h->stream));
+    CU(cudaMemsetAsync(d_status, 0, (size_t)nc * 4, h->stream));
+    PatchAsmArgs aa{};
+    aa.dim = dim; aa.mb = mb; aa.MP = MP; aa.ldK = L.m;
+    aa.nx = L.n[0]; aa.ny = L.n[1]; aa.nz = L.n[2];
+    for (int i = 0; i < 3; ++i) aa.na[i] = g.na[i];
+    aa.nasm = g.nasm; aa.aoff = g.aoff;
+    aa.anchors = d_anc; aa.alist = d_alist; aa.mq = mq; aa.dirich = d_dir;
+    aa.kind = types ? nullptr : h->d_kind; aa.cut_idx = h->d_cut_idx;
+    aa.Kref = h->d_Kref; aa.cutK = h->d_cutK; aa.alpha = h->alpha; aa.W = W;
+    k_patch_asm<<<(unsigned)nc, 256, 0, h->stream>>>(aa);
+    CU(cudaGetLastError());
+    const int nt64 = (MP + 63) / 64;
+    for (int k = 0; k < nt; ++k) {
+      k_gj_pivot<<<(unsigned)nc, 256, 0, h->stream>>>(W, MP, k, d_status);
+      if (nt > 1) {
+        k_gj_row<<<dim3(nt - 1, (unsigned)nc), 256, 0, h->stream>>>(W, MP, k);
+        k_gj_update<<<dim3(nt64 * nt64, (unsigned)nc), 256, 0, h->stream>>>(W, MP, k);
+        k_gj_col<<<dim3(nt - 1, (unsigned)nc), 256, 0, h->stream>>>(W, MP, k);
+      }
+    }
+    CU(cudaGetLastError());
+    if (types) {
+      if (MP == mb)
+        CU(cudaMemcpyAsync(Lv.type_inv + (size_t)c0 * mb * mb, W, (size_t)nc * mb * mb * 8, cudaMemcpyDeviceToDevice,
+                           h->stream));
+      else   // one 2D copy per block (rows MP apart in the workspace)
+        for (int64_t b = 0; b < nc; ++b)
+          CU(cudaMemcpy2DAsync(Lv.type_inv + (size_t)(c0 + b) * mb * mb, (size_t)mb * 8, W + (size_t)b * MP * MP,
+                               (size_t)MP * 8, (size_t)mb * 8, (size_t)mb, cudaMemcpyDeviceToDevice, h->stream));
+    } else {
+      k_pack_tiles<<<dim3(nt * (nt + 1) / 2, (unsigned)nc), 256, 0, h->stream>>>(
+          W, MP, nt, Lv.irr_inv + (size_t)(c0 - ntypes) * Lv.pstride, Lv.pstride);
+      CU(cudaGetLastError());
+    }
+    CU(cudaMemcpyAsync(status.data(), d_status, nc * 4, cudaMemcpyDeviceToHost, h->stream));
+    CU(cudaStreamSynchronize(h->stream));
+    for (int64_t b = 0; b < nc; ++b)
+      if (status[b]) {
+        rc = fail(FCM_ESINGULAR, "singular Schwarz block on level q=%d: %s patch block at anchor %lld", q,
+                  types ? "shared-type" : "individual", (long long)blocks[c0 + b]);
+        break;
+      }
+    c0 += nc;
+  }
+  for (void* ptr : {(void*)W, (void*)d_anc, (void*)d_dir, (void*)d_alist, (void*)d_status}) cudaFreeAsync(ptr, h->stream);
+  CU(cudaStreamSynchronize(h->stream));
+  if (rc != FCM_OK) return rc;
+  Lv.n_irr = n_irr;
+  std::vector<int32_t> reg;
+  for (int64_t A = 0; A < (int64_t)blk.size(); ++A)
+    if (blk[A] < 0 && blk[A] != kBlkNone) reg.push_back((int32_t)A);
+  Lv.n_reg = (int64_t)reg.size();
+  RC(h->alloc(&Lv.reg_list, std::max<size_t>(reg.size(), 1)));
+  if (!reg.empty()) CU(cudaMemcpyAsync(Lv.reg_list, reg.data(), reg.size() * 4, cudaMemcpyHostToDevice, h->stream));
+  RC(h->alloc(&Lv.d_mem, mb));
+  RC(h->alloc(&Lv.d_loc, mb));
+  CU(cudaMemcpyAsync(Lv.d_mem, g.mem.data(), mb, cudaMemcpyHostToDevice, h->stream));
+  CU(cudaMemcpyAsync(Lv.d_loc, g.loc.data(), mb * 2, cudaMemcpyHostToDevice, h->stream));
+  Lv.patch = true;
+  Lv.mb = mb;
+  Lv.nmem = g.nmem;
+  for (int k = 0; k < 8; ++k)
+    for (int i = 0; i < 3; ++i) Lv.mo[k][i] = g.mo[k][i];
+  for (int i = 0; i < 3; ++i) Lv.na[i] = g.na[i];
+  Lv.nanchor = (int64_t)blk.size();
+  Lv.has_as = true;
+  Lv.n_types = (int32_t)ntypes;
+  Lv.blk_h = blk;
+  CU(cudaStreamSynchronize(h->stream));
+  return FCM_OK;
+}
+
 static int setup_schwarz(fcm_mg* h, int q, const std::vector<uint8_t>& kind,
                          const std::vector<int32_t>& cut_idx) {
   const Layout& L = h->L;
@@ -1322,6 +1703,7 @@ static int setup_schwarz(fcm_mg* h, int q, const std::vector<uint8_t>& kind,
     int ac[3] = {(int)(A % g.na[0]), (int)((A / g.na[0]) % g.na[1]), (int)(A / ((int64_t)g.na[0] * g.na[1]))};
     for (int l = 0; l < mb; ++l) dir[(size_t)b * mb + l] = block_dof_index(L, q, g, l, ac) < 0;
   }
+  if (patch) return setup_patch_blocks(h, q, g, blk, blocks, ntypes, dir);
   // device buffers
   int64_t* d_anchors;
   uint8_t* d_virt;
@@ -1978,8 +2360,10 @@ static int setup_impl(const fcm_grid* g, const fcm_params* prm, const fcm_slab* 
       RC(setup_schwarz(h.get(), q, kind, cut_idx));
   for (int q = 2; q <= g->p; ++q)
     if (h->lev[q].patch) {
-      const size_t sm = block_smem(h->lev[q].m, h->lev[q].mb);
-      RC(allow_smem((const void*)k_block_smooth, sm));
+      RC(setup_patch_fd(h.get(), q, K_ref));
+      if (h->lev[q].fd) RC(allow_smem((const void*)k_patch_fd, fd_smem(h.get(), q)));
+      else RC(allow_smem((const void*)k_block_smooth, block_smem(h->lev[q].m, h->lev[q].mb)));
+      RC(allow_smem((const void*)k_patch_irr, irr_smem(h->lev[q].nt)));
     }
   RC(h->alloc(&h->d_coarse_iters, 2));
   CU(cudaMemsetAsync(h->d_coarse_iters, 0, 8, h->stream));
@@ -2651,6 +3035,18 @@ extern "C" int fcm_mg_export_block_inverses(const fcm_mg* h, int32_t q, int64_t*
       const int32_t bq = Lv.blk_h[A];
       const double* src;
       double scale = 1.0;
+      if (bq >= 0 && Lv.patch) {   // tile-packed lower triangle (patch.cuh)
+        std::vector<double> pk(Lv.pstride);
+        CU(cudaMemcpy(pk.data(), Lv.irr_inv + (size_t)bq * Lv.pstride, Lv.pstride * 8, cudaMemcpyDeviceToHost));
+        for (int r = 0; r < mb; ++r)
+          for (int c = 0; c <= r; ++c) {
+            const int I = r / 32, J = c / 32, rr = r % 32, cc = c % 32;
+            const double v = I != J ? pk[tile_off(I, J) + rr * 32 + cc] : pk[tile_off(I, I) + rr * (rr + 1) / 2 + cc];
+            inv[i * mm + (size_t)r * mb + c] = v;
+            inv[i * mm + (size_t)c * mb + r] = v;
+          }
+        continue;
+      }
       if (bq >= 0) {
         src = Lv.irr_inv + (size_t)bq * mm;
       } else {

@@ -67,6 +67,26 @@ static void modes1d(int p, double xi, double* v, double* d) {
   }
 }
 
+// 1D reference matrices on [-1, 1] of modes 0..p (row-major (p+1)^2): M_ij = int N_i N_j,
+// K_ij = int N_i' N_j' (p+1-point Gauss: exact for degree 2p).  Used by the patch smoother's
+// fast-diagonalisation setup (fcm_mg.cu), which checks K_ref against their Kronecker form.
+void ref1d_matrices(int p, double* M, double* K) {
+  std::vector<double> x, w;
+  gauss_legendre(p + 1, x, w);
+  const int P1 = p + 1;
+  std::fill(M, M + P1 * P1, 0.0);
+  std::fill(K, K + P1 * P1, 0.0);
+  double v[kMaxP + 1], d[kMaxP + 1];
+  for (int g = 0; g < P1; ++g) {
+    modes1d(p, x[g], v, d);
+    for (int i = 0; i < P1; ++i)
+      for (int j = 0; j < P1; ++j) {
+        M[i * P1 + j] += w[g] * v[i] * v[j];
+        K[i * P1 + j] += w[g] * d[i] * d[j];
+      }
+  }
+}
+
 struct Voids {
   int dim;
   int64_t nv;

@@ -1,0 +1,536 @@
+// patch.cuh -- patchwise additive Schwarz at scale (config 3: PAPER.md:259 patchwise blocks,
+// Table 1 P:316-320 m_max = (2p+1)^d, Eq. AdditiveSchwarz, block inversion P:326).
+//
+//  * INDIVIDUAL (irregular) patch inverses are stored TILE-PACKED SYMMETRIC: the lower triangle
+//    of 32x32 tiles, row-major over tile rows; off-diagonal tiles full (1024 doubles, row-major),
+//    diagonal tiles as packed lower triangles (528 doubles).  729-slot patches: 271,216 doubles
+//    (+1.9 % over m(m+1)/2).  k_patch_irr streams them with 1D bulk copies (cp.async.bulk into a
+//    per-warp ring of shared-memory stages, mbarrier completion): per tile a warp reads the 32
+//    rows (lane = column), accumulates the transposed product in a register and the row
+//    product with one butterfly reduce-scatter (31 shuffles per tile).
+//  * REGULAR patches (every cell of the 4^d neighbourhood uncut and of one kind) of a tensor
+//    Poisson level are applied by FAST DIAGONALISATION: A_i = s sum_g (x)_a (K|M)_a restricted
+//    to the patch's per-axis slot sets, so A_i^{-1} = (S_z x S_y x S_x) D^{-1} (...)^T with the
+//    1D generalised eigenvectors S_a^T M_a S_a = I, S_a^T K_a S_a = Lambda_a (setup, host) --
+//    6 one-axis contractions of (2q+1)^3 values instead of a (2q+1)^3-square GEMV.
+//  * SETUP: batched cell-loop assembly of A_i into a full workspace (ld = MP, multiple of 32),
+//    batched blocked Gauss-Jordan inversion (32-wide pivot blocks; the trailing rank-32 update is
+//    a batched register-blocked DFMA GEMM), then packing into tiles (symmetrised).
+#pragma once
+#include <cstdint>
+
+#include "cellop.cuh"
+
+namespace fcm {
+
+constexpr int kTileDiag = 528;    // 32*33/2
+constexpr int kIrrWarps = 8;      // warps per CTA of k_patch_irr
+constexpr int kIrrStages = 3;     // ring depth per warp
+constexpr int kFdWarps = 8;       // warps per CTA of k_patch_fd
+constexpr int kFdMaxS = 9;        // 2q+1 <= 9 (q <= 4)
+
+__host__ __device__ constexpr int64_t tile_pack_size(int nt) {
+  return (int64_t)nt * (nt - 1) / 2 * 1024 + (int64_t)nt * kTileDiag;
+}
+__host__ __device__ inline int64_t tile_off(int I, int J) {   // J <= I
+  return (int64_t)I * (I - 1) / 2 * 1024 + (int64_t)I * kTileDiag + (int64_t)J * 1024;
+}
+
+// ---- setup: cell-loop assembly --------------------------------------------------------------
+struct PatchAsmArgs {
+  int dim, mb, MP, ldK;
+  int nx, ny, nz;
+  int na[3];
+  int nasm, aoff;
+  const int64_t* anchors;     // [nblocks]
+  const int16_t* alist;       // [nas][mq] compact (slot) per assembly cell: slot of local DOF a, -1
+  int mq;
+  const int8_t* dirich;       // [nblocks][mb]
+  const uint8_t* kind;        // owned cells (single GPU); nullptr: every cell uncut physical (type blocks)
+  const int32_t* cut_idx;
+  const double* Kref;
+  const double* cutK;
+  double alpha;
+  double* W;                  // [nblocks][MP][MP], zeroed
+};
+
+__global__ void __launch_bounds__(256) k_patch_asm(PatchAsmArgs a) {
+  const int64_t blk = blockIdx.x;
+  const int64_t A = a.anchors[blk];
+  const int ax = (int)(A % a.na[0]), ay = (int)((A / a.na[0]) % a.na[1]), az = (int)(A / ((int64_t)a.na[0] * a.na[1]));
+  double* W = a.W + blk * (int64_t)a.MP * a.MP;
+  const int8_t* dir = a.dirich + blk * a.mb;
+  const int ncz = a.dim == 3 ? a.nasm : 1, ncy = a.dim >= 2 ? a.nasm : 1;
+  const int nas = a.nasm * ncy * ncz;
+  const int mq = a.mq;
+  for (int d = 0; d < nas; ++d) {
+    const int cx = ax + a.aoff + d % a.nasm;
+    const int cy = a.dim >= 2 ? ay + a.aoff + (d / a.nasm) % a.nasm : 0;
+    const int cz = a.dim == 3 ? az + a.aoff + d / (a.nasm * a.nasm) : 0;
+    if (cx < 0 || cy < 0 || cz < 0 || cx >= a.nx || cy >= a.ny || cz >= a.nz) continue;   // uniform
+    const int64_t c = ((int64_t)cz * a.ny + cy) * a.nx + cx;
+    const uint8_t k = a.kind ? a.kind[c] : 0;
+    const double* K = k == 2 ? a.cutK + (int64_t)a.cut_idx[c] * a.ldK * a.ldK : a.Kref;
+    const double s = k == 1 ? a.alpha : 1.0;
+    const int16_t* sl = a.alist + (int64_t)d * mq;
+    for (int e = threadIdx.x; e < mq * mq; e += blockDim.x) {
+      const int ia = e / mq, ib = e % mq;
+      const int li = sl[ia], lj = sl[ib];
+      if (li < 0 || lj < 0 || dir[li] || dir[lj]) continue;
+      W[(int64_t)li * a.MP + lj] += s * K[(int64_t)ia * a.ldK + ib];
+    }
+    __syncthreads();   // next cell may hit the same entries
+  }
+  // identity rows for absent / Dirichlet slots and the padding
+  for (int l = threadIdx.x; l < a.MP; l += blockDim.x)
+    if (l >= a.mb || dir[l]) W[(int64_t)l * a.MP + l] = 1.0;
+}
+
+// ---- setup: batched blocked Gauss-Jordan inversion (SPD, no pivoting) -----------------------
+// step k: P = A_kk -> P^-1 (in place); A_kj := P^-1 A_kj (j != k); A_ij -= A_ik A_kj (i,j != k);
+// A_ik := -A_ik P^-1 (i != k).  A^-1 overwrites A.
+__global__ void __launch_bounds__(256) k_gj_pivot(double* W, int MP, int k, int* status) {
+  __shared__ double P[32][33];
+  __shared__ double rowt[32], colt[32];
+  double* A = W + (int64_t)blockIdx.x * MP * MP + (int64_t)(32 * k) * MP + 32 * k;
+  for (int e = threadIdx.x; e < 1024; e += blockDim.x) P[e / 32][e % 32] = A[(int64_t)(e / 32) * MP + e % 32];
+  __syncthreads();
+  // in-place Gauss-Jordan on the 32x32 pivot block (SPD: diagonal pivots, no exchanges)
+  for (int t = 0; t < 32; ++t) {
+    if (threadIdx.x < 32) rowt[threadIdx.x] = P[t][threadIdx.x];
+    else if (threadIdx.x < 64) colt[threadIdx.x - 32] = P[threadIdx.x - 32][t];
+    __syncthreads();
+    const double piv = rowt[t];
+    if (threadIdx.x == 0 && !(piv > 0.0 && isfinite(piv))) status[blockIdx.x] = 1;
+    const double ip = 1.0 / piv;
+    for (int e = threadIdx.x; e < 1024; e += blockDim.x) {
+      const int i = e / 32, j = e % 32;
+      double v;
+      if (i == t && j == t) v = ip;
+      else if (i == t) v = rowt[j] * ip;
+      else if (j == t) v = -colt[i] * ip;
+      else v = P[i][j] - colt[i] * rowt[j] * ip;
+      P[i][j] = v;
+    }
+    __syncthreads();
+  }
+  for (int e = threadIdx.x; e < 1024; e += blockDim.x) A[(int64_t)(e / 32) * MP + e % 32] = P[e / 32][e % 32];
+}
+
+// A_kj := P^-1 A_kj for column tile j (blockIdx.x), matrix blockIdx.y; skips j == k
+__global__ void __launch_bounds__(256) k_gj_row(double* W, int MP, int k) {
+  const int j = blockIdx.x >= (unsigned)k ? blockIdx.x + 1 : blockIdx.x;
+  __shared__ double P[32][33], B[32][33];
+  double* M = W + (int64_t)blockIdx.y * MP * MP;
+  const double* Pg = M + (int64_t)(32 * k) * MP + 32 * k;
+  double* Bg = M + (int64_t)(32 * k) * MP + 32 * j;
+  for (int e = threadIdx.x; e < 1024; e += blockDim.x) {
+    P[e / 32][e % 32] = Pg[(int64_t)(e / 32) * MP + e % 32];
+    B[e / 32][e % 32] = Bg[(int64_t)(e / 32) * MP + e % 32];
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < 1024; e += blockDim.x) {
+    const int r = e / 32, c = e % 32;
+    double s = 0.0;
+#pragma unroll 8
+    for (int t = 0; t < 32; ++t) s = fma(P[r][t], B[t][c], s);
+    Bg[(int64_t)r * MP + c] = s;
+  }
+}
+
+// A_ik := -A_ik P^-1 for row tile i (blockIdx.x), skips i == k
+__global__ void __launch_bounds__(256) k_gj_col(double* W, int MP, int k) {
+  const int i = blockIdx.x >= (unsigned)k ? blockIdx.x + 1 : blockIdx.x;
+  __shared__ double P[32][33], B[32][33];
+  double* M = W + (int64_t)blockIdx.y * MP * MP;
+  const double* Pg = M + (int64_t)(32 * k) * MP + 32 * k;
+  double* Bg = M + (int64_t)(32 * i) * MP + 32 * k;
+  for (int e = threadIdx.x; e < 1024; e += blockDim.x) {
+    P[e / 32][e % 32] = Pg[(int64_t)(e / 32) * MP + e % 32];
+    B[e / 32][e % 32] = Bg[(int64_t)(e / 32) * MP + e % 32];
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < 1024; e += blockDim.x) {
+    const int r = e / 32, c = e % 32;
+    double s = 0.0;
+#pragma unroll 8
+    for (int t = 0; t < 32; ++t) s = fma(B[r][t], P[t][c], s);
+    Bg[(int64_t)r * MP + c] = -s;
+  }
+}
+
+// trailing update A_ij -= A_ik A_kj over 64x64 output tiles (rows/cols of pivot block k
+// skipped): grid (tiles, matrices); 256 threads, 4x4 outputs each, K = 32 staged in smem
+__global__ void __launch_bounds__(256) k_gj_update(double* W, int MP, int k) {
+  const int nt64 = (MP + 63) / 64;
+  const int ti = blockIdx.x / nt64, tj = blockIdx.x % nt64;
+  __shared__ __align__(16) double U[32][64 + 2];   // U[t][r] = A[r0 + r][32k + t]
+  __shared__ __align__(16) double V[32][64 + 2];   // V[t][c] = A[32k + t][c0 + c]
+  double* M = W + (int64_t)blockIdx.y * MP * MP;
+  const int r0 = 64 * ti, c0 = 64 * tj, kk = 32 * k;
+  for (int e = threadIdx.x; e < 2048; e += blockDim.x) {
+    const int r = e / 32, t = e % 32;   // coalesced along t (row-major source)
+    U[t][r] = (r0 + r < MP) ? M[(int64_t)(r0 + r) * MP + kk + t] : 0.0;
+    const int t2 = e / 64, c = e % 64;
+    V[t2][c] = (c0 + c < MP) ? M[(int64_t)(kk + t2) * MP + c0 + c] : 0.0;
+  }
+  __syncthreads();
+  const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
+  double acc[4][4] = {};
+#pragma unroll 4
+  for (int t = 0; t < 32; ++t) {
+    double u[4], v[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) u[i] = U[t][ty * 4 + i];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) v[j] = V[t][tx * 4 + j];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc[i][j] = fma(u[i], v[j], acc[i][j]);
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int r = r0 + ty * 4 + i;
+    if (r >= MP || (r >= kk && r < kk + 32)) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int c = c0 + tx * 4 + j;
+      if (c >= MP || (c >= kk && c < kk + 32)) continue;
+      M[(int64_t)r * MP + c] -= acc[i][j];
+    }
+  }
+}
+
+// full workspace (ld MP) -> tile-packed lower storage (symmetrised); grid (tiles, matrices)
+__global__ void k_pack_tiles(const double* W, int MP, int nt, double* out, int64_t stride) {
+  int t = blockIdx.x;
+  int I = 0;
+  while ((I + 1) * (I + 2) / 2 <= t) ++I;
+  const int J = t - I * (I + 1) / 2;
+  const double* M = W + (int64_t)blockIdx.y * MP * MP;
+  double* o = out + (int64_t)blockIdx.y * stride + tile_off(I, J);
+  for (int e = threadIdx.x; e < 1024; e += blockDim.x) {
+    const int r = e / 32, c = e % 32;
+    const int64_t gi = 32 * I + r, gj = 32 * J + c;
+    const double v = 0.5 * (M[gi * MP + gj] + M[gj * MP + gi]);
+    if (I != J) o[e] = v;
+    else if (c <= r) o[r * (r + 1) / 2 + c] = v;
+  }
+}
+
+// ---- hot path: individual patch inverses, streamed ------------------------------------------
+struct PatchIrrOp {
+  int nx, ny, nz;
+  int na[3];
+  int mb, nt;                 // block slots, tiles per dim (32 nt >= mb)
+  int64_t stride;             // doubles per packed inverse
+  int64_t n_irr;
+  const int64_t* anchors;     // [n_irr] anchor of individual block i
+  const int8_t* mem;          // [mb] member cell of slot l
+  const int16_t* loc;         // [mb] local DOF of slot l
+  int mo[8][3];
+  const int64_t* base;        // level table
+  const int32_t* stride3;
+  const int16_t* cmin;
+  const int16_t* cmax;
+  int m;
+  const double* inv;          // [n_irr][stride]
+  const double* in;
+  double* out;
+  double coef;
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}\n"
+      ::"r"(smem_u32(bar)), "r"(parity) : "memory");
+}
+
+// 32 per-lane row partials -> lane r holds the warp sum of partial r (reduce-scatter butterfly)
+__device__ __forceinline__ double warp_reduce_scatter32(double (&p)[32]) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int h = 16; h >= 1; h >>= 1) {
+    const bool up = lane & h;
+#pragma unroll
+    for (int i = 0; i < h; ++i) {
+      // keep half: lanes with bit h set keep the upper half [h, 2h), others the lower [0, h)
+      const double send = up ? p[i] : p[i + h];
+      const double keep = up ? p[i + h] : p[i];
+      p[i] = keep + __shfl_xor_sync(0xffffffffu, send, h);
+    }
+  }
+  return p[0];
+}
+
+// smem: [xs: 32 nt doubles][ys: 32 nt doubles][ids: 32 nt ints][per warp: kIrrStages x 1024
+// doubles][per warp: kIrrStages mbarriers]
+__global__ void __launch_bounds__(kIrrWarps * 32, 1) k_patch_irr(PatchIrrOp op) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int MPd = 32 * op.nt;
+  double* xs = reinterpret_cast<double*>(smem);
+  double* ys = xs + MPd;
+  int* ids = reinterpret_cast<int*>(ys + MPd);
+  double* ring = reinterpret_cast<double*>(smem + ((size_t)MPd * 20 + 127) / 128 * 128);
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double* myring = ring + (size_t)w * kIrrStages * 1024;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(ring + (size_t)kIrrWarps * kIrrStages * 1024) + w * kIrrStages;
+  Tab* Tp = reinterpret_cast<Tab*>(bars + (kIrrWarps - w) * kIrrStages);   // after all barriers
+  Tab& T = *Tp;
+  for (int a = threadIdx.x; a < op.m; a += blockDim.x) {
+    T.g[a] = make_int4((int32_t)op.base[a], op.stride3[a * 3 + 1], op.stride3[a * 3 + 2], 0);
+    T.lo[a] = make_int4(op.cmin[a * 3 + 0], op.cmin[a * 3 + 1], op.cmin[a * 3 + 2], 0);
+    T.hi[a] = make_int4(op.cmax[a * 3 + 0], op.cmax[a * 3 + 1], op.cmax[a * 3 + 2], 0);
+  }
+  if (lane == 0)
+    for (int s = 0; s < kIrrStages; ++s) mbar_init(&bars[s], 1);
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  __syncthreads();
+  const int nt = op.nt;
+  const int ntiles = nt * (nt + 1) / 2;
+  const int ntw = w < ntiles ? (ntiles - w + kIrrWarps - 1) / kIrrWarps : 0;   // tiles of this warp per patch
+  const int64_t npatch = op.n_irr > blockIdx.x ? (op.n_irr - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+  const int64_t nitems = npatch * ntw;
+  // item i of this warp: patch k = i / ntw (block b = blockIdx.x + k gridDim.x), tile w + 8 (i % ntw)
+  auto tile_of = [&](int t, int& I, int& J) {
+    I = (int)((sqrtf(8.0f * t + 1.0f) - 1.0f) * 0.5f);
+    while (I * (I + 1) / 2 > t) --I;
+    while ((I + 1) * (I + 2) / 2 <= t) ++I;
+    J = t - I * (I + 1) / 2;
+  };
+  auto issue = [&](int64_t i) {
+    const int64_t k = i / ntw;
+    const int t = w + kIrrWarps * (int)(i % ntw);
+    int I, J;
+    tile_of(t, I, J);
+    const int64_t b = blockIdx.x + k * gridDim.x;
+    const double* src = op.inv + b * op.stride + tile_off(I, J);
+    const uint32_t bytes = (I == J ? kTileDiag : 1024) * 8;
+    const int s = (int)(i % kIrrStages);
+    mbar_expect_tx(&bars[s], bytes);
+    bulk_g2s(myring + s * 1024, src, bytes, &bars[s]);
+  };
+  if (lane == 0)
+    for (int64_t i = 0; i < kIrrStages && i < nitems; ++i) issue(i);
+  int64_t item = 0;
+  for (int64_t k = 0; k < npatch; ++k) {
+    const int64_t b = blockIdx.x + k * gridDim.x;
+    const int64_t A = op.anchors[b];
+    const int ax = (int)(A % op.na[0]), ay = (int)((A / op.na[0]) % op.na[1]), az = (int)(A / ((int64_t)op.na[0] * op.na[1]));
+    for (int l = threadIdx.x; l < MPd; l += blockDim.x) {
+      int idx = -1;
+      if (l < op.mb) {
+        const int km = op.mem[l], a = op.loc[l];
+        const int cx = ax + op.mo[km][0], cy = ay + op.mo[km][1], cz = az + op.mo[km][2];
+        const bool ok = cx >= 0 && cy >= 0 && cz >= 0 && cx < op.nx && cy < op.ny && cz < op.nz && dof_free(T, a, cx, cy, cz);
+        idx = ok ? dof_index(T, a, cx, cy, cz) : -1;
+      }
+      ids[l] = idx;
+      xs[l] = idx >= 0 ? __ldg(op.in + idx) : 0.0;
+      ys[l] = 0.0;
+    }
+    __syncthreads();
+    for (int j = 0; j < ntw; ++j, ++item) {
+      const int t = w + kIrrWarps * j;
+      int I, J;
+      tile_of(t, I, J);
+      const int s = (int)(item % kIrrStages);
+      mbar_wait(&bars[s], (uint32_t)((item / kIrrStages) & 1));
+      const double* tl = myring + s * 1024;
+      const double xJ = xs[32 * J + lane];
+      double yJ = 0.0;
+      double p[32];
+      if (I != J) {
+#pragma unroll
+        for (int r = 0; r < 32; ++r) {
+          const double a = tl[r * 32 + lane];
+          p[r] = a * xJ;
+          yJ = fma(a, xs[32 * I + r], yJ);
+        }
+      } else {
+#pragma unroll
+        for (int r = 0; r < 32; ++r) {
+          const double a = lane <= r ? tl[r * (r + 1) / 2 + lane] : 0.0;
+          p[r] = a * xJ;
+          if (lane < r) yJ = fma(a, xs[32 * I + r], yJ);
+        }
+      }
+      __syncwarp();
+      if (lane == 0 && item + kIrrStages < nitems) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        issue(item + kIrrStages);
+      }
+      const double yI = warp_reduce_scatter32(p);
+      atomicAdd(&ys[32 * I + lane], yI);
+      if (I != J || true) atomicAdd(&ys[32 * J + lane], yJ);
+    }
+    __syncthreads();
+    for (int l = threadIdx.x; l < op.mb; l += blockDim.x) {
+      const int idx = ids[l];
+      if (idx >= 0) atomicAdd(op.out + idx, op.coef * ys[l]);
+    }
+    __syncthreads();
+  }
+}
+
+// ---- hot path: regular patches by fast diagonalisation --------------------------------------
+struct PatchFdOp {
+  int nx, ny, nz, dim;
+  int na[3];
+  int q, S;                   // level, slots per axis (2q+1)
+  int64_t nreg;
+  const int32_t* anchors;     // [nreg] regular anchors
+  const int32_t* blk;         // per anchor: type code (alpha flag in bit 12 of -blk-1)
+  const int* cls;             // [3][na] axis class of each anchor coordinate
+  const double* tabs;         // [3][ncls][S*S + S]: S_a (row i = slot, col j = mode), lambda_a
+  int ncls;
+  double s_fac, inv_alpha;
+  const int16_t* modeidx;     // [(q+1)^3] local DOF of element mode (kx,ky,kz), kx fastest
+  const int64_t* base;
+  const int32_t* stride3;
+  const int16_t* cmin;
+  const int16_t* cmax;
+  int m;
+  const double* in;
+  double* out;
+  double coef;
+};
+
+// slot s (0..2q) of an axis at vertex v: cell offset and 1D mode (vertex slots pick a cell in
+// the grid: v-1 | internals of cell v-1 | v | internals of cell v | v+1)
+__device__ __forceinline__ void fd_slot(int s, int q, int v, int n, int& cell, int& k) {
+  if (s == 0) { cell = v - 1; k = 0; }
+  else if (s < q) { cell = v - 1; k = s + 1; }
+  else if (s == q) { if (v < n) { cell = v; k = 0; } else { cell = v - 1; k = 1; } }
+  else if (s < 2 * q) { cell = v; k = s - q + 1; }
+  else { cell = v; k = 1; }
+}
+
+// smem: [Tab][tables: 3*ncls*(S*S+S)][modeidx][per warp: X, Y (S^3 doubles each), ids (S^3 ints)]
+__global__ void __launch_bounds__(kFdWarps * 32) k_patch_fd(PatchFdOp op) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  Tab& T = *reinterpret_cast<Tab*>(smem);
+  const int S = op.S, S2 = S * S, S3 = op.dim == 3 ? S2 * S : S2;
+  const int tsz = S * S + S;
+  double* tab = reinterpret_cast<double*>(smem + sizeof(Tab));
+  int16_t* midx = reinterpret_cast<int16_t*>(tab + 3 * op.ncls * tsz);
+  const int nmi = (op.q + 1) * (op.q + 1) * (op.q + 1);
+  double* wbase = reinterpret_cast<double*>(smem + sizeof(Tab) + (size_t)3 * op.ncls * tsz * 8 + ((nmi * 2 + 15) / 16) * 16);
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double* X = wbase + (size_t)w * (2 * S3 + (S3 + 1) / 2);
+  double* Y = X + S3;
+  int* ids = reinterpret_cast<int*>(Y + S3);
+  for (int a = threadIdx.x; a < op.m; a += blockDim.x) {
+    T.g[a] = make_int4((int32_t)op.base[a], op.stride3[a * 3 + 1], op.stride3[a * 3 + 2], 0);
+    T.lo[a] = make_int4(op.cmin[a * 3 + 0], op.cmin[a * 3 + 1], op.cmin[a * 3 + 2], 0);
+    T.hi[a] = make_int4(op.cmax[a * 3 + 0], op.cmax[a * 3 + 1], op.cmax[a * 3 + 2], 0);
+  }
+  for (int e = threadIdx.x; e < 3 * op.ncls * tsz; e += blockDim.x) tab[e] = op.tabs[e];
+  for (int e = threadIdx.x; e < nmi; e += blockDim.x) midx[e] = op.modeidx[e];
+  __syncthreads();
+  const int q = op.q, dim = op.dim;
+  const int Sz = dim == 3 ? S : 1;
+  const int n3 = S2 * Sz;   // slots of this patch (S^2 in 2D)
+  for (int64_t i = (int64_t)blockIdx.x * kFdWarps + w; i < op.nreg; i += (int64_t)gridDim.x * kFdWarps) {
+    const int A = op.anchors[i];
+    const int vx = A % op.na[0], vy = (A / op.na[0]) % op.na[1], vz = A / (op.na[0] * op.na[1]);
+    const int t = -op.blk[A] - 1;
+    const double sc = (t >> 12) ? op.inv_alpha : 1.0;
+    const double* Tx = tab + (0 * op.ncls + op.cls[vx]) * tsz;
+    const double* Ty = tab + (1 * op.ncls + op.cls[op.na[0] + vy]) * tsz;
+    const double* Tz = tab + (2 * op.ncls + (dim == 3 ? op.cls[op.na[0] + op.na[1] + vz] : 0)) * tsz;
+    // gather (absent slots: S rows are zero there, so any finite value works; use 0)
+    for (int l = lane; l < n3; l += 32) {
+      const int sx = l % S, sy = (l / S) % S, sz = l / S2;
+      int cx, kx, cy, ky, cz = 0, kz = 0;
+      fd_slot(sx, q, vx, op.nx, cx, kx);
+      fd_slot(sy, q, vy, op.ny, cy, ky);
+      if (dim == 3) fd_slot(sz, q, vz, op.nz, cz, kz);
+      int idx = -1;
+      if (cx >= 0 && cy >= 0 && cz >= 0 && cx < op.nx && cy < op.ny && cz < op.nz) {
+        const int a = midx[(kz * (q + 1) + ky) * (q + 1) + kx];
+        if (dof_free(T, a, cx, cy, cz)) idx = dof_index(T, a, cx, cy, cz);
+      }
+      ids[l] = idx;
+      X[l] = idx >= 0 ? __ldg(op.in + idx) : 0.0;
+    }
+    __syncwarp();
+    // forward: Y = (S^T x S^T x S^T) X, axis by axis (X -> Y -> X -> Y)
+    // x-axis: out[.., j] = sum_i Sx[i][j] in[.., i]
+    for (int l = lane; l < n3; l += 32) {
+      const int j = l % S, row = l - j;
+      double s = 0.0;
+      for (int ii = 0; ii < S; ++ii) s = fma(Tx[ii * S + j], X[row + ii], s);
+      Y[l] = s;
+    }
+    __syncwarp();
+    for (int l = lane; l < n3; l += 32) {
+      const int j = (l / S) % S, off = l - j * S;
+      double s = 0.0;
+      for (int ii = 0; ii < S; ++ii) s = fma(Ty[ii * S + j], Y[off + ii * S], s);
+      X[l] = s;
+    }
+    __syncwarp();
+    if (dim == 3) {
+      for (int l = lane; l < n3; l += 32) {
+        const int j = l / S2, off = l - j * S2;
+        double s = 0.0;
+        for (int ii = 0; ii < S; ++ii) s = fma(Tz[ii * S + j], X[off + ii * S2], s);
+        Y[l] = s;
+      }
+    } else {
+      for (int l = lane; l < n3; l += 32) Y[l] = X[l];
+    }
+    __syncwarp();
+    // D^-1
+    for (int l = lane; l < n3; l += 32) {
+      const int jx = l % S, jy = (l / S) % S, jz = l / S2;
+      const double lam = Tx[S * S + jx] + Ty[S * S + jy] + (dim == 3 ? Tz[S * S + jz] : 0.0);
+      X[l] = Y[l] * (sc / (op.s_fac * lam));
+    }
+    __syncwarp();
+    // backward: Z = (S x S x S) Y: out[.., i] = sum_j S[i][j] in[.., j]
+    if (dim == 3) {
+      for (int l = lane; l < n3; l += 32) {
+        const int ii = l / S2, off = l - ii * S2;
+        double s = 0.0;
+        for (int j = 0; j < S; ++j) s = fma(Tz[ii * S + j], X[off + j * S2], s);
+        Y[l] = s;
+      }
+    } else {
+      for (int l = lane; l < n3; l += 32) Y[l] = X[l];
+    }
+    __syncwarp();
+    for (int l = lane; l < n3; l += 32) {
+      const int ii = (l / S) % S, off = l - ii * S;
+      double s = 0.0;
+      for (int j = 0; j < S; ++j) s = fma(Ty[ii * S + j], Y[off + j * S], s);
+      X[l] = s;
+    }
+    __syncwarp();
+    for (int l = lane; l < n3; l += 32) {
+      const int ii = l % S, row = l - ii;
+      double s = 0.0;
+      for (int j = 0; j < S; ++j) s = fma(Tx[ii * S + j], X[row + j], s);
+      const int idx = ids[l];
+      if (idx >= 0) atomicAdd(op.out + idx, op.coef * s);
+    }
+    __syncwarp();
+  }
+}
+
+}  // namespace fcm
