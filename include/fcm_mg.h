@@ -235,6 +235,13 @@ int fcm_apply(fcm_mg* h, int32_t q, const double* x, double* y);
  * AdditiveSchwarz P:254-257) on level q; omega_q = params.omega (q >= 2) or 1 (q = 1).     */
 int fcm_mg_smooth(fcm_mg* h, int32_t q, const double* r, double* x);
 
+/* One population of a patchwise level's smoother (measurement, parity by parts): part 1 = the
+ * individual (irregular) patches only (k_patch_irr, streaming the tile-packed inverses),
+ * part 2 = the shared-type (regular) patches only, 0 = both (= fcm_mg_smooth).  Parts 1 and 2
+ * sum to part 0 (up to the order of the fp64 scatter additions).  FCM_EINVAL on elementwise
+ * levels.                                                                                   */
+int fcm_mg_smooth_part(fcm_mg* h, int32_t q, int32_t part, const double* r, double* x);
+
 /* x = A_1^{-1} r by the configured coarse solver; *iters (host, may be NULL)
  * receives the inner CG iterations (0 for direct).                                         */
 int fcm_mg_coarse_solve(fcm_mg* h, const double* r, double* x, int32_t* iters);

@@ -64,6 +64,7 @@ _SIGS = {
     "fcm_mg_load": (I32, [P, P, P, P, I32, P]),
     "fcm_apply": (I32, [P, I32, P, P]),
     "fcm_mg_smooth": (I32, [P, I32, P, P]),
+    "fcm_mg_smooth_part": (I32, [P, I32, I32, P, P]),
     "fcm_mg_coarse_solve": (I32, [P, P, P, P]),
     "fcm_mg_vcycle": (I32, [P, P, P]),
     "fcm_pcg_solve": (I32, [P, P, P, D, I32, P, P]),

@@ -941,14 +941,15 @@ static size_t block_smem(int m, int mb) {
 // diagonalisation (k_patch_fd) or, off the tensor-Poisson case, the dense shared-type kernel
 static size_t fd_smem(const fcm_mg* h, int q);
 static size_t irr_smem(int nt);
-static int launch_block_smooth(fcm_mg* h, int q, const double* r, double* x, double coef) {
+static int launch_block_smooth(fcm_mg* h, int q, const double* r, double* x, double coef, int part = 0) {
   LevelDev& Lv = h->lev[q];
-  const bool fork = Lv.n_irr > 0 && Lv.n_reg > 0;
+  const bool do_irr = part != 2 && Lv.n_irr > 0, do_reg = part != 1 && Lv.n_reg > 0;
+  const bool fork = do_irr && do_reg;
   if (fork) {
     CU(cudaEventRecord(h->ev_fork, h->stream));
     CU(cudaStreamWaitEvent(h->stream2, h->ev_fork, 0));
   }
-  if (Lv.n_irr > 0) {
+  if (do_irr) {
     PatchIrrOp op{};
     op.nx = h->L.n[0]; op.ny = h->L.n[1]; op.nz = h->L.n[2];
     for (int i = 0; i < 3; ++i) op.na[i] = Lv.na[i];
@@ -963,7 +964,7 @@ static int launch_block_smooth(fcm_mg* h, int q, const double* r, double* x, dou
     h->count();
     CU(cudaGetLastError());
   }
-  if (Lv.n_reg > 0) {
+  if (do_reg) {
     if (Lv.fd) {
       PatchFdOp op{};
       op.nx = h->L.n[0]; op.ny = h->L.n[1]; op.nz = h->L.n[2]; op.dim = h->L.dim;
@@ -2604,6 +2605,16 @@ extern "C" int fcm_mg_smooth(fcm_mg* h, int32_t q, const double* r, double* x) {
   if (!h->lev[q].has_as) return fail(FCM_EINVAL, "level q=%d has no Schwarz smoother", q);
   StreamGuard sg(h);
   return smooth(h, q, r, x);
+}
+
+extern "C" int fcm_mg_smooth_part(fcm_mg* h, int32_t q, int32_t part, const double* r, double* x) {
+  clear_error();
+  if (!h || !r || !x || q < 1 || q > h->g.p || part < 0 || part > 2) return fail(FCM_EINVAL, "bad argument");
+  if (!h->lev[q].has_as) return fail(FCM_EINVAL, "level q=%d has no Schwarz smoother", q);
+  if (part == 0) return fcm_mg_smooth(h, q, r, x);
+  if (!h->lev[q].patch || h->multi) return fail(FCM_EINVAL, "smoother parts exist on patchwise levels only");
+  StreamGuard sg(h);
+  return launch_block_smooth(h, q, r, x, h->lev[q].omega, part);
 }
 
 extern "C" int fcm_mg_coarse_solve(fcm_mg* h, const double* r, double* x, int32_t* iters) {

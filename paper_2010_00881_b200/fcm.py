@@ -303,6 +303,12 @@ class Solver:
         check(_lib.lib().fcm_mg_block_counts(self._h, q, C.byref(n), C.byref(t)))
         return n.value
 
+    def block_size(self, q) -> int:
+        """m_b of level q's Schwarz blocks (element size, or (2q+1)^d patch slots)."""
+        n, mb = C.c_int64(), C.c_int32()
+        check(_lib.lib().fcm_mg_export_block_inverses(self._h, q, C.byref(n), C.byref(mb), None, None, None))
+        return mb.value
+
     def block_counts(self, q):
         n, t = C.c_int64(), C.c_int32()
         check(_lib.lib().fcm_mg_block_counts(self._h, q, C.byref(n), C.byref(t)))
@@ -369,6 +375,12 @@ class Solver:
     def smooth(self, r: torch.Tensor, x: torch.Tensor, q=None) -> torch.Tensor:
         q = self.cfg.p if q is None else q
         check(_lib.lib().fcm_mg_smooth(self._h, q, self._dv(r, q, "r"), self._dv(x, q, "x")))
+        return x
+
+    def smooth_part(self, r: torch.Tensor, x: torch.Tensor, q, part: int) -> torch.Tensor:
+        """x += omega M^-1 r restricted to one block population of a patch level
+        (fcm_mg_smooth_part: 1 individual patches, 2 shared-type patches, 0 both)."""
+        check(_lib.lib().fcm_mg_smooth_part(self._h, q, part, self._dv(r, q, "r"), self._dv(x, q, "x")))
         return x
 
     def coarse_solve(self, r: torch.Tensor):

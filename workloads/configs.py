@@ -101,3 +101,36 @@ def small_config(dim=3, n=4, p=2, space="tensor", physics="poisson", voids=None,
         kw.setdefault("traction_face", 1)
     return Config(f"small_d{dim}_n{n}_p{p}_{space}_{physics}", dim=dim, n=n, p=p, space=space,
                   physics=physics, geometry=geom, **kw)
+
+
+def window_config(cfg: Config, k: int, corner=None) -> Config:
+    """A bounded spatial SAMPLE of a workload (for the CPU-oracle timing legs of bench.py):
+    the k^d cells of `cfg` starting at cell `corner` (default: the k^d window holding the most
+    void volume near the domain centre), rescaled to [0,1]^d with k cells per axis -- same p,
+    space, physics, smoother and solver constants, the voids that touch the window mapped by
+    x -> (x - corner h) / (k h), u = 0 on the window faces.  No method arithmetic."""
+    from .voids import config_voids
+    import numpy as np
+    c, r = config_voids(cfg)
+    h = 1.0 / cfg.n
+    d = cfg.dim
+    if corner is None:
+        mid = (cfg.n - k) // 2
+        best, corner = -1.0, (mid,) * d
+        for off in range(-(cfg.n // 4), cfg.n // 4 + 1, max(1, k // 2)):
+            cand = tuple(min(max(mid + off, 0), cfg.n - k) for _ in range(d))
+            lo = np.array(cand) * h
+            hi = lo + k * h
+            near = np.clip(c, lo, hi)
+            touch = np.sum((c - near) ** 2, axis=1) < r ** 2
+            vol = float(np.sum(r[touch] ** d))
+            if vol > best:
+                best, corner = vol, cand
+    lo = np.array(corner, dtype=np.float64) * h
+    hi = lo + k * h
+    near = np.clip(c, lo, hi)
+    touch = np.sum((c - near) ** 2, axis=1) < r ** 2
+    cs = (c[touch] - lo) / (k * h)
+    rs = r[touch] / (k * h)
+    geom = {"kind": "explicit", "centres": cs.tolist(), "radii": rs.tolist()}
+    return dataclasses.replace(cfg, name=f"{cfg.name}_window{k}", n=k, geometry=geom)
