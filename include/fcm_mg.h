@@ -286,6 +286,8 @@ int fcm_mg_solve(fcm_mg* h, const double* b, double* x, double rtol, int32_t max
  *   inv       [n_blocks * m_b^2]    the inverse, row-major, in the block's slot order; shared-type
  *                                   blocks are expanded (and scaled by 1/alpha for all-fictitious
  *                                   neighbourhoods), individual blocks unpacked.
+ * Level 1 with the direct coarse solver exports the dense A_1^{-1} it applies as ONE block of
+ * size ndofs(1) (dof_index = 0..ndofs(1)-1).
  * Errors: FCM_EINVAL (bad handle/level, level without a smoother), FCM_ECUDA.                */
 int fcm_mg_export_block_inverses(const fcm_mg* h, int32_t q, int64_t* n_blocks, int32_t* block_size,
                                  int64_t* anchors, int32_t* dof_index, double* inv);

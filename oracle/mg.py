@@ -144,10 +144,17 @@ class Hierarchy:
             self.diag = c.A.diagonal()
         self.coarse_iters = []
 
+    def set_coarse_inverse(self, inv):
+        """Identical-setup parity protocol: apply an externally supplied
+        dense A_1^{-1} as the direct coarse solve instead of this oracle's own LU."""
+        self.coarse_inv = np.asarray(inv, dtype=np.float64)
+
     # -- coarse level (P:141, P:180, P:343) --------------------------------------
     def coarse_solve(self, b):
         lv = self.levels[1]
         if self.coarse == "direct":
+            if getattr(self, "coarse_inv", None) is not None:
+                return self.coarse_inv @ b
             return sla.lu_solve(self.lu, b)
         prec = lv.schwarz if self.coarse == "as_pcg" else (lambda r: r / self.diag)
         x, it = pcg(lambda v: lv.A @ v, b, prec, self.coarse_rtol, self.coarse_maxit,

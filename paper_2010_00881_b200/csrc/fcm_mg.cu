@@ -637,7 +637,7 @@ const void* reg_kernel(int m, int* M_out) {
 }
 const void* mma_kernel(int m) {
 #define CASE(MM) case MM: return (const void*)k_cell_mma<MM, gsz<MM>()>;
-  switch (m) { FCM_FOR_M(CASE) CASE(64) default: break; }   // 64: tensor p = 3 (config 5)
+  switch (m) { FCM_FOR_M(CASE) CASE(64) CASE(125) default: break; }   // 64 / 125: tensor p = 3 / 4 (configs 5 / 3)
 #undef CASE
   return nullptr;
 }
@@ -941,6 +941,12 @@ static size_t block_smem(int m, int mb) {
 // diagonalisation (k_patch_fd) or, off the tensor-Poisson case, the dense shared-type kernel
 static size_t fd_smem(const fcm_mg* h, int q);
 static size_t irr_smem(int nt);
+static const void* fd_kernel(int S, int dim) {
+  if (dim == 3) return S == 3 ? (const void*)k_patch_fd<3, 3> : S == 5 ? (const void*)k_patch_fd<5, 3>
+                     : S == 7 ? (const void*)k_patch_fd<7, 3> : (const void*)k_patch_fd<9, 3>;
+  return S == 3 ? (const void*)k_patch_fd<3, 2> : S == 5 ? (const void*)k_patch_fd<5, 2>
+         : S == 7 ? (const void*)k_patch_fd<7, 2> : (const void*)k_patch_fd<9, 2>;
+}
 static int launch_block_smooth(fcm_mg* h, int q, const double* r, double* x, double coef, int part = 0) {
   LevelDev& Lv = h->lev[q];
   const bool do_irr = part != 2 && Lv.n_irr > 0, do_reg = part != 1 && Lv.n_reg > 0;
@@ -975,7 +981,9 @@ static int launch_block_smooth(fcm_mg* h, int q, const double* r, double* x, dou
       op.base = Lv.base; op.stride3 = Lv.stride; op.cmin = Lv.cmin; op.cmax = Lv.cmax; op.m = Lv.m;
       op.in = r; op.out = x; op.coef = coef;
       const int nb = (int)std::max<int64_t>(1, std::min<int64_t>((Lv.n_reg + kFdWarps - 1) / kFdWarps, (int64_t)h->num_sms * 2));
-      k_patch_fd<<<nb, kFdWarps * 32, fd_smem(h, q), h->stream>>>(op);
+      const void* kfd = fd_kernel(2 * q + 1, h->L.dim);
+      void* args[] = {&op};
+      CU(cudaLaunchKernel(kfd, dim3(nb), dim3(kFdWarps * 32), args, fd_smem(h, q), h->stream));
     } else {
       BlockOp op{};
       op.nx = h->L.n[0]; op.ny = h->L.n[1]; op.nz = h->L.n[2];
@@ -1490,7 +1498,7 @@ static int setup_patch_fd(fcm_mg* h, int q, const double* K_ref_host) {
 static size_t fd_smem(const fcm_mg* h, int q) {
   const int S = 2 * q + 1, S3 = h->L.dim == 3 ? S * S * S : S * S, nmi = (q + 1) * (q + 1) * (q + 1);
   return sizeof(Tab) + (size_t)3 * h->lev[q].fd_ncls * (S * S + S) * 8 + ((nmi * 2 + 15) / 16) * 16 +
-         (size_t)kFdWarps * (2 * S3 + (S3 + 1) / 2) * 8;
+         (size_t)kFdWarps * 2 * S3 * 8;
 }
 static size_t irr_smem(int nt) {
   const size_t MPd = 32 * (size_t)nt;
@@ -2362,7 +2370,7 @@ static int setup_impl(const fcm_grid* g, const fcm_params* prm, const fcm_slab* 
   for (int q = 2; q <= g->p; ++q)
     if (h->lev[q].patch) {
       RC(setup_patch_fd(h.get(), q, K_ref));
-      if (h->lev[q].fd) RC(allow_smem((const void*)k_patch_fd, fd_smem(h.get(), q)));
+      if (h->lev[q].fd) RC(allow_smem(fd_kernel(2 * q + 1, g->dim), fd_smem(h.get(), q)));
       else RC(allow_smem((const void*)k_block_smooth, block_smem(h->lev[q].m, h->lev[q].mb)));
       RC(allow_smem((const void*)k_patch_irr, irr_smem(h->lev[q].nt)));
     }
@@ -3024,8 +3032,18 @@ extern "C" int fcm_mg_export_block_inverses(const fcm_mg* h, int32_t q, int64_t*
   clear_error();
   if (!h || q < 1 || q > h->g.p) return fail(FCM_EINVAL, "bad handle or level");
   const LevelDev& Lv = h->lev[q];
-  if (!Lv.has_as) return fail(FCM_EINVAL, "level %d has no additive-Schwarz smoother", q);
   if (!n_blocks || !block_size) return fail(FCM_EINVAL, "NULL count arguments");
+  if (q == 1 && h->prm.coarse == FCM_COARSE_DIRECT && h->d_A0inv) {   // the direct coarse inverse: one block
+    const int64_t n1 = Lv.ndof;
+    *n_blocks = 1;
+    *block_size = (int32_t)n1;
+    if (anchors) anchors[0] = 0;
+    if (dof_index)
+      for (int64_t l = 0; l < n1; ++l) dof_index[l] = (int32_t)l;
+    if (inv) CU(cudaMemcpy(inv, h->d_A0inv, (size_t)n1 * n1 * 8, cudaMemcpyDeviceToHost));
+    return FCM_OK;
+  }
+  if (!Lv.has_as) return fail(FCM_EINVAL, "level %d has no additive-Schwarz smoother", q);
   const BlockGeom g = block_geom(h->L, q, Lv.patch);
   const int mb = g.mb;
   std::vector<int64_t> list;

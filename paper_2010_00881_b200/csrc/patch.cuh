@@ -26,7 +26,7 @@ namespace fcm {
 constexpr int kTileDiag = 528;    // 32*33/2
 constexpr int kIrrWarps = 8;      // warps per CTA of k_patch_irr
 constexpr int kIrrStages = 3;     // ring depth per warp
-constexpr int kFdWarps = 8;       // warps per CTA of k_patch_fd
+constexpr int kFdWarps = 12;      // warps per CTA of k_patch_fd
 constexpr int kFdMaxS = 9;        // 2q+1 <= 9 (q <= 4)
 
 __host__ __device__ constexpr int64_t tile_pack_size(int nt) {
@@ -420,20 +420,26 @@ __device__ __forceinline__ void fd_slot(int s, int q, int v, int n, int& cell, i
   else { cell = v; k = 1; }
 }
 
-// smem: [Tab][tables: 3*ncls*(S*S+S)][modeidx][per warp: X, Y (S^3 doubles each), ids (S^3 ints)]
+// smem: [Tab][tables: 3*ncls*(S*S+S)][modeidx][per warp: X, Y (S^d doubles each)].
+// Compile-time S (slots per axis) and DIM: every lane owns slots l = lane + 32 j, whose DOF
+// indices and gathered values live in registers (all NL loads in flight before the first use:
+// the gather is one memory latency per patch, not one per slot), and the same slots are
+// scattered at the end.
+template <int S, int DIM>
 __global__ void __launch_bounds__(kFdWarps * 32) k_patch_fd(PatchFdOp op) {
+  constexpr int S2 = S * S, N3 = DIM == 3 ? S2 * S : S2;
+  constexpr int NL = (N3 + 31) / 32;
+  constexpr int tsz = S * S + S;
   extern __shared__ __align__(16) unsigned char smem[];
   Tab& T = *reinterpret_cast<Tab*>(smem);
-  const int S = op.S, S2 = S * S, S3 = op.dim == 3 ? S2 * S : S2;
-  const int tsz = S * S + S;
   double* tab = reinterpret_cast<double*>(smem + sizeof(Tab));
   int16_t* midx = reinterpret_cast<int16_t*>(tab + 3 * op.ncls * tsz);
-  const int nmi = (op.q + 1) * (op.q + 1) * (op.q + 1);
+  const int q = op.q;
+  const int nmi = (q + 1) * (q + 1) * (q + 1);
   double* wbase = reinterpret_cast<double*>(smem + sizeof(Tab) + (size_t)3 * op.ncls * tsz * 8 + ((nmi * 2 + 15) / 16) * 16);
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  double* X = wbase + (size_t)w * (2 * S3 + (S3 + 1) / 2);
-  double* Y = X + S3;
-  int* ids = reinterpret_cast<int*>(Y + S3);
+  double* X = wbase + (size_t)w * 2 * N3;
+  double* Y = X + N3;
   for (int a = threadIdx.x; a < op.m; a += blockDim.x) {
     T.g[a] = make_int4((int32_t)op.base[a], op.stride3[a * 3 + 1], op.stride3[a * 3 + 2], 0);
     T.lo[a] = make_int4(op.cmin[a * 3 + 0], op.cmin[a * 3 + 1], op.cmin[a * 3 + 2], 0);
@@ -442,9 +448,7 @@ __global__ void __launch_bounds__(kFdWarps * 32) k_patch_fd(PatchFdOp op) {
   for (int e = threadIdx.x; e < 3 * op.ncls * tsz; e += blockDim.x) tab[e] = op.tabs[e];
   for (int e = threadIdx.x; e < nmi; e += blockDim.x) midx[e] = op.modeidx[e];
   __syncthreads();
-  const int q = op.q, dim = op.dim;
-  const int Sz = dim == 3 ? S : 1;
-  const int n3 = S2 * Sz;   // slots of this patch (S^2 in 2D)
+  const double coef = op.coef;
   for (int64_t i = (int64_t)blockIdx.x * kFdWarps + w; i < op.nreg; i += (int64_t)gridDim.x * kFdWarps) {
     const int A = op.anchors[i];
     const int vx = A % op.na[0], vy = (A / op.na[0]) % op.na[1], vz = A / (op.na[0] * op.na[1]);
@@ -452,82 +456,116 @@ __global__ void __launch_bounds__(kFdWarps * 32) k_patch_fd(PatchFdOp op) {
     const double sc = (t >> 12) ? op.inv_alpha : 1.0;
     const double* Tx = tab + (0 * op.ncls + op.cls[vx]) * tsz;
     const double* Ty = tab + (1 * op.ncls + op.cls[op.na[0] + vy]) * tsz;
-    const double* Tz = tab + (2 * op.ncls + (dim == 3 ? op.cls[op.na[0] + op.na[1] + vz] : 0)) * tsz;
-    // gather (absent slots: S rows are zero there, so any finite value works; use 0)
-    for (int l = lane; l < n3; l += 32) {
-      const int sx = l % S, sy = (l / S) % S, sz = l / S2;
-      int cx, kx, cy, ky, cz = 0, kz = 0;
-      fd_slot(sx, q, vx, op.nx, cx, kx);
-      fd_slot(sy, q, vy, op.ny, cy, ky);
-      if (dim == 3) fd_slot(sz, q, vz, op.nz, cz, kz);
+    const double* Tz = tab + (2 * op.ncls + (DIM == 3 ? op.cls[op.na[0] + op.na[1] + vz] : 0)) * tsz;
+    int ids[NL];
+    double xv[NL];
+#pragma unroll
+    for (int j = 0; j < NL; ++j) {
+      const int l = lane + 32 * j;
       int idx = -1;
-      if (cx >= 0 && cy >= 0 && cz >= 0 && cx < op.nx && cy < op.ny && cz < op.nz) {
-        const int a = midx[(kz * (q + 1) + ky) * (q + 1) + kx];
-        if (dof_free(T, a, cx, cy, cz)) idx = dof_index(T, a, cx, cy, cz);
+      if (l < N3) {
+        const int sx = l % S, sy = (l / S) % S, sz = DIM == 3 ? l / S2 : 0;
+        int cx, kx, cy, ky, cz = 0, kz = 0;
+        fd_slot(sx, q, vx, op.nx, cx, kx);
+        fd_slot(sy, q, vy, op.ny, cy, ky);
+        if (DIM == 3) fd_slot(sz, q, vz, op.nz, cz, kz);
+        if (cx >= 0 && cy >= 0 && cz >= 0 && cx < op.nx && cy < op.ny && cz < op.nz) {
+          const int a = midx[(kz * (q + 1) + ky) * (q + 1) + kx];
+          if (dof_free(T, a, cx, cy, cz)) idx = dof_index(T, a, cx, cy, cz);
+        }
       }
-      ids[l] = idx;
-      X[l] = idx >= 0 ? __ldg(op.in + idx) : 0.0;
+      ids[j] = idx;
     }
+#pragma unroll
+    for (int j = 0; j < NL; ++j) xv[j] = ids[j] >= 0 ? __ldg(op.in + ids[j]) : 0.0;
+#pragma unroll
+    for (int j = 0; j < NL; ++j)
+      if (lane + 32 * j < N3) X[lane + 32 * j] = xv[j];
     __syncwarp();
-    // forward: Y = (S^T x S^T x S^T) X, axis by axis (X -> Y -> X -> Y)
-    // x-axis: out[.., j] = sum_i Sx[i][j] in[.., i]
-    for (int l = lane; l < n3; l += 32) {
-      const int j = l % S, row = l - j;
+    // forward: Y = (S^T x S^T x S^T) X, one axis at a time
+#pragma unroll
+    for (int j = 0; j < NL; ++j) {
+      const int l = lane + 32 * j;
+      if (l >= N3) break;
+      const int jj = l % S, row = l - jj;
       double s = 0.0;
-      for (int ii = 0; ii < S; ++ii) s = fma(Tx[ii * S + j], X[row + ii], s);
+#pragma unroll
+      for (int ii = 0; ii < S; ++ii) s = fma(Tx[ii * S + jj], X[row + ii], s);
       Y[l] = s;
     }
     __syncwarp();
-    for (int l = lane; l < n3; l += 32) {
-      const int j = (l / S) % S, off = l - j * S;
+#pragma unroll
+    for (int j = 0; j < NL; ++j) {
+      const int l = lane + 32 * j;
+      if (l >= N3) break;
+      const int jj = (l / S) % S, off = l - jj * S;
       double s = 0.0;
-      for (int ii = 0; ii < S; ++ii) s = fma(Ty[ii * S + j], Y[off + ii * S], s);
+#pragma unroll
+      for (int ii = 0; ii < S; ++ii) s = fma(Ty[ii * S + jj], Y[off + ii * S], s);
       X[l] = s;
     }
     __syncwarp();
-    if (dim == 3) {
-      for (int l = lane; l < n3; l += 32) {
-        const int j = l / S2, off = l - j * S2;
+    if (DIM == 3) {
+#pragma unroll
+      for (int j = 0; j < NL; ++j) {
+        const int l = lane + 32 * j;
+        if (l >= N3) break;
+        const int jj = l / S2, off = l - jj * S2;
         double s = 0.0;
-        for (int ii = 0; ii < S; ++ii) s = fma(Tz[ii * S + j], X[off + ii * S2], s);
+#pragma unroll
+        for (int ii = 0; ii < S; ++ii) s = fma(Tz[ii * S + jj], X[off + ii * S2], s);
         Y[l] = s;
       }
-    } else {
-      for (int l = lane; l < n3; l += 32) Y[l] = X[l];
+      __syncwarp();
+    }
+    const double* Z = DIM == 3 ? Y : X;   // forward result
+    double* U = DIM == 3 ? X : Y;         // scaled
+#pragma unroll
+    for (int j = 0; j < NL; ++j) {
+      const int l = lane + 32 * j;
+      if (l >= N3) break;
+      const int jx = l % S, jy = (l / S) % S, jz = DIM == 3 ? l / S2 : 0;
+      const double lam = Tx[S * S + jx] + Ty[S * S + jy] + (DIM == 3 ? Tz[S * S + jz] : 0.0);
+      U[l] = Z[l] * (sc / (op.s_fac * lam));
     }
     __syncwarp();
-    // D^-1
-    for (int l = lane; l < n3; l += 32) {
-      const int jx = l % S, jy = (l / S) % S, jz = l / S2;
-      const double lam = Tx[S * S + jx] + Ty[S * S + jy] + (dim == 3 ? Tz[S * S + jz] : 0.0);
-      X[l] = Y[l] * (sc / (op.s_fac * lam));
-    }
-    __syncwarp();
-    // backward: Z = (S x S x S) Y: out[.., i] = sum_j S[i][j] in[.., j]
-    if (dim == 3) {
-      for (int l = lane; l < n3; l += 32) {
+    // backward: (S x S x S) U
+    double* V1 = U;
+    double* V2 = DIM == 3 ? Y : X;
+    if (DIM == 3) {
+#pragma unroll
+      for (int j = 0; j < NL; ++j) {
+        const int l = lane + 32 * j;
+        if (l >= N3) break;
         const int ii = l / S2, off = l - ii * S2;
         double s = 0.0;
-        for (int j = 0; j < S; ++j) s = fma(Tz[ii * S + j], X[off + j * S2], s);
-        Y[l] = s;
+#pragma unroll
+        for (int jj = 0; jj < S; ++jj) s = fma(Tz[ii * S + jj], V1[off + jj * S2], s);
+        V2[l] = s;
       }
-    } else {
-      for (int l = lane; l < n3; l += 32) Y[l] = X[l];
+      __syncwarp();
+      double* tmp = V1; V1 = V2; V2 = tmp;
     }
-    __syncwarp();
-    for (int l = lane; l < n3; l += 32) {
+#pragma unroll
+    for (int j = 0; j < NL; ++j) {
+      const int l = lane + 32 * j;
+      if (l >= N3) break;
       const int ii = (l / S) % S, off = l - ii * S;
       double s = 0.0;
-      for (int j = 0; j < S; ++j) s = fma(Ty[ii * S + j], Y[off + j * S], s);
-      X[l] = s;
+#pragma unroll
+      for (int jj = 0; jj < S; ++jj) s = fma(Ty[ii * S + jj], V1[off + jj * S], s);
+      V2[l] = s;
     }
     __syncwarp();
-    for (int l = lane; l < n3; l += 32) {
+#pragma unroll
+    for (int j = 0; j < NL; ++j) {
+      const int l = lane + 32 * j;
+      if (l >= N3) break;
       const int ii = l % S, row = l - ii;
       double s = 0.0;
-      for (int j = 0; j < S; ++j) s = fma(Tx[ii * S + j], X[row + j], s);
-      const int idx = ids[l];
-      if (idx >= 0) atomicAdd(op.out + idx, op.coef * s);
+#pragma unroll
+      for (int jj = 0; jj < S; ++jj) s = fma(Tx[ii * S + jj], V2[row + jj], s);
+      if (ids[j] >= 0) atomicAdd(op.out + ids[j], coef * s);
     }
     __syncwarp();
   }

@@ -71,6 +71,16 @@ class Pair:
                 assert all(np.all(b >= 0) for b in blocks)
                 assert {frozenset(b.tolist()) for b in blocks} == {frozenset(b.tolist()) for b in lv.blocks}, q
                 lv.set_blocks(blocks, invs)
+            if self.cfg.coarse == "direct":   # the dense coarse inverse the GPU applies
+                _, idx, inv = self.S.export_block_inverses(1)
+                lv1 = Hi.levels[1]
+                lpos = np.full(self.P.dof.ndof, -1)
+                lpos[lv1.idx] = np.arange(lv1.n)
+                o = lpos[self.pos[idx[0]]]
+                assert np.all(o >= 0) and len(o) == lv1.n
+                A0inv = np.zeros((lv1.n, lv1.n))
+                A0inv[np.ix_(o, o)] = inv[0]
+                Hi.set_coarse_inverse(A0inv)
             self.Hi = Hi
         return self.Hi
 
