@@ -939,75 +939,69 @@ static size_t block_smem(int m, int mb) {
 // patchwise smoother (patch.cuh): the individual (irregular) patches stream their tile-packed
 // inverses (k_patch_irr, forked onto the second stream) while the regular patches run by fast
 // diagonalisation (k_patch_fd) or, off the tensor-Poisson case, the dense shared-type kernel
-static size_t fd_smem(const fcm_mg* h, int q);
-static size_t irr_smem(int nt);
-static const void* fd_kernel(int S, int dim) {
-  if (dim == 3) return S == 3 ? (const void*)k_patch_fd<3, 3> : S == 5 ? (const void*)k_patch_fd<5, 3>
-                     : S == 7 ? (const void*)k_patch_fd<7, 3> : (const void*)k_patch_fd<9, 3>;
-  return S == 3 ? (const void*)k_patch_fd<3, 2> : S == 5 ? (const void*)k_patch_fd<5, 2>
-         : S == 7 ? (const void*)k_patch_fd<7, 2> : (const void*)k_patch_fd<9, 2>;
+static size_t patch_smem(const fcm_mg* h, int q);
+template <int S, int DIM>
+static const void* patch_kernel_s(int irr, int fd) {
+  if (irr && fd) return (const void*)k_patch_smooth<S, DIM, true, true>;
+  if (irr) return (const void*)k_patch_smooth<S, DIM, true, false>;
+  return (const void*)k_patch_smooth<S, DIM, false, true>;
 }
+static const void* patch_kernel(int S, int dim, int irr, int fd) {
+  if (dim == 3) return S == 3 ? patch_kernel_s<3, 3>(irr, fd) : S == 5 ? patch_kernel_s<5, 3>(irr, fd)
+                     : S == 7 ? patch_kernel_s<7, 3>(irr, fd) : patch_kernel_s<9, 3>(irr, fd);
+  return S == 3 ? patch_kernel_s<3, 2>(irr, fd) : S == 5 ? patch_kernel_s<5, 2>(irr, fd)
+         : S == 7 ? patch_kernel_s<7, 2>(irr, fd) : patch_kernel_s<9, 2>(irr, fd);
+}
+// patchwise smoother (patch.cuh): ONE warp-specialised launch (k_patch_smooth) streams the
+// individual patches' tile-packed inverses and applies the regular patches by fast
+// diagonalisation on the same SMs; off the tensor-Poisson case the regular patches use the
+// dense shared-type kernel (k_block_smooth) after the streaming launch.
 static int launch_block_smooth(fcm_mg* h, int q, const double* r, double* x, double coef, int part = 0) {
   LevelDev& Lv = h->lev[q];
   const bool do_irr = part != 2 && Lv.n_irr > 0, do_reg = part != 1 && Lv.n_reg > 0;
-  const bool fork = do_irr && do_reg;
-  if (fork) {
-    CU(cudaEventRecord(h->ev_fork, h->stream));
-    CU(cudaStreamWaitEvent(h->stream2, h->ev_fork, 0));
+  const bool fd = do_reg && Lv.fd;
+  PatchIrrOp io{};
+  io.nx = h->L.n[0]; io.ny = h->L.n[1]; io.nz = h->L.n[2];
+  for (int i = 0; i < 3; ++i) io.na[i] = Lv.na[i];
+  io.mb = Lv.mb; io.nt = Lv.nt; io.stride = Lv.pstride; io.n_irr = do_irr ? Lv.n_irr : 0;
+  io.anchors = Lv.irr_anchor; io.mem = Lv.d_mem; io.loc = Lv.d_loc;
+  for (int k = 0; k < 8; ++k)
+    for (int i = 0; i < 3; ++i) io.mo[k][i] = Lv.mo[k][i];
+  io.base = Lv.base; io.stride3 = Lv.stride; io.cmin = Lv.cmin; io.cmax = Lv.cmax; io.m = Lv.m;
+  io.inv = Lv.irr_inv; io.in = r; io.out = x; io.coef = coef;
+  PatchFdOp fo{};
+  fo.nx = h->L.n[0]; fo.ny = h->L.n[1]; fo.nz = h->L.n[2]; fo.dim = h->L.dim;
+  for (int i = 0; i < 3; ++i) fo.na[i] = Lv.na[i];
+  fo.q = q; fo.S = 2 * q + 1; fo.nreg = fd ? Lv.n_reg : 0; fo.anchors = Lv.reg_list; fo.blk = Lv.blk;
+  fo.cls = Lv.fd_cls; fo.tabs = Lv.fd_tabs; fo.ncls = Lv.fd ? Lv.fd_ncls : 0; fo.s_fac = Lv.fd_s;
+  fo.inv_alpha = 1.0 / h->alpha; fo.modeidx = Lv.fd_midx;
+  fo.base = Lv.base; fo.stride3 = Lv.stride; fo.cmin = Lv.cmin; fo.cmax = Lv.cmax; fo.m = Lv.m;
+  fo.in = r; fo.out = x; fo.coef = coef;
+  if (do_irr || fd) {
+    const void* k = patch_kernel(2 * q + 1, h->L.dim, do_irr, fd);
+    void* args[] = {&io, &fo};
+    CU(cudaLaunchKernel(k, dim3(h->num_sms), dim3((kIrrWarps + kFdWarps) * 32), args, patch_smem(h, q), h->stream));
+    h->count();
   }
-  if (do_irr) {
-    PatchIrrOp op{};
+  if (do_reg && !Lv.fd) {
+    BlockOp op{};
     op.nx = h->L.n[0]; op.ny = h->L.n[1]; op.nz = h->L.n[2];
     for (int i = 0; i < 3; ++i) op.na[i] = Lv.na[i];
-    op.mb = Lv.mb; op.nt = Lv.nt; op.stride = Lv.pstride; op.n_irr = Lv.n_irr;
-    op.anchors = Lv.irr_anchor; op.mem = Lv.d_mem; op.loc = Lv.d_loc;
+    op.nanchor = Lv.nanchor;
+    op.mb = Lv.mb;
+    op.nmem = Lv.nmem;
     for (int k = 0; k < 8; ++k)
       for (int i = 0; i < 3; ++i) op.mo[k][i] = Lv.mo[k][i];
-    op.base = Lv.base; op.stride3 = Lv.stride; op.cmin = Lv.cmin; op.cmax = Lv.cmax; op.m = Lv.m;
-    op.inv = Lv.irr_inv; op.in = r; op.out = x; op.coef = coef;
-    const int nb = (int)std::min<int64_t>(Lv.n_irr, h->num_sms);
-    k_patch_irr<<<nb, kIrrWarps * 32, irr_smem(Lv.nt), fork ? h->stream2 : h->stream>>>(op);
+    op.mem = Lv.d_mem; op.loc = Lv.d_loc;
+    op.m = Lv.m; op.base = Lv.base; op.stride = Lv.stride; op.cmin = Lv.cmin; op.cmax = Lv.cmax;
+    op.blk = Lv.blk; op.type_inv = Lv.type_inv; op.irr_inv = nullptr; op.inv_alpha = 1.0 / h->alpha;
+    op.in = r; op.out = x; op.coef = coef;
+    const int64_t wpb = kThreads / 32;
+    const int nb = (int)std::max<int64_t>(1, std::min<int64_t>((Lv.nanchor + wpb - 1) / wpb, (int64_t)h->num_sms * 8));
+    k_block_smooth<<<nb, kThreads, block_smem(Lv.m, Lv.mb), h->stream>>>(op);
     h->count();
-    CU(cudaGetLastError());
   }
-  if (do_reg) {
-    if (Lv.fd) {
-      PatchFdOp op{};
-      op.nx = h->L.n[0]; op.ny = h->L.n[1]; op.nz = h->L.n[2]; op.dim = h->L.dim;
-      for (int i = 0; i < 3; ++i) op.na[i] = Lv.na[i];
-      op.q = q; op.S = 2 * q + 1; op.nreg = Lv.n_reg; op.anchors = Lv.reg_list; op.blk = Lv.blk;
-      op.cls = Lv.fd_cls; op.tabs = Lv.fd_tabs; op.ncls = Lv.fd_ncls; op.s_fac = Lv.fd_s;
-      op.inv_alpha = 1.0 / h->alpha; op.modeidx = Lv.fd_midx;
-      op.base = Lv.base; op.stride3 = Lv.stride; op.cmin = Lv.cmin; op.cmax = Lv.cmax; op.m = Lv.m;
-      op.in = r; op.out = x; op.coef = coef;
-      const int nb = (int)std::max<int64_t>(1, std::min<int64_t>((Lv.n_reg + kFdWarps - 1) / kFdWarps, (int64_t)h->num_sms * 2));
-      const void* kfd = fd_kernel(2 * q + 1, h->L.dim);
-      void* args[] = {&op};
-      CU(cudaLaunchKernel(kfd, dim3(nb), dim3(kFdWarps * 32), args, fd_smem(h, q), h->stream));
-    } else {
-      BlockOp op{};
-      op.nx = h->L.n[0]; op.ny = h->L.n[1]; op.nz = h->L.n[2];
-      for (int i = 0; i < 3; ++i) op.na[i] = Lv.na[i];
-      op.nanchor = Lv.nanchor;
-      op.mb = Lv.mb;
-      op.nmem = Lv.nmem;
-      for (int k = 0; k < 8; ++k)
-        for (int i = 0; i < 3; ++i) op.mo[k][i] = Lv.mo[k][i];
-      op.mem = Lv.d_mem; op.loc = Lv.d_loc;
-      op.m = Lv.m; op.base = Lv.base; op.stride = Lv.stride; op.cmin = Lv.cmin; op.cmax = Lv.cmax;
-      op.blk = Lv.blk; op.type_inv = Lv.type_inv; op.irr_inv = nullptr; op.inv_alpha = 1.0 / h->alpha;
-      op.in = r; op.out = x; op.coef = coef;
-      const int64_t wpb = kThreads / 32;
-      const int nb = (int)std::max<int64_t>(1, std::min<int64_t>((Lv.nanchor + wpb - 1) / wpb, (int64_t)h->num_sms * 8));
-      k_block_smooth<<<nb, kThreads, block_smem(Lv.m, Lv.mb), h->stream>>>(op);
-    }
-    h->count();
-    CU(cudaGetLastError());
-  }
-  if (fork) {
-    CU(cudaEventRecord(h->ev_join, h->stream2));
-    CU(cudaStreamWaitEvent(h->stream, h->ev_join, 0));
-  }
+  CU(cudaGetLastError());
   return FCM_OK;
 }
 
@@ -1495,15 +1489,16 @@ static int setup_patch_fd(fcm_mg* h, int q, const double* K_ref_host) {
   return FCM_OK;
 }
 
-static size_t fd_smem(const fcm_mg* h, int q) {
+// k_patch_smooth's dynamic shared memory (layout in patch.cuh)
+static size_t patch_smem(const fcm_mg* h, int q) {
+  const LevelDev& Lv = h->lev[q];
   const int S = 2 * q + 1, S3 = h->L.dim == 3 ? S * S * S : S * S, nmi = (q + 1) * (q + 1) * (q + 1);
-  return sizeof(Tab) + (size_t)3 * h->lev[q].fd_ncls * (S * S + S) * 8 + ((nmi * 2 + 15) / 16) * 16 +
-         (size_t)kFdWarps * 2 * S3 * 8;
-}
-static size_t irr_smem(int nt) {
-  const size_t MPd = 32 * (size_t)nt;
-  return (MPd * 20 + 127) / 128 * 128 + (size_t)kIrrWarps * kIrrStages * 1024 * 8 +
-         (size_t)kIrrWarps * kIrrStages * 8 + sizeof(Tab);
+  const size_t MPd = 32 * (size_t)Lv.nt;
+  size_t o = (sizeof(Tab) + MPd * 20 + 127) / 128 * 128;
+  o += (size_t)kIrrWarps * kIrrStages * 1024 * 8 + (size_t)kIrrWarps * kIrrStages * 8;
+  o += (size_t)3 * (Lv.fd ? Lv.fd_ncls : 0) * (S * S + S) * 8 + ((nmi * 2 + 15) / 16) * 16;
+  o += (size_t)kFdWarps * 2 * S3 * 8;
+  return o;
 }
 
 // Assemble and invert the patch blocks of level q: shared types (full storage, type_inv) and
@@ -2370,9 +2365,9 @@ static int setup_impl(const fcm_grid* g, const fcm_params* prm, const fcm_slab* 
   for (int q = 2; q <= g->p; ++q)
     if (h->lev[q].patch) {
       RC(setup_patch_fd(h.get(), q, K_ref));
-      if (h->lev[q].fd) RC(allow_smem(fd_kernel(2 * q + 1, g->dim), fd_smem(h.get(), q)));
-      else RC(allow_smem((const void*)k_block_smooth, block_smem(h->lev[q].m, h->lev[q].mb)));
-      RC(allow_smem((const void*)k_patch_irr, irr_smem(h->lev[q].nt)));
+      if (!h->lev[q].fd) RC(allow_smem((const void*)k_block_smooth, block_smem(h->lev[q].m, h->lev[q].mb)));
+      for (int f = 0; f < 3; ++f)
+        RC(allow_smem(patch_kernel(2 * q + 1, g->dim, f != 2, f != 1), patch_smem(h.get(), q)));
     }
   RC(h->alloc(&h->d_coarse_iters, 2));
   CU(cudaMemsetAsync(h->d_coarse_iters, 0, 8, h->stream));

@@ -24,9 +24,9 @@
 namespace fcm {
 
 constexpr int kTileDiag = 528;    // 32*33/2
-constexpr int kIrrWarps = 8;      // warps per CTA of k_patch_irr
-constexpr int kIrrStages = 3;     // ring depth per warp
-constexpr int kFdWarps = 12;      // warps per CTA of k_patch_fd
+constexpr int kIrrWarps = 8;      // k_patch_smooth: warps streaming the individual patches
+constexpr int kIrrStages = 2;     // ring depth per streaming warp (8 KB stages)
+constexpr int kFdWarps = 4;       // k_patch_smooth: warps applying the regular patches
 constexpr int kFdMaxS = 9;        // 2q+1 <= 9 (q <= 4)
 
 __host__ __device__ constexpr int64_t tile_pack_size(int nt) {
@@ -277,35 +277,27 @@ __device__ __forceinline__ double warp_reduce_scatter32(double (&p)[32]) {
   return p[0];
 }
 
-// smem: [xs: 32 nt doubles][ys: 32 nt doubles][ids: 32 nt ints][per warp: kIrrStages x 1024
-// doubles][per warp: kIrrStages mbarriers]
-__global__ void __launch_bounds__(kIrrWarps * 32, 1) k_patch_irr(PatchIrrOp op) {
-  extern __shared__ __align__(16) unsigned char smem[];
+__device__ __forceinline__ void group_sync(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+// Individual patches, streamed: nw warps (index w) of the CTA, synchronised among themselves
+// with named barrier bar_id.  xs/ys/ids: 32 nt slots each; ring: nw x kIrrStages x 1024
+// doubles; bars: nw x kIrrStages mbarriers (initialised by the caller).
+__device__ __forceinline__ void irr_loop(const PatchIrrOp& op, const Tab& T, double* xs, double* ys, int* ids,
+                                         double* ring, uint64_t* bars_all, int w, int nw, int bar_id) {
+  const int lane = threadIdx.x & 31;
   const int MPd = 32 * op.nt;
-  double* xs = reinterpret_cast<double*>(smem);
-  double* ys = xs + MPd;
-  int* ids = reinterpret_cast<int*>(ys + MPd);
-  double* ring = reinterpret_cast<double*>(smem + ((size_t)MPd * 20 + 127) / 128 * 128);
-  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   double* myring = ring + (size_t)w * kIrrStages * 1024;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(ring + (size_t)kIrrWarps * kIrrStages * 1024) + w * kIrrStages;
-  Tab* Tp = reinterpret_cast<Tab*>(bars + (kIrrWarps - w) * kIrrStages);   // after all barriers
-  Tab& T = *Tp;
-  for (int a = threadIdx.x; a < op.m; a += blockDim.x) {
-    T.g[a] = make_int4((int32_t)op.base[a], op.stride3[a * 3 + 1], op.stride3[a * 3 + 2], 0);
-    T.lo[a] = make_int4(op.cmin[a * 3 + 0], op.cmin[a * 3 + 1], op.cmin[a * 3 + 2], 0);
-    T.hi[a] = make_int4(op.cmax[a * 3 + 0], op.cmax[a * 3 + 1], op.cmax[a * 3 + 2], 0);
-  }
-  if (lane == 0)
-    for (int s = 0; s < kIrrStages; ++s) mbar_init(&bars[s], 1);
-  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  __syncthreads();
+  uint64_t* bars = bars_all + w * kIrrStages;
+  const int nthr = nw * 32;
+  const int tid = w * 32 + lane;
   const int nt = op.nt;
   const int ntiles = nt * (nt + 1) / 2;
-  const int ntw = w < ntiles ? (ntiles - w + kIrrWarps - 1) / kIrrWarps : 0;   // tiles of this warp per patch
+  const int ntw = w < ntiles ? (ntiles - w + nw - 1) / nw : 0;   // tiles of this warp per patch
   const int64_t npatch = op.n_irr > blockIdx.x ? (op.n_irr - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
   const int64_t nitems = npatch * ntw;
-  // item i of this warp: patch k = i / ntw (block b = blockIdx.x + k gridDim.x), tile w + 8 (i % ntw)
+  // item i of this warp: patch k = i / ntw (block b = blockIdx.x + k gridDim.x), tile w + nw (i % ntw)
   auto tile_of = [&](int t, int& I, int& J) {
     I = (int)((sqrtf(8.0f * t + 1.0f) - 1.0f) * 0.5f);
     while (I * (I + 1) / 2 > t) --I;
@@ -314,7 +306,7 @@ __global__ void __launch_bounds__(kIrrWarps * 32, 1) k_patch_irr(PatchIrrOp op) 
   };
   auto issue = [&](int64_t i) {
     const int64_t k = i / ntw;
-    const int t = w + kIrrWarps * (int)(i % ntw);
+    const int t = w + nw * (int)(i % ntw);
     int I, J;
     tile_of(t, I, J);
     const int64_t b = blockIdx.x + k * gridDim.x;
@@ -331,7 +323,7 @@ __global__ void __launch_bounds__(kIrrWarps * 32, 1) k_patch_irr(PatchIrrOp op) 
     const int64_t b = blockIdx.x + k * gridDim.x;
     const int64_t A = op.anchors[b];
     const int ax = (int)(A % op.na[0]), ay = (int)((A / op.na[0]) % op.na[1]), az = (int)(A / ((int64_t)op.na[0] * op.na[1]));
-    for (int l = threadIdx.x; l < MPd; l += blockDim.x) {
+    for (int l = tid; l < MPd; l += nthr) {
       int idx = -1;
       if (l < op.mb) {
         const int km = op.mem[l], a = op.loc[l];
@@ -343,9 +335,9 @@ __global__ void __launch_bounds__(kIrrWarps * 32, 1) k_patch_irr(PatchIrrOp op) 
       xs[l] = idx >= 0 ? __ldg(op.in + idx) : 0.0;
       ys[l] = 0.0;
     }
-    __syncthreads();
+    group_sync(bar_id, nthr);
     for (int j = 0; j < ntw; ++j, ++item) {
-      const int t = w + kIrrWarps * j;
+      const int t = w + nw * j;
       int I, J;
       tile_of(t, I, J);
       const int s = (int)(item % kIrrStages);
@@ -376,14 +368,14 @@ __global__ void __launch_bounds__(kIrrWarps * 32, 1) k_patch_irr(PatchIrrOp op) 
       }
       const double yI = warp_reduce_scatter32(p);
       atomicAdd(&ys[32 * I + lane], yI);
-      if (I != J || true) atomicAdd(&ys[32 * J + lane], yJ);
+      atomicAdd(&ys[32 * J + lane], yJ);
     }
-    __syncthreads();
-    for (int l = threadIdx.x; l < op.mb; l += blockDim.x) {
+    group_sync(bar_id, nthr);
+    for (int l = tid; l < op.mb; l += nthr) {
       const int idx = ids[l];
       if (idx >= 0) atomicAdd(op.out + idx, op.coef * ys[l]);
     }
-    __syncthreads();
+    group_sync(bar_id, nthr);
   }
 }
 
@@ -420,36 +412,23 @@ __device__ __forceinline__ void fd_slot(int s, int q, int v, int n, int& cell, i
   else { cell = v; k = 1; }
 }
 
-// smem: [Tab][tables: 3*ncls*(S*S+S)][modeidx][per warp: X, Y (S^d doubles each)].
+// Regular patches by fast diagonalisation: nw warps (index w), independent (no CTA barrier).
 // Compile-time S (slots per axis) and DIM: every lane owns slots l = lane + 32 j, whose DOF
 // indices and gathered values live in registers (all NL loads in flight before the first use:
 // the gather is one memory latency per patch, not one per slot), and the same slots are
-// scattered at the end.
+// scattered at the end.  wbase: nw x 2 S^d doubles.
 template <int S, int DIM>
-__global__ void __launch_bounds__(kFdWarps * 32) k_patch_fd(PatchFdOp op) {
+__device__ __forceinline__ void fd_loop(const PatchFdOp& op, const Tab& T, const double* tab, const int16_t* midx,
+                                        double* wbase, int w, int nw) {
   constexpr int S2 = S * S, N3 = DIM == 3 ? S2 * S : S2;
   constexpr int NL = (N3 + 31) / 32;
   constexpr int tsz = S * S + S;
-  extern __shared__ __align__(16) unsigned char smem[];
-  Tab& T = *reinterpret_cast<Tab*>(smem);
-  double* tab = reinterpret_cast<double*>(smem + sizeof(Tab));
-  int16_t* midx = reinterpret_cast<int16_t*>(tab + 3 * op.ncls * tsz);
   const int q = op.q;
-  const int nmi = (q + 1) * (q + 1) * (q + 1);
-  double* wbase = reinterpret_cast<double*>(smem + sizeof(Tab) + (size_t)3 * op.ncls * tsz * 8 + ((nmi * 2 + 15) / 16) * 16);
-  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int lane = threadIdx.x & 31;
   double* X = wbase + (size_t)w * 2 * N3;
   double* Y = X + N3;
-  for (int a = threadIdx.x; a < op.m; a += blockDim.x) {
-    T.g[a] = make_int4((int32_t)op.base[a], op.stride3[a * 3 + 1], op.stride3[a * 3 + 2], 0);
-    T.lo[a] = make_int4(op.cmin[a * 3 + 0], op.cmin[a * 3 + 1], op.cmin[a * 3 + 2], 0);
-    T.hi[a] = make_int4(op.cmax[a * 3 + 0], op.cmax[a * 3 + 1], op.cmax[a * 3 + 2], 0);
-  }
-  for (int e = threadIdx.x; e < 3 * op.ncls * tsz; e += blockDim.x) tab[e] = op.tabs[e];
-  for (int e = threadIdx.x; e < nmi; e += blockDim.x) midx[e] = op.modeidx[e];
-  __syncthreads();
   const double coef = op.coef;
-  for (int64_t i = (int64_t)blockIdx.x * kFdWarps + w; i < op.nreg; i += (int64_t)gridDim.x * kFdWarps) {
+  for (int64_t i = (int64_t)blockIdx.x * nw + w; i < op.nreg; i += (int64_t)gridDim.x * nw) {
     const int A = op.anchors[i];
     const int vx = A % op.na[0], vy = (A / op.na[0]) % op.na[1], vz = A / (op.na[0] * op.na[1]);
     const int t = -op.blk[A] - 1;
@@ -568,6 +547,55 @@ __global__ void __launch_bounds__(kFdWarps * 32) k_patch_fd(PatchFdOp op) {
       if (ids[j] >= 0) atomicAdd(op.out + ids[j], coef * s);
     }
     __syncwarp();
+  }
+}
+
+__device__ __forceinline__ void load_tab_from(Tab& T, int m, const int64_t* base, const int32_t* stride3,
+                                              const int16_t* cmin, const int16_t* cmax) {
+  for (int a = threadIdx.x; a < m; a += blockDim.x) {
+    T.g[a] = make_int4((int32_t)base[a], stride3[a * 3 + 1], stride3[a * 3 + 2], 0);
+    T.lo[a] = make_int4(cmin[a * 3 + 0], cmin[a * 3 + 1], cmin[a * 3 + 2], 0);
+    T.hi[a] = make_int4(cmax[a * 3 + 0], cmax[a * 3 + 1], cmax[a * 3 + 2], 0);
+  }
+}
+
+// One patchwise smoother sweep in ONE launch, warp-specialised (one CTA per SM, persistent):
+// warps [0, kIrrWarps) stream the individual patches' tile-packed inverses (HBM-bound), warps
+// [kIrrWarps, kIrrWarps + kFdWarps) apply the regular patches by fast diagonalisation (latency
+// / FMA-bound) -- the two populations overlap on every SM instead of queueing behind each
+// other.  IRR / FD select the populations (fcm_mg_smooth_part).
+// smem: [Tab][xs, ys: 32 nt doubles][ids: 32 nt ints][ring: kIrrWarps x kIrrStages x 8 KB]
+//       [mbarriers][FD tables][modeidx][FD: kFdWarps x 2 S^d doubles]
+template <int S, int DIM, bool IRR, bool FD>
+__global__ void __launch_bounds__((kIrrWarps + kFdWarps) * 32, 1) k_patch_smooth(PatchIrrOp io, PatchFdOp fo) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  Tab& T = *reinterpret_cast<Tab*>(smem);
+  const int MPd = 32 * io.nt;
+  double* xs = reinterpret_cast<double*>(smem + sizeof(Tab));
+  double* ys = xs + MPd;
+  int* ids = reinterpret_cast<int*>(ys + MPd);
+  const size_t o_ring = (sizeof(Tab) + (size_t)MPd * 20 + 127) / 128 * 128;
+  double* ring = reinterpret_cast<double*>(smem + o_ring);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(ring + (size_t)kIrrWarps * kIrrStages * 1024);
+  constexpr int tsz = S * S + S;
+  double* tab = reinterpret_cast<double*>(bars + kIrrWarps * kIrrStages);
+  int16_t* midx = reinterpret_cast<int16_t*>(tab + 3 * fo.ncls * tsz);
+  const int nmi = (fo.q + 1) * (fo.q + 1) * (fo.q + 1);
+  double* wbase = reinterpret_cast<double*>(reinterpret_cast<unsigned char*>(midx) + ((nmi * 2 + 15) / 16) * 16);
+  const int w = threadIdx.x >> 5;
+  load_tab_from(T, io.m, io.base, io.stride3, io.cmin, io.cmax);
+  if (FD) {
+    for (int e = threadIdx.x; e < 3 * fo.ncls * tsz; e += blockDim.x) tab[e] = fo.tabs[e];
+    for (int e = threadIdx.x; e < nmi; e += blockDim.x) midx[e] = fo.modeidx[e];
+  }
+  if (IRR && w < kIrrWarps && (threadIdx.x & 31) == 0)
+    for (int s = 0; s < kIrrStages; ++s) mbar_init(&bars[w * kIrrStages + s], 1);
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  __syncthreads();
+  if (w < kIrrWarps) {
+    if (IRR) irr_loop(io, T, xs, ys, ids, ring, bars, w, kIrrWarps, 1);
+  } else {
+    if (FD) fd_loop<S, DIM>(fo, T, tab, midx, wbase, w - kIrrWarps, kFdWarps);
   }
 }
 
