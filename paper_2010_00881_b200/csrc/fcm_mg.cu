@@ -940,6 +940,14 @@ static size_t block_smem(int m, int mb) {
 // inverses (k_patch_irr, forked onto the second stream) while the regular patches run by fast
 // diagonalisation (k_patch_fd) or, off the tensor-Poisson case, the dense shared-type kernel
 static size_t patch_smem(const fcm_mg* h, int q);
+// streaming warps per patch: about 8+ tiles per warp (level 4: 276 tiles -> 8 warps on one patch;
+// level 3: 66 tiles -> 4; level 2: 10 tiles -> 1 warp per patch, 8 patches in flight per CTA)
+static int patch_wpp(int nt) {
+  const int ntiles = nt * (nt + 1) / 2;
+  int w = 1;
+  while (w < kIrrWarps && ntiles / (2 * w) > 8) w *= 2;
+  return w;
+}
 template <int S, int DIM>
 static const void* patch_kernel_s(int irr, int fd) {
   if (irr && fd) return (const void*)k_patch_smooth<S, DIM, true, true>;
@@ -964,6 +972,7 @@ static int launch_block_smooth(fcm_mg* h, int q, const double* r, double* x, dou
   io.nx = h->L.n[0]; io.ny = h->L.n[1]; io.nz = h->L.n[2];
   for (int i = 0; i < 3; ++i) io.na[i] = Lv.na[i];
   io.mb = Lv.mb; io.nt = Lv.nt; io.stride = Lv.pstride; io.n_irr = do_irr ? Lv.n_irr : 0;
+  io.wpp = patch_wpp(Lv.nt);
   io.anchors = Lv.irr_anchor; io.mem = Lv.d_mem; io.loc = Lv.d_loc;
   for (int k = 0; k < 8; ++k)
     for (int i = 0; i < 3; ++i) io.mo[k][i] = Lv.mo[k][i];
@@ -1494,7 +1503,7 @@ static size_t patch_smem(const fcm_mg* h, int q) {
   const LevelDev& Lv = h->lev[q];
   const int S = 2 * q + 1, S3 = h->L.dim == 3 ? S * S * S : S * S, nmi = (q + 1) * (q + 1) * (q + 1);
   const size_t MPd = 32 * (size_t)Lv.nt;
-  size_t o = (sizeof(Tab) + MPd * 20 + 127) / 128 * 128;
+  size_t o = (sizeof(Tab) + (size_t)(kIrrWarps / patch_wpp(Lv.nt)) * MPd * 20 + 127) / 128 * 128;
   o += (size_t)kIrrWarps * kIrrStages * 1024 * 8 + (size_t)kIrrWarps * kIrrStages * 8;
   o += (size_t)3 * (Lv.fd ? Lv.fd_ncls : 0) * (S * S + S) * 8 + ((nmi * 2 + 15) / 16) * 16;
   o += (size_t)kFdWarps * 2 * S3 * 8;

@@ -224,6 +224,7 @@ struct PatchIrrOp {
   int nx, ny, nz;
   int na[3];
   int mb, nt;                 // block slots, tiles per dim (32 nt >= mb)
+  int wpp;                    // streaming warps per patch (kIrrWarps / wpp patches in flight per CTA)
   int64_t stride;             // doubles per packed inverse
   int64_t n_irr;
   const int64_t* anchors;     // [n_irr] anchor of individual block i
@@ -285,17 +286,18 @@ __device__ __forceinline__ void group_sync(int id, int nthreads) {
 // with named barrier bar_id.  xs/ys/ids: 32 nt slots each; ring: nw x kIrrStages x 1024
 // doubles; bars: nw x kIrrStages mbarriers (initialised by the caller).
 __device__ __forceinline__ void irr_loop(const PatchIrrOp& op, const Tab& T, double* xs, double* ys, int* ids,
-                                         double* ring, uint64_t* bars_all, int w, int nw, int bar_id) {
+                                         double* ring, uint64_t* bars_all, int w, int nw, int bar_id,
+                                         int64_t p0, int64_t pstep, int wring) {
   const int lane = threadIdx.x & 31;
   const int MPd = 32 * op.nt;
-  double* myring = ring + (size_t)w * kIrrStages * 1024;
-  uint64_t* bars = bars_all + w * kIrrStages;
+  double* myring = ring + (size_t)wring * kIrrStages * 1024;
+  uint64_t* bars = bars_all + wring * kIrrStages;
   const int nthr = nw * 32;
   const int tid = w * 32 + lane;
   const int nt = op.nt;
   const int ntiles = nt * (nt + 1) / 2;
   const int ntw = w < ntiles ? (ntiles - w + nw - 1) / nw : 0;   // tiles of this warp per patch
-  const int64_t npatch = op.n_irr > blockIdx.x ? (op.n_irr - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+  const int64_t npatch = op.n_irr > p0 ? (op.n_irr - p0 + pstep - 1) / pstep : 0;
   const int64_t nitems = npatch * ntw;
   // item i of this warp: patch k = i / ntw (block b = blockIdx.x + k gridDim.x), tile w + nw (i % ntw)
   auto tile_of = [&](int t, int& I, int& J) {
@@ -309,7 +311,7 @@ __device__ __forceinline__ void irr_loop(const PatchIrrOp& op, const Tab& T, dou
     const int t = w + nw * (int)(i % ntw);
     int I, J;
     tile_of(t, I, J);
-    const int64_t b = blockIdx.x + k * gridDim.x;
+    const int64_t b = p0 + k * pstep;
     const double* src = op.inv + b * op.stride + tile_off(I, J);
     const uint32_t bytes = (I == J ? kTileDiag : 1024) * 8;
     const int s = (int)(i % kIrrStages);
@@ -320,7 +322,7 @@ __device__ __forceinline__ void irr_loop(const PatchIrrOp& op, const Tab& T, dou
     for (int64_t i = 0; i < kIrrStages && i < nitems; ++i) issue(i);
   int64_t item = 0;
   for (int64_t k = 0; k < npatch; ++k) {
-    const int64_t b = blockIdx.x + k * gridDim.x;
+    const int64_t b = p0 + k * pstep;
     const int64_t A = op.anchors[b];
     const int ax = (int)(A % op.na[0]), ay = (int)((A / op.na[0]) % op.na[1]), az = (int)(A / ((int64_t)op.na[0] * op.na[1]));
     for (int l = tid; l < MPd; l += nthr) {
@@ -571,10 +573,9 @@ __global__ void __launch_bounds__((kIrrWarps + kFdWarps) * 32, 1) k_patch_smooth
   extern __shared__ __align__(16) unsigned char smem[];
   Tab& T = *reinterpret_cast<Tab*>(smem);
   const int MPd = 32 * io.nt;
-  double* xs = reinterpret_cast<double*>(smem + sizeof(Tab));
-  double* ys = xs + MPd;
-  int* ids = reinterpret_cast<int*>(ys + MPd);
-  const size_t o_ring = (sizeof(Tab) + (size_t)MPd * 20 + 127) / 128 * 128;
+  const int ngrp = kIrrWarps / io.wpp;   // patches in flight per CTA
+  double* xs0 = reinterpret_cast<double*>(smem + sizeof(Tab));
+  const size_t o_ring = (sizeof(Tab) + (size_t)ngrp * MPd * 20 + 127) / 128 * 128;
   double* ring = reinterpret_cast<double*>(smem + o_ring);
   uint64_t* bars = reinterpret_cast<uint64_t*>(ring + (size_t)kIrrWarps * kIrrStages * 1024);
   constexpr int tsz = S * S + S;
@@ -593,7 +594,14 @@ __global__ void __launch_bounds__((kIrrWarps + kFdWarps) * 32, 1) k_patch_smooth
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   __syncthreads();
   if (w < kIrrWarps) {
-    if (IRR) irr_loop(io, T, xs, ys, ids, ring, bars, w, kIrrWarps, 1);
+    if (IRR) {
+      const int g = w / io.wpp;
+      double* xs = xs0 + (size_t)g * MPd * 2;
+      double* ys = xs + MPd;
+      int* ids = reinterpret_cast<int*>(xs0 + (size_t)ngrp * MPd * 2) + (size_t)g * MPd;
+      irr_loop(io, T, xs, ys, ids, ring, bars, w % io.wpp, io.wpp, 1 + g, (int64_t)blockIdx.x * ngrp + g,
+               (int64_t)gridDim.x * ngrp, w);
+    }
   } else {
     if (FD) fd_loop<S, DIM>(fo, T, tab, midx, wbase, w - kIrrWarps, kFdWarps);
   }
