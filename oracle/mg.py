@@ -21,7 +21,9 @@ before every smoothing sweep, P:124-126 fixed-point smoothing), x~ = 0 on
 entry, n_s pre and post sweeps.
 Coarse level: 'direct' dense LU; 'as_pcg' CG with the
 undamped elementwise AS preconditioner at p = 1, x0 = 0, stop at
-||r|| < rtol ||r0|| (reading R4); 'jacobi_pcg' the same with diag(A0).
+||r|| < rtol ||r0|| (reading R4); 'jacobi_pcg' the same with diag(A0); 'gmg_pcg'
+the same CG preconditioned by one geometric V-cycle over h-coarsened p=1 grids
+(P:227 Remark, class GeometricLevels, reading R21).
 Outer solver: flexible (Polak-Ribiere) PCG, x0 = 0, stop at the recursive
 ||r_k||_2 / ||b||_2 < rtol (readings R5, R6).
 """
@@ -29,6 +31,7 @@ from __future__ import annotations
 
 import numpy as np
 import scipy.linalg as sla
+import scipy.sparse as sp
 
 
 class Level:
@@ -104,6 +107,111 @@ class Level:
         return np.bincount(idx, weights=vals, minlength=self.n)
 
 
+def _vertex_dofs(n, dim, n_f, dmask):
+    """Free p=1 DOFs of a vertex grid with n cells per axis, Dirichlet faces removed (R7), in
+    the oracle's order (z, y, x slowest to fastest, then component).  Returns [N, dim+1]
+    (positions per axis, component)."""
+    import itertools
+    out = []
+    rng = []
+    for a in range(dim):
+        lo = 1 if (dmask >> (2 * a)) & 1 else 0
+        hi = n - 1 if (dmask >> (2 * a + 1)) & 1 else n
+        rng.append(range(lo, hi + 1))
+    for pos in itertools.product(*reversed(rng)):
+        pos = tuple(reversed(pos))
+        for c in range(n_f):
+            out.append(pos + (c,))
+    return np.array(out, dtype=np.int64).reshape(-1, dim + 1)
+
+
+class GeometricLevels:
+    """h-coarsening of the p=1 level (PAPER.md:227 Remark: "the p=1, k=0 problem can be
+    coarsened further using a standard geometric multigrid algorithm"), reading R21 of
+    DESIGN.md: vertex grids n, n/2, n/4, ... (coarsen while n is even and n > 4), standard
+    (bi/tri)linear interpolation P between nested vertex grids restricted to the free DOFs,
+    Galerkin operators A_{i+1} = P^T A_i P (P:118's R A R^T with R = P^T), elementwise additive
+    Schwarz on every level (blocks = the free DOFs of one cell of that level's grid, assembled
+    A_i sub-blocks, dense inverses, omega of P:300), V(n_pre, n_post) cycles of Algorithm 1's
+    form (R1), LU on the coarsest grid.  Level 0 is the p=1 level itself (its matrix A_1 and its
+    elementwise blocks come from the caller)."""
+
+    def __init__(self, cfg, A1, keys1, blocks0, inv0, omega, n_pre, n_post):
+        d, n_f, p = cfg.dim, cfg.n_f, cfg.p
+        per = (p + 1) ** 3 * n_f
+        ent = keys1 // per
+        comp = keys1 % n_f
+        X = [(ent // (2 * cfg.n + 1) ** a) % (2 * cfg.n + 1) for a in range(d)]
+        assert all(np.all(x % 2 == 0) for x in X), "level-1 DOFs are vertex DOFs"
+        self.pos = [np.stack([x // 2 for x in X] + [comp], axis=1)]
+        self.A = [A1.tocsr()]
+        self.blocks = [blocks0]
+        self.inv = [inv0]
+        self.P = []
+        self.n = [cfg.n]
+        self.omega, self.n_pre, self.n_post = omega, n_pre, n_post
+        n = cfg.n
+        while n % 2 == 0 and n > 4:
+            nc = n // 2
+            cpos = _vertex_dofs(nc, d, n_f, cfg.dirichlet_mask)
+            index = {tuple(r): i for i, r in enumerate(cpos.tolist())}
+            rows, cols, vals = [], [], []
+            for i, r in enumerate(self.pos[-1].tolist()):
+                par = [[(r[a] // 2, 1.0)] if r[a] % 2 == 0 else [((r[a] - 1) // 2, 0.5), ((r[a] + 1) // 2, 0.5)]
+                       for a in range(d)]
+                import itertools
+                for combo in itertools.product(*par):
+                    key = tuple(c[0] for c in combo) + (r[d],)
+                    j = index.get(key)
+                    if j is not None:
+                        rows.append(i)
+                        cols.append(j)
+                        vals.append(float(np.prod([c[1] for c in combo])))
+            P = sp.csr_matrix((vals, (rows, cols)), shape=(len(self.pos[-1]), len(cpos)))
+            Ac = (P.T @ self.A[-1] @ P).tocsr()
+            # elementwise blocks of the coarse grid: the free DOFs of each cell
+            blocks = []
+            for cell in range(nc ** d):
+                cc = [(cell // nc ** a) % nc for a in range(d)]
+                ids = []
+                for corner in range(1 << d):
+                    v = tuple(cc[a] + ((corner >> a) & 1) for a in range(d))
+                    for c in range(n_f):
+                        j = index.get(v + (c,))
+                        if j is not None:
+                            ids.append(j)
+                if ids:
+                    blocks.append(np.array(sorted(ids), dtype=np.int64))
+            inv = [np.linalg.inv(Ac[b][:, b].toarray()) for b in blocks]
+            self.P.append(P)
+            self.A.append(Ac)
+            self.blocks.append(blocks)
+            self.inv.append(inv)
+            self.pos.append(cpos)
+            self.n.append(nc)
+            n = nc
+        self.lu = sla.lu_factor(self.A[-1].toarray())
+
+    def _schwarz(self, i, r):
+        idx = np.concatenate(self.blocks[i])
+        vals = np.concatenate([self.inv[i][k] @ r[b] for k, b in enumerate(self.blocks[i])])
+        return np.bincount(idx, weights=vals, minlength=self.A[i].shape[0])
+
+    def vcycle(self, b, i=0):
+        """Geometric V-cycle on h-level i (x = 0 on entry; residual before every sweep, R1)."""
+        if i == len(self.A) - 1:
+            return sla.lu_solve(self.lu, b)
+        A, w = self.A[i], self.omega
+        x = np.zeros_like(b)
+        for _ in range(self.n_pre):
+            x = x + w * self._schwarz(i, b - A @ x)
+        r = b - A @ x
+        x = x + self.P[i] @ self.vcycle(self.P[i].T @ r, i + 1)
+        for _ in range(self.n_post):
+            x = x + w * self._schwarz(i, b - A @ x)
+        return x
+
+
 class Hierarchy:
     def __init__(self, prob, block=None, omega=None, n_pre=None, n_post=None, coarse=None,
                  coarse_rtol=None, coarse_maxit=None, inv="lu", patch_rule="closure"):
@@ -122,7 +230,7 @@ class Hierarchy:
         self.levels = {}
         for q in range(cfg.p, 0, -1):
             blk = self.block if q > 1 else "element"   # coarse AS is elementwise (R11)
-            need_blocks = q > 1 or self.coarse == "as_pcg"
+            need_blocks = q > 1 or self.coarse in ("as_pcg", "gmg_pcg")
             if need_blocks:
                 self.levels[q] = Level(prob, q, blk, A, self.omega if q > 1 else 1.0, inv_method=inv,
                                        patch_rule=patch_rule)
@@ -142,6 +250,11 @@ class Hierarchy:
             self.lu = sla.lu_factor(c.A.toarray())
         elif self.coarse == "jacobi_pcg":
             self.diag = c.A.diagonal()
+        elif self.coarse == "gmg_pcg":
+            # the level-1 smoother of the h-hierarchy uses the ELEMENTWISE omega (R21)
+            w_el = cfg.replace(block="element", omega=None).omega_value
+            self.gmg = GeometricLevels(cfg, c.A, prob.dof.keys[c.idx], c.blocks, c.inv, w_el,
+                                       self.n_pre, self.n_post)
         self.coarse_iters = []
 
     def set_coarse_inverse(self, inv):
@@ -156,7 +269,12 @@ class Hierarchy:
             if getattr(self, "coarse_inv", None) is not None:
                 return self.coarse_inv @ b
             return sla.lu_solve(self.lu, b)
-        prec = lv.schwarz if self.coarse == "as_pcg" else (lambda r: r / self.diag)
+        if self.coarse == "gmg_pcg":
+            prec = self.gmg.vcycle
+        elif self.coarse == "as_pcg":
+            prec = lv.schwarz
+        else:
+            prec = lambda r: r / self.diag  # noqa: E731
         x, it = pcg(lambda v: lv.A @ v, b, prec, self.coarse_rtol, self.coarse_maxit,
                     rel_to="r0")
         self.coarse_iters.append(it)

@@ -371,3 +371,73 @@ def test_patch_membership_matches_key_enumeration(dim, n, p):
                 assert len(g) == (2 * q + 1) ** dim
         assert blocks == ref, q
         assert max(len(b) for b in lv.blocks) <= (2 * q + 1) ** dim
+
+
+# ---- h-coarsening below p = 1 (PAPER.md:227 Remark; reading R21) ---------------------------
+def _p1_levels(n, dim=3, voids=None, **kw):
+    from oracle.mg import GeometricLevels
+    cfg = small_config(dim, n, 1, voids=voids, coarse="direct", **kw)
+    P = Problem(cfg)
+    H = Hierarchy(P, coarse="as_pcg")
+    lv = H.levels[1]
+    G = GeometricLevels(cfg, lv.A, P.dof.keys[lv.idx], lv.blocks, lv.inv, 2.0 / 15.0 if dim == 3 else 1.0 / 3.0,
+                        5, 5)
+    return cfg, P, G
+
+
+@pytest.mark.parametrize("dim", [2, 3])
+def test_gmg_prolongation_reproduces_multilinear_functions(dim):
+    # standard (bi/tri)linear interpolation: P maps any multilinear function sampled on the
+    # coarse vertices to the same function on the fine vertices (no Dirichlet elimination here)
+    _, _, G = _p1_levels(8, dim, dirichlet=0)
+    rng = np.random.default_rng(3)
+    c = rng.standard_normal(1 << dim)
+    def f(pos, n):
+        x = pos[:, :dim] / n
+        out = np.zeros(len(pos))
+        for m in range(1 << dim):
+            t = np.ones(len(pos))
+            for a in range(dim):
+                if (m >> a) & 1:
+                    t = t * x[:, a]
+            out += c[m] * t
+        return out
+    fc = f(G.pos[1], G.n[1])
+    ff = f(G.pos[0], G.n[0])
+    assert np.abs(G.P[0] @ fc - ff).max() < 1e-13
+    # each fine vertex's weights sum to 1 (partition of unity)
+    assert np.allclose(np.asarray(G.P[0].sum(axis=1)).ravel(), 1.0, atol=1e-15)
+
+
+@pytest.mark.parametrize("dim", [2, 3])
+def test_gmg_galerkin_equals_rediscretisation(dim):
+    # on a void-free box the Galerkin operator P^T A_h P of nested (bi/tri)linear spaces is the
+    # operator rediscretised on the coarse grid (independent assembly by the oracle's Problem)
+    cfg, P, G = _p1_levels(8, dim)
+    coarse = Problem(small_config(dim, 4, 1, coarse="direct"))
+    assert np.array_equal(G.pos[1][:, :dim] * 2, np.stack(
+        [((coarse.dof.keys // 8) // (9 ** a)) % 9 for a in range(dim)], 1))
+    assert abs(G.A[1] - coarse.A).max() < 1e-13 * abs(coarse.A).max()
+
+
+def test_gmg_vcycle_symmetric_and_pcg_exact():
+    cfg, P, G = _p1_levels(8, 3, voids=2, seed=4)
+    rng = np.random.default_rng(5)
+    r1, r2 = rng.standard_normal((2, G.A[0].shape[0]))
+    assert abs(r2 @ G.vcycle(r1) - r1 @ G.vcycle(r2)) < 1e-10 * abs(r1 @ G.vcycle(r1))
+    x, it = pcg(lambda v: G.A[0] @ v, r1, G.vcycle, 1e-12, 100, rel_to="r0")
+    xs = spla.spsolve(G.A[0].tocsc(), r1)
+    assert np.linalg.norm(x - xs) <= 1e-9 * np.linalg.norm(xs) and it <= 15
+
+
+def test_gmg_coarse_iterations_h_independent():
+    # the geometric V-cycle makes the p=1 solve's iteration count nearly h-independent
+    # (CG + elementwise AS alone grows like 1/h)
+    its = []
+    for n in (8, 16):
+        P = Problem(small_config(3, n, 2, coarse="gmg_pcg"))
+        H = Hierarchy(P)
+        I1 = P.dof.level_dofs(1)
+        H.coarse_solve(P.b[I1])
+        its.append(H.coarse_iters[-1])
+    assert its[1] <= its[0] + 2 and its[1] <= 10, its
