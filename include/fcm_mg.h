@@ -75,6 +75,10 @@ extern "C" {
 #define FCM_COARSE_DIRECT 0   /* dense direct solve of the p=1 level         */
 #define FCM_COARSE_AS_PCG 1   /* CG + undamped elementwise AS at p=1         */
 #define FCM_COARSE_JACOBI_PCG 2 /* CG + diagonal preconditioner (BASELINE.json variant)     */
+#define FCM_COARSE_GMG_PCG 3  /* CG preconditioned by a geometric V-cycle over h-coarsened
+                                 p=1 grids (PAPER.md:227 Remark; R21): trilinear P,
+                                 Galerkin P^T A P element by element, elementwise AS on every
+                                 h-level, dense solve on the coarsest grid (single GPU)     */
 #define FCM_PHYS_POISSON 0
 #define FCM_PHYS_ELASTICITY 1
 
@@ -304,6 +308,7 @@ int fcm_mg_stats(const fcm_mg* h, int64_t* coarse_iters_total, int64_t* vcycles)
 #define FCM_COARSE_KERNEL_DIRECT 0
 #define FCM_COARSE_KERNEL_GRID 1
 #define FCM_COARSE_KERNEL_TILED 2
+#define FCM_COARSE_KERNEL_GMG 3   /* CG + geometric V-cycle (nested graph loop); blocks = h-levels */
 int fcm_mg_coarse_info(const fcm_mg* h, int32_t* kind, int32_t* blocks, int32_t* tile);
 
 /* Counters of kernels launched by the library since setup (for the bench's gpu_launches). */

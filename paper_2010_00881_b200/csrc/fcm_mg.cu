@@ -65,6 +65,13 @@ namespace {
 constexpr int kThreads = 256;
 constexpr int kMaxPartials = 2048;
 
+// coarse CG preconditioned by the geometric V-cycle (FCM_COARSE_GMG_PCG): device scalars
+struct GcgScalars {
+  double rz, rz_new, rr0, rr, pq;
+  int it, maxit, flag, pad;
+  double rtol2;
+};
+
 struct Scalars {
   double rz, pq, rr, zr, zr_old, bb;
   int flag;  // bit0: p^T A p <= 0
@@ -211,6 +218,19 @@ struct fcm_mg {
   double* c_send = nullptr;
   double* c_recv = nullptr;         // [nranks][c_max]
   int64_t* c_unpack = nullptr;      // [nranks * c_max] global level-1 slot (-1 padding)
+  // h-coarsening below p = 1 (FCM_COARSE_GMG_PCG, PAPER.md:227 Remark): child handles of the
+  // p=1 problem on grids n/2, n/4, ... (their level 1 = the h-level; the last one solves
+  // directly); per h-level right-hand side / solution buffers; the coarse CG scalars
+  std::vector<fcm_mg*> gmg;         // h-levels 1..L
+  std::vector<double*> gmg_b, gmg_x;   // [L + 1] (index 0 unused: the coarse CG's r / z)
+  double gmg_omega = 1.0;
+  GcgScalars* gcg = nullptr;
+  cudaStream_t st_c[2] = {nullptr, nullptr};   // capture streams of the nested conditional bodies
+  cudaGraphExec_t g_coarse = nullptr;          // stand-alone coarse solve (fcm_mg_coarse_solve)
+  double *c_bst = nullptr, *c_xst = nullptr;   // its staged input / output
+  int64_t n_gcg_body = 0;                      // kernels per coarse CG trip (launch accounting)
+  int64_t n_coarse_g = 0;
+  bool gmg_child = false;
   int64_t* c_extract = nullptr;     // [ndof_1 local] global level-1 slot
   double* c_bg = nullptr;
   double* c_xg = nullptr;
@@ -245,6 +265,10 @@ struct fcm_mg {
 };
 fcm_mg::~fcm_mg() {
   if (hg) delete hg;
+  for (fcm_mg* c : gmg) delete c;
+  if (g_coarse) cudaGraphExecDestroy(g_coarse);
+  for (auto st : st_c)
+    if (st) cudaStreamDestroy(st);
   if (comm && nccl().ok) nccl().CommDestroy(comm);
   release();
 }
@@ -531,6 +555,127 @@ __global__ void k_dense_gemv(const double* __restrict__ A, const double* __restr
     for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
     if (lane == 0) x[row] = s;
   }
+}
+
+// ---- h-coarsening below p = 1 (FCM_COARSE_GMG_PCG; PAPER.md:227 Remark, reading R21) ----------
+// free vertex boxes of a p = 1 level: one class per component, x fastest (layout.hpp)
+struct GmgBox {
+  int nf;
+  int64_t off[3];
+  int lo[3][3], size[3][3];
+};
+__device__ __forceinline__ int64_t gmg_index(const GmgBox& B, int c, const int x[3]) {
+  return B.off[c] + (x[0] - B.lo[c][0]) + ((int64_t)(x[1] - B.lo[c][1]) + (int64_t)(x[2] - B.lo[c][2]) * B.size[c][1]) * B.size[c][0];
+}
+__device__ __forceinline__ bool gmg_in(const GmgBox& B, int c, const int x[3]) {
+  return x[0] >= B.lo[c][0] && x[0] < B.lo[c][0] + B.size[c][0] && x[1] >= B.lo[c][1] &&
+         x[1] < B.lo[c][1] + B.size[c][1] && x[2] >= B.lo[c][2] && x[2] < B.lo[c][2] + B.size[c][2];
+}
+__device__ __forceinline__ void gmg_decode(const GmgBox& B, int64_t i, int& c, int x[3]) {
+  c = 0;
+  while (c + 1 < B.nf && i >= B.off[c + 1]) ++c;
+  int64_t t = i - B.off[c];
+  x[0] = (int)(t % B.size[c][0]) + B.lo[c][0];
+  t /= B.size[c][0];
+  x[1] = (int)(t % B.size[c][1]) + B.lo[c][1];
+  x[2] = (int)(t / B.size[c][1]) + B.lo[c][2];
+}
+// b_coarse = P^T r_fine: each coarse vertex gathers its 3^d fine neighbours with the (bi/tri)linear
+// weights prod_a (1 - |d_a| / 2) (deterministic, no atomics)
+__global__ void k_gmg_restrict(double* __restrict__ bc, const double* __restrict__ rf, GmgBox C, GmgBox F, int dim,
+                               int64_t nc) {
+  FCM_PDL_ENTRY();
+  for (int64_t J = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; J < nc; J += (int64_t)gridDim.x * blockDim.x) {
+    int c, X[3];
+    gmg_decode(C, J, c, X);
+    double s = 0.0;
+    const int dz0 = dim == 3 ? -1 : 0, dz1 = dim == 3 ? 1 : 0;
+    for (int dz = dz0; dz <= dz1; ++dz)
+      for (int dy = -1; dy <= 1; ++dy)
+        for (int dx = -1; dx <= 1; ++dx) {
+          const int x[3] = {2 * X[0] + dx, 2 * X[1] + dy, 2 * X[2] + dz};
+          if (!gmg_in(F, c, x)) continue;
+          const double w = (dx ? 0.5 : 1.0) * (dy ? 0.5 : 1.0) * (dz ? 0.5 : 1.0);
+          s = fma(w, rf[gmg_index(F, c, x)], s);
+        }
+    bc[J] = s;
+  }
+}
+// x_fine += P e_coarse: each fine vertex gathers its 1, 2, 4 or 8 coarse parents
+__global__ void k_gmg_prolong(double* __restrict__ xf, const double* __restrict__ ec, GmgBox F, GmgBox C, int dim,
+                              int64_t nfine) {
+  FCM_PDL_ENTRY();
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nfine; i += (int64_t)gridDim.x * blockDim.x) {
+    int c, x[3];
+    gmg_decode(F, i, c, x);
+    double s = 0.0;
+    const int nz = (dim == 3 && (x[2] & 1)) ? 2 : 1, ny = (x[1] & 1) ? 2 : 1, nx = (x[0] & 1) ? 2 : 1;
+    for (int kz = 0; kz < nz; ++kz)
+      for (int ky = 0; ky < ny; ++ky)
+        for (int kx = 0; kx < nx; ++kx) {
+          const int X[3] = {(x[0] - (nx - 1)) / 2 + kx, (x[1] - (ny - 1)) / 2 + ky, (x[2] - (nz - 1)) / 2 + kz};
+          if (!gmg_in(C, c, X)) continue;
+          s = fma((nx == 2 ? 0.5 : 1.0) * (ny == 2 ? 0.5 : 1.0) * (nz == 2 ? 0.5 : 1.0), ec[gmg_index(C, c, X)], s);
+        }
+    xf[i] += s;
+  }
+}
+// coarse CG (standard PCG, P:343 form) around the geometric V-cycle; the loop is a device-side
+// WHILE node, the V-cycle + beta part an IF node inside it (both set by k_gcg_check)
+__global__ void k_gcg_init(GcgScalars* s, const double* pA, const double* pB, int np, double* p, const double* z,
+                           int64_t n, cudaGraphConditionalHandle cw) {
+  const double rz = sum_partials(pA, np), rr = sum_partials(pB, np);
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    s->rz = rz; s->rr0 = rr; s->rr = rr; s->it = 0; s->flag = 0;
+    cudaGraphSetConditional(cw, (rr > 0.0 && s->maxit > 0) ? 1u : 0u);
+  }
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) p[i] = z[i];
+}
+__global__ void k_gcg_update(GcgScalars* s, const double* ppq, int npq, double* __restrict__ x, double* __restrict__ r,
+                             const double* __restrict__ p, const double* __restrict__ q, int64_t n, double* prr) {
+  FCM_PDL_ENTRY();
+  __shared__ double red[32];
+  const double pq = sum_partials(ppq, npq);
+  const double a = s->rz / pq;
+  double rr = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    x[i] = fma(a, p[i], x[i]);
+    const double rn = fma(-a, q[i], r[i]);
+    r[i] = rn;
+    rr = fma(rn, rn, rr);
+  }
+  rr = block_sum(rr, red);
+  if (threadIdx.x == 0) prr[blockIdx.x] = rr;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    s->pq = pq;
+    if (!(pq > 0.0)) s->flag = 1;
+  }
+}
+__global__ void k_gcg_check(GcgScalars* s, const double* prr, int np, cudaGraphConditionalHandle cw,
+                            cudaGraphConditionalHandle ci, int* iters) {
+  FCM_PDL_ENTRY();
+  const double rr = sum_partials(prr, np);
+  if (threadIdx.x == 0) {
+    s->rr = rr;
+    const int it = ++s->it;
+    const bool stop = s->flag || !(rr == rr) || rr < s->rtol2 * s->rr0 || it >= s->maxit;
+    cudaGraphSetConditional(cw, stop ? 0u : 1u);
+    cudaGraphSetConditional(ci, stop ? 0u : 1u);
+    if (stop) { iters[0] = it; iters[1] += it; }
+  }
+}
+__global__ void k_gcg_update2(GcgScalars* s, const double* prz, int np, double* __restrict__ p,
+                              const double* __restrict__ z, int64_t n) {
+  FCM_PDL_ENTRY();
+  const double rzn = sum_partials(prz, np);
+  const double beta = rzn / s->rz;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = fma(beta, p[i], z[i]);
+  if (blockIdx.x == 0 && threadIdx.x == 0) s->rz_new = rzn;
+}
+__global__ void k_gcg_setrz(GcgScalars* s) {
+  FCM_PDL_ENTRY();
+  if (threadIdx.x == 0) s->rz = s->rz_new;
 }
 
 // Inversion of SPD blocks: Cholesky A = L L^T (right-looking, L in shared memory), then
@@ -1069,8 +1214,10 @@ static int enqueue_coarse_slab(fcm_mg* h, const double* b, double* x) {
   return FCM_OK;
 }
 
+static int enqueue_coarse_gmg(fcm_mg* h, const double* b, double* x);
 static int enqueue_coarse(fcm_mg* h, const double* b, double* x) {
   if (h->hg) return enqueue_coarse_slab(h, b, x);
+  if (h->prm.coarse == FCM_COARSE_GMG_PCG) return enqueue_coarse_gmg(h, b, x);
   LevelDev& L1 = h->lev[1];
   const int64_t n = L1.ndof;
   if (h->prm.coarse == FCM_COARSE_DIRECT) {
@@ -1150,6 +1297,310 @@ static int enqueue_coarse(fcm_mg* h, const double* b, double* x) {
   return FCM_OK;
 }
 
+
+// ---- h-coarsening below p = 1 (FCM_COARSE_GMG_PCG): host side ------------------------------
+static int dot_blocks(fcm_mg* h);
+static GmgBox gmg_box(const Layout& L) {
+  GmgBox B{};
+  B.nf = L.n_f;
+  for (int c = 0; c < L.n_f; ++c) {   // level-1 classes: the vertex class of each component first
+    const DofClass& dc = L.classes[c];
+    B.off[c] = dc.off;
+    for (int a = 0; a < 3; ++a) { B.lo[c][a] = dc.lo[a]; B.size[c][a] = std::max(1, dc.size[a]); }
+  }
+  return B;
+}
+static void set_stream(fcm_mg* h, cudaStream_t st) {
+  h->stream = st;
+  for (fcm_mg* c : h->gmg) c->stream = st;
+}
+// Add a conditional node (WHILE / IF) on `cond` to the graph being captured on h->stream and
+// capture its body -- body() enqueued with h and its h-level children switched to `sub`.
+template <typename F>
+static int captured_conditional(fcm_mg* h, cudaGraphConditionalHandle cond, cudaGraphConditionalNodeType type,
+                                cudaStream_t sub, F&& body) {
+  cudaStreamCaptureStatus st;
+  cudaGraph_t g;
+  const cudaGraphNode_t* deps = nullptr;
+  size_t nd = 0;
+  CU(cudaStreamGetCaptureInfo_v3(h->stream, &st, nullptr, &g, &deps, nullptr, &nd));
+  cudaGraphNodeParams cp{};
+  cp.type = cudaGraphNodeTypeConditional;
+  cp.conditional.handle = cond;
+  cp.conditional.type = type;
+  cp.conditional.size = 1;
+  cudaGraphNode_t node;
+  CU(cudaGraphAddNode(&node, g, deps, nd, &cp));
+  CU(cudaStreamUpdateCaptureDependencies(h->stream, &node, 1, cudaStreamSetCaptureDependencies));
+  cudaGraph_t bodyg = cp.conditional.phGraph_out[0];
+  cudaStream_t saved = h->stream;
+  set_stream(h, sub);
+  cudaError_t e = cudaStreamBeginCaptureToGraph(sub, bodyg, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal);
+  int rc = e == cudaSuccess ? body() : FCM_ECUDA;
+  cudaGraph_t outg;
+  cudaError_t e2 = e == cudaSuccess ? cudaStreamEndCapture(sub, &outg) : e;
+  set_stream(h, saved);
+  if (rc < 0) return rc == FCM_ECUDA && e != cudaSuccess ? fail(FCM_ECUDA, "conditional body capture: %s", cudaGetErrorString(e)) : rc;
+  if (e2 != cudaSuccess) return fail(FCM_ECUDA, "conditional body capture: %s", cudaGetErrorString(e2));
+  return FCM_OK;
+}
+static cudaGraphConditionalHandle capture_cond_handle(fcm_mg* h, unsigned dflt, int* rc) {
+  cudaStreamCaptureStatus st;
+  cudaGraph_t g;
+  cudaGraphConditionalHandle c = 0;
+  cudaError_t e = cudaStreamGetCaptureInfo_v3(h->stream, &st, nullptr, &g, nullptr, nullptr, nullptr);
+  if (e == cudaSuccess) e = cudaGraphConditionalHandleCreate(&c, g, dflt, cudaGraphCondAssignDefault);
+  *rc = e == cudaSuccess ? FCM_OK : fail(FCM_ECUDA, "conditional handle: %s", cudaGetErrorString(e));
+  return c;
+}
+
+// level-1 AS sweep with an explicit coefficient (the h-levels' damped smoother)
+static int smooth_w(fcm_mg* h, const double* r, double* x, double w) {
+  return launch_cellop(h, 1, make_op(h, 1, OP_SMOOTH, r, x, w, nullptr));
+}
+// geometric V-cycle on h-level i (0: this handle's level 1), x = 0 on entry, residual before
+// every sweep (R1), trilinear transfers, dense solve on the coarsest grid (oracle:
+// GeometricLevels.vcycle)
+static int gmg_vcycle(fcm_mg* h, int i, const double* b, double* x) {
+  const int L = (int)h->gmg.size();
+  fcm_mg* hi = i == 0 ? h : h->gmg[i - 1];
+  const int64_t n = hi->lev[1].ndof;
+  if (i == L) {
+    k_dense_gemv<<<grid_for(n * 32, h->num_sms), kThreads, 0, h->stream>>>(hi->d_A0inv, b, x, n);
+    h->count();
+    CU(cudaGetLastError());
+    return FCM_OK;
+  }
+  double* r = hi->lev[1].r;
+  const double w = h->gmg_omega;
+  RC(fill(hi, x, 0.0, n));
+  for (int s2 = 0; s2 < h->prm.n_pre; ++s2) {
+    if (s2 == 0) { RC(smooth_w(hi, b, x, w)); continue; }
+    RC(residual(hi, 1, b, x, r));
+    RC(smooth_w(hi, r, x, w));
+  }
+  RC(residual(hi, 1, b, x, r));
+  const GmgBox F = gmg_box(hi->L), C = gmg_box(h->gmg[i]->L);
+  const int64_t nc = h->gmg[i]->lev[1].ndof;
+  CU(pdl_launch(h, k_gmg_restrict, dim3(grid_for(nc, h->num_sms)), dim3(kThreads), h->gmg_b[i + 1],
+                (const double*)r, C, F, h->L.dim, nc));
+  h->count();
+  RC(gmg_vcycle(h, i + 1, h->gmg_b[i + 1], h->gmg_x[i + 1]));
+  CU(pdl_launch(h, k_gmg_prolong, dim3(grid_for(n, h->num_sms)), dim3(kThreads), x, (const double*)h->gmg_x[i + 1],
+                F, C, h->L.dim, n));
+  h->count();
+  for (int s2 = 0; s2 < h->prm.n_post; ++s2) {
+    RC(residual(hi, 1, b, x, r));
+    RC(smooth_w(hi, r, x, w));
+  }
+  return FCM_OK;
+}
+
+// x = A_1^{-1} b by CG preconditioned with the geometric V-cycle, stop at ||r|| < rtol ||r0||
+// (reading R4), as nested conditional graph nodes: must be enqueued inside a stream capture
+static int enqueue_coarse_gmg(fcm_mg* h, const double* b, double* x) {
+  cudaStreamCaptureStatus cs;
+  CU(cudaStreamIsCapturing(h->stream, &cs));
+  if (cs != cudaStreamCaptureStatusActive) return fail(FCM_EINVAL, "internal: GMG coarse solve outside a capture");
+  const int64_t n = h->lev[1].ndof;
+  double *r = h->c_vec[0], *z = h->c_vec[1], *p = h->c_vec[2], *q = h->c_vec[3];
+  double *pA = h->c_part, *pB = h->c_part + kMaxPartials, *pC = h->c_part + 2 * kMaxPartials,
+         *pD = h->c_part + 4 * kMaxPartials;
+  const int nbd = dot_blocks(h);
+  const int nbc = cellop_nblocks(h, 1, OP_APPLY);
+  for (fcm_mg* c : h->gmg) c->count_target = h->count_target ? h->count_target : &h->launches;
+  k_fcg_start<<<grid_for(n, h->num_sms), kThreads, 0, h->stream>>>(x, r, b, n);
+  h->count();
+  RC(gmg_vcycle(h, 0, r, z));
+  CU(pdl_launch(h, k_dot, dim3(nbd), dim3(kThreads), (const double*)r, (const double*)z, n, pA, (const uint8_t*)nullptr));
+  CU(pdl_launch(h, k_dot, dim3(nbd), dim3(kThreads), (const double*)r, (const double*)r, n, pB, (const uint8_t*)nullptr));
+  h->count(2);
+  int rc = FCM_OK;
+  cudaGraphConditionalHandle cw = capture_cond_handle(h, 0, &rc);
+  RC(rc);
+  k_gcg_init<<<grid_for(n, h->num_sms), kThreads, 0, h->stream>>>(h->gcg, pA, pB, nbd, p, z, n, cw);
+  h->count();
+  CU(cudaGetLastError());
+  int64_t* tgt = h->count_target ? h->count_target : &h->launches;
+  const int64_t k0 = *tgt;
+  rc = captured_conditional(h, cw, cudaGraphCondTypeWhile, h->st_c[0], [&]() -> int {
+    RC(fill(h, q, 0.0, n));
+    RC(launch_cellop(h, 1, make_op(h, 1, OP_APPLY, p, q, 1.0, pC)));
+    CU(pdl_launch(h, k_gcg_update, dim3(nbd), dim3(kThreads), h->gcg, (const double*)pC, nbc, x, r, (const double*)p,
+                  (const double*)q, n, pD));
+    h->count();
+    int rc2 = FCM_OK;
+    cudaGraphConditionalHandle ci = capture_cond_handle(h, 0, &rc2);
+    RC(rc2);
+    CU(pdl_launch(h, k_gcg_check, dim3(1), dim3(32), h->gcg, (const double*)pD, nbd, cw, ci, h->d_coarse_iters));
+    h->count();
+    return captured_conditional(h, ci, cudaGraphCondTypeIf, h->st_c[1], [&]() -> int {
+      RC(gmg_vcycle(h, 0, r, z));
+      CU(pdl_launch(h, k_dot, dim3(nbd), dim3(kThreads), (const double*)r, (const double*)z, n, pA,
+                    (const uint8_t*)nullptr));
+      CU(pdl_launch(h, k_gcg_update2, dim3(grid_for(n, h->num_sms)), dim3(kThreads), h->gcg, (const double*)pA, nbd,
+                    p, (const double*)z, n));
+      CU(pdl_launch(h, k_gcg_setrz, dim3(1), dim3(32), h->gcg));
+      h->count(3);
+      return FCM_OK;
+    });
+  });
+  h->n_gcg_body = *tgt - k0;
+  for (fcm_mg* c : h->gmg) c->count_target = nullptr;
+  return rc;
+}
+
+// build the h-levels: Galerkin element matrices K_C = sum_f W_f^T K_f W_f of every coarse cell
+// (W_f: trilinear weights of the coarse cell's 2^d vertices at child f's vertices, (x) I_nf), a
+// child handle per level (p = 1 grid, its own elementwise AS); the coarsest solves directly
+static thread_local bool tl_gmg_child = false;
+static int setup_impl(const fcm_grid* g, const fcm_params* prm, const fcm_slab* slab, const double* K_ref,
+                      const uint8_t* cell_kind, double alpha, int64_t n_cut, const int64_t* cut_cells,
+                      const double* cut_K, int64_t n_cc, const int64_t* cc_cells, const double* cc_K1,
+                      fcm_mg** out);
+static int setup_gmg(fcm_mg* h, const double* K_ref, const std::vector<uint8_t>& kind_own,
+                     const std::vector<int32_t>& cut_idx_own, const double* cut_K) {
+  const Layout& L0 = h->L;
+  const int dim = L0.dim, nf = L0.n_f, m = L0.m, m1 = L0.m_level[1];
+  const int nv = 1 << dim;
+  int n[3] = {L0.n[0], L0.n[1], L0.n[2]};
+  auto even_all = [&]() {
+    for (int a = 0; a < dim; ++a)
+      if (n[a] % 2 || n[a] <= 4) return false;
+    return true;
+  };
+  if (!even_all()) return fail(FCM_EINVAL, "GMG coarse solve needs even cell counts > 4 per axis (grid %d)", n[0]);
+  // level-0 data: leading p=1 blocks
+  std::vector<double> K1((size_t)m1 * m1);
+  for (int r = 0; r < m1; ++r)
+    for (int c = 0; c < m1; ++c) K1[(size_t)r * m1 + c] = K_ref[(size_t)r * m + c];
+  std::vector<uint8_t> kinds = kind_own;
+  std::vector<int64_t> ind_idx(kinds.size(), -1);   // cell -> index in ind_K
+  std::vector<double> ind_K;
+  for (size_t c = 0; c < kinds.size(); ++c)
+    if (kinds[c] == 2) {
+      ind_idx[c] = (int64_t)(ind_K.size() / ((size_t)m1 * m1));
+      const double* src = cut_K + (size_t)cut_idx_own[c] * m * m;
+      for (int r = 0; r < m1; ++r)
+        for (int cc = 0; cc < m1; ++cc) ind_K.push_back(src[(size_t)r * m + cc]);
+    }
+  // trilinear child weights W_f[a_fine][A_coarse] (local DOF = vertex mode * nf + comp, mode = sum k_a 2^a)
+  std::vector<std::vector<double>> W(nv, std::vector<double>((size_t)m1 * m1, 0.0));
+  for (int f = 0; f < nv; ++f)
+    for (int vf = 0; vf < nv; ++vf)
+      for (int vc = 0; vc < nv; ++vc) {
+        double w = 1.0;
+        for (int a = 0; a < dim; ++a) {
+          const double t = 0.5 * (((f >> a) & 1) + ((vf >> a) & 1));
+          w *= ((vc >> a) & 1) ? t : 1.0 - t;
+        }
+        for (int c = 0; c < nf; ++c) W[f][(size_t)(vf * nf + c) * m1 + vc * nf + c] = w;
+      }
+  auto galerkin = [&](const std::vector<const double*>& Kf, const std::vector<double>& sc, double* out) {
+    std::vector<double> T((size_t)m1 * m1);
+    std::fill(out, out + (size_t)m1 * m1, 0.0);
+    for (int f = 0; f < nv; ++f) {
+      if (!Kf[f]) continue;
+      // T = K_f W_f, out += W_f^T T
+      for (int i = 0; i < m1; ++i)
+        for (int j = 0; j < m1; ++j) {
+          double t = 0.0;
+          for (int k = 0; k < m1; ++k) t += Kf[f][(size_t)i * m1 + k] * W[f][(size_t)k * m1 + j];
+          T[(size_t)i * m1 + j] = t * sc[f];
+        }
+      for (int i = 0; i < m1; ++i)
+        for (int j = 0; j < m1; ++j) {
+          double t = 0.0;
+          for (int k = 0; k < m1; ++k) t += W[f][(size_t)k * m1 + i] * T[(size_t)k * m1 + j];
+          out[(size_t)i * m1 + j] += t;
+        }
+    }
+  };
+  h->gmg_b.assign(1, nullptr);
+  h->gmg_x.assign(1, nullptr);
+  h->gmg_omega = dim == 3 ? 2.0 / 15.0 : 1.0 / 3.0;   // elementwise omega of P:300 (R21)
+  while (even_all()) {
+    int nc[3] = {1, 1, 1};
+    for (int a = 0; a < dim; ++a) nc[a] = n[a] / 2;
+    const int64_t ncell_c = (int64_t)nc[0] * nc[1] * nc[2];
+    std::vector<uint8_t> kc(ncell_c);
+    std::vector<int64_t> icells;
+    std::vector<double> iK;
+    std::vector<double> K1c((size_t)m1 * m1);
+    {
+      std::vector<const double*> kf(nv, K1.data());
+      std::vector<double> sc(nv, 1.0);
+      galerkin(kf, sc, K1c.data());
+    }
+    std::vector<int64_t> ind_idx_c(ncell_c, -1);
+    std::vector<double> tmp((size_t)m1 * m1);
+    for (int64_t C = 0; C < ncell_c; ++C) {
+      const int cx = (int)(C % nc[0]), cy = (int)((C / nc[0]) % nc[1]), cz = (int)(C / ((int64_t)nc[0] * nc[1]));
+      std::vector<const double*> kf(nv, nullptr);
+      std::vector<double> sc(nv, 1.0);
+      int k0 = -1;
+      bool uniform = true;
+      for (int f = 0; f < nv; ++f) {
+        const int fx = 2 * cx + (f & 1), fy = 2 * cy + ((f >> 1) & 1), fz = dim == 3 ? 2 * cz + ((f >> 2) & 1) : 0;
+        const int64_t fc = ((int64_t)fz * n[1] + fy) * n[0] + fx;
+        const int k = kinds[fc];
+        if (k == 2) kf[f] = ind_K.data() + (size_t)ind_idx[fc] * m1 * m1;
+        else { kf[f] = K1.data(); sc[f] = k == 1 ? h->alpha : 1.0; }
+        if (k == 2 || (k0 >= 0 && k != k0)) uniform = false;
+        k0 = k;
+      }
+      if (uniform) { kc[C] = (uint8_t)k0; continue; }
+      kc[C] = 2;
+      galerkin(kf, sc, tmp.data());
+      ind_idx_c[C] = (int64_t)icells.size();
+      icells.push_back(C);
+      iK.insert(iK.end(), tmp.begin(), tmp.end());
+    }
+    // child handle: p = 1 on the coarse grid
+    fcm_grid gc = h->g;
+    gc.p = 1;
+    for (int a = 0; a < dim; ++a) gc.n[a] = nc[a];
+    gc.h = h->g.h * 2.0;
+    for (int a = 0; a < dim; ++a) n[a] = nc[a];
+    const bool bottom = !even_all();
+    fcm_params pc = h->prm;
+    pc.coarse = bottom ? FCM_COARSE_DIRECT : FCM_COARSE_AS_PCG;
+    pc.stream = (void*)h->stream;
+    fcm_mg* child = nullptr;
+    tl_gmg_child = !bottom;
+    const int rc = setup_impl(&gc, &pc, nullptr, K1c.data(), kc.data(), h->alpha, (int64_t)icells.size(),
+                              icells.data(), iK.data(), 0, nullptr, nullptr, &child);
+    tl_gmg_child = false;
+    RC(rc);
+    CU(cudaStreamSynchronize(child->stream));
+    CU(cudaStreamDestroy(child->stream));
+    child->stream = h->stream;
+    child->borrowed_stream = true;
+    h->gmg.push_back(child);
+    double *bb, *xx;
+    RC(h->alloc(&bb, child->lev[1].ndof));
+    RC(h->alloc(&xx, child->lev[1].ndof));
+    h->gmg_b.push_back(bb);
+    h->gmg_x.push_back(xx);
+    K1 = K1c;
+    kinds = kc;
+    ind_idx = ind_idx_c;
+    ind_K.swap(iK);
+  }
+  const int64_t n1 = h->lev[1].ndof;
+  for (int i = 0; i < 9; ++i) RC(h->alloc(&h->c_vec[i], n1));
+  RC(h->alloc(&h->c_part, 6 * kMaxPartials));
+  RC(h->alloc(&h->gcg, 1));
+  RC(h->alloc(&h->c_bst, n1));
+  RC(h->alloc(&h->c_xst, n1));
+  GcgScalars gs{};
+  gs.maxit = h->prm.coarse_maxit;
+  gs.rtol2 = h->prm.coarse_rtol * h->prm.coarse_rtol;
+  CU(cudaMemcpyAsync(h->gcg, &gs, sizeof(gs), cudaMemcpyHostToDevice, h->stream));
+  for (auto& st : h->st_c) CU(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  CU(cudaStreamSynchronize(h->stream));
+  return FCM_OK;
+}
 // Algorithm 1 on level q: x = V_q(b), x~ = 0 on entry; reading R1.
 static int enqueue_vcycle(fcm_mg* h, int q, const double* b, double* x) {
   if (q == 1) return enqueue_coarse(h, b, x);
@@ -2187,6 +2638,8 @@ static int setup_impl(const fcm_grid* g, const fcm_params* prm, const fcm_slab* 
                       const uint8_t* cell_kind, double alpha, int64_t n_cut, const int64_t* cut_cells,
                       const double* cut_K, int64_t n_cc, const int64_t* cc_cells, const double* cc_K1,
                       fcm_mg** out) {
+  const bool gmg_child = tl_gmg_child;   // an h-level of a parent's GMG coarse solve
+  tl_gmg_child = false;
   if (!g || !prm || !K_ref || !cell_kind || !out) return fail(FCM_EINVAL, "NULL argument");
   *out = nullptr;
   int me = fcm_element_size(g);
@@ -2195,7 +2648,7 @@ static int setup_impl(const fcm_grid* g, const fcm_params* prm, const fcm_slab* 
   if (n_cut < 0 || (n_cut > 0 && (!cut_cells || !cut_K))) return fail(FCM_EINVAL, "bad cut-cell buffers");
   if (!(alpha > 0)) return fail(FCM_EINVAL, "alpha must be > 0");
   if (prm->n_pre < 0 || prm->n_post < 0) return fail(FCM_EINVAL, "negative sweep count");
-  if (prm->coarse < 0 || prm->coarse > 2) return fail(FCM_EINVAL, "unknown coarse solver");
+  if (prm->coarse < 0 || prm->coarse > 3) return fail(FCM_EINVAL, "unknown coarse solver");
   if (prm->block != FCM_BLOCK_ELEMENT && prm->block != FCM_BLOCK_PATCH) return fail(FCM_EINVAL, "unknown block kind %d", prm->block);
   const int dim = g->dim, sax = dim - 1;
   const int nsax = g->n[sax];
@@ -2203,6 +2656,7 @@ static int setup_impl(const fcm_grid* g, const fcm_params* prm, const fcm_slab* 
   h->g = *g;
   h->prm = *prm;
   h->alpha = alpha;
+  h->gmg_child = gmg_child;
   // blocks per SM of the two k_cell_mma populations; clamped so that one launch never has more
   // blocks than the 2 * kMaxPartials energy partials d_partA/B/C hold (sum_partials reads them all)
   const int bps_cap = std::max(1, (2 * kMaxPartials) / (2 * std::max(1, h->num_sms)));
@@ -2369,7 +2823,7 @@ static int setup_impl(const fcm_grid* g, const fcm_params* prm, const fcm_slab* 
     RC(h->alloc(&h->x_recv, 2 * std::max<int64_t>(max_plane, 1)));
   }
   for (int q = 1; q <= g->p; ++q)
-    if (q >= 2 || (prm->coarse == FCM_COARSE_AS_PCG && !h->multi))
+    if (q >= 2 || ((prm->coarse == FCM_COARSE_AS_PCG || prm->coarse == FCM_COARSE_GMG_PCG) && !h->multi))
       RC(setup_schwarz(h.get(), q, kind, cut_idx));
   for (int q = 2; q <= g->p; ++q)
     if (h->lev[q].patch) {
@@ -2442,6 +2896,10 @@ static int setup_impl(const fcm_grid* g, const fcm_params* prm, const fcm_slab* 
     CU(cudaMemcpyAsync(h->c_unpack, unpack.data(), unpack.size() * 8, cudaMemcpyHostToDevice, h->stream));
     CU(cudaMemcpyAsync(h->c_extract, extract.data(), extract.size() * 8, cudaMemcpyHostToDevice, h->stream));
     CU(cudaMemsetAsync(h->c_send, 0, h->c_max * 8, h->stream));
+  } else if (gmg_child) {
+    // an h-level of the parent's geometric V-cycle: operator + elementwise AS only
+  } else if (prm->coarse == FCM_COARSE_GMG_PCG) {
+    RC(setup_gmg(h.get(), K_ref, kind_own, cut_idx_own, cut_K));
   } else if (prm->coarse == FCM_COARSE_DIRECT) {
     if (n1 > 8192) return fail(FCM_EINVAL, "direct coarse solve limited to 8192 DOFs (level 1 has %lld)", (long long)n1);
     std::vector<double> A0;
@@ -2633,7 +3091,14 @@ extern "C" int fcm_mg_coarse_solve(fcm_mg* h, const double* r, double* x, int32_
   clear_error();
   if (!h || !r || !x) return fail(FCM_EINVAL, "NULL argument");
   StreamGuard sg(h);
-  RC(enqueue_coarse(h, r, x));
+  if (h->prm.coarse == FCM_COARSE_GMG_PCG && !h->hg) {   // nested conditional nodes: graph only
+    RC(capture(h, &h->g_coarse, &h->n_coarse_g, [&]() { return enqueue_coarse_gmg(h, h->c_bst, h->c_xst); }));
+    CU(cudaMemcpyAsync(h->c_bst, r, h->lev[1].ndof * 8, cudaMemcpyDeviceToDevice, h->stream));
+    RC(run_graph(h, h->g_coarse, h->n_coarse_g));
+    CU(cudaMemcpyAsync(x, h->c_xst, h->lev[1].ndof * 8, cudaMemcpyDeviceToDevice, h->stream));
+  } else {
+    RC(enqueue_coarse(h, r, x));
+  }
   if (iters) {
     if (h->prm.coarse == FCM_COARSE_DIRECT) *iters = 0;
     else {
@@ -2860,6 +3325,11 @@ static int pcg_core(fcm_mg* h, double rtol, int32_t maxit, int32_t* iters, doubl
     const Scalars s = *h->h_s;
     it = s.it;
     h->launches += h->n_head + (int64_t)(it - 1) * h->n_loop;
+    if (h->prm.coarse == FCM_COARSE_GMG_PCG && h->n_gcg_body > 0) {   // coarse CG trips beyond the first
+      int ci[2] = {0, 0};
+      CU(cudaMemcpy(ci, h->d_coarse_iters, 8, cudaMemcpyDeviceToHost));
+      h->launches += std::max<int64_t>(0, ci[1] - it) * h->n_gcg_body;
+    }
     h->stat_vcycles = it;
     if (hist && it > 0) {
       std::vector<double> hh(it + 1);
@@ -3007,6 +3477,7 @@ extern "C" int fcm_mg_coarse_info(const fcm_mg* h, int32_t* kind, int32_t* block
   if (!h || !kind || !blocks) return fail(FCM_EINVAL, "NULL argument");
   if (h->hg) return fcm_mg_coarse_info(h->hg, kind, blocks, tile);
   if (h->prm.coarse == FCM_COARSE_DIRECT) { *kind = FCM_COARSE_KERNEL_DIRECT; *blocks = 0; }
+  else if (h->prm.coarse == FCM_COARSE_GMG_PCG) { *kind = FCM_COARSE_KERNEL_GMG; *blocks = (int32_t)h->gmg.size(); }
   else if (h->ktiled) { *kind = FCM_COARSE_KERNEL_TILED; *blocks = h->t_blocks; }
   else { *kind = FCM_COARSE_KERNEL_GRID; *blocks = h->coarse_blocks; }
   if (tile)

@@ -17,7 +17,7 @@ import torch
 from . import _lib
 from ._lib import Grid, Params, Physics, Slab, check
 
-COARSE = {"direct": 0, "as_pcg": 1, "jacobi_pcg": 2}
+COARSE = {"direct": 0, "as_pcg": 1, "jacobi_pcg": 2, "gmg_pcg": 3}
 BLOCK = {"element": 0, "patch": 1}
 
 
@@ -343,7 +343,7 @@ class Solver:
         k, nb = C.c_int32(), C.c_int32()
         t = (C.c_int32 * 3)()
         check(_lib.lib().fcm_mg_coarse_info(self._h, C.byref(k), C.byref(nb), t))
-        name = {0: "k_dense_gemv", 1: "k_coarse_pcg", 2: "k_coarse_tiled"}[k.value]
+        name = {0: "k_dense_gemv", 1: "k_coarse_pcg", 2: "k_coarse_tiled", 3: "gmg_pcg"}[k.value]
         return name, nb.value, tuple(t)
 
     def stats(self):

@@ -116,6 +116,12 @@ CASES = {
     # 729-slot vertex patches with full interior patches (n = 4: vertex 2 touches no Dirichlet face)
     "3d_p4_elem": lambda: small_config(3, 4, 4, voids=2, seed=9),
     "3d_p4_patch729": lambda: small_config(3, 4, 4, voids=1, seed=10, block="patch"),
+    # h-coarsening below p = 1 (P:227 Remark, R21): CG + geometric V-cycle on the p=1 level,
+    # one (n = 8: 8 -> 4) or two (n = 12: 12 -> 6 -> 3) h-levels, scalar 3D / 2D and elasticity
+    "3d_p2_gmg": lambda: small_config(3, 8, 2, voids=3, seed=1, coarse="gmg_pcg"),
+    "3d_p2_gmg_n12": lambda: small_config(3, 12, 2, voids=2, seed=3, coarse="gmg_pcg"),
+    "2d_p3_gmg": lambda: small_config(2, 16, 3, voids=1, seed=2, coarse="gmg_pcg"),
+    "3d_elast_gmg": lambda: small_config(3, 8, 2, physics="elasticity", voids=2, seed=6, coarse="gmg_pcg"),
 }
 
 
