@@ -8,6 +8,8 @@ from paper_2010_00881_b200.fcm import Solver, generate
 from workloads import get_config
 
 cfg = get_config(os.environ.get("CFG", "cfg5"))
+if os.environ.get("COARSE"):
+    cfg = cfg.replace(coarse=os.environ["COARSE"])
 out = {"workload": cfg.name}
 t = time.time(); G = generate(cfg); out["generator_s"] = time.time() - t
 t = time.time(); S = Solver.from_problem(cfg, G); b = S.load(G); torch.cuda.synchronize()
@@ -43,9 +45,9 @@ x = torch.zeros_like(b)
 ts, _ = ev_time(lambda: S.smooth(b, x, cfg.p), 3)
 nirr = S.irregular_blocks(cfg.p)
 ncut = out["cut_cells"]
-# algorithmic bytes: 24 B per DOF (x read, y RMW) + stored individual matrices (full m*m)
-bytes_apply = 24 * N + ncut * m * m * 8
-bytes_smooth = 24 * N + nirr * m * m * 8
+# algorithmic bytes: 24 B per DOF (x read, y RMW) + individual matrices counted packed m(m+1)/2
+bytes_apply = 24 * N + ncut * m * (m + 1) // 2 * 8   # packed
+bytes_smooth = 24 * N + nirr * m * (m + 1) // 2 * 8
 peak = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "MEASURED_PEAKS.json"))).get("hbm_gbs", 6550.0) \
     if os.path.exists(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "MEASURED_PEAKS.json")) else 6650.0
 out["level_p_apply"] = {"ms": ta, "algo_bytes": bytes_apply, "GBps": bytes_apply / ta / 1e6, "frac": bytes_apply / ta / 1e6 / peak}
