@@ -34,6 +34,7 @@
 #include "blocks.cuh"
 #include "patch.cuh"
 #include "cellmma.cuh"
+#include "cellws.cuh"
 #include "common.hpp"
 #include "layout.hpp"
 #include "nccl_dl.hpp"
@@ -110,6 +111,13 @@ struct LevelDev {
   int32_t* gS_cells = nullptr;     // smoother groups (8 regular cells of one type slot)
   int32_t* gS_mat = nullptr;
   int64_t nS = 0;
+  // warp-specialised launch (cellws.cuh): MMA warps for the regular cells + streaming warps for
+  // the tile-packed individual matrices (operator: the fine cut-cell copy; smoother: irr_tp)
+  const void* kws = nullptr;
+  int ws_ns = 0;                   // streaming warps per CTA
+  int ntq = 0;                     // 32-tiles per dimension of the level block (ceil(m / 32))
+  double* irr_tp = nullptr;        // tile-packed individual elementwise inverses (replaces irr_inv)
+  int64_t irr_tps = 0;             // doubles per packed inverse
   std::vector<int32_t> blk_h;      // host copy of blk (tiled coarse setup)
   // patchwise blocks (blocks.cuh): anchors are grid vertices, blk is per anchor
   bool patch = false;
@@ -166,6 +174,8 @@ struct fcm_mg {
   const void* kcoarse = nullptr;
   double* d_Kref = nullptr;
   double* d_cutK = nullptr;
+  double* d_cutK_tp = nullptr;      // tile-packed copy of the cut-cell matrices (k_cell_ws levels)
+  int64_t cut_tps = 0;              // doubles per packed cut-cell matrix
   std::vector<LevelDev> lev;  // index q = 1..p
   // coarse
   double* d_A0inv = nullptr;   // direct
@@ -204,6 +214,7 @@ struct fcm_mg {
   int rank = 0, nranks = 1, z0 = 0, z1 = 0;
   bool multi = false;               // slab mode (nranks > 1, or FCM_FORCE_SLAB on one rank: tests)
   int mma_bps = 4, list_bps = 8;    // blocks per SM of the MMA / list parts of k_cell_mma
+  int ws_ctas = 148;                // CTAs of a k_cell_ws launch (num_sms; FCM_WS_CTAS: tests)
   int pdl = 1;                      // programmatic dependent launch of k_cell_mma (FCM_PDL)
   int ext_lo = 0, ext_n = 0;        // ghost-extended cell layers along the slab axis (relative)
   int64_t cut_first = 0;            // first owned cut cell in the cut-matrix array
@@ -334,6 +345,78 @@ __global__ void __launch_bounds__(kThreads, M > 32 ? 2 : 4) k_cell_mma(MmaOp g, 
   if (g.op.partials) {
     const double t = block_sum(e, red);
     if (threadIdx.x == 0) g.op.partials[blockIdx.x] = t;
+  }
+}
+
+// One cell operation as a warp-specialised persistent launch (cellws.cuh): warps [0, NS) stream
+// the tile-packed individual matrices, warps [NS, NS + kWsMmaWarps) run the regular cells as fp64
+// MMA groups.  smem [Tab][A fragments][ring: NS x kIrrStages x 8 KB][mbarriers][xs, ys, ids].
+template <int M, int NS>
+__host__ __device__ constexpr size_t ws_smem() {
+  return sizeof(Tab) + (size_t)((M + 7) / 8) * ((M + 3) / 4) * 32 * 8 + ws_stream_smem((M + 31) / 32, NS);
+}
+template <int M, int NS>
+__global__ void __launch_bounds__((NS + kWsMmaWarps) * 32, 1) k_cell_ws(MmaOp g, TileListOp tl) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  constexpr int MT = (M + 7) / 8, KT = (M + 3) / 4;
+  Tab& T = *reinterpret_cast<Tab*>(smem);
+  double* As = reinterpret_cast<double*>(smem + sizeof(Tab));
+  double* ring = As + MT * KT * 32;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(ring + (size_t)NS * kIrrStages * 1024);
+  double* xs0 = reinterpret_cast<double*>(bars + NS * kIrrStages);
+  __shared__ double red[32];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int MPd = 32 * tl.ntq;
+  const int ntl = tl.ntq * (tl.ntq + 1) / 2;
+  const int64_t gw = (int64_t)blockIdx.x * NS + w, W = (int64_t)gridDim.x * NS;
+  load_tab(T, g.op);
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  const bool apply = g.op.mode == OP_APPLY;
+  stage_fragments<M>(As, apply ? g.op.Kref : g.op.type_inv, apply ? g.op.ldK : M);
+  if (w < NS && lane == 0)
+    for (int s = 0; s < kIrrStages; ++s) mbar_init(&bars[w * kIrrStages + s], 1);
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  __syncthreads();
+  if (w < NS && lane == 0) {   // the first tiles: setup data, so before griddepcontrol.wait
+    const int64_t nitems = (tl.nlist > gw ? (tl.nlist - gw + W - 1) / W : 0) * ntl;
+    for (int64_t i = 0; i < kIrrStages && i < nitems; ++i)
+      ws_issue(tl, ntl, gw, W, i, ring + (size_t)w * kIrrStages * 1024, bars + w * kIrrStages, g.op.m);
+  }
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  double e;
+  if (w < NS) {
+    double* xs = xs0 + (size_t)w * MPd * 2;
+    int* ids = reinterpret_cast<int*>(xs0 + (size_t)NS * MPd * 2) + (size_t)w * MPd;
+    e = ws_stream_cells(g.op, tl, T, xs, xs + MPd, ids, ring + (size_t)w * kIrrStages * 1024, bars + w * kIrrStages,
+                        gw, W);
+  } else {
+    e = mma_cells<M>(g.op, g.grp_cells, g.grp_mat, g.ngroups, T, As, apply ? -1 : 0,
+                     blockIdx.x * kWsMmaWarps + (w - NS), gridDim.x * kWsMmaWarps);
+  }
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < g.cp_n; i += (int64_t)gridDim.x * blockDim.x)
+    g.cp_dst[i] = g.cp_src[i];
+  if (g.op.partials) {
+    const double t = block_sum(e, red);
+    if (threadIdx.x == 0) g.op.partials[blockIdx.x] = t;
+  }
+}
+
+// symmetric m x m matrices (row-major, consecutive at mstride doubles) -> tile-packed lower
+// storage with nt tiles per dimension (patch.cuh layout; entries beyond m are 0); grid (tiles, matrices)
+__global__ void k_pack_tiles_ld(const double* __restrict__ A, int m, int64_t mstride, int nt, double* __restrict__ out,
+                                int64_t ostride) {
+  const int t = blockIdx.x;
+  int I = 0;
+  while ((I + 1) * (I + 2) / 2 <= t) ++I;
+  const int J = t - I * (I + 1) / 2;
+  const double* M = A + (int64_t)blockIdx.y * mstride;
+  double* o = out + (int64_t)blockIdx.y * ostride + tile_off(I, J);
+  for (int e = threadIdx.x; e < 1024; e += blockDim.x) {
+    const int r = e / 32, c = e % 32;
+    const int gi = 32 * I + r, gj = 32 * J + c;
+    const double v = (gi < m && gj < m) ? 0.5 * (M[(int64_t)gi * m + gj] + M[(int64_t)gj * m + gi]) : 0.0;
+    if (I != J) o[e] = v;
+    else if (c <= r) o[r * (r + 1) / 2 + c] = v;
   }
 }
 
@@ -786,6 +869,17 @@ const void* mma_kernel(int m) {
 #undef CASE
   return nullptr;
 }
+// warp-specialised cell kernel (cellws.cuh) for the elementwise levels that carry most bytes:
+// m = 27 / 64 / 125 (tensor p = 2 / 3 / 4); *ns = its streaming warps, *smem its dynamic smem
+const void* ws_kernel(int m, int* ns, size_t* smem) {
+  switch (m) {
+    case 27: *ns = 8; *smem = ws_smem<27, 8>(); return (const void*)k_cell_ws<27, 8>;
+    case 64: *ns = 8; *smem = ws_smem<64, 8>(); return (const void*)k_cell_ws<64, 8>;
+    case 125: *ns = 4; *smem = ws_smem<125, 4>(); return (const void*)k_cell_ws<125, 4>;
+    default: break;
+  }
+  return nullptr;
+}
 const void* list_kernel(int G) {
   switch (G) {
     case 4: return (const void*)k_cell_list<4>;
@@ -894,9 +988,18 @@ static CellOp make_op(fcm_mg* h, int q, int mode, const double* in, double* out,
   return op;
 }
 
+// the level's cell operation runs as one warp-specialised launch (cellws.cuh)
+static bool ws_on(const LevelDev& Lv, int mode) {
+  return Lv.kws && (mode == OP_APPLY || (!Lv.patch && Lv.has_as && (Lv.irr_tp || Lv.n_irr == 0)));
+}
 // grid of one cell-operator launch: regular thread-per-cell blocks + individual-list blocks
 static void cellop_grid(const fcm_mg* h, int q, int mode, int* nb_reg, int* nb_list) {
   const LevelDev& Lv = h->lev[q];
+  if (ws_on(Lv, mode)) {   // persistent: one CTA per SM
+    *nb_reg = h->ws_ctas;
+    *nb_list = 0;
+    return;
+  }
   const int64_t cap = (int64_t)h->num_sms * 8;
   const int64_t cpb = (kThreads / 32) * (32 / Lv.G);  // cells per block on the list path
   const bool mma = Lv.kmma && (mode == OP_APPLY ? Lv.gA_cells != nullptr : Lv.gS_cells != nullptr);
@@ -936,6 +1039,43 @@ static int launch_cellop(fcm_mg* h, int q, const CellOp& op, double* cp_dst = nu
   int nb_reg, nb_list;
   cellop_grid(h, q, op.mode, &nb_reg, &nb_list);
   CellOp o = op;
+  if (ws_on(Lv, op.mode)) {
+    MmaOp g{};
+    g.op = o;
+    TileListOp tl{};
+    tl.ntq = Lv.ntq;
+    if (op.mode == OP_APPLY) {
+      g.grp_cells = Lv.gA_cells; g.grp_mat = Lv.gA_mat; g.ngroups = Lv.nA;
+      tl.list = h->d_cut_list; tl.nlist = (int32_t)h->ncut;
+      tl.mats = h->d_cutK_tp + (size_t)h->cut_first * h->cut_tps; tl.stride = h->cut_tps;
+    } else {
+      g.grp_cells = Lv.gS_cells; g.grp_mat = Lv.gS_mat; g.ngroups = Lv.nS;
+      tl.list = Lv.irr_list; tl.nlist = (int32_t)Lv.n_irr; tl.mats = Lv.irr_tp; tl.stride = Lv.irr_tps;
+    }
+    g.cp_src = cp_src; g.cp_dst = cp_dst; g.cp_n = cp_dst ? cp_n : 0;
+    const char* wp = getenv("FCM_WS_PART");   // measurement hook, read per launch
+    const int part = wp ? atoi(wp) : 0;
+    if (part == 1) g.ngroups = 0;
+    if (part == 2) tl.nlist = 0;
+    void* args[] = {&g, &tl};
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(h->ws_ctas);
+    cfg.blockDim = dim3((Lv.ws_ns + kWsMmaWarps) * 32);
+    int ns;
+    size_t sm;
+    ws_kernel(Lv.m, &ns, &sm);
+    cfg.dynamicSmemBytes = sm;
+    cfg.stream = h->stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = h->pdl ? 1 : 0;
+    cudaError_t e = cudaLaunchKernelExC(&cfg, Lv.kws, args);
+    h->count();
+    if (e != cudaSuccess) return fail(FCM_ECUDA, "ws kernel launch: %s", cudaGetErrorString(e));
+    return FCM_OK;
+  }
   if (Lv.kmma && (op.mode == OP_APPLY ? Lv.gA_cells != nullptr : Lv.gS_cells != nullptr)) {
     // one launch: regular cells as fp64 MMA groups, the individual list in the other blocks
     MmaOp g{};
@@ -1957,6 +2097,7 @@ static size_t patch_smem(const fcm_mg* h, int q) {
   size_t o = (sizeof(Tab) + (size_t)(kIrrWarps / patch_wpp(Lv.nt)) * MPd * 20 + 127) / 128 * 128;
   o += (size_t)kIrrWarps * kIrrStages * 1024 * 8 + (size_t)kIrrWarps * kIrrStages * 8;
   o += (size_t)3 * (Lv.fd ? Lv.fd_ncls : 0) * (S * S + S) * 8 + ((nmi * 2 + 15) / 16) * 16;
+  o += ((size_t)S3 * 4 + 15) / 16 * 16;   // FD slot codes
   o += (size_t)kFdWarps * 2 * S3 * 8;
   return o;
 }
@@ -2083,6 +2224,25 @@ static int setup_patch_blocks(fcm_mg* h, int q, const BlockGeom& g, const std::v
   Lv.n_types = (int32_t)ntypes;
   Lv.blk_h = blk;
   CU(cudaStreamSynchronize(h->stream));
+  return FCM_OK;
+}
+
+// n symmetric m x m matrices (consecutive at mstride) -> tile-packed (nt tiles per dimension)
+static int pack_tiles(fcm_mg* h, const double* A, int m, int64_t mstride, int nt, double* out, int64_t ostride,
+                      int64_t n) {
+  const int ntiles = nt * (nt + 1) / 2;
+  for (int64_t c0 = 0; c0 < n; c0 += 65535) {
+    const int64_t cn = std::min<int64_t>(65535, n - c0);
+    k_pack_tiles_ld<<<dim3(ntiles, (unsigned)cn), 256, 0, h->stream>>>(A + c0 * mstride, m, mstride, nt,
+                                                                        out + c0 * ostride, ostride);
+    CU(cudaGetLastError());
+  }
+  return FCM_OK;
+}
+static int free_alloc(fcm_mg* h, void* p) {
+  auto it = std::find(h->allocs.begin(), h->allocs.end(), p);
+  if (it != h->allocs.end()) h->allocs.erase(it);
+  CU(cudaFree(p));
   return FCM_OK;
 }
 
@@ -2225,6 +2385,20 @@ static int setup_schwarz(fcm_mg* h, int q, const std::vector<uint8_t>& kind,
   Lv.type_inv = d_mats;                       // slots 0..ntypes-1
   Lv.irr_inv = d_mats + (size_t)ntypes * mb * mb;
   Lv.n_irr = (int64_t)irr.size();
+  if (!patch && Lv.kws && Lv.n_irr > 0) {
+    // warp-specialised level: the individual inverses are streamed tile-packed (half the bytes
+    // of full storage); the full copies are dropped, the shared types kept
+    Lv.irr_tps = tile_pack_size(Lv.ntq);
+    RC(h->alloc(&Lv.irr_tp, (size_t)Lv.n_irr * Lv.irr_tps));
+    RC(pack_tiles(h, Lv.irr_inv, mb, (int64_t)mb * mb, Lv.ntq, Lv.irr_tp, Lv.irr_tps, Lv.n_irr));
+    double* ti = nullptr;
+    RC(h->alloc(&ti, (size_t)std::max<int64_t>(ntypes, 1) * mb * mb));
+    if (ntypes > 0) CU(cudaMemcpyAsync(ti, d_mats, (size_t)ntypes * mb * mb * 8, cudaMemcpyDeviceToDevice, h->stream));
+    CU(cudaStreamSynchronize(h->stream));
+    RC(free_alloc(h, d_mats));
+    Lv.type_inv = ti;
+    Lv.irr_inv = nullptr;
+  }
   if (!patch) {
     std::vector<int32_t> il(irr.begin(), irr.end());
     RC(h->alloc(&Lv.irr_list, il.size()));
@@ -2702,6 +2876,8 @@ static int setup_impl(const fcm_grid* g, const fcm_params* prm, const fcm_slab* 
     return fail(FCM_EINVAL, "grid too large for 32-bit cell/DOF indexing on one device");
   CU(cudaGetDevice(&h->dev));
   CU(cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, h->dev));
+  h->ws_ctas = h->num_sms;
+  if (const char* e = getenv("FCM_WS_CTAS")) h->ws_ctas = std::min(h->num_sms, std::max(1, atoi(e)));
   // cells: owned layers [z0, z1) plus one ghost layer on each side that exists
   int64_t plane = 1;
   for (int i = 0; i < sax; ++i) plane *= g->n[i];
@@ -2790,6 +2966,14 @@ static int setup_impl(const fcm_grid* g, const fcm_params* prm, const fcm_slab* 
         CU(cudaStreamSynchronize(h->stream));
       }
     }
+    if (Lv.kmma && q >= 2 && !(getenv("FCM_CELL_WS") && atoi(getenv("FCM_CELL_WS")) == 0)) {
+      size_t wsm = 0;
+      Lv.kws = ws_kernel(Lv.m, &Lv.ws_ns, &wsm);
+      if (Lv.kws) {
+        Lv.ntq = (Lv.m + 31) / 32;
+        RC(allow_smem(Lv.kws, wsm));
+      }
+    }
     if (Lv.kreg) RC(allow_smem(Lv.kreg, level_reg_smem(Lv)));
     RC(allow_smem(Lv.klist, list_smem(Lv.m, Lv.G)));
     Lv.omega = q >= 2 ? prm->omega : 1.0;
@@ -2821,6 +3005,16 @@ static int setup_impl(const fcm_grid* g, const fcm_params* prm, const fcm_slab* 
   if (h->multi) {
     RC(h->alloc(&h->x_send, 2 * std::max<int64_t>(max_plane, 1)));
     RC(h->alloc(&h->x_recv, 2 * std::max<int64_t>(max_plane, 1)));
+  }
+  {   // tile-packed copy of the cut-cell matrices for the warp-specialised levels (cellws.cuh)
+    bool any_ws = false;
+    for (int q = 2; q <= g->p; ++q) any_ws = any_ws || h->lev[q].kws != nullptr;
+    if (any_ws) {
+      const int ntf = (m + 31) / 32;
+      h->cut_tps = tile_pack_size(ntf);
+      RC(h->alloc(&h->d_cutK_tp, (size_t)std::max<int64_t>(n_cut, 1) * h->cut_tps));
+      RC(pack_tiles(h.get(), h->d_cutK, m, (int64_t)m * m, ntf, h->d_cutK_tp, h->cut_tps, n_cut));
+    }
   }
   for (int q = 1; q <= g->p; ++q)
     if (q >= 2 || ((prm->coarse == FCM_COARSE_AS_PCG || prm->coarse == FCM_COARSE_GMG_PCG) && !h->multi))
@@ -3539,9 +3733,10 @@ extern "C" int fcm_mg_export_block_inverses(const fcm_mg* h, int32_t q, int64_t*
       const int32_t bq = Lv.blk_h[A];
       const double* src;
       double scale = 1.0;
-      if (bq >= 0 && Lv.patch) {   // tile-packed lower triangle (patch.cuh)
-        std::vector<double> pk(Lv.pstride);
-        CU(cudaMemcpy(pk.data(), Lv.irr_inv + (size_t)bq * Lv.pstride, Lv.pstride * 8, cudaMemcpyDeviceToHost));
+      if (bq >= 0 && (Lv.patch || Lv.irr_tp)) {   // tile-packed lower triangle (patch.cuh / cellws.cuh)
+        const int64_t ps = Lv.patch ? Lv.pstride : Lv.irr_tps;
+        std::vector<double> pk(ps);
+        CU(cudaMemcpy(pk.data(), (Lv.patch ? Lv.irr_inv : Lv.irr_tp) + (size_t)bq * ps, ps * 8, cudaMemcpyDeviceToHost));
         for (int r = 0; r < mb; ++r)
           for (int c = 0; c <= r; ++c) {
             const int I = r / 32, J = c / 32, rr = r % 32, cc = c % 32;

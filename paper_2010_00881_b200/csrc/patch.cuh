@@ -414,14 +414,73 @@ __device__ __forceinline__ void fd_slot(int s, int q, int v, int n, int& cell, i
   else { cell = v; k = 1; }
 }
 
+// One one-axis contraction of the S^DIM slot tensor (x fastest) by a 1D factor Tm (S x S,
+// row i = slot, column j = mode): forward out_j = sum_i Tm[i][j] in_i (S^T), backward
+// out_i = sum_j Tm[i][j] in_j (S).  LINE-BASED: each lane owns whole lines along AXIS (S inputs
+// and S outputs in registers, S independent accumulators), the factor is read as warp-uniform
+// broadcast words.  SCALE (the last forward axis): multiply by sc / (lambda_x + lambda_y (+ lambda_z)).
+template <int S, int DIM, int AXIS, bool FWD, bool SCALE>
+__device__ __forceinline__ void fd_pass(const double* __restrict__ in, double* __restrict__ out, const double* Tm,
+                                        const double* lx, const double* ly, const double* lz, double sc) {
+  constexpr int NLINE = DIM == 3 ? S * S : S;
+  constexpr int ST = AXIS == 0 ? 1 : (AXIS == 1 ? S : S * S);
+  const int lane = threadIdx.x & 31;
+#pragma unroll 1
+  for (int line = lane; line < NLINE; line += 32) {
+    const int base = AXIS == 0 ? line * S : (AXIS == 1 ? (line / S) * S * S + line % S : line);
+    // an opaque zero, so the S^2 factor words are re-read per line (broadcast LDS) instead of
+    // being hoisted into registers (S = 9: 162 registers -> spills)
+    int z0;
+    asm volatile("mov.b32 %0, 0;" : "=r"(z0));
+    const double* Tl = Tm + z0;
+    double v[S], o[S];
+#pragma unroll
+    for (int i = 0; i < S; ++i) {
+      v[i] = in[base + i * ST];
+      o[i] = 0.0;
+    }
+#pragma unroll
+    for (int i = 0; i < S; ++i)
+#pragma unroll
+      for (int j = 0; j < S; ++j) {
+        if (FWD) o[j] = fma(Tl[i * S + j], v[i], o[j]);
+        else o[i] = fma(Tl[i * S + j], v[j], o[i]);
+      }
+    if (SCALE) {   // element (line, j) of the last axis: 3D line = y S + x, 2D line = x
+      const int xx = line % S, yy = DIM == 3 ? line / S : 0;
+#pragma unroll
+      for (int j = 0; j < S; ++j) {
+        const double lam = DIM == 3 ? lx[xx] + ly[yy] + lz[j] : lx[xx] + ly[j];
+        o[j] *= sc / lam;
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < S; ++j) out[base + j * ST] = o[j];
+  }
+}
+
+// slot code of an INTERIOR anchor (every cell of the patch inside the grid, no Dirichlet DOF):
+// local DOF a (bits 0-9) and, per axis, whether the slot's cell is v - 1 (bits 10, 11, 12)
+__device__ __forceinline__ int fd_slot_code(int l, int S, int q, int DIM, const int16_t* midx) {
+  const int sx = l % S, sy = (l / S) % S, sz = DIM == 3 ? l / (S * S) : 0;
+  int cx, kx, cy, ky, cz = 2, kz = 0;
+  fd_slot(sx, q, 2, 1 << 20, cx, kx);
+  fd_slot(sy, q, 2, 1 << 20, cy, ky);
+  if (DIM == 3) fd_slot(sz, q, 2, 1 << 20, cz, kz);
+  const int a = midx[(kz * (q + 1) + ky) * (q + 1) + kx];
+  return a | ((2 - cx) << 10) | ((2 - cy) << 11) | ((2 - cz) << 12);
+}
+
 // Regular patches by fast diagonalisation: nw warps (index w), independent (no CTA barrier).
 // Compile-time S (slots per axis) and DIM: every lane owns slots l = lane + 32 j, whose DOF
 // indices and gathered values live in registers (all NL loads in flight before the first use:
 // the gather is one memory latency per patch, not one per slot), and the same slots are
-// scattered at the end.  wbase: nw x 2 S^d doubles.
+// scattered at the end.  Interior anchors compute the indices from the slot-code table (one
+// LDS + the level table entry); boundary anchors take the general path.  The six one-axis
+// contractions are line-based (fd_pass).  wbase: nw x 2 S^d doubles.
 template <int S, int DIM>
 __device__ __forceinline__ void fd_loop(const PatchFdOp& op, const Tab& T, const double* tab, const int16_t* midx,
-                                        double* wbase, int w, int nw) {
+                                        const int* scode, double* wbase, int w, int nw) {
   constexpr int S2 = S * S, N3 = DIM == 3 ? S2 * S : S2;
   constexpr int NL = (N3 + 31) / 32;
   constexpr int tsz = S * S + S;
@@ -434,120 +493,72 @@ __device__ __forceinline__ void fd_loop(const PatchFdOp& op, const Tab& T, const
     const int A = op.anchors[i];
     const int vx = A % op.na[0], vy = (A / op.na[0]) % op.na[1], vz = A / (op.na[0] * op.na[1]);
     const int t = -op.blk[A] - 1;
-    const double sc = (t >> 12) ? op.inv_alpha : 1.0;
+    const double sc = ((t >> 12) ? op.inv_alpha : 1.0) / op.s_fac;
     const double* Tx = tab + (0 * op.ncls + op.cls[vx]) * tsz;
     const double* Ty = tab + (1 * op.ncls + op.cls[op.na[0] + vy]) * tsz;
     const double* Tz = tab + (2 * op.ncls + (DIM == 3 ? op.cls[op.na[0] + op.na[1] + vz] : 0)) * tsz;
+    const bool inner = vx >= 2 && vx <= op.nx - 2 && vy >= 2 && vy <= op.ny - 2 &&
+                       (DIM == 2 || (vz >= 2 && vz <= op.nz - 2));
     int ids[NL];
-    double xv[NL];
 #pragma unroll
     for (int j = 0; j < NL; ++j) {
       const int l = lane + 32 * j;
       int idx = -1;
       if (l < N3) {
-        const int sx = l % S, sy = (l / S) % S, sz = DIM == 3 ? l / S2 : 0;
-        int cx, kx, cy, ky, cz = 0, kz = 0;
-        fd_slot(sx, q, vx, op.nx, cx, kx);
-        fd_slot(sy, q, vy, op.ny, cy, ky);
-        if (DIM == 3) fd_slot(sz, q, vz, op.nz, cz, kz);
-        if (cx >= 0 && cy >= 0 && cz >= 0 && cx < op.nx && cy < op.ny && cz < op.nz) {
-          const int a = midx[(kz * (q + 1) + ky) * (q + 1) + kx];
-          if (dof_free(T, a, cx, cy, cz)) idx = dof_index(T, a, cx, cy, cz);
+        if (inner) {
+          const int code = scode[l];
+          const int4 g = T.g[code & 1023];
+          idx = g.x + (vx - ((code >> 10) & 1)) + (vy - ((code >> 11) & 1)) * g.y +
+                (DIM == 3 ? (vz - ((code >> 12) & 1)) * g.z : 0);
+        } else {
+          const int sx = l % S, sy = (l / S) % S, sz = DIM == 3 ? l / S2 : 0;
+          int cx, kx, cy, ky, cz = 0, kz = 0;
+          fd_slot(sx, q, vx, op.nx, cx, kx);
+          fd_slot(sy, q, vy, op.ny, cy, ky);
+          if (DIM == 3) fd_slot(sz, q, vz, op.nz, cz, kz);
+          if (cx >= 0 && cy >= 0 && cz >= 0 && cx < op.nx && cy < op.ny && cz < op.nz) {
+            const int a = midx[(kz * (q + 1) + ky) * (q + 1) + kx];
+            if (dof_free(T, a, cx, cy, cz)) idx = dof_index(T, a, cx, cy, cz);
+          }
         }
       }
       ids[j] = idx;
     }
+    {
+      double xv[NL];
 #pragma unroll
-    for (int j = 0; j < NL; ++j) xv[j] = ids[j] >= 0 ? __ldg(op.in + ids[j]) : 0.0;
+      for (int j = 0; j < NL; ++j) xv[j] = ids[j] >= 0 ? __ldg(op.in + ids[j]) : 0.0;
+#pragma unroll
+      for (int j = 0; j < NL; ++j)
+        if (lane + 32 * j < N3) X[lane + 32 * j] = xv[j];
+    }
+    __syncwarp();
+    // forward (S^T x S^T x S^T) X with the D^-1 scaling fused into the last axis, then backward
+    if (DIM == 3) {
+      fd_pass<S, DIM, 0, true, false>(X, Y, Tx, nullptr, nullptr, nullptr, 0.0);
+      __syncwarp();
+      fd_pass<S, DIM, 1, true, false>(Y, X, Ty, nullptr, nullptr, nullptr, 0.0);
+      __syncwarp();
+      fd_pass<S, DIM, 2, true, true>(X, Y, Tz, Tx + S2, Ty + S2, Tz + S2, sc);
+      __syncwarp();
+      fd_pass<S, DIM, 2, false, false>(Y, X, Tz, nullptr, nullptr, nullptr, 0.0);
+      __syncwarp();
+      fd_pass<S, DIM, 1, false, false>(X, Y, Ty, nullptr, nullptr, nullptr, 0.0);
+      __syncwarp();
+      fd_pass<S, DIM, 0, false, false>(Y, X, Tx, nullptr, nullptr, nullptr, 0.0);
+    } else {
+      fd_pass<S, DIM, 0, true, false>(X, Y, Tx, nullptr, nullptr, nullptr, 0.0);
+      __syncwarp();
+      fd_pass<S, DIM, 1, true, true>(Y, X, Ty, Tx + S2, Ty + S2, nullptr, sc);
+      __syncwarp();
+      fd_pass<S, DIM, 1, false, false>(X, Y, Ty, nullptr, nullptr, nullptr, 0.0);
+      __syncwarp();
+      fd_pass<S, DIM, 0, false, false>(Y, X, Tx, nullptr, nullptr, nullptr, 0.0);
+    }
+    __syncwarp();
 #pragma unroll
     for (int j = 0; j < NL; ++j)
-      if (lane + 32 * j < N3) X[lane + 32 * j] = xv[j];
-    __syncwarp();
-    // forward: Y = (S^T x S^T x S^T) X, one axis at a time
-#pragma unroll
-    for (int j = 0; j < NL; ++j) {
-      const int l = lane + 32 * j;
-      if (l >= N3) break;
-      const int jj = l % S, row = l - jj;
-      double s = 0.0;
-#pragma unroll
-      for (int ii = 0; ii < S; ++ii) s = fma(Tx[ii * S + jj], X[row + ii], s);
-      Y[l] = s;
-    }
-    __syncwarp();
-#pragma unroll
-    for (int j = 0; j < NL; ++j) {
-      const int l = lane + 32 * j;
-      if (l >= N3) break;
-      const int jj = (l / S) % S, off = l - jj * S;
-      double s = 0.0;
-#pragma unroll
-      for (int ii = 0; ii < S; ++ii) s = fma(Ty[ii * S + jj], Y[off + ii * S], s);
-      X[l] = s;
-    }
-    __syncwarp();
-    if (DIM == 3) {
-#pragma unroll
-      for (int j = 0; j < NL; ++j) {
-        const int l = lane + 32 * j;
-        if (l >= N3) break;
-        const int jj = l / S2, off = l - jj * S2;
-        double s = 0.0;
-#pragma unroll
-        for (int ii = 0; ii < S; ++ii) s = fma(Tz[ii * S + jj], X[off + ii * S2], s);
-        Y[l] = s;
-      }
-      __syncwarp();
-    }
-    const double* Z = DIM == 3 ? Y : X;   // forward result
-    double* U = DIM == 3 ? X : Y;         // scaled
-#pragma unroll
-    for (int j = 0; j < NL; ++j) {
-      const int l = lane + 32 * j;
-      if (l >= N3) break;
-      const int jx = l % S, jy = (l / S) % S, jz = DIM == 3 ? l / S2 : 0;
-      const double lam = Tx[S * S + jx] + Ty[S * S + jy] + (DIM == 3 ? Tz[S * S + jz] : 0.0);
-      U[l] = Z[l] * (sc / (op.s_fac * lam));
-    }
-    __syncwarp();
-    // backward: (S x S x S) U
-    double* V1 = U;
-    double* V2 = DIM == 3 ? Y : X;
-    if (DIM == 3) {
-#pragma unroll
-      for (int j = 0; j < NL; ++j) {
-        const int l = lane + 32 * j;
-        if (l >= N3) break;
-        const int ii = l / S2, off = l - ii * S2;
-        double s = 0.0;
-#pragma unroll
-        for (int jj = 0; jj < S; ++jj) s = fma(Tz[ii * S + jj], V1[off + jj * S2], s);
-        V2[l] = s;
-      }
-      __syncwarp();
-      double* tmp = V1; V1 = V2; V2 = tmp;
-    }
-#pragma unroll
-    for (int j = 0; j < NL; ++j) {
-      const int l = lane + 32 * j;
-      if (l >= N3) break;
-      const int ii = (l / S) % S, off = l - ii * S;
-      double s = 0.0;
-#pragma unroll
-      for (int jj = 0; jj < S; ++jj) s = fma(Ty[ii * S + jj], V1[off + jj * S], s);
-      V2[l] = s;
-    }
-    __syncwarp();
-#pragma unroll
-    for (int j = 0; j < NL; ++j) {
-      const int l = lane + 32 * j;
-      if (l >= N3) break;
-      const int ii = l % S, row = l - ii;
-      double s = 0.0;
-#pragma unroll
-      for (int jj = 0; jj < S; ++jj) s = fma(Tx[ii * S + jj], V2[row + jj], s);
-      if (ids[j] >= 0) atomicAdd(op.out + ids[j], coef * s);
-    }
+      if (ids[j] >= 0) atomicAdd(op.out + ids[j], coef * X[lane + 32 * j]);
     __syncwarp();
   }
 }
@@ -582,13 +593,18 @@ __global__ void __launch_bounds__((kIrrWarps + kFdWarps) * 32, 1) k_patch_smooth
   double* tab = reinterpret_cast<double*>(bars + kIrrWarps * kIrrStages);
   int16_t* midx = reinterpret_cast<int16_t*>(tab + 3 * fo.ncls * tsz);
   const int nmi = (fo.q + 1) * (fo.q + 1) * (fo.q + 1);
-  double* wbase = reinterpret_cast<double*>(reinterpret_cast<unsigned char*>(midx) + ((nmi * 2 + 15) / 16) * 16);
+  constexpr int N3 = DIM == 3 ? S * S * S : S * S;
+  int* scode = reinterpret_cast<int*>(reinterpret_cast<unsigned char*>(midx) + ((nmi * 2 + 15) / 16) * 16);
+  double* wbase = reinterpret_cast<double*>(reinterpret_cast<unsigned char*>(scode) + ((N3 * 4 + 15) / 16) * 16);
   const int w = threadIdx.x >> 5;
   load_tab_from(T, io.m, io.base, io.stride3, io.cmin, io.cmax);
   if (FD) {
     for (int e = threadIdx.x; e < 3 * fo.ncls * tsz; e += blockDim.x) tab[e] = fo.tabs[e];
     for (int e = threadIdx.x; e < nmi; e += blockDim.x) midx[e] = fo.modeidx[e];
   }
+  __syncthreads();
+  if (FD)
+    for (int l = threadIdx.x; l < N3; l += blockDim.x) scode[l] = fd_slot_code(l, S, fo.q, DIM, midx);
   if (IRR && w < kIrrWarps && (threadIdx.x & 31) == 0)
     for (int s = 0; s < kIrrStages; ++s) mbar_init(&bars[w * kIrrStages + s], 1);
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -603,7 +619,7 @@ __global__ void __launch_bounds__((kIrrWarps + kFdWarps) * 32, 1) k_patch_smooth
                (int64_t)gridDim.x * ngrp, w);
     }
   } else {
-    if (FD) fd_loop<S, DIM>(fo, T, tab, midx, wbase, w - kIrrWarps, kFdWarps);
+    if (FD) fd_loop<S, DIM>(fo, T, tab, midx, scode, wbase, w - kIrrWarps, kFdWarps);
   }
 }
 

@@ -477,16 +477,51 @@ def test_tiled_coarse_block_order_sums_bit_reproducible(case, monkeypatch):
     assert rel(pair.from_gpu(x1, 1), ref) <= 1e-10 and abs(it1 - H.coarse_iters[-1]) <= 1
 
 
-@pytest.mark.parametrize("env", [("FCM_PDL", "0"), ("FCM_HOST_LOOP", "1"), ("FCM_CELL_MMA", "0")])
-def test_fcg_fallback_switches(env, monkeypatch):
+@pytest.mark.parametrize("env", [("FCM_PDL", "0"), ("FCM_HOST_LOOP", "1"), ("FCM_CELL_MMA", "0"), ("FCM_CELL_WS", "0")])
+@pytest.mark.parametrize("case", ["3d_p2", "3d_p3_ragged"])
+def test_fcg_fallback_switches(env, case, monkeypatch):
     # the non-default launch modes (no programmatic dependent launch; per-iteration host loop;
-    # generic cell kernels instead of the fp64-MMA groups) against the oracle (L5)
+    # generic cell kernels instead of the fp64-MMA groups; k_cell_mma blocks instead of the
+    # warp-specialised launch with tile-packed individual matrices) against the oracle (L5)
     monkeypatch.setenv(*env)
-    pair = Pair(CASES["3d_p2"]())
+    pair = Pair(CASES[case]())
     xo, ito, _ = pair.hier().fcg(pair.P.b)
     x, it, hist = pair.S.pcg_solve(pair.to_gpu(pair.P.b))
     assert abs(it - ito) <= 1 and hist[-1] < pair.cfg.rtol
     assert rel(pair.from_gpu(x), xo) <= 1e-8
+
+
+@pytest.mark.parametrize("case", ["3d_p3_ragged", "3d_p4_elem", "3d_p2"])
+def test_ws_single_cta(case, monkeypatch):
+    # the warp-specialised cell launch (cellws.cuh) with ONE CTA: every streaming warp walks many
+    # cells, so the bulk-copy ring runs across cell boundaries and partial (prefix) tiles of the
+    # fine cut-cell copy; operator at every level (L1) and one smoother sweep on identical setup (L2)
+    monkeypatch.setenv("FCM_WS_CTAS", "1")
+    pair = Pair(CASES[case]())
+    rng = np.random.default_rng(5)
+    x = rng.standard_normal(pair.P.dof.ndof)
+    for q in range(1, pair.cfg.p + 1):
+        I = pair.P.dof.level_dofs(q)
+        xq = np.zeros_like(x)
+        xq[I] = x[I]
+        ref = np.zeros_like(x)
+        ref[I] = pair.P.A[I][:, I] @ x[I]
+        y = pair.from_gpu(pair.S.apply(pair.to_gpu(xq, q), q), q)
+        assert rel(y, ref) <= 1e-13, q
+    Hi = pair.hier_identical()
+    for q, lv in Hi.levels.items():
+        if q == 1 or not hasattr(lv, "blocks"):
+            continue
+        r = np.zeros(pair.P.dof.ndof)
+        r[lv.idx] = rng.standard_normal(lv.n)
+        ref = np.zeros_like(r)
+        ref[lv.idx] = lv.omega * lv.schwarz(r[lv.idx])
+        xs = torch.zeros(pair.S.ndofs(q), dtype=torch.float64, device="cuda")
+        pair.S.smooth(pair.to_gpu(r, q), xs, q)
+        assert rel(pair.from_gpu(xs, q), ref) <= 1e-12, q
+    xo, ito, _ = pair.hier().fcg(pair.P.b)
+    xg, it, hist = pair.S.pcg_solve(pair.to_gpu(pair.P.b))
+    assert abs(it - ito) <= 1 and rel(pair.from_gpu(xg), xo) <= 1e-8
 
 
 def test_maxit_zero_and_bad_vectors():
