@@ -33,6 +33,8 @@ struct MmaOp {
   int64_t cp_n;
 };
 
+// volatile: mma.sync.aligned must stay in warp-converged code (a non-volatile asm may be
+// duplicated into divergent branch arms); the callers order independent chains explicitly
 __device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, double b, double c0, double c1) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%4,%5};"
                : "=d"(d0), "=d"(d1)
@@ -70,7 +72,7 @@ __device__ __forceinline__ void stage_fragments(double* As, const double* K, int
   }
 }
 
-template <int M, bool FUSE = false>
+template <int M, bool FUSE = false, bool PF = false>
 __device__ __forceinline__ double mma_cells(const CellOp& op, const int32_t* __restrict__ grp_cells,
                                             const int32_t* __restrict__ grp_mat, int64_t ngroups,
                                             const Tab& T, const double* __restrict__ As,
@@ -81,48 +83,71 @@ __device__ __forceinline__ double mma_cells(const CellOp& op, const int32_t* __r
   const int ar = lane >> 2, ac = lane & 3;
   double energy = 0.0;
   const bool want_e = op.partials != nullptr;
-  // the next group's descriptor is loaded one trip ahead (software pipelining: its latency
-  // overlaps this group's gathers and MMAs)
-  int n_slot = 0, n_cg = -1, n_c0 = -1, n_c1 = -1;
-  if (warp < ngroups) {
-    const int* cells = grp_cells + (int64_t)warp * 8;
-    n_slot = __ldg(grp_mat + warp);
-    n_cg = __ldg(cells + ar); n_c0 = __ldg(cells + 2 * ac); n_c1 = __ldg(cells + 2 * ac + 1);
-  }
-  for (int64_t gi = warp; gi < ngroups; gi += nwarps) {
-    const int slot = n_slot;   // warp-uniform
-    const int cg = n_cg;       // B column / gather cell of this lane
-    const int c0 = n_c0, c1 = n_c1;   // output cells
-    if (gi + nwarps < ngroups) {
-      const int* cells = grp_cells + (gi + nwarps) * 8;
-      n_slot = __ldg(grp_mat + gi + nwarps);
-      n_cg = __ldg(cells + ar); n_c0 = __ldg(cells + 2 * ac); n_c1 = __ldg(cells + 2 * ac + 1);
-    }
-    // gather: B[kt] = x[dof kt*4 + ac] of cell cg
-    double B[KT];
+  // software pipeline: the descriptor of the group two trips ahead and the gathered column of
+  // the next group are loaded while this group's MMAs run (the gather latency is hidden)
+  int n_slot = 0, n_cg = -1, n_c0 = -1, n_c1 = -1;   // next group
+  int m_slot = 0, m_cg = -1, m_c0 = -1, m_c1 = -1;   // the one after
+  auto load_desc = [&](int64_t g, int& sl, int& cg, int& c0, int& c1) {
+    const int* cells = grp_cells + g * 8;
+    sl = __ldg(grp_mat + g);
+    cg = __ldg(cells + ar); c0 = __ldg(cells + 2 * ac); c1 = __ldg(cells + 2 * ac + 1);
+  };
+  double Bn[KT];
+  auto gather = [&](int cg) {   // Bn[kt] = x[dof kt*4 + ac] of cell cg
 #pragma unroll
     for (int kt = 0; kt < KT; ++kt) {
       const int idx = mma_dof_index<M>(T, kt * 4 + ac, cg);
-      B[kt] = idx >= 0 ? load_in<FUSE>(op, idx) : 0.0;
+      Bn[kt] = idx >= 0 ? load_in<FUSE>(op, idx) : 0.0;
     }
+  };
+  // (PF = false, register-tight kernels: only the descriptor runs one trip ahead)
+  if (warp < ngroups) load_desc(warp, n_slot, n_cg, n_c0, n_c1);
+  if (warp + nwarps < ngroups) load_desc(warp + nwarps, m_slot, m_cg, m_c0, m_c1);
+  if (PF) gather(n_cg);
+  for (int64_t gi = warp; gi < ngroups; gi += nwarps) {
+    const int slot = n_slot;   // warp-uniform
+    const int c0 = n_c0, c1 = n_c1;   // output cells
+    if (!PF) gather(n_cg);
+    double B[KT];
+#pragma unroll
+    for (int kt = 0; kt < KT; ++kt) B[kt] = Bn[kt];
+    n_slot = m_slot; n_cg = m_cg; n_c0 = m_c0; n_c1 = m_c1;
+    if (gi + 2 * nwarps < ngroups) load_desc(gi + 2 * nwarps, m_slot, m_cg, m_c0, m_c1);
+    if (PF && gi + nwarps < ngroups) gather(n_cg);
     const double s0 = op.coef * cell_scale(op, c0), s1 = op.coef * cell_scale(op, c1);
     const bool main = slot == main_slot;
     const double* K = slot < 0 ? op.Kref : op.type_inv + (size_t)slot * M * M;
     const int ld = slot < 0 ? op.ldK : M;
+    // row tiles in chunks of RC: k-steps outer, row tiles inner, so consecutive MMAs are
+    // independent (RC accumulator pairs) instead of one dependent chain per row tile
+    constexpr int RC = (PF && KT > 8) ? (MT < 4 ? MT : 4) : (MT < 8 ? MT : 8);
 #pragma unroll
-    for (int rt = 0; rt < MT; ++rt) {
-      double d0 = 0.0, d1 = 0.0;
+    for (int rb = 0; rb < MT; rb += RC) {
+    double D[RC][2];
 #pragma unroll
-      for (int kt = 0; kt < KT; ++kt) {
-        double af;
-        if (main) {
-          af = As[(rt * KT + kt) * 32 + lane];
-        } else {
-          const int r = rt * 8 + ar, k = kt * 4 + ac;
-          af = (r < M && k < M) ? __ldg(K + r * ld + k) : 0.0;
-        }
-        dmma_8x8x4(d0, d1, af, B[kt], d0, d1);
-      }
+    for (int u = 0; u < RC; ++u) D[u][0] = D[u][1] = 0.0;
+    if (main) {
+#pragma unroll
+      for (int kt = 0; kt < KT; ++kt)
+#pragma unroll
+        for (int u = 0; u < RC; ++u)
+          if (rb + u < MT) dmma_8x8x4(D[u][0], D[u][1], As[((rb + u) * KT + kt) * 32 + lane], B[kt], D[u][0], D[u][1]);
+    } else {
+#pragma unroll
+      for (int kt = 0; kt < KT; ++kt)
+#pragma unroll
+        for (int u = 0; u < RC; ++u)
+          if (rb + u < MT) {
+            const int r = (rb + u) * 8 + ar, k = kt * 4 + ac;
+            const double af = (r < M && k < M) ? __ldg(K + r * ld + k) : 0.0;
+            dmma_8x8x4(D[u][0], D[u][1], af, B[kt], D[u][0], D[u][1]);
+          }
+    }
+#pragma unroll
+    for (int u = 0; u < RC; ++u) {
+      const int rt = rb + u;
+      if (rt >= MT) break;
+      const double d0 = D[u][0], d1 = D[u][1];
       const int a = rt * 8 + ar;
       const int i0 = mma_dof_index<M>(T, a, c0), i1 = mma_dof_index<M>(T, a, c1);
       double x0 = 0.0, x1 = 0.0;
@@ -146,6 +171,7 @@ __device__ __forceinline__ double mma_cells(const CellOp& op, const int32_t* __r
         atomicAdd(op.out + i1, s1 * d1);
         if (want_e) energy = fma(x1, s1 / op.coef * d1, energy);
       }
+    }
     }
   }
   return energy;

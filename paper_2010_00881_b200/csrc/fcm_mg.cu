@@ -113,8 +113,10 @@ struct LevelDev {
   int64_t nS = 0;
   // warp-specialised launch (cellws.cuh): MMA warps for the regular cells + streaming warps for
   // the tile-packed individual matrices (operator: the fine cut-cell copy; smoother: irr_tp)
-  const void* kws = nullptr;
-  int ws_ns = 0;                   // streaming warps per CTA
+  const void* kws = nullptr;       // the level has warp-specialised launches (= kws_m[OP_APPLY])
+  const void* kws_m[2] = {nullptr, nullptr};   // per mode (OP_APPLY / OP_SMOOTH): warp split variant
+  int ws_threads[2] = {0, 0};      // threads per CTA
+  size_t ws_smem_b[2] = {0, 0};    // dynamic smem
   int ntq = 0;                     // 32-tiles per dimension of the level block (ceil(m / 32))
   double* irr_tp = nullptr;        // tile-packed individual elementwise inverses (replaces irr_inv)
   int64_t irr_tps = 0;             // doubles per packed inverse
@@ -243,6 +245,19 @@ struct fcm_mg {
   int64_t n_coarse_g = 0;
   bool gmg_child = false;
   int64_t* c_extract = nullptr;     // [ndof_1 local] global level-1 slot
+  // slab mode + h-coarsening (FCM_COARSE_GMG_PCG): DISTRIBUTED coarse solve -- the p=1 level
+  // stays z-slab partitioned ("reuse the parallel data structures"), the coarse CG and the
+  // h-level-0 smoothing run on the slabs with the interface exchange and all-reduced dots; the
+  // restricted residual of h-level 1 is all-reduced and the geometric V-cycle below it runs
+  // replicated (hg's h-levels).  The coarse CG is host-driven (one small D2H per iteration), so
+  // the slab V-cycle/FCG run eagerly (no graphs: NCCL work stays out of conditional nodes).
+  bool dist = false;
+  bool eager = false;
+  std::map<const void*, std::function<int()>> eager_fn;   // capture() bodies in eager mode
+  double* d_dcg = nullptr;          // [8] reduced scalars of the distributed coarse CG
+  double* h_dcg = nullptr;          // pinned copy
+  int* h_ci = nullptr;              // pinned {iterations of the last coarse solve, total}
+  int dist_cz0 = 0, dist_cz1 = 0;   // global coarse (h-level 1) vertex layers this slab restricts to
   double* c_bg = nullptr;
   double* c_xg = nullptr;
 
@@ -261,8 +276,11 @@ struct fcm_mg {
   }
   ~fcm_mg();
   void release() {
-    for (auto g : {g_vc, g_it1, g_it2, g_init, g_mgit, g_solve})
-      if (g) cudaGraphExecDestroy(g);
+    if (!eager)   // eager mode stores sentinels, not graphs
+      for (auto g : {g_vc, g_it1, g_it2, g_init, g_mgit, g_solve})
+        if (g) cudaGraphExecDestroy(g);
+    if (h_dcg) cudaFreeHost(h_dcg);
+    if (h_ci) cudaFreeHost(h_ci);
     for (void* p : allocs) cudaFree(p);
     if (h_s) cudaFreeHost(h_s);
     if (h_iters) cudaFreeHost(h_iters);
@@ -349,21 +367,21 @@ __global__ void __launch_bounds__(kThreads, M > 32 ? 2 : 4) k_cell_mma(MmaOp g, 
 }
 
 // One cell operation as a warp-specialised persistent launch (cellws.cuh): warps [0, NS) stream
-// the tile-packed individual matrices, warps [NS, NS + kWsMmaWarps) run the regular cells as fp64
-// MMA groups.  smem [Tab][A fragments][ring: NS x kIrrStages x 8 KB][mbarriers][xs, ys, ids].
-template <int M, int NS>
+// the tile-packed individual matrices through STG-deep rings, warps [NS, NS + NM) run the regular
+// cells as fp64 MMA groups.  smem [Tab][A fragments][ring: NS x STG x 8 KB][mbarriers][xs, ys, ids].
+template <int M, int NS, int NM, int STG, bool PF = true>
 __host__ __device__ constexpr size_t ws_smem() {
-  return sizeof(Tab) + (size_t)((M + 7) / 8) * ((M + 3) / 4) * 32 * 8 + ws_stream_smem((M + 31) / 32, NS);
+  return sizeof(Tab) + (size_t)((M + 7) / 8) * ((M + 3) / 4) * 32 * 8 + ws_stream_smem((M + 31) / 32, NS, STG);
 }
-template <int M, int NS>
-__global__ void __launch_bounds__((NS + kWsMmaWarps) * 32, 1) k_cell_ws(MmaOp g, TileListOp tl) {
+template <int M, int NS, int NM, int STG, bool PF>
+__global__ void __launch_bounds__((NS + NM) * 32, 1) k_cell_ws(MmaOp g, TileListOp tl) {
   extern __shared__ __align__(16) unsigned char smem[];
   constexpr int MT = (M + 7) / 8, KT = (M + 3) / 4;
   Tab& T = *reinterpret_cast<Tab*>(smem);
   double* As = reinterpret_cast<double*>(smem + sizeof(Tab));
   double* ring = As + MT * KT * 32;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(ring + (size_t)NS * kIrrStages * 1024);
-  double* xs0 = reinterpret_cast<double*>(bars + NS * kIrrStages);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(ring + (size_t)NS * STG * 1024);
+  double* xs0 = reinterpret_cast<double*>(bars + NS * STG);
   __shared__ double red[32];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int MPd = 32 * tl.ntq;
@@ -374,24 +392,24 @@ __global__ void __launch_bounds__((NS + kWsMmaWarps) * 32, 1) k_cell_ws(MmaOp g,
   const bool apply = g.op.mode == OP_APPLY;
   stage_fragments<M>(As, apply ? g.op.Kref : g.op.type_inv, apply ? g.op.ldK : M);
   if (w < NS && lane == 0)
-    for (int s = 0; s < kIrrStages; ++s) mbar_init(&bars[w * kIrrStages + s], 1);
+    for (int s = 0; s < STG; ++s) mbar_init(&bars[w * STG + s], 1);
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   __syncthreads();
   if (w < NS && lane == 0) {   // the first tiles: setup data, so before griddepcontrol.wait
     const int64_t nitems = (tl.nlist > gw ? (tl.nlist - gw + W - 1) / W : 0) * ntl;
-    for (int64_t i = 0; i < kIrrStages && i < nitems; ++i)
-      ws_issue(tl, ntl, gw, W, i, ring + (size_t)w * kIrrStages * 1024, bars + w * kIrrStages, g.op.m);
+    for (int64_t i = 0; i < STG && i < nitems; ++i)
+      ws_issue<STG>(tl, ntl, gw, W, i, ring + (size_t)w * STG * 1024, bars + w * STG, g.op.m);
   }
   asm volatile("griddepcontrol.wait;" ::: "memory");
   double e;
   if (w < NS) {
     double* xs = xs0 + (size_t)w * MPd * 2;
     int* ids = reinterpret_cast<int*>(xs0 + (size_t)NS * MPd * 2) + (size_t)w * MPd;
-    e = ws_stream_cells(g.op, tl, T, xs, xs + MPd, ids, ring + (size_t)w * kIrrStages * 1024, bars + w * kIrrStages,
-                        gw, W);
+    e = ws_stream_cells<(M + 31) / 32, STG>(g.op, tl, T, xs, xs + MPd, ids, ring + (size_t)w * STG * 1024,
+                                            bars + w * STG, gw, W);
   } else {
-    e = mma_cells<M>(g.op, g.grp_cells, g.grp_mat, g.ngroups, T, As, apply ? -1 : 0,
-                     blockIdx.x * kWsMmaWarps + (w - NS), gridDim.x * kWsMmaWarps);
+    e = mma_cells<M, false, PF && (M + 3) / 4 <= 16>(g.op, g.grp_cells, g.grp_mat, g.ngroups, T, As, apply ? -1 : 0,
+                                               blockIdx.x * NM + (w - NS), gridDim.x * NM);
   }
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < g.cp_n; i += (int64_t)gridDim.x * blockDim.x)
     g.cp_dst[i] = g.cp_src[i];
@@ -703,6 +721,75 @@ __global__ void k_gmg_prolong(double* __restrict__ xf, const double* __restrict_
     xf[i] += s;
   }
 }
+// distributed h-coarsening (slab mode): partial restriction of this slab's OWNED fine vertices
+// (local slab-axis index >= own_lo) into the global coarse layers [cz0, cz1); the caller zeroes
+// the global vector first and all-reduces it after (sum over slabs = P^T r of the whole grid)
+__global__ void k_gmg_restrict_dist(double* __restrict__ bc, const double* __restrict__ rf, GmgBox C, GmgBox F,
+                                    int dim, int zoff, int own_lo, int cz0, int cz1) {
+  const int ax = dim - 1;
+  for (int c = 0; c < C.nf; ++c) {
+    int64_t plane = 1;
+    for (int a = 0; a < ax; ++a) plane *= C.size[c][a];
+    const int z0 = max(cz0, C.lo[c][ax]), z1 = min(cz1, C.lo[c][ax] + C.size[c][ax]);
+    const int64_t n = z0 < z1 ? plane * (z1 - z0) : 0;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
+      int X[3] = {0, 0, 0};
+      int64_t u = t;
+      for (int a = 0; a < ax; ++a) { X[a] = (int)(u % C.size[c][a]) + C.lo[c][a]; u /= C.size[c][a]; }
+      X[ax] = z0 + (int)u;
+      double s = 0.0;
+      const int dz0 = dim == 3 ? -1 : 0, dz1 = dim == 3 ? 1 : 0;
+      for (int dz = dz0; dz <= dz1; ++dz)
+        for (int dy = -1; dy <= 1; ++dy)
+          for (int dx = -1; dx <= 1; ++dx) {
+            int x[3] = {2 * X[0] + dx, 2 * X[1] + dy, dim == 3 ? 2 * X[2] + dz : 0};
+            x[ax] -= zoff;   // global -> local slab index
+            if (x[ax] < own_lo || !gmg_in(F, c, x)) continue;
+            const double w = (dx ? 0.5 : 1.0) * (dy ? 0.5 : 1.0) * (dz ? 0.5 : 1.0);
+            s = fma(w, rf[gmg_index(F, c, x)], s);
+          }
+      bc[gmg_index(C, c, X)] = s;
+    }
+  }
+}
+// x_local += P e_coarse (replicated e): every local fine vertex, interface planes included
+__global__ void k_gmg_prolong_dist(double* __restrict__ xf, const double* __restrict__ ec, GmgBox F, GmgBox C,
+                                   int dim, int zoff, int64_t nfine) {
+  const int ax = dim - 1;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nfine; i += (int64_t)gridDim.x * blockDim.x) {
+    int c, x[3];
+    gmg_decode(F, i, c, x);
+    x[ax] += zoff;   // local -> global
+    double s = 0.0;
+    const int nz = (dim == 3 && (x[2] & 1)) ? 2 : 1, ny = (x[1] & 1) ? 2 : 1, nx = (x[0] & 1) ? 2 : 1;
+    for (int kz = 0; kz < nz; ++kz)
+      for (int ky = 0; ky < ny; ++ky)
+        for (int kx = 0; kx < nx; ++kx) {
+          const int X[3] = {(x[0] - (nx - 1)) / 2 + kx, (x[1] - (ny - 1)) / 2 + ky, (x[2] - (nz - 1)) / 2 + kz};
+          if (!gmg_in(C, c, X)) continue;
+          s = fma((nx == 2 ? 0.5 : 1.0) * (ny == 2 ? 0.5 : 1.0) * (nz == 2 ? 0.5 : 1.0), ec[gmg_index(C, c, X)], s);
+        }
+    xf[i] += s;
+  }
+}
+// distributed coarse CG updates from all-reduced scalars d[]: {rz, pq, rr, rz_new, rr0}
+__global__ void k_dcg_update(const double* __restrict__ d, double* __restrict__ x, double* __restrict__ r,
+                             const double* __restrict__ p, const double* __restrict__ q, int64_t n) {
+  const double a = d[0] / d[1];
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    x[i] = fma(a, p[i], x[i]);
+    r[i] = fma(-a, q[i], r[i]);
+  }
+}
+__global__ void k_dcg_update2(double* __restrict__ d, double* __restrict__ p, const double* __restrict__ z, int64_t n) {
+  const double beta = d[3] / d[0];
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = fma(beta, p[i], z[i]);
+}
+__global__ void k_dcg_setrz(double* d) {
+  if (threadIdx.x == 0) d[0] = d[3];
+}
+
 // coarse CG (standard PCG, P:343 form) around the geometric V-cycle; the loop is a device-side
 // WHILE node, the V-cycle + beta part an IF node inside it (both set by k_gcg_check)
 __global__ void k_gcg_init(GcgScalars* s, const double* pA, const double* pB, int np, double* p, const double* z,
@@ -871,13 +958,28 @@ const void* mma_kernel(int m) {
 }
 // warp-specialised cell kernel (cellws.cuh) for the elementwise levels that carry most bytes:
 // m = 27 / 64 / 125 (tensor p = 2 / 3 / 4); *ns = its streaming warps, *smem its dynamic smem
-const void* ws_kernel(int m, int* ns, size_t* smem) {
+// variant (FCM_WS_VARIANT, measurement): 0 = 8 streaming warps x 2 stages + 8 MMA warps with
+// the gather prefetch; 1 = the same without the prefetch; 2 = 4 streaming warps x 4 stages + 12
+// MMA warps (prefetch); 3 = 2 without the prefetch
+const void* ws_kernel(int m, int variant, int* nthreads, size_t* smem) {
+#define WS(MM, NS, NM, STG, PF) \
+  { *nthreads = (NS + NM) * 32; *smem = ws_smem<MM, NS, NM, STG>(); return (const void*)k_cell_ws<MM, NS, NM, STG, PF>; }
+#define WSV(MM) \
+  case MM: \
+    switch (variant) { \
+      case 1: WS(MM, 8, 8, 2, false) \
+      case 2: WS(MM, 4, 12, 4, true) \
+      case 3: WS(MM, 4, 12, 4, false) \
+      default: WS(MM, 8, 8, 2, true) \
+    }
   switch (m) {
-    case 27: *ns = 8; *smem = ws_smem<27, 8>(); return (const void*)k_cell_ws<27, 8>;
-    case 64: *ns = 8; *smem = ws_smem<64, 8>(); return (const void*)k_cell_ws<64, 8>;
-    case 125: *ns = 4; *smem = ws_smem<125, 4>(); return (const void*)k_cell_ws<125, 4>;
+    WSV(27)
+    WSV(64)
+    case 125: WS(125, 4, 8, 2, false)
     default: break;
   }
+#undef WSV
+#undef WS
   return nullptr;
 }
 const void* list_kernel(int G) {
@@ -1060,18 +1162,15 @@ static int launch_cellop(fcm_mg* h, int q, const CellOp& op, double* cp_dst = nu
     void* args[] = {&g, &tl};
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(h->ws_ctas);
-    cfg.blockDim = dim3((Lv.ws_ns + kWsMmaWarps) * 32);
-    int ns;
-    size_t sm;
-    ws_kernel(Lv.m, &ns, &sm);
-    cfg.dynamicSmemBytes = sm;
+    cfg.blockDim = dim3(Lv.ws_threads[op.mode]);
+    cfg.dynamicSmemBytes = Lv.ws_smem_b[op.mode];
     cfg.stream = h->stream;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = h->pdl ? 1 : 0;
-    cudaError_t e = cudaLaunchKernelExC(&cfg, Lv.kws, args);
+    cudaError_t e = cudaLaunchKernelExC(&cfg, Lv.kws_m[op.mode], args);
     h->count();
     if (e != cudaSuccess) return fail(FCM_ECUDA, "ws kernel launch: %s", cudaGetErrorString(e));
     return FCM_OK;
@@ -1355,8 +1454,9 @@ static int enqueue_coarse_slab(fcm_mg* h, const double* b, double* x) {
 }
 
 static int enqueue_coarse_gmg(fcm_mg* h, const double* b, double* x);
+static int coarse_dist(fcm_mg* h, const double* b, double* x);
 static int enqueue_coarse(fcm_mg* h, const double* b, double* x) {
-  if (h->hg) return enqueue_coarse_slab(h, b, x);
+  if (h->hg) return h->dist ? coarse_dist(h, b, x) : enqueue_coarse_slab(h, b, x);
   if (h->prm.coarse == FCM_COARSE_GMG_PCG) return enqueue_coarse_gmg(h, b, x);
   LevelDev& L1 = h->lev[1];
   const int64_t n = L1.ndof;
@@ -1590,6 +1690,116 @@ static int enqueue_coarse_gmg(fcm_mg* h, const double* b, double* x) {
   return rc;
 }
 
+// ---- distributed coarse solve (slab mode, FCM_COARSE_GMG_PCG) -------------------------------
+// owner-masked dot of two local level-1 vectors, all-reduced into d[slot]
+static int dot_dist(fcm_mg* h, const double* a, const double* b, int64_t n, int slot) {
+  const int nbd = dot_blocks(h);
+  k_dot<<<nbd, kThreads, 0, h->stream>>>(a, b, n, h->d_partA, h->d_own);
+  k_finalize<<<1, 32, 0, h->stream>>>(h->d_dcg + slot, h->d_partA, nbd);
+  h->count(2);
+  CU(cudaGetLastError());
+  return allreduce(h, h->d_dcg + slot, 1);
+}
+// damped level-1 AS sweep on the slab: x += w M^-1 r (increment summed over the interface)
+static int smooth_dist(fcm_mg* h, const double* r, double* x, double w, bool x_is_zero) {
+  LevelDev& L1 = h->lev[1];
+  if (x_is_zero) {
+    RC(launch_cellop(h, 1, make_op(h, 1, OP_SMOOTH, r, x, w, nullptr)));
+    return exchange(h, 1, x);
+  }
+  RC(fill(h, L1.d, 0.0, L1.ndof));
+  RC(launch_cellop(h, 1, make_op(h, 1, OP_SMOOTH, r, L1.d, w, nullptr)));
+  RC(exchange(h, 1, L1.d));
+  k_axpy<<<grid_for(L1.ndof, h->num_sms), kThreads, 0, h->stream>>>(x, 1.0, L1.d, L1.ndof);
+  h->count();
+  CU(cudaGetLastError());
+  return FCM_OK;
+}
+// geometric V-cycle with h-level 0 on the slabs (same steps as gmg_vcycle at i = 0) and the
+// levels below replicated (the global handle's gmg_vcycle from h-level 1)
+static int gmg_vcycle_dist(fcm_mg* h, const double* b, double* x) {
+  fcm_mg* hg = h->hg;
+  LevelDev& L1 = h->lev[1];
+  const int64_t n = L1.ndof;
+  double* r = L1.r;
+  const double w = hg->gmg_omega;
+  RC(fill(h, x, 0.0, n));
+  for (int s2 = 0; s2 < h->prm.n_pre; ++s2) {
+    if (s2 == 0) { RC(smooth_dist(h, b, x, w, true)); continue; }
+    RC(residual(h, 1, b, x, r));
+    RC(smooth_dist(h, r, x, w, false));
+  }
+  RC(residual(h, 1, b, x, r));
+  fcm_mg* c1 = hg->gmg[0];
+  const int64_t nc = c1->lev[1].ndof;
+  const GmgBox F = gmg_box(h->L), C = gmg_box(c1->L);
+  CU(cudaMemsetAsync(hg->gmg_b[1], 0, nc * 8, h->stream));
+  k_gmg_restrict_dist<<<grid_for(nc, h->num_sms), kThreads, 0, h->stream>>>(
+      hg->gmg_b[1], r, C, F, h->L.dim, h->z0, h->rank > 0 ? 1 : 0, h->dist_cz0, h->dist_cz1);
+  h->count();
+  CU(cudaGetLastError());
+  RC(allreduce(h, hg->gmg_b[1], (int)nc));
+  hg->count_target = h->count_target;
+  const int rc = gmg_vcycle(hg, 1, hg->gmg_b[1], hg->gmg_x[1]);
+  h->launches += hg->launches;
+  hg->launches = 0;
+  hg->count_target = nullptr;
+  RC(rc);
+  k_gmg_prolong_dist<<<grid_for(n, h->num_sms), kThreads, 0, h->stream>>>(x, hg->gmg_x[1], F, C, h->L.dim, h->z0, n);
+  h->count();
+  CU(cudaGetLastError());
+  for (int s2 = 0; s2 < h->prm.n_post; ++s2) {
+    RC(residual(h, 1, b, x, r));
+    RC(smooth_dist(h, r, x, w, false));
+  }
+  return FCM_OK;
+}
+// x = A_1^{-1} b by CG + the geometric V-cycle on the slabs, ||r|| < rtol ||r0|| (reading R4);
+// host-driven: one D2H of the reduced scalars per iteration (eager mode)
+static int coarse_dist(fcm_mg* h, const double* b, double* x) {
+  const int64_t n = h->lev[1].ndof;
+  double *r = h->c_vec[0], *z = h->c_vec[1], *pv = h->c_vec[2], *q = h->c_vec[3];
+  const int g = grid_for(n, h->num_sms);
+  k_fcg_start<<<g, kThreads, 0, h->stream>>>(x, r, b, n);
+  h->count();
+  RC(gmg_vcycle_dist(h, r, z));
+  RC(dot_dist(h, r, z, n, 0));   // rz
+  RC(dot_dist(h, r, r, n, 4));   // rr0
+  RC(copy(h, pv, z, n));
+  CU(cudaMemcpyAsync(h->h_dcg, h->d_dcg, 8 * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+  CU(cudaStreamSynchronize(h->stream));
+  const double rr0 = h->h_dcg[4];
+  const double rtol2 = h->prm.coarse_rtol * h->prm.coarse_rtol;
+  int it = 0;
+  if (rr0 > 0.0 && h->prm.coarse_maxit > 0) {
+    while (true) {
+      RC(fill(h, q, 0.0, n));
+      RC(launch_cellop(h, 1, make_op(h, 1, OP_APPLY, pv, q, 1.0, nullptr)));
+      RC(exchange(h, 1, q));
+      RC(dot_dist(h, pv, q, n, 1));   // pq
+      k_dcg_update<<<g, kThreads, 0, h->stream>>>(h->d_dcg, x, r, pv, q, n);
+      h->count();
+      RC(dot_dist(h, r, r, n, 2));    // rr
+      CU(cudaMemcpyAsync(h->h_dcg, h->d_dcg, 8 * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+      CU(cudaStreamSynchronize(h->stream));
+      ++it;
+      const double pq = h->h_dcg[1], rr = h->h_dcg[2];
+      if (!(pq > 0.0) || !(rr == rr) || rr < rtol2 * rr0 || it >= h->prm.coarse_maxit) break;
+      RC(gmg_vcycle_dist(h, r, z));
+      RC(dot_dist(h, r, z, n, 3));    // rz_new
+      k_dcg_update2<<<g, kThreads, 0, h->stream>>>(h->d_dcg, pv, z, n);
+      k_dcg_setrz<<<1, 32, 0, h->stream>>>(h->d_dcg);
+      h->count(2);
+      CU(cudaGetLastError());
+    }
+  }
+  h->h_ci[0] = it;
+  h->h_ci[1] += it;
+  CU(cudaMemcpyAsync(h->hg->d_coarse_iters, h->h_ci, 2 * sizeof(int), cudaMemcpyHostToDevice, h->stream));
+  CU(cudaStreamSynchronize(h->stream));   // h_ci is reused by the next solve
+  return FCM_OK;
+}
+
 // build the h-levels: Galerkin element matrices K_C = sum_f W_f^T K_f W_f of every coarse cell
 // (W_f: trilinear weights of the coarse cell's 2^d vertices at child f's vertices, (x) I_nf), a
 // child handle per level (p = 1 grid, its own elementwise AS); the coarsest solves directly
@@ -1784,6 +1994,12 @@ static int enqueue_vcycle(fcm_mg* h, int q, const double* b, double* x) {
 template <typename F>
 static int capture(fcm_mg* h, cudaGraphExec_t* exec, int64_t* nkernels, F&& body) {
   if (*exec) return FCM_OK;
+  if (h->eager) {   // keep the body (it must capture by value); run_graph calls it
+    h->eager_fn[(const void*)exec] = std::function<int()>(body);
+    *exec = reinterpret_cast<cudaGraphExec_t>(exec);
+    *nkernels = 0;
+    return FCM_OK;
+  }
   cudaGraph_t graph;
   *nkernels = 0;
   h->count_target = nkernels;
@@ -1800,6 +2016,11 @@ static int capture(fcm_mg* h, cudaGraphExec_t* exec, int64_t* nkernels, F&& body
 }
 
 static int run_graph(fcm_mg* h, cudaGraphExec_t g, int64_t nk) {
+  if (h->eager) {
+    auto it = h->eager_fn.find((const void*)g);
+    if (it == h->eager_fn.end()) return fail(FCM_EINVAL, "internal: eager body missing");
+    return it->second();
+  }
   CU(cudaGraphLaunch(g, h->stream));
   h->launches += nk;
   return FCM_OK;
@@ -2967,12 +3188,16 @@ static int setup_impl(const fcm_grid* g, const fcm_params* prm, const fcm_slab* 
       }
     }
     if (Lv.kmma && q >= 2 && !(getenv("FCM_CELL_WS") && atoi(getenv("FCM_CELL_WS")) == 0)) {
-      size_t wsm = 0;
-      Lv.kws = ws_kernel(Lv.m, &Lv.ws_ns, &wsm);
-      if (Lv.kws) {
-        Lv.ntq = (Lv.m + 31) / 32;
-        RC(allow_smem(Lv.kws, wsm));
+      // measured on config 5 (profiles/r02_s2_ws_variants_cfg5.json): the operator is bound by its
+      // MMA warps (12 MMA + 4 streaming warps), the smoother by its streaming warps (8 + 8)
+      const char* ev = getenv("FCM_WS_VARIANT");
+      for (int mode = 0; mode < 2; ++mode) {
+        const int var = ev ? atoi(ev) : (mode == OP_APPLY ? (Lv.m > 32 ? 3 : 2) : (Lv.m > 32 ? 1 : 0));
+        Lv.kws_m[mode] = ws_kernel(Lv.m, var, &Lv.ws_threads[mode], &Lv.ws_smem_b[mode]);
+        if (Lv.kws_m[mode]) RC(allow_smem(Lv.kws_m[mode], Lv.ws_smem_b[mode]));
       }
+      Lv.kws = Lv.kws_m[OP_APPLY];
+      if (Lv.kws) Lv.ntq = (Lv.m + 31) / 32;
     }
     if (Lv.kreg) RC(allow_smem(Lv.kreg, level_reg_smem(Lv)));
     RC(allow_smem(Lv.klist, list_smem(Lv.m, Lv.G)));
@@ -3016,8 +3241,10 @@ static int setup_impl(const fcm_grid* g, const fcm_params* prm, const fcm_slab* 
       RC(pack_tiles(h.get(), h->d_cutK, m, (int64_t)m * m, ntf, h->d_cutK_tp, h->cut_tps, n_cut));
     }
   }
+  h->dist = h->multi && prm->coarse == FCM_COARSE_GMG_PCG;
+  h->eager = h->dist;
   for (int q = 1; q <= g->p; ++q)
-    if (q >= 2 || ((prm->coarse == FCM_COARSE_AS_PCG || prm->coarse == FCM_COARSE_GMG_PCG) && !h->multi))
+    if (q >= 2 || ((prm->coarse == FCM_COARSE_AS_PCG || prm->coarse == FCM_COARSE_GMG_PCG) && !h->multi) || h->dist)
       RC(setup_schwarz(h.get(), q, kind, cut_idx));
   for (int q = 2; q <= g->p; ++q)
     if (h->lev[q].patch) {
@@ -3046,7 +3273,7 @@ static int setup_impl(const fcm_grid* g, const fcm_params* prm, const fcm_slab* 
     h->hg = hg;
     CU(cudaStreamSynchronize(hg->stream));
     CU(cudaStreamDestroy(hg->stream));
-    hg->stream = h->stream;
+    set_stream(hg, h->stream);   // its h-level children too (they borrowed hg's setup stream)
     hg->borrowed_stream = true;
     // all-gather maps: rank j's owned level-1 slots -> global level-1 slots
     Layout Lg;
@@ -3090,6 +3317,19 @@ static int setup_impl(const fcm_grid* g, const fcm_params* prm, const fcm_slab* 
     CU(cudaMemcpyAsync(h->c_unpack, unpack.data(), unpack.size() * 8, cudaMemcpyHostToDevice, h->stream));
     CU(cudaMemcpyAsync(h->c_extract, extract.data(), extract.size() * 8, cudaMemcpyHostToDevice, h->stream));
     CU(cudaMemsetAsync(h->c_send, 0, h->c_max * 8, h->stream));
+    if (h->dist) {   // distributed coarse CG on the slab (coarse_dist)
+      if (hg->gmg.empty()) return fail(FCM_EINVAL, "distributed h-coarsening needs at least one h-level");
+      for (int i = 0; i < 4; ++i) RC(h->alloc(&h->c_vec[i], n1));
+      RC(h->alloc(&h->d_dcg, 8));
+      CU(cudaMemsetAsync(h->d_dcg, 0, 64, h->stream));
+      CU(cudaMallocHost((void**)&h->h_dcg, 8 * sizeof(double)));
+      CU(cudaMallocHost((void**)&h->h_ci, 2 * sizeof(int)));
+      h->h_ci[0] = h->h_ci[1] = 0;
+      // owned fine (p = 1) vertex layers [f0, f1] (global); the coarse layers they restrict to
+      const int f0 = h->z0 + (h->rank > 0 ? 1 : 0), f1 = h->z1;
+      h->dist_cz0 = f0 / 2;
+      h->dist_cz1 = (f1 + 1) / 2 + 1;
+    }
   } else if (gmg_child) {
     // an h-level of the parent's geometric V-cycle: operator + elementwise AS only
   } else if (prm->coarse == FCM_COARSE_GMG_PCG) {
@@ -3333,7 +3573,7 @@ extern "C" int fcm_mg_coarse_solve(fcm_mg* h, const double* r, double* x, int32_
 
 static int capture_vcycle(fcm_mg* h) {
   const int p = h->g.p;
-  return capture(h, &h->g_vc, &h->n_vc, [&]() { return enqueue_vcycle(h, p, h->f_r, h->lev[p].x); });
+  return capture(h, &h->g_vc, &h->n_vc, [=]() { return enqueue_vcycle(h, p, h->f_r, h->lev[p].x); });
 }
 
 extern "C" int fcm_mg_vcycle(fcm_mg* h, const double* r, double* z) {
@@ -3362,7 +3602,7 @@ static int capture_fcg(fcm_mg* h) {
   const uint8_t* own = slab ? h->d_own : nullptr;
   double* red = h->d_s->red;
   // init: x = 0, r = b, z = V(r), rz = z.r, p = z
-  auto init_body = [&]() -> int {
+  auto init_body = [=]() -> int {
     k_fcg_start<<<grid_for(N, h->num_sms), kThreads, 0, h->stream>>>(h->f_x, h->f_r, h->f_b, N);
     h->count();
     RC(enqueue_vcycle(h, p, h->f_r, z));
@@ -3380,7 +3620,7 @@ static int capture_fcg(fcm_mg* h) {
     return FCM_OK;
   };
   // iteration part 1: q = A p (energy partials pq), update x, r, r_old, rr
-  auto it1_body = [&](bool d2h) -> int {
+  auto it1_body = [=](bool d2h) -> int {
     RC(fill(h, h->f_q, 0.0, N));
     RC(launch_cellop(h, p, make_op(h, p, OP_APPLY, h->f_p, h->f_q, 1.0, h->d_partB)));
     RC(exchange(h, p, h->f_q));
@@ -3400,7 +3640,7 @@ static int capture_fcg(fcm_mg* h) {
     return FCM_OK;
   };
   // iteration part 2: z = V(r), beta, p = z + beta p
-  auto it2_body = [&]() -> int {
+  auto it2_body = [=]() -> int {
     RC(enqueue_vcycle(h, p, h->f_r, z));
     CU(pdl_launch(h, k_dot2, dim3(nbd), dim3(kThreads), z, h->f_r, h->f_ro, N, h->d_partA, h->d_partB, own));
     h->count();
@@ -3418,7 +3658,7 @@ static int capture_fcg(fcm_mg* h) {
     return FCM_OK;
   };
   RC(capture(h, &h->g_init, &h->n_init, init_body));
-  RC(capture(h, &h->g_it1, &h->n_it1, [&]() { return it1_body(true); }));
+  RC(capture(h, &h->g_it1, &h->n_it1, [=]() { return it1_body(true); }));
   RC(capture(h, &h->g_it2, &h->n_it2, it2_body));
   // the whole solve as ONE graph with a device-side WHILE loop (conditional node): no host
   // round trip per iteration (FCM_HOST_LOOP=1 keeps the per-iteration host loop)
@@ -3502,6 +3742,7 @@ static int pcg_core(fcm_mg* h, double rtol, int32_t maxit, int32_t* iters, doubl
   if (hist) hist[0] = bb > 0 ? 1.0 : 0.0;
   h->stat_coarse = 0;
   CU(cudaMemsetAsync((h->hg ? h->hg : h)->d_coarse_iters, 0, 8, h->stream));
+  if (h->h_ci) h->h_ci[0] = h->h_ci[1] = 0;
   h->stat_vcycles = 0;
   if (!(bb > 0) || maxit == 0) {   // b = 0: x = 0 (R6); maxit = 0: no x-update, x = x0 = 0
     RC(fill(h, h->f_x, 0.0, N));
@@ -3595,7 +3836,7 @@ static int mg_solve_core(fcm_mg* h, double rtol, int32_t maxit, int32_t* iters, 
   const int nbd = dot_blocks(h);
   const uint8_t* own = h->multi ? h->d_own : nullptr;
   if (!h->g_mgit) {
-    RC(capture(h, &h->g_mgit, &h->n_mgit, [&]() -> int {
+    RC(capture(h, &h->g_mgit, &h->n_mgit, [=]() -> int {
       RC(enqueue_vcycle(h, p, h->f_r, z));
       k_axpy<<<grid_for(N, h->num_sms), kThreads, 0, h->stream>>>(h->f_x, 1.0, z, N);
       h->count();
@@ -3617,6 +3858,7 @@ static int mg_solve_core(fcm_mg* h, double rtol, int32_t maxit, int32_t* iters, 
   RC(fill(h, h->f_x, 0.0, N));
   RC(copy(h, h->f_r, h->f_b, N));   // r_0 = b (x_0 = 0)
   CU(cudaMemsetAsync((h->hg ? h->hg : h)->d_coarse_iters, 0, 8, h->stream));
+  if (h->h_ci) h->h_ci[0] = h->h_ci[1] = 0;
   CU(cudaStreamSynchronize(h->stream));
   const double bb = h->h_s->bb;
   h->stat_coarse = 0;

@@ -433,12 +433,14 @@ def test_cfg2_full_size():
     assert rel(xo, seen[its]) <= 1e-8
 
 
-@pytest.mark.parametrize("case", ["3d_p2", "3d_trunk_elast"])
+@pytest.mark.parametrize("case", ["3d_p2", "3d_trunk_elast", "3d_p2_gmg", "3d_p2_gmg_n12", "2d_p3_gmg", "3d_elast_gmg"])
 def test_forced_slab_mode_single_rank(case, monkeypatch):
     # the slab machinery on one rank (FCM_FORCE_SLAB): NCCL communicator of size 1, all-reduced
-    # dots with the owner mask, smoother increments through d, and the REPLICATED coarse level
-    # (all-gather of the coarse residual + the global p = 1 handle on the same stream) -- the
-    # device side of the multi-GPU path minus the plane exchange, against the single-GPU path
+    # dots with the owner mask, smoother increments through d, and the coarse level -- REPLICATED
+    # (all-gather of the coarse residual + the global p = 1 handle on the same stream) for AS-PCG,
+    # DISTRIBUTED for the h-coarsened solve (slab CG + slab h-level-0 smoothing, all-reduced
+    # restriction, replicated h-levels below, eager host-driven loop) -- the device side of the
+    # multi-GPU path minus the plane exchange, against the single-GPU path
     from paper_2010_00881_b200.fcm import Solver, generate
     cfg = CASES[case]()
     G = generate(cfg)

@@ -169,3 +169,137 @@ def test_slab_bounds_partition():
             assert all(b[r][1] == b[r + 1][0] for r in range(world - 1))
             sizes = [z1 - z0 for z0, z1 in b]
             assert max(sizes) - min(sizes) <= 1
+
+
+def _allreduce_np(v):
+    t = torch.from_numpy(np.ascontiguousarray(v, dtype=np.float64))
+    dist.all_reduce(t)
+    return t.numpy()
+
+
+def _dist_gmg_worker(rank, world, port, cfg_args, results):
+    """The DISTRIBUTED h-coarsened coarse solve (library: coarse_dist / gmg_vcycle_dist; P:227
+    Remark) emulated with numpy on each rank's slab: the p=1 level stays slab partitioned (its
+    operator and its h-level-0 elementwise AS sweeps over the owned cells + interface exchange,
+    owned dots all-reduced), the restriction to h-level 1 is each slab's OWNED rows of P^T r
+    all-reduced, the h-levels below run replicated, the prolongation is the slab's rows of P e.
+    Must reproduce the oracle's global CG + geometric V-cycle (GeometricLevels)."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from oracle.mg import Hierarchy
+        from oracle.problem import Problem
+        from paper_2010_00881_b200.fcm import slab_bounds, slab_layout
+        from workloads import small_config
+
+        cfg = small_config(**cfg_args, coarse="gmg_pcg")
+        P = Problem(cfg)
+        H = Hierarchy(P)
+        G = H.gmg
+        lv = H.levels[1]
+        n, dim = cfg.n, cfg.dim
+        z0, z1 = slab_bounds(n, world, rank)
+        plane = n ** (dim - 1)
+        keys, own, lo, hi = slab_layout(cfg, z0, z1, 1)
+        gpos = np.searchsorted(P.dof.keys, keys)          # global DOF of each local slot
+        lpos = np.full(P.dof.ndof, -1)
+        lpos[lv.idx] = np.arange(lv.n)
+        l1 = lpos[gpos]                                    # level-1 (oracle order) position of each local slot
+        assert np.all(l1 >= 0)
+        m1 = P.dof.level_m(1)
+        owned_cells = set(range(z0 * plane, z1 * plane))
+        # local operator / smoother over the owned cells, then the interface exchange
+        cell_blocks = []
+        bi = 0
+        for c in range(n ** dim):
+            g = P.dof.cell_dofs[c, :m1]
+            if not np.any(g >= 0):
+                continue
+            if c in owned_cells:
+                cell_blocks.append((c, lv.blocks[bi], lv.inv[bi]))
+            bi += 1
+        inv_l1 = np.full(lv.n, -1)
+        inv_l1[l1] = np.arange(len(l1))
+
+        def apply(v):
+            y = np.zeros(lv.n)
+            vg = np.zeros(lv.n)
+            vg[l1] = v
+            for c, _, _ in cell_blocks:
+                idx = P.dof.cell_dofs[c, :m1]
+                ok = idx >= 0
+                K = _cell_matrix(P, c)[:m1, :m1]
+                rows = lpos[idx[ok]]
+                y[rows] += K[np.ix_(ok, ok)] @ vg[rows]
+            return _exchange(y[l1], lo, hi, rank, world)
+
+        def smooth(r, w):
+            d = np.zeros(lv.n)
+            rg = np.zeros(lv.n)
+            rg[l1] = r
+            for _, blk, inv in cell_blocks:
+                d[blk] += w * (inv @ rg[blk])
+            return _exchange(d[l1], lo, hi, rank, world)
+
+        def dot(a, b):
+            return float(_allreduce_np(np.array([np.dot(a[own], b[own])]))[0])
+
+        def vcycle_dist(b):
+            w = G.omega
+            x = np.zeros_like(b)
+            for _ in range(G.n_pre):
+                x = x + smooth(b - apply(x), w)
+            r = b - apply(x)
+            full = np.zeros(lv.n)
+            full[l1[own]] = r[own]                         # this slab's owned rows only
+            bc = _allreduce_np(G.P[0].T @ full)            # all-reduced restriction
+            ec = G.vcycle(bc, 1)                           # replicated h-levels
+            x = x + (G.P[0] @ ec)[l1]
+            for _ in range(G.n_post):
+                x = x + smooth(b - apply(x), w)
+            return x
+
+        # right-hand side: the level-1 part of the load
+        b_glob = P.b[lv.idx]
+        ref = H.coarse_solve(b_glob)
+        it_ref = H.coarse_iters[-1]
+        b = b_glob[l1]
+        x = np.zeros_like(b)
+        r = b.copy()
+        z = vcycle_dist(r)
+        rz, rr0 = dot(r, z), dot(r, r)
+        p = z.copy()
+        it = 0
+        while True:
+            q = apply(p)
+            a = rz / dot(p, q)
+            x += a * p
+            r -= a * q
+            it += 1
+            if dot(r, r) < H.coarse_rtol ** 2 * rr0 or it >= H.coarse_maxit:
+                break
+            z = vcycle_dist(r)
+            rzn = dot(r, z)
+            p = z + (rzn / rz) * p
+            rz = rzn
+        rel = np.linalg.norm(x - ref[l1]) / np.linalg.norm(ref[l1])
+        results[rank] = {"rel": float(rel), "it": it, "it_ref": int(it_ref)}
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("cfg_args", [
+    dict(dim=3, n=8, p=2, voids=2, seed=5),
+    dict(dim=2, n=16, p=3, voids=1, seed=2),
+    dict(dim=3, n=8, p=2, physics="elasticity", voids=1, seed=6),
+])
+def test_distributed_gmg_coarse_matches_oracle(world, cfg_args):
+    mgr = mp.Manager()
+    results = mgr.dict()
+    mp.spawn(_dist_gmg_worker, args=(world, _free_port(), cfg_args, results), nprocs=world, join=True)
+    assert len(results) == world
+    for rank, out in results.items():
+        assert abs(out["it"] - out["it_ref"]) <= 1, (rank, out)
+        assert out["rel"] <= 1e-9, (rank, out)
