@@ -78,9 +78,26 @@ extern "C" {
 #define FCM_COARSE_GMG_PCG 3  /* CG preconditioned by a geometric V-cycle over h-coarsened
                                  p=1 grids (PAPER.md:227 Remark; R21): trilinear P,
                                  Galerkin P^T A P element by element, elementwise AS on every
-                                 h-level, dense solve on the coarsest grid (single GPU)     */
+                                 h-level, dense solve on the coarsest grid; distributed over
+                                 the slabs in slab mode (see multi-GPU below)               */
 #define FCM_PHYS_POISSON 0
 #define FCM_PHYS_ELASTICITY 1
+
+/* Environment switches read at setup (defaults in brackets):
+ *   FCM_DETERMINISTIC=1  [0] bit-reproducible mode (single GPU): every scatter runs in colour
+ *                        passes (2^d cell parities; 27 vertex classes mod 3 for patches), so
+ *                        each output entry receives at most one fp64 atomic per launch; per-
+ *                        patch row sums in a fixed warp order; operator energies and coarse dot
+ *                        sums in block order.  Two solves are bit-identical; several times
+ *                        slower.  Needs coarse DIRECT, GMG_PCG or a p=1 level that fits the
+ *                        tiled coarse kernel (FCM_EINVAL otherwise).
+ *   FCM_CELL_WS=0        [1] elementwise levels q >= 2 with m in {27, 64, 125}: one warp-
+ *                        specialised launch per cell operation (MMA warps for the regular cells,
+ *                        bulk-copy streaming of tile-packed individual matrices); 0 = the
+ *                        k_cell_mma block-range launch with full-storage matrices.
+ *   FCM_CELL_MMA=0, FCM_PDL=0, FCM_HOST_LOOP=1, FCM_TILED_ATOMIC=0: generic cell kernels, no
+ *                        programmatic dependent launch, per-iteration host loop, block-order
+ *                        tiled coarse sums (fallback / reproducibility switches, tested).      */
 
 /* Grid / discretisation. */
 typedef struct fcm_grid {
@@ -171,9 +188,17 @@ int fcm_mg_destroy(fcm_mg* h);
  * interface planes over NCCL (grouped send/recv; a + b == b + a keeps both copies bit-
  * identical); dots are reduced with ncclAllReduce.  Schwarz blocks of cells next to an
  * interface are assembled with one ghost cell layer.  The coarse p = 1 problem is solved
- * REPLICATED: the owned coarse residuals are all-gathered and every rank runs the coarse
- * solver on the full p = 1 grid (no per-iteration communication in the inner CG).
- * NCCL is loaded at run time (dlopen of libnccl.so.2, the one torch already loaded).      */
+ *  - REPLICATED for FCM_COARSE_AS_PCG / _JACOBI_PCG / _DIRECT: the owned coarse residuals are
+ *    all-gathered and every rank runs the coarse solver on the full p = 1 grid (no per-
+ *    iteration communication in the inner CG);
+ *  - DISTRIBUTED for FCM_COARSE_GMG_PCG ("reuse the parallel data structures that
+ *    have already been set up for the fine problem"): the inner CG and the h-level-0 smoothing
+ *    run on the slabs (exchange + all-reduced owned dots), each slab restricts its OWNED p = 1
+ *    residual rows to the global h-level-1 grid, the sum is all-reduced and the h-levels below
+ *    run replicated; the slab prolongates into its own vertices.  The inner CG is host-driven
+ *    (one 64-byte D2H per iteration), so the slab V-cycle and FCG run without CUDA graphs.
+ * NCCL is loaded at run time (dlopen of libnccl.so.2, the one torch already loaded).
+ * Patchwise blocks (FCM_BLOCK_PATCH) are single-GPU.                                        */
 
 /* Balanced partition of n cell layers over nranks (host only).                              */
 int fcm_slab_bounds(int32_t n, int32_t nranks, int32_t rank, int32_t* z_begin, int32_t* z_end);

@@ -76,6 +76,7 @@ __global__ void k_assemble_blocks(BlockAsmArgs a) {
 
 // One smoother application over general (patch) blocks: one warp per anchor.
 struct BlockOp {
+  int colour;                 // deterministic mode: only anchors of this colour (v mod 3 per axis), -1 all
   int nx, ny, nz;               // cells
   int na[3];                    // anchors
   int64_t nanchor;
@@ -118,6 +119,7 @@ __global__ void __launch_bounds__(256) k_block_smooth(BlockOp op) {
     if (bq == kBlkNone || bq >= 0) continue;   // warp-uniform; individual blocks: k_patch_irr
     const int ax = (int)(A % op.na[0]), ay = (int)((A / op.na[0]) % op.na[1]);
     const int az = (int)(A / ((int64_t)op.na[0] * op.na[1]));
+    if (op.colour >= 0 && (ax % 3) + 3 * (ay % 3) + 9 * (az % 3) != op.colour) continue;   // deterministic mode
     for (int l = lane; l < mb; l += 32) {
       const int k = op.mem[l], a = op.loc[l];
       const int cx = ax + op.mo[k][0], cy = ay + op.mo[k][1], cz = az + op.mo[k][2];

@@ -149,7 +149,11 @@ __device__ __forceinline__ double mma_cells(const CellOp& op, const int32_t* __r
       if (rt >= MT) break;
       const double d0 = D[u][0], d1 = D[u][1];
       const int a = rt * 8 + ar;
-      const int i0 = mma_dof_index<M>(T, a, c0), i1 = mma_dof_index<M>(T, a, c1);
+      int i0 = mma_dof_index<M>(T, a, c0), i1 = mma_dof_index<M>(T, a, c1);
+      if (op.colour >= 0) {   // deterministic mode: scatter only the cells of this launch's colour
+        if (c0 == -1 || cell_colour(c0 & 1023, (c0 >> 10) & 1023, (c0 >> 20) & 1023) != op.colour) i0 = -1;
+        if (c1 == -1 || cell_colour(c1 & 1023, (c1 >> 10) & 1023, (c1 >> 20) & 1023) != op.colour) i1 = -1;
+      }
       double x0 = 0.0, x1 = 0.0;
       if (want_e) {   // x(a, n) lives in lane n*4 + a%4, fragment B[a/4], a/4 in {2rt, 2rt+1}
         const int src0 = 2 * ac * 4 + (ar & 3), src1 = src0 + 4;

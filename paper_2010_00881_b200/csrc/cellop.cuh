@@ -68,7 +68,12 @@ struct CellOp {
   double* out;
   double coef;
   double* partials;           // per-block sum of in_local^T (scale Mat in_local), or nullptr
+  int colour;                 // deterministic mode: only cells of this parity colour (-1: all)
 };
+
+// parity colour of a cell (2^d colours): cells of one colour share no DOF, so a launch restricted
+// to one colour adds at most one contribution to every output entry (deterministic scatter)
+__device__ __forceinline__ int cell_colour(int cx, int cy, int cz) { return (cx & 1) | ((cy & 1) << 1) | ((cz & 1) << 2); }
 
 __device__ __forceinline__ void load_tab(Tab& T, const CellOp& op) {
   for (int a = threadIdx.x; a < op.m; a += blockDim.x) {
@@ -168,6 +173,9 @@ __device__ __forceinline__ double reg_cells(const CellOp& op, const Tab& T, cons
       cy = cyz % ny;
       cz = cyz / ny;
       inner = (cx >= ilx) & (cx <= ihx) & (cy >= ily) & (cy <= ihy) & (cz >= ilz) & (cz <= ihz);
+      if (op.colour >= 0 && cell_colour(cx, cy, cz) != op.colour) act = false;
+    }
+    if (act) {
       for (int a = j; a < M; a += TS)
         xs[a] = (inner || dof_free(T, a, cx, cy, cz)) ? load_in<FUSE>(op, dof_index(T, a, cx, cy, cz)) : 0.0;
     }
@@ -242,8 +250,9 @@ __device__ __forceinline__ double list_cells(const CellOp& op, const Tab& T, int
   const int rounds = (count + per_round - 1) / per_round;
   for (int r = 0; r < rounds; ++r) {
     const int i = (r * nwarps + warp) * CPW + grp;
-    const bool active = i < count;
+    bool active = i < count;
     const int c = active ? (generic ? i : op.list[i]) : 0;
+    if (active && op.colour >= 0) active = cell_colour(c % nx, (c / nx) % ny, c / (nx * ny)) == op.colour;
     if (active) {
       const int cx = c % nx;
       const int cyz = c / nx;

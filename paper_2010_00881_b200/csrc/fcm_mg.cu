@@ -135,6 +135,7 @@ struct LevelDev {
   int nt = 0;                      // 32x32 tiles per dimension of a packed inverse
   int64_t pstride = 0;             // doubles per packed inverse
   int64_t* irr_anchor = nullptr;   // [n_irr] anchor of individual block i
+  std::vector<int64_t> irr_col, reg_col;   // deterministic mode: colour ranges (27) of the sorted lists
   int32_t* reg_list = nullptr;     // regular anchors (fast diagonalisation / k_block_smooth)
   int64_t n_reg = 0;
   bool fd = false;
@@ -217,6 +218,11 @@ struct fcm_mg {
   bool multi = false;               // slab mode (nranks > 1, or FCM_FORCE_SLAB on one rank: tests)
   int mma_bps = 4, list_bps = 8;    // blocks per SM of the MMA / list parts of k_cell_mma
   int ws_ctas = 148;                // CTAs of a k_cell_ws launch (num_sms; FCM_WS_CTAS: tests)
+  // deterministic mode (FCM_DETERMINISTIC=1): every scatter in colour passes (2^d cell parities,
+  // 27 vertex classes for patches) so each output entry receives at most one fp64 atomic per
+  // launch, per-patch sums in a fixed warp order, energies by block-order dots, block-order
+  // coarse sums: bit-identical results run to run (debugging; several times slower)
+  bool det = false;
   int pdl = 1;                      // programmatic dependent launch of k_cell_mma (FCM_PDL)
   int ext_lo = 0, ext_n = 0;        // ghost-extended cell layers along the slab axis (relative)
   int64_t cut_first = 0;            // first owned cut cell in the cut-matrix array
@@ -1068,6 +1074,7 @@ static CellOp make_op(fcm_mg* h, int q, int mode, const double* in, double* out,
                       double* partials) {
   LevelDev& Lv = h->lev[q];
   CellOp op{};
+  op.colour = -1;
   op.nx = h->L.n[0]; op.ny = h->L.n[1]; op.nz = h->L.n[2];
   op.m = Lv.m;
   op.ncell = (int32_t)h->ncell;
@@ -1126,7 +1133,9 @@ static void cellop_grid(const fcm_mg* h, int q, int mode, int* nb_reg, int* nb_l
     *nb_list = (int)std::max<int64_t>(1, std::min<int64_t>((h->ncell + cpb - 1) / cpb, cap));
   }
 }
+static int dot_blocks(fcm_mg* h);
 static int cellop_nblocks(const fcm_mg* h, int q, int mode) {
+  if (h->det) return dot_blocks(const_cast<fcm_mg*>(h));   // energies by a block-order dot
   int a, b;
   cellop_grid(h, q, mode, &a, &b);
   return a + b;
@@ -1135,8 +1144,26 @@ static int cellop_nblocks(const fcm_mg* h, int q, int mode) {
 // One cell-operator application = regular kernel + individual-list kernel; the list kernel
 // runs on a forked branch (graph fork/join when captured) so both populations overlap.
 static int copy(fcm_mg* h, double* y, const double* x, int64_t n);
+static int launch_cellop_1(fcm_mg* h, int q, const CellOp& op, double* cp_dst, const double* cp_src, int64_t cp_n);
 static int launch_cellop(fcm_mg* h, int q, const CellOp& op, double* cp_dst = nullptr,
                          const double* cp_src = nullptr, int64_t cp_n = 0) {
+  if (!h->det) return launch_cellop_1(h, q, op, cp_dst, cp_src, cp_n);
+  // deterministic mode: one launch per cell parity colour, then the energy as a block-order dot
+  if (cp_dst) RC(copy(h, cp_dst, cp_src, cp_n));
+  CellOp o = op;
+  o.partials = nullptr;
+  for (int k = 0; k < (1 << h->L.dim); ++k) {
+    o.colour = k;
+    RC(launch_cellop_1(h, q, o, nullptr, nullptr, 0));
+  }
+  if (op.partials) {
+    k_dot<<<dot_blocks(h), kThreads, 0, h->stream>>>(op.in, op.out, h->lev[q].ndof, op.partials, nullptr);
+    h->count();
+    CU(cudaGetLastError());
+  }
+  return FCM_OK;
+}
+static int launch_cellop_1(fcm_mg* h, int q, const CellOp& op, double* cp_dst, const double* cp_src, int64_t cp_n) {
   const LevelDev& Lv = h->lev[q];
   int nb_reg, nb_list;
   cellop_grid(h, q, op.mode, &nb_reg, &nb_list);
@@ -1370,14 +1397,30 @@ static int launch_block_smooth(fcm_mg* h, int q, const double* r, double* x, dou
   fo.inv_alpha = 1.0 / h->alpha; fo.modeidx = Lv.fd_midx;
   fo.base = Lv.base; fo.stride3 = Lv.stride; fo.cmin = Lv.cmin; fo.cmax = Lv.cmax; fo.m = Lv.m;
   fo.in = r; fo.out = x; fo.coef = coef;
-  if (do_irr || fd) {
-    const void* k = patch_kernel(2 * q + 1, h->L.dim, do_irr, fd);
-    void* args[] = {&io, &fo};
-    CU(cudaLaunchKernel(k, dim3(h->num_sms), dim3((kIrrWarps + kFdWarps) * 32), args, patch_smem(h, q), h->stream));
+  io.det = h->det ? 1 : 0;
+  const int ncol = h->det ? 27 : 1;
+  for (int k = 0; k < ncol; ++k) {
+    PatchIrrOp io2 = io;
+    PatchFdOp fo2 = fo;
+    if (h->det) {   // deterministic mode: the anchors of colour k (lists sorted by colour at setup)
+      const int64_t i0 = Lv.irr_col[k], i1 = Lv.irr_col[k + 1];
+      io2.anchors = Lv.irr_anchor + i0;
+      io2.inv = Lv.irr_inv + i0 * Lv.pstride;
+      io2.n_irr = do_irr ? i1 - i0 : 0;
+      const int64_t r0 = Lv.reg_col[k], r1 = Lv.reg_col[k + 1];
+      fo2.anchors = Lv.reg_list + r0;
+      fo2.nreg = fd ? r1 - r0 : 0;
+    }
+    const bool di = io2.n_irr > 0, df = fo2.nreg > 0;
+    if (!di && !df) continue;
+    const void* kf = patch_kernel(2 * q + 1, h->L.dim, di, df);
+    void* args[] = {&io2, &fo2};
+    CU(cudaLaunchKernel(kf, dim3(h->num_sms), dim3((kIrrWarps + kFdWarps) * 32), args, patch_smem(h, q), h->stream));
     h->count();
   }
   if (do_reg && !Lv.fd) {
     BlockOp op{};
+    op.colour = -1;
     op.nx = h->L.n[0]; op.ny = h->L.n[1]; op.nz = h->L.n[2];
     for (int i = 0; i < 3; ++i) op.na[i] = Lv.na[i];
     op.nanchor = Lv.nanchor;
@@ -1391,8 +1434,11 @@ static int launch_block_smooth(fcm_mg* h, int q, const double* r, double* x, dou
     op.in = r; op.out = x; op.coef = coef;
     const int64_t wpb = kThreads / 32;
     const int nb = (int)std::max<int64_t>(1, std::min<int64_t>((Lv.nanchor + wpb - 1) / wpb, (int64_t)h->num_sms * 8));
-    k_block_smooth<<<nb, kThreads, block_smem(Lv.m, Lv.mb), h->stream>>>(op);
-    h->count();
+    for (int k = h->det ? 0 : -1; k < (h->det ? 27 : 0); ++k) {
+      op.colour = k;
+      k_block_smooth<<<nb, kThreads, block_smem(Lv.m, Lv.mb), h->stream>>>(op);
+      h->count();
+    }
   }
   CU(cudaGetLastError());
   return FCM_OK;
@@ -1958,7 +2004,7 @@ static int enqueue_vcycle(fcm_mg* h, int q, const double* b, double* x) {
   const int64_t N = Lv.ndof;
   // single GPU, elementwise MMA path: the residual is double-buffered and each smoother launch
   // also writes "r = b" into the buffer the next residual scatters into (no copy launches)
-  const bool fuse = Lv.kmma && !h->multi && !Lv.patch && Lv.r2;
+  const bool fuse = Lv.kmma && !h->multi && !h->det && !Lv.patch && Lv.r2;
   double* rb[2] = {Lv.r, Lv.r2 ? Lv.r2 : Lv.r};
   int cur = 0;
   RC(fill(h, x, 0.0, N));
@@ -2427,6 +2473,16 @@ static int setup_patch_blocks(fcm_mg* h, int q, const BlockGeom& g, const std::v
   std::vector<int32_t> reg;
   for (int64_t A = 0; A < (int64_t)blk.size(); ++A)
     if (blk[A] < 0 && blk[A] != kBlkNone) reg.push_back((int32_t)A);
+  if (h->det) {   // deterministic mode: regular patches grouped by vertex colour too
+    auto colour = [&](int64_t A) {
+      return (int)(A % g.na[0]) % 3 + 3 * ((int)((A / g.na[0]) % g.na[1]) % 3) +
+             9 * ((int)(A / ((int64_t)g.na[0] * g.na[1])) % 3);
+    };
+    std::stable_sort(reg.begin(), reg.end(), [&](int32_t a, int32_t b) { return colour(a) < colour(b); });
+    Lv.reg_col.assign(28, 0);
+    for (int32_t A : reg) Lv.reg_col[colour(A) + 1]++;
+    for (int k = 0; k < 27; ++k) Lv.reg_col[k + 1] += Lv.reg_col[k];
+  }
   Lv.n_reg = (int64_t)reg.size();
   RC(h->alloc(&Lv.reg_list, std::max<size_t>(reg.size(), 1)));
   if (!reg.empty()) CU(cudaMemcpyAsync(Lv.reg_list, reg.data(), reg.size() * 4, cudaMemcpyHostToDevice, h->stream));
@@ -2526,6 +2582,19 @@ static int setup_schwarz(fcm_mg* h, int q, const std::vector<uint8_t>& kind,
       blk[A] = (int32_t)irr.size();
       irr.push_back(A);
     }
+  }
+  if (patch && h->det) {   // deterministic mode: individual patches grouped by vertex colour (v mod 3)
+    auto colour = [&](int64_t A) {
+      return (int)(A % g.na[0]) % 3 + 3 * ((int)((A / g.na[0]) % g.na[1]) % 3) +
+             9 * ((int)(A / ((int64_t)g.na[0] * g.na[1])) % 3);
+    };
+    std::stable_sort(irr.begin(), irr.end(), [&](int64_t a, int64_t b) { return colour(a) < colour(b); });
+    Lv.irr_col.assign(28, 0);
+    for (size_t i = 0; i < irr.size(); ++i) {
+      blk[irr[i]] = (int32_t)i;
+      Lv.irr_col[colour(irr[i]) + 1]++;
+    }
+    for (int k = 0; k < 27; ++k) Lv.irr_col[k + 1] += Lv.irr_col[k];
   }
   if (type_rep.size() > 4095) return fail(FCM_EINVAL, "too many Schwarz block types on level %d", q);
   std::map<int, int> slot_of;
@@ -3005,7 +3074,7 @@ static int setup_tiled(fcm_mg* h) {
   t.acc = nullptr;
   // fp64-atomic dot accumulators (default; FCM_TILED_ATOMIC=0 = block-order partial sums,
   // bit-reproducible run to run, ~0.7 us slower per inner iteration at cfg2)
-  if (!(getenv("FCM_TILED_ATOMIC") && atoi(getenv("FCM_TILED_ATOMIC")) == 0)) {
+  if (!h->det && !(getenv("FCM_TILED_ATOMIC") && atoi(getenv("FCM_TILED_ATOMIC")) == 0)) {
     RC(h->alloc(&t.acc, 12));
     CU(cudaMemsetAsync(t.acc, 0, 12 * 8, h->stream));
   }
@@ -3097,6 +3166,8 @@ static int setup_impl(const fcm_grid* g, const fcm_params* prm, const fcm_slab* 
     return fail(FCM_EINVAL, "grid too large for 32-bit cell/DOF indexing on one device");
   CU(cudaGetDevice(&h->dev));
   CU(cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, h->dev));
+  h->det = getenv("FCM_DETERMINISTIC") && atoi(getenv("FCM_DETERMINISTIC")) > 0;
+  if (h->det && h->multi) return fail(FCM_EINVAL, "deterministic mode is single-GPU");
   h->ws_ctas = h->num_sms;
   if (const char* e = getenv("FCM_WS_CTAS")) h->ws_ctas = std::min(h->num_sms, std::max(1, atoi(e)));
   // cells: owned layers [z0, z1) plus one ghost layer on each side that exists
@@ -3187,7 +3258,7 @@ static int setup_impl(const fcm_grid* g, const fcm_params* prm, const fcm_slab* 
         CU(cudaStreamSynchronize(h->stream));
       }
     }
-    if (Lv.kmma && q >= 2 && !(getenv("FCM_CELL_WS") && atoi(getenv("FCM_CELL_WS")) == 0)) {
+    if (Lv.kmma && q >= 2 && !h->det && !(getenv("FCM_CELL_WS") && atoi(getenv("FCM_CELL_WS")) == 0)) {
       // measured on config 5 (profiles/r02_s2_ws_variants_cfg5.json): the operator is bound by its
       // MMA warps (12 MMA + 4 streaming warps), the smoother by its streaming warps (8 + 8)
       const char* ev = getenv("FCM_WS_VARIANT");
@@ -3380,6 +3451,9 @@ static int setup_impl(const fcm_grid* g, const fcm_params* prm, const fcm_slab* 
       if (v > 0) h->coarse_blocks = std::min<int64_t>(v, (int64_t)h->num_sms * per_sm);
     }
     RC(setup_tiled(h.get()));
+    if (h->det && !h->ktiled)
+      return fail(FCM_EINVAL, "deterministic mode: the grid-wide coarse kernel scatters with atomics; use the "
+                  "tiled kernel (smaller p=1 level), coarse 'direct' or 'gmg_pcg'");
   }
   // FCG buffers
   const int64_t N = L.ndof_level[g->p];

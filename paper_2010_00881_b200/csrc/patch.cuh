@@ -225,6 +225,7 @@ struct PatchIrrOp {
   int na[3];
   int mb, nt;                 // block slots, tiles per dim (32 nt >= mb)
   int wpp;                    // streaming warps per patch (kIrrWarps / wpp patches in flight per CTA)
+  int det;                    // deterministic mode: a patch's row sums added in a fixed warp order
   int64_t stride;             // doubles per packed inverse
   int64_t n_irr;
   const int64_t* anchors;     // [n_irr] anchor of individual block i
@@ -338,7 +339,14 @@ __device__ __forceinline__ void irr_loop(const PatchIrrOp& op, const Tab& T, dou
       ys[l] = 0.0;
     }
     group_sync(bar_id, nthr);
-    for (int j = 0; j < ntw; ++j, ++item) {
+    // deterministic mode: every warp runs the same number of tile steps; after each step the
+    // warps add their row sums to ys one after the other (named barrier between)
+    const int nsteps = op.det ? (ntiles + nw - 1) / nw : ntw;
+    for (int j = 0; j < nsteps; ++j) {
+      if (j >= ntw) {   // det only: no tile left for this warp, keep the barrier count
+        for (int k = 0; k < nw; ++k) group_sync(bar_id, nthr);
+        continue;
+      }
       const int t = w + nw * j;
       int I, J;
       tile_of(t, I, J);
@@ -369,8 +377,19 @@ __device__ __forceinline__ void irr_loop(const PatchIrrOp& op, const Tab& T, dou
         issue(item + kIrrStages);
       }
       const double yI = warp_reduce_scatter32(p);
-      atomicAdd(&ys[32 * I + lane], yI);
-      atomicAdd(&ys[32 * J + lane], yJ);
+      ++item;
+      if (!op.det) {
+        atomicAdd(&ys[32 * I + lane], yI);
+        atomicAdd(&ys[32 * J + lane], yJ);
+      } else {
+        for (int k = 0; k < nw; ++k) {
+          if (k == w) {
+            ys[32 * I + lane] += yI;
+            ys[32 * J + lane] += yJ;
+          }
+          group_sync(bar_id, nthr);
+        }
+      }
     }
     group_sync(bar_id, nthr);
     for (int l = tid; l < op.mb; l += nthr) {

@@ -202,16 +202,22 @@ def test_smoother_identical_setup(pair, tol_log):
 
 
 def test_vcycle_identical_setup(pair, tol_log):
-    # L4: V-cycle on identical setup data (same element matrices, same block inverses):
-    # <= 1e-10 with no widening; the independent-setup difference is logged beside it
+    # L4: V-cycle on identical setup data (same element matrices, same block inverses): 1e-10,
+    # widened only by the GPU's OWN run-to-run spread (reading R18: the fp64-atomic summation
+    # order changes between runs; on alpha = 1e-8 cut fragments the V-cycle amplifies that
+    # rounding to ~kappa eps -- 2D p = 4 measured 0.4 .. 1.7e-10 over four runs); the
+    # independent-setup difference is logged beside it
     Hi = pair.hier_identical()
     rng = np.random.default_rng(12)
     for k, r in enumerate((pair.P.b, rng.standard_normal(pair.P.dof.ndof))):
-        z = pair.from_gpu(pair.S.vcycle(pair.to_gpu(r)))
-        e = rel(z, Hi.vcycle(r))
-        tol_log(pair, f"L4_vcycle_identical_r{k}", pair.cfg.p, e, 1e-10,
-                independent=rel(z, pair.hier().vcycle(r)))
-        assert e <= 1e-10, e
+        rg = pair.to_gpu(r)
+        zs = [pair.from_gpu(pair.S.vcycle(rg)) for _ in range(3)]
+        spread = max(rel(zs[i], zs[j]) for i in range(3) for j in range(i))
+        tol = pair.tol(1e-10, spread)
+        e = rel(zs[0], Hi.vcycle(r))
+        tol_log(pair, f"L4_vcycle_identical_r{k}", pair.cfg.p, e, tol, gpu_spread=spread,
+                independent=rel(zs[0], pair.hier().vcycle(r)))
+        assert e <= tol, (e, spread)
 
 
 def test_coarse_solve_matches_oracle(pair):
@@ -524,6 +530,24 @@ def test_ws_single_cta(case, monkeypatch):
     xo, ito, _ = pair.hier().fcg(pair.P.b)
     xg, it, hist = pair.S.pcg_solve(pair.to_gpu(pair.P.b))
     assert abs(it - ito) <= 1 and rel(pair.from_gpu(xg), xo) <= 1e-8
+
+
+@pytest.mark.parametrize("case", ["cfg1", "3d_p2", "3d_p3_ragged", "3d_trunk_elast", "3d_p3_patch", "3d_p4_patch729",
+                                  "2d_p3_patch", "3d_p2_gmg"])
+def test_deterministic_mode_bit_identical(case, monkeypatch):
+    # FCM_DETERMINISTIC=1: colour-pass scatters (cell parities / vertex classes mod 3), fixed-order
+    # per-patch sums, block-order energies and coarse sums -> two solves are bit-identical, and
+    # the solve still matches the oracle (L5)
+    monkeypatch.setenv("FCM_DETERMINISTIC", "1")
+    pair = Pair(CASES[case]())
+    b = pair.to_gpu(pair.P.b)
+    z1, z2 = pair.S.vcycle(b), pair.S.vcycle(b)
+    assert torch.equal(z1, z2)
+    x1, it1, _ = pair.S.pcg_solve(b)
+    x2, it2, _ = pair.S.pcg_solve(b)
+    assert it1 == it2 and torch.equal(x1, x2)
+    xo, ito, _ = pair.hier().fcg(pair.P.b)
+    assert abs(it1 - ito) <= 1 and rel(pair.from_gpu(x1), xo) <= 1e-8
 
 
 def test_maxit_zero_and_bad_vectors():
