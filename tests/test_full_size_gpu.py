@@ -1,0 +1,145 @@
+"""Parity at the FULL size of the bench workload (config 3: 64^3 cells, p = 4, patchwise,
+16.6M free DOFs), in the launch configuration bench.py times: sampled outputs that the oracle
+computes one by one (oracle/sample.py, pinned by tests/test_oracle_sample.py) --
+  * the level operator A_q x at every level q = 4..1 (vertex / edge / face / interior DOFs of
+    cut, fictitious, boundary and regular cells) -- <= 1e-12 of the row's absolute sum;
+  * one patchwise smoother sweep at level 4 (individual patches streamed by k_patch_smooth's
+    bulk-copy warps, regular patches by its fast-diagonalisation warps, boundary-type patches)
+    -- 1e-10 or reading R18 (4x the oracle's own LU-vs-Cholesky spread);
+  * the FCG solution: sampled rows of b - A x below the solver's stopping bound.
+"""
+import os
+import sys
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+
+@pytest.fixture(scope="module")
+def cfg3():
+    from oracle.sample import LazyCells
+    from paper_2010_00881_b200.fcm import Solver, generate
+    from workloads import get_config
+    cfg = get_config("cfg3")
+    G = generate(cfg)
+    S = Solver.from_problem(cfg, G)
+    b = S.load(G)
+    del G
+    L = LazyCells(cfg)
+    keys = S.dof_keys()
+    perm = np.searchsorted(L.dof.keys, keys)
+    assert np.array_equal(L.dof.keys[perm], keys), "GPU layout is a permutation of the oracle's DOFs"
+    yield cfg, S, b, L, perm
+    S.close()
+
+
+def _mode_index(L, mode):
+    return [tuple(m) for m in L.modes].index(tuple(mode))
+
+
+def _sample_cells(L):
+    n = L.cfg.n
+    kinds = L.kinds.reshape(n, n, n)   # [z, y, x]
+    cut = np.argwhere(kinds == 2)
+    fict = np.argwhere(kinds == 1)
+    # a regular cell: its 5^3 neighbourhood all uncut physical
+    reg = None
+    for z in range(8, n - 8, 5):
+        for y in range(8, n - 8, 5):
+            for x in range(8, n - 8, 5):
+                if np.all(kinds[z - 2:z + 3, y - 2:y + 3, x - 2:x + 3] == 0):
+                    reg = (z, y, x)
+                    break
+            if reg: break
+        if reg: break
+    assert reg is not None
+    zyx = [tuple(cut[len(cut) // 3]), tuple(cut[2 * len(cut) // 3]), tuple(fict[len(fict) // 2]), reg,
+           (n // 2, n // 3, 0), (n - 1, n // 2, n // 4)]
+    return [int((z * n + y) * n + x) for z, y, x in zyx]
+
+
+def test_cfg3_operator_rows(cfg3):
+    from oracle.sample import operator_row
+    cfg, S, b, L, perm = cfg3
+    rng = np.random.default_rng(21)
+    cells = _sample_cells(L)
+    modes = [(0, 0, 0), (1, 1, 1), (2, 0, 0), (0, 3, 1), (2, 3, 0), (2, 2, 2), (4, 3, 2), (4, 4, 4)]
+    for q in range(cfg.p, 0, -1):
+        nq = S.ndofs(q)
+        x = np.zeros(L.dof.ndof)
+        Iq = perm[:nq]
+        x[Iq] = rng.standard_normal(nq)
+        xg = torch.from_numpy(x[Iq]).cuda()
+        y = S.apply(xg, q).cpu().numpy()
+        yo = np.zeros(L.dof.ndof)
+        yo[Iq] = y
+        m = L.dof.level_m(q)
+        checked = 0
+        for c in cells:
+            for md in modes:
+                if max(md) > q:
+                    continue
+                i = int(L.dof.cell_dofs[c, _mode_index(L, md)])
+                if i < 0:
+                    continue
+                ref = operator_row(L, x, i, q)
+                scale = sum(float(np.abs(L.K(cc)[a, :m]) @ np.abs(x[np.maximum(L.dof.cell_dofs[cc, :m], 0)]))
+                            for cc, a in L.cells_of(i, q))
+                assert abs(yo[i] - ref) <= 1e-12 * scale, (q, c, md, yo[i], ref, scale)
+                checked += 1
+        assert checked >= 8, q
+
+
+def test_cfg3_patch_smoother_rows(cfg3):
+    from oracle.sample import schwarz_row
+    cfg, S, b, L, perm = cfg3
+    q = cfg.p
+    rng = np.random.default_rng(22)
+    nq = S.ndofs(q)
+    r = np.zeros(L.dof.ndof)
+    r[perm[:nq]] = rng.standard_normal(nq)
+    xs = torch.zeros(nq, dtype=torch.float64, device="cuda")
+    S.smooth(torch.from_numpy(r[perm[:nq]]).cuda(), xs, q)
+    xo = np.zeros(L.dof.ndof)
+    xo[perm[:nq]] = xs.cpu().numpy()
+    omega = cfg.omega_value
+    a_int = _mode_index(L, (2, 2, 2))
+    cells = _sample_cells(L)
+    # interior DOFs (8 patches each) of: a cut cell, a fictitious cell, a regular cell, a cell on
+    # the x = 0 Dirichlet face (boundary-type patches)
+    rows = [int(L.dof.cell_dofs[c, a_int]) for c in (cells[0], cells[2], cells[3], cells[4])]
+    got, lu, ch = [], [], []
+    for i in rows:
+        got.append(xo[i])
+        lu.append(schwarz_row(L, r, i, q, "patch", omega, inv="lu"))
+        ch.append(schwarz_row(L, r, i, q, "patch", omega, inv="chol"))
+    got, lu, ch = map(np.array, (got, lu, ch))
+    spread = np.linalg.norm(ch - lu) / np.linalg.norm(lu)
+    err = np.linalg.norm(got - lu) / np.linalg.norm(lu)
+    assert err <= max(1e-10, 4 * spread), (err, spread, got, lu)
+
+
+def test_cfg3_fcg_sampled_residual(cfg3):
+    from oracle.sample import load_row, operator_row
+    cfg, S, b, L, perm = cfg3
+    x, it, hist = S.pcg_solve(b)
+    assert hist[-1] < cfg.rtol and it <= 12
+    xo = np.zeros(L.dof.ndof)
+    xo[perm] = x.cpu().numpy()
+    bo = np.zeros(L.dof.ndof)
+    bo[perm] = b.cpu().numpy()
+    bnorm = float(np.linalg.norm(bo))
+    cells = _sample_cells(L)
+    for c in cells:
+        for md in [(0, 0, 0), (2, 0, 0), (2, 3, 0), (2, 2, 2), (4, 4, 4)]:
+            i = int(L.dof.cell_dofs[c, _mode_index(L, md)])
+            if i < 0:
+                continue
+            assert abs(load_row(L, i) - bo[i]) <= 1e-13 * max(abs(bo[i]), 1e-300) + 1e-18, (c, md)
+            res = bo[i] - operator_row(L, xo, i, cfg.p)
+            assert abs(res) <= 2 * cfg.rtol * bnorm, (c, md, res, bnorm)
