@@ -8,5 +8,5 @@ CPU oracle (``oracle/``) consume these inputs; neither imports the other.
 
 Geometry recipe: DESIGN.md "Input recipe" / SURVEY.md §8(c) reading R12.
 """
-from .configs import CONFIGS, Config, get_config, small_config  # noqa: F401
+from .configs import CONFIGS, Config, get_config, hp_plate, small_config  # noqa: F401
 from .voids import sample_voids, config_voids  # noqa: F401

@@ -42,6 +42,8 @@ class Config:
     maxit: int = 500
     E: float = 1.0
     nu: float = 0.3
+    kmax: int = 0               # multi-level hp refinement depth (0 = uniform grid)
+    refine: str = "cut"         # which elements are refined while depth < kmax: "cut" | "all"
 
     @property
     def n_f(self) -> int:
@@ -78,6 +80,22 @@ CONFIGS = {
     "cfg5": Config("cfg5", dim=3, n=256, p=3,
                    geometry={"kind": "seeded", "count": 1000, "r_min": 0.01, "r_max": 0.03, "seed": 5}),
 }
+
+
+def hp_plate(n: int, k: int, p: int = 2, block: str = "patch", **kw) -> Config:
+    """The perforated linear-elastic plate of PAPER.md:709-713 (Sec. 4.2) on a multi-level hp
+    grid ("elements that are intersected by the immersed boundary are refined
+    recursively to a predefined depth"), scaled from l = 4 to the unit square (2D elasticity is
+    scale-invariant): four circular cavities r = 0.3 sqrt(2) / 4 centred at (0.25 | 0.75)^2
+    (reading R28: the figure is not reproduced in the text), E = 2.069e5, nu = 0.29, clamped at
+    x = 0 (strong, R7), traction (1, 0) on x = 1 (R8), alpha = 1e-8, n = 1/h cells per axis."""
+    r = 0.3 * 2 ** 0.5 / 4
+    geom = {"kind": "explicit", "centres": [[0.25, 0.25], [0.75, 0.25], [0.25, 0.75], [0.75, 0.75]],
+            "radii": [r] * 4}
+    kw.setdefault("coarse", "direct")
+    return Config(f"hp_plate_n{n}_k{k}_p{p}_{block}", dim=2, n=n, p=p, physics="elasticity",
+                  geometry=geom, dirichlet=0b0001, traction_face=1, block=block, kmax=k,
+                  E=2.069e5, nu=0.29, **kw)
 
 
 def get_config(name: str) -> Config:
