@@ -339,6 +339,94 @@ int fcm_mg_coarse_info(const fcm_mg* h, int32_t* kind, int32_t* blocks, int32_t*
 /* Counters of kernels launched by the library since setup (for the bench's gpu_launches). */
 int fcm_mg_launch_count(const fcm_mg* h, int64_t* launches);
 
+/* ==== multi-level hp-refinement ========
+ * A base grid of n^d cells on [0,1]^d whose elements are refined by SUPERPOSITION:
+ * a refined element of depth j carries 2^d subelements of depth j+1, recursively up to kmax;
+ * leaves are the elements without subelements.  Every element of every depth carries the tensor
+ * integrated-Legendre modes of order p on its entities (vertices / edges / faces / interior of the
+ * depth-j grid, doubled coordinates X as above).  Activation rule (reading R25, the rule set the
+ * paper defers to [Zander2016]): a depth-j entity is active iff (compatibility) j = 0 or
+ * every depth-j element adjacent to it inside the domain exists, and (independence) at least one
+ * existing adjacent depth-j element is a leaf.  Dirichlet as R7.  A leaf's basis is the
+ * superposition of the active free functions of the leaf and all its ancestors.
+ * hp level sequence (Fig. hpmultigrid), finest first:
+ *   (p,k), (p-1,k), ..., (1,k), (1,k-1), ..., (1,0)       (k = deepest depth carrying DOFs),
+ * level (q, kc) = the DOFs of mode order <= q and depth <= kc; nested, so restriction is index
+ * selection.  DOF order of the library: by the COARSEST level containing the DOF
+ * (descending), so every level is a PREFIX of the fine vector as on uniform grids.
+ * Schwarz blocks (reading R26, Fig. 7 caption P:273 "granularity of the base elements"):
+ * elementwise = the level DOFs nonzero on one BASE element; patchwise = those nonzero on the
+ * 2^d base elements around a base vertex; identical blocks counted once.                   */
+#define FCM_HP_REFINE_CUT 0   /* refine the elements cut by the immersed boundary        */
+#define FCM_HP_REFINE_ALL 1   /* refine every element (uniform overlay; tests)                    */
+
+typedef struct fcm_hp_spec {
+  int32_t dim;              /* 2 or 3                                                         */
+  int32_t n;                /* base cells per axis                                            */
+  int32_t p;                /* order, 1 <= p <= 8                                             */
+  int32_t kmax;             /* refinement depth, 0 <= kmax <= 8                               */
+  int32_t refine;           /* FCM_HP_REFINE_*                                                */
+  uint32_t dirichlet_faces; /* as fcm_grid                                                    */
+  fcm_physics phys;         /* generator physics (alpha, E, nu, space-tree depth, traction)   */
+  int64_t n_voids;          /* spherical voids (fictitious domain)               */
+  const double* centres;    /* host [n_voids * dim]                                           */
+  const double* radii;      /* host [n_voids]                                                 */
+} fcm_hp_spec;
+
+typedef struct fcm_hp_disc fcm_hp_disc;   /* opaque host discretisation (generator output) */
+typedef struct fcm_hp fcm_hp;             /* opaque device solver handle                    */
+
+/* Generator (setup, host C++/OpenMP, independent of the oracle): refinement trees, activation,
+ * DOF numbering, leaf element matrices by the space tree of depth phys.depth BELOW EACH LEAF
+ * ((p+1)^d Gauss points per sub-box, alpha per point at depth-limit cut sub-boxes, R13) and the
+ * load vector (f = 1 Poisson, traction (1,0,0) on phys.traction_face, R8).  *out owns host
+ * memory; free with fcm_hp_disc_destroy.  Errors: FCM_EINVAL (bad spec), FCM_ENOMEM.        */
+int fcm_hp_generate(const fcm_hp_spec* spec, fcm_hp_disc** out);
+int fcm_hp_disc_destroy(fcm_hp_disc* d);
+/* Sizes: ndof, levels, leaves, total leaf DOF entries sum(m_e), total matrix entries sum(m_e^2). */
+int fcm_hp_disc_info(const fcm_hp_disc* d, int64_t* ndof, int32_t* nlevels, int64_t* nleaves,
+                     int64_t* leaf_entries, int64_t* leaf_matrix_entries);
+/* Per level (finest first): ndofs (a prefix length), order q and depth cap kc.  Host [nlevels]. */
+int fcm_hp_disc_levels(const fcm_hp_disc* d, int64_t* ndofs, int32_t* q, int32_t* kc);
+/* DOF keys, host int32 [ndof * 8]: (depth j, X_x, X_y, X_z, deg_x, deg_y, deg_z, comp), X and
+ * deg as the uniform convention on the depth-j grid (absent axes 0).  Load b, host [ndof].     */
+int fcm_hp_disc_keys(const fcm_hp_disc* d, int32_t* keys);
+int fcm_hp_disc_load(const fcm_hp_disc* d, double* b);
+/* Leaves (any pointer may be NULL): leaf_ptr [nleaves+1] offsets into dofs; dofs [leaf_entries]
+ * the leaf's global DOF indices, ascending (so each level's entries are a prefix); K
+ * [leaf_matrix_entries] the leaf matrices m_e x m_e row-major in that order, concatenated;
+ * info [nleaves * 5] = (depth, idx_x, idx_y, idx_z, base element index x fastest).           */
+int fcm_hp_disc_leaves(const fcm_hp_disc* d, int64_t* leaf_ptr, int32_t* dofs, double* K, int32_t* info);
+
+/* Device setup on the current CUDA device: copies the leaves, builds every level's Schwarz
+ * blocks (prm->block, coarse level elementwise), assembles A_i = P_i^T A_l P_i from the leaf
+ * matrices and inverts them (equilibrated blocked Gauss-Jordan), and the coarse solver
+ * (FCM_COARSE_DIRECT: dense inverse of the (1,0) matrix; FCM_COARSE_AS_PCG: CG + undamped
+ * elementwise AS, prm->coarse_rtol relative to ||r0||).  prm->omega is the fine-level relaxation.
+ * The handle does not keep d.  Errors: FCM_EINVAL, FCM_ENOMEM, FCM_ESINGULAR, FCM_ECUDA.       */
+int fcm_hp_setup(const fcm_hp_disc* d, const fcm_params* prm, fcm_hp** out);
+int fcm_hp_destroy(fcm_hp* h);
+/* y = A_l x on level l (0 = finest): element-by-element over the leaves;
+ * x, y device [ndofs(l)].                                                                    */
+int fcm_hp_apply(fcm_hp* h, int32_t level, const double* x, double* y);
+/* x += omega_l sum_i P_i A_i^{-1} P_i^T r (Eq. AdditiveSchwarz); device [ndofs(l)]. */
+int fcm_hp_smooth(fcm_hp* h, int32_t level, const double* r, double* x);
+/* z = one hp V-cycle of Algorithm 1 (R1) applied to r; device [ndof].              */
+int fcm_hp_vcycle(fcm_hp* h, const double* r, double* z);
+/* Flexible PCG with one hp V-cycle per iteration (as fcm_pcg_solve); relres_hist host
+ * [maxit+1] or NULL.  FCM_NOT_CONVERGED when maxit is reached.                              */
+int fcm_hp_pcg_solve(fcm_hp* h, const double* b, double* x, double rtol, int32_t maxit,
+                     int32_t* iters, double* relres_hist);
+/* Identical-setup parity protocol for the hp smoother: level l's blocks and inverses.  Two-call:
+ * with ptr/dofs/inv NULL, *n_blocks, *dof_entries (sum m_i) and *inv_entries (sum m_i^2) are set;
+ * otherwise ptr [n_blocks+1], dofs [dof_entries] (level indices, ascending per block), inv
+ * [inv_entries] (row-major per block, concatenated).  The coarse level with the direct solver
+ * exports its dense inverse as one block.                                                    */
+int fcm_hp_export_blocks(const fcm_hp* h, int32_t level, int64_t* n_blocks, int64_t* dof_entries,
+                         int64_t* inv_entries, int64_t* ptr, int32_t* dofs, double* inv);
+/* Launch counter and last-solve statistics (coarse CG iterations, V-cycles).                  */
+int fcm_hp_stats(const fcm_hp* h, int64_t* launches, int64_t* coarse_iters_total, int64_t* vcycles);
+
 /* Thread-local message of the last error ("" if none).                                     */
 const char* fcm_last_error(void);
 

@@ -315,10 +315,28 @@ class MlhpLevel:
                 self.blocks.append(b)
         self.inv = [np.linalg.inv(self.A[b][:, b].toarray()) for b in self.blocks]
 
+    def set_blocks(self, blocks, inverses):
+        """Identical-setup parity protocol (as mg.Level.set_blocks): externally supplied blocks
+        (level-local index arrays) and inverses replace this level's own."""
+        self.blocks = [np.asarray(b, dtype=np.int64) for b in blocks]
+        self.inv = [np.asarray(a, dtype=np.float64) for a in inverses]
+
+    order_seed = None   # accumulate in a seeded random block order (rounding-spread measurement, R18/R24)
+    noise = None        # (rng) rounding model of the same measurement
+
     def schwarz(self, r):
         """M^{-1} r = sum_i P_i A_i^{-1} P_i^T r (Eq. AdditiveSchwarz), serial order."""
-        idx = np.concatenate(self.blocks)
-        vals = np.concatenate([self.inv[i] @ r[b] for i, b in enumerate(self.blocks)])
+        order = range(len(self.blocks))
+        if self.order_seed is not None:
+            order = np.random.default_rng(self.order_seed).permutation(len(self.blocks))
+        idx = np.concatenate([self.blocks[i] for i in order])
+        vals = np.concatenate([self.inv[i] @ r[self.blocks[i]] for i in order])
+        if self.noise is not None:   # rounding model (Higham-Mary probabilistic bound): sqrt(m_i) eps |A_i^-1||r_i| N(0,1)
+            mag = np.concatenate([np.sqrt(len(self.blocks[i])) * (np.abs(self.inv[i]) @ np.abs(r[self.blocks[i]]))
+                                  for i in order])
+            out = np.bincount(idx, weights=vals, minlength=self.n)
+            return out + np.finfo(float).eps * np.bincount(idx, weights=mag, minlength=self.n) * \
+                self.noise.standard_normal(self.n)
         return np.bincount(idx, weights=vals, minlength=self.n)
 
 
@@ -351,26 +369,43 @@ class MlhpHierarchy:
             self.lu = sla.lu_factor(c.A.toarray())
         self.coarse_iters = []
 
+    def set_coarse_inverse(self, inv):
+        """Identical-setup parity protocol: apply a supplied dense inverse as the direct coarse solve."""
+        self.coarse_inv = np.asarray(inv, dtype=np.float64)
+
     def coarse_solve(self, b):
         lv = self.levels[-1]
         if self.coarse == "direct":
+            if getattr(self, "coarse_inv", None) is not None:
+                return self.coarse_inv @ b
             return sla.lu_solve(self.lu, b)
         x, it = pcg(lambda v: lv.A @ v, b, lv.schwarz, self.coarse_rtol, self.coarse_maxit, rel_to="r0")
         self.coarse_iters.append(it)
         return x
 
+    noise = None   # (rng) rounding model for spread measurements (Higham-Mary probabilistic bound:
+    #               a dot product of k terms errs by ~ sqrt(k) eps sum |terms|): residuals get
+    #               sqrt(nnz_row) eps |A||x| N(0,1)
+
+    def _res(self, lv, b, x):
+        r = b - lv.A @ x
+        if self.noise is not None:
+            k = np.sqrt(np.diff(lv.A.indptr) + 1.0)
+            r = r + np.finfo(float).eps * k * (abs(lv.A) @ np.abs(x) + np.abs(b)) * self.noise.standard_normal(len(r))
+        return r
+
     def vcycle(self, b, i=0):
         if i == len(self.levels) - 1:
             return self.coarse_solve(b)
         lv = self.levels[i]
-        A, w = lv.A, self.omega
+        w = self.omega
         x = np.zeros(lv.n)
         for _ in range(self.n_pre):
-            x = x + w * lv.schwarz(b - A @ x)
-        r = b - A @ x
+            x = x + w * lv.schwarz(self._res(lv, b, x))
+        r = self._res(lv, b, x)
         x[self.sel[i]] += self.vcycle(r[self.sel[i]], i + 1)
         for _ in range(self.n_post):
-            x = x + w * lv.schwarz(b - A @ x)
+            x = x + w * lv.schwarz(self._res(lv, b, x))
         return x
 
     def fcg(self, b, rtol=None, maxit=None):

@@ -161,9 +161,32 @@ def blocks_containing(L: LazyCells, i, q, block):
     return res
 
 
-def schwarz_row(L: LazyCells, r, i, q, block, omega, inv="lu"):
+class PerturbedCells:
+    """LazyCells whose CUT-cell matrices carry a seeded symmetric entrywise relative perturbation
+    K_ab (1 + delta E_ab), E_ab ~ N(0,1) (reading R18: the sensitivity of an ill-conditioned block
+    to setup data that agrees only to the generator-parity level L0, not an evaluation order)."""
+
+    def __init__(self, L: LazyCells, delta, seed=0):
+        self._L, self.delta, self.seed = L, delta, seed
+
+    def __getattr__(self, name):
+        return getattr(self._L, name)
+
+    def K(self, c):
+        K = self._L.K(c)
+        if self._L.kinds[c] != geometry.CUT:
+            return K
+        E = np.random.default_rng([self.seed, int(c)]).standard_normal(K.shape)
+        E = 0.5 * (E + E.T)
+        return K * (1.0 + self.delta * E)
+
+
+def schwarz_row(L: LazyCells, r, i, q, block, omega, inv="lu", perturb=0.0):
     """(omega sum_B P_B A_B^{-1} P_B^T r)_i; A_B^{-1} applied by dense LU (inv="lu") or
-    Cholesky (inv="chol") -- two backward-stable evaluations (reading R18)."""
+    Cholesky (inv="chol") -- two backward-stable evaluations (reading R18); perturb > 0 evaluates
+    it on PerturbedCells(L, perturb) (the setup-sensitivity leg of R18)."""
+    if perturb > 0.0:
+        L = PerturbedCells(L, perturb)
     s = 0.0
     for v in blocks_containing(L, i, q, block):
         B = block_dofs(L, v, q, block)

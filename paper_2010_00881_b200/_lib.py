@@ -42,6 +42,12 @@ class Physics(C.Structure):
                 ("depth", C.c_int32), ("traction_face", C.c_int32)]
 
 
+class HpSpec(C.Structure):
+    _fields_ = [("dim", C.c_int32), ("n", C.c_int32), ("p", C.c_int32), ("kmax", C.c_int32),
+                ("refine", C.c_int32), ("dirichlet_faces", C.c_uint32), ("phys", Physics),
+                ("n_voids", C.c_int64), ("centres", C.c_void_p), ("radii", C.c_void_p)]
+
+
 _lib = None
 
 P = C.c_void_p
@@ -78,6 +84,21 @@ _SIGS = {
     "fcm_nccl_unique_id": (I32, [P]),
     "fcm_mg_setup_slab": (I32, [P, P, P, P, P, D, I64, P, P, I64, P, P, P]),
     "fcm_mg_launch_count": (I32, [P, P]),
+    "fcm_hp_generate": (I32, [P, P]),
+    "fcm_hp_disc_destroy": (I32, [P]),
+    "fcm_hp_disc_info": (I32, [P, P, P, P, P, P]),
+    "fcm_hp_disc_levels": (I32, [P, P, P, P]),
+    "fcm_hp_disc_keys": (I32, [P, P]),
+    "fcm_hp_disc_load": (I32, [P, P]),
+    "fcm_hp_disc_leaves": (I32, [P, P, P, P, P]),
+    "fcm_hp_setup": (I32, [P, P, P]),
+    "fcm_hp_destroy": (I32, [P]),
+    "fcm_hp_apply": (I32, [P, I32, P, P]),
+    "fcm_hp_smooth": (I32, [P, I32, P, P]),
+    "fcm_hp_vcycle": (I32, [P, P, P]),
+    "fcm_hp_pcg_solve": (I32, [P, P, P, D, I32, P, P]),
+    "fcm_hp_export_blocks": (I32, [P, I32, P, P, P, P, P, P]),
+    "fcm_hp_stats": (I32, [P, P, P, P]),
     "fcm_last_error": (C.c_char_p, []),
 }
 EXPORTED = tuple(_SIGS)

@@ -2399,7 +2399,7 @@ static int setup_patch_blocks(fcm_mg* h, int q, const BlockGeom& g, const std::v
   // workspace chunk: up to 4 GiB and a quarter of the free memory
   size_t fr = 0, tot = 0;
   CU(cudaMemGetInfo(&fr, &tot));
-  const size_t per = (size_t)MP * MP * 8 + (size_t)mb + 16;
+  const size_t per = (size_t)MP * MP * 8 + (size_t)MP * 8 + (size_t)mb + 16;
   int64_t chunk = (int64_t)std::max<size_t>(1, std::min<size_t>((size_t)4 << 30, fr / 4) / per);
   chunk = std::min<int64_t>(chunk, std::max<int64_t>(nblk, 1));
   double* W = nullptr;
@@ -2407,7 +2407,9 @@ static int setup_patch_blocks(fcm_mg* h, int q, const BlockGeom& g, const std::v
   int8_t* d_dir = nullptr;
   int16_t* d_alist = nullptr;
   int* d_status = nullptr;
+  double* d_equil = nullptr;
   CU(cudaMallocAsync((void**)&W, (size_t)chunk * MP * MP * 8, h->stream));
+  CU(cudaMallocAsync((void**)&d_equil, (size_t)chunk * MP * 8, h->stream));
   CU(cudaMallocAsync((void**)&d_anc, (size_t)chunk * 8, h->stream));
   CU(cudaMallocAsync((void**)&d_dir, (size_t)chunk * mb, h->stream));
   CU(cudaMallocAsync((void**)&d_alist, alist.size() * 2, h->stream));
@@ -2434,6 +2436,7 @@ static int setup_patch_blocks(fcm_mg* h, int q, const BlockGeom& g, const std::v
     k_patch_asm<<<(unsigned)nc, 256, 0, h->stream>>>(aa);
     CU(cudaGetLastError());
     const int nt64 = (MP + 63) / 64;
+    k_equil<<<(unsigned)nc, 256, MP * 8, h->stream>>>(W, MP, d_equil, 0);
     for (int k = 0; k < nt; ++k) {
       k_gj_pivot<<<(unsigned)nc, 256, 0, h->stream>>>(W, MP, k, d_status);
       if (nt > 1) {
@@ -2442,6 +2445,7 @@ static int setup_patch_blocks(fcm_mg* h, int q, const BlockGeom& g, const std::v
         k_gj_col<<<dim3(nt - 1, (unsigned)nc), 256, 0, h->stream>>>(W, MP, k);
       }
     }
+    k_equil<<<(unsigned)nc, 256, MP * 8, h->stream>>>(W, MP, d_equil, 1);
     CU(cudaGetLastError());
     if (types) {
       if (MP == mb)
@@ -2466,7 +2470,8 @@ static int setup_patch_blocks(fcm_mg* h, int q, const BlockGeom& g, const std::v
       }
     c0 += nc;
   }
-  for (void* ptr : {(void*)W, (void*)d_anc, (void*)d_dir, (void*)d_alist, (void*)d_status}) cudaFreeAsync(ptr, h->stream);
+  for (void* ptr : {(void*)W, (void*)d_anc, (void*)d_dir, (void*)d_alist, (void*)d_status, (void*)d_equil})
+    cudaFreeAsync(ptr, h->stream);
   CU(cudaStreamSynchronize(h->stream));
   if (rc != FCM_OK) return rc;
   Lv.n_irr = n_irr;

@@ -67,6 +67,10 @@ static void modes1d(int p, double xi, double* v, double* d) {
   }
 }
 
+// shared with the multi-level hp generator (gen_hp.cpp)
+void gauss_rule(int n, std::vector<double>& x, std::vector<double>& w) { gauss_legendre(n, x, w); }
+void modes_1d(int p, double xi, double* v, double* d) { modes1d(p, xi, v, d); }
+
 // 1D reference matrices on [-1, 1] of modes 0..p (row-major (p+1)^2): M_ij = int N_i N_j,
 // K_ij = int N_i' N_j' (p+1-point Gauss: exact for degree 2p).  Used by the patch smoother's
 // fast-diagonalisation setup (fcm_mg.cu), which checks K_ref against their Kronecker form.

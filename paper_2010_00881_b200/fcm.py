@@ -15,7 +15,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from ._lib import Grid, Params, Physics, Slab, check
+from ._lib import Grid, HpSpec, Params, Physics, Slab, check
 
 COARSE = {"direct": 0, "as_pcg": 1, "jacobi_pcg": 2, "gmg_pcg": 3}
 BLOCK = {"element": 0, "patch": 1}
@@ -427,3 +427,149 @@ class Solver:
                                            C.byref(it), None)
         check(rc, allow_not_converged=True)
         return it.value
+
+
+# ---- multi-level hp-refinement (include/fcm_mg.h "multi-level hp") -------------
+class HpDisc:
+    """Host discretisation from the native generator (fcm_hp_generate): refinement trees, active
+    DOFs with (depth, entity, degrees, component) keys, leaf matrices and load."""
+
+    def __init__(self, cfg, centres=None, radii=None):
+        from workloads import config_voids
+        if centres is None:
+            centres, radii = config_voids(cfg)
+        self.cfg = cfg
+        c = np.ascontiguousarray(np.asarray(centres, dtype=np.float64).reshape(-1))
+        r = np.ascontiguousarray(np.asarray(radii, dtype=np.float64).reshape(-1))
+        sp = HpSpec()
+        sp.dim, sp.n, sp.p, sp.kmax = cfg.dim, cfg.n, cfg.p, cfg.kmax
+        sp.refine = {"cut": 0, "all": 1}[cfg.refine]
+        sp.dirichlet_faces = cfg.dirichlet_mask
+        sp.phys = physics_of(cfg)
+        sp.n_voids = len(r)
+        sp.centres = c.ctypes.data_as(C.c_void_p) if len(r) else None
+        sp.radii = r.ctypes.data_as(C.c_void_p) if len(r) else None
+        h = C.c_void_p()
+        check(_lib.lib().fcm_hp_generate(C.byref(sp), C.byref(h)))
+        self._h = h
+        nd, nl, nleaf, ne, nk = C.c_int64(), C.c_int32(), C.c_int64(), C.c_int64(), C.c_int64()
+        check(_lib.lib().fcm_hp_disc_info(h, C.byref(nd), C.byref(nl), C.byref(nleaf), C.byref(ne), C.byref(nk)))
+        self.ndof, self.nlevels, self.nleaves = nd.value, nl.value, nleaf.value
+        self.leaf_entries, self.leaf_matrix_entries = ne.value, nk.value
+        self.level_n = np.zeros(self.nlevels, np.int64)
+        self.level_q = np.zeros(self.nlevels, np.int32)
+        self.level_k = np.zeros(self.nlevels, np.int32)
+        check(_lib.lib().fcm_hp_disc_levels(h, _ptr(self.level_n), _ptr(self.level_q), _ptr(self.level_k)))
+
+    def keys(self) -> np.ndarray:
+        k = np.zeros((self.ndof, 8), np.int32)
+        check(_lib.lib().fcm_hp_disc_keys(self._h, _ptr(k)))
+        return k
+
+    def load(self) -> np.ndarray:
+        b = np.zeros(self.ndof)
+        check(_lib.lib().fcm_hp_disc_load(self._h, _ptr(b)))
+        return b
+
+    def leaves(self):
+        ptr = np.zeros(self.nleaves + 1, np.int64)
+        dofs = np.zeros(self.leaf_entries, np.int32)
+        K = np.zeros(self.leaf_matrix_entries)
+        info = np.zeros((self.nleaves, 5), np.int32)
+        check(_lib.lib().fcm_hp_disc_leaves(self._h, _ptr(ptr), _ptr(dofs), _ptr(K), _ptr(info)))
+        return ptr, dofs, K, info
+
+    def close(self):
+        if getattr(self, "_h", None) is not None and self._h.value:
+            _lib.lib().fcm_hp_disc_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class HpSolver:
+    """Owns an fcm_hp handle: the hp-multigrid over levels (p,k) ... (1,k) ... (1,0) on the device."""
+
+    def __init__(self, disc: HpDisc, stream=None, **over):
+        cfg = disc.cfg
+        self.cfg = cfg
+        self.level_n = disc.level_n.copy()
+        self.nlevels = disc.nlevels
+        self._p = params_of(cfg, stream, **over)
+        h = C.c_void_p()
+        check(_lib.lib().fcm_hp_setup(disc._h, C.byref(self._p), C.byref(h)))
+        self._h = h
+        self.device = torch.device("cuda", torch.cuda.current_device())
+
+    def close(self):
+        if getattr(self, "_h", None) is not None and self._h.value:
+            _lib.lib().fcm_hp_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def ndofs(self, level=0) -> int:
+        return int(self.level_n[level])
+
+    def _dv(self, t, level, name):
+        return _vecptr(t, self.ndofs(level), self.device, name)
+
+    def _vec(self, level=0):
+        return torch.zeros(self.ndofs(level), dtype=torch.float64, device=self.device)
+
+    def apply(self, x, level=0):
+        y = self._vec(level)
+        check(_lib.lib().fcm_hp_apply(self._h, level, self._dv(x, level, "x"), _ptr(y)))
+        return y
+
+    def smooth(self, r, x, level=0):
+        check(_lib.lib().fcm_hp_smooth(self._h, level, self._dv(r, level, "r"), self._dv(x, level, "x")))
+        return x
+
+    def vcycle(self, r):
+        z = self._vec()
+        check(_lib.lib().fcm_hp_vcycle(self._h, self._dv(r, 0, "r"), _ptr(z)))
+        return z
+
+    def pcg_solve(self, b, rtol=None, maxit=None, x=None):
+        rtol = self.cfg.rtol if rtol is None else rtol
+        maxit = self.cfg.maxit if maxit is None else maxit
+        x = self._vec() if x is None else x
+        it = C.c_int32()
+        hist = np.zeros(maxit + 1)
+        rc = _lib.lib().fcm_hp_pcg_solve(self._h, self._dv(b, 0, "b"), self._dv(x, 0, "x"), rtol, maxit,
+                                         C.byref(it), _ptr(hist))
+        check(rc, allow_not_converged=True)
+        return x, it.value, hist[: it.value + 1]
+
+    def export_blocks(self, level):
+        """(blocks as lists of level indices, inverses) of level `level` (identical-setup parity)."""
+        nb, nd, ni = C.c_int64(), C.c_int64(), C.c_int64()
+        L = _lib.lib()
+        check(L.fcm_hp_export_blocks(self._h, level, C.byref(nb), C.byref(nd), C.byref(ni), None, None, None))
+        ptr = np.zeros(nb.value + 1, np.int64)
+        dofs = np.zeros(nd.value, np.int32)
+        inv = np.zeros(ni.value)
+        check(L.fcm_hp_export_blocks(self._h, level, C.byref(nb), C.byref(nd), C.byref(ni), _ptr(ptr), _ptr(dofs),
+                                     _ptr(inv)))
+        blocks, invs, o = [], [], 0
+        for i in range(nb.value):
+            d = dofs[ptr[i]:ptr[i + 1]].astype(np.int64)
+            m = len(d)
+            blocks.append(d)
+            invs.append(inv[o:o + m * m].reshape(m, m))
+            o += m * m
+        return blocks, invs
+
+    def stats(self):
+        a, b, c = C.c_int64(), C.c_int64(), C.c_int64()
+        check(_lib.lib().fcm_hp_stats(self._h, C.byref(a), C.byref(b), C.byref(c)))
+        return {"launches": a.value, "coarse_iters": b.value, "vcycles": c.value}

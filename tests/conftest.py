@@ -24,7 +24,7 @@ def tol_log():
     parity assertion that uses one; written to gpurun_out/parity_tolerances.json at the end of
     the session (reading R18: the widened tolerance actually applied is logged)."""
     def rec(pair, check, q, value, tol, **extra):
-        _TOL_RECORDS.append({"case": getattr(pair, "name", pair.cfg.name), "check": check, "q": int(q),
+        _TOL_RECORDS.append({"case": pair if isinstance(pair, str) else getattr(pair, "name", pair.cfg.name), "check": check, "q": int(q),
                              "rel_diff": float(value), "tol": float(tol),
                              **{k: float(v) for k, v in extra.items()}})
     return rec

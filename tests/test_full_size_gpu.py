@@ -95,7 +95,7 @@ def test_cfg3_operator_rows(cfg3):
         assert checked >= 8, q
 
 
-def test_cfg3_patch_smoother_rows(cfg3):
+def test_cfg3_patch_smoother_rows(cfg3, tol_log):
     from oracle.sample import schwarz_row
     cfg, S, b, L, perm = cfg3
     q = cfg.p
@@ -113,15 +113,20 @@ def test_cfg3_patch_smoother_rows(cfg3):
     # interior DOFs (8 patches each) of: a cut cell, a fictitious cell, a regular cell, a cell on
     # the x = 0 Dirichlet face (boundary-type patches)
     rows = [int(L.dof.cell_dofs[c, a_int]) for c in (cells[0], cells[2], cells[3], cells[4])]
-    got, lu, ch = [], [], []
+    # reading R18: the tolerance is 1e-10, widened per row by 4x the larger of (a) the oracle's
+    # own LU-vs-Cholesky spread and (b) its sensitivity to cut-cell matrices perturbed at the
+    # generator-parity level (entrywise 1e-13 relative; L0 measures 2e-14 Frobenius): the patches
+    # of a fictitious cell next to cut cells are graded by alpha = 1e-8, so two setups that agree
+    # to 1e-14 give inverses that agree only to kappa * 1e-14.
     for i in rows:
-        got.append(xo[i])
-        lu.append(schwarz_row(L, r, i, q, "patch", omega, inv="lu"))
-        ch.append(schwarz_row(L, r, i, q, "patch", omega, inv="chol"))
-    got, lu, ch = map(np.array, (got, lu, ch))
-    spread = np.linalg.norm(ch - lu) / np.linalg.norm(lu)
-    err = np.linalg.norm(got - lu) / np.linalg.norm(lu)
-    assert err <= max(1e-10, 4 * spread), (err, spread, got, lu)
+        lu = schwarz_row(L, r, i, q, "patch", omega, inv="lu")
+        ch = schwarz_row(L, r, i, q, "patch", omega, inv="chol")
+        pt = schwarz_row(L, r, i, q, "patch", omega, inv="lu", perturb=1e-13)
+        spread = max(abs(ch - lu), abs(pt - lu)) / abs(lu)
+        err = abs(xo[i] - lu) / abs(lu)
+        tol_log("cfg3_full_size", f"L3_patch_smoother_row_{i}", q, err, max(1e-10, 4 * spread),
+                lu_chol=abs(ch - lu) / abs(lu), setup_sensitivity=abs(pt - lu) / abs(lu))
+        assert err <= max(1e-10, 4 * spread), (i, err, spread, xo[i], lu, ch, pt)
 
 
 def test_cfg3_fcg_sampled_residual(cfg3):
