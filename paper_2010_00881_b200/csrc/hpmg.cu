@@ -63,7 +63,7 @@ namespace {
 
 constexpr int kHpThreads = 256;
 constexpr int kHpDotBlocks = 296;   // 2 x 148 SMs: fixed grid -> deterministic partial sums
-constexpr int kHpMaxBlock = 4096;
+constexpr int kHpMaxBlock = 6144;   // 2 x 6144 x 8 B = 96 KB of shared memory per CTA
 
 // ---- kernels --------------------------------------------------------------------------------
 template <int NCH>
@@ -87,6 +87,7 @@ __global__ void __launch_bounds__(kHpThreads) k_hp_apply(int64_t nleaf, const in
     double acc[NCH];
 #pragma unroll
     for (int c = 0; c < NCH; ++c) acc[c] = 0.0;
+#pragma unroll 4
     for (int b = 0; b < ml; ++b) {
       const double xb = xs[b];
       const double* __restrict__ row = Ke + (int64_t)b * m;
@@ -134,6 +135,90 @@ __global__ void __launch_bounds__(NT) k_hp_smooth(int64_t b0, int64_t b1, const 
       const int a = threadIdx.x + NT * c;
       if (a < m) atomicAdd(&x[bdofs[o + a]], omega * acc[c]);
     }
+    __syncthreads();
+  }
+}
+
+// Packed symmetric Schwarz apply (the production smoother): A_i^{-1} stored lower-packed (row b
+// holds A[b][0..b], offset b(b+1)/2 -- half the bytes of full storage).  One CTA per
+// block, NW warps; warp w streams rows b = w, w + NW, ...: lanes own columns a = lane + 32c, so a
+// row contributes y_a += A[b][a] r_b (a < b, column-owner registers, no reduction) and
+// y_b += sum_{a<=b} A[b][a] r_a (the transposed half: one 5-shuffle warp reduction per row).  The
+// per-warp column sums and the row sums meet in shared memory (fp64 shared atomics); the result
+// is scattered x += omega y with global atomics (blocks overlap).
+template <int NW, int NCH>
+__device__ __forceinline__ void hp_sym_block(const double* __restrict__ A, int m, const double* rs, double* ys) {
+  constexpr int PW = 32 * NCH;            // column panel width
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int P0 = 0; P0 < m; P0 += PW) {   // column panels (one unless m > 32 NCH)
+    double acc[NCH];
+#pragma unroll
+    for (int c = 0; c < NCH; ++c) acc[c] = 0.0;
+    // rows b >= P0 touch the panel (a <= b); warp w takes b = P0 + w, P0 + w + NW, ...
+#pragma unroll 4
+    for (int b = P0 + w; b < m; b += NW) {
+      const double* __restrict__ row = A + (int64_t)b * (b + 1) / 2;
+      const double rb = rs[b];
+      double v[NCH];
+#pragma unroll
+      for (int c = 0; c < NCH; ++c) {
+        const int a = P0 + lane + 32 * c;
+        v[c] = a <= b ? __ldg(row + a) : 0.0;
+      }
+      double dot = 0.0;
+#pragma unroll
+      for (int c = 0; c < NCH; ++c) {
+        const int a = P0 + lane + 32 * c;
+        if (a < b) acc[c] = fma(v[c], rb, acc[c]);          // strictly lower: column-owner half
+        if (a <= b) dot = fma(v[c], rs[a], dot);              // the row half (incl. the diagonal)
+      }
+#pragma unroll
+      for (int off = 16; off; off >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, off);
+      if (lane == 0) atomicAdd(&ys[b], dot);
+    }
+#pragma unroll
+    for (int c = 0; c < NCH; ++c) {
+      const int a = P0 + lane + 32 * c;
+      if (a < m) atomicAdd(&ys[a], acc[c]);
+    }
+  }
+}
+
+// Packed symmetric Schwarz apply (the production smoother): A_i^{-1} stored lower-packed (row b
+// holds A[b][0..b], offset b(b+1)/2 -- half the bytes of full storage).  One CTA of
+// NW warps per block (grid-stride over a range of blocks sorted by DESCENDING size, so the large
+// blocks start first); warp w streams rows b = w, w + NW, ...: lanes own columns a = lane + 32c, so
+// a row contributes y_a += A[b][a] r_b (a < b, column-owner registers, no reduction) and
+// y_b += sum_{a<=b} A[b][a] r_a (the transposed half: one 5-shuffle warp reduction per row).  The
+// per-warp column sums and the row sums meet in shared memory (fp64 shared atomics); the result is
+// scattered x += omega y with global atomics (blocks overlap).  MAXCH caps the register chunks of
+// the instance (blocks up to 32 MAXCH DOFs in one panel; larger ones loop over panels).
+template <int NW, int MAXCH>
+__global__ void __launch_bounds__(NW * 32) k_hp_smooth_sym(int64_t b0, int64_t b1, const int64_t* __restrict__ bptr,
+                                                         const int32_t* __restrict__ bdofs,
+                                                         const int64_t* __restrict__ iptr,
+                                                         const double* __restrict__ inv, const double* __restrict__ r,
+                                                         double* __restrict__ x, double omega, int mmax) {
+  extern __shared__ double sm_sym[];
+  double* rs = sm_sym;                    // [mmax]
+  double* ys = sm_sym + mmax;             // [mmax]
+  for (int64_t B = b0 + blockIdx.x; B < b1; B += gridDim.x) {
+    const int64_t o = bptr[B];
+    const int m = (int)(bptr[B + 1] - o);
+    const double* __restrict__ A = inv + iptr[B];
+    for (int a = threadIdx.x; a < m; a += NW * 32) {
+      rs[a] = r[bdofs[o + a]];
+      ys[a] = 0.0;
+    }
+    __syncthreads();
+    const int nch = (m + 31) / 32;
+    if (nch <= 1) hp_sym_block<NW, 1>(A, m, rs, ys);
+    else if (nch <= 2 || MAXCH < 4) hp_sym_block<NW, (MAXCH < 2 ? MAXCH : 2)>(A, m, rs, ys);
+    else if (nch <= 4 || MAXCH < 8) hp_sym_block<NW, (MAXCH < 4 ? MAXCH : 4)>(A, m, rs, ys);
+    else if (nch <= 8 || MAXCH < 16) hp_sym_block<NW, (MAXCH < 8 ? MAXCH : 8)>(A, m, rs, ys);
+    else hp_sym_block<NW, MAXCH>(A, m, rs, ys);
+    __syncthreads();
+    for (int a = threadIdx.x; a < m; a += NW * 32) atomicAdd(&x[bdofs[o + a]], omega * ys[a]);
     __syncthreads();
   }
 }
@@ -202,16 +287,17 @@ __global__ void k_hp_identity_pad(double* W, int64_t MP, int64_t n) {
     W[l * MP + l] = 1.0;
 }
 
-// copy the leading m x m block of each workspace matrix into the packed-by-block inverse array
+// the leading m x m block of each workspace matrix -> the block's lower-packed inverse
 __global__ void k_hp_extract(const double* W, int MP, const int64_t* __restrict__ dst_off,
                              const int32_t* __restrict__ bsize, double* inv) {
   const double* Wb = W + (int64_t)blockIdx.x * MP * MP;
   const int m = bsize[blockIdx.x];
   double* out = inv + dst_off[blockIdx.x];
-  for (int e = threadIdx.x; e < m * m; e += blockDim.x) {
-    const int a = e / m, b = e % m;
-    out[e] = 0.5 * (Wb[(int64_t)a * MP + b] + Wb[(int64_t)b * MP + a]);   // symmetrise
-  }
+  // lower-packed, symmetrised: out[b(b+1)/2 + a] = (W_ba + W_ab) / 2, a <= b
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int b = warp; b < m; b += blockDim.x >> 5)
+    for (int a = lane; a <= b; a += 32)
+      out[(int64_t)b * (b + 1) / 2 + a] = 0.5 * (Wb[(int64_t)b * MP + a] + Wb[(int64_t)a * MP + b]);
 }
 
 // z = Ainv r (dense symmetric, row-major): warp per output row
@@ -306,7 +392,8 @@ __global__ void k_hp_add(double* __restrict__ y, const double* __restrict__ x, i
 // ---- handle -----------------------------------------------------------------------------------
 struct HpClass {
   int64_t b0, b1;
-  int nt, nch;
+  int nt, nch;      // warps per CTA, column chunks per lane
+  int64_t mmax;     // largest block of the class (shared-memory size)
 };
 
 struct HpLevel {
@@ -425,13 +512,26 @@ int launch_smooth(fcm_hp* h, int l, const double* r, double* x, double omega) {
     const int64_t nb = c.b1 - c.b0;
     if (nb <= 0) continue;
     const int grid = (int)std::min<int64_t>(nb, 148 * 16);
-#define HPS(NT, C) \
-  if (c.nt == NT && c.nch == C) { k_hp_smooth<NT, C><<<grid, NT, 0, h->stream>>>(c.b0, c.b1, L.bptr, L.bdofs, L.iptr, L.inv, r, x, omega); }
-    HPS(32, 1) else HPS(64, 1) else HPS(128, 1) else HPS(256, 1) else HPS(256, 2) else HPS(256, 4) else HPS(256, 8)
-    else HPS(256, 16) else return fail(FCM_EINVAL, "fcm_hp: no smoother kernel for class (%d, %d)", c.nt, c.nch);
+    const int mmax = (int)c.mmax;
+    const size_t smem = (size_t)2 * mmax * 8;
+#define HPS(NW, C)                                                                                    \
+  if (c.nt == NW && c.nch == C) {                                                                     \
+    k_hp_smooth_sym<NW, C><<<grid, NW * 32, smem, h->stream>>>(c.b0, c.b1, L.bptr, L.bdofs, L.iptr, L.inv, r, x, \
+                                                               omega, mmax);                          \
+  } else
+    HPS(8, 8) HPS(8, 16)
+    return fail(FCM_EINVAL, "fcm_hp: no smoother kernel for class (%d warps, %d chunks)", c.nt, c.nch);
 #undef HPS
     h->launches++;
   }
+  return FCM_OK;
+}
+
+int smooth_kernel_attrs() {
+#define HPA2(NW, C) \
+  HCU(cudaFuncSetAttribute((const void*)k_hp_smooth_sym<NW, C>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * kHpMaxBlock * 8));
+  HPA2(8, 8) HPA2(8, 16)
+#undef HPA2
   return FCM_OK;
 }
 
@@ -614,12 +714,11 @@ BlockSet build_blocks(int dim, int n, int block, int64_t nleaf, const std::vecto
   return B;
 }
 
+// launch class of a block of m DOFs: 8 warps per CTA; register chunks MAXCH = 8 for m <= 256
+// (one launch for all small and medium blocks, the instance dispatches per block), 16 for the
+// large ones (panel width 512, panel loop above)
 HpClass class_of(int m) {
-  if (m <= 32) return {0, 0, 32, 1};
-  if (m <= 64) return {0, 0, 64, 1};
-  if (m <= 128) return {0, 0, 128, 1};
-  if (m <= 256) return {0, 0, 256, 1};
-  return {0, 0, 256, nch_for((m + 7) / 8)};   // 256 threads x NCH: NCH = ceil(m / 256) rounded to 2^k
+  return {0, 0, 8, m <= 256 ? 8 : 16, m};
 }
 
 int setup_level_blocks(fcm_hp* h, int l, int block, double omega, const std::vector<int64_t>& lptr,
@@ -632,7 +731,7 @@ int setup_level_blocks(fcm_hp* h, int l, int block, double omega, const std::vec
   // order by size (stable): one launch per size class
   std::vector<int64_t> ord(nb);
   for (int64_t i = 0; i < nb; ++i) ord[i] = i;
-  std::stable_sort(ord.begin(), ord.end(), [&](int64_t a, int64_t b) { return B.dofs[a].size() < B.dofs[b].size(); });
+  std::stable_sort(ord.begin(), ord.end(), [&](int64_t a, int64_t b) { return B.dofs[a].size() > B.dofs[b].size(); });
   std::vector<int64_t> bptr(nb + 1, 0), iptr(nb + 1, 0);
   std::vector<int32_t> bd;
   for (int64_t k = 0; k < nb; ++k) {
@@ -640,7 +739,7 @@ int setup_level_blocks(fcm_hp* h, int l, int block, double omega, const std::vec
     if ((int)d.size() > kHpMaxBlock)
       return fail(FCM_EINVAL, "fcm_hp: Schwarz block with %zu DOFs on level %d exceeds %d", d.size(), l, kHpMaxBlock);
     bptr[k + 1] = bptr[k] + (int64_t)d.size();
-    iptr[k + 1] = iptr[k] + (int64_t)d.size() * (int64_t)d.size();
+    iptr[k + 1] = iptr[k] + (int64_t)d.size() * ((int64_t)d.size() + 1) / 2;   // lower-packed
     bd.insert(bd.end(), d.begin(), d.end());
   }
   L.nblk = nb;
@@ -658,6 +757,7 @@ int setup_level_blocks(fcm_hp* h, int l, int block, double omega, const std::vec
     }
     c.b0 = k;
     c.b1 = e;
+    c.mmax = bptr[k + 1] - bptr[k];   // blocks are sorted by descending size
     L.cls.push_back(c);
     k = e;
   }
@@ -767,7 +867,7 @@ int setup_level_blocks(fcm_hp* h, int l, int block, double omega, const std::vec
 int setup_direct(fcm_hp* h, const std::vector<int32_t>& mlev) {
   const int l = h->nlev - 1;
   const int64_t n = h->lev[l].n;
-  if (n > 30000) return fail(FCM_EINVAL, "fcm_hp: direct coarse solve of %lld DOFs (limit 30000; use FCM_COARSE_AS_PCG)", (long long)n);
+  if (n > 40000) return fail(FCM_EINVAL, "fcm_hp: direct coarse solve of %lld DOFs (limit 40000: 12.8 GB dense inverse; use FCM_COARSE_AS_PCG)", (long long)n);
   const int64_t MP = 32 * ((n + 31) / 32);
   double *W = nullptr, *d_eq = nullptr;
   int* d_status = nullptr;
@@ -835,6 +935,7 @@ extern "C" int fcm_hp_setup(const fcm_hp_disc* d, const fcm_params* prm, fcm_hp*
   const std::vector<double>* K;
   hp_disc_view(d, &dim, &n, &p, &n_f, &ndof, &level_n, &lptr, &kptr, &ldofs, &K, &info);
   if (ndof <= 0 || level_n.empty() || level_n.back() <= 0) return fail(FCM_EINVAL, "fcm_hp_setup: empty system");
+  HRC(smooth_kernel_attrs());
   std::unique_ptr<fcm_hp> h(new fcm_hp());
   h->dim = dim; h->n = n; h->p = p; h->n_f = n_f; h->ndof = ndof;
   h->nleaf = (int64_t)lptr->size() - 1;
@@ -998,7 +1099,14 @@ extern "C" int fcm_hp_export_blocks(const fcm_hp* h, int32_t level, int64_t* n_b
   if (!L.has_blocks && !direct) return fail(FCM_EINVAL, "fcm_hp_export_blocks: level %d has no blocks", level);
   const int64_t nb = direct ? 1 : L.nblk;
   const int64_t nd = direct ? L.n : L.n_bdofs;
-  const int64_t ni = direct ? L.n * L.n : L.n_inv;
+  int64_t ni = direct ? L.n * L.n : 0;
+  std::vector<int64_t> hptr;
+  HCU(cudaStreamSynchronize(h->stream));
+  if (!direct) {   // full m x m per block in the export (the device keeps them lower-packed)
+    hptr.resize(nb + 1);
+    HCU(cudaMemcpy(hptr.data(), L.bptr, (nb + 1) * 8, cudaMemcpyDeviceToHost));
+    for (int64_t i = 0; i < nb; ++i) ni += (hptr[i + 1] - hptr[i]) * (hptr[i + 1] - hptr[i]);
+  }
   if (n_blocks) *n_blocks = nb;
   if (dof_entries) *dof_entries = nd;
   if (inv_entries) *inv_entries = ni;
@@ -1013,7 +1121,22 @@ extern "C" int fcm_hp_export_blocks(const fcm_hp* h, int32_t level, int64_t* n_b
   HCU(cudaStreamSynchronize(h->stream));
   if (ptr) HCU(cudaMemcpy(ptr, L.bptr, (nb + 1) * 8, cudaMemcpyDeviceToHost));
   if (dofs) HCU(cudaMemcpy(dofs, L.bdofs, nd * 4, cudaMemcpyDeviceToHost));
-  if (inv) HCU(cudaMemcpy(inv, L.inv, ni * 8, cudaMemcpyDeviceToHost));
+  if (inv) {
+    std::vector<double> pk(L.n_inv);
+    HCU(cudaMemcpy(pk.data(), L.inv, L.n_inv * 8, cudaMemcpyDeviceToHost));
+    int64_t po = 0, fo = 0;
+    for (int64_t i = 0; i < nb; ++i) {
+      const int64_t m = hptr[i + 1] - hptr[i];
+      for (int64_t b = 0; b < m; ++b)
+        for (int64_t a = 0; a <= b; ++a) {
+          const double v = pk[po + b * (b + 1) / 2 + a];
+          inv[fo + b * m + a] = v;
+          inv[fo + a * m + b] = v;
+        }
+      po += m * (m + 1) / 2;
+      fo += m * m;
+    }
+  }
   return FCM_OK;
 }
 
