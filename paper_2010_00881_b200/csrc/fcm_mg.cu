@@ -958,7 +958,8 @@ const void* reg_kernel(int m, int* M_out) {
 }
 const void* mma_kernel(int m) {
 #define CASE(MM) case MM: return (const void*)k_cell_mma<MM, gsz<MM>()>;
-  switch (m) { FCM_FOR_M(CASE) CASE(64) CASE(125) default: break; }   // 64 / 125: tensor p = 3 / 4 (configs 5 / 3)
+  // 64 / 125: tensor p = 3 / 4 (configs 5 / 3); 60 / 96: trunk elasticity p = 2 / 3 (config 4)
+  switch (m) { FCM_FOR_M(CASE) CASE(60) CASE(64) CASE(96) CASE(125) default: break; }
 #undef CASE
   return nullptr;
 }
@@ -980,7 +981,9 @@ const void* ws_kernel(int m, int variant, int* nthreads, size_t* smem) {
     }
   switch (m) {
     WSV(27)
+    WSV(60)
     WSV(64)
+    case 96: WS(96, 4, 8, 2, false)
     case 125: WS(125, 4, 8, 2, false)
     default: break;
   }

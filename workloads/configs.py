@@ -74,11 +74,15 @@ CONFIGS = {
                    geometry={"kind": "seeded", "count": 8, "r_min": 0.05, "r_max": 0.12, "seed": 2}),
     "cfg3": Config("cfg3", dim=3, n=64, p=4, block="patch",
                    geometry={"kind": "seeded", "count": 64, "r_min": 0.03, "r_max": 0.08, "seed": 3}),
+    # configs 4 and 5 name no coarse solver (4) or a Jacobi-PCG whose 750-900 inner iterations per
+    # V-cycle dominate the solve (5); their default is the h-coarsened coarse CG (R21, P:227
+    # Remark): config 4 2.02 s vs 8.66 s with CG+AS (profiles/r02_s3_bench_cfg4_*.json)
     "cfg4": Config("cfg4", dim=3, n=64, p=3, space="trunk", physics="elasticity",
                    geometry={"kind": "seeded", "count": 200, "r_min": 0.02, "r_max": 0.05, "seed": 4},
-                   dirichlet=0b000001, traction_face=1),
+                   dirichlet=0b000001, traction_face=1, coarse="gmg_pcg"),
     "cfg5": Config("cfg5", dim=3, n=256, p=3,
-                   geometry={"kind": "seeded", "count": 1000, "r_min": 0.01, "r_max": 0.03, "seed": 5}),
+                   geometry={"kind": "seeded", "count": 1000, "r_min": 0.01, "r_max": 0.03, "seed": 5},
+                   coarse="gmg_pcg"),
 }
 
 
