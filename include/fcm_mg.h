@@ -352,7 +352,7 @@ int fcm_mg_launch_count(const fcm_mg* h, int64_t* launches);
  * hp level sequence (Fig. hpmultigrid), finest first:
  *   (p,k), (p-1,k), ..., (1,k), (1,k-1), ..., (1,0)       (k = deepest depth carrying DOFs),
  * level (q, kc) = the DOFs of mode order <= q and depth <= kc; nested, so restriction is index
- * selection.  DOF order of the library: by the COARSEST level containing the DOF
+ * selection; trailing levels without DOFs are dropped.  DOF order of the library: by the COARSEST level containing the DOF
  * (descending), so every level is a PREFIX of the fine vector as on uniform grids.
  * Schwarz blocks (reading R26, Fig. 7 caption P:273 "granularity of the base elements"):
  * elementwise = the level DOFs nonzero on one BASE element; patchwise = those nonzero on the

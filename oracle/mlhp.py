@@ -259,8 +259,13 @@ class MlhpProblem:
 
     # -- hp level sequence (Fig. hpmultigrid) --------------------------------
     def level_sequence(self):
+        """(p,k) ... (1,k), (1,k-1) ... (1,0); trailing levels without DOFs are dropped
+        (when every base element is refined, no base vertex is active and (1,0) is empty)."""
         p, k = self.cfg.p, int(self.dof_depth.max()) if self.ndof else 0
-        return [(q, k) for q in range(p, 0, -1)] + [(1, kc) for kc in range(k - 1, -1, -1)]
+        seq = [(q, k) for q in range(p, 0, -1)] + [(1, kc) for kc in range(k - 1, -1, -1)]
+        while len(seq) > 1 and len(self.level_dofs(*seq[-1])) == 0:
+            seq.pop()
+        return seq
 
     def level_dofs(self, q, kc):
         return np.nonzero((self.dof_order <= q) & (self.dof_depth <= kc))[0]

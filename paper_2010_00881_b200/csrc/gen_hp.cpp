@@ -269,6 +269,12 @@ extern "C" int fcm_hp_generate(const fcm_hp_spec* s, fcm_hp_disc** out) {
   D->level_n.assign(nlev, 0);
   for (auto& o : order)
     for (int l = 0; l <= (int)(-o.first); ++l) D->level_n[l] += n_f;
+  // trailing levels without DOFs are dropped (every base element refined: (1,0) is empty)
+  while (D->level_n.size() > 1 && D->level_n.back() == 0) {
+    D->level_n.pop_back();
+    D->level_q.pop_back();
+    D->level_k.pop_back();
+  }
   D->keys.assign((size_t)D->ndof * 8, 0);
   for (int64_t i = 0; i < nscal; ++i) {
     int64_t t = order[i].second;

@@ -63,7 +63,7 @@ namespace {
 
 constexpr int kHpThreads = 256;
 constexpr int kHpDotBlocks = 296;   // 2 x 148 SMs: fixed grid -> deterministic partial sums
-constexpr int kHpMaxBlock = 6144;   // 2 x 6144 x 8 B = 96 KB of shared memory per CTA
+constexpr int kHpMaxBlock = 4096;   // tile-streamed blocks: 64 KB of vectors + 128 KB of rings per CTA
 
 // ---- kernels --------------------------------------------------------------------------------
 template <int NCH>
@@ -220,6 +220,183 @@ __global__ void __launch_bounds__(NW * 32) k_hp_smooth_sym(int64_t b0, int64_t b
     __syncthreads();
     for (int a = threadIdx.x; a < m; a += NW * 32) atomicAdd(&x[bdofs[o + a]], omega * ys[a]);
     __syncthreads();
+  }
+}
+
+// ---- large blocks: tile-packed inverses streamed by bulk copies ------------------------------
+// Blocks with more than kHpTileMin DOFs store A_i^{-1} TILE-PACKED (the lower triangle of 32x32
+// tiles, row-major over tile rows; off-diagonal tiles full 1024 doubles, diagonal tiles packed
+// lower 528; padding rows/columns hold the identity of the padded inverse).  One CTA of 8 warps
+// per block (grid-stride over the large blocks, descending size); each warp owns tiles
+// t = w, w + 8, ... of the block and streams them through a 2-stage ring of 8 KB shared-memory
+// stages filled by cp.async.bulk (mbarrier complete_tx), issuing across block boundaries.  A
+// tile (I, J) is read row by row with lane = column: y_J += T^T r_I in a register, the row
+// products y_I += T r_J by one 31-shuffle reduce-scatter (the layout and arithmetic of the
+// patch-smoother streaming warps, patch.cuh).
+constexpr int kHpTileMin = 128;
+constexpr int kHpTileMax = 4096;
+constexpr int kHpTileWarps = 8;
+constexpr int kHpStages = 2;
+constexpr int kHpDiag = 528;
+
+__host__ __device__ inline int64_t hp_tile_pack_size(int nt) {
+  return (int64_t)nt * (nt - 1) / 2 * 1024 + (int64_t)nt * kHpDiag;
+}
+__host__ __device__ inline int64_t hp_tile_off(int I, int J) {   // J <= I
+  return (int64_t)I * (I - 1) / 2 * 1024 + (int64_t)I * kHpDiag + (int64_t)J * 1024;
+}
+__device__ __forceinline__ uint32_t hp_smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void hp_mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(hp_smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void hp_mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(hp_smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void hp_bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               ::"r"(hp_smem_u32(dst)), "l"(src), "r"(bytes), "r"(hp_smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void hp_mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}\n"
+      ::"r"(hp_smem_u32(bar)), "r"(parity) : "memory");
+}
+// 32 per-lane row partials -> lane r holds the warp sum of partial r (reduce-scatter butterfly)
+__device__ __forceinline__ double hp_reduce_scatter32(double (&p)[32]) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int hh = 16; hh >= 1; hh >>= 1) {
+    const bool up = lane & hh;
+#pragma unroll
+    for (int i = 0; i < hh; ++i) {
+      const double send = up ? p[i] : p[i + hh];
+      const double keep = up ? p[i + hh] : p[i];
+      p[i] = keep + __shfl_xor_sync(0xffffffffu, send, hh);
+    }
+  }
+  return p[0];
+}
+
+__global__ void __launch_bounds__(kHpTileWarps * 32, 1)
+k_hp_smooth_tiles(int64_t b0, int64_t b1, const int64_t* __restrict__ bptr, const int32_t* __restrict__ bdofs,
+                  const int64_t* __restrict__ iptr, const double* __restrict__ inv, const double* __restrict__ r,
+                  double* __restrict__ x, double omega, int ntmax) {
+  extern __shared__ __align__(128) double sm_t[];
+  double* ring_all = sm_t;                                          // [8][2][1024]
+  uint64_t* bars_all = (uint64_t*)(ring_all + kHpTileWarps * kHpStages * 1024);   // [8][2]
+  double* xs = (double*)(bars_all + kHpTileWarps * kHpStages);      // [32 ntmax]
+  double* ys = xs + 32 * ntmax;                                     // [32 ntmax]
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  double* ring = ring_all + w * kHpStages * 1024;
+  uint64_t* bars = bars_all + w * kHpStages;
+  if (lane == 0)
+    for (int s = 0; s < kHpStages; ++s) hp_mbar_init(&bars[s], 1);
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  __syncthreads();
+  // issue cursor of this warp over (block, tile) in processing order
+  int64_t iB = b0 + blockIdx.x;
+  int it = w;
+  auto ntiles_of = [&](int64_t B) {
+    const int m = (int)(bptr[B + 1] - bptr[B]);
+    const int nt = (m + 31) / 32;
+    return nt * (nt + 1) / 2;
+  };
+  auto advance = [&]() {   // next (block, tile) with a tile for this warp
+    while (iB < b1) {
+      if (it < ntiles_of(iB)) return true;
+      iB += gridDim.x;
+      it = w;
+    }
+    return false;
+  };
+  int64_t issued = 0;
+  auto issue_next = [&]() {
+    if (!advance()) return;
+    int I = (int)((sqrtf(8.0f * it + 1.0f) - 1.0f) * 0.5f);
+    while (I * (I + 1) / 2 > it) --I;
+    while ((I + 1) * (I + 2) / 2 <= it) ++I;
+    const int J = it - I * (I + 1) / 2;
+    const uint32_t bytes = (I == J ? kHpDiag : 1024) * 8;
+    const int s = (int)(issued % kHpStages);
+    hp_mbar_expect_tx(&bars[s], bytes);
+    hp_bulk_g2s(ring + s * 1024, inv + iptr[iB] + hp_tile_off(I, J), bytes, &bars[s]);
+    ++issued;
+    it += kHpTileWarps;
+  };
+  if (lane == 0)
+    for (int s = 0; s < kHpStages; ++s) issue_next();
+  int64_t item = 0;
+  for (int64_t B = b0 + blockIdx.x; B < b1; B += gridDim.x) {
+    const int64_t o = bptr[B];
+    const int m = (int)(bptr[B + 1] - o);
+    const int nt = (m + 31) / 32;
+    for (int a = threadIdx.x; a < 32 * nt; a += blockDim.x) {
+      xs[a] = a < m ? r[bdofs[o + a]] : 0.0;
+      ys[a] = 0.0;
+    }
+    __syncthreads();
+    const int ntiles = nt * (nt + 1) / 2;
+    for (int t = w; t < ntiles; t += kHpTileWarps) {
+      int I = (int)((sqrtf(8.0f * t + 1.0f) - 1.0f) * 0.5f);
+      while (I * (I + 1) / 2 > t) --I;
+      while ((I + 1) * (I + 2) / 2 <= t) ++I;
+      const int J = t - I * (I + 1) / 2;
+      const int s = (int)(item % kHpStages);
+      hp_mbar_wait(&bars[s], (uint32_t)((item / kHpStages) & 1));
+      const double* tl = ring + s * 1024;
+      const double xJ = xs[32 * J + lane];
+      double yJ = 0.0;
+      double pr[32];
+      if (I != J) {
+#pragma unroll
+        for (int rr = 0; rr < 32; ++rr) {
+          const double a = tl[rr * 32 + lane];
+          pr[rr] = a * xJ;
+          yJ = fma(a, xs[32 * I + rr], yJ);
+        }
+      } else {
+#pragma unroll
+        for (int rr = 0; rr < 32; ++rr) {
+          const double a = lane <= rr ? tl[rr * (rr + 1) / 2 + lane] : 0.0;
+          pr[rr] = a * xJ;
+          if (lane < rr) yJ = fma(a, xs[32 * I + rr], yJ);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        issue_next();
+      }
+      const double yI = hp_reduce_scatter32(pr);
+      ++item;
+      atomicAdd(&ys[32 * I + lane], yI);
+      atomicAdd(&ys[32 * J + lane], yJ);
+    }
+    __syncthreads();
+    for (int a = threadIdx.x; a < m; a += blockDim.x) atomicAdd(&x[bdofs[o + a]], omega * ys[a]);
+    __syncthreads();
+  }
+}
+
+// workspace (ld MP) -> tile-packed lower storage, symmetrised; grid (tiles of the largest block,
+// blocks of the chunk)
+__global__ void k_hp_pack_tiles(const double* W, int MP, const int64_t* __restrict__ dst_off,
+                                const int32_t* __restrict__ bsize, double* inv) {
+  const int m = bsize[blockIdx.y];
+  const int nt = (m + 31) / 32;
+  const int t = blockIdx.x;
+  if (t >= nt * (nt + 1) / 2) return;
+  int I = 0;
+  while ((I + 1) * (I + 2) / 2 <= t) ++I;
+  const int J = t - I * (I + 1) / 2;
+  const double* Wb = W + (int64_t)blockIdx.y * MP * MP;
+  double* out = inv + dst_off[blockIdx.y] + hp_tile_off(I, J);
+  for (int e = threadIdx.x; e < 1024; e += blockDim.x) {
+    const int rr = e / 32, c = e % 32;
+    const int gi = 32 * I + rr, gj = 32 * J + c;
+    const double v = 0.5 * (Wb[(int64_t)gi * MP + gj] + Wb[(int64_t)gj * MP + gi]);
+    if (I != J) out[e] = v;
+    else if (c <= rr) out[rr * (rr + 1) / 2 + c] = v;
   }
 }
 
@@ -513,6 +690,15 @@ int launch_smooth(fcm_hp* h, int l, const double* r, double* x, double omega) {
     if (nb <= 0) continue;
     const int grid = (int)std::min<int64_t>(nb, 148 * 16);
     const int mmax = (int)c.mmax;
+    if (c.nt == -1) {
+      const int ntm = (mmax + 31) / 32;
+      const size_t smt = (size_t)kHpTileWarps * kHpStages * 1024 * 8 + kHpTileWarps * kHpStages * 8 + 2 * 32 * ntm * 8;
+      const int gt = (int)std::min<int64_t>(nb, 148);
+      k_hp_smooth_tiles<<<gt, kHpTileWarps * 32, smt, h->stream>>>(c.b0, c.b1, L.bptr, L.bdofs, L.iptr, L.inv, r, x,
+                                                                    omega, ntm);
+      h->launches++;
+      continue;
+    }
     const size_t smem = (size_t)2 * mmax * 8;
 #define HPS(NW, C)                                                                                    \
   if (c.nt == NW && c.nch == C) {                                                                     \
@@ -532,6 +718,8 @@ int smooth_kernel_attrs() {
   HCU(cudaFuncSetAttribute((const void*)k_hp_smooth_sym<NW, C>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * kHpMaxBlock * 8));
   HPA2(8, 8) HPA2(8, 16)
 #undef HPA2
+  HCU(cudaFuncSetAttribute((const void*)k_hp_smooth_tiles, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           kHpTileWarps * kHpStages * 1024 * 8 + kHpTileWarps * kHpStages * 8 + 2 * kHpTileMax * 8));
   return FCM_OK;
 }
 
@@ -718,7 +906,8 @@ BlockSet build_blocks(int dim, int n, int block, int64_t nleaf, const std::vecto
 // (one launch for all small and medium blocks, the instance dispatches per block), 16 for the
 // large ones (panel width 512, panel loop above)
 HpClass class_of(int m) {
-  return {0, 0, 8, m <= 256 ? 8 : 16, m};
+  if (m > kHpTileMin) return {0, 0, -1, 0, m};   // tile-streamed (k_hp_smooth_tiles)
+  return {0, 0, 8, 8, m};
 }
 
 int setup_level_blocks(fcm_hp* h, int l, int block, double omega, const std::vector<int64_t>& lptr,
@@ -739,7 +928,8 @@ int setup_level_blocks(fcm_hp* h, int l, int block, double omega, const std::vec
     if ((int)d.size() > kHpMaxBlock)
       return fail(FCM_EINVAL, "fcm_hp: Schwarz block with %zu DOFs on level %d exceeds %d", d.size(), l, kHpMaxBlock);
     bptr[k + 1] = bptr[k] + (int64_t)d.size();
-    iptr[k + 1] = iptr[k] + (int64_t)d.size() * ((int64_t)d.size() + 1) / 2;   // lower-packed
+    const int64_t md = (int64_t)d.size();   // lower-packed, or tile-packed for the large blocks
+    iptr[k + 1] = iptr[k] + (md > kHpTileMin ? hp_tile_pack_size((int)((md + 31) / 32)) : md * (md + 1) / 2);
     bd.insert(bd.end(), d.begin(), d.end());
   }
   L.nblk = nb;
@@ -847,7 +1037,12 @@ int setup_level_blocks(fcm_hp* h, int l, int block, double omega, const std::vec
       }
     }
     k_equil<<<(unsigned)nc, 256, MP * 8, h->stream>>>(W, MP, d_eq, 1);
-    k_hp_extract<<<(unsigned)nc, 256, 0, h->stream>>>(W, MP, d_off, d_bsize, L.inv);
+    if (MP > kHpTileMin) {   // the chunk holds blocks of one padded size MP: all tiled or all packed
+      const int ntm = MP / 32;
+      k_hp_pack_tiles<<<dim3(ntm * (ntm + 1) / 2, (unsigned)nc), 256, 0, h->stream>>>(W, MP, d_off, d_bsize, L.inv);
+    } else {
+      k_hp_extract<<<(unsigned)nc, 256, 0, h->stream>>>(W, MP, d_off, d_bsize, L.inv);
+    }
     HCU(cudaGetLastError());
     HCU(cudaMemcpyAsync(status.data(), d_status, nc * 4, cudaMemcpyDeviceToHost, h->stream));
     HCU(cudaStreamSynchronize(h->stream));
@@ -1127,13 +1322,20 @@ extern "C" int fcm_hp_export_blocks(const fcm_hp* h, int32_t level, int64_t* n_b
     int64_t po = 0, fo = 0;
     for (int64_t i = 0; i < nb; ++i) {
       const int64_t m = hptr[i + 1] - hptr[i];
+      const bool tiled = m > kHpTileMin;
       for (int64_t b = 0; b < m; ++b)
         for (int64_t a = 0; a <= b; ++a) {
-          const double v = pk[po + b * (b + 1) / 2 + a];
+          double v;
+          if (!tiled) {
+            v = pk[po + b * (b + 1) / 2 + a];
+          } else {
+            const int I = (int)(b / 32), J = (int)(a / 32), rr = (int)(b % 32), cc = (int)(a % 32);
+            v = pk[po + hp_tile_off(I, J) + (I == J ? rr * (rr + 1) / 2 + cc : rr * 32 + cc)];
+          }
           inv[fo + b * m + a] = v;
           inv[fo + a * m + b] = v;
         }
-      po += m * (m + 1) / 2;
+      po += tiled ? hp_tile_pack_size((int)((m + 31) / 32)) : m * (m + 1) / 2;
       fo += m * m;
     }
   }

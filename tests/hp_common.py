@@ -23,6 +23,8 @@ HP_CASES = {
     "poisson2d_p2_k2_element_aspcg": dict(kind="small", dim=2, n=4, p=2, k=2, block="element", coarse="as_pcg"),
     "poisson3d_p2_k1_patch": dict(kind="small", dim=3, n=3, p=2, k=1, block="patch"),
     "elast3d_p2_k1_element": dict(kind="small", dim=3, n=3, p=2, k=1, block="element", physics="elasticity"),
+    # every base element cut and refined: (1,0) is empty and dropped (degenerate case)
+    "poisson2d_fully_refined": dict(kind="small", dim=2, n=2, p=2, k=1, block="patch", void=([[0.5, 0.5]], [0.3])),
 }
 
 
@@ -32,7 +34,7 @@ def hp_config(name):
     if c.pop("kind") == "plate":
         return hp_plate(c["n"], c["k"], block=c["block"])
     dim = c["dim"]
-    void = ([[0.45] * dim], [0.28]) if dim == 2 else ([[0.3] * dim], [0.15])
+    void = c.get("void") or (([[0.45] * dim], [0.28]) if dim == 2 else ([[0.3] * dim], [0.15]))
     kw = {"block": c["block"], "coarse": c.get("coarse", "direct")}
     phys = c.get("physics", "poisson")
     if phys == "poisson":

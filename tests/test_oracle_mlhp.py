@@ -208,3 +208,14 @@ def test_plate_paper_counts():
         assert el[2] > 2 * el[0], (n, el)
         assert max(pa) - min(pa) <= 1, (n, pa)
         assert all(abs(a - g) <= 2 for a, g in zip(pa, g_pa)), (n, pa, g_pa)
+
+
+def test_fully_refined_base_drops_empty_coarse_level():
+    """Every base element cut (n = 2, one large void) and refined: no base vertex is active (R25),
+    so (1,0) is empty and dropped; the V-cycle still solves (coarsest level (1,1) direct)."""
+    cfg = small_config(2, 2, 2, voids=([[0.5, 0.5]], [0.3]), kmax=1, dirichlet=0b0101)
+    P = MlhpProblem(cfg)
+    assert len(P.level_dofs(1, 0)) == 0
+    assert P.level_sequence() == [(2, 1), (1, 1)]
+    x, it, hist = MlhpHierarchy(P).fcg(P.b)
+    assert hist[-1] < cfg.rtol
