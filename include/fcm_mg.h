@@ -247,6 +247,16 @@ int fcm_mg_level_m(const fcm_mg* h, int32_t q, int32_t* m);
  * influenced neighbourhood) and *n_shared_types inverses shared by all regular blocks of a
  * boundary type (inverse scaled by 1/alpha for all-fictitious neighbourhoods).            */
 int fcm_mg_block_counts(const fcm_mg* h, int32_t q, int64_t* n_individual, int32_t* n_shared_types);
+/* Individual patches stored as low-rank corrections of the regular patch (patchwise levels with
+ * fast diagonalisation, single GPU; FCM_PATCH_WB=0 disables): every member cell uncut and
+ * physical, so A_i = A0 + P_S E P_S^T differs from the regular (Kronecker) patch matrix A0 only on
+ * the k slots S touched by the outer ring's cut / fictitious cells, and (Woodbury)
+ * A_i^{-1} r = z - A0^{-1} P_S C P_S^T z, z = A0^{-1} r, C = H - H (H + E)^{-1} H, H = (P_S^T A0^{-1}
+ * P_S)^{-1} -- the same operator as the explicit inverse (Eq. AdditiveSchwarz), with k x k
+ * instead of m(m+1)/2 stored numbers.  *n_lowrank of the *n_individual blocks of
+ * fcm_mg_block_counts are of this kind; *c_entries = sum of k^2 (the C matrices, full storage).
+ * fcm_mg_export_block_inverses expands them to explicit inverses.                           */
+int fcm_mg_lowrank_info(const fcm_mg* h, int32_t q, int64_t* n_lowrank, int64_t* c_entries);
 
 /* DOF keys of the fine layout (host buffer of ndofs(p) int64, see CONVENTIONS).            */
 int fcm_mg_dof_keys(const fcm_mg* h, int64_t* keys);

@@ -64,6 +64,7 @@ _SIGS = {
     "fcm_mg_ndofs": (I32, [P, I32, P]),
     "fcm_mg_level_m": (I32, [P, I32, P]),
     "fcm_mg_block_counts": (I32, [P, I32, P, P]),
+    "fcm_mg_lowrank_info": (I32, [P, I32, P, P]),
     "fcm_gen_cut_matrices_device": (I32, [P, P, C.c_int64, P, P, C.c_int64, P, P, P]),
     "fcm_mg_export_block_inverses": (I32, [P, I32, P, P, P, P, P]),
     "fcm_mg_dof_keys": (I32, [P, P]),

@@ -14,6 +14,7 @@
 namespace fcm {
 
 constexpr int kBlkNone = INT32_MIN;   // anchor whose block has no free DOF (skipped)
+constexpr int kBlkWb = INT32_MIN + 1;  // individual patch applied as a low-rank correction (patch_wb.cuh)
 
 struct BlockAsmArgs {
   int nx, ny, nz, dim;          // owned cell grid (anchor coordinates are relative to it)

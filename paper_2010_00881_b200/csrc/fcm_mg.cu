@@ -33,6 +33,7 @@
 #include "coarse_tiled.cuh"
 #include "blocks.cuh"
 #include "patch.cuh"
+#include "patch_wb.cuh"
 #include "cellmma.cuh"
 #include "cellws.cuh"
 #include "common.hpp"
@@ -144,6 +145,18 @@ struct LevelDev {
   int fd_ncls = 0;
   int16_t* fd_midx = nullptr;      // [(q+1)^3] local DOF of element mode (kx,ky,kz)
   double fd_s = 1.0;
+  std::vector<double> fd_tabs_h;   // host copies (low-rank patch setup)
+  std::vector<int> fd_cls_h;
+  // individual patches as low-rank corrections of the regular patch (patch_wb.cuh)
+  int64_t n_wb = 0;
+  int64_t* wb_anchor = nullptr;    // [n_wb]
+  int64_t* wb_soff = nullptr;      // [n_wb + 1]
+  int16_t* wb_slots = nullptr;     // S lists (block slots)
+  int64_t* wb_coff = nullptr;      // [n_wb + 1]
+  double* wb_C = nullptr;          // k x k per patch
+  int16_t* wb_tsl = nullptr;       // [mb] tensor slot of block slot l
+  std::vector<int64_t> wb_anchor_h, wb_soff_h, wb_coff_h;
+  std::vector<int16_t> wb_slots_h, wb_tsl_h;
   // slab mode: interface planes (exchange order) and the smoother increment vector
   int32_t* lo_idx = nullptr;
   int32_t* hi_idx = nullptr;
@@ -169,6 +182,8 @@ struct fcm_mg {
   int dev = 0, num_sms = 148;
   double alpha = 1e-8;
   int64_t ncell = 0, ncut = 0;
+  const double* Kref_host = nullptr;   // setup only (low-rank patch corrections)
+  const double* cutK_host = nullptr;
   uint8_t* d_kind = nullptr;        // owned cells (= d_kind_ext + owned offset)
   int32_t* d_cut_idx = nullptr;
   uint8_t* d_kind_ext = nullptr;    // owned + ghost cell layers (Schwarz assembly)
@@ -1374,10 +1389,23 @@ static const void* patch_kernel(int S, int dim, int irr, int fd) {
   return S == 3 ? patch_kernel_s<3, 2>(irr, fd) : S == 5 ? patch_kernel_s<5, 2>(irr, fd)
          : S == 7 ? patch_kernel_s<7, 2>(irr, fd) : patch_kernel_s<9, 2>(irr, fd);
 }
+static const void* wb_kernel(int S, int dim) {
+  if (dim == 3) return S == 3 ? (const void*)k_patch_wb<3, 3> : S == 5 ? (const void*)k_patch_wb<5, 3>
+                     : S == 7 ? (const void*)k_patch_wb<7, 3> : (const void*)k_patch_wb<9, 3>;
+  return S == 3 ? (const void*)k_patch_wb<3, 2> : S == 5 ? (const void*)k_patch_wb<5, 2>
+         : S == 7 ? (const void*)k_patch_wb<7, 2> : (const void*)k_patch_wb<9, 2>;
+}
+static size_t wb_smem_rt(int S, int dim, int mb) {
+  if (dim == 3) return S == 3 ? wb_smem<3, 3>(mb) : S == 5 ? wb_smem<5, 3>(mb) : S == 7 ? wb_smem<7, 3>(mb) : wb_smem<9, 3>(mb);
+  return S == 3 ? wb_smem<3, 2>(mb) : S == 5 ? wb_smem<5, 2>(mb) : S == 7 ? wb_smem<7, 2>(mb) : wb_smem<9, 2>(mb);
+}
+
 // patchwise smoother (patch.cuh): ONE warp-specialised launch (k_patch_smooth) streams the
 // individual patches' tile-packed inverses and applies the regular patches by fast
 // diagonalisation on the same SMs; off the tensor-Poisson case the regular patches use the
 // dense shared-type kernel (k_block_smooth) after the streaming launch.
+// the low-rank patches belong to the individual population (smoother part 1, and part 0)
+static bool do_irr_wb(const fcm_mg* h, int q, int part) { return part != 2 && h->lev[q].n_wb > 0; }
 static int launch_block_smooth(fcm_mg* h, int q, const double* r, double* x, double coef, int part = 0) {
   LevelDev& Lv = h->lev[q];
   const bool do_irr = part != 2 && Lv.n_irr > 0, do_reg = part != 1 && Lv.n_reg > 0;
@@ -1419,6 +1447,24 @@ static int launch_block_smooth(fcm_mg* h, int q, const double* r, double* x, dou
     const void* kf = patch_kernel(2 * q + 1, h->L.dim, di, df);
     void* args[] = {&io2, &fo2};
     CU(cudaLaunchKernel(kf, dim3(h->num_sms), dim3((kIrrWarps + kFdWarps) * 32), args, patch_smem(h, q), h->stream));
+    h->count();
+  }
+  if (do_irr_wb(h, q, part)) {   // low-rank individual patches (patch_wb.cuh)
+    PatchWbOp wo{};
+    wo.nx = h->L.n[0]; wo.ny = h->L.n[1]; wo.nz = h->L.n[2]; wo.dim = h->L.dim;
+    for (int i = 0; i < 3; ++i) wo.na[i] = Lv.na[i];
+    wo.q = q; wo.S = 2 * q + 1; wo.mb = Lv.mb; wo.ncls = Lv.fd_ncls; wo.n_wb = Lv.n_wb;
+    wo.anchors = Lv.wb_anchor; wo.soff = Lv.wb_soff; wo.slots = Lv.wb_slots; wo.coff = Lv.wb_coff; wo.C = Lv.wb_C;
+    wo.tsl = Lv.wb_tsl; wo.mem = Lv.d_mem; wo.loc = Lv.d_loc;
+    for (int k = 0; k < 8; ++k)
+      for (int i = 0; i < 3; ++i) wo.mo[k][i] = Lv.mo[k][i];
+    wo.cls = Lv.fd_cls; wo.tabs = Lv.fd_tabs; wo.s_fac = Lv.fd_s;
+    wo.base = Lv.base; wo.stride3 = Lv.stride; wo.cmin = Lv.cmin; wo.cmax = Lv.cmax; wo.m = Lv.m;
+    wo.in = r; wo.out = x; wo.coef = coef;
+    void* args[] = {&wo};
+    const int grid = (int)std::min<int64_t>(Lv.n_wb, (int64_t)h->num_sms * 4);
+    CU(cudaLaunchKernel(wb_kernel(2 * q + 1, h->L.dim), dim3(grid), dim3(kWbThreads), args,
+                        wb_smem_rt(2 * q + 1, h->L.dim, Lv.mb), h->stream));
     h->count();
   }
   if (do_reg && !Lv.fd) {
@@ -2354,6 +2400,8 @@ static int setup_patch_fd(fcm_mg* h, int q, const double* K_ref_host) {
   CU(cudaMemcpyAsync(Lv.fd_midx, midx.data(), midx.size() * 2, cudaMemcpyHostToDevice, h->stream));
   CU(cudaStreamSynchronize(h->stream));
   Lv.fd_ncls = ncls;
+  Lv.fd_tabs_h = tabs;
+  Lv.fd_cls_h = cls;
   Lv.fd_s = sfac;
   Lv.fd = !(getenv("FCM_PATCH_FD") && atoi(getenv("FCM_PATCH_FD")) == 0);
   return FCM_OK;
@@ -2480,7 +2528,7 @@ static int setup_patch_blocks(fcm_mg* h, int q, const BlockGeom& g, const std::v
   Lv.n_irr = n_irr;
   std::vector<int32_t> reg;
   for (int64_t A = 0; A < (int64_t)blk.size(); ++A)
-    if (blk[A] < 0 && blk[A] != kBlkNone) reg.push_back((int32_t)A);
+    if (blk[A] < 0 && blk[A] != kBlkNone && blk[A] != kBlkWb) reg.push_back((int32_t)A);
   if (h->det) {   // deterministic mode: regular patches grouped by vertex colour too
     auto colour = [&](int64_t A) {
       return (int)(A % g.na[0]) % 3 + 3 * ((int)((A / g.na[0]) % g.na[1]) % 3) +
@@ -2528,6 +2576,179 @@ static int free_alloc(fcm_mg* h, void* p) {
   auto it = std::find(h->allocs.begin(), h->allocs.end(), p);
   if (it != h->allocs.end()) h->allocs.erase(it);
   CU(cudaFree(p));
+  return FCM_OK;
+}
+
+// Low-rank patch corrections (patch_wb.cuh): per patch, C = H - H F^{-1} H with G = P_S^T A0^{-1} P_S
+// (from the fast-diagonalisation tables), H = G^{-1}, F = H + E, E = sum over the outer ring's
+// non-regular cells of (K_c - K_ref) on S.  Host fp64 (OpenMP), k <= kWbMaxK.
+static bool chol_inv(int k, std::vector<double>& A) {   // in place: A (SPD, k x k) -> A^{-1}
+  std::vector<double> L((size_t)k * k, 0.0);
+  for (int j = 0; j < k; ++j) {
+    double d = A[(size_t)j * k + j];
+    for (int t = 0; t < j; ++t) d -= L[(size_t)j * k + t] * L[(size_t)j * k + t];
+    if (!(d > 0.0) || !std::isfinite(d)) return false;
+    const double ljj = std::sqrt(d);
+    L[(size_t)j * k + j] = ljj;
+    for (int i = j + 1; i < k; ++i) {
+      double v = A[(size_t)i * k + j];
+      for (int t = 0; t < j; ++t) v -= L[(size_t)i * k + t] * L[(size_t)j * k + t];
+      L[(size_t)i * k + j] = v / ljj;
+    }
+  }
+  // inv(L) by forward substitution, then A^{-1} = inv(L)^T inv(L)
+  std::vector<double> Li((size_t)k * k, 0.0);
+  for (int c = 0; c < k; ++c)
+    for (int i = c; i < k; ++i) {
+      double v = i == c ? 1.0 : 0.0;
+      for (int t = c; t < i; ++t) v -= L[(size_t)i * k + t] * Li[(size_t)t * k + c];
+      Li[(size_t)i * k + c] = v / L[(size_t)i * k + i];
+    }
+  for (int i = 0; i < k; ++i)
+    for (int j = 0; j <= i; ++j) {
+      double v = 0.0;
+      for (int t = i; t < k; ++t) v += Li[(size_t)t * k + i] * Li[(size_t)t * k + j];
+      A[(size_t)i * k + j] = A[(size_t)j * k + i] = v;
+    }
+  return true;
+}
+
+static int setup_patch_wb(fcm_mg* h, int q, const BlockGeom& g, const std::vector<int64_t>& wb,
+                          const std::vector<std::vector<int16_t>>& wb_S, const std::vector<uint8_t>& kind,
+                          const std::vector<int32_t>& cut_idx) {
+  LevelDev& Lv = h->lev[q];
+  Lv.n_wb = (int64_t)wb.size();
+  if (wb.empty()) return FCM_OK;
+  const Layout& L = h->L;
+  const int dim = L.dim, mb = g.mb, S = 2 * q + 1, m = L.m, TSZ = S * S + S;
+  const int N = dim == 3 ? S * S * S : S * S;
+  const int nas = (int)(g.amap.size() / mb);
+  // tensor slot of every block slot
+  std::vector<int16_t> tsl(mb);
+  for (int l = 0; l < mb; ++l) {
+    int t = 0, mul = 1;
+    for (int ax = 0; ax < dim; ++ax) {
+      const int k1 = L.modes[g.loc[l]].k[ax], mo = g.mo[g.mem[l]][ax];
+      const int sa = k1 >= 2 ? (mo == -1 ? k1 - 1 : q + k1 - 1) : (mo + k1 + 1) * q;
+      t += sa * mul;
+      mul *= S;
+    }
+    tsl[l] = (int16_t)t;
+  }
+  std::vector<int64_t> soff(wb.size() + 1, 0), coff(wb.size() + 1, 0);
+  for (size_t p = 0; p < wb.size(); ++p) {
+    const int64_t k = (int64_t)wb_S[p].size();
+    soff[p + 1] = soff[p] + k;
+    coff[p + 1] = coff[p] + k * k;
+  }
+  std::vector<int16_t> slots(soff.back());
+  for (size_t p = 0; p < wb.size(); ++p) std::copy(wb_S[p].begin(), wb_S[p].end(), slots.begin() + soff[p]);
+  std::vector<double> Call((size_t)coff.back());
+  const int* cls = Lv.fd_cls_h.data();
+  const double* tabs = Lv.fd_tabs_h.data();
+  const int ncls = Lv.fd_ncls;
+  const double sfac = Lv.fd_s, alpha = h->alpha;
+  int bad = 0;
+  int64_t bad_anchor = -1;
+#pragma omp parallel for schedule(dynamic, 16)
+  for (int64_t p = 0; p < (int64_t)wb.size(); ++p) {
+    const int64_t A = wb[p];
+    const int ac[3] = {(int)(A % g.na[0]), (int)((A / g.na[0]) % g.na[1]), (int)(A / ((int64_t)g.na[0] * g.na[1]))};
+    const std::vector<int16_t>& Sl = wb_S[p];
+    const int k = (int)Sl.size();
+    const double* tb[3];
+    int co = 0;
+    for (int ax = 0; ax < 3; ++ax) {
+      tb[ax] = tabs + ((size_t)ax * ncls + cls[co + ac[ax]]) * TSZ;
+      co += g.na[ax];
+    }
+    // U[i][mode] = prod_ax T_ax(slot_ax(i), mode_ax) / sqrt(sfac Lambda), G = U U^T
+    std::vector<double> U((size_t)k * N);
+    for (int i = 0; i < k; ++i) {
+      const int t = tsl[Sl[i]];
+      const int sx = t % S, sy = (t / S) % S, sz = dim == 3 ? t / (S * S) : 0;
+      for (int e = 0; e < N; ++e) {
+        const int mx = e % S, my = (e / S) % S, mz = dim == 3 ? e / (S * S) : 0;
+        const double lam = tb[0][S * S + mx] + tb[1][S * S + my] + (dim == 3 ? tb[2][S * S + mz] : 0.0);
+        double v = tb[0][sx * S + mx] * tb[1][sy * S + my] / std::sqrt(sfac * lam);
+        if (dim == 3) v *= tb[2][sz * S + mz];
+        U[(size_t)i * N + e] = v;
+      }
+    }
+    std::vector<double> H((size_t)k * k), E((size_t)k * k, 0.0);
+    for (int i = 0; i < k; ++i)
+      for (int j = 0; j <= i; ++j) {
+        double v = 0.0;
+        for (int e = 0; e < N; ++e) v += U[(size_t)i * N + e] * U[(size_t)j * N + e];
+        H[(size_t)i * k + j] = H[(size_t)j * k + i] = v;   // G
+      }
+    bool ok = chol_inv(k, H);   // H = G^{-1}
+    // E: the outer ring's non-regular cells, (K_c - K_ref) on S
+    for (int d = 0; d < nas && ok; ++d) {
+      int c3[3] = {ac[0] + g.aoff + d % g.nasm, dim >= 2 ? ac[1] + g.aoff + (d / g.nasm) % g.nasm : 0,
+                   dim == 3 ? ac[2] + g.aoff + d / (g.nasm * g.nasm) : 0};
+      bool inside = true;
+      for (int i = 0; i < 3; ++i) inside = inside && c3[i] >= 0 && c3[i] < (i < dim ? L.n[i] : 1);
+      if (!inside) continue;
+      const int64_t c = ((int64_t)c3[2] * L.n[1] + c3[1]) * L.n[0] + c3[0];
+      const int kd = kind[c];
+      if (kd == 0) continue;
+      const double* Kc = kd == 2 ? h->cutK_host + (size_t)cut_idx[c] * m * m : nullptr;
+      for (int i = 0; i < k; ++i) {
+        const int a = g.amap[(size_t)d * mb + Sl[i]];
+        if (a < 0) continue;
+        for (int j = 0; j < k; ++j) {
+          const int b = g.amap[(size_t)d * mb + Sl[j]];
+          if (b < 0) continue;
+          const double kr = h->Kref_host[(size_t)a * m + b];
+          E[(size_t)i * k + j] += (Kc ? Kc[(size_t)a * m + b] : alpha * kr) - kr;
+        }
+      }
+    }
+    // F = H + E -> F^{-1};  C = H - H F^{-1} H
+    std::vector<double> F((size_t)k * k);
+    for (size_t e = 0; e < F.size(); ++e) F[e] = H[e] + E[e];
+    ok = ok && chol_inv(k, F);
+    if (!ok) {
+#pragma omp critical
+      { bad = 1; bad_anchor = A; }
+      continue;
+    }
+    std::vector<double> T1((size_t)k * k, 0.0);   // F^{-1} H
+    for (int i = 0; i < k; ++i)
+      for (int t = 0; t < k; ++t) {
+        const double f = F[(size_t)i * k + t];
+        for (int j = 0; j < k; ++j) T1[(size_t)i * k + j] += f * H[(size_t)t * k + j];
+      }
+    double* C = Call.data() + coff[p];
+    for (int i = 0; i < k; ++i)
+      for (int j = 0; j < k; ++j) {
+        double v = 0.0;
+        for (int t = 0; t < k; ++t) v += H[(size_t)i * k + t] * T1[(size_t)t * k + j];
+        C[(size_t)i * k + j] = H[(size_t)i * k + j] - v;
+      }
+    for (int i = 0; i < k; ++i)   // symmetrise
+      for (int j = 0; j < i; ++j) C[(size_t)i * k + j] = C[(size_t)j * k + i] = 0.5 * (C[(size_t)i * k + j] + C[(size_t)j * k + i]);
+  }
+  if (bad) return fail(FCM_ESINGULAR, "low-rank patch correction not SPD on level q=%d at anchor %lld", q, (long long)bad_anchor);
+  RC(h->alloc(&Lv.wb_anchor, wb.size()));
+  RC(h->alloc(&Lv.wb_soff, soff.size()));
+  RC(h->alloc(&Lv.wb_slots, std::max<size_t>(slots.size(), 1)));
+  RC(h->alloc(&Lv.wb_coff, coff.size()));
+  RC(h->alloc(&Lv.wb_C, std::max<size_t>(Call.size(), 1)));
+  RC(h->alloc(&Lv.wb_tsl, mb));
+  CU(cudaMemcpyAsync(Lv.wb_anchor, wb.data(), wb.size() * 8, cudaMemcpyHostToDevice, h->stream));
+  CU(cudaMemcpyAsync(Lv.wb_soff, soff.data(), soff.size() * 8, cudaMemcpyHostToDevice, h->stream));
+  CU(cudaMemcpyAsync(Lv.wb_slots, slots.data(), slots.size() * 2, cudaMemcpyHostToDevice, h->stream));
+  CU(cudaMemcpyAsync(Lv.wb_coff, coff.data(), coff.size() * 8, cudaMemcpyHostToDevice, h->stream));
+  CU(cudaMemcpyAsync(Lv.wb_C, Call.data(), Call.size() * 8, cudaMemcpyHostToDevice, h->stream));
+  CU(cudaMemcpyAsync(Lv.wb_tsl, tsl.data(), mb * 2, cudaMemcpyHostToDevice, h->stream));
+  CU(cudaStreamSynchronize(h->stream));
+  Lv.wb_anchor_h = wb;
+  Lv.wb_soff_h = soff;
+  Lv.wb_coff_h = coff;
+  Lv.wb_slots_h = slots;
+  Lv.wb_tsl_h = tsl;
   return FCM_OK;
 }
 
@@ -2591,6 +2812,51 @@ static int setup_schwarz(fcm_mg* h, int q, const std::vector<uint8_t>& kind,
       irr.push_back(A);
     }
   }
+  // individual patches whose member cells are all uncut and physical: low-rank corrections of the
+  // regular patch (patch_wb.cuh), when the level has fast-diagonalisation tables
+  std::vector<int64_t> wb;
+  std::vector<std::vector<int16_t>> wb_S;
+  if (patch && Lv.fd && !h->det && !h->multi && h->cutK_host && h->Kref_host &&
+      !(getenv("FCM_PATCH_WB") && atoi(getenv("FCM_PATCH_WB")) == 0)) {
+    std::vector<int64_t> keep;
+    for (int64_t A : irr) {
+      int ac[3] = {(int)(A % g.na[0]), (int)((A / g.na[0]) % g.na[1]), (int)(A / ((int64_t)g.na[0] * g.na[1]))};
+      bool inner_ok = true;
+      for (int k = 0; k < g.nmem && inner_ok; ++k) {
+        int c3[3] = {0, 0, 0};
+        bool inside = true;
+        for (int i = 0; i < dim; ++i) {
+          c3[i] = ac[i] + g.mo[k][i];
+          inside = inside && c3[i] >= 0 && c3[i] < L.n[i];
+        }
+        if (!inside) continue;
+        inner_ok = kind[((int64_t)c3[2] * ene[1] + c3[1]) * ene[0] + c3[0]] == 0;
+      }
+      std::vector<char> touched(mb, 0);
+      if (inner_ok)
+        for (int d = 0; d < nas; ++d) {
+          int c3[3] = {ac[0] + g.aoff + d % g.nasm, dim >= 2 ? ac[1] + g.aoff + (d / g.nasm) % g.nasm : 0,
+                       dim == 3 ? ac[2] + g.aoff + d / (g.nasm * g.nasm) : 0};
+          bool inside = true;
+          for (int i = 0; i < 3; ++i) inside = inside && c3[i] >= 0 && c3[i] < (i < dim ? L.n[i] : 1);
+          if (!inside || kind[((int64_t)c3[2] * ene[1] + c3[1]) * ene[0] + c3[0]] == 0) continue;
+          for (int l = 0; l < mb; ++l)
+            if (g.amap[(size_t)d * mb + l] >= 0 && block_dof_index(L, q, g, l, ac) >= 0) touched[l] = 1;
+        }
+      std::vector<int16_t> Sl;
+      for (int l = 0; l < mb; ++l)
+        if (touched[l]) Sl.push_back((int16_t)l);
+      if (inner_ok && !Sl.empty() && (int)Sl.size() <= kWbMaxK) {
+        blk[A] = kBlkWb;
+        wb.push_back(A);
+        wb_S.push_back(std::move(Sl));
+      } else {
+        blk[A] = (int32_t)keep.size();
+        keep.push_back(A);
+      }
+    }
+    irr.swap(keep);
+  }
   if (patch && h->det) {   // deterministic mode: individual patches grouped by vertex colour (v mod 3)
     auto colour = [&](int64_t A) {
       return (int)(A % g.na[0]) % 3 + 3 * ((int)((A / g.na[0]) % g.na[1]) % 3) +
@@ -2625,7 +2891,10 @@ static int setup_schwarz(fcm_mg* h, int q, const std::vector<uint8_t>& kind,
     int ac[3] = {(int)(A % g.na[0]), (int)((A / g.na[0]) % g.na[1]), (int)(A / ((int64_t)g.na[0] * g.na[1]))};
     for (int l = 0; l < mb; ++l) dir[(size_t)b * mb + l] = block_dof_index(L, q, g, l, ac) < 0;
   }
-  if (patch) return setup_patch_blocks(h, q, g, blk, blocks, ntypes, dir);
+  if (patch) {
+    RC(setup_patch_blocks(h, q, g, blk, blocks, ntypes, dir));
+    return setup_patch_wb(h, q, g, wb, wb_S, kind, cut_idx);
+  }
   // device buffers
   int64_t* d_anchors;
   uint8_t* d_virt;
@@ -3322,12 +3591,20 @@ static int setup_impl(const fcm_grid* g, const fcm_params* prm, const fcm_slab* 
   }
   h->dist = h->multi && prm->coarse == FCM_COARSE_GMG_PCG;
   h->eager = h->dist;
+  // fast-diagonalisation tables first: the Schwarz setup of a patch level uses them for the
+  // low-rank individual patches (patch_wb.cuh)
+  if (prm->block == FCM_BLOCK_PATCH)
+    for (int q = 2; q <= g->p; ++q) RC(setup_patch_fd(h.get(), q, K_ref));
+  h->Kref_host = K_ref;
+  h->cutK_host = cut_K;
   for (int q = 1; q <= g->p; ++q)
     if (q >= 2 || ((prm->coarse == FCM_COARSE_AS_PCG || prm->coarse == FCM_COARSE_GMG_PCG) && !h->multi) || h->dist)
       RC(setup_schwarz(h.get(), q, kind, cut_idx));
+  h->Kref_host = nullptr;
+  h->cutK_host = nullptr;
   for (int q = 2; q <= g->p; ++q)
     if (h->lev[q].patch) {
-      RC(setup_patch_fd(h.get(), q, K_ref));
+      if (h->lev[q].n_wb > 0) RC(allow_smem(wb_kernel(2 * q + 1, g->dim), wb_smem_rt(2 * q + 1, g->dim, h->lev[q].mb)));
       if (!h->lev[q].fd) RC(allow_smem((const void*)k_block_smooth, block_smem(h->lev[q].m, h->lev[q].mb)));
       for (int f = 0; f < 3; ++f)
         RC(allow_smem(patch_kernel(2 * q + 1, g->dim, f != 2, f != 1), patch_smem(h.get(), q)));
@@ -4014,8 +4291,17 @@ extern "C" const char* fcm_last_error(void) { return last_error().c_str(); }
 extern "C" int fcm_mg_block_counts(const fcm_mg* h, int32_t q, int64_t* n_individual,
                                    int32_t* n_shared_types) {
   if (!h || q < 1 || q > h->g.p) return fail(FCM_EINVAL, "bad level");
-  if (n_individual) *n_individual = h->lev[q].n_irr;
+  if (n_individual) *n_individual = h->lev[q].n_irr + h->lev[q].n_wb;
   if (n_shared_types) *n_shared_types = h->lev[q].n_types;
+  return FCM_OK;
+}
+
+extern "C" int fcm_mg_lowrank_info(const fcm_mg* h, int32_t q, int64_t* n_lowrank, int64_t* c_entries) {
+  clear_error();
+  if (!h || q < 1 || q > h->g.p) return fail(FCM_EINVAL, "bad level");
+  const LevelDev& Lv = h->lev[q];
+  if (n_lowrank) *n_lowrank = Lv.n_wb;
+  if (c_entries) *c_entries = Lv.n_wb > 0 ? Lv.wb_coff_h.back() : 0;
   return FCM_OK;
 }
 
@@ -4053,6 +4339,59 @@ extern "C" int fcm_mg_export_block_inverses(const fcm_mg* h, int32_t q, int64_t*
     int ac[3] = {(int)(A % g.na[0]), (int)((A / g.na[0]) % g.na[1]), (int)(A / ((int64_t)g.na[0] * g.na[1]))};
     if (dof_index)
       for (int l = 0; l < mb; ++l) dof_index[i * mb + l] = (int32_t)block_dof_index(h->L, q, g, l, ac);
+    if (inv && Lv.blk_h[A] == kBlkWb) {   // low-rank patch: A0^{-1} - Z C Z^T, Z = A0^{-1}[:, S]
+      const auto it = std::lower_bound(Lv.wb_anchor_h.begin(), Lv.wb_anchor_h.end(), A);
+      const int64_t p = it - Lv.wb_anchor_h.begin();
+      const int S = 2 * q + 1, TSZ = S * S + S, dim = h->L.dim;
+      const int N = dim == 3 ? S * S * S : S * S;
+      const int k = (int)(Lv.wb_soff_h[p + 1] - Lv.wb_soff_h[p]);
+      std::vector<double> C((size_t)k * k);
+      CU(cudaMemcpy(C.data(), Lv.wb_C + Lv.wb_coff_h[p], C.size() * 8, cudaMemcpyDeviceToHost));
+      const double* tb[3];
+      int co = 0;
+      for (int ax = 0; ax < 3; ++ax) {
+        tb[ax] = Lv.fd_tabs_h.data() + ((size_t)ax * Lv.fd_ncls + Lv.fd_cls_h[co + ac[ax]]) * TSZ;
+        co += g.na[ax];
+      }
+      std::vector<double> U((size_t)mb * N, 0.0);   // U[l][mode], 0 for absent slots
+      std::vector<char> pres(mb);
+      for (int l = 0; l < mb; ++l) {
+        pres[l] = block_dof_index(h->L, q, g, l, ac) >= 0;
+        if (!pres[l]) continue;
+        const int t = Lv.wb_tsl_h[l];
+        const int sx = t % S, sy = (t / S) % S, sz = dim == 3 ? t / (S * S) : 0;
+        for (int e = 0; e < N; ++e) {
+          const int mx = e % S, my = (e / S) % S, mz = dim == 3 ? e / (S * S) : 0;
+          const double lam = tb[0][S * S + mx] + tb[1][S * S + my] + (dim == 3 ? tb[2][S * S + mz] : 0.0);
+          double v = tb[0][sx * S + mx] * tb[1][sy * S + my] / std::sqrt(Lv.fd_s * lam);
+          if (dim == 3) v *= tb[2][sz * S + mz];
+          U[(size_t)l * N + e] = v;
+        }
+      }
+      std::vector<double> A0((size_t)mb * mb);
+#pragma omp parallel for schedule(static)
+      for (int a = 0; a < mb; ++a)
+        for (int b = 0; b < mb; ++b) {
+          double v = 0.0;
+          for (int e = 0; e < N; ++e) v += U[(size_t)a * N + e] * U[(size_t)b * N + e];
+          A0[(size_t)a * mb + b] = v;
+        }
+      const int16_t* Sl = Lv.wb_slots_h.data() + Lv.wb_soff_h[p];
+      std::vector<double> ZC((size_t)mb * k, 0.0);   // Z C
+      for (int a = 0; a < mb; ++a)
+        for (int i = 0; i < k; ++i) {
+          const double z = A0[(size_t)a * mb + Sl[i]];
+          for (int j = 0; j < k; ++j) ZC[(size_t)a * k + j] += z * C[(size_t)i * k + j];
+        }
+#pragma omp parallel for schedule(static)
+      for (int a = 0; a < mb; ++a)
+        for (int b = 0; b < mb; ++b) {
+          double v = A0[(size_t)a * mb + b];
+          for (int j = 0; j < k; ++j) v -= ZC[(size_t)a * k + j] * A0[(size_t)b * mb + Sl[j]];
+          inv[i * mm + (size_t)a * mb + b] = (pres[a] && pres[b]) ? v : (a == b ? 1.0 : 0.0);
+        }
+      continue;
+    }
     if (inv) {
       const int32_t bq = Lv.blk_h[A];
       const double* src;

@@ -314,6 +314,12 @@ class Solver:
         check(_lib.lib().fcm_mg_block_counts(self._h, q, C.byref(n), C.byref(t)))
         return n.value, t.value
 
+    def lowrank_info(self, q):
+        """(number of low-rank individual patches, total entries of their C matrices) on level q."""
+        a, b = C.c_int64(), C.c_int64()
+        check(_lib.lib().fcm_mg_lowrank_info(self._h, q, C.byref(a), C.byref(b)))
+        return a.value, b.value
+
     def export_block_inverses(self, q):
         """(anchors [n], dof_index [n, m_b] (-1: no free DOF), inverses [n, m_b, m_b]) of level
         q's Schwarz blocks exactly as the smoother applies them (fcm_mg_export_block_inverses,
