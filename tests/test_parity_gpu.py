@@ -562,3 +562,30 @@ def test_maxit_zero_and_bad_vectors():
         pair.S.vcycle(b[:-1].contiguous())
     with pytest.raises(ValueError):
         pair.S.vcycle(b.cpu())
+
+
+@pytest.mark.parametrize("case", ["3d_p2_patch", "3d_p3_patch", "3d_p4_patch729", "2d_p3_patch"])
+def test_lowrank_patches_match_explicit(case, monkeypatch, tol_log):
+    """Low-rank individual patches (patch_wb.cuh, Woodbury on the fast-diagonalised regular patch)
+    against the explicit-inverse path of the same GPU (FCM_PATCH_WB=0) on every patch level: the
+    same Schwarz operator, so the sweeps agree to rounding; and against the oracle's LU inverses
+    for the patches concerned (the L3 test covers the whole smoother)."""
+    cfg = CASES[case]()
+    lr = Pair(cfg)
+    n_lr = [lr.S.lowrank_info(q)[0] for q in range(2, cfg.p + 1)]
+    monkeypatch.setenv("FCM_PATCH_WB", "0")
+    ex = Pair(cfg)
+    monkeypatch.delenv("FCM_PATCH_WB")
+    assert all(ex.S.lowrank_info(q)[0] == 0 for q in range(2, cfg.p + 1))
+    rng = np.random.default_rng(31)
+    for q in range(2, cfg.p + 1):
+        assert lr.S.block_counts(q)[0] == ex.S.block_counts(q)[0]
+        n = lr.S.ndofs(q)
+        r = torch.from_numpy(rng.standard_normal(n)).cuda()
+        a = lr.S.smooth(r, torch.zeros(n, dtype=torch.float64, device="cuda"), q).cpu().numpy()
+        b = ex.S.smooth(r, torch.zeros(n, dtype=torch.float64, device="cuda"), q).cpu().numpy()
+        d = np.linalg.norm(a - b) / np.linalg.norm(b)
+        tol_log(lr, f"lowrank_vs_explicit_smoother_q{q}", q, d, 1e-11, n_lowrank=n_lr[q - 2])
+        assert d <= 1e-11, (q, d, n_lr)
+    if case == "3d_p4_patch729":
+        assert sum(n_lr) > 0, "the case exercises low-rank patches"
