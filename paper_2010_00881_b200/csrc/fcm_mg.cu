@@ -1395,6 +1395,10 @@ static const void* wb_kernel(int S, int dim) {
   return S == 3 ? (const void*)k_patch_wb<3, 2> : S == 5 ? (const void*)k_patch_wb<5, 2>
          : S == 7 ? (const void*)k_patch_wb<7, 2> : (const void*)k_patch_wb<9, 2>;
 }
+static int wb_threads_rt(int S, int dim) {
+  if (dim == 3) return S == 3 ? wb_threads<3, 3>() : S == 5 ? wb_threads<5, 3>() : S == 7 ? wb_threads<7, 3>() : wb_threads<9, 3>();
+  return S == 3 ? wb_threads<3, 2>() : S == 5 ? wb_threads<5, 2>() : S == 7 ? wb_threads<7, 2>() : wb_threads<9, 2>();
+}
 static size_t wb_smem_rt(int S, int dim, int mb) {
   if (dim == 3) return S == 3 ? wb_smem<3, 3>(mb) : S == 5 ? wb_smem<5, 3>(mb) : S == 7 ? wb_smem<7, 3>(mb) : wb_smem<9, 3>(mb);
   return S == 3 ? wb_smem<3, 2>(mb) : S == 5 ? wb_smem<5, 2>(mb) : S == 7 ? wb_smem<7, 2>(mb) : wb_smem<9, 2>(mb);
@@ -1462,8 +1466,9 @@ static int launch_block_smooth(fcm_mg* h, int q, const double* r, double* x, dou
     wo.base = Lv.base; wo.stride3 = Lv.stride; wo.cmin = Lv.cmin; wo.cmax = Lv.cmax; wo.m = Lv.m;
     wo.in = r; wo.out = x; wo.coef = coef;
     void* args[] = {&wo};
-    const int grid = (int)std::min<int64_t>(Lv.n_wb, (int64_t)h->num_sms * 4);
-    CU(cudaLaunchKernel(wb_kernel(2 * q + 1, h->L.dim), dim3(grid), dim3(kWbThreads), args,
+    const int ng = wb_threads_rt(2 * q + 1, h->L.dim) / 32;   // upper bound of the patch groups per CTA
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((Lv.n_wb + ng - 1) / ng + Lv.n_wb / 8, (int64_t)h->num_sms * 3));
+    CU(cudaLaunchKernel(wb_kernel(2 * q + 1, h->L.dim), dim3(grid), dim3(wb_threads_rt(2 * q + 1, h->L.dim)), args,
                         wb_smem_rt(2 * q + 1, h->L.dim, Lv.mb), h->stream));
     h->count();
   }
