@@ -155,6 +155,8 @@ struct LevelDev {
   int64_t* wb_coff = nullptr;      // [n_wb + 1]
   double* wb_C = nullptr;          // k x k per patch
   int16_t* wb_tsl = nullptr;       // [mb] tensor slot of block slot l
+  int16_t* wb_tS = nullptr;        // S lists as tensor slots (the fused path in k_patch_smooth)
+  bool wb_fused = false;           // low-rank patches by k_patch_smooth's FD warps (else k_patch_wb)
   std::vector<int64_t> wb_anchor_h, wb_soff_h, wb_coff_h;
   std::vector<int16_t> wb_slots_h, wb_tsl_h;
   // slab mode: interface planes (exchange order) and the smoother increment vector
@@ -182,6 +184,7 @@ struct fcm_mg {
   int dev = 0, num_sms = 148;
   double alpha = 1e-8;
   int64_t ncell = 0, ncut = 0;
+  int wb_mode = 0;                     // FCM_WB_KERNEL: 0 cost model, 1 always k_patch_wb, 2 always fused
   const double* Kref_host = nullptr;   // setup only (low-rank patch corrections)
   const double* cutK_host = nullptr;
   uint8_t* d_kind = nullptr;        // owned cells (= d_kind_ext + owned offset)
@@ -1432,6 +1435,11 @@ static int launch_block_smooth(fcm_mg* h, int q, const double* r, double* x, dou
   fo.inv_alpha = 1.0 / h->alpha; fo.modeidx = Lv.fd_midx;
   fo.base = Lv.base; fo.stride3 = Lv.stride; fo.cmin = Lv.cmin; fo.cmax = Lv.cmax; fo.m = Lv.m;
   fo.in = r; fo.out = x; fo.coef = coef;
+  // low-rank individual patches: by the fast-diagonalisation warps of the same launch (they finish
+  // the regular patches long before the streaming warps; FCM_WB_KERNEL=1: separate k_patch_wb)
+  const bool wb_fused = do_irr_wb(h, q, part) && Lv.wb_fused;
+  fo.n_wb = wb_fused ? Lv.n_wb : 0;
+  fo.wb_anchor = Lv.wb_anchor; fo.wb_soff = Lv.wb_soff; fo.wb_tS = Lv.wb_tS; fo.wb_coff = Lv.wb_coff; fo.wb_C = Lv.wb_C;
   io.det = h->det ? 1 : 0;
   const int ncol = h->det ? 27 : 1;
   for (int k = 0; k < ncol; ++k) {
@@ -1446,14 +1454,14 @@ static int launch_block_smooth(fcm_mg* h, int q, const double* r, double* x, dou
       fo2.anchors = Lv.reg_list + r0;
       fo2.nreg = fd ? r1 - r0 : 0;
     }
-    const bool di = io2.n_irr > 0, df = fo2.nreg > 0;
+    const bool di = io2.n_irr > 0, df = fo2.nreg + fo2.n_wb > 0;
     if (!di && !df) continue;
     const void* kf = patch_kernel(2 * q + 1, h->L.dim, di, df);
     void* args[] = {&io2, &fo2};
     CU(cudaLaunchKernel(kf, dim3(h->num_sms), dim3((kIrrWarps + kFdWarps) * 32), args, patch_smem(h, q), h->stream));
     h->count();
   }
-  if (do_irr_wb(h, q, part)) {   // low-rank individual patches (patch_wb.cuh)
+  if (do_irr_wb(h, q, part) && !Lv.wb_fused) {   // low-rank individual patches, separate launch
     PatchWbOp wo{};
     wo.nx = h->L.n[0]; wo.ny = h->L.n[1]; wo.nz = h->L.n[2]; wo.dim = h->L.dim;
     for (int i = 0; i < 3; ++i) wo.na[i] = Lv.na[i];
@@ -2742,6 +2750,10 @@ static int setup_patch_wb(fcm_mg* h, int q, const BlockGeom& g, const std::vecto
   RC(h->alloc(&Lv.wb_coff, coff.size()));
   RC(h->alloc(&Lv.wb_C, std::max<size_t>(Call.size(), 1)));
   RC(h->alloc(&Lv.wb_tsl, mb));
+  std::vector<int16_t> tS(slots.size());
+  for (size_t i = 0; i < slots.size(); ++i) tS[i] = tsl[slots[i]];
+  RC(h->alloc(&Lv.wb_tS, std::max<size_t>(tS.size(), 1)));
+  CU(cudaMemcpyAsync(Lv.wb_tS, tS.data(), tS.size() * 2, cudaMemcpyHostToDevice, h->stream));
   CU(cudaMemcpyAsync(Lv.wb_anchor, wb.data(), wb.size() * 8, cudaMemcpyHostToDevice, h->stream));
   CU(cudaMemcpyAsync(Lv.wb_soff, soff.data(), soff.size() * 8, cudaMemcpyHostToDevice, h->stream));
   CU(cudaMemcpyAsync(Lv.wb_slots, slots.data(), slots.size() * 2, cudaMemcpyHostToDevice, h->stream));
@@ -2749,6 +2761,15 @@ static int setup_patch_wb(fcm_mg* h, int q, const BlockGeom& g, const std::vecto
   CU(cudaMemcpyAsync(Lv.wb_C, Call.data(), Call.size() * 8, cudaMemcpyHostToDevice, h->stream));
   CU(cudaMemcpyAsync(Lv.wb_tsl, tsl.data(), mb * 2, cudaMemcpyHostToDevice, h->stream));
   CU(cudaStreamSynchronize(h->stream));
+  // fused into k_patch_smooth's fast-diagonalisation warps when they stay off the critical path:
+  // the explicit patches' stream (at ~6 TB/s) must outlast the FD warps' work (measured ~21.5 ns per
+  // 729-slot regular patch per GPU, a low-rank patch ~2.2 of them); level 4 of config 3: 11.8 ms
+  // stream vs 8.9 ms FD (x 1.5) -> fused; level 3: 2.3 vs 4.6 ms -> separate (launch lists)
+  {
+    const double stream_s = (double)Lv.n_irr * Lv.pstride * 8 / 6.0e12;
+    const double fd_s = ((double)Lv.n_reg + 2.2 * Lv.n_wb) * 21.5e-9 * N / 729.0;
+    Lv.wb_fused = h->wb_mode == 2 || (h->wb_mode == 0 && stream_s > 1.5 * fd_s);
+  }
   Lv.wb_anchor_h = wb;
   Lv.wb_soff_h = soff;
   Lv.wb_coff_h = coff;
@@ -3602,6 +3623,7 @@ static int setup_impl(const fcm_grid* g, const fcm_params* prm, const fcm_slab* 
     for (int q = 2; q <= g->p; ++q) RC(setup_patch_fd(h.get(), q, K_ref));
   h->Kref_host = K_ref;
   h->cutK_host = cut_K;
+  h->wb_mode = getenv("FCM_WB_KERNEL") ? atoi(getenv("FCM_WB_KERNEL")) : 0;
   for (int q = 1; q <= g->p; ++q)
     if (q >= 2 || ((prm->coarse == FCM_COARSE_AS_PCG || prm->coarse == FCM_COARSE_GMG_PCG) && !h->multi) || h->dist)
       RC(setup_schwarz(h.get(), q, kind, cut_idx));

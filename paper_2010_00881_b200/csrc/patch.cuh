@@ -292,6 +292,14 @@ struct PatchFdOp {
   int na[3];
   int q, S;                   // level, slots per axis (2q+1)
   int64_t nreg;
+  // low-rank individual patches (patch_wb.cuh) handled by the same warps after the regular ones:
+  // z = A0^{-1} r, w = C z_S, x += coef (z - A0^{-1} P_S w)
+  int64_t n_wb;
+  const int64_t* wb_anchor;   // [n_wb]
+  const int64_t* wb_soff;     // [n_wb + 1]
+  const int16_t* wb_tS;       // S lists as TENSOR slots (x fastest)
+  const int64_t* wb_coff;     // [n_wb + 1]
+  const double* wb_C;         // k x k row-major per patch
   const int32_t* anchors;     // [nreg] regular anchors
   const int32_t* blk;         // per anchor: type code (alpha flag in bit 12 of -blk-1)
   const int* cls;             // [3][na] axis class of each anchor coordinate
@@ -394,10 +402,13 @@ __device__ __forceinline__ void fd_loop(const PatchFdOp& op, const Tab& T, const
   double* X = wbase + (size_t)w * 2 * N3;
   double* Y = X + N3;
   const double coef = op.coef;
-  for (int64_t i = (int64_t)blockIdx.x * nw + w; i < op.nreg; i += (int64_t)gridDim.x * nw) {
-    const int A = op.anchors[i];
+  const int64_t ntot = op.nreg + op.n_wb;
+  for (int64_t i = (int64_t)blockIdx.x * nw + w; i < ntot; i += (int64_t)gridDim.x * nw) {
+    const bool lowrank = i >= op.nreg;
+    const int64_t pw = i - op.nreg;
+    const int A = lowrank ? (int)op.wb_anchor[pw] : op.anchors[i];
     const int vx = A % op.na[0], vy = (A / op.na[0]) % op.na[1], vz = A / (op.na[0] * op.na[1]);
-    const int t = -op.blk[A] - 1;
+    const int t = lowrank ? 0 : -op.blk[A] - 1;   // low-rank patches: physical regular A0
     const double sc = ((t >> 12) ? op.inv_alpha : 1.0) / op.s_fac;
     const double* Tx = tab + (0 * op.ncls + op.cls[vx]) * tsz;
     const double* Ty = tab + (1 * op.ncls + op.cls[op.na[0] + vy]) * tsz;
@@ -439,31 +450,63 @@ __device__ __forceinline__ void fd_loop(const PatchFdOp& op, const Tab& T, const
     }
     __syncwarp();
     // forward (S^T x S^T x S^T) X with the D^-1 scaling fused into the last axis, then backward
-    if (DIM == 3) {
-      fd_pass<S, DIM, 0, true, false>(X, Y, Tx, nullptr, nullptr, nullptr, 0.0);
+    auto fd_apply = [&]() {
+      if (DIM == 3) {
+        fd_pass<S, DIM, 0, true, false>(X, Y, Tx, nullptr, nullptr, nullptr, 0.0);
+        __syncwarp();
+        fd_pass<S, DIM, 1, true, false>(Y, X, Ty, nullptr, nullptr, nullptr, 0.0);
+        __syncwarp();
+        fd_pass<S, DIM, 2, true, true>(X, Y, Tz, Tx + S2, Ty + S2, Tz + S2, sc);
+        __syncwarp();
+        fd_pass<S, DIM, 2, false, false>(Y, X, Tz, nullptr, nullptr, nullptr, 0.0);
+        __syncwarp();
+        fd_pass<S, DIM, 1, false, false>(X, Y, Ty, nullptr, nullptr, nullptr, 0.0);
+        __syncwarp();
+        fd_pass<S, DIM, 0, false, false>(Y, X, Tx, nullptr, nullptr, nullptr, 0.0);
+      } else {
+        fd_pass<S, DIM, 0, true, false>(X, Y, Tx, nullptr, nullptr, nullptr, 0.0);
+        __syncwarp();
+        fd_pass<S, DIM, 1, true, true>(Y, X, Ty, Tx + S2, Ty + S2, nullptr, sc);
+        __syncwarp();
+        fd_pass<S, DIM, 1, false, false>(X, Y, Ty, nullptr, nullptr, nullptr, 0.0);
+        __syncwarp();
+        fd_pass<S, DIM, 0, false, false>(Y, X, Tx, nullptr, nullptr, nullptr, 0.0);
+      }
       __syncwarp();
-      fd_pass<S, DIM, 1, true, false>(Y, X, Ty, nullptr, nullptr, nullptr, 0.0);
+    };
+    fd_apply();   // X = A0^{-1} r
+    if (!lowrank) {
+#pragma unroll
+      for (int j = 0; j < NL; ++j)
+        if (ids[j] >= 0) atomicAdd(op.out + ids[j], coef * X[lane + 32 * j]);
       __syncwarp();
-      fd_pass<S, DIM, 2, true, true>(X, Y, Tz, Tx + S2, Ty + S2, Tz + S2, sc);
-      __syncwarp();
-      fd_pass<S, DIM, 2, false, false>(Y, X, Tz, nullptr, nullptr, nullptr, 0.0);
-      __syncwarp();
-      fd_pass<S, DIM, 1, false, false>(X, Y, Ty, nullptr, nullptr, nullptr, 0.0);
-      __syncwarp();
-      fd_pass<S, DIM, 0, false, false>(Y, X, Tx, nullptr, nullptr, nullptr, 0.0);
-    } else {
-      fd_pass<S, DIM, 0, true, false>(X, Y, Tx, nullptr, nullptr, nullptr, 0.0);
-      __syncwarp();
-      fd_pass<S, DIM, 1, true, true>(Y, X, Ty, Tx + S2, Ty + S2, nullptr, sc);
-      __syncwarp();
-      fd_pass<S, DIM, 1, false, false>(X, Y, Ty, nullptr, nullptr, nullptr, 0.0);
-      __syncwarp();
-      fd_pass<S, DIM, 0, false, false>(Y, X, Tx, nullptr, nullptr, nullptr, 0.0);
+      continue;
+    }
+    // low-rank patch: z = X kept in registers, w = C z_S (row by row, lanes over columns) into Y,
+    // then X = A0^{-1} P_S w and x += coef (z - X)
+    double zr[NL];
+#pragma unroll
+    for (int j = 0; j < NL; ++j) zr[j] = lane + 32 * j < N3 ? X[lane + 32 * j] : 0.0;
+    for (int l = lane; l < N3; l += 32) Y[l] = 0.0;
+    __syncwarp();
+    const int64_t s0 = op.wb_soff[pw];
+    const int k = (int)(op.wb_soff[pw + 1] - s0);
+    const double* Cp = op.wb_C + op.wb_coff[pw];
+    const int16_t* tS = op.wb_tS + s0;
+    for (int r = 0; r < k; ++r) {
+      double sum = 0.0;
+      for (int c = lane; c < k; c += 32) sum = fma(__ldg(Cp + (int64_t)r * k + c), X[tS[c]], sum);
+#pragma unroll
+      for (int off = 16; off; off >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, off);
+      if (lane == 0) Y[tS[r]] = sum;
     }
     __syncwarp();
+    for (int l = lane; l < N3; l += 32) X[l] = Y[l];
+    __syncwarp();
+    fd_apply();
 #pragma unroll
     for (int j = 0; j < NL; ++j)
-      if (ids[j] >= 0) atomicAdd(op.out + ids[j], coef * X[lane + 32 * j]);
+      if (ids[j] >= 0) atomicAdd(op.out + ids[j], coef * (zr[j] - X[lane + 32 * j]));
     __syncwarp();
   }
 }

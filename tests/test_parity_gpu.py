@@ -564,14 +564,18 @@ def test_maxit_zero_and_bad_vectors():
         pair.S.vcycle(b.cpu())
 
 
+@pytest.mark.parametrize("wb_kernel", ["1", "2"])
 @pytest.mark.parametrize("case", ["3d_p2_patch", "3d_p3_patch", "3d_p4_patch729", "2d_p3_patch"])
-def test_lowrank_patches_match_explicit(case, monkeypatch, tol_log):
+def test_lowrank_patches_match_explicit(case, wb_kernel, monkeypatch, tol_log):
     """Low-rank individual patches (patch_wb.cuh, Woodbury on the fast-diagonalised regular patch)
     against the explicit-inverse path of the same GPU (FCM_PATCH_WB=0) on every patch level: the
-    same Schwarz operator, so the sweeps agree to rounding; and against the oracle's LU inverses
-    for the patches concerned (the L3 test covers the whole smoother)."""
+    same Schwarz operator, so the sweeps agree to rounding.  Both executions of the low-rank patches
+    are covered: the separate k_patch_wb launch (FCM_WB_KERNEL=1) and the fast-diagonalisation warps
+    of k_patch_smooth (=2; the cost model picks it for config 3's level 4)."""
     cfg = CASES[case]()
+    monkeypatch.setenv("FCM_WB_KERNEL", wb_kernel)
     lr = Pair(cfg)
+    monkeypatch.delenv("FCM_WB_KERNEL")
     n_lr = [lr.S.lowrank_info(q)[0] for q in range(2, cfg.p + 1)]
     monkeypatch.setenv("FCM_PATCH_WB", "0")
     ex = Pair(cfg)
