@@ -10,6 +10,8 @@ from workloads import get_config  # noqa: E402
 
 cfg = get_config(sys.argv[1] if len(sys.argv) > 1 else "cfg3")
 what = sys.argv[2] if len(sys.argv) > 2 else "solve"
+if len(sys.argv) > 3:
+    cfg = cfg.replace(coarse=sys.argv[3])
 G = generate(cfg)
 S = Solver.from_problem(cfg, G)
 b = S.load(G)
