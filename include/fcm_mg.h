@@ -255,7 +255,8 @@ int fcm_mg_block_counts(const fcm_mg* h, int32_t q, int64_t* n_individual, int32
  * P_S)^{-1} -- the same operator as the explicit inverse (Eq. AdditiveSchwarz), with k x k
  * instead of m(m+1)/2 stored numbers.  *n_lowrank of the *n_individual blocks of
  * fcm_mg_block_counts are of this kind; *c_entries = sum of k^2 (the C matrices, full storage).
- * fcm_mg_export_block_inverses expands them to explicit inverses.                           */
+ * fcm_mg_export_block_inverses expands them to explicit inverses.  Used on levels whose patches
+ * have >= 300 slots (FCM_PATCH_WB=2: every patch level).                                     */
 int fcm_mg_lowrank_info(const fcm_mg* h, int32_t q, int64_t* n_lowrank, int64_t* c_entries);
 
 /* DOF keys of the fine layout (host buffer of ndofs(p) int64, see CONVENTIONS).            */

@@ -2842,8 +2842,12 @@ static int setup_schwarz(fcm_mg* h, int q, const std::vector<uint8_t>& kind,
   // regular patch (patch_wb.cuh), when the level has fast-diagonalisation tables
   std::vector<int64_t> wb;
   std::vector<std::vector<int16_t>> wb_S;
-  if (patch && Lv.fd && !h->det && !h->multi && h->cutK_host && h->Kref_host &&
-      !(getenv("FCM_PATCH_WB") && atoi(getenv("FCM_PATCH_WB")) == 0)) {
+  // levels with small patches keep the explicit inverses: a 125-slot inverse is 63 KB (~13 ns of
+  // stream), less than the two fast diagonalisations that replace it (cfg3 level 2: 1.27 ms per sweep
+  // explicit vs 1.52 ms low-rank); FCM_PATCH_WB=0 disables, =2 forces every patch level (tests)
+  const int wb_env = getenv("FCM_PATCH_WB") ? atoi(getenv("FCM_PATCH_WB")) : 1;
+  if (patch && Lv.fd && !h->det && !h->multi && h->cutK_host && h->Kref_host && wb_env != 0 &&
+      (wb_env == 2 || mb >= 300)) {
     std::vector<int64_t> keep;
     for (int64_t A : irr) {
       int ac[3] = {(int)(A % g.na[0]), (int)((A / g.na[0]) % g.na[1]), (int)(A / ((int64_t)g.na[0] * g.na[1]))};

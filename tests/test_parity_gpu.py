@@ -574,8 +574,10 @@ def test_lowrank_patches_match_explicit(case, wb_kernel, monkeypatch, tol_log):
     of k_patch_smooth (=2; the cost model picks it for config 3's level 4)."""
     cfg = CASES[case]()
     monkeypatch.setenv("FCM_WB_KERNEL", wb_kernel)
+    monkeypatch.setenv("FCM_PATCH_WB", "2")     # every patch level (default: patches of >= 300 slots)
     lr = Pair(cfg)
     monkeypatch.delenv("FCM_WB_KERNEL")
+    monkeypatch.delenv("FCM_PATCH_WB")
     n_lr = [lr.S.lowrank_info(q)[0] for q in range(2, cfg.p + 1)]
     monkeypatch.setenv("FCM_PATCH_WB", "0")
     ex = Pair(cfg)
