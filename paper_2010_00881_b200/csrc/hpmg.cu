@@ -713,6 +713,22 @@ int launch_smooth(fcm_hp* h, int l, const double* r, double* x, double omega) {
   return FCM_OK;
 }
 
+// setup temporaries: freed on every return path (error returns included)
+struct DevTmp {
+  std::vector<void*> p;
+  template <class T>
+  cudaError_t alloc(T** ptr, size_t bytes) {
+    void* q = nullptr;
+    const cudaError_t e = cudaMalloc(&q, bytes);
+    if (e == cudaSuccess) p.push_back(q);
+    *ptr = (T*)q;
+    return e;
+  }
+  ~DevTmp() {
+    for (void* q : p) cudaFree(q);
+  }
+};
+
 int smooth_kernel_attrs() {
 #define HPA2(NW, C) \
   HCU(cudaFuncSetAttribute((const void*)k_hp_smooth_sym<NW, C>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * kHpMaxBlock * 8));
@@ -978,16 +994,17 @@ int setup_level_blocks(fcm_hp* h, int l, int block, double omega, const std::vec
   int64_t *d_cleaf = nullptr, *d_cmap = nullptr, *d_cptr = nullptr, *d_off = nullptr;
   int32_t *d_amap = nullptr, *d_bsize = nullptr, *d_status = nullptr;
   double *W = nullptr, *d_eq = nullptr;
-  HCU(cudaMalloc(&d_cleaf, std::max<size_t>(cleaf.size(), 1) * 8));
-  HCU(cudaMalloc(&d_cmap, std::max<size_t>(cmap.size(), 1) * 8));
-  HCU(cudaMalloc(&d_amap, std::max<size_t>(amap.size(), 1) * 4));
+  DevTmp tmp;
+  HCU(tmp.alloc(&d_cleaf, std::max<size_t>(cleaf.size(), 1) * 8));
+  HCU(tmp.alloc(&d_cmap, std::max<size_t>(cmap.size(), 1) * 8));
+  HCU(tmp.alloc(&d_amap, std::max<size_t>(amap.size(), 1) * 4));
   HCU(cudaMemcpyAsync(d_cleaf, cleaf.data(), cleaf.size() * 8, cudaMemcpyHostToDevice, h->stream));
   HCU(cudaMemcpyAsync(d_cmap, cmap.data(), cmap.size() * 8, cudaMemcpyHostToDevice, h->stream));
   HCU(cudaMemcpyAsync(d_amap, amap.data(), amap.size() * 4, cudaMemcpyHostToDevice, h->stream));
   int rc = FCM_OK;
   // chunks of equal padded size MP, workspace <= 2 GiB
   const size_t wsz = (size_t)2 << 30;
-  HCU(cudaMalloc(&W, wsz));
+  HCU(tmp.alloc(&W, wsz));
   int64_t maxchunk = 1;
   for (int64_t k = 0; k < nb;) {
     const int m0 = (int)(bptr[k + 1] - bptr[k]);
@@ -998,11 +1015,11 @@ int setup_level_blocks(fcm_hp* h, int l, int block, double omega, const std::vec
     maxchunk = std::max(maxchunk, e - k);
     k = e;
   }
-  HCU(cudaMalloc(&d_cptr, (maxchunk + 1) * 8));
-  HCU(cudaMalloc(&d_off, maxchunk * 8));
-  HCU(cudaMalloc(&d_bsize, maxchunk * 4));
-  HCU(cudaMalloc(&d_status, maxchunk * 4));
-  HCU(cudaMalloc(&d_eq, (size_t)maxchunk * 32 * ((kHpMaxBlock + 31) / 32) * 8));
+  HCU(tmp.alloc(&d_cptr, (maxchunk + 1) * 8));
+  HCU(tmp.alloc(&d_off, maxchunk * 8));
+  HCU(tmp.alloc(&d_bsize, maxchunk * 4));
+  HCU(tmp.alloc(&d_status, maxchunk * 4));
+  HCU(tmp.alloc(&d_eq, (size_t)maxchunk * 32 * ((kHpMaxBlock + 31) / 32) * 8));
   std::vector<int> status(maxchunk);
   for (int64_t k = 0; k < nb && rc == FCM_OK;) {
     const int m0 = (int)(bptr[k + 1] - bptr[k]);
@@ -1053,9 +1070,7 @@ int setup_level_blocks(fcm_hp* h, int l, int block, double omega, const std::vec
       }
     k = e;
   }
-  for (void* q : {(void*)d_cleaf, (void*)d_cmap, (void*)d_amap, (void*)d_cptr, (void*)d_off, (void*)d_bsize,
-                  (void*)d_status, (void*)W, (void*)d_eq})
-    cudaFree(q);
+  HCU(cudaStreamSynchronize(h->stream));   // temporaries are freed by tmp
   return rc;
 }
 
@@ -1066,9 +1081,10 @@ int setup_direct(fcm_hp* h, const std::vector<int32_t>& mlev) {
   const int64_t MP = 32 * ((n + 31) / 32);
   double *W = nullptr, *d_eq = nullptr;
   int* d_status = nullptr;
-  HCU(cudaMalloc(&W, (size_t)MP * MP * 8));
-  HCU(cudaMalloc(&d_eq, (size_t)MP * 8));
-  HCU(cudaMalloc(&d_status, 4));
+  DevTmp tmp;
+  HCU(tmp.alloc(&W, (size_t)MP * MP * 8));
+  HCU(tmp.alloc(&d_eq, (size_t)MP * 8));
+  HCU(tmp.alloc(&d_status, 4));
   HCU(cudaMemsetAsync(W, 0, (size_t)MP * MP * 8, h->stream));
   HCU(cudaMemsetAsync(d_status, 0, 4, h->stream));
   k_hp_asm_dense<<<grid_for(h->nleaf * 32), kHpThreads, 0, h->stream>>>(W, MP, h->nleaf, h->lptr, h->kptr, h->ldofs, h->K,
@@ -1091,9 +1107,6 @@ int setup_direct(fcm_hp* h, const std::vector<int32_t>& mlev) {
   int st = 0;
   HCU(cudaMemcpyAsync(&st, d_status, 4, cudaMemcpyDeviceToHost, h->stream));
   HCU(cudaStreamSynchronize(h->stream));
-  cudaFree(W);
-  cudaFree(d_eq);
-  cudaFree(d_status);
   (void)mlev;
   if (st) return fail(FCM_ESINGULAR, "fcm_hp: the coarse matrix (%lld DOFs) is not SPD", (long long)n);
   return FCM_OK;
@@ -1232,16 +1245,12 @@ extern "C" int fcm_hp_vcycle(fcm_hp* h, const double* r, double* z) {
   return leave(h, FCM_OK);
 }
 
-extern "C" int fcm_hp_pcg_solve(fcm_hp* h, const double* b, double* x, double rtol, int32_t maxit, int32_t* iters,
-                                double* hist) {
-  clear_error();
-  if (!h || !check_vec(b) || !check_vec(x) || !(rtol > 0) || maxit < 0)
-    return fail(FCM_EINVAL, "fcm_hp_pcg_solve: invalid argument");
+static int hp_pcg_body(fcm_hp* h, const double* b, double* x, double rtol, int32_t maxit, int32_t* iters,
+                       double* hist) {
   const int64_t n = h->ndof;
   HpScal* s = h->s;
   h->coarse_iters = 0;
   h->vcycles = 0;
-  HRC(enter(h));
   HCU(cudaMemsetAsync(x, 0, n * 8, h->stream));
   if (iters) *iters = 0;
   HRC(dot(h, b, b, n, &s->bb));
@@ -1249,7 +1258,7 @@ extern "C" int fcm_hp_pcg_solve(fcm_hp* h, const double* b, double* x, double rt
   HCU(cudaStreamSynchronize(h->stream));
   const double bb = h->h_pin[0];
   if (hist) hist[0] = bb == 0.0 ? 0.0 : 1.0;
-  if (bb == 0.0 || maxit == 0) return leave(h, FCM_OK);
+  if (bb == 0.0 || maxit == 0) return FCM_OK;
   double* r = h->w_r;
   k_hp_copy<<<grid_for(n), kHpThreads, 0, h->stream>>>(r, b, n);
   h->launches++;
@@ -1282,7 +1291,16 @@ extern "C" int fcm_hp_pcg_solve(fcm_hp* h, const double* b, double* x, double rt
   }
   if (iters) *iters = it;
   HCU(cudaGetLastError());
-  return leave(h, rc);
+  return rc;
+}
+
+extern "C" int fcm_hp_pcg_solve(fcm_hp* h, const double* b, double* x, double rtol, int32_t maxit, int32_t* iters,
+                                double* hist) {
+  clear_error();
+  if (!h || !check_vec(b) || !check_vec(x) || !(rtol > 0) || maxit < 0)
+    return fail(FCM_EINVAL, "fcm_hp_pcg_solve: invalid argument");
+  HRC(enter(h));
+  return leave(h, hp_pcg_body(h, b, x, rtol, maxit, iters, hist));   // the caller's stream joins on every path
 }
 
 extern "C" int fcm_hp_export_blocks(const fcm_hp* h, int32_t level, int64_t* n_blocks, int64_t* dof_entries,
