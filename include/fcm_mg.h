@@ -422,6 +422,9 @@ int fcm_hp_destroy(fcm_hp* h);
 int fcm_hp_apply(fcm_hp* h, int32_t level, const double* x, double* y);
 /* x += omega_l sum_i P_i A_i^{-1} P_i^T r (Eq. AdditiveSchwarz); device [ndofs(l)]. */
 int fcm_hp_smooth(fcm_hp* h, int32_t level, const double* r, double* x);
+/* Measurement: reps back-to-back smoother sweeps of level l (x accumulates), timed with CUDA events
+ * on the library's stream (no host gaps); *ms = mean per sweep.                                */
+int fcm_hp_time_smooth(fcm_hp* h, int32_t level, const double* r, double* x, int32_t reps, float* ms);
 /* z = one hp V-cycle of Algorithm 1 (R1) applied to r; device [ndof].              */
 int fcm_hp_vcycle(fcm_hp* h, const double* r, double* z);
 /* Flexible PCG with one hp V-cycle per iteration (as fcm_pcg_solve); relres_hist host

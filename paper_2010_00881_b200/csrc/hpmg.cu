@@ -1236,6 +1236,28 @@ extern "C" int fcm_hp_smooth(fcm_hp* h, int32_t level, const double* r, double* 
   return leave(h, FCM_OK);
 }
 
+extern "C" int fcm_hp_time_smooth(fcm_hp* h, int32_t level, const double* r, double* x, int32_t reps, float* ms) {
+  clear_error();
+  if (!h || level < 0 || level >= h->nlev || !h->lev[level].has_blocks || !check_vec(r) || !check_vec(x) || reps < 1 ||
+      !ms)
+    return fail(FCM_EINVAL, "fcm_hp_time_smooth: invalid argument");
+  HRC(enter(h));
+  cudaEvent_t e0, e1;
+  HCU(cudaEventCreate(&e0));
+  HCU(cudaEventCreate(&e1));
+  int rc = launch_smooth(h, level, r, x, h->lev[level].omega);   // warm-up
+  HCU(cudaEventRecord(e0, h->stream));
+  for (int i = 0; i < reps && rc >= 0; ++i) rc = launch_smooth(h, level, r, x, h->lev[level].omega);
+  HCU(cudaEventRecord(e1, h->stream));
+  HCU(cudaEventSynchronize(e1));
+  float t = 0.f;
+  HCU(cudaEventElapsedTime(&t, e0, e1));
+  *ms = t / reps;
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  return leave(h, rc);
+}
+
 extern "C" int fcm_hp_vcycle(fcm_hp* h, const double* r, double* z) {
   clear_error();
   if (!h || !check_vec(r) || !check_vec(z)) return fail(FCM_EINVAL, "fcm_hp_vcycle: invalid argument");

@@ -545,6 +545,14 @@ class HpSolver:
         check(_lib.lib().fcm_hp_vcycle(self._h, self._dv(r, 0, "r"), _ptr(z)))
         return z
 
+    def time_smooth(self, r, x, level=0, reps=20) -> float:
+        """Mean ms per smoother sweep of `level` over `reps` back-to-back sweeps (events on the
+        library's stream)."""
+        ms = C.c_float()
+        check(_lib.lib().fcm_hp_time_smooth(self._h, level, self._dv(r, level, "r"), self._dv(x, level, "x"), reps,
+                                            C.byref(ms)))
+        return ms.value
+
     def pcg_solve(self, b, rtol=None, maxit=None, x=None):
         rtol = self.cfg.rtol if rtol is None else rtol
         maxit = self.cfg.maxit if maxit is None else maxit
