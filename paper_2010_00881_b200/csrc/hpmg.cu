@@ -597,6 +597,8 @@ struct fcm_hp {
   cudaStream_t stream = nullptr;    // the library's own stream (capturable)
   cudaStream_t ustream = nullptr;   // the caller's stream: joined by events at entry and exit
   cudaEvent_t ev_in = nullptr, ev_out = nullptr;
+  cudaStream_t stream2 = nullptr;   // side branch: concurrent smoother size classes
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   int64_t* lptr = nullptr;
   int64_t* kptr = nullptr;
   int32_t* ldofs = nullptr;
@@ -639,6 +641,9 @@ struct fcm_hp {
     if (ev_in) cudaEventDestroy(ev_in);
     if (ev_out) cudaEventDestroy(ev_out);
     if (stream) cudaStreamDestroy(stream);
+    if (stream2) cudaStreamDestroy(stream2);
+    if (ev_fork) cudaEventDestroy(ev_fork);
+    if (ev_join) cudaEventDestroy(ev_join);
     for (void* q : allocs) cudaFree(q);
     if (h_pin) cudaFreeHost(h_pin);
   }
@@ -683,9 +688,19 @@ int residual(fcm_hp* h, int l, const double* b, const double* x, double* y) {
   return launch_apply(h, l, x, y, -1.0);
 }
 
+// The size classes run CONCURRENTLY: the tile-streamed large blocks on the main stream (one CTA
+// per SM, ~150 KB of rings) and the packed small blocks on a side stream, whose CTAs fill the
+// remaining threads of the same SMs (fork / join by events; parallel branches in the graph).
 int launch_smooth(fcm_hp* h, int l, const double* r, double* x, double omega) {
   HpLevel& L = h->lev[l];
-  for (const HpClass& c : L.cls) {
+  const bool fork = L.cls.size() > 1;
+  if (fork) {
+    HCU(cudaEventRecord(h->ev_fork, h->stream));
+    HCU(cudaStreamWaitEvent(h->stream2, h->ev_fork, 0));
+  }
+  for (size_t ci = 0; ci < L.cls.size(); ++ci) {
+    const HpClass& c = L.cls[ci];
+    cudaStream_t st = (fork && ci > 0) ? h->stream2 : h->stream;
     const int64_t nb = c.b1 - c.b0;
     if (nb <= 0) continue;
     const int grid = (int)std::min<int64_t>(nb, 148 * 16);
@@ -694,21 +709,25 @@ int launch_smooth(fcm_hp* h, int l, const double* r, double* x, double omega) {
       const int ntm = (mmax + 31) / 32;
       const size_t smt = (size_t)kHpTileWarps * kHpStages * 1024 * 8 + kHpTileWarps * kHpStages * 8 + 2 * 32 * ntm * 8;
       const int gt = (int)std::min<int64_t>(nb, 148);
-      k_hp_smooth_tiles<<<gt, kHpTileWarps * 32, smt, h->stream>>>(c.b0, c.b1, L.bptr, L.bdofs, L.iptr, L.inv, r, x,
-                                                                    omega, ntm);
+      k_hp_smooth_tiles<<<gt, kHpTileWarps * 32, smt, st>>>(c.b0, c.b1, L.bptr, L.bdofs, L.iptr, L.inv, r, x,
+                                                             omega, ntm);
       h->launches++;
       continue;
     }
     const size_t smem = (size_t)2 * mmax * 8;
 #define HPS(NW, C)                                                                                    \
   if (c.nt == NW && c.nch == C) {                                                                     \
-    k_hp_smooth_sym<NW, C><<<grid, NW * 32, smem, h->stream>>>(c.b0, c.b1, L.bptr, L.bdofs, L.iptr, L.inv, r, x, \
-                                                               omega, mmax);                          \
+    k_hp_smooth_sym<NW, C><<<grid, NW * 32, smem, st>>>(c.b0, c.b1, L.bptr, L.bdofs, L.iptr, L.inv, r, x,        \
+                                                        omega, mmax);                                 \
   } else
     HPS(8, 8) HPS(8, 16)
     return fail(FCM_EINVAL, "fcm_hp: no smoother kernel for class (%d warps, %d chunks)", c.nt, c.nch);
 #undef HPS
     h->launches++;
+  }
+  if (fork) {
+    HCU(cudaEventRecord(h->ev_join, h->stream2));
+    HCU(cudaStreamWaitEvent(h->stream, h->ev_join, 0));
   }
   return FCM_OK;
 }
@@ -1152,6 +1171,9 @@ extern "C" int fcm_hp_setup(const fcm_hp_disc* d, const fcm_params* prm, fcm_hp*
   HCU(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
   HCU(cudaEventCreateWithFlags(&h->ev_in, cudaEventDisableTiming));
   HCU(cudaEventCreateWithFlags(&h->ev_out, cudaEventDisableTiming));
+  HCU(cudaStreamCreateWithFlags(&h->stream2, cudaStreamNonBlocking));
+  HCU(cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming));
+  HCU(cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming));
   HRC(enter(h.get()));
   h->coarse = prm->coarse;
   h->coarse_rtol = prm->coarse_rtol;
