@@ -170,3 +170,26 @@ def test_hp_zero_rhs_and_bad_vectors(pair):
         pair.S.apply(torch.zeros(pair.S.ndofs(), dtype=torch.float32, device="cuda"))
     with pytest.raises(ValueError):
         pair.S.vcycle(torch.zeros(pair.S.ndofs() + 1, dtype=torch.float64, device="cuda"))
+
+
+def test_hp_plate_bench_size():
+    """The hp bench workload at its full size (bench.py --config hp_plate: the paper's plate at
+    h = 1/64, k = 3, p = 2, patchwise, 63k DOFs) in the launch configuration bench.py times: FCG
+    iterations +-1 and the solution (energy norm <= 1e-9, l2 <= 1e-7, R29) against the oracle."""
+    from oracle.mlhp import MlhpHierarchy, MlhpProblem
+    from paper_2010_00881_b200.fcm import HpDisc, HpSolver
+    from workloads import hp_plate
+    cfg = hp_plate(64, 3)
+    D = HpDisc(cfg)
+    S = HpSolver(D)
+    x, it, hist = S.pcg_solve(torch.from_numpy(D.load()).cuda())
+    P = MlhpProblem(cfg)
+    perm = key_perm(P, D.keys())
+    xo, ito, _ = MlhpHierarchy(P).fcg(P.b)
+    assert abs(it - ito) <= 1, (it, ito)
+    xg = np.zeros(P.ndof)
+    xg[perm] = x.cpu().numpy()
+    d = xg - xo
+    assert np.sqrt(d @ (P.A @ d) / (xo @ (P.A @ xo))) <= 1e-9
+    assert np.linalg.norm(d) / np.linalg.norm(xo) <= 1e-7
+    assert np.linalg.norm(P.b - P.A @ xg) < 2 * cfg.rtol * np.linalg.norm(P.b)
