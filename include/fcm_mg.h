@@ -431,6 +431,11 @@ int fcm_hp_vcycle(fcm_hp* h, const double* r, double* z);
  * [maxit+1] or NULL.  FCM_NOT_CONVERGED when maxit is reached.                              */
 int fcm_hp_pcg_solve(fcm_hp* h, const double* b, double* x, double rtol, int32_t maxit,
                      int32_t* iters, double* relres_hist);
+/* hp-multigrid as a stand-alone solver: x_0 = 0, x_i = x_{i-1} + V(b - A x_{i-1})
+ * until ||b - A x_i|| / ||b|| < rtol (strict) or maxit cycles; relres_hist host [maxit+1] or NULL
+ * (the contraction numbers rho_i = hist[i] / hist[i-1], Eq. contraction).                */
+int fcm_hp_mg_solve(fcm_hp* h, const double* b, double* x, double rtol, int32_t maxit,
+                    int32_t* iters, double* relres_hist);
 /* Identical-setup parity protocol for the hp smoother: level l's blocks and inverses.  Two-call:
  * with ptr/dofs/inv NULL, *n_blocks, *dof_entries (sum m_i) and *inv_entries (sum m_i^2) are set;
  * otherwise ptr [n_blocks+1], dofs [dof_entries] (level indices, ascending per block), inv

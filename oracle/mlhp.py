@@ -413,6 +413,29 @@ class MlhpHierarchy:
             x = x + w * lv.schwarz(self._res(lv, b, x))
         return x
 
+    def mg_solve(self, b, rtol=None, maxit=None):
+        """hp-multigrid as a stand-alone solver (as mg.Hierarchy.mg_solve):
+        x_i = x_{i-1} + V(b - A x_{i-1}), stop at ||r_i|| / ||b|| < rtol or maxit V-cycles."""
+        cfg = self.prob.cfg
+        rtol = cfg.rtol if rtol is None else rtol
+        maxit = cfg.maxit if maxit is None else maxit
+        A = self.levels[0].A
+        nb = np.linalg.norm(b)
+        x = np.zeros_like(b)
+        if nb == 0:
+            return x, 0, [0.0]
+        r = b.copy()
+        hist = [1.0]
+        it = 0
+        while it < maxit:
+            x = x + self.vcycle(r)
+            r = b - A @ x
+            it += 1
+            hist.append(np.linalg.norm(r) / nb)
+            if hist[-1] < rtol:
+                break
+        return x, it, hist
+
     def fcg(self, b, rtol=None, maxit=None):
         cfg = self.prob.cfg
         rtol = cfg.rtol if rtol is None else rtol

@@ -99,6 +99,7 @@ _SIGS = {
     "fcm_hp_time_smooth": (I32, [P, I32, P, P, I32, P]),
     "fcm_hp_vcycle": (I32, [P, P, P]),
     "fcm_hp_pcg_solve": (I32, [P, P, P, D, I32, P, P]),
+    "fcm_hp_mg_solve": (I32, [P, P, P, D, I32, P, P]),
     "fcm_hp_export_blocks": (I32, [P, I32, P, P, P, P, P, P]),
     "fcm_hp_stats": (I32, [P, P, P, P]),
     "fcm_last_error": (C.c_char_p, []),

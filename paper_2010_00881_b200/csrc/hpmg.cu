@@ -1347,6 +1347,53 @@ extern "C" int fcm_hp_pcg_solve(fcm_hp* h, const double* b, double* x, double rt
   return leave(h, hp_pcg_body(h, b, x, rtol, maxit, iters, hist));   // the caller's stream joins on every path
 }
 
+// stand-alone hp-multigrid: x_i = x_{i-1} + V(b - A x_{i-1}); one 8-byte D2H per cycle
+static int hp_mg_body(fcm_hp* h, const double* b, double* x, double rtol, int32_t maxit, int32_t* iters,
+                      double* hist) {
+  const int64_t n = h->ndof;
+  HpScal* s = h->s;
+  h->coarse_iters = 0;
+  h->vcycles = 0;
+  HCU(cudaMemsetAsync(x, 0, n * 8, h->stream));
+  if (iters) *iters = 0;
+  HRC(dot(h, b, b, n, &s->bb));
+  HCU(cudaMemcpyAsync(h->h_pin, &s->bb, 8, cudaMemcpyDeviceToHost, h->stream));
+  HCU(cudaStreamSynchronize(h->stream));
+  const double bb = h->h_pin[0];
+  if (hist) hist[0] = bb == 0.0 ? 0.0 : 1.0;
+  if (bb == 0.0 || maxit == 0) return FCM_OK;
+  double* r = h->w_r;
+  k_hp_copy<<<grid_for(n), kHpThreads, 0, h->stream>>>(r, b, n);
+  h->launches++;
+  int it = 0, rc = FCM_NOT_CONVERGED;
+  while (it < maxit) {
+    HRC(vcycle(h, r, h->w_z));
+    k_hp_add<<<grid_for(n), kHpThreads, 0, h->stream>>>(x, h->w_z, n);   // x += V(r)
+    h->launches++;
+    HRC(residual(h, 0, b, x, r));                                          // r = b - A x
+    HRC(dot(h, r, r, n, &s->rr));
+    HCU(cudaMemcpyAsync(h->h_pin, &s->rr, 8, cudaMemcpyDeviceToHost, h->stream));
+    HCU(cudaStreamSynchronize(h->stream));
+    ++it;
+    const double rel2 = h->h_pin[0] / bb;
+    if (hist) hist[it] = std::sqrt(rel2);
+    if (!(rel2 == rel2)) { rc = fail(FCM_EINDEF, "fcm_hp_mg_solve: NaN residual at cycle %d", it); break; }
+    if (rel2 < rtol * rtol) { rc = FCM_OK; break; }
+  }
+  if (iters) *iters = it;
+  HCU(cudaGetLastError());
+  return rc;
+}
+
+extern "C" int fcm_hp_mg_solve(fcm_hp* h, const double* b, double* x, double rtol, int32_t maxit, int32_t* iters,
+                               double* hist) {
+  clear_error();
+  if (!h || !check_vec(b) || !check_vec(x) || !(rtol > 0) || maxit < 0)
+    return fail(FCM_EINVAL, "fcm_hp_mg_solve: invalid argument");
+  HRC(enter(h));
+  return leave(h, hp_mg_body(h, b, x, rtol, maxit, iters, hist));
+}
+
 extern "C" int fcm_hp_export_blocks(const fcm_hp* h, int32_t level, int64_t* n_blocks, int64_t* dof_entries,
                                     int64_t* inv_entries, int64_t* ptr, int32_t* dofs, double* inv) {
   clear_error();

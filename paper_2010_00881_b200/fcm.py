@@ -564,6 +564,18 @@ class HpSolver:
         check(rc, allow_not_converged=True)
         return x, it.value, hist[: it.value + 1]
 
+    def mg_solve(self, b, rtol=None, maxit=None, x=None):
+        """Stand-alone hp-multigrid x_i = x_{i-1} + V(b - A x_{i-1}) (fcm_hp_mg_solve)."""
+        rtol = self.cfg.rtol if rtol is None else rtol
+        maxit = self.cfg.maxit if maxit is None else maxit
+        x = self._vec() if x is None else x
+        it = C.c_int32()
+        hist = np.zeros(maxit + 1)
+        rc = _lib.lib().fcm_hp_mg_solve(self._h, self._dv(b, 0, "b"), self._dv(x, 0, "x"), rtol, maxit,
+                                        C.byref(it), _ptr(hist))
+        check(rc, allow_not_converged=True)
+        return x, it.value, hist[: it.value + 1]
+
     def export_blocks(self, level):
         """(blocks as lists of level indices, inverses) of level `level` (identical-setup parity)."""
         nb, nd, ni = C.c_int64(), C.c_int64(), C.c_int64()

@@ -193,3 +193,19 @@ def test_hp_plate_bench_size():
     assert np.sqrt(d @ (P.A @ d) / (xo @ (P.A @ xo))) <= 1e-9
     assert np.linalg.norm(d) / np.linalg.norm(xo) <= 1e-7
     assert np.linalg.norm(P.b - P.A @ xg) < 2 * cfg.rtol * np.linalg.norm(P.b)
+
+
+def test_hp_mg_solver_matches_oracle(pair):
+    """hp-multigrid as a stand-alone solver: cycles +-1, history (contraction numbers)
+    and iterate against the oracle's MlhpHierarchy.mg_solve, to 1e-8."""
+    cfg = pair.cfg
+    x, it, hist = pair.S.mg_solve(pair.b, rtol=1e-8, maxit=200)
+    xo, ito, ho = pair.H.mg_solve(pair.P.b, rtol=1e-8, maxit=200)
+    assert abs(it - ito) <= 1, (it, ito)
+    assert (hist[-1] < 1e-8) == (ho[-1] < 1e-8)   # elementwise hp smoothing may need > 200 cycles
+    k = min(len(hist), len(ho))
+    assert np.allclose(hist[:k], ho[:k], rtol=1e-6, atol=1e-12)
+    xg = pair.to_oracle(x)
+    d = xg - xo
+    A = pair.P.A
+    assert np.sqrt(d @ (A @ d) / (xo @ (A @ xo))) <= 1e-7

@@ -219,3 +219,34 @@ def test_fully_refined_base_drops_empty_coarse_level():
     assert P.level_sequence() == [(2, 1), (1, 1)]
     x, it, hist = MlhpHierarchy(P).fcg(P.b)
     assert hist[-1] < cfg.rtol
+
+
+@pytest.mark.parametrize("block", ["element", "patch"])
+def test_k0_hp_hierarchy_equals_uniform_oracle(block):
+    """k = 0 (no refinement): the hp oracle is the uniform p-multigrid -- same DOF set, same blocks
+    (base element = cell; base-vertex patch = the closure patch, R19/R26), same V-cycle, so the
+    stand-alone MG histories and FCG iterates coincide to rounding."""
+    from oracle.mg import Hierarchy
+    from oracle.problem import Problem
+    cfg = small_config(2, 5, 3, voids=([[0.47, 0.52]], [0.26]), kmax=0, block=block, coarse="direct",
+                       dirichlet=0b0101)
+    P = MlhpProblem(cfg)
+    U = Problem(cfg)
+    assert P.ndof == U.dof.ndof
+    perm = np.zeros(P.ndof, dtype=np.int64)   # hp DOF -> uniform DOF via the entity keys
+    n = cfg.n
+    p = cfg.p
+    for i, (k, c) in enumerate(P.keys):
+        X, dg = k[1:3], k[3:5]
+        # the uniform key convention of dofmap.py (X_z = deg_z = 0 in 2D)
+        key = ((((X[1] * (2 * n + 1) + X[0]) * (p + 1) + 0) * (p + 1) + dg[1]) * (p + 1) + dg[0]) * cfg.n_f + c
+        perm[i] = np.searchsorted(U.dof.keys, key)
+        assert U.dof.keys[perm[i]] == key
+    assert len(np.unique(perm)) == P.ndof
+    Hh, Hu = MlhpHierarchy(P), Hierarchy(U)
+    _, ih, hh = Hh.mg_solve(P.b, rtol=1e-10, maxit=60)
+    _, iu, hu = Hu.mg_solve(U.b, rtol=1e-10, maxit=60)
+    assert ih == iu and np.allclose(hh, hu, rtol=1e-8, atol=1e-14)
+    xh, _, _ = Hh.fcg(P.b)
+    xu, _, _ = Hu.fcg(U.b)
+    assert np.allclose(xh, xu[perm], rtol=0, atol=1e-9 * np.abs(xu).max())
