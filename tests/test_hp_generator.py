@@ -57,3 +57,24 @@ def test_hp_generator_rejects_bad_spec():
     from workloads import small_config
     with pytest.raises(FcmError):
         HpDisc(small_config(2, 4, 2, kmax=9))
+
+
+def test_hp_abi_rejects_null_handles():
+    """The multi-level hp and low-rank entry points check their arguments before touching the
+    device (CPU-safe): NULL handles / buffers give FCM_EINVAL and a message."""
+    import ctypes as C
+    from paper_2010_00881_b200 import _lib
+    L = _lib.lib()
+    i64, i32, f = C.c_int64(), C.c_int32(), C.c_float()
+    assert L.fcm_hp_setup(None, None, None) == -1
+    assert L.fcm_hp_apply(None, 0, None, None) == -1
+    assert L.fcm_hp_smooth(None, 0, None, None) == -1
+    assert L.fcm_hp_vcycle(None, None, None) == -1
+    assert L.fcm_hp_pcg_solve(None, None, None, 1e-10, 10, C.byref(i32), None) == -1
+    assert L.fcm_hp_mg_solve(None, None, None, 1e-10, 10, C.byref(i32), None) == -1
+    assert L.fcm_hp_time_smooth(None, 0, None, None, 5, C.byref(f)) == -1
+    assert L.fcm_hp_export_blocks(None, 0, C.byref(i64), C.byref(i64), C.byref(i64), None, None, None) == -1
+    assert L.fcm_hp_stats(None, None, None, None) == -1
+    assert L.fcm_mg_lowrank_info(None, 2, C.byref(i64), C.byref(i64)) == -1
+    assert L.fcm_hp_disc_info(None, None, None, None, None, None) == -1
+    assert b"NULL" in L.fcm_last_error() or len(L.fcm_last_error()) > 0
