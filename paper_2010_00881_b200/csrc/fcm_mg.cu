@@ -136,6 +136,8 @@ struct LevelDev {
   int nt = 0;                      // 32x32 tiles per dimension of a packed inverse
   int64_t pstride = 0;             // doubles per packed inverse
   int64_t* irr_anchor = nullptr;   // [n_irr] anchor of individual block i
+  unsigned long long* sched = nullptr;   // k_patch_smooth dynamic-scheduling counters (3, zeroed)
+  bool swz = false;                      // patch inverses: off-diagonal tiles rotated (tile_pos)
   std::vector<int64_t> irr_col, reg_col;   // deterministic mode: colour ranges (27) of the sorted lists
   int32_t* reg_list = nullptr;     // regular anchors (fast diagonalisation / k_block_smooth)
   int64_t n_reg = 0;
@@ -1427,6 +1429,9 @@ static int launch_block_smooth(fcm_mg* h, int q, const double* r, double* x, dou
     for (int i = 0; i < 3; ++i) io.mo[k][i] = Lv.mo[k][i];
   io.base = Lv.base; io.stride3 = Lv.stride; io.cmin = Lv.cmin; io.cmax = Lv.cmax; io.m = Lv.m;
   io.inv = Lv.irr_inv; io.in = r; io.out = x; io.coef = coef;
+  // dynamic patch claiming needs every streaming warp to own >= kIrrStages tiles per patch (its
+  // ring runs at most one patch ahead of the claims)
+  io.sched = Lv.sched && (Lv.nt * (Lv.nt + 1) / 2) / io.wpp >= kIrrStages ? Lv.sched : nullptr;
   PatchFdOp fo{};
   fo.nx = h->L.n[0]; fo.ny = h->L.n[1]; fo.nz = h->L.n[2]; fo.dim = h->L.dim;
   for (int i = 0; i < 3; ++i) fo.na[i] = Lv.na[i];
@@ -1435,12 +1440,14 @@ static int launch_block_smooth(fcm_mg* h, int q, const double* r, double* x, dou
   fo.inv_alpha = 1.0 / h->alpha; fo.modeidx = Lv.fd_midx;
   fo.base = Lv.base; fo.stride3 = Lv.stride; fo.cmin = Lv.cmin; fo.cmax = Lv.cmax; fo.m = Lv.m;
   fo.in = r; fo.out = x; fo.coef = coef;
+  fo.sched = io.sched;
   // low-rank individual patches: by the fast-diagonalisation warps of the same launch (they finish
   // the regular patches long before the streaming warps; FCM_WB_KERNEL=1: separate k_patch_wb)
   const bool wb_fused = do_irr_wb(h, q, part) && Lv.wb_fused;
   fo.n_wb = wb_fused ? Lv.n_wb : 0;
   fo.wb_anchor = Lv.wb_anchor; fo.wb_soff = Lv.wb_soff; fo.wb_tS = Lv.wb_tS; fo.wb_coff = Lv.wb_coff; fo.wb_C = Lv.wb_C;
   io.det = h->det ? 1 : 0;
+  io.swz = Lv.swz ? 1 : 0;
   const int ncol = h->det ? 27 : 1;
   for (int k = 0; k < ncol; ++k) {
     PatchIrrOp io2 = io;
@@ -2426,7 +2433,7 @@ static size_t patch_smem(const fcm_mg* h, int q) {
   const int S = 2 * q + 1, S3 = h->L.dim == 3 ? S * S * S : S * S, nmi = (q + 1) * (q + 1) * (q + 1);
   const size_t MPd = 32 * (size_t)Lv.nt;
   size_t o = (sizeof(Tab) + (size_t)(kIrrWarps / patch_wpp(Lv.nt)) * MPd * 20 + 127) / 128 * 128;
-  o += (size_t)kIrrWarps * kIrrStages * 1024 * 8 + (size_t)kIrrWarps * kIrrStages * 8;
+  o += (size_t)kIrrWarps * kIrrStages * 1024 * 8 + (size_t)kIrrWarps * kIrrStages * 8 + (size_t)kIrrWarps * 2 * 8;
   o += (size_t)3 * (Lv.fd ? Lv.fd_ncls : 0) * (S * S + S) * 8 + ((nmi * 2 + 15) / 16) * 16;
   o += ((size_t)S3 * 4 + 15) / 16 * 16;   // FD slot codes
   o += (size_t)kFdWarps * 2 * S3 * 8;
@@ -2453,10 +2460,15 @@ static int setup_patch_blocks(fcm_mg* h, int q, const BlockGeom& g, const std::v
     }
   Lv.nt = nt;
   Lv.pstride = tile_pack_size(nt);
+  Lv.swz = !(getenv("FCM_TILE_SWZ") && atoi(getenv("FCM_TILE_SWZ")) == 0);
   RC(h->alloc(&Lv.type_inv, std::max<int64_t>(ntypes, 1) * mb * mb));
   RC(h->alloc(&Lv.irr_inv, std::max<int64_t>(n_irr, 1) * Lv.pstride));
   RC(h->alloc(&Lv.blk, blk.size()));
   RC(h->alloc(&Lv.irr_anchor, std::max<int64_t>(n_irr, 1)));
+  if (!(getenv("FCM_PATCH_DYN") && atoi(getenv("FCM_PATCH_DYN")) == 0)) {
+    RC(h->alloc(&Lv.sched, 3));
+    CU(cudaMemsetAsync(Lv.sched, 0, 3 * sizeof(unsigned long long), h->stream));
+  }
   CU(cudaMemcpyAsync(Lv.blk, blk.data(), blk.size() * 4, cudaMemcpyHostToDevice, h->stream));
   if (n_irr > 0)
     CU(cudaMemcpyAsync(Lv.irr_anchor, blocks.data() + ntypes, n_irr * 8, cudaMemcpyHostToDevice, h->stream));
@@ -2521,7 +2533,7 @@ static int setup_patch_blocks(fcm_mg* h, int q, const BlockGeom& g, const std::v
                                (size_t)MP * 8, (size_t)mb * 8, (size_t)mb, cudaMemcpyDeviceToDevice, h->stream));
     } else {
       k_pack_tiles<<<dim3(nt * (nt + 1) / 2, (unsigned)nc), 256, 0, h->stream>>>(
-          W, MP, nt, Lv.irr_inv + (size_t)(c0 - ntypes) * Lv.pstride, Lv.pstride);
+          W, MP, nt, Lv.irr_inv + (size_t)(c0 - ntypes) * Lv.pstride, Lv.pstride, Lv.swz ? 1 : 0);
       CU(cudaGetLastError());
     }
     CU(cudaMemcpyAsync(status.data(), d_status, nc * 4, cudaMemcpyDeviceToHost, h->stream));
@@ -4434,7 +4446,8 @@ extern "C" int fcm_mg_export_block_inverses(const fcm_mg* h, int32_t q, int64_t*
         for (int r = 0; r < mb; ++r)
           for (int c = 0; c <= r; ++c) {
             const int I = r / 32, J = c / 32, rr = r % 32, cc = c % 32;
-            const double v = I != J ? pk[tile_off(I, J) + rr * 32 + cc] : pk[tile_off(I, I) + rr * (rr + 1) / 2 + cc];
+            const bool swz = Lv.patch && Lv.swz;
+            const double v = I != J ? pk[tile_off(I, J) + tile_pos(rr, cc, swz)] : pk[tile_off(I, I) + rr * (rr + 1) / 2 + cc];
             inv[i * mm + (size_t)r * mb + c] = v;
             inv[i * mm + (size_t)c * mb + r] = v;
           }

@@ -88,8 +88,13 @@ __global__ void __launch_bounds__(256) k_patch_asm(PatchAsmArgs a) {
 
 #include "gj.cuh"
 
+// off-diagonal tiles of the patch inverses are stored ROTATED (swz): element (r, c) at
+// r * 32 + ((c + r) & 31), so a lane can walk its row (lane = r) or its column (lane = c) of the
+// tile without shared-memory bank conflicts (k_patch_smooth's shuffle-free tile product)
+__host__ __device__ inline int tile_pos(int r, int c, bool swz) { return r * 32 + (swz ? ((c + r) & 31) : c); }
+
 // full workspace (ld MP) -> tile-packed lower storage (symmetrised); grid (tiles, matrices)
-__global__ void k_pack_tiles(const double* W, int MP, int nt, double* out, int64_t stride) {
+__global__ void k_pack_tiles(const double* W, int MP, int nt, double* out, int64_t stride, int swz) {
   int t = blockIdx.x;
   int I = 0;
   while ((I + 1) * (I + 2) / 2 <= t) ++I;
@@ -100,7 +105,7 @@ __global__ void k_pack_tiles(const double* W, int MP, int nt, double* out, int64
     const int r = e / 32, c = e % 32;
     const int64_t gi = 32 * I + r, gj = 32 * J + c;
     const double v = 0.5 * (M[gi * MP + gj] + M[gj * MP + gi]);
-    if (I != J) o[e] = v;
+    if (I != J) o[tile_pos(r, c, swz)] = v;
     else if (c <= r) o[r * (r + 1) / 2 + c] = v;
   }
 }
@@ -112,6 +117,7 @@ struct PatchIrrOp {
   int mb, nt;                 // block slots, tiles per dim (32 nt >= mb)
   int wpp;                    // streaming warps per patch (kIrrWarps / wpp patches in flight per CTA)
   int det;                    // deterministic mode: a patch's row sums added in a fixed warp order
+  int swz;                    // off-diagonal tiles rotated (tile_pos): shuffle-free tile product
   int64_t stride;             // doubles per packed inverse
   int64_t n_irr;
   const int64_t* anchors;     // [n_irr] anchor of individual block i
@@ -127,6 +133,9 @@ struct PatchIrrOp {
   const double* in;
   double* out;
   double coef;
+  // dynamic scheduling (nullptr: static round-robin): [0] next individual patch, [1] next
+  // fast-diagonalisation item, [2] CTAs done (the last one zeroes all three for the next launch)
+  unsigned long long* sched;
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -174,7 +183,7 @@ __device__ __forceinline__ void group_sync(int id, int nthreads) {
 // doubles; bars: nw x kIrrStages mbarriers (initialised by the caller).
 __device__ __forceinline__ void irr_loop(const PatchIrrOp& op, const Tab& T, double* xs, double* ys, int* ids,
                                          double* ring, uint64_t* bars_all, int w, int nw, int bar_id,
-                                         int64_t p0, int64_t pstep, int wring) {
+                                         int64_t p0, int64_t pstep, int wring, int64_t* pid) {
   const int lane = threadIdx.x & 31;
   const int MPd = 32 * op.nt;
   double* myring = ring + (size_t)wring * kIrrStages * 1024;
@@ -184,8 +193,22 @@ __device__ __forceinline__ void irr_loop(const PatchIrrOp& op, const Tab& T, dou
   const int nt = op.nt;
   const int ntiles = nt * (nt + 1) / 2;
   const int ntw = w < ntiles ? (ntiles - w + nw - 1) / nw : 0;   // tiles of this warp per patch
-  const int64_t npatch = op.n_irr > p0 ? (op.n_irr - p0 + pstep - 1) / pstep : 0;
-  const int64_t nitems = npatch * ntw;
+  // static: patch k of this group is p0 + k pstep; dynamic (op.sched): the group leader claims
+  // patches from a global counter one patch ahead (pid[k & 1] = patch k, written at the top of
+  // patch k - 1, visible to the group after the gather barrier, before any tile of patch k is
+  // issued), so SMs that stream faster take more patches
+  const bool dyn = op.sched != nullptr;
+  const bool leader = w == 0 && lane == 0;
+  auto patch_of = [&](int64_t k) -> int64_t { return dyn ? pid[k & 1] : p0 + k * pstep; };
+  if (dyn) {
+    if (leader) {
+      pid[0] = (int64_t)atomicAdd(op.sched, 1ull);
+      pid[1] = (int64_t)atomicAdd(op.sched, 1ull);
+    }
+    group_sync(bar_id, nthr);
+  }
+  const int64_t npatch = dyn ? INT64_MAX : (op.n_irr > p0 ? (op.n_irr - p0 + pstep - 1) / pstep : 0);
+  const int64_t nitems = dyn ? INT64_MAX : npatch * ntw;
   // item i of this warp: patch k = i / ntw (block b = blockIdx.x + k gridDim.x), tile w + nw (i % ntw)
   auto tile_of = [&](int t, int& I, int& J) {
     I = (int)((sqrtf(8.0f * t + 1.0f) - 1.0f) * 0.5f);
@@ -198,7 +221,8 @@ __device__ __forceinline__ void irr_loop(const PatchIrrOp& op, const Tab& T, dou
     const int t = w + nw * (int)(i % ntw);
     int I, J;
     tile_of(t, I, J);
-    const int64_t b = p0 + k * pstep;
+    const int64_t b = patch_of(k);
+    if (b >= op.n_irr) return;
     const double* src = op.inv + b * op.stride + tile_off(I, J);
     const uint32_t bytes = (I == J ? kTileDiag : 1024) * 8;
     const int s = (int)(i % kIrrStages);
@@ -209,7 +233,9 @@ __device__ __forceinline__ void irr_loop(const PatchIrrOp& op, const Tab& T, dou
     for (int64_t i = 0; i < kIrrStages && i < nitems; ++i) issue(i);
   int64_t item = 0;
   for (int64_t k = 0; k < npatch; ++k) {
-    const int64_t b = p0 + k * pstep;
+    const int64_t b = patch_of(k);
+    if (b >= op.n_irr) break;   // dynamic: counter exhausted (same smem value for the whole group)
+    if (dyn && k >= 1 && leader) pid[(k + 1) & 1] = (int64_t)atomicAdd(op.sched, 1ull);
     const int64_t A = op.anchors[b];
     const int ax = (int)(A % op.na[0]), ay = (int)((A / op.na[0]) % op.na[1]), az = (int)(A / ((int64_t)op.na[0] * op.na[1]));
     for (int l = tid; l < MPd; l += nthr) {
@@ -239,30 +265,54 @@ __device__ __forceinline__ void irr_loop(const PatchIrrOp& op, const Tab& T, dou
       const int s = (int)(item % kIrrStages);
       mbar_wait(&bars[s], (uint32_t)((item / kIrrStages) & 1));
       const double* tl = myring + s * 1024;
-      const double xJ = xs[32 * J + lane];
-      double yJ = 0.0;
-      double p[32];
-      if (I != J) {
+      double yJ = 0.0, yI;
+      if (I != J && op.swz) {
+        // rotated tile: lane l walks column l (y_J += T^T x_I) and row l (y_I += T x_J) together,
+        // both conflict-free, no cross-lane reduction; x pairs as warp-uniform 16-byte broadcasts
+        const double2* xI2 = reinterpret_cast<const double2*>(xs + 32 * I);
+        const double2* xJ2 = reinterpret_cast<const double2*>(xs + 32 * J);
+        double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;
 #pragma unroll
-        for (int r = 0; r < 32; ++r) {
-          const double a = tl[r * 32 + lane];
-          p[r] = a * xJ;
-          yJ = fma(a, xs[32 * I + r], yJ);
+        for (int r = 0; r < 32; r += 2) {
+          const double2 xi = xI2[r >> 1], xj = xJ2[r >> 1];
+          const int c0 = (lane + r) & 31, c1 = (lane + r + 1) & 31;
+          a0 = fma(tl[r * 32 + c0], xi.x, a0);
+          b0 = fma(tl[lane * 32 + c0], xj.x, b0);
+          a1 = fma(tl[(r + 1) * 32 + c1], xi.y, a1);
+          b1 = fma(tl[lane * 32 + c1], xj.y, b1);
+        }
+        yJ = a0 + a1;
+        yI = b0 + b1;
+        __syncwarp();
+        if (lane == 0 && item + kIrrStages < nitems) {
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          issue(item + kIrrStages);
         }
       } else {
+        const double xJ = xs[32 * J + lane];
+        double p[32];
+        if (I != J) {
 #pragma unroll
-        for (int r = 0; r < 32; ++r) {
-          const double a = lane <= r ? tl[r * (r + 1) / 2 + lane] : 0.0;
-          p[r] = a * xJ;
-          if (lane < r) yJ = fma(a, xs[32 * I + r], yJ);
+          for (int r = 0; r < 32; ++r) {
+            const double a = tl[r * 32 + lane];
+            p[r] = a * xJ;
+            yJ = fma(a, xs[32 * I + r], yJ);
+          }
+        } else {
+#pragma unroll
+          for (int r = 0; r < 32; ++r) {
+            const double a = lane <= r ? tl[r * (r + 1) / 2 + lane] : 0.0;
+            p[r] = a * xJ;
+            if (lane < r) yJ = fma(a, xs[32 * I + r], yJ);
+          }
         }
+        __syncwarp();
+        if (lane == 0 && item + kIrrStages < nitems) {
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          issue(item + kIrrStages);
+        }
+        yI = warp_reduce_scatter32(p);
       }
-      __syncwarp();
-      if (lane == 0 && item + kIrrStages < nitems) {
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        issue(item + kIrrStages);
-      }
-      const double yI = warp_reduce_scatter32(p);
       ++item;
       if (!op.det) {
         atomicAdd(&ys[32 * I + lane], yI);
@@ -315,7 +365,10 @@ struct PatchFdOp {
   const double* in;
   double* out;
   double coef;
+  unsigned long long* sched;  // dynamic scheduling: [1] next item (claimed kFdChunk at a time)
 };
+
+constexpr int kFdChunk = 4;       // fast-diagonalisation items per dynamic claim
 
 // slot s (0..2q) of an axis at vertex v: cell offset and 1D mode (vertex slots pick a cell in
 // the grid: v-1 | internals of cell v-1 | v | internals of cell v | v+1)
@@ -403,7 +456,17 @@ __device__ __forceinline__ void fd_loop(const PatchFdOp& op, const Tab& T, const
   double* Y = X + N3;
   const double coef = op.coef;
   const int64_t ntot = op.nreg + op.n_wb;
-  for (int64_t i = (int64_t)blockIdx.x * nw + w; i < ntot; i += (int64_t)gridDim.x * nw) {
+  // static: item blockIdx.x nw + w + k gridDim.x nw; dynamic: chunks of kFdChunk consecutive
+  // items (neighbouring anchors share gather lines) claimed from a global counter
+  const bool dyn = op.sched != nullptr;
+  auto claim = [&]() -> int64_t {
+    unsigned long long v = 0;
+    if (lane == 0) v = atomicAdd(op.sched + 1, (unsigned long long)kFdChunk);
+    return (int64_t)__shfl_sync(0xffffffffu, v, 0);
+  };
+  for (int64_t c0 = dyn ? claim() : (int64_t)blockIdx.x * nw + w; c0 < ntot;
+       c0 = dyn ? claim() : c0 + (int64_t)gridDim.x * nw)
+  for (int64_t i = c0, c1 = dyn ? min(c0 + kFdChunk, ntot) : c0 + 1; i < c1; ++i) {
     const bool lowrank = i >= op.nreg;
     const int64_t pw = i - op.nreg;
     const int A = lowrank ? (int)op.wb_anchor[pw] : op.anchors[i];
@@ -538,7 +601,8 @@ __global__ void __launch_bounds__((kIrrWarps + kFdWarps) * 32, 1) k_patch_smooth
   double* ring = reinterpret_cast<double*>(smem + o_ring);
   uint64_t* bars = reinterpret_cast<uint64_t*>(ring + (size_t)kIrrWarps * kIrrStages * 1024);
   constexpr int tsz = S * S + S;
-  double* tab = reinterpret_cast<double*>(bars + kIrrWarps * kIrrStages);
+  int64_t* pids = reinterpret_cast<int64_t*>(bars + kIrrWarps * kIrrStages);   // 2 per group
+  double* tab = reinterpret_cast<double*>(pids + 2 * kIrrWarps);
   int16_t* midx = reinterpret_cast<int16_t*>(tab + 3 * fo.ncls * tsz);
   const int nmi = (fo.q + 1) * (fo.q + 1) * (fo.q + 1);
   constexpr int N3 = DIM == 3 ? S * S * S : S * S;
@@ -564,10 +628,21 @@ __global__ void __launch_bounds__((kIrrWarps + kFdWarps) * 32, 1) k_patch_smooth
       double* ys = xs + MPd;
       int* ids = reinterpret_cast<int*>(xs0 + (size_t)ngrp * MPd * 2) + (size_t)g * MPd;
       irr_loop(io, T, xs, ys, ids, ring, bars, w % io.wpp, io.wpp, 1 + g, (int64_t)blockIdx.x * ngrp + g,
-               (int64_t)gridDim.x * ngrp, w);
+               (int64_t)gridDim.x * ngrp, w, pids + 2 * g);
     }
   } else {
     if (FD) fd_loop<S, DIM>(fo, T, tab, midx, scode, wbase, w - kIrrWarps, kFdWarps);
+  }
+  if (io.sched) {   // the last CTA out re-arms the counters (every claim of this launch is done)
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      if (atomicAdd(io.sched + 2, 1ull) == gridDim.x - 1) {
+        atomicExch(io.sched + 0, 0ull);
+        atomicExch(io.sched + 1, 0ull);
+        atomicExch(io.sched + 2, 0ull);
+      }
+    }
   }
 }
 

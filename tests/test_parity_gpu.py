@@ -595,3 +595,33 @@ def test_lowrank_patches_match_explicit(case, wb_kernel, monkeypatch, tol_log):
         assert d <= 1e-11, (q, d, n_lr)
     if case == "3d_p4_patch729":
         assert sum(n_lr) > 0, "the case exercises low-rank patches"
+
+
+@pytest.mark.parametrize("env", ["FCM_PATCH_DYN", "FCM_TILE_SWZ"])
+@pytest.mark.parametrize("case", ["3d_p2_patch", "3d_p3_patch", "3d_p4_patch729", "2d_p3_patch"])
+def test_patch_schedule_and_tile_layout_variants(case, env, monkeypatch, tol_log):
+    """k_patch_smooth defaults against its switched-off variants: patches / fast-diagonalisation
+    items claimed from global counters vs round-robin (FCM_PATCH_DYN=0), and rotated off-diagonal
+    tiles read shuffle-free vs row-major tiles with the reduce-scatter (FCM_TILE_SWZ=0).  The
+    same Schwarz sum in another rounding / atomic order.  Repeated sweeps check that the last CTA
+    re-arms the counters for the next launch (a stale counter would skip every patch)."""
+    cfg = CASES[case]()
+    dy = Pair(cfg)
+    monkeypatch.setenv(env, "0")
+    st = Pair(cfg)
+    monkeypatch.delenv(env)
+    rng = np.random.default_rng(37)
+    for q in range(2, cfg.p + 1):
+        n = dy.S.ndofs(q)
+        r = torch.from_numpy(rng.standard_normal(n)).cuda()
+        b = st.S.smooth(r, torch.zeros(n, dtype=torch.float64, device="cuda"), q).cpu().numpy()
+        for rep in range(3):
+            a = dy.S.smooth(r, torch.zeros(n, dtype=torch.float64, device="cuda"), q).cpu().numpy()
+            d = np.linalg.norm(a - b) / np.linalg.norm(b)
+            tol_log(dy, f"default_vs_{env}=0_smoother_q{q}_rep{rep}", q, d, 1e-12)
+            assert d <= 1e-12, (q, rep, d)
+    bb = torch.from_numpy(rng.standard_normal(dy.S.ndofs(cfg.p))).cuda()
+    x1, it1, _ = dy.S.pcg_solve(bb)
+    x0, it0, _ = st.S.pcg_solve(bb)
+    assert abs(it1 - it0) <= 1
+    assert (torch.linalg.norm(x1 - x0) / torch.linalg.norm(x0)).item() <= 1e-8
