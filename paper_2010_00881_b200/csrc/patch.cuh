@@ -118,6 +118,7 @@ struct PatchIrrOp {
   int wpp;                    // streaming warps per patch (kIrrWarps / wpp patches in flight per CTA)
   int det;                    // deterministic mode: a patch's row sums added in a fixed warp order
   int swz;                    // off-diagonal tiles rotated (tile_pos): shuffle-free tile product
+  int l2ef;                   // stream the inverses with an L2 evict_first policy
   int64_t stride;             // doubles per packed inverse
   int64_t n_irr;
   const int64_t* anchors;     // [n_irr] anchor of individual block i
@@ -150,6 +151,17 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
                ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+// the same copy with an L2 eviction policy (evict_first for data read once per sweep, so the
+// streamed inverses do not push the gathered / scattered vectors out of L2)
+__device__ __forceinline__ void bulk_g2s_hint(void* dst, const void* src, uint32_t bytes, uint64_t* bar, uint64_t pol) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
+               ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol) : "memory");
+}
+__device__ __forceinline__ uint64_t l2_evict_first_policy() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(
@@ -216,6 +228,7 @@ __device__ __forceinline__ void irr_loop(const PatchIrrOp& op, const Tab& T, dou
     while ((I + 1) * (I + 2) / 2 <= t) ++I;
     J = t - I * (I + 1) / 2;
   };
+  const uint64_t pol = l2_evict_first_policy();
   auto issue = [&](int64_t i) {
     const int64_t k = i / ntw;
     const int t = w + nw * (int)(i % ntw);
@@ -227,7 +240,8 @@ __device__ __forceinline__ void irr_loop(const PatchIrrOp& op, const Tab& T, dou
     const uint32_t bytes = (I == J ? kTileDiag : 1024) * 8;
     const int s = (int)(i % kIrrStages);
     mbar_expect_tx(&bars[s], bytes);
-    bulk_g2s(myring + s * 1024, src, bytes, &bars[s]);
+    if (op.l2ef) bulk_g2s_hint(myring + s * 1024, src, bytes, &bars[s], pol);
+    else bulk_g2s(myring + s * 1024, src, bytes, &bars[s]);
   };
   if (lane == 0)
     for (int64_t i = 0; i < kIrrStages && i < nitems; ++i) issue(i);
