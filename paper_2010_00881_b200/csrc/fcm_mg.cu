@@ -2434,7 +2434,7 @@ static size_t patch_smem(const fcm_mg* h, int q) {
   const LevelDev& Lv = h->lev[q];
   const int S = 2 * q + 1, S3 = h->L.dim == 3 ? S * S * S : S * S, nmi = (q + 1) * (q + 1) * (q + 1);
   const size_t MPd = 32 * (size_t)Lv.nt;
-  size_t o = (sizeof(Tab) + (size_t)(kIrrWarps / patch_wpp(Lv.nt)) * MPd * 20 + 127) / 128 * 128;
+  size_t o = (sizeof(Tab) + (size_t)(kIrrWarps / patch_wpp(Lv.nt)) * MPd * 20 + 255) / 256 * 256 + 256;
   o += (size_t)kIrrWarps * kIrrStages * 1024 * 8 + (size_t)kIrrWarps * kIrrStages * 8 + (size_t)kIrrWarps * 2 * 8;
   o += (size_t)3 * (Lv.fd ? Lv.fd_ncls : 0) * (S * S + S) * 8 + ((nmi * 2 + 15) / 16) * 16;
   o += ((size_t)S3 * 4 + 15) / 16 * 16;   // FD slot codes

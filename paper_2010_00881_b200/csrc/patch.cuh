@@ -88,10 +88,11 @@ __global__ void __launch_bounds__(256) k_patch_asm(PatchAsmArgs a) {
 
 #include "gj.cuh"
 
-// off-diagonal tiles of the patch inverses are stored ROTATED (swz): element (r, c) at
-// r * 32 + ((c + r) & 31), so a lane can walk its row (lane = r) or its column (lane = c) of the
-// tile without shared-memory bank conflicts (k_patch_smooth's shuffle-free tile product)
-__host__ __device__ inline int tile_pos(int r, int c, bool swz) { return r * 32 + (swz ? ((c + r) & 31) : c); }
+// off-diagonal tiles of the patch inverses are stored SWIZZLED (swz): element (r, c) at
+// r * 32 + (c ^ r), so a lane can walk its row (lane = r) or its column (lane = c) of the tile
+// without shared-memory bank conflicts (k_patch_smooth's shuffle-free tile product), and both
+// walks address the element by one LOP3 (see SwzTile)
+__host__ __device__ inline int tile_pos(int r, int c, bool swz) { return r * 32 + (swz ? (c ^ r) : c); }
 
 // full workspace (ld MP) -> tile-packed lower storage (symmetrised); grid (tiles, matrices)
 __global__ void k_pack_tiles(const double* W, int MP, int nt, double* out, int64_t stride, int swz) {
@@ -190,6 +191,34 @@ __device__ __forceinline__ void group_sync(int id, int nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
 
+// One swizzled off-diagonal tile, lane l: y_J[l] += sum_r T[r][l] x_I[r] (column walk) and
+// y_I[l] += sum_r T[l][r] x_J[r] (row walk).  T[r][l] sits at byte (tb | (8 l ^ 8 r)) + 256 r
+// (the 256 r as the load's immediate) and T[l][r] at (rb | (8 l ^ 8 r)) with rb = tb + 256 l
+// (tb 256-aligned, so OR = ADD below bit 8): each element costs one LOP3 and one LDS.64.  R steps in pairs
+// (16-byte x broadcasts), four independent FMA chains.
+template <int R>
+struct SwzTile {
+  static __device__ __forceinline__ void run(uint32_t tb, uint32_t rb, uint32_t lb, const double2* xI2,
+                                             const double2* xJ2, double& a0, double& a1, double& b0, double& b1) {
+    double c0, c1, r0, r1;
+    asm volatile("ld.shared.f64 %0, [%1+%2];" : "=d"(c0) : "r"(tb | (lb ^ (8u * R))), "n"(256 * R));
+    asm volatile("ld.shared.f64 %0, [%1];" : "=d"(r0) : "r"(rb | (lb ^ (8u * R))));
+    asm volatile("ld.shared.f64 %0, [%1+%2];" : "=d"(c1) : "r"(tb | (lb ^ (8u * (R + 1)))), "n"(256 * (R + 1)));
+    asm volatile("ld.shared.f64 %0, [%1];" : "=d"(r1) : "r"(rb | (lb ^ (8u * (R + 1)))));
+    const double2 xi = xI2[R >> 1], xj = xJ2[R >> 1];
+    a0 = fma(c0, xi.x, a0);
+    b0 = fma(r0, xj.x, b0);
+    a1 = fma(c1, xi.y, a1);
+    b1 = fma(r1, xj.y, b1);
+    SwzTile<R + 2>::run(tb, rb, lb, xI2, xJ2, a0, a1, b0, b1);
+  }
+};
+template <>
+struct SwzTile<32> {
+  static __device__ __forceinline__ void run(uint32_t, uint32_t, uint32_t, const double2*, const double2*, double&,
+                                             double&, double&, double&) {}
+};
+
 // Individual patches, streamed: nw warps (index w) of the CTA, synchronised among themselves
 // with named barrier bar_id.  xs/ys/ids: 32 nt slots each; ring: nw x kIrrStages x 1024
 // doubles; bars: nw x kIrrStages mbarriers (initialised by the caller).
@@ -220,32 +249,43 @@ __device__ __forceinline__ void irr_loop(const PatchIrrOp& op, const Tab& T, dou
     group_sync(bar_id, nthr);
   }
   const int64_t npatch = dyn ? INT64_MAX : (op.n_irr > p0 ? (op.n_irr - p0 + pstep - 1) / pstep : 0);
-  const int64_t nitems = dyn ? INT64_MAX : npatch * ntw;
-  // item i of this warp: patch k = i / ntw (block b = blockIdx.x + k gridDim.x), tile w + nw (i % ntw)
-  auto tile_of = [&](int t, int& I, int& J) {
-    I = (int)((sqrtf(8.0f * t + 1.0f) - 1.0f) * 0.5f);
-    while (I * (I + 1) / 2 > t) --I;
-    while ((I + 1) * (I + 2) / 2 <= t) ++I;
-    J = t - I * (I + 1) / 2;
+  // tile t = w + nw j of a patch (lower tiles row-major): (I0, J0) for j = 0, then J += nw with
+  // the row carried (no division / square root per tile)
+  int I0 = 0, J0 = w;
+  while (J0 > I0) { J0 -= I0 + 1; ++I0; }
+  auto next_tile = [&](int& I, int& J) {
+    J += nw;
+    while (J > I) { J -= I + 1; ++I; }
   };
+  // the ring's producer (lane 0) walks the items (patch k, step j, tile (I, J)) of this warp in
+  // order, kIrrStages ahead of the consumer; beyond the last patch it issues nothing
   const uint64_t pol = l2_evict_first_policy();
-  auto issue = [&](int64_t i) {
-    const int64_t k = i / ntw;
-    const int t = w + nw * (int)(i % ntw);
-    int I, J;
-    tile_of(t, I, J);
-    const int64_t b = patch_of(k);
-    if (b >= op.n_irr) return;
-    const double* src = op.inv + b * op.stride + tile_off(I, J);
-    const uint32_t bytes = (I == J ? kTileDiag : 1024) * 8;
-    const int s = (int)(i % kIrrStages);
-    mbar_expect_tx(&bars[s], bytes);
-    if (op.l2ef) bulk_g2s_hint(myring + s * 1024, src, bytes, &bars[s], pol);
-    else bulk_g2s(myring + s * 1024, src, bytes, &bars[s]);
+  int64_t is_k = 0;
+  uint32_t is_i = 0;
+  int is_j = 0, is_I = I0, is_J = J0;
+  auto issue_next = [&]() {
+    const int64_t b = patch_of(is_k);
+    if (b < op.n_irr) {
+      const double* src = op.inv + b * op.stride + tile_off(is_I, is_J);
+      const uint32_t bytes = (is_I == is_J ? kTileDiag : 1024) * 8;
+      const int s = (int)(is_i % kIrrStages);
+      mbar_expect_tx(&bars[s], bytes);
+      if (op.l2ef) bulk_g2s_hint(myring + s * 1024, src, bytes, &bars[s], pol);
+      else bulk_g2s(myring + s * 1024, src, bytes, &bars[s]);
+    }
+    ++is_i;
+    if (++is_j == ntw) {
+      is_j = 0;
+      ++is_k;
+      is_I = I0;
+      is_J = J0;
+    } else {
+      next_tile(is_I, is_J);
+    }
   };
-  if (lane == 0)
-    for (int64_t i = 0; i < kIrrStages && i < nitems; ++i) issue(i);
-  int64_t item = 0;
+  if (lane == 0 && ntw > 0)
+    for (int i = 0; i < kIrrStages; ++i) issue_next();
+  uint32_t item = 0;
   for (int64_t k = 0; k < npatch; ++k) {
     const int64_t b = patch_of(k);
     if (b >= op.n_irr) break;   // dynamic: counter exhausted (same smem value for the whole group)
@@ -268,39 +308,30 @@ __device__ __forceinline__ void irr_loop(const PatchIrrOp& op, const Tab& T, dou
     // deterministic mode: every warp runs the same number of tile steps; after each step the
     // warps add their row sums to ys one after the other (named barrier between)
     const int nsteps = op.det ? (ntiles + nw - 1) / nw : ntw;
+    int I = I0, J = J0;
     for (int j = 0; j < nsteps; ++j) {
       if (j >= ntw) {   // det only: no tile left for this warp, keep the barrier count
         for (int k = 0; k < nw; ++k) group_sync(bar_id, nthr);
         continue;
       }
-      const int t = w + nw * j;
-      int I, J;
-      tile_of(t, I, J);
+      if (j > 0) next_tile(I, J);
       const int s = (int)(item % kIrrStages);
-      mbar_wait(&bars[s], (uint32_t)((item / kIrrStages) & 1));
+      mbar_wait(&bars[s], (item / kIrrStages) & 1);
       const double* tl = myring + s * 1024;
       double yJ = 0.0, yI;
       if (I != J && op.swz) {
-        // rotated tile: lane l walks column l (y_J += T^T x_I) and row l (y_I += T x_J) together,
+        // swizzled tile: lane l walks column l (y_J += T^T x_I) and row l (y_I += T x_J) together,
         // both conflict-free, no cross-lane reduction; x pairs as warp-uniform 16-byte broadcasts
-        const double2* xI2 = reinterpret_cast<const double2*>(xs + 32 * I);
-        const double2* xJ2 = reinterpret_cast<const double2*>(xs + 32 * J);
+        const uint32_t tb = smem_u32(tl), lb = 8u * lane;
         double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;
-#pragma unroll
-        for (int r = 0; r < 32; r += 2) {
-          const double2 xi = xI2[r >> 1], xj = xJ2[r >> 1];
-          const int c0 = (lane + r) & 31, c1 = (lane + r + 1) & 31;
-          a0 = fma(tl[r * 32 + c0], xi.x, a0);
-          b0 = fma(tl[lane * 32 + c0], xj.x, b0);
-          a1 = fma(tl[(r + 1) * 32 + c1], xi.y, a1);
-          b1 = fma(tl[lane * 32 + c1], xj.y, b1);
-        }
+        SwzTile<0>::run(tb, tb + 256u * lane, lb, reinterpret_cast<const double2*>(xs + 32 * I),
+                        reinterpret_cast<const double2*>(xs + 32 * J), a0, a1, b0, b1);
         yJ = a0 + a1;
         yI = b0 + b1;
         __syncwarp();
-        if (lane == 0 && item + kIrrStages < nitems) {
+        if (lane == 0) {
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-          issue(item + kIrrStages);
+          issue_next();
         }
       } else {
         const double xJ = xs[32 * J + lane];
@@ -321,9 +352,9 @@ __device__ __forceinline__ void irr_loop(const PatchIrrOp& op, const Tab& T, dou
           }
         }
         __syncwarp();
-        if (lane == 0 && item + kIrrStages < nitems) {
+        if (lane == 0) {
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-          issue(item + kIrrStages);
+          issue_next();
         }
         yI = warp_reduce_scatter32(p);
       }
@@ -611,7 +642,10 @@ __global__ void __launch_bounds__((kIrrWarps + kFdWarps) * 32, 1) k_patch_smooth
   const int MPd = 32 * io.nt;
   const int ngrp = kIrrWarps / io.wpp;   // patches in flight per CTA
   double* xs0 = reinterpret_cast<double*>(smem + sizeof(Tab));
-  const size_t o_ring = (sizeof(Tab) + (size_t)ngrp * MPd * 20 + 127) / 128 * 128;
+  // the ring starts 256-aligned in the shared window (SwzTile's OR addressing): the dynamic
+  // segment is at least 16-aligned, so pad by up to 240 bytes (patch_smem reserves them)
+  const uint32_t s0 = smem_u32(smem);
+  const size_t o_ring = ((s0 + sizeof(Tab) + (size_t)ngrp * MPd * 20 + 255) / 256 * 256) - s0;
   double* ring = reinterpret_cast<double*>(smem + o_ring);
   uint64_t* bars = reinterpret_cast<uint64_t*>(ring + (size_t)kIrrWarps * kIrrStages * 1024);
   constexpr int tsz = S * S + S;
