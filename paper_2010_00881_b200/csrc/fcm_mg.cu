@@ -243,6 +243,7 @@ struct fcm_mg {
   // launch, per-patch sums in a fixed warp order, energies by block-order dots, block-order
   // coarse sums: bit-identical results run to run (debugging; several times slower)
   bool det = false;
+  int wmap = 0;        // k_patch_smooth warp-role map (FCM_PATCH_WMAP, patch.cuh patch_role)
   bool l2ef = true;    // stream read-once matrices with an L2 evict_first policy (FCM_L2_EVICT_FIRST=0: off)
   int pdl = 1;                      // programmatic dependent launch of k_cell_mma (FCM_PDL)
   int ext_lo = 0, ext_n = 0;        // ghost-extended cell layers along the slab axis (relative)
@@ -1450,6 +1451,7 @@ static int launch_block_smooth(fcm_mg* h, int q, const double* r, double* x, dou
   io.det = h->det ? 1 : 0;
   io.swz = Lv.swz ? 1 : 0;
   io.l2ef = h->l2ef ? 1 : 0;
+  io.wmap = h->wmap;
   const int ncol = h->det ? 27 : 1;
   for (int k = 0; k < ncol; ++k) {
     PatchIrrOp io2 = io;
@@ -3488,6 +3490,7 @@ static int setup_impl(const fcm_grid* g, const fcm_params* prm, const fcm_slab* 
   CU(cudaGetDevice(&h->dev));
   CU(cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, h->dev));
   h->det = getenv("FCM_DETERMINISTIC") && atoi(getenv("FCM_DETERMINISTIC")) > 0;
+  h->wmap = getenv("FCM_PATCH_WMAP") ? atoi(getenv("FCM_PATCH_WMAP")) : 0;
   h->l2ef = !(getenv("FCM_L2_EVICT_FIRST") && atoi(getenv("FCM_L2_EVICT_FIRST")) == 0);
   if (h->det && h->multi) return fail(FCM_EINVAL, "deterministic mode is single-GPU");
   h->ws_ctas = h->num_sms;
