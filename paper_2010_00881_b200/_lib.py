@@ -7,8 +7,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-# FCM_LIB_PATH: a variant build of the same sources (tools/ A/B runs only)
-LIB_PATH = os.environ.get("FCM_LIB_PATH") or os.path.join(HERE, "libfcm_mg.so")
+LIB_PATH = os.path.join(HERE, "libfcm_mg.so")
 
 FCM_OK = 0
 FCM_NOT_CONVERGED = 1

@@ -243,7 +243,7 @@ struct fcm_mg {
   // launch, per-patch sums in a fixed warp order, energies by block-order dots, block-order
   // coarse sums: bit-identical results run to run (debugging; several times slower)
   bool det = false;
-  int wmap = 0;        // k_patch_smooth warp-role map (FCM_PATCH_WMAP, patch.cuh patch_role)
+  unsigned long long* patch_prof = nullptr;   // FCM_PATCH_PROF=1: k_patch_smooth population end times
   bool l2ef = true;    // stream read-once matrices with an L2 evict_first policy (FCM_L2_EVICT_FIRST=0: off)
   int pdl = 1;                      // programmatic dependent launch of k_cell_mma (FCM_PDL)
   int ext_lo = 0, ext_n = 0;        // ghost-extended cell layers along the slab axis (relative)
@@ -1451,7 +1451,6 @@ static int launch_block_smooth(fcm_mg* h, int q, const double* r, double* x, dou
   io.det = h->det ? 1 : 0;
   io.swz = Lv.swz ? 1 : 0;
   io.l2ef = h->l2ef ? 1 : 0;
-  io.wmap = h->wmap;
   const int ncol = h->det ? 27 : 1;
   for (int k = 0; k < ncol; ++k) {
     PatchIrrOp io2 = io;
@@ -1469,8 +1468,30 @@ static int launch_block_smooth(fcm_mg* h, int q, const double* r, double* x, dou
     if (!di && !df) continue;
     const void* kf = patch_kernel(2 * q + 1, h->L.dim, di, df);
     void* args[] = {&io2, &fo2};
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(h->stream, &cap);
+    const bool prof = h->patch_prof && cap == cudaStreamCaptureStatusNone;
+    if (prof) {
+      CU(cudaMemsetAsync(h->patch_prof, 0, (size_t)h->num_sms * 32, h->stream));
+      io2.prof = h->patch_prof;
+    }
     CU(cudaLaunchKernel(kf, dim3(h->num_sms), dim3((kIrrWarps + kFdWarps) * 32), args, patch_smem(h, q), h->stream));
     h->count();
+    if (prof) {   // diagnostic: when did the two warp populations finish (ms after the first CTA started)
+      std::vector<unsigned long long> t((size_t)h->num_sms * 4);
+      CU(cudaMemcpyAsync(t.data(), h->patch_prof, t.size() * 8, cudaMemcpyDeviceToHost, h->stream));
+      CU(cudaStreamSynchronize(h->stream));
+      unsigned long long t0 = ~0ull;
+      for (int b = 0; b < h->num_sms; ++b) t0 = std::min(t0, t[4 * b]);
+      double s[2][3] = {{1e30, 0, 0}, {1e30, 0, 0}};
+      for (int b = 0; b < h->num_sms; ++b)
+        for (int j = 0; j < 2; ++j) {
+          const double ms = t[4 * b + 1 + j] ? (double)(t[4 * b + 1 + j] - t0) * 1e-6 : 0.0;
+          s[j][0] = std::min(s[j][0], ms); s[j][1] += ms / h->num_sms; s[j][2] = std::max(s[j][2], ms);
+        }
+      fprintf(stderr, "[patch_prof] q=%d part=%d n_irr=%lld nreg=%lld n_wb=%lld: streaming done min/mean/max %.3f %.3f %.3f ms, FD done %.3f %.3f %.3f ms\n",
+              q, part, (long long)io2.n_irr, (long long)fo2.nreg, (long long)fo2.n_wb, s[0][0], s[0][1], s[0][2], s[1][0], s[1][1], s[1][2]);
+    }
   }
   if (do_irr_wb(h, q, part) && !Lv.wb_fused) {   // low-rank individual patches, separate launch
     PatchWbOp wo{};
@@ -3490,7 +3511,7 @@ static int setup_impl(const fcm_grid* g, const fcm_params* prm, const fcm_slab* 
   CU(cudaGetDevice(&h->dev));
   CU(cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, h->dev));
   h->det = getenv("FCM_DETERMINISTIC") && atoi(getenv("FCM_DETERMINISTIC")) > 0;
-  h->wmap = getenv("FCM_PATCH_WMAP") ? atoi(getenv("FCM_PATCH_WMAP")) : 0;
+  if (getenv("FCM_PATCH_PROF") && atoi(getenv("FCM_PATCH_PROF"))) RC(h->alloc(&h->patch_prof, (int64_t)h->num_sms * 4));
   h->l2ef = !(getenv("FCM_L2_EVICT_FIRST") && atoi(getenv("FCM_L2_EVICT_FIRST")) == 0);
   if (h->det && h->multi) return fail(FCM_EINVAL, "deterministic mode is single-GPU");
   h->ws_ctas = h->num_sms;

@@ -120,7 +120,6 @@ struct PatchIrrOp {
   int det;                    // deterministic mode: a patch's row sums added in a fixed warp order
   int swz;                    // off-diagonal tiles rotated (tile_pos): shuffle-free tile product
   int l2ef;                   // stream the inverses with an L2 evict_first policy
-  int wmap;                   // warp-role map (patch_role)
   int64_t stride;             // doubles per packed inverse
   int64_t n_irr;
   const int64_t* anchors;     // [n_irr] anchor of individual block i
@@ -139,6 +138,9 @@ struct PatchIrrOp {
   // dynamic scheduling (nullptr: static round-robin): [0] next individual patch, [1] next
   // fast-diagonalisation item, [2] CTAs done (the last one zeroes all three for the next launch)
   unsigned long long* sched;
+  // diagnostic (FCM_PATCH_PROF=1, else nullptr): per CTA [0] start, [1] last streaming warp done,
+  // [2] last fast-diagonalisation warp done (globaltimer ns)
+  unsigned long long* prof;
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -583,45 +585,6 @@ __device__ __forceinline__ void fd_loop(const PatchFdOp& op, const Tab& T, const
       }
       __syncwarp();
     };
-#ifdef FCM_FD_ONECOPY
-    // ONE copy of the six contractions in the code (a low-rank patch runs it twice: the warp's
-    // instruction footprint per item stays ~20 KB instead of ~40 KB)
-    double zr[NL];
-#pragma unroll 1
-    for (int rep = 0; rep < (lowrank ? 2 : 1); ++rep) {
-      fd_apply();   // rep 0: X = A0^{-1} r; rep 1: X = A0^{-1} P_S w
-      if (!lowrank) {
-#pragma unroll
-        for (int j = 0; j < NL; ++j)
-          if (ids[j] >= 0) atomicAdd(op.out + ids[j], coef * X[lane + 32 * j]);
-      } else if (rep == 0) {
-#pragma unroll
-        for (int j = 0; j < NL; ++j) zr[j] = lane + 32 * j < N3 ? X[lane + 32 * j] : 0.0;
-        for (int l = lane; l < N3; l += 32) Y[l] = 0.0;
-        __syncwarp();
-        const int64_t s0 = op.wb_soff[pw];
-        const int k = (int)(op.wb_soff[pw + 1] - s0);
-        const double* Cp = op.wb_C + op.wb_coff[pw];
-        const int16_t* tS = op.wb_tS + s0;
-        for (int r = 0; r < k; ++r) {
-          double sum = 0.0;
-          for (int c = lane; c < k; c += 32) sum = fma(__ldg(Cp + (int64_t)r * k + c), X[tS[c]], sum);
-#pragma unroll
-          for (int off = 16; off; off >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, off);
-          if (lane == 0) Y[tS[r]] = sum;
-        }
-        __syncwarp();
-        for (int l = lane; l < N3; l += 32) X[l] = Y[l];
-      } else {
-#pragma unroll
-        for (int j = 0; j < NL; ++j)
-          if (ids[j] >= 0) atomicAdd(op.out + ids[j], coef * (zr[j] - X[lane + 32 * j]));
-      }
-      __syncwarp();
-    }
-  }
-}
-#else
     fd_apply();   // X = A0^{-1} r
     if (!lowrank) {
 #pragma unroll
@@ -630,26 +593,30 @@ __device__ __forceinline__ void fd_loop(const PatchFdOp& op, const Tab& T, const
       __syncwarp();
       continue;
     }
-    // low-rank patch: z = X kept in registers, w = C z_S (row by row, lanes over columns) into Y,
-    // then X = A0^{-1} P_S w and x += coef (z - X)
+    // low-rank patch: z = X kept in registers, z_S compacted into Y, X = P_S w with w = C z_S, then
+    // X = A0^{-1} P_S w and x += coef (z - X).  C is symmetric (symmetrised at setup), so lane r
+    // accumulates row r by walking COLUMN r of the row-major array: the loads of one step are
+    // coalesced across the lanes and independent across steps (eight in flight), z_S[c] is a
+    // warp-uniform shared-memory broadcast, no cross-lane reduction
     double zr[NL];
 #pragma unroll
     for (int j = 0; j < NL; ++j) zr[j] = lane + 32 * j < N3 ? X[lane + 32 * j] : 0.0;
-    for (int l = lane; l < N3; l += 32) Y[l] = 0.0;
-    __syncwarp();
     const int64_t s0 = op.wb_soff[pw];
     const int k = (int)(op.wb_soff[pw + 1] - s0);
     const double* Cp = op.wb_C + op.wb_coff[pw];
     const int16_t* tS = op.wb_tS + s0;
-    for (int r = 0; r < k; ++r) {
-      double sum = 0.0;
-      for (int c = lane; c < k; c += 32) sum = fma(__ldg(Cp + (int64_t)r * k + c), X[tS[c]], sum);
-#pragma unroll
-      for (int off = 16; off; off >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, off);
-      if (lane == 0) Y[tS[r]] = sum;
-    }
+    for (int c = lane; c < k; c += 32) Y[c] = X[tS[c]];
     __syncwarp();
-    for (int l = lane; l < N3; l += 32) X[l] = Y[l];
+    for (int l = lane; l < N3; l += 32) X[l] = 0.0;
+    __syncwarp();
+    for (int r0 = 0; r0 < k; r0 += 32) {
+      const int r = min(r0 + lane, k - 1);
+      const double* Cr = Cp + r;
+      double sum = 0.0;
+#pragma unroll 8
+      for (int c = 0; c < k; ++c) sum = fma(__ldg(Cr + (int64_t)c * k), Y[c], sum);
+      if (r0 + lane < k) X[tS[r]] = sum;
+    }
     __syncwarp();
     fd_apply();
 #pragma unroll
@@ -659,8 +626,6 @@ __device__ __forceinline__ void fd_loop(const PatchFdOp& op, const Tab& T, const
   }
 }
 
-#endif
-
 __device__ __forceinline__ void load_tab_from(Tab& T, int m, const int64_t* base, const int32_t* stride3,
                                               const int16_t* cmin, const int16_t* cmax) {
   for (int a = threadIdx.x; a < m; a += blockDim.x) {
@@ -668,18 +633,6 @@ __device__ __forceinline__ void load_tab_from(Tab& T, int m, const int64_t* base
     T.lo[a] = make_int4(cmin[a * 3 + 0], cmin[a * 3 + 1], cmin[a * 3 + 2], 0);
     T.hi[a] = make_int4(cmax[a * 3 + 0], cmax[a * 3 + 1], cmax[a * 3 + 2], 0);
   }
-}
-
-// Logical warp (0..kIrrWarps-1 streaming, then the fast-diagonalisation warps) of hardware warp
-// hw.  Hardware warps go to the SM's four schedulers round-robin (hw mod 4), and the two
-// populations run different code (44 KB streaming, 125 KB FD at S = 9): map 0 puts two streaming
-// warps and one FD warp on every scheduler; map 1 keeps the FD warps on scheduler 3 (hw 3, 7, 11;
-// the fourth shares scheduler 2), so schedulers 0 and 1 fetch only the streaming loop.
-__device__ __forceinline__ int patch_role(int hw, int wmap) {
-  if (wmap != 1) return hw;
-  if ((hw & 3) == 3) return kIrrWarps + (hw >> 2);
-  if (hw == 10) return kIrrWarps + 3;
-  return hw - (hw >> 2);
 }
 
 // One patchwise smoother sweep in ONE launch, warp-specialised (one CTA per SM, persistent):
@@ -710,7 +663,7 @@ __global__ void __launch_bounds__((kIrrWarps + kFdWarps) * 32, 1) k_patch_smooth
   constexpr int N3 = DIM == 3 ? S * S * S : S * S;
   int* scode = reinterpret_cast<int*>(reinterpret_cast<unsigned char*>(midx) + ((nmi * 2 + 15) / 16) * 16);
   double* wbase = reinterpret_cast<double*>(reinterpret_cast<unsigned char*>(scode) + ((N3 * 4 + 15) / 16) * 16);
-  const int w = patch_role(threadIdx.x >> 5, io.wmap);
+  const int w = threadIdx.x >> 5;
   load_tab_from(T, io.m, io.base, io.stride3, io.cmin, io.cmax);
   if (FD) {
     for (int e = threadIdx.x; e < 3 * fo.ncls * tsz; e += blockDim.x) tab[e] = fo.tabs[e];
@@ -723,6 +676,12 @@ __global__ void __launch_bounds__((kIrrWarps + kFdWarps) * 32, 1) k_patch_smooth
     for (int s = 0; s < kIrrStages; ++s) mbar_init(&bars[w * kIrrStages + s], 1);
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   __syncthreads();
+  auto now_ns = []() -> unsigned long long {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+  };
+  if (io.prof && threadIdx.x == 0) io.prof[4 * blockIdx.x] = now_ns();
   if (w < kIrrWarps) {
     if (IRR) {
       const int g = w / io.wpp;
@@ -735,6 +694,7 @@ __global__ void __launch_bounds__((kIrrWarps + kFdWarps) * 32, 1) k_patch_smooth
   } else {
     if (FD) fd_loop<S, DIM>(fo, T, tab, midx, scode, wbase, w - kIrrWarps, kFdWarps);
   }
+  if (io.prof && (threadIdx.x & 31) == 0) atomicMax(io.prof + 4 * blockIdx.x + (w < kIrrWarps ? 1 : 2), now_ns());
   if (io.sched) {   // the last CTA out re-arms the counters (every claim of this launch is done)
     __syncthreads();
     if (threadIdx.x == 0) {
