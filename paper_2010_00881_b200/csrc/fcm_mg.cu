@@ -159,6 +159,7 @@ struct LevelDev {
   int16_t* wb_tsl = nullptr;       // [mb] tensor slot of block slot l
   int16_t* wb_tS = nullptr;        // S lists as tensor slots (the fused path in k_patch_smooth)
   bool wb_fused = false;           // low-rank patches by k_patch_smooth's FD warps (else k_patch_wb)
+  bool fd_roll = false;            // FD passes with the input loop rolled (small code; streaming-dominated levels)
   std::vector<int64_t> wb_anchor_h, wb_soff_h, wb_coff_h;
   std::vector<int16_t> wb_slots_h, wb_tsl_h;
   // slab mode: interface planes (exchange order) and the smoother increment vector
@@ -244,6 +245,7 @@ struct fcm_mg {
   // coarse sums: bit-identical results run to run (debugging; several times slower)
   bool det = false;
   unsigned long long* patch_prof = nullptr;   // FCM_PATCH_PROF=1: k_patch_smooth population end times
+  int fd_roll_mode = -1;   // FCM_FD_ROLL: -1 per-level cost model, 0 never, 1 always (patch.cuh fd_pass ROLL)
   bool l2ef = true;    // stream read-once matrices with an L2 evict_first policy (FCM_L2_EVICT_FIRST=0: off)
   int pdl = 1;                      // programmatic dependent launch of k_cell_mma (FCM_PDL)
   int ext_lo = 0, ext_n = 0;        // ghost-extended cell layers along the slab axis (relative)
@@ -1443,6 +1445,7 @@ static int launch_block_smooth(fcm_mg* h, int q, const double* r, double* x, dou
   fo.base = Lv.base; fo.stride3 = Lv.stride; fo.cmin = Lv.cmin; fo.cmax = Lv.cmax; fo.m = Lv.m;
   fo.in = r; fo.out = x; fo.coef = coef;
   fo.sched = io.sched;
+  fo.roll = Lv.fd_roll ? 1 : 0;
   // low-rank individual patches: by the fast-diagonalisation warps of the same launch (they finish
   // the regular patches long before the streaming warps; FCM_WB_KERNEL=1: separate k_patch_wb)
   const bool wb_fused = do_irr_wb(h, q, part) && Lv.wb_fused;
@@ -2805,7 +2808,8 @@ static int setup_patch_wb(fcm_mg* h, int q, const BlockGeom& g, const std::vecto
   {
     const double stream_s = (double)Lv.n_irr * Lv.pstride * 8 / 6.0e12;
     const double fd_s = ((double)Lv.n_reg + 2.2 * Lv.n_wb) * 21.5e-9 * N / 729.0;
-    Lv.wb_fused = h->wb_mode == 2 || (h->wb_mode == 0 && stream_s > 1.5 * fd_s);
+    // rolled FD passes are slower per patch: with them the low-rank patches go to k_patch_wb (measured)
+    Lv.wb_fused = h->wb_mode == 2 || (h->wb_mode == 0 && stream_s > 1.5 * fd_s && !Lv.fd_roll);
   }
   Lv.wb_anchor_h = wb;
   Lv.wb_soff_h = soff;
@@ -2960,6 +2964,18 @@ static int setup_schwarz(fcm_mg* h, int q, const std::vector<uint8_t>& kind,
   }
   if (patch) {
     RC(setup_patch_blocks(h, q, g, blk, blocks, ntypes, dir));
+    {
+      // Rolled FD passes (3 KB of code per patch instead of 20 KB) where the explicit stream dominates
+      // the sweep: there the unrolled FD code cycling through the SM's instruction cache costs the
+      // streaming warps more than the rolled loop costs the FD warps (cfg3, one box: level 4
+      // 15.75 -> 14.83 ms with the low-rank patches in k_patch_wb; levels 3 / 2 are FD-bound and
+      // lose 0.3 / 0.2 ms when rolled).  Regular-patch FD work as in the fusion model below.
+      LevelDev& Lv = h->lev[q];
+      const int64_t N = (int64_t)mb;
+      const double stream_s = (double)Lv.n_irr * Lv.pstride * 8 / 6.0e12;
+      const double fd_reg_s = (double)Lv.n_reg * 21.5e-9 * N / 729.0;
+      Lv.fd_roll = h->fd_roll_mode == 1 || (h->fd_roll_mode < 0 && Lv.fd && stream_s > 2.0 * fd_reg_s);
+    }
     return setup_patch_wb(h, q, g, wb, wb_S, kind, cut_idx);
   }
   // device buffers
@@ -3512,6 +3528,7 @@ static int setup_impl(const fcm_grid* g, const fcm_params* prm, const fcm_slab* 
   CU(cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, h->dev));
   h->det = getenv("FCM_DETERMINISTIC") && atoi(getenv("FCM_DETERMINISTIC")) > 0;
   if (getenv("FCM_PATCH_PROF") && atoi(getenv("FCM_PATCH_PROF"))) RC(h->alloc(&h->patch_prof, (int64_t)h->num_sms * 4));
+  h->fd_roll_mode = getenv("FCM_FD_ROLL") ? atoi(getenv("FCM_FD_ROLL")) : -1;
   h->l2ef = !(getenv("FCM_L2_EVICT_FIRST") && atoi(getenv("FCM_L2_EVICT_FIRST")) == 0);
   if (h->det && h->multi) return fail(FCM_EINVAL, "deterministic mode is single-GPU");
   h->ws_ctas = h->num_sms;

@@ -414,6 +414,7 @@ struct PatchFdOp {
   double* out;
   double coef;
   unsigned long long* sched;  // dynamic scheduling: [1] next item (claimed kFdChunk at a time)
+  int roll;                   // fd_pass ROLL form (FCM_FD_ROLL=0: fully unrolled passes)
 };
 
 constexpr int kFdChunk = 4;       // fast-diagonalisation items per dynamic claim
@@ -433,12 +434,47 @@ __device__ __forceinline__ void fd_slot(int s, int q, int v, int n, int& cell, i
 // out_i = sum_j Tm[i][j] in_j (S).  LINE-BASED: each lane owns whole lines along AXIS (S inputs
 // and S outputs in registers, S independent accumulators), the factor is read as warp-uniform
 // broadcast words.  SCALE (the last forward axis): multiply by sc / (lambda_x + lambda_y (+ lambda_z)).
-template <int S, int DIM, int AXIS, bool FWD, bool SCALE>
+// ROLL: the loop over the INPUT index stays rolled (one line value + S factor words + S FMAs per
+// trip), so a pass is ~0.5 KB of code instead of ~3.2 KB and the six passes of a patch ~3 KB
+// instead of ~20 KB: the fast-diagonalisation warps stop cycling the SM's instruction cache under
+// the streaming warps' tile loop (ncu: stall_no_instructions was the largest stall of the fused
+// kernel, two thirds of it in the streaming code).
+template <int S, int DIM, int AXIS, bool FWD, bool SCALE, bool ROLL>
 __device__ __forceinline__ void fd_pass(const double* __restrict__ in, double* __restrict__ out, const double* Tm,
                                         const double* lx, const double* ly, const double* lz, double sc) {
   constexpr int NLINE = DIM == 3 ? S * S : S;
   constexpr int ST = AXIS == 0 ? 1 : (AXIS == 1 ? S : S * S);
   const int lane = threadIdx.x & 31;
+  if (ROLL) {
+#pragma unroll 1
+    for (int line = lane; line < NLINE; line += 32) {
+      const int base = AXIS == 0 ? line * S : (AXIS == 1 ? (line / S) * S * S + line % S : line);
+      double o[S];
+#pragma unroll
+      for (int b = 0; b < S; ++b) o[b] = 0.0;
+      const double* pin = in + base;
+      const double* pt = Tm;   // FWD: row a of the factor; backward: column a
+#pragma unroll 1
+      for (int a = 0; a < S; ++a) {
+        const double va = *pin;
+#pragma unroll
+        for (int b = 0; b < S; ++b) o[b] = fma(FWD ? pt[b] : pt[b * S], va, o[b]);
+        pin += ST;
+        pt += FWD ? S : 1;
+      }
+      if (SCALE) {
+        const int xx = line % S, yy = DIM == 3 ? line / S : 0;
+#pragma unroll
+        for (int j = 0; j < S; ++j) {
+          const double lam = DIM == 3 ? lx[xx] + ly[yy] + lz[j] : lx[xx] + ly[j];
+          o[j] *= sc / lam;
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < S; ++j) out[base + j * ST] = o[j];
+    }
+    return;
+  }
 #pragma unroll 1
   for (int line = lane; line < NLINE; line += 32) {
     const int base = AXIS == 0 ? line * S : (AXIS == 1 ? (line / S) * S * S + line % S : line);
@@ -492,7 +528,7 @@ __device__ __forceinline__ int fd_slot_code(int l, int S, int q, int DIM, const 
 // scattered at the end.  Interior anchors compute the indices from the slot-code table (one
 // LDS + the level table entry); boundary anchors take the general path.  The six one-axis
 // contractions are line-based (fd_pass).  wbase: nw x 2 S^d doubles.
-template <int S, int DIM>
+template <int S, int DIM, bool ROLL>
 __device__ __forceinline__ void fd_loop(const PatchFdOp& op, const Tab& T, const double* tab, const int16_t* midx,
                                         const int* scode, double* wbase, int w, int nw) {
   constexpr int S2 = S * S, N3 = DIM == 3 ? S2 * S : S2;
@@ -563,25 +599,25 @@ __device__ __forceinline__ void fd_loop(const PatchFdOp& op, const Tab& T, const
     // forward (S^T x S^T x S^T) X with the D^-1 scaling fused into the last axis, then backward
     auto fd_apply = [&]() {
       if (DIM == 3) {
-        fd_pass<S, DIM, 0, true, false>(X, Y, Tx, nullptr, nullptr, nullptr, 0.0);
+        fd_pass<S, DIM, 0, true, false, ROLL>(X, Y, Tx, nullptr, nullptr, nullptr, 0.0);
         __syncwarp();
-        fd_pass<S, DIM, 1, true, false>(Y, X, Ty, nullptr, nullptr, nullptr, 0.0);
+        fd_pass<S, DIM, 1, true, false, ROLL>(Y, X, Ty, nullptr, nullptr, nullptr, 0.0);
         __syncwarp();
-        fd_pass<S, DIM, 2, true, true>(X, Y, Tz, Tx + S2, Ty + S2, Tz + S2, sc);
+        fd_pass<S, DIM, 2, true, true, ROLL>(X, Y, Tz, Tx + S2, Ty + S2, Tz + S2, sc);
         __syncwarp();
-        fd_pass<S, DIM, 2, false, false>(Y, X, Tz, nullptr, nullptr, nullptr, 0.0);
+        fd_pass<S, DIM, 2, false, false, ROLL>(Y, X, Tz, nullptr, nullptr, nullptr, 0.0);
         __syncwarp();
-        fd_pass<S, DIM, 1, false, false>(X, Y, Ty, nullptr, nullptr, nullptr, 0.0);
+        fd_pass<S, DIM, 1, false, false, ROLL>(X, Y, Ty, nullptr, nullptr, nullptr, 0.0);
         __syncwarp();
-        fd_pass<S, DIM, 0, false, false>(Y, X, Tx, nullptr, nullptr, nullptr, 0.0);
+        fd_pass<S, DIM, 0, false, false, ROLL>(Y, X, Tx, nullptr, nullptr, nullptr, 0.0);
       } else {
-        fd_pass<S, DIM, 0, true, false>(X, Y, Tx, nullptr, nullptr, nullptr, 0.0);
+        fd_pass<S, DIM, 0, true, false, ROLL>(X, Y, Tx, nullptr, nullptr, nullptr, 0.0);
         __syncwarp();
-        fd_pass<S, DIM, 1, true, true>(Y, X, Ty, Tx + S2, Ty + S2, nullptr, sc);
+        fd_pass<S, DIM, 1, true, true, ROLL>(Y, X, Ty, Tx + S2, Ty + S2, nullptr, sc);
         __syncwarp();
-        fd_pass<S, DIM, 1, false, false>(X, Y, Ty, nullptr, nullptr, nullptr, 0.0);
+        fd_pass<S, DIM, 1, false, false, ROLL>(X, Y, Ty, nullptr, nullptr, nullptr, 0.0);
         __syncwarp();
-        fd_pass<S, DIM, 0, false, false>(Y, X, Tx, nullptr, nullptr, nullptr, 0.0);
+        fd_pass<S, DIM, 0, false, false, ROLL>(Y, X, Tx, nullptr, nullptr, nullptr, 0.0);
       }
       __syncwarp();
     };
@@ -692,7 +728,10 @@ __global__ void __launch_bounds__((kIrrWarps + kFdWarps) * 32, 1) k_patch_smooth
                (int64_t)gridDim.x * ngrp, w, pids + 2 * g);
     }
   } else {
-    if (FD) fd_loop<S, DIM>(fo, T, tab, midx, scode, wbase, w - kIrrWarps, kFdWarps);
+    if (FD) {
+      if (fo.roll) fd_loop<S, DIM, true>(fo, T, tab, midx, scode, wbase, w - kIrrWarps, kFdWarps);
+      else fd_loop<S, DIM, false>(fo, T, tab, midx, scode, wbase, w - kIrrWarps, kFdWarps);
+    }
   }
   if (io.prof && (threadIdx.x & 31) == 0) atomicMax(io.prof + 4 * blockIdx.x + (w < kIrrWarps ? 1 : 2), now_ns());
   if (io.sched) {   // the last CTA out re-arms the counters (every claim of this launch is done)
