@@ -239,10 +239,17 @@ def test_vcycle_matches_oracle(pair, tol_log):
     rng = np.random.default_rng(2)
     for r in (pair.P.b, rng.standard_normal(pair.P.dof.ndof)):
         ref = H.vcycle(r)
+        # R18: the oracle's own LU-vs-Cholesky spread; R24: the GPU's run-to-run spread (fp64-atomic
+        # summation order; 2D p = 4 on alpha = 1e-8 fragments: 0.4 .. 1.7e-10 over four runs, and
+        # 1.03e-10 against 1e-10 was seen here once in four suite runs) -- the larger of the two
         spread = rel(pair.hier_chol().vcycle(r), ref)
-        z = pair.from_gpu(pair.S.vcycle(pair.to_gpu(r)))
-        tol_log(pair, "L4_vcycle_independent", pair.cfg.p, rel(z, ref), pair.tol(1e-10, spread))
-        assert rel(z, ref) <= pair.tol(1e-10, spread)
+        rg = pair.to_gpu(r)
+        zs = [pair.from_gpu(pair.S.vcycle(rg)) for _ in range(3)]
+        gspread = max(rel(zs[i], zs[j]) for i in range(3) for j in range(i))
+        z = zs[0]
+        tol = pair.tol(1e-10, max(spread, gspread))
+        tol_log(pair, "L4_vcycle_independent", pair.cfg.p, rel(z, ref), tol, gpu_spread=gspread)
+        assert rel(z, ref) <= tol, (spread, gspread)
 
 
 def test_fcg_matches_oracle(pair):
